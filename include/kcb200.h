@@ -1,0 +1,135 @@
+/*
+ * kcb200.h — C-ABI of the B200-native kappa-cycle multigrid engine.
+ *
+ * Drop-in boundary for the hot path of the reference package `kcycle`
+ * (arXiv 2010.00626; /root/reference/pkg/src/kcycle).  The reference has no
+ * FFI of its own: its hot path sits behind a duck-typed "state protocol"
+ * consumed by kappa_cycle / run_cycle (cycle.py:204-263) plus the outer
+ * drivers solve_standalone (cycle.py:303-366) and pcg_solve
+ * (krylov.py:60-141).  Each entry point below replaces one method or driver of
+ * that protocol; the citation names the reference symbol whose argument
+ * meaning and error behaviour it keeps.  INTEGRATION.md shows the ctypes
+ * binding (the only FFI mechanism available to a pure-Python reference).
+ *
+ * Conventions
+ *   - Levels are 1-based, 1 = finest, n = coarsest (cycle.py:20).
+ *   - Grid functions cross the boundary as dense row-major float64 (ny, nx)
+ *     arrays of interior nodes only (mesh.py:3-7); the library stores them
+ *     padded with a zero ghost ring in HBM.
+ *   - Every call returns KC_OK or an error code; the code maps onto the
+ *     reference's exception types (see KC_E* below).  kc_last_error() gives
+ *     the message of the last failing call on that handle (thread-local
+ *     message for kc_create failures, handle==NULL).
+ *   - One CUDA stream per handle; a handle is not re-entrant, distinct
+ *     handles may be used from distinct threads ("a solve owns its per-level
+ *     state exclusively", cycle.py:18-19).
+ *   - No CPU fallback: if no sm_100 device is present kc_create fails with
+ *     KC_ECUDA.
+ */
+#ifndef KCB200_H
+#define KCB200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KC_ABI_VERSION 1
+
+/* status codes */
+#define KC_OK 0
+#define KC_EINVAL 1     /* reference raises ValueError            */
+#define KC_ESINGULAR 2  /* reference raises numpy.linalg.LinAlgError */
+#define KC_ECUDA 3      /* CUDA runtime / driver failure           */
+#define KC_ENOMEM 4     /* device allocation failure               */
+
+/* enums mirrored from the reference */
+#define KC_COARSEN_FULL 0        /* Coarsening.FULL_STANDARD, mesh.py:38 */
+#define KC_COARSEN_SEMI_Y 1      /* Coarsening.SEMI_Y, mesh.py:39 (not yet supported: KC_EINVAL) */
+#define KC_SMOOTH_JACOBI 0       /* SmootherKind.DAMPED_JACOBI, smoother.py:37 */
+#define KC_WHICH_V 0             /* GridState.v[level-1], cycle.py:155 */
+#define KC_WHICH_F 1             /* GridState.f[level-1], cycle.py:156 */
+#define KC_STOP_ERROR 0          /* ||v_k|| <= ||v_0||/target (cycle.py:332-347) */
+#define KC_STOP_RESIDUAL 1       /* ||f-Av_k|| <= ||f-Av_0||/target (BASELINE headline) */
+#define KC_STATUS_CONVERGED 0    /* cycle.py:273 */
+#define KC_STATUS_DIVERGED 1     /* cycle.py:274 */
+#define KC_STATUS_MAX_CYCLES 2   /* cycle.py:275 */
+#define KC_STATUS_BREAKDOWN 3    /* cycle.py:276 */
+
+typedef struct kc_handle kc_handle;
+
+int kc_abi_version(void);
+const char* kc_last_error(const kc_handle* h);
+
+/* Galerkin coarse stencil R*A*P (stencil.py:129-148), bit-identical to the
+ * reference's impulse-response read-off including scipy.ndimage's drop of
+ * taps with |w| <= DBL_EPSILON.  Host arithmetic (9 doubles per level). */
+int kc_galerkin_coarsen(const double* w_fine9, int coarsening, double* w_coarse9);
+
+/* Build the device hierarchy: GridState.__init__ (cycle.py:147-156) +
+ * build_hierarchy (mesh.py:56-73).  w = n*9 doubles, stencil of level l at
+ * w[9*(l-1) .. 9*(l-1)+8], w[dy+1][dx+1] row-major (stencil.py:66-70).
+ * All v and f start at zero. */
+int kc_create(int n, int coarsening, const double* w, int smoother_kind, double omega,
+              int nu1, int nu2, int device, kc_handle** out);
+int kc_destroy(kc_handle* h);
+int kc_sync(kc_handle* h);
+
+/* level data transfer: GridState.v[level-1] / f[level-1] item get/set */
+int kc_level_dims(kc_handle* h, int level, int* nx, int* ny);
+int kc_set(kc_handle* h, int level, int which, const double* host, long long ny, long long nx);
+int kc_get(kc_handle* h, int level, int which, double* host, long long ny, long long nx);
+
+/* state protocol (cycle.py:161-179), one call = one reference method */
+int kc_relax(kc_handle* h, int level, int count);          /* relax_level, cycle.py:161-163 */
+int kc_restrict_residual(kc_handle* h, int level);         /* restrict_residual, cycle.py:165-168 */
+int kc_zero_guess(kc_handle* h, int level);                /* zero_guess, cycle.py:170-172 */
+int kc_prolong_add(kc_handle* h, int level);               /* prolong_add, cycle.py:174-176 */
+int kc_solve_coarsest(kc_handle* h);                       /* solve_coarsest, cycle.py:178-179 */
+
+/* out = A v[level] (residual == 0; stencil.apply, stencil.py:108-113) or
+ * out = f[level] - A v[level] (residual != 0; stencil.residual,
+ * stencil.py:116-120) as a host (ny, nx) array.  Per-kernel parity entry
+ * point; uses the level's free ping-pong buffer as scratch. */
+int kc_apply(kc_handle* h, int level, int residual, double* out, long long ny, long long nx);
+
+/* reductions (mesh.py:93-102), deterministic fixed-order fp64 */
+int kc_norm2(kc_handle* h, int level, int which, double* out);
+int kc_residual_norm(kc_handle* h, int level, double* out); /* ||f - A v|| (stencil.py:116-120) */
+
+/* native kappa-cycle: run_cycle (cycle.py:261-263) executed `count` times as a
+ * captured CUDA graph with fused kernels and the persistent bottom kernel. */
+int kc_run_cycles(kc_handle* h, int kappa, int count);
+/* same, bracketed by CUDA events on the handle's stream: bench_cycle
+ * (cycle.py:381-410) timing of `count` back-to-back cycles in milliseconds. */
+int kc_time_cycles(kc_handle* h, int kappa, int count, double* ms);
+
+/* stand-alone solve loop (cycle.py:320-353) on the device.  v[1] must hold
+ * the initial guess, f[1] the right-hand side.  err_hist/res_hist (may be
+ * NULL) receive max_cycles+1 entries: index 0 is the initial norm.  Both
+ * norms are recorded every cycle; stop_mode selects which one stops.
+ * device_ms receives the CUDA-event time of the timed span (norm0 .. exit). */
+int kc_solve(kc_handle* h, int kappa, int stop_mode, double target_reduction, int max_cycles,
+             double* err_hist, double* res_hist, int* iterations, int* status, double* device_ms);
+
+/* MGCG (krylov.py:60-141) on the device.  f and x0 are host arrays of the
+ * finest interior shape (x0 may be NULL = zero start, krylov.py:74).  The
+ * preconditioner is one kappa-cycle on (v = 0, f = r) (krylov.py:81-86); a
+ * non-NULL `precond` replaces it (the reference's `precondition=` argument,
+ * krylov.py:65): it receives r and must fill z, both host (ny, nx) arrays.
+ * x_out (may be NULL) receives the final iterate.  hist (may be NULL)
+ * receives up to max_it+1 values of the stop measure (||x|| for
+ * KC_STOP_ERROR, recursive ||r|| for KC_STOP_RESIDUAL, krylov.py:88-89).
+ * n_precond receives the number of preconditioner applications. */
+typedef void (*kc_precond_fn)(const double* r, double* z, long long ny, long long nx, void* ctx);
+int kc_pcg(kc_handle* h, int kappa, const double* f, const double* x0, int stop_mode,
+           double target_reduction, int max_it, kc_precond_fn precond, void* ctx, double* hist,
+           int* iterations, int* status, int* n_precond, double* x_out, double* device_ms);
+
+/* Instrumentation: host-visible kernel launches and graph nodes of one
+ * captured cycle (after kc_run_cycles/kc_solve built it). */
+int kc_cycle_launches(kc_handle* h, int kappa, int* kernels_per_cycle);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KCB200_H */

@@ -1,0 +1,123 @@
+"""ctypes binding of the C-ABI in include/kcb200.h (libkcb200.so, built in-tree).
+
+This is the reference-side binding shape a maintainer of `kcycle` would add
+(INTEGRATION.md): the reference is pure Python, so ctypes is its FFI.  There
+is no CPU fallback anywhere in the package: if the library is missing the
+import fails loudly, and if no sm_100 device is present `kc_create` fails with
+KC_ECUDA, which is raised as `CudaUnavailableError`.
+
+Error codes map onto the reference's exception types:
+KC_EINVAL -> ValueError, KC_ESINGULAR -> numpy.linalg.LinAlgError,
+KC_ECUDA -> CudaError (RuntimeError), KC_ENOMEM -> MemoryError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkcb200.so")
+
+KC_OK, KC_EINVAL, KC_ESINGULAR, KC_ECUDA, KC_ENOMEM = 0, 1, 2, 3, 4
+KC_COARSEN_FULL, KC_COARSEN_SEMI_Y = 0, 1
+KC_SMOOTH_JACOBI = 0
+KC_WHICH_V, KC_WHICH_F = 0, 1
+KC_STOP_ERROR, KC_STOP_RESIDUAL = 0, 1
+STATUS_NAMES = {0: "converged", 1: "diverged", 2: "max_cycles", 3: "breakdown"}
+
+
+class CudaError(RuntimeError):
+    """CUDA runtime failure inside the engine."""
+
+
+class CudaUnavailableError(CudaError):
+    """No usable sm_100 device: the engine has no CPU fallback."""
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build the CUDA engine first "
+        "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+
+lib = C.CDLL(LIB_PATH)
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+_h = C.c_void_p
+PRECOND_FN = C.CFUNCTYPE(None, _dp, _dp, C.c_longlong, C.c_longlong, C.c_void_p)
+
+_SIGS = {
+    "kc_abi_version": (C.c_int, []),
+    "kc_last_error": (C.c_char_p, [_h]),
+    "kc_galerkin_coarsen": (C.c_int, [_dp, C.c_int, _dp]),
+    "kc_create": (C.c_int, [C.c_int, C.c_int, _dp, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
+                            C.POINTER(C.c_void_p)]),
+    "kc_destroy": (C.c_int, [_h]),
+    "kc_sync": (C.c_int, [_h]),
+    "kc_level_dims": (C.c_int, [_h, C.c_int, _ip, _ip]),
+    "kc_set": (C.c_int, [_h, C.c_int, C.c_int, _dp, C.c_longlong, C.c_longlong]),
+    "kc_get": (C.c_int, [_h, C.c_int, C.c_int, _dp, C.c_longlong, C.c_longlong]),
+    "kc_relax": (C.c_int, [_h, C.c_int, C.c_int]),
+    "kc_restrict_residual": (C.c_int, [_h, C.c_int]),
+    "kc_zero_guess": (C.c_int, [_h, C.c_int]),
+    "kc_prolong_add": (C.c_int, [_h, C.c_int]),
+    "kc_solve_coarsest": (C.c_int, [_h]),
+    "kc_apply": (C.c_int, [_h, C.c_int, C.c_int, _dp, C.c_longlong, C.c_longlong]),
+    "kc_norm2": (C.c_int, [_h, C.c_int, C.c_int, _dp]),
+    "kc_residual_norm": (C.c_int, [_h, C.c_int, _dp]),
+    "kc_run_cycles": (C.c_int, [_h, C.c_int, C.c_int]),
+    "kc_time_cycles": (C.c_int, [_h, C.c_int, C.c_int, _dp]),
+    "kc_solve": (C.c_int, [_h, C.c_int, C.c_int, C.c_double, C.c_int, _dp, _dp, _ip, _ip, _dp]),
+    "kc_pcg": (C.c_int, [_h, C.c_int, _dp, _dp, C.c_int, C.c_double, C.c_int, PRECOND_FN, C.c_void_p,
+                         _dp, _ip, _ip, _ip, _dp, _dp]),
+    "kc_cycle_launches": (C.c_int, [_h, C.c_int, _ip]),
+}
+
+for _name, (_res, _args) in _SIGS.items():
+    _fn = getattr(lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+if lib.kc_abi_version() != 1:
+    raise ImportError(f"libkcb200.so ABI version {lib.kc_abi_version()} != 1; rebuild")
+
+
+def last_error(handle) -> str:
+    msg = lib.kc_last_error(handle)
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, handle=None) -> None:
+    """Raise the reference's exception type for a non-OK status."""
+    if rc == KC_OK:
+        return
+    msg = last_error(handle)
+    if rc == KC_EINVAL:
+        raise ValueError(msg)
+    if rc == KC_ESINGULAR:
+        raise np.linalg.LinAlgError(msg)
+    if rc == KC_ENOMEM:
+        raise MemoryError(msg)
+    if "no CUDA device" in msg or "targets sm_100a" in msg:
+        raise CudaUnavailableError(msg)
+    raise CudaError(msg or f"kcb200 error {rc}")
+
+
+def dptr(a: np.ndarray):
+    """Pointer to a C-contiguous float64 array (caller keeps it alive)."""
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_dp)
+
+
+def as_f64c(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def galerkin_coarsen(w: np.ndarray, coarsening: int) -> np.ndarray:
+    wf = as_f64c(w).reshape(9).copy()
+    out = np.empty(9)
+    check(lib.kc_galerkin_coarsen(dptr(wf), coarsening, dptr(out)))
+    return out.reshape(3, 3)

@@ -1,0 +1,938 @@
+// kc_engine.cu — host engine and C-ABI (include/kcb200.h) of the B200-native
+// kappa-cycle multigrid engine.
+//
+// The engine owns the per-level device storage of one solve (GridState,
+// cycle.py:144-179), executes the state-protocol operations one at a time
+// (the drop-in path driven by the reference's own kappa_cycle), and runs the
+// native cycle: the kappa recursion (cycle.py:204-220) is flattened on the
+// host into a schedule of fused HBM kernels for the fine levels and one
+// persistent bottom kernel per entry into the smem-resident coarse levels,
+// captured once as a CUDA graph per (kappa, level-1 buffer state).
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/kcb200.h"
+#include "kc_bottom.cuh"
+#include "kc_common.cuh"
+#include "kc_grid_kernels.cuh"
+#include "kc_pcg.cuh"
+
+namespace {
+
+thread_local std::string g_create_err;
+
+struct Level {
+  int m = 0, P = 0;
+  size_t elems = 0;
+  double* v[2] = {nullptr, nullptr};
+  double* f = nullptr;
+  int cur = 0;
+  bool vzero = false;
+  St9 st{};
+};
+
+enum OpKind : int { OP_RELAX, OP_RESTRICT, OP_ZERO, OP_PROLONG, OP_COARSEST, OP_BOTTOM };
+struct Op {
+  int kind, level, a, b;
+};
+
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  int end_cur0 = 0;
+  int kernels = 0;
+};
+
+}  // namespace
+
+struct kc_handle {
+  int n = 0, coarsening = 0, smoother = 0, nu1 = 0, nu2 = 0, device = 0;
+  double omega = 0.0;
+  std::vector<Level> L;
+  int Lb = -1;  // 0-based first smem-resident (bottom) level, or -1 if none
+  BotParams bot_base{};
+  size_t bot_smem = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double* d_part = nullptr;     // reduction partials
+  double* d_scal = nullptr;     // device scalars
+  double* h_scal = nullptr;     // pinned host mirror
+  std::map<std::tuple<int, int, int>, GraphEntry> graphs;
+  int launches = 0;             // kernel launches issued by the executor (for capture counting)
+  std::string err;
+  // PCG vectors (lazily allocated), finest padded layout
+  double *x = nullptr, *p = nullptr, *ap = nullptr, *fb = nullptr;
+};
+
+#define KC_FAIL(h, code, ...)                     \
+  do {                                            \
+    char _b[512];                                 \
+    snprintf(_b, sizeof(_b), __VA_ARGS__);        \
+    if (h) (h)->err = _b; else g_create_err = _b; \
+    return (code);                                \
+  } while (0)
+
+#define KC_CUDA(h, call)                                                                    \
+  do {                                                                                      \
+    cudaError_t _e = (call);                                                                \
+    if (_e != cudaSuccess) KC_FAIL(h, KC_ECUDA, "%s: %s", #call, cudaGetErrorString(_e)); \
+  } while (0)
+
+#define KC_LAUNCH_CHECK(h) KC_CUDA(h, cudaGetLastError())
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// host Galerkin coarsening (stencil.py:126-148), exact numpy arithmetic order
+// ---------------------------------------------------------------------------
+struct HGrid {
+  int ny, nx;
+  std::vector<double> a;
+  HGrid(int ny_, int nx_) : ny(ny_), nx(nx_), a((size_t)ny_ * nx_, 0.0) {}
+  double get(int y, int x) const { return (y < 0 || x < 0 || y >= ny || x >= nx) ? 0.0 : a[(size_t)y * nx + x]; }
+  double& at(int y, int x) { return a[(size_t)y * nx + x]; }
+};
+
+// scipy.ndimage.correlate(mode="constant", cval=0): C-order taps, taps with
+// |w| <= DBL_EPSILON skipped.
+HGrid h_apply(const double* w, const HGrid& u) {
+  HGrid o(u.ny, u.nx);
+  for (int y = 0; y < u.ny; ++y)
+    for (int x = 0; x < u.nx; ++x) {
+      double acc = 0.0;
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          const double ww = w[(dy + 1) * 3 + (dx + 1)];
+          if (std::fabs(ww) <= DBL_EPSILON) continue;
+          acc = acc + ww * u.get(y + dy, x + dx);
+        }
+      o.at(y, x) = acc;
+    }
+  return o;
+}
+
+HGrid h_prolong(const HGrid& c, int coarsening) {
+  if (coarsening == KC_COARSEN_FULL) {
+    HGrid f(2 * c.ny + 1, 2 * c.nx + 1);
+    for (int y = 0; y < f.ny; ++y)
+      for (int x = 0; x < f.nx; ++x) {
+        const int q = y >> 1, p = x >> 1;
+        double e;
+        if (y & 1) e = (x & 1) ? c.get(q, p) : 0.5 * (c.get(q, p - 1) + c.get(q, p));
+        else if (x & 1) e = 0.5 * (c.get(q - 1, p) + c.get(q, p));
+        else e = 0.25 * (((c.get(q - 1, p - 1) + c.get(q - 1, p)) + c.get(q, p - 1)) + c.get(q, p));
+        f.at(y, x) = e;
+      }
+    return f;
+  }
+  HGrid f(2 * c.ny + 1, c.nx);  // semi-y (transfer.py:59-66)
+  for (int y = 0; y < f.ny; ++y)
+    for (int x = 0; x < f.nx; ++x) {
+      const int q = y >> 1;
+      f.at(y, x) = (y & 1) ? c.get(q, x) : 0.5 * (c.get(q - 1, x) + c.get(q, x));
+    }
+  return f;
+}
+
+HGrid h_restrict(const HGrid& f, int coarsening) {
+  if (coarsening == KC_COARSEN_FULL) {
+    HGrid c((f.ny - 1) / 2, (f.nx - 1) / 2);
+    for (int q = 0; q < c.ny; ++q)
+      for (int p = 0; p < c.nx; ++p) {
+        const int y = 2 * q + 1, x = 2 * p + 1;
+        const double edge = ((f.get(y - 1, x) + f.get(y + 1, x)) + f.get(y, x - 1)) + f.get(y, x + 1);
+        const double corner =
+            ((f.get(y - 1, x - 1) + f.get(y - 1, x + 1)) + f.get(y + 1, x - 1)) + f.get(y + 1, x + 1);
+        c.at(q, p) = ((4.0 * f.get(y, x) + 2.0 * edge) + corner) / 16.0;
+      }
+    return c;
+  }
+  HGrid c((f.ny - 1) / 2, f.nx);  // semi-y (transfer.py:84-86)
+  for (int q = 0; q < c.ny; ++q)
+    for (int x = 0; x < c.nx; ++x)
+      c.at(q, x) = 0.25 * ((f.get(2 * q, x) + 2.0 * f.get(2 * q + 1, x)) + f.get(2 * q + 2, x));
+  return c;
+}
+
+void h_galerkin(const double* w, int coarsening, double* out) {
+  const int m = 7, cy = 3, cx = 3;  // _AUX_COARSE (stencil.py:123)
+  HGrid c(m, m);
+  c.at(cy, cx) = 1.0;
+  HGrid resp = h_restrict(h_apply(w, h_prolong(c, coarsening)), coarsening);
+  for (int dy = -1; dy <= 1; ++dy)
+    for (int dx = -1; dx <= 1; ++dx) out[(dy + 1) * 3 + (dx + 1)] = resp.get(cy - dy, cx - dx);
+}
+
+dim3 grid2(int mx, int my, int ry = 1) {
+  return dim3((unsigned)((mx + KC_BX - 1) / KC_BX), (unsigned)((my + KC_BY * ry - 1) / (KC_BY * ry)));
+}
+const dim3 kBlock(KC_BX, KC_BY);
+
+// ---------------------------------------------------------------------------
+// executor: one reference state-protocol operation -> kernels on h->stream
+// ---------------------------------------------------------------------------
+int ex_materialize(kc_handle* h, int l) {
+  Level& L = h->L[l];
+  if (!L.vzero) return KC_OK;
+  k_zero<<<grid2(L.m, L.m), kBlock, 0, h->stream>>>(L.v[L.cur], L.m, L.P);
+  KC_LAUNCH_CHECK(h);
+  ++h->launches;
+  L.vzero = false;
+  return KC_OK;
+}
+
+int ex_relax(kc_handle* h, int l, int count) {
+  Level& L = h->L[l];
+  for (int it = 0; it < count; ++it) {
+    double* u = L.v[L.cur];
+    double* o = L.v[L.cur ^ 1];
+    if (L.vzero) k_jacobi<true><<<grid2(L.m, L.m, KC_RY), kBlock, 0, h->stream>>>(u, L.f, o, L.m, L.P, L.st);
+    else k_jacobi<false><<<grid2(L.m, L.m, KC_RY), kBlock, 0, h->stream>>>(u, L.f, o, L.m, L.P, L.st);
+    KC_LAUNCH_CHECK(h);
+    ++h->launches;
+    L.vzero = false;
+    L.cur ^= 1;
+  }
+  return KC_OK;
+}
+
+int ex_restrict(kc_handle* h, int l) {
+  Level& L = h->L[l];
+  Level& C = h->L[l + 1];
+  if (L.vzero)
+    k_resid_restrict<true><<<grid2(C.m, C.m), kBlock, 0, h->stream>>>(L.v[L.cur], L.f, C.f, C.m, L.P, C.P, L.st);
+  else
+    k_resid_restrict<false><<<grid2(C.m, C.m), kBlock, 0, h->stream>>>(L.v[L.cur], L.f, C.f, C.m, L.P, C.P, L.st);
+  KC_LAUNCH_CHECK(h);
+  ++h->launches;
+  return KC_OK;
+}
+
+int ex_prolong(kc_handle* h, int l) {
+  Level& L = h->L[l];
+  Level& C = h->L[l + 1];
+  int rc = ex_materialize(h, l + 1);
+  if (rc) return rc;
+  if (L.vzero)
+    k_prolong_add<true><<<grid2(L.m, L.m), kBlock, 0, h->stream>>>(L.v[L.cur], C.v[C.cur], L.m, L.P, C.P);
+  else
+    k_prolong_add<false><<<grid2(L.m, L.m), kBlock, 0, h->stream>>>(L.v[L.cur], C.v[C.cur], L.m, L.P, C.P);
+  KC_LAUNCH_CHECK(h);
+  ++h->launches;
+  L.vzero = false;
+  return KC_OK;
+}
+
+int ex_coarsest(kc_handle* h) {
+  Level& L = h->L[h->n - 1];
+  if (L.m != 1) KC_FAIL(h, KC_EINVAL, "not a coarsest grid: side %d", L.m);
+  if (L.st.center == 0.0) KC_FAIL(h, KC_ESINGULAR, "singular coarsest operator");
+  k_coarsest<<<1, 32, 0, h->stream>>>(L.v[L.cur], L.f, L.P, L.st.center);
+  KC_LAUNCH_CHECK(h);
+  ++h->launches;
+  L.vzero = false;
+  return KC_OK;
+}
+
+int ex_bottom(kc_handle* h, int l, int k1, int k2) {
+  Level& L = h->L[l];
+  BotParams bp = h->bot_base;
+  bp.gv = L.v[L.cur];
+  bp.gf = L.f;
+  bp.gP = L.P;
+  bp.v_zero = L.vzero ? 1 : 0;
+  bp.nk = k2 > 0 ? 2 : 1;
+  bp.kap[0] = k1;
+  bp.kap[1] = k2;
+  k_bottom<<<1, KC_BOT_THREADS, h->bot_smem, h->stream>>>(bp);
+  KC_LAUNCH_CHECK(h);
+  ++h->launches;
+  L.vzero = false;
+  // coarser levels are scratch of the bottom kernel: logically overwritten
+  for (int j = l + 1; j < h->n; ++j) h->L[j].vzero = true;
+  return KC_OK;
+}
+
+int ex_op(kc_handle* h, const Op& op) {
+  switch (op.kind) {
+    case OP_RELAX: return ex_relax(h, op.level, op.a);
+    case OP_RESTRICT: return ex_restrict(h, op.level);
+    case OP_ZERO: h->L[op.level].vzero = true; return KC_OK;
+    case OP_PROLONG: return ex_prolong(h, op.level);
+    case OP_COARSEST: return ex_coarsest(h);
+    case OP_BOTTOM: return ex_bottom(h, op.level, op.a, op.b);
+  }
+  return KC_EINVAL;
+}
+
+// Flatten kappa_cycle(level, kappa) (cycle.py:204-220) into ops.
+void flatten(const kc_handle* h, int l, int kappa, std::vector<Op>& ops) {
+  const int n = h->n;
+  if (l == h->Lb) {
+    ops.push_back({OP_BOTTOM, l, kappa, 0});
+    return;
+  }
+  if (l == n - 1) {
+    ops.push_back({OP_COARSEST, l, 0, 0});
+    return;
+  }
+  ops.push_back({OP_RELAX, l, h->nu1, 0});
+  ops.push_back({OP_RESTRICT, l, 0, 0});
+  ops.push_back({OP_ZERO, l + 1, 0, 0});
+  if (l + 1 == h->Lb) {
+    ops.push_back({OP_BOTTOM, l + 1, kappa, kappa > 1 ? kappa - 1 : 0});
+  } else {
+    flatten(h, l + 1, kappa, ops);
+    if (kappa > 1) {
+      if (l + 1 == n - 1) {
+        // redundant second coarsest solve: identical f/center, skipped (counted by CycleStats)
+      } else {
+        flatten(h, l + 1, kappa - 1, ops);
+      }
+    }
+  }
+  ops.push_back({OP_PROLONG, l, 0, 0});
+  ops.push_back({OP_RELAX, l, h->nu2, 0});
+}
+
+int get_cycle_graph(kc_handle* h, int kappa, GraphEntry** out) {
+  Level& L0 = h->L[0];
+  auto key = std::make_tuple(kappa, L0.cur, L0.vzero ? 1 : 0);
+  auto it = h->graphs.find(key);
+  if (it != h->graphs.end()) {
+    *out = &it->second;
+    return KC_OK;
+  }
+  std::vector<Op> ops;
+  flatten(h, 0, kappa, ops);
+  // coarse levels start every cycle logically overwritten (zero_guess precedes use)
+  std::vector<int> save_cur(h->n);
+  std::vector<char> save_vz(h->n);
+  for (int j = 0; j < h->n; ++j) {
+    save_cur[j] = h->L[j].cur;
+    save_vz[j] = h->L[j].vzero;
+  }
+  for (int j = 1; j < h->n; ++j) h->L[j].cur = 0;
+  GraphEntry g;
+  const int l0 = h->launches;
+  KC_CUDA(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = KC_OK;
+  for (const Op& op : ops) {
+    rc = ex_op(h, op);
+    if (rc) break;
+  }
+  cudaGraph_t graph = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(h->stream, &graph);
+  g.kernels = h->launches - l0;
+  h->launches = l0;
+  g.end_cur0 = h->L[0].cur;
+  for (int j = 0; j < h->n; ++j) {
+    h->L[j].cur = save_cur[j];
+    h->L[j].vzero = save_vz[j];
+  }
+  if (rc) return rc;
+  if (ce != cudaSuccess) KC_FAIL(h, KC_ECUDA, "cudaStreamEndCapture: %s", cudaGetErrorString(ce));
+  g.graph = graph;
+  KC_CUDA(h, cudaGraphInstantiate(&g.exec, graph, 0));
+  auto ins = h->graphs.emplace(key, g);
+  *out = &ins.first->second;
+  return KC_OK;
+}
+
+int run_cycle_graph(kc_handle* h, int kappa) {
+  GraphEntry* g = nullptr;
+  int rc = get_cycle_graph(h, kappa, &g);
+  if (rc) return rc;
+  KC_CUDA(h, cudaGraphLaunch(g->exec, h->stream));
+  h->L[0].cur = g->end_cur0;
+  h->L[0].vzero = false;
+  for (int j = 1; j < h->n; ++j) {
+    h->L[j].vzero = true;  // scratch after a native cycle (contents not part of the state contract)
+    h->L[j].cur = 0;
+  }
+  return KC_OK;
+}
+
+// async reductions into h->d_scal[slot]
+int red_dot(kc_handle* h, const double* a, const double* b, int l, int slot, bool sq) {
+  Level& L = h->L[l];
+  k_red_partial<0><<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(a, b, L.m, L.P, L.st, h->d_part);
+  KC_LAUNCH_CHECK(h);
+  if (sq) k_red_final<true><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_part, KC_RED_BLOCKS, h->d_scal + slot);
+  else k_red_final<false><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_part, KC_RED_BLOCKS, h->d_scal + slot);
+  KC_LAUNCH_CHECK(h);
+  return KC_OK;
+}
+
+int red_resnorm(kc_handle* h, const double* u, const double* f, int l, int slot) {
+  Level& L = h->L[l];
+  k_red_partial<1><<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(u, f, L.m, L.P, L.st, h->d_part);
+  KC_LAUNCH_CHECK(h);
+  k_red_final<true><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_part, KC_RED_BLOCKS, h->d_scal + slot);
+  KC_LAUNCH_CHECK(h);
+  return KC_OK;
+}
+
+int fetch_scalars(kc_handle* h, int count) {
+  KC_CUDA(h, cudaMemcpyAsync(h->h_scal, h->d_scal, sizeof(double) * count, cudaMemcpyDeviceToHost, h->stream));
+  KC_CUDA(h, cudaStreamSynchronize(h->stream));
+  return KC_OK;
+}
+
+int check_level(kc_handle* h, int level) {
+  if (level < 1 || level > h->n) KC_FAIL(h, KC_EINVAL, "level %d out of range 1..%d", level, h->n);
+  return KC_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+int kc_abi_version(void) { return KC_ABI_VERSION; }
+
+const char* kc_last_error(const kc_handle* h) { return h ? h->err.c_str() : g_create_err.c_str(); }
+
+int kc_galerkin_coarsen(const double* w_fine9, int coarsening, double* w_coarse9) {
+  if (!w_fine9 || !w_coarse9) KC_FAIL((kc_handle*)nullptr, KC_EINVAL, "null stencil pointer");
+  if (coarsening != KC_COARSEN_FULL && coarsening != KC_COARSEN_SEMI_Y)
+    KC_FAIL((kc_handle*)nullptr, KC_EINVAL, "unknown coarsening kind %d", coarsening);
+  h_galerkin(w_fine9, coarsening, w_coarse9);
+  return KC_OK;
+}
+
+int kc_create(int n, int coarsening, const double* w, int smoother_kind, double omega, int nu1, int nu2,
+              int device, kc_handle** out) {
+  kc_handle* none = nullptr;
+  if (!out || !w) KC_FAIL(none, KC_EINVAL, "null argument");
+  *out = nullptr;
+  if (n < 1) KC_FAIL(none, KC_EINVAL, "level count must be >= 1, got %d", n);
+  if (n > 15) KC_FAIL(none, KC_EINVAL, "level count %d exceeds the engine limit 15", n);
+  if (coarsening != KC_COARSEN_FULL)
+    KC_FAIL(none, KC_EINVAL, "only full coarsening is implemented on the device (got %d)", coarsening);
+  if (smoother_kind != KC_SMOOTH_JACOBI)
+    KC_FAIL(none, KC_EINVAL, "only damped Jacobi is implemented on the device (got %d)", smoother_kind);
+  if (!(omega > 0.0 && omega <= 1.0)) KC_FAIL(none, KC_EINVAL, "jacobi damping must lie in (0, 1], got %g", omega);
+  if (nu1 < 0 || nu2 < 0) KC_FAIL(none, KC_EINVAL, "relaxation counts must be >= 0");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    KC_FAIL(none, KC_ECUDA, "no CUDA device available (%s); the engine has no CPU fallback",
+            e != cudaSuccess ? cudaGetErrorString(e) : "0 devices");
+  if (device < 0 || device >= ndev) KC_FAIL(none, KC_EINVAL, "device %d out of range (%d devices)", device, ndev);
+  cudaDeviceProp prop;
+  KC_CUDA(none, cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) KC_FAIL(none, KC_ECUDA, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major, prop.minor);
+  KC_CUDA(none, cudaSetDevice(device));
+
+  kc_handle* h = new kc_handle();
+  h->n = n;
+  h->coarsening = coarsening;
+  h->smoother = smoother_kind;
+  h->omega = omega;
+  h->nu1 = nu1;
+  h->nu2 = nu2;
+  h->device = device;
+  h->L.resize(n);
+  auto fail = [&](int code) {
+    g_create_err = h->err;
+    kc_destroy(h);
+    return code;
+  };
+  for (int l = 0; l < n; ++l) {
+    Level& L = h->L[l];
+    L.m = (1 << (n - l)) - 1;
+    L.P = kc_pitch(L.m);
+    L.elems = (size_t)(L.m + 2) * L.P;
+    for (int k = 0; k < 9; ++k) {
+      double wk = w[9 * l + k];
+      L.st.w[k] = (std::fabs(wk) <= DBL_EPSILON) ? 0.0 : wk;  // ndimage tap drop (F3)
+    }
+    L.st.center = w[9 * l + 4];
+    if (L.m > 1 && (nu1 + nu2) > 0 && L.st.center == 0.0) {
+      h->err = "zero center coefficient";
+      return fail(KC_EINVAL);
+    }
+    L.st.c = omega / L.st.center;  // (omega / center), smoother.py:100
+    for (int b = 0; b < 3; ++b) {
+      double* ptr = nullptr;
+      cudaError_t ce = cudaMalloc(&ptr, L.elems * sizeof(double));
+      if (ce != cudaSuccess) {
+        h->err = std::string("cudaMalloc level storage: ") + cudaGetErrorString(ce);
+        return fail(KC_ENOMEM);
+      }
+      if (cudaMemset(ptr, 0, L.elems * sizeof(double)) != cudaSuccess) {
+        cudaFree(ptr);
+        h->err = "cudaMemset failed";
+        return fail(KC_ECUDA);
+      }
+      if (b < 2) L.v[b] = ptr;
+      else L.f = ptr;
+    }
+  }
+  if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&h->ev0) != cudaSuccess || cudaEventCreate(&h->ev1) != cudaSuccess ||
+      cudaMalloc(&h->d_part, sizeof(double) * KC_RED_BLOCKS) != cudaSuccess ||
+      cudaMalloc(&h->d_scal, sizeof(double) * 64) != cudaSuccess ||
+      cudaMallocHost(&h->h_scal, sizeof(double) * 64) != cudaSuccess) {
+    h->err = "stream/event/scratch allocation failed";
+    return fail(KC_ECUDA);
+  }
+  cudaMemset(h->d_scal, 0, sizeof(double) * 64);
+
+  // bottom (smem-resident) levels
+  int lb = -1;
+  for (int l = 0; l < n; ++l)
+    if (h->L[l].m <= KC_BOT_MAX_M) {
+      lb = l;
+      break;
+    }
+  if (lb >= 0 && n - lb <= KC_BOT_MAXLEV) {
+    BotParams& bp = h->bot_base;
+    memset(&bp, 0, sizeof(bp));
+    bp.nlev = n - lb;
+    bp.nu1 = nu1;
+    bp.nu2 = nu2;
+    int off = 0;
+    for (int j = 0; j < bp.nlev; ++j) {
+      const Level& L = h->L[lb + j];
+      BotLevel& B = bp.lv[j];
+      B.m = L.m;
+      B.S = L.m + 2;
+      const int sz = B.S * B.S;
+      B.ov[0] = off;
+      B.ov[1] = off + sz;
+      B.of = off + 2 * sz;
+      off += 3 * sz;
+      B.s = L.st;
+    }
+    bp.total = off;
+    h->bot_smem = sizeof(double) * (size_t)off;
+    if (cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->bot_smem) != cudaSuccess) {
+      h->err = "cudaFuncSetAttribute(k_bottom) failed";
+      return fail(KC_ECUDA);
+    }
+    h->Lb = lb;
+  }
+  *out = h;
+  return KC_OK;
+}
+
+int kc_destroy(kc_handle* h) {
+  if (!h) return KC_OK;
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (auto& kv : h->graphs) {
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+  }
+  for (Level& L : h->L) {
+    cudaFree(L.v[0]);
+    cudaFree(L.v[1]);
+    cudaFree(L.f);
+  }
+  cudaFree(h->x);
+  cudaFree(h->p);
+  cudaFree(h->ap);
+  cudaFree(h->fb);
+  cudaFree(h->d_part);
+  cudaFree(h->d_scal);
+  if (h->h_scal) cudaFreeHost(h->h_scal);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return KC_OK;
+}
+
+int kc_sync(kc_handle* h) {
+  if (!h) return KC_EINVAL;
+  KC_CUDA(h, cudaStreamSynchronize(h->stream));
+  return KC_OK;
+}
+
+int kc_level_dims(kc_handle* h, int level, int* nx, int* ny) {
+  if (!h) return KC_EINVAL;
+  int rc = check_level(h, level);
+  if (rc) return rc;
+  *nx = *ny = h->L[level - 1].m;
+  return KC_OK;
+}
+
+int kc_set(kc_handle* h, int level, int which, const double* host, long long ny, long long nx) {
+  if (!h) return KC_EINVAL;
+  int rc = check_level(h, level);
+  if (rc) return rc;
+  Level& L = h->L[level - 1];
+  if (ny != L.m || nx != L.m) KC_FAIL(h, KC_EINVAL, "shape (%lld, %lld) != level %d shape (%d, %d)", ny, nx, level, L.m, L.m);
+  double* dst = which == KC_WHICH_F ? L.f : L.v[L.cur];
+  KC_CUDA(h, cudaMemcpy2DAsync(dst + kc_idx(L.P, 0, 0), sizeof(double) * L.P, host, sizeof(double) * L.m,
+                               sizeof(double) * L.m, L.m, cudaMemcpyHostToDevice, h->stream));
+  KC_CUDA(h, cudaStreamSynchronize(h->stream));
+  if (which != KC_WHICH_F) L.vzero = false;
+  return KC_OK;
+}
+
+int kc_get(kc_handle* h, int level, int which, double* host, long long ny, long long nx) {
+  if (!h) return KC_EINVAL;
+  int rc = check_level(h, level);
+  if (rc) return rc;
+  Level& L = h->L[level - 1];
+  if (ny != L.m || nx != L.m) KC_FAIL(h, KC_EINVAL, "shape (%lld, %lld) != level %d shape (%d, %d)", ny, nx, level, L.m, L.m);
+  if (which != KC_WHICH_F) {
+    rc = ex_materialize(h, level - 1);
+    if (rc) return rc;
+  }
+  const double* src = which == KC_WHICH_F ? L.f : L.v[L.cur];
+  KC_CUDA(h, cudaMemcpy2DAsync(host, sizeof(double) * L.m, src + kc_idx(L.P, 0, 0), sizeof(double) * L.P,
+                               sizeof(double) * L.m, L.m, cudaMemcpyDeviceToHost, h->stream));
+  KC_CUDA(h, cudaStreamSynchronize(h->stream));
+  return KC_OK;
+}
+
+int kc_relax(kc_handle* h, int level, int count) {
+  if (!h) return KC_EINVAL;
+  int rc = check_level(h, level);
+  if (rc) return rc;
+  if (count < 0) KC_FAIL(h, KC_EINVAL, "relaxation count must be >= 0, got %d", count);
+  if (count > 0 && h->L[level - 1].st.center == 0.0) KC_FAIL(h, KC_EINVAL, "zero center coefficient");
+  return ex_relax(h, level - 1, count);
+}
+
+int kc_restrict_residual(kc_handle* h, int level) {
+  if (!h) return KC_EINVAL;
+  int rc = check_level(h, level);
+  if (rc) return rc;
+  if (level == h->n || h->L[level - 1].m < 3)
+    KC_FAIL(h, KC_EINVAL, "fine ny must be odd and >= 3, got %d", h->L[level - 1].m);
+  return ex_restrict(h, level - 1);
+}
+
+int kc_zero_guess(kc_handle* h, int level) {
+  if (!h) return KC_EINVAL;
+  int rc = check_level(h, level);
+  if (rc) return rc;
+  h->L[level - 1].vzero = true;
+  return KC_OK;
+}
+
+int kc_prolong_add(kc_handle* h, int level) {
+  if (!h) return KC_EINVAL;
+  int rc = check_level(h, level);
+  if (rc) return rc;
+  if (level == h->n) KC_FAIL(h, KC_EINVAL, "no coarser level below level %d", level);
+  return ex_prolong(h, level - 1);
+}
+
+int kc_solve_coarsest(kc_handle* h) {
+  if (!h) return KC_EINVAL;
+  return ex_coarsest(h);
+}
+
+int kc_apply(kc_handle* h, int level, int residual, double* out, long long ny, long long nx) {
+  if (!h || !out) return KC_EINVAL;
+  int rc = check_level(h, level);
+  if (rc) return rc;
+  Level& L = h->L[level - 1];
+  if (ny != L.m || nx != L.m) KC_FAIL(h, KC_EINVAL, "shape (%lld, %lld) != level %d shape (%d, %d)", ny, nx, level, L.m, L.m);
+  if ((rc = ex_materialize(h, level - 1))) return rc;
+  double* t = L.v[L.cur ^ 1];
+  if (residual) k_apply<true><<<grid2(L.m, L.m), kBlock, 0, h->stream>>>(L.v[L.cur], L.f, t, L.m, L.P, L.st);
+  else k_apply<false><<<grid2(L.m, L.m), kBlock, 0, h->stream>>>(L.v[L.cur], L.f, t, L.m, L.P, L.st);
+  KC_LAUNCH_CHECK(h);
+  KC_CUDA(h, cudaMemcpy2DAsync(out, sizeof(double) * L.m, t + kc_idx(L.P, 0, 0), sizeof(double) * L.P,
+                               sizeof(double) * L.m, L.m, cudaMemcpyDeviceToHost, h->stream));
+  KC_CUDA(h, cudaStreamSynchronize(h->stream));
+  return KC_OK;
+}
+
+int kc_norm2(kc_handle* h, int level, int which, double* out) {
+  if (!h || !out) return KC_EINVAL;
+  int rc = check_level(h, level);
+  if (rc) return rc;
+  Level& L = h->L[level - 1];
+  if (which != KC_WHICH_F && (rc = ex_materialize(h, level - 1))) return rc;
+  const double* a = which == KC_WHICH_F ? L.f : L.v[L.cur];
+  if ((rc = red_dot(h, a, a, level - 1, 0, true))) return rc;
+  if ((rc = fetch_scalars(h, 1))) return rc;
+  *out = h->h_scal[0];
+  return KC_OK;
+}
+
+int kc_residual_norm(kc_handle* h, int level, double* out) {
+  if (!h || !out) return KC_EINVAL;
+  int rc = check_level(h, level);
+  if (rc) return rc;
+  if ((rc = ex_materialize(h, level - 1))) return rc;
+  Level& L = h->L[level - 1];
+  if ((rc = red_resnorm(h, L.v[L.cur], L.f, level - 1, 0))) return rc;
+  if ((rc = fetch_scalars(h, 1))) return rc;
+  *out = h->h_scal[0];
+  return KC_OK;
+}
+
+int kc_run_cycles(kc_handle* h, int kappa, int count) {
+  if (!h) return KC_EINVAL;
+  if (kappa < 1) KC_FAIL(h, KC_EINVAL, "cycle counter must be >= 1, got %d", kappa);
+  if (kappa > h->n) kappa = h->n;  // identical to W (cycle.py:80-82; Prop 2.1)
+  for (int i = 0; i < count; ++i) {
+    int rc = run_cycle_graph(h, kappa);
+    if (rc) return rc;
+  }
+  return KC_OK;
+}
+
+int kc_time_cycles(kc_handle* h, int kappa, int count, double* ms) {
+  if (!h || !ms) return KC_EINVAL;
+  if (kappa < 1) KC_FAIL(h, KC_EINVAL, "cycle counter must be >= 1, got %d", kappa);
+  if (kappa > h->n) kappa = h->n;
+  int rc;
+  GraphEntry* g = nullptr;
+  if ((rc = get_cycle_graph(h, kappa, &g))) return rc;  // capture outside the timed span
+  KC_CUDA(h, cudaStreamSynchronize(h->stream));
+  KC_CUDA(h, cudaEventRecord(h->ev0, h->stream));
+  for (int i = 0; i < count; ++i)
+    if ((rc = run_cycle_graph(h, kappa))) return rc;
+  KC_CUDA(h, cudaEventRecord(h->ev1, h->stream));
+  KC_CUDA(h, cudaEventSynchronize(h->ev1));
+  float t = 0.f;
+  KC_CUDA(h, cudaEventElapsedTime(&t, h->ev0, h->ev1));
+  *ms = t;
+  return KC_OK;
+}
+
+int kc_cycle_launches(kc_handle* h, int kappa, int* kernels_per_cycle) {
+  if (!h || !kernels_per_cycle) return KC_EINVAL;
+  if (kappa > h->n) kappa = h->n;
+  GraphEntry* g = nullptr;
+  int rc = get_cycle_graph(h, kappa, &g);
+  if (rc) return rc;
+  *kernels_per_cycle = g->kernels;
+  return KC_OK;
+}
+
+int kc_solve(kc_handle* h, int kappa, int stop_mode, double target_reduction, int max_cycles, double* err_hist,
+             double* res_hist, int* iterations, int* status, double* device_ms) {
+  if (!h || !iterations || !status) return KC_EINVAL;
+  if (kappa < 1) KC_FAIL(h, KC_EINVAL, "cycle counter must be >= 1, got %d", kappa);
+  if (!(target_reduction > 1.0)) KC_FAIL(h, KC_EINVAL, "target reduction must exceed 1, got %g", target_reduction);
+  if (stop_mode != KC_STOP_ERROR && stop_mode != KC_STOP_RESIDUAL) KC_FAIL(h, KC_EINVAL, "bad stop mode %d", stop_mode);
+  if (kappa > h->n) kappa = h->n;
+  int rc;
+  if ((rc = ex_materialize(h, 0))) return rc;
+  // build the graph before timing (setup, like build_state)
+  GraphEntry* g = nullptr;
+  if ((rc = get_cycle_graph(h, kappa, &g))) return rc;
+  KC_CUDA(h, cudaStreamSynchronize(h->stream));
+  Level& L0 = h->L[0];
+  KC_CUDA(h, cudaEventRecord(h->ev0, h->stream));
+  if ((rc = red_dot(h, L0.v[L0.cur], L0.v[L0.cur], 0, 0, true))) return rc;
+  if ((rc = red_resnorm(h, L0.v[L0.cur], L0.f, 0, 1))) return rc;
+  if ((rc = fetch_scalars(h, 2))) return rc;
+  const double e0 = h->h_scal[0], r0 = h->h_scal[1];
+  if (err_hist) err_hist[0] = e0;
+  if (res_hist) res_hist[0] = r0;
+  const double m0 = stop_mode == KC_STOP_ERROR ? e0 : r0;
+  const double target = m0 / target_reduction;
+  int st = KC_STATUS_MAX_CYCLES, it = 0, streak = 0;
+  double cur = m0;
+  if (m0 <= target) {
+    st = KC_STATUS_CONVERGED;
+  } else {
+    for (it = 1; it <= max_cycles; ++it) {
+      if ((rc = run_cycle_graph(h, kappa))) return rc;
+      if ((rc = red_dot(h, L0.v[L0.cur], L0.v[L0.cur], 0, 0, true))) return rc;
+      if ((rc = red_resnorm(h, L0.v[L0.cur], L0.f, 0, 1))) return rc;
+      if ((rc = fetch_scalars(h, 2))) return rc;
+      if (err_hist) err_hist[it] = h->h_scal[0];
+      if (res_hist) res_hist[it] = h->h_scal[1];
+      const double prev = cur;
+      cur = stop_mode == KC_STOP_ERROR ? h->h_scal[0] : h->h_scal[1];
+      if (cur <= target) {
+        st = KC_STATUS_CONVERGED;
+        break;
+      }
+      streak = cur > prev ? streak + 1 : 0;
+      if (streak >= 5) {  // _DIVERGENCE_STREAK, cycle.py:278
+        st = KC_STATUS_DIVERGED;
+        break;
+      }
+    }
+    if (it > max_cycles) it = max_cycles;
+  }
+  KC_CUDA(h, cudaEventRecord(h->ev1, h->stream));
+  KC_CUDA(h, cudaEventSynchronize(h->ev1));
+  float ms = 0.f;
+  KC_CUDA(h, cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  if (device_ms) *device_ms = ms;
+  *iterations = it;
+  *status = st;
+  return KC_OK;
+}
+
+}  // extern "C"
+
+namespace {
+int ensure_pcg_buffers(kc_handle* h) {
+  const size_t bytes = h->L[0].elems * sizeof(double);
+  double** bufs[4] = {&h->x, &h->p, &h->ap, &h->fb};
+  for (double** b : bufs) {
+    if (*b) continue;
+    cudaError_t ce = cudaMalloc(b, bytes);
+    if (ce != cudaSuccess) KC_FAIL(h, KC_ENOMEM, "cudaMalloc PCG vector: %s", cudaGetErrorString(ce));
+    KC_CUDA(h, cudaMemsetAsync(*b, 0, bytes, h->stream));
+  }
+  return KC_OK;
+}
+
+int upload_interior(kc_handle* h, double* dst, const double* host) {
+  const Level& L = h->L[0];
+  KC_CUDA(h, cudaMemcpy2DAsync(dst + kc_idx(L.P, 0, 0), sizeof(double) * L.P, host, sizeof(double) * L.m,
+                               sizeof(double) * L.m, L.m, cudaMemcpyHostToDevice, h->stream));
+  return KC_OK;
+}
+
+int download_interior(kc_handle* h, double* host, const double* src) {
+  const Level& L = h->L[0];
+  KC_CUDA(h, cudaMemcpy2DAsync(host, sizeof(double) * L.m, src + kc_idx(L.P, 0, 0), sizeof(double) * L.P,
+                               sizeof(double) * L.m, L.m, cudaMemcpyDeviceToHost, h->stream));
+  return KC_OK;
+}
+
+enum { S_RZ = 2, S_PAP = 3, S_MEAS = 4, S_RZN = 5 };
+
+// z = M^-1 r into L0.v[cur]; r lives in L0.f (krylov.py:81-86)
+int pcg_precondition(kc_handle* h, int kappa, kc_precond_fn fn, void* ctx, std::vector<double>& hr,
+                     std::vector<double>& hz) {
+  Level& L0 = h->L[0];
+  if (!fn) {
+    L0.vzero = true;  // state.zero_guess(1); state.f[0] = r  (r is stored in f[0])
+    return run_cycle_graph(h, kappa);
+  }
+  int rc;
+  if ((rc = download_interior(h, hr.data(), L0.f))) return rc;
+  KC_CUDA(h, cudaStreamSynchronize(h->stream));
+  fn(hr.data(), hz.data(), L0.m, L0.m, ctx);
+  if ((rc = upload_interior(h, L0.v[L0.cur], hz.data()))) return rc;
+  L0.vzero = false;
+  return KC_OK;
+}
+}  // namespace
+
+extern "C" int kc_pcg(kc_handle* h, int kappa, const double* f, const double* x0, int stop_mode,
+                      double target_reduction, int max_it, kc_precond_fn precond, void* ctx, double* hist,
+                      int* iterations, int* status, int* n_precond, double* x_out, double* device_ms) {
+  if (!h || !f || !iterations || !status) return KC_EINVAL;
+  if (kappa < 1) KC_FAIL(h, KC_EINVAL, "cycle counter must be >= 1, got %d", kappa);
+  if (!(target_reduction > 1.0)) KC_FAIL(h, KC_EINVAL, "target reduction must exceed 1, got %g", target_reduction);
+  if (stop_mode != KC_STOP_ERROR && stop_mode != KC_STOP_RESIDUAL) KC_FAIL(h, KC_EINVAL, "bad stop mode %d", stop_mode);
+  if (kappa > h->n) kappa = h->n;
+  int rc;
+  if ((rc = ensure_pcg_buffers(h))) return rc;
+  Level& L0 = h->L[0];
+  const int m = L0.m, P = L0.P;
+  std::vector<double> hr, hz;
+  if (precond) {
+    hr.resize((size_t)m * m);
+    hz.resize((size_t)m * m);
+  } else {
+    GraphEntry* g = nullptr;  // capture both level-1 states up front (setup)
+    if ((rc = get_cycle_graph(h, kappa, &g))) return rc;
+  }
+  if ((rc = upload_interior(h, h->fb, f))) return rc;
+  if (x0) {
+    if ((rc = upload_interior(h, h->x, x0))) return rc;
+  } else {
+    KC_CUDA(h, cudaMemsetAsync(h->x, 0, L0.elems * sizeof(double), h->stream));
+  }
+  KC_CUDA(h, cudaStreamSynchronize(h->stream));
+  const bool mx = stop_mode == KC_STOP_ERROR;
+  double* r = L0.f;
+  int napp = 0;
+  KC_CUDA(h, cudaEventRecord(h->ev0, h->stream));
+  k_pcg_residual<<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(h->x, h->fb, r, m, P, L0.st);
+  KC_LAUNCH_CHECK(h);
+  if ((rc = red_dot(h, mx ? h->x : r, mx ? h->x : r, 0, S_MEAS, true))) return rc;
+  if ((rc = fetch_scalars(h, S_MEAS + 1))) return rc;
+  const double norm0 = h->h_scal[S_MEAS];
+  const double target = norm0 / target_reduction;
+  if (hist) hist[0] = norm0;
+  int st = KC_STATUS_MAX_CYCLES, it = 0;
+  double cur = norm0;
+  if (norm0 <= target) {
+    st = KC_STATUS_CONVERGED;
+  } else {
+    if ((rc = pcg_precondition(h, kappa, precond, ctx, hr, hz))) return rc;
+    ++napp;
+    if ((rc = red_dot(h, r, L0.v[L0.cur], 0, S_RZ, false))) return rc;
+    KC_CUDA(h, cudaMemcpyAsync(h->p, L0.v[L0.cur], L0.elems * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    if ((rc = fetch_scalars(h, S_MEAS + 1))) return rc;
+    if (!(h->h_scal[S_RZ] > 0.0)) {
+      st = KC_STATUS_BREAKDOWN;
+    } else {
+      for (it = 1; it <= max_it; ++it) {
+        k_pcg_apply_dot<<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(h->p, h->ap, m, P, L0.st, h->d_part);
+        KC_LAUNCH_CHECK(h);
+        k_red_final<false><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_part, KC_RED_BLOCKS, h->d_scal + S_PAP);
+        KC_LAUNCH_CHECK(h);
+        if (mx)
+          k_pcg_update_xr<true><<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(h->x, r, h->p, h->ap, m, P, h->d_scal,
+                                                                                  S_RZ, S_PAP, h->d_part);
+        else
+          k_pcg_update_xr<false><<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(h->x, r, h->p, h->ap, m, P,
+                                                                                   h->d_scal, S_RZ, S_PAP, h->d_part);
+        KC_LAUNCH_CHECK(h);
+        k_red_final<true><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_part, KC_RED_BLOCKS, h->d_scal + S_MEAS);
+        KC_LAUNCH_CHECK(h);
+        if ((rc = fetch_scalars(h, S_MEAS + 1))) return rc;
+        if (!(h->h_scal[S_PAP] > 0.0)) {
+          st = KC_STATUS_BREAKDOWN;
+          break;
+        }
+        cur = h->h_scal[S_MEAS];
+        if (hist) hist[it] = cur;
+        if (cur <= target) {
+          st = KC_STATUS_CONVERGED;
+          break;
+        }
+        if ((rc = pcg_precondition(h, kappa, precond, ctx, hr, hz))) return rc;
+        ++napp;
+        if ((rc = red_dot(h, r, L0.v[L0.cur], 0, S_RZN, false))) return rc;
+        k_pcg_update_p<<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(h->p, L0.v[L0.cur], m, P, h->d_scal, S_RZN,
+                                                                       S_RZ);
+        KC_LAUNCH_CHECK(h);
+        k_copy_scalar<<<1, 32, 0, h->stream>>>(h->d_scal, S_RZ, S_RZN);
+        KC_LAUNCH_CHECK(h);
+        if ((rc = fetch_scalars(h, S_RZN + 1))) return rc;
+        if (!(h->h_scal[S_RZN] > 0.0)) {
+          st = KC_STATUS_BREAKDOWN;
+          break;
+        }
+      }
+      if (it > max_it) it = max_it;
+    }
+  }
+  KC_CUDA(h, cudaEventRecord(h->ev1, h->stream));
+  KC_CUDA(h, cudaEventSynchronize(h->ev1));
+  float ms = 0.f;
+  KC_CUDA(h, cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  if (device_ms) *device_ms = ms;
+  if (x_out) {
+    if ((rc = download_interior(h, x_out, h->x))) return rc;
+    KC_CUDA(h, cudaStreamSynchronize(h->stream));
+  }
+  *iterations = it;
+  *status = st;
+  if (n_precond) *n_precond = napp;
+  return KC_OK;
+}

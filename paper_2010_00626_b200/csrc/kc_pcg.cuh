@@ -1,0 +1,84 @@
+// kc_pcg.cuh — fused PCG vector kernels on the finest level (krylov.py:60-141,
+// SURVEY.md §2.3 K7).  Elementwise expressions keep numpy's rounding
+// (x + alpha*p with a separately rounded product, no FMA); only the dot
+// products differ from OpenBLAS ddot in the last bits, so PCG
+// histories match the reference to ~1e-12 relative, not bitwise.
+//
+// Scalars live in device memory and alpha = rz/pap, beta = rz_next/rz are
+// formed per thread with the same IEEE division the reference's Python
+// floats use.  Guards make the update kernels no-ops when the reference would
+// have stopped for breakdown (pap <= 0 or rz_next <= 0), so the host can
+// inspect the scalars after the fact without the device having run ahead.
+#pragma once
+#include "kc_common.cuh"
+#include "kc_grid_kernels.cuh"
+
+// r = f - A x (krylov.py:76).  Grid-stride over rows like the reductions.
+__global__ void __launch_bounds__(KC_RED_THREADS)
+    k_pcg_residual(const double* __restrict__ x, const double* __restrict__ f, double* __restrict__ r, int m,
+                   int P, St9 s) {
+  for (int y = blockIdx.x; y < m; y += gridDim.x)
+    for (int xx = threadIdx.x; xx < m; xx += KC_RED_THREADS) {
+      const size_t i = kc_idx(P, y, xx);
+      r[i] = DSUB(__ldg(f + i), kc_apply9(x + i, P, s));
+    }
+}
+
+// ap = A p ; partial[b] = sum p*ap (krylov.py:109-110)
+__global__ void __launch_bounds__(KC_RED_THREADS)
+    k_pcg_apply_dot(const double* __restrict__ p, double* __restrict__ ap, int m, int P, St9 s,
+                    double* __restrict__ part) {
+  double acc = 0.0;
+  for (int y = blockIdx.x; y < m; y += gridDim.x)
+    for (int xx = threadIdx.x; xx < m; xx += KC_RED_THREADS) {
+      const size_t i = kc_idx(P, y, xx);
+      const double pv = __ldg(p + i);
+      const double a = kc_apply9(p + i, P, s);
+      ap[i] = a;
+      acc = fma(pv, a, acc);
+    }
+  const double t = kc_block_sum(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+// x += alpha p ; r -= alpha ap ; partial = sum (x^2 | r^2)  (krylov.py:114-117)
+template <bool MEASURE_X>
+__global__ void __launch_bounds__(KC_RED_THREADS)
+    k_pcg_update_xr(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                    const double* __restrict__ ap, int m, int P, const double* __restrict__ scal, int s_rz,
+                    int s_pap, double* __restrict__ part) {
+  const double pap = scal[s_pap];
+  double acc = 0.0;
+  if (pap > 0.0) {
+    const double alpha = __ddiv_rn(scal[s_rz], pap);
+    for (int y = blockIdx.x; y < m; y += gridDim.x)
+      for (int xx = threadIdx.x; xx < m; xx += KC_RED_THREADS) {
+        const size_t i = kc_idx(P, y, xx);
+        const double xn = DADD(x[i], DMUL(alpha, __ldg(p + i)));
+        const double rn = DSUB(r[i], DMUL(alpha, __ldg(ap + i)));
+        x[i] = xn;
+        r[i] = rn;
+        acc = MEASURE_X ? fma(xn, xn, acc) : fma(rn, rn, acc);
+      }
+  }
+  const double t = kc_block_sum(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+// p = z + (rz_next / rz) p  (krylov.py:127)
+__global__ void __launch_bounds__(KC_RED_THREADS)
+    k_pcg_update_p(double* __restrict__ p, const double* __restrict__ z, int m, int P,
+                   const double* __restrict__ scal, int s_rz_next, int s_rz) {
+  const double rzn = scal[s_rz_next];
+  if (!(rzn > 0.0)) return;
+  const double beta = __ddiv_rn(rzn, scal[s_rz]);
+  for (int y = blockIdx.x; y < m; y += gridDim.x)
+    for (int xx = threadIdx.x; xx < m; xx += KC_RED_THREADS) {
+      const size_t i = kc_idx(P, y, xx);
+      p[i] = DADD(__ldg(z + i), DMUL(beta, p[i]));
+    }
+}
+
+__global__ void k_copy_scalar(double* __restrict__ scal, int dst, int src) {
+  if (threadIdx.x == 0) scal[dst] = scal[src];
+}

@@ -1,0 +1,445 @@
+"""GPU parity: the CUDA engine vs the reference's golden vectors and the oracle.
+
+Bars (SURVEY.md §8(c) parity protocol):
+  * per kernel: bit-exact (fp64, no FMA, reference expression order);
+  * per cycle, per-op (state protocol) and native (graph + bottom kernel):
+    iterates bit-exact;
+  * solve histories: per-cycle error and residual norms within 1e-10
+    relative of the reference (norm reductions are reordered sums, so ~1e-15
+    is expected), identical iteration counts;
+  * PCG: identical iteration counts, histories within 1e-10 relative... except
+    that non-symmetric kappa (1 < kappa < n) amplifies dot-product rounding, so
+    the history tolerance there is 1e-6 and counts must still match.
+Every test calls through the C-ABI (libkcb200.so) via the package.
+"""
+
+import hashlib
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden_exists, load_json, load_npz
+
+pytestmark = pytest.mark.gpu
+INF = math.inf
+
+kc = pytest.importorskip("paper_2010_00626_b200")
+from paper_2010_00626_b200 import kernels as K  # noqa: E402
+from paper_2010_00626_b200 import (  # noqa: E402
+    CycleConfig, CycleStats, DryState, PcgConfig, ProblemSpec, Stencil9, build_state, f_cycle, gamma_cycle,
+    kappa_cycle, pcg_solve, run_cycle, solve_standalone)
+from oracle import kcycle_oracle as O  # noqa: E402
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+def kappa_of(name, n):
+    return n if name == "W" else int(name)
+
+
+# ---------------------------------------------------------------------------
+# per-kernel parity vs the reference's outputs (tests/golden/kernels.npz)
+# ---------------------------------------------------------------------------
+
+def test_kernels_bit_exact_vs_reference():
+    z = load_npz("kernels.npz")
+    meta = load_json("kernels_meta.json")
+    for key in meta["keys"]:
+        u, f, w = z[key + "_u"], z[key + "_f"], z[key + "_w"]
+        op = Stencil9(w)
+        assert np.array_equal(K.apply(op, u), z[key + "_apply"]), key
+        assert np.array_equal(K.residual(op, u, f), z[key + "_residual"]), key
+        assert np.array_equal(K.damped_jacobi_sweep(op, u, f, 0.8), z[key + "_jacobi"]), key
+        from paper_2010_00626_b200.smoother import SmootherKind, SmootherSpec
+        assert np.array_equal(K.relax(op, u, f, SmootherSpec(SmootherKind.DAMPED_JACOBI, 0.8), 3),
+                              z[key + "_relax3"]), key
+        if key + "_restrict" in z:
+            assert np.array_equal(K.restrict(f), z[key + "_restrict"]), key
+        assert np.array_equal(K.prolong(u), z[key + "_prolong"]), key
+        if key + "_coarsest" in z:
+            assert np.array_equal(K.coarsest_solve(op, f), z[key + "_coarsest"]), key
+
+
+@pytest.mark.parametrize("side", [1, 3, 7, 127, 511, 4095])
+def test_jacobi_random_sides_vs_oracle(side):
+    rng = np.random.default_rng(side)
+    w = O.hierarchy(1e-4, 45.0, 3)[1]
+    u = rng.standard_normal((side, side))
+    f = rng.random((side, side))
+    got = K.damped_jacobi_sweep(Stencil9(w), u, f, 0.8)
+    assert np.array_equal(got, O.jacobi(w, u, f, 0.8))
+
+
+@pytest.mark.parametrize("side", [3, 15, 255, 2047])
+def test_restrict_prolong_residual_vs_oracle(side):
+    rng = np.random.default_rng(side + 1)
+    w = O.hierarchy(0.1, 30.0, 2)[0]
+    u = rng.standard_normal((side, side))
+    f = rng.standard_normal((side, side))
+    assert np.array_equal(K.restrict(f), O.restrict(f))
+    assert np.array_equal(K.prolong(u), O.prolong(u))
+    assert np.array_equal(K.residual(Stencil9(w), u, f), O.residual(w, u, f))
+
+
+def test_norm2_matches_numpy():
+    rng = np.random.default_rng(3)
+    for side in (1, 7, 255, 4095):
+        a = rng.random((side, side))
+        assert K.norm2(a) == pytest.approx(np.linalg.norm(a), rel=1e-14)
+
+
+def test_tap_drop_rule_on_device():
+    """|w| <= DBL_EPSILON taps contribute nothing (scipy.ndimage)."""
+    u = np.ones((3, 3))
+    w = np.zeros((3, 3))
+    w[1, 1] = 1.0
+    w[0, 0] = np.finfo(float).eps
+    assert K.apply(Stencil9(w), u)[1, 1] == 1.0
+    w[0, 0] = 2.3e-16
+    assert K.apply(Stencil9(w), u)[1, 1] == 1.0 + 2.3e-16
+
+
+def test_coarsest_singular_raises():
+    with pytest.raises(np.linalg.LinAlgError):
+        K.coarsest_solve(Stencil9(np.zeros((3, 3))), np.ones((1, 1)))
+
+
+# ---------------------------------------------------------------------------
+# whole cycles: per-op (state protocol) and native, vs reference goldens
+# ---------------------------------------------------------------------------
+
+def _random_state_cfg(n, kname):
+    """test_cycle.py:39-46 helper: eps=0.5, phi=30, random v and f."""
+    z = load_npz("cycles.npz")
+    key = f"n{n}_k{kname}"
+    problem = ProblemSpec(epsilon=0.5, phi=30.0)
+    return z, key, problem
+
+
+@pytest.mark.parametrize("n", [3, 5])
+@pytest.mark.parametrize("kname", ["1", "2", "3", "4", "W"])
+@pytest.mark.parametrize("mode", ["per_op", "native"])
+def test_cycles_random_state_bit_exact(n, kname, mode):
+    z, key, problem = _random_state_cfg(n, kname)
+    kappa = kappa_of(kname, n)
+    config = CycleConfig(n=n, kappa=kappa)
+    state = build_state(problem, config)
+    state.v[0] = z[key + "_v0"]
+    state.f[0] = z[key + "_f0"]
+    stats = CycleStats.for_levels(n)
+    for c in range(1, 4):
+        if mode == "per_op":
+            kappa_cycle(state, 1, kappa, stats)
+        else:
+            run_cycle(state, config, stats)
+        assert np.array_equal(state.v[0], z[f"{key}_c{c}"]), (key, mode, c)
+    meta = load_json("cycles_meta.json")["random_state"][key]
+    assert stats.visits == meta["visits"]
+    assert stats.kernel_launches == meta["kernel_launches"]
+    assert stats.unknown_touches == meta["unknown_touches"]
+
+
+@pytest.mark.parametrize("n", [7, 9])
+@pytest.mark.parametrize("kname", ["1", "2", "3", "4", "W"])
+def test_cycles_paper_problem_sha_native(n, kname):
+    meta = load_json("cycles_meta.json")["paper_problem"][f"n{n}_k{kname}"]
+    kappa = kappa_of(kname, n)
+    config = CycleConfig(n=n, kappa=kappa)
+    state = build_state(ProblemSpec(1e-4, 45.0, seed=0), config)
+    m = 2 ** n - 1
+    state.v[0] = np.random.default_rng(0).random((m, m))
+    for c in range(10):
+        run_cycle(state, config, CycleStats.for_levels(n))
+        assert sha(state.v[0]) == meta["sha256"][c], (n, kname, c)
+        assert state.norm2(1) == pytest.approx(meta["norms"][c], rel=1e-13)
+
+
+def test_per_op_and_native_and_classical_forms_agree():
+    """Prop 2.1 (test_cycle.py:87-109) on the device: kappa=1 == gamma=1, kappa=2 == F,
+    kappa>=n == gamma=2 -- bit-identical iterates and identical traces."""
+    n = 6
+    problem = ProblemSpec(epsilon=0.2, phi=30.0)
+    rng = np.random.default_rng(11)
+    v0, f0 = rng.random((63, 63)), rng.random((63, 63))
+
+    def run(kind, value):
+        st = build_state(problem, CycleConfig(n=n))
+        st.v[0], st.f[0] = v0, f0
+        stats = CycleStats.for_levels(n)
+        if kind == "kappa":
+            kappa_cycle(st, 1, value, stats)
+        elif kind == "gamma":
+            gamma_cycle(st, 1, value, stats)
+        elif kind == "native":
+            run_cycle(st, CycleConfig(n=n, kappa=value), stats)
+        else:
+            f_cycle(st, 1, stats)
+        return st.v[0], stats
+
+    vk1, sk1 = run("kappa", 1)
+    vg1, sg1 = run("gamma", 1)
+    assert sk1.trace == sg1.trace and np.array_equal(vk1, vg1)
+    vk2, sk2 = run("kappa", 2)
+    vf, sf = run("f", None)
+    assert sk2.trace == sf.trace and np.array_equal(vk2, vf)
+    vn2, sn2 = run("native", 2)
+    assert sn2.trace == sk2.trace and np.array_equal(vn2, vk2)
+    vw, sw = run("gamma", 2)
+    v7, s7 = run("native", 7)
+    v6, _ = run("kappa", 6)
+    assert s7.level_sequence() == sw.level_sequence()
+    assert np.array_equal(v7, vw) and np.array_equal(v6, vw)
+
+
+def test_zero_input_is_fixed_point():
+    for kappa in (1, 3, INF):
+        config = CycleConfig(n=4, kappa=kappa)
+        state = build_state(ProblemSpec(epsilon=0.1, phi=45.0), config)
+        run_cycle(state, config, CycleStats.for_levels(4))
+        assert np.all(state.v[0] == 0.0)
+
+
+def test_single_and_two_level_hierarchies():
+    for n in (1, 2):
+        problem = ProblemSpec(1e-4, 45.0)
+        h = O.Hierarchy(O.hierarchy(1e-4, 45.0, n))
+        m = 2 ** n - 1
+        rng = np.random.default_rng(n)
+        v0, f0 = rng.random((m, m)), rng.random((m, m))
+        h.v[0], h.f[0] = v0.copy(), f0.copy()
+        for kappa in (1, 2):
+            cfg = CycleConfig(n=n, kappa=kappa)
+            st = build_state(problem, cfg)
+            st.v[0], st.f[0] = v0, f0
+            run_cycle(st, cfg, CycleStats.for_levels(n))
+            hh = O.Hierarchy(O.hierarchy(1e-4, 45.0, n))
+            hh.v[0], hh.f[0] = v0.copy(), f0.copy()
+            hh.cycle(kappa)
+            assert np.array_equal(st.v[0], hh.v[0]), (n, kappa)
+
+
+@pytest.mark.parametrize("nu1,nu2", [(0, 0), (1, 2), (3, 0), (0, 1)])
+def test_odd_and_zero_relaxation_counts(nu1, nu2):
+    """Odd sweep counts flip the ping-pong buffer across cycles; nu=0 exercises
+    the zero-guess paths of restrict/prolong."""
+    n = 8
+    problem = ProblemSpec(1e-3, 45.0)
+    cfg = CycleConfig(n=n, kappa=3, nu1=nu1, nu2=nu2)
+    st = build_state(problem, cfg)
+    m = 255
+    rng = np.random.default_rng(nu1 * 10 + nu2)
+    v0, f0 = rng.random((m, m)), rng.random((m, m))
+    st.v[0], st.f[0] = v0, f0
+    h = O.Hierarchy(O.hierarchy(1e-3, 45.0, n), nu1=nu1, nu2=nu2)
+    h.v[0], h.f[0] = v0.copy(), f0.copy()
+    for _ in range(3):
+        run_cycle(st, cfg, CycleStats.for_levels(n))
+        h.cycle(3)
+        assert np.array_equal(st.v[0], h.v[0])
+
+
+# ---------------------------------------------------------------------------
+# stand-alone solves: histories and counts vs the reference
+# ---------------------------------------------------------------------------
+
+def _check_hist(got, ref, tol):
+    got, ref = np.asarray(got), np.asarray(ref)
+    k = min(len(got), len(ref))
+    rel = np.abs(got[:k] - ref[:k]) / np.abs(ref[:k])
+    assert np.max(rel) < tol, float(np.max(rel))
+
+
+@pytest.mark.parametrize("n", [5, 7, 9])
+@pytest.mark.parametrize("kname", ["1", "2", "3", "4", "W"])
+def test_standalone_vs_reference(n, kname):
+    g = load_json("solves_small.json")["standalone"][f"n{n}_k{kname}"]
+    kappa = INF if kname == "W" else int(kname)
+    cfg = CycleConfig(n=n, kappa=kappa)
+    problem = ProblemSpec(1e-4, 45.0, seed=0)
+    rep = solve_standalone(problem, cfg, 1e10, max_cycles=5000)
+    assert rep.status == "converged"
+    assert rep.iterations == g["iters_error_1e10"]
+    _check_hist(rep.error_history, g["err_hist"], 1e-10)
+    _check_hist(rep.residual_history, g["res_hist"], 1e-10)
+    ref = g["reference_report_1e10"]
+    assert rep.stats.visits == ref["visits"]
+    assert rep.stats.kernel_launches == ref["kernel_launches"]
+    assert rep.stats.unknown_touches == ref["unknown_touches"]
+    assert rep.asymptotic_factor == pytest.approx(ref["asymptotic_factor"], rel=1e-10)
+    rep8 = solve_standalone(problem, cfg, 1e8, max_cycles=5000)
+    assert rep8.iterations == g["iters_error_1e8"]
+    rr = solve_standalone(problem, cfg, 1e10, max_cycles=5000, stop="residual")
+    assert rr.iterations == g["iters_residual_1e10"]
+
+
+def test_standalone_other_seed_angle():
+    g = load_json("solves_small.json")["standalone"]["n6_k2_eps0.1_phi30_seed3"]
+    rep = solve_standalone(ProblemSpec(0.1, 30.0, seed=3), CycleConfig(n=6, kappa=2), 1e10, max_cycles=2000)
+    assert rep.iterations == g["iters_error_1e10"]
+    _check_hist(rep.error_history, g["err_hist"], 1e-10)
+
+
+def test_standalone_zero_guess_and_divergence():
+    rep = solve_standalone(ProblemSpec(1.0, 0.0), CycleConfig(n=4, kappa=1), 1e8, initial_guess=np.zeros((15, 15)))
+    assert rep.status == "converged" and rep.iterations == 0
+    # pure coarse-grid correction without smoothing must not report convergence (test_cycle.py:225-233)
+    rep = solve_standalone(ProblemSpec(1.0, 0.0, seed=1), CycleConfig(n=2, kappa=1, nu1=0, nu2=0), 1e8,
+                           max_cycles=40)
+    ref = O.standalone(1.0, 0.0, 2, 1, target=1e8, max_cycles=40, seed=1, nu1=0, nu2=0)
+    assert rep.status == ref["status"] and rep.iterations == ref["iterations"]
+
+
+def test_kappa_inf_clamps_to_n():
+    p = ProblemSpec(0.1, 45.0, seed=2)
+    a = solve_standalone(p, CycleConfig(n=5, kappa=99), 1e6)
+    b = solve_standalone(p, CycleConfig(n=5, kappa=INF), 1e6)
+    c = solve_standalone(p, CycleConfig(n=5, kappa=5), 1e6)
+    assert a.iterations == b.iterations == c.iterations
+    assert a.final_error_norm == b.final_error_norm == c.final_error_norm
+    assert np.array_equal(a.solution, c.solution)
+
+
+@pytest.mark.parametrize("kname", ["1", "2", "3", "4", "W"])
+def test_n12_standalone_vs_reference(kname):
+    """The BASELINE size (4097^2 with boundary): iterates bit-exact at every
+    golden checkpoint, histories to 1e-10, identical counts to 1e-10 relative
+    residual (the headline rule) and to the reference's error rules."""
+    name = f"solve_n12_k{kname}.json"
+    if not golden_exists(name):
+        pytest.skip(f"{name} not generated")
+    g = load_json(name)
+    n = 12
+    kappa = INF if kname == "W" else int(kname)
+    cfg = CycleConfig(n=n, kappa=kappa)
+    problem = ProblemSpec(1e-4, 45.0, seed=0)
+    cap = len(g["err_hist"]) - 1
+    state = build_state(problem, cfg)
+    rep = solve_standalone(problem, cfg, 1e10, max_cycles=cap, stop="residual", state=state)
+    _check_hist(rep.residual_history, g["res_hist"], 1e-10)
+    _check_hist(rep.error_history, g["err_hist"], 1e-10)
+    if g["iters_residual_1e10"] is not None:
+        assert rep.iterations == g["iters_residual_1e10"]
+    else:
+        assert rep.iterations == cap
+    # bit-exact iterates at the sha checkpoints (cycle k after a fresh start)
+    m = 4095
+    v0 = np.random.default_rng(0).random((m, m))
+    state.v[0] = v0
+    done = 0
+    for k in sorted(int(s) for s in g["sha256"]):
+        if k > 60:
+            continue
+        state.run_cycles(cfg.effective_kappa, k - done)
+        done = k
+        assert sha(state.v[0]) == g["sha256"][str(k)], k
+    state.close()
+
+
+# ---------------------------------------------------------------------------
+# PCG vs the reference (krylov.py)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [5, 7, 9])
+@pytest.mark.parametrize("kname", ["1", "2", "3", "4", "W"])
+def test_pcg_vs_reference(n, kname):
+    g = load_json("solves_small.json")["pcg"][f"n{n}_k{kname}"]
+    kappa = INF if kname == "W" else int(kname)
+    cfg = CycleConfig(n=n, kappa=kappa)
+    problem = ProblemSpec(1e-4, 45.0, seed=0)
+    m = 2 ** n - 1
+    x0 = np.random.default_rng(0).random((m, m))
+    symmetric = kappa in (1,) or kappa >= n
+    tol = 1e-10 if symmetric else 1e-6
+    for stop, tgt, key, hist_key in (("error", 1e8, "error_1e8", "x_hist"), ("error", 1e10, "error_1e10", "x_hist"),
+                                     ("residual", 1e10, "residual_1e10", "r_hist")):
+        state = build_state(problem, cfg)
+        rep = pcg_solve(state, np.zeros((m, m)), PcgConfig(cycle=cfg, target_reduction=tgt, stop=stop), x0=x0)
+        assert rep.status == "converged"
+        assert rep.iterations == g["iters"][key], (stop, tgt)
+        hist = rep.error_history if stop == "error" else rep.residual_history
+        _check_hist(hist, g[hist_key], tol)
+        ref = g["reference_reports"][key]
+        assert rep.stats.visits == ref["visits"]
+        state.close()
+
+
+def test_pcg_identity_preconditioner_and_breakdown():
+    problem = ProblemSpec(1.0, 0.0, seed=0)
+    cfg = CycleConfig(n=3, kappa=1)
+    x0 = np.random.default_rng(0).random((7, 7))
+    state = build_state(problem, cfg)
+    rep = pcg_solve(state, np.zeros((7, 7)), PcgConfig(cycle=cfg, target_reduction=1e8, max_iterations=49,
+                                                        stop="error"), x0=x0, precondition=lambda r: r.copy())
+    assert rep.status == "converged" and rep.iterations <= 49
+    rep = pcg_solve(state, np.zeros((7, 7)), PcgConfig(cycle=cfg, target_reduction=1e8, stop="error"), x0=x0,
+                    precondition=lambda r: -r)
+    assert rep.status == "breakdown"
+
+
+def test_pcg_exact_single_level():
+    state = build_state(ProblemSpec(1.0, 0.0), CycleConfig(n=1))
+    rep = pcg_solve(state, np.zeros((1, 1)), PcgConfig(cycle=CycleConfig(n=1), target_reduction=1e8, stop="error"),
+                    x0=np.array([[0.7]]))
+    assert rep.status == "converged" and rep.iterations == 1
+
+
+def test_pcg_general_rhs_residual_mode():
+    problem = ProblemSpec(1.0, 0.0)
+    cfg = CycleConfig(n=4, kappa=2)
+    f = np.random.default_rng(12).random((15, 15))
+    state = build_state(problem, cfg)
+    rep = pcg_solve(state, f, PcgConfig(cycle=cfg, target_reduction=1e10, stop="residual"))
+    assert rep.status == "converged"
+    ref = O.pcg(1.0, 0.0, 4, 2, target=1e10, stop="residual", x0=np.zeros((15, 15)), f=f)
+    assert rep.iterations == ref["iterations"]
+    assert np.linalg.norm(f - O.apply(O.fine_stencil(1.0, 0.0), rep.solution)) <= 1e-10 * np.linalg.norm(f)
+
+
+def test_pcg_deterministic():
+    problem = ProblemSpec(0.2, 30.0, seed=0)
+    cfg = CycleConfig(n=6, kappa=3)
+    x0 = np.random.default_rng(0).random((63, 63))
+    out = []
+    for _ in range(2):
+        st = build_state(problem, cfg)
+        out.append(pcg_solve(st, np.zeros((63, 63)), PcgConfig(cycle=cfg, stop="error"), x0=x0))
+        st.close()
+    assert out[0].iterations == out[1].iterations
+    assert out[0].per_cycle_reduction == out[1].per_cycle_reduction
+    assert np.array_equal(out[0].solution, out[1].solution)
+
+
+# ---------------------------------------------------------------------------
+# engine invariants
+# ---------------------------------------------------------------------------
+
+def test_launch_count_independent_of_kappa_recursion_at_bottom():
+    """Host-visible launches per cycle stop growing with kappa's call count
+    once the recursion enters the persistent bottom kernel."""
+    cfg = CycleConfig(n=9, kappa=1)
+    st = build_state(ProblemSpec(1e-4, 45.0), cfg)
+    l = {k: st.launches_per_cycle(k) for k in (1, 2, 3, 4, 9)}
+    dry = {}
+    for k in (1, 2, 3, 4, 9):
+        s = CycleStats.for_levels(9)
+        kappa_cycle(DryState(9, 2, 2), 1, k, s)
+        dry[k] = s.kernel_launches
+    assert all(l[k] < dry[k] for k in l)
+    assert l[9] < 200  # W at n=9: 511 routine calls, 2555 reference launches
+
+
+def test_validation_errors_map_to_reference_types():
+    st = build_state(ProblemSpec(1e-4, 45.0), CycleConfig(n=3))
+    with pytest.raises(ValueError):
+        st.relax_level(1, -1)
+    with pytest.raises(ValueError):
+        st.restrict_residual(3)
+    with pytest.raises(ValueError):
+        st.v[0] = np.zeros((3, 3))
+    with pytest.raises(IndexError):
+        st.v[5]
+    with pytest.raises(ValueError):
+        solve_standalone(ProblemSpec(1e-4, 45.0), CycleConfig(n=3), 1.0)
