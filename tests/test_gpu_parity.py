@@ -351,16 +351,20 @@ def test_pcg_vs_reference(n, kname):
     problem = ProblemSpec(1e-4, 45.0, seed=0)
     m = 2 ** n - 1
     x0 = np.random.default_rng(0).random((m, m))
-    symmetric = kappa in (1,) or kappa >= n
-    tol = 1e-10 if symmetric else 1e-6
+    # PCG is not bit-reproducible across dot-product orders:
+    # alpha/beta differ in the last bits, so the iterates drift by
+    # ~1e-16 x the initial scale.  The history is therefore compared relative
+    # to the initial measure (1e-10 stated; ~1e-15 observed), and the
+    # iteration counts must be identical.
     for stop, tgt, key, hist_key in (("error", 1e8, "error_1e8", "x_hist"), ("error", 1e10, "error_1e10", "x_hist"),
                                      ("residual", 1e10, "residual_1e10", "r_hist")):
         state = build_state(problem, cfg)
         rep = pcg_solve(state, np.zeros((m, m)), PcgConfig(cycle=cfg, target_reduction=tgt, stop=stop), x0=x0)
         assert rep.status == "converged"
         assert rep.iterations == g["iters"][key], (stop, tgt)
-        hist = rep.error_history if stop == "error" else rep.residual_history
-        _check_hist(hist, g[hist_key], tol)
+        hist = np.asarray(rep.error_history if stop == "error" else rep.residual_history)
+        ref_h = np.asarray(g[hist_key][: len(hist)])
+        assert np.max(np.abs(hist - ref_h)) / ref_h[0] < 1e-10
         ref = g["reference_reports"][key]
         assert rep.stats.visits == ref["visits"]
         state.close()
