@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark: time to 1e-10 relative residual on rotated anisotropic diffusion
+at 4097^2 (n = 12 levels, 4095^2 interior unknowns), best kappa, B200.
+
+BASELINE.json metric: "time to 1e-10 rel. residual, rotated aniso 2D 4097^2,
+best kappa; HBM GB/s".  Workload = BASELINE config[1]:
+eps = 1e-4, phi = 45 deg, damped Jacobi omega = 0.8, nu = (2, 2), full
+coarsening, Galerkin, f = 0, v0 = default_rng(0).random((4095, 4095)).
+
+One "step" = one complete stand-alone solve from v0 until
+||f - A v_k|| <= 1e-10 ||f - A v_0||, with the per-cycle error and residual
+norms computed on the device every cycle (the stopping test needs them).
+
+  value  : device time per solve (ms), CUDA events on the engine's stream,
+           v0 already resident in HBM (restored on-device before each step).
+  e2e    : the same metric through the public API solve_standalone(...)
+           with a pinned host v0: H2D of v0 and D2H of the solution inside
+           the timed region.
+  roofline: the dominant kernel = level-1 damped-Jacobi sweep (24 B per
+           unknown algorithmic), timed with CUDA events op-by-op in an eager
+           profile cycle on the same stream right after the timed region.
+  cpu_baseline: the CPU oracle (numpy restatement of the reference, 1 core)
+           timed on a bounded sample (a few n = 12 cycles) and extrapolated
+           by the reference's own cycle count (tests/golden).
+
+`--impl reference` times the reference's CPU algorithm (the oracle port; the
+reference is pure Python/numpy and cannot travel to the GPU box) on the same
+config: each step is one n = 12 cycle; value = mean cycle time x the
+reference's cycle count to the same target.
+
+Multi-GPU (torchrun, N > 1): the stand-alone solve of this config runs as N
+independent replicas; value = max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
+METRIC = "time to 1e-10 rel. residual, rotated aniso 2D 4097², best κ; HBM GB/s"
+EPS, PHI, OMEGA = 1e-4, 45.0, 0.8
+KAPPAS = ("1", "2", "3", "4", "W")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=12)
+    ap.add_argument("--kappa", default="best", help="1,2,3,4,W or best")
+    ap.add_argument("--target", type=float, default=1e10)
+    ap.add_argument("--cpu-cycles", type=int, default=2, help="oracle cycles timed for cpu_baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="skip e2e and kappa sweep (profiling runs)")
+    return ap.parse_args()
+
+
+def kappa_value(name: str, n: int):
+    return math.inf if name == "W" else int(name)
+
+
+def golden_counts(n: int) -> dict:
+    """Reference cycle counts to 1e-10 relative residual (tests/golden, produced
+    by the real reference with tests/golden/make_golden.py)."""
+    out = {}
+    for k in KAPPAS:
+        p = os.path.join(ROOT, "tests", "golden", f"solve_n{n}_k{k}.json")
+        if os.path.exists(p):
+            with open(p) as fh:
+                d = json.load(fh)
+            out[k] = {"residual_1e10": d.get("iters_residual_1e10"), "tracked": len(d["err_hist"]) - 1,
+                      "complete": d.get("complete")}
+    return out
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            with open(self.path) as fh:
+                for line in fh:
+                    parts = [p.strip() for p in line.split(",")]
+                    if len(parts) >= 9:
+                        rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        sm = [num(r[1]) for r in rows if num(r[1]) is not None]
+        smax = [num(r[2]) for r in rows if num(r[2]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------
+
+def oracle_cycle_seconds(n: int, kname: str, cycles: int, v0=None):
+    """Time `cycles` cycles of the CPU oracle (numpy restatement of the
+    reference, oracle/kcycle_oracle.py) at level count n."""
+    import numpy as np
+
+    from oracle import kcycle_oracle as O
+    h = O.Hierarchy(O.hierarchy(EPS, PHI, n))
+    m = 2 ** n - 1
+    h.v[0] = np.random.default_rng(0).random((m, m)) if v0 is None else v0.copy()
+    k = n if kname == "W" else int(kname)
+    times = []
+    for _ in range(cycles):
+        t0 = time.perf_counter()
+        h.cycle(k)
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args, rank: int, world: int):
+    """--impl reference: the reference's CPU algorithm (oracle port), 1 core."""
+    if rank != 0:
+        return
+    n = args.n
+    counts = golden_counts(n)
+    cands = KAPPAS if args.kappa == "best" else (args.kappa,)
+    # pick the CPU-best kappa from one timed cycle each (warm-up, untimed)
+    est = {}
+    for k in cands:
+        c = counts.get(k, {}).get("residual_1e10")
+        if c is None:
+            continue
+        t = oracle_cycle_seconds(n, k, 1)[0]
+        est[k] = t * c
+    best = min(est, key=est.get) if est else cands[0]
+    count = counts[best]["residual_1e10"]
+    for _ in range(max(0, args.warmup - 1)):
+        oracle_cycle_seconds(n, best, 1)
+    times = oracle_cycle_seconds(n, best, args.steps)
+    per_cycle_ms = 1e3 * statistics.mean(times)
+    value = per_cycle_ms * count
+    line = {
+        "metric": METRIC, "value": value, "unit": "ms", "impl": "reference", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_cycle_ms, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"rotated anisotropic diffusion eps=1e-4 phi=45, {2**n+1}^2 (n={n}), "
+                               f"stand-alone kappa-cycle to 1e-10 rel. residual, best kappa",
+                   "kappa": best, "cycles_to_target": count, "n_levels": n},
+        "cpu_baseline": {"value": value, "unit": "ms", "cores": 1, "kind": "port",
+                         "sample": f"{args.steps} timed kappa={best} cycles of the numpy oracle at n={n} "
+                                   f"(4095^2), x {count} reference cycles to 1e-10 rel. residual (extrapolated)",
+                         "cpu": cpu_model(), "per_kappa_estimate_ms": {k: 1e3 * v for k, v in est.items()}},
+        "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our engine
+# ---------------------------------------------------------------------------
+
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import numpy as np
+    import torch
+
+    import paper_2010_00626_b200 as kc
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    device = local_rank
+    torch.cuda.set_device(device)
+    n = args.n
+    m = 2 ** n - 1
+    problem = kc.ProblemSpec(EPS, PHI, seed=0)
+    base_cfg = kc.CycleConfig(n=n, kappa=1)
+    state = kc.build_state(problem, base_cfg, device=device)
+    stream = torch.cuda.ExternalStream(state.stream_ptr(), device=device)
+    v0 = np.random.default_rng(0).random((m, m))
+    state.v[0] = v0
+    state.snapshot()
+
+    def solve(kname):
+        k = n if kname == "W" else int(kname)
+        state.restore()
+        return state.solve_device(k, "residual", args.target, 20000)
+
+    # kappa selection (untimed setup): one solve per candidate
+    cands = KAPPAS if args.kappa == "best" else (args.kappa,)
+    sweep = {}
+    for kname in cands:
+        k = n if kname == "W" else int(kname)
+        L = state.launches_per_cycle(k)
+        it, status, dms, err, res = solve(kname)
+        sweep[kname] = {"cycles": it, "status": status, "ms_to_solution": dms,
+                        "ms_per_cycle": dms / max(1, it), "launches_per_cycle": L,
+                        "final_rel_residual": res[-1] / res[0]}
+    best = min(sweep, key=lambda kk: sweep[kk]["ms_to_solution"])
+    if world > 1:  # every rank must run the same kappa
+        t = torch.tensor([KAPPAS.index(best)], device=f"cuda:{device}")
+        dist.broadcast(t, 0)
+        best = KAPPAS[int(t.item())]
+    kbest = n if best == "W" else int(best)
+    cycles = sweep[best]["cycles"]
+    for _ in range(args.warmup):
+        solve(best)
+
+    # ---- timed region: K solves, inputs resident in HBM ---------------------
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(device) as clk:
+        ev0.record(stream)
+        results = []
+        for _ in range(args.steps):
+            results.append(solve(best))
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = ev0.elapsed_time(ev1)
+    ms_per_step = total_ms / args.steps
+    if world > 1:
+        t = torch.tensor([ms_per_step], device=f"cuda:{device}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_per_step = float(t.item())
+    assert all(r[1] == "converged" and r[0] == cycles for r in results), "non-deterministic solve"
+    clocks = clk.summary()
+
+    # kernels launched per solve: cycle graph kernels + 4 reduction kernels per
+    # cycle (error norm, residual norm: partial + final each) + 4 initial
+    launches_per_cycle = state.launches_per_cycle(kbest)
+    gpu_launches = args.steps * (cycles * (launches_per_cycle + 4) + 4)
+
+    # ---- roofline: level-1 Jacobi sweep, eager profile on the same stream ---
+    state.restore()
+    prof = []
+    for _ in range(3):
+        prof = state.profile_cycle(kbest)
+    relax1 = [p for p in prof if p["op"] == "relax" and p["level"] == 1 and p["arg"] > 0]
+    sweeps = sum(p["arg"] for p in relax1)
+    sweep_ms = sum(p["ms"] for p in relax1) / max(1, sweeps)
+    alg_bytes = 24.0 * m * m  # read u, f; write u'
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(peaks_path):
+        with open(peaks_path) as fh:
+            peak = float(json.load(fh)["hbm_gbs"])
+        peak_src = "measured"
+    else:
+        peak, peak_src = 6650.0, "fallback"
+    achieved = alg_bytes / (sweep_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get("k_jacobi_level1_bytes_per_launch")
+    per_level = {}
+    for p in prof:
+        per_level.setdefault(str(p["level"]), 0.0)
+        per_level[str(p["level"])] += p["ms"]
+    cycle_ms_eager = sum(p["ms"] for p in prof)
+    bottom_ms = sum(p["ms"] for p in prof if p["op"] == "bottom")
+
+    # ---- e2e through the public API (pinned host v0, solution back) --------
+    e2e = None
+    if not args.quick:
+        pinned = torch.empty((m, m), dtype=torch.float64, pin_memory=True)
+        pinned.numpy()[...] = v0
+        cfg = kc.CycleConfig(n=n, kappa=math.inf if best == "W" else kbest)
+        rep = kc.solve_standalone(problem, cfg, args.target, max_cycles=20000, initial_guess=pinned.numpy(),
+                                  stop="residual", state=state)  # warm
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        walls = []
+        e0.record(stream)
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            rep = kc.solve_standalone(problem, cfg, args.target, max_cycles=20000, initial_guess=pinned.numpy(),
+                                      stop="residual", state=state)
+            walls.append((time.perf_counter() - t0) * 1e3)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / args.steps
+        assert rep.iterations == cycles and rep.status == "converged"
+        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 8 * m * m,
+               "d2h_bytes_per_step": 8 * m * m + 16 * (cycles + 1), "host_wall_ms": statistics.mean(walls),
+               "api": "paper_2010_00626_b200.solve_standalone(initial_guess=pinned host v0, stop='residual')"}
+
+    # ---- CPU baseline (oracle, rank 0, N = 1 only) ---------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        counts = golden_counts(n)
+        ref_count = counts.get(best, {}).get("residual_1e10")
+        t = oracle_cycle_seconds(n, best, args.cpu_cycles, v0)
+        per_cycle = statistics.mean(t)
+        count = ref_count if ref_count is not None else cycles
+        cpu = {"value": 1e3 * per_cycle * count, "unit": "ms", "cores": 1, "kind": "port",
+               "sample": f"{args.cpu_cycles} kappa={best} cycles of the numpy oracle at n={n} (4095^2), "
+                         f"{1e3 * per_cycle:.0f} ms/cycle x {count} reference cycles to 1e-10 rel. residual "
+                         f"(extrapolated)", "cpu": cpu_model()}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": ms_per_step, "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"rotated anisotropic diffusion eps=1e-4 phi=45, {2**n+1}^2 (n={n}), "
+                                   f"stand-alone kappa-cycle to 1e-10 rel. residual, best kappa",
+                       "kappa": best, "cycles_to_target": cycles, "n_levels": n, "nu": [2, 2], "omega": OMEGA,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (3 x 134 MB finest arrays + hierarchy > 126 MB)",
+                       "reference_cycles_to_target": golden_counts(n).get(best, {}).get("residual_1e10")},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "k_jacobi (level 1, 4095^2, 24 B/unknown algorithmic)",
+                         "kernel_ms": sweep_ms, "algorithmic_bytes_per_launch": alg_bytes},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": gpu_launches,
+            "clocks": clocks,
+            "sweep": sweep,
+            "cycle_profile": {"eager_cycle_ms": cycle_ms_eager, "bottom_kernel_ms": bottom_ms,
+                              "per_level_ms": per_level},
+        }
+        print(json.dumps(line), flush=True)
+    state.close()
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

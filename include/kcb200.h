@@ -129,6 +129,27 @@ int kc_pcg(kc_handle* h, int kappa, const double* f, const double* x0, int stop_
  * captured cycle (after kc_run_cycles/kc_solve built it). */
 int kc_cycle_launches(kc_handle* h, int kappa, int* kernels_per_cycle);
 
+/* Instrumentation: run ONE cycle eagerly (no graph) with a CUDA-event pair
+ * around every scheduled op on the handle's stream; op_kind/op_level/op_arg/
+ * op_ms receive up to max_ops entries (kinds: 0 relax, 1 restrict_residual,
+ * 2 zero_guess, 3 prolong_add, 4 coarsest, 5 bottom sub-cycle).  Used for the
+ * per-level cost fit of the run-time model and the
+ * roofline of the fine-level kernels. */
+int kc_profile_cycle(kc_handle* h, int kappa, int max_ops, int* op_kind, int* op_level, int* op_arg,
+                     double* op_ms, int* n_ops);
+
+/* the handle's CUDA stream (cudaStream_t as an opaque pointer) so a host
+ * harness can record its own events on the stream the kernels run on */
+int kc_stream(kc_handle* h, void** stream);
+
+/* keep a device-resident copy of the finest v (kc_snapshot) and copy it back
+ * (kc_restore): re-running a solve from the same start without host traffic */
+int kc_snapshot(kc_handle* h);
+int kc_restore(kc_handle* h);
+
+/* v[level] (which = KC_WHICH_V) or f[level] = 0 on the device */
+int kc_fill_zero(kc_handle* h, int level, int which);
+
 #ifdef __cplusplus
 }
 #endif

@@ -74,6 +74,11 @@ _SIGS = {
     "kc_pcg": (C.c_int, [_h, C.c_int, _dp, _dp, C.c_int, C.c_double, C.c_int, PRECOND_FN, C.c_void_p,
                          _dp, _ip, _ip, _ip, _dp, _dp]),
     "kc_cycle_launches": (C.c_int, [_h, C.c_int, _ip]),
+    "kc_profile_cycle": (C.c_int, [_h, C.c_int, C.c_int, _ip, _ip, _ip, _dp, _ip]),
+    "kc_stream": (C.c_int, [_h, C.POINTER(C.c_void_p)]),
+    "kc_fill_zero": (C.c_int, [_h, C.c_int, C.c_int]),
+    "kc_snapshot": (C.c_int, [_h]),
+    "kc_restore": (C.c_int, [_h]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

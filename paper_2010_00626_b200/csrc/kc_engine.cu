@@ -71,6 +71,7 @@ struct kc_handle {
   std::string err;
   // PCG vectors (lazily allocated), finest padded layout
   double *x = nullptr, *p = nullptr, *ap = nullptr, *fb = nullptr;
+  double* snap = nullptr;  // kc_snapshot copy of the finest v
 };
 
 #define KC_FAIL(h, code, ...)                     \
@@ -545,6 +546,7 @@ int kc_destroy(kc_handle* h) {
   cudaFree(h->p);
   cudaFree(h->ap);
   cudaFree(h->fb);
+  cudaFree(h->snap);
   cudaFree(h->d_part);
   cudaFree(h->d_scal);
   if (h->h_scal) cudaFreeHost(h->h_scal);
@@ -708,6 +710,88 @@ int kc_time_cycles(kc_handle* h, int kappa, int count, double* ms) {
   float t = 0.f;
   KC_CUDA(h, cudaEventElapsedTime(&t, h->ev0, h->ev1));
   *ms = t;
+  return KC_OK;
+}
+
+int kc_profile_cycle(kc_handle* h, int kappa, int max_ops, int* op_kind, int* op_level, int* op_arg,
+                     double* op_ms, int* n_ops) {
+  if (!h || !n_ops) return KC_EINVAL;
+  if (kappa < 1) KC_FAIL(h, KC_EINVAL, "cycle counter must be >= 1, got %d", kappa);
+  if (kappa > h->n) kappa = h->n;
+  std::vector<Op> ops;
+  flatten(h, 0, kappa, ops);
+  std::vector<cudaEvent_t> ev(ops.size() + 1);
+  for (auto& e : ev) KC_CUDA(h, cudaEventCreate(&e));
+  for (int j = 1; j < h->n; ++j) h->L[j].cur = 0;
+  int rc = KC_OK;
+  KC_CUDA(h, cudaEventRecord(ev[0], h->stream));
+  for (size_t i = 0; i < ops.size(); ++i) {
+    if ((rc = ex_op(h, ops[i]))) break;
+    KC_CUDA(h, cudaEventRecord(ev[i + 1], h->stream));
+  }
+  cudaError_t se = cudaStreamSynchronize(h->stream);
+  int k = 0;
+  if (!rc && se == cudaSuccess) {
+    for (size_t i = 0; i < ops.size() && k < max_ops; ++i, ++k) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, ev[i], ev[i + 1]);
+      if (op_kind) op_kind[k] = ops[i].kind;
+      if (op_level) op_level[k] = ops[i].level + 1;
+      if (op_arg) op_arg[k] = ops[i].a;
+      if (op_ms) op_ms[k] = t;
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  for (int j = 1; j < h->n; ++j) {
+    h->L[j].vzero = true;
+    h->L[j].cur = 0;
+  }
+  if (rc) return rc;
+  if (se != cudaSuccess) KC_FAIL(h, KC_ECUDA, "profile cycle: %s", cudaGetErrorString(se));
+  *n_ops = (int)ops.size();
+  return KC_OK;
+}
+
+int kc_snapshot(kc_handle* h) {
+  if (!h) return KC_EINVAL;
+  Level& L = h->L[0];
+  int rc;
+  if ((rc = ex_materialize(h, 0))) return rc;
+  if (!h->snap) {
+    cudaError_t ce = cudaMalloc(&h->snap, L.elems * sizeof(double));
+    if (ce != cudaSuccess) KC_FAIL(h, KC_ENOMEM, "cudaMalloc snapshot: %s", cudaGetErrorString(ce));
+  }
+  KC_CUDA(h, cudaMemcpyAsync(h->snap, L.v[L.cur], L.elems * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  return KC_OK;
+}
+
+int kc_restore(kc_handle* h) {
+  if (!h) return KC_EINVAL;
+  if (!h->snap) KC_FAIL(h, KC_EINVAL, "kc_restore without kc_snapshot");
+  Level& L = h->L[0];
+  KC_CUDA(h, cudaMemcpyAsync(L.v[L.cur], h->snap, L.elems * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  L.vzero = false;
+  return KC_OK;
+}
+
+int kc_stream(kc_handle* h, void** stream) {
+  if (!h || !stream) return KC_EINVAL;
+  *stream = (void*)h->stream;
+  return KC_OK;
+}
+
+int kc_fill_zero(kc_handle* h, int level, int which) {
+  if (!h) return KC_EINVAL;
+  int rc = check_level(h, level);
+  if (rc) return rc;
+  Level& L = h->L[level - 1];
+  if (which == KC_WHICH_F) {
+    k_zero<<<grid2(L.m, L.m), kBlock, 0, h->stream>>>(L.f, L.m, L.P);
+    KC_LAUNCH_CHECK(h);
+  } else {
+    L.vzero = true;
+    if ((rc = ex_materialize(h, level - 1))) return rc;
+  }
   return KC_OK;
 }
 

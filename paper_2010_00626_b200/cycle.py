@@ -295,6 +295,48 @@ class CudaGridState:
     def sync(self):
         N.check(N.lib.kc_sync(self._h), self._h)
 
+    def stream_ptr(self) -> int:
+        """cudaStream_t of the handle (for torch.cuda.ExternalStream timing)."""
+        p = C.c_void_p()
+        N.check(N.lib.kc_stream(self._h, C.byref(p)), self._h)
+        return p.value or 0
+
+    def solve_device(self, kappa: int, stop: str = "error", target_reduction: float = 1e8,
+                     max_cycles: int = 10000):
+        """kc_solve on the current v[0]/f[0]: (iterations, status, device_ms, err_hist, res_hist)."""
+        err = np.zeros(max_cycles + 1)
+        res = np.zeros(max_cycles + 1)
+        it, st, dms = C.c_int(), C.c_int(), C.c_double()
+        N.check(N.lib.kc_solve(self._h, int(kappa), N.KC_STOP_ERROR if stop == "error" else N.KC_STOP_RESIDUAL,
+                               float(target_reduction), int(max_cycles), N.dptr(err), N.dptr(res),
+                               C.byref(it), C.byref(st), C.byref(dms)), self._h)
+        k = it.value
+        return k, N.STATUS_NAMES[st.value], dms.value, err[: k + 1].tolist(), res[: k + 1].tolist()
+
+    def snapshot(self):
+        """Keep a device copy of the finest v (restore() puts it back)."""
+        N.check(N.lib.kc_snapshot(self._h), self._h)
+
+    def restore(self):
+        N.check(N.lib.kc_restore(self._h), self._h)
+
+    def fill_zero(self, level: int = 1, which: str = "f"):
+        N.check(N.lib.kc_fill_zero(self._h, level, N.KC_WHICH_F if which == "f" else N.KC_WHICH_V), self._h)
+
+    OP_NAMES = ("relax", "restrict_residual", "zero_guess", "prolong_add", "coarsest", "bottom")
+
+    def profile_cycle(self, kappa: int) -> list[dict]:
+        """One eager cycle with CUDA events around every scheduled op."""
+        cap = 1 << 16
+        kind = (C.c_int * cap)()
+        lev = (C.c_int * cap)()
+        arg = (C.c_int * cap)()
+        ms = (C.c_double * cap)()
+        nops = C.c_int()
+        N.check(N.lib.kc_profile_cycle(self._h, int(kappa), cap, kind, lev, arg, ms, C.byref(nops)), self._h)
+        return [{"op": self.OP_NAMES[kind[i]], "level": lev[i], "arg": arg[i], "ms": ms[i]}
+                for i in range(min(nops.value, cap))]
+
 
 GridState = CudaGridState
 
@@ -440,31 +482,21 @@ def solve_standalone(
     else:
         if initial_guess.shape != (ny, nx):
             raise ValueError(f"initial guess shape {initial_guess.shape} != {(ny, nx)}")
-        v0 = initial_guess.astype(float).copy()
+        v0 = N.as_f64c(initial_guess)  # the upload is the reference's defensive copy
     state.v[0] = v0
     if not fresh:  # a fresh hierarchy starts with f = 0 on every level
-        state.f[0] = np.zeros((ny, nx))
+        state.fill_zero(1, "f")
     kappa = config.effective_kappa
     state.launches_per_cycle(kappa)  # capture the cycle graph outside the timed span
 
-    err = np.zeros(max_cycles + 1)
-    res = np.zeros(max_cycles + 1)
-    it = C.c_int()
-    st = C.c_int()
-    dms = C.c_double()
     t0 = time.perf_counter()
-    N.check(N.lib.kc_solve(state._h, kappa, N.KC_STOP_ERROR if stop == "error" else N.KC_STOP_RESIDUAL,
-                           float(target_reduction), int(max_cycles), N.dptr(err), N.dptr(res),
-                           C.byref(it), C.byref(st), C.byref(dms)), state._h)
+    k, status, dev_ms, err_hist, res_hist = state.solve_device(kappa, stop, target_reduction, max_cycles)
     wall_ms = (time.perf_counter() - t0) * 1e3
-    k = it.value
-    err_hist = err[: k + 1].tolist()
-    res_hist = res[: k + 1].tolist()
     stats = CycleStats.for_levels(config.n)
     stats.absorb(state.cycle_stats(kappa), k)
     reductions = _reductions(err_hist if stop == "error" else res_hist)
     return SolveReport(
-        status=N.STATUS_NAMES[st.value],
+        status=status,
         iterations=k,
         initial_error_norm=err_hist[0],
         final_error_norm=err_hist[k],
@@ -476,7 +508,7 @@ def solve_standalone(
         error_history=err_hist,
         residual_history=res_hist,
         stop=stop,
-        device_time_ms=dms.value,
+        device_time_ms=dev_ms,
     )
 
 

@@ -1,0 +1,66 @@
+"""Summarise ncu outputs into profiles/: a launch list CSV (gpu__time_duration
+per launch) -> per-kernel totals/shares; a --set full report -> key metrics.
+
+  python tools/ncu_summary.py launches gpurun_out/launches.csv
+  python tools/ncu_summary.py full gpurun_out/prof.ncu-rep
+"""
+
+import collections
+import csv
+import json
+import subprocess
+import sys
+
+SCALE = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6}
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hdr, data = None, []
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            data.append(dict(zip(hdr, r)))
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for d in data:
+        if d["Metric Name"] != "gpu__time_duration.sum":
+            continue
+        name = d["Kernel Name"].split("(")[0].replace("void ", "")
+        us = float(d["Metric Value"].replace(",", "")) * SCALE.get(d["Metric Unit"], 1.0)
+        agg[name][0] += 1
+        agg[name][1] += us
+    tot = sum(v[1] for v in agg.values())
+    out = {"total_us": tot, "launches": sum(v[0] for v in agg.values()), "kernels": {}}
+    for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
+        out["kernels"][k] = {"launches": v[0], "us": v[1], "share": v[1] / tot if tot else 0.0}
+    return out
+
+
+FULL = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "lts__t_bytes.sum", "l1tex__t_bytes.sum",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__occupancy_limit_registers",
+        "smsp__inst_executed.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]
+
+
+def full(path):
+    txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(txt.splitlines()))
+    hdr, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        rec = {"kernel": r[hdr.index("Kernel Name")] if "Kernel Name" in hdr else ""}
+        for w in FULL:
+            if w in hdr:
+                i = hdr.index(w)
+                rec[w] = f"{r[i]} {units[i]}".strip()
+        res.append(rec)
+    return res
+
+
+if __name__ == "__main__":
+    kind, path = sys.argv[1], sys.argv[2]
+    print(json.dumps(launches(path) if kind == "launches" else full(path), indent=1))
