@@ -3,194 +3,315 @@
 //
 // Below a side of KC_BOT_MAX_M (63) every remaining level (v ping-pong pair
 // and f, each with its zero ghost ring) fits in shared memory (~137 KB for
-// 63^2 .. 1^2).  One CTA of 1024 threads loads f (and v unless it is the zero
-// guess) of the entry level from HBM, runs the reference's kappa_cycle
-// recursion (cycle.py:204-220) as an explicit stack on the device, and writes
-// v back.  Every routine call of the bottom levels therefore costs CTA
-// barriers instead of kernel launches, so host-visible launches per cycle no
-// longer grow with kappa's polynomial call count.
+// 63^2 .. 1^2).  One CTA loads f (and v unless it is the zero guess) of the
+// entry level from HBM, runs the reference's kappa_cycle recursion
+// (cycle.py:204-220) as a device-side state machine, and writes v back.
+// Every routine call of the bottom levels costs barriers instead of kernel
+// launches, so host-visible launches per cycle no longer grow with kappa's
+// polynomial call count.
 //
+// Design for latency (measured on B200, tools/micro: fp64 dependent op 8
+// cycles, __syncthreads 47-115, __syncwarp 31, a bare 3x3 Jacobi phase ~340):
+//  * one control loop yields one phase per iteration and executes it at a
+//    single inlined site, so the kernel is small (instruction-cache
+//    resident) and has no calls; the recursion stack is bit-packed in a
+//    register (stage, counter and sweep count per level);
+//  * the warps that work on a level scale with its size: 16 warps for
+//    sides >= 31 (CTA barrier), 8 warps for 15 (named barrier), 1 warp for
+//    sides <= 7 (__syncwarp), and idle warps skip the phase;
+//  * stencil phases are register-blocked 4 rows per thread (3 new loads per
+//    row instead of 9), halving shared-memory traffic on the 63^2/31^2 levels;
+//  * the coarsest 1x1 solve is folded into its parent's restriction.
 // Per-point arithmetic is identical to the HBM kernels (kc_common.cuh), so
 // iterates stay bit-identical to the reference.  The redundant second
 // coarsest solve under level n-1 (cycle.py:7-10) recomputes the identical
-// f/center and is skipped; CycleStats still counts it (host side).
+// f/center and is skipped; CycleStats still counts it.
 #pragma once
 #include "kc_common.cuh"
 
 #define KC_BOT_MAX_M 63
 #define KC_BOT_MAXLEV 8
-#define KC_BOT_THREADS 1024
+#define KC_BOT_THREADS 512
+#define KC_BOT_WARPS (KC_BOT_THREADS / 32)
+#define KC_BOT_RB 4  // rows per thread in stencil phases
 
-struct BotLevel {
-  int m;      // interior side
-  int S;      // smem row stride (m + 2)
-  int ov[2];  // smem offsets (doubles) of the v ping-pong pair, at element (-1,-1)
-  int of;     // smem offset of f
-  St9 s;
-};
+#define KC_BOT_MAXPH 4096  // phase descriptors per launch (host-checked)
 
 struct BotParams {
   int nlev;  // levels resident in smem: entry level .. coarsest
-  int nu1, nu2;
-  int total;  // smem doubles
-  BotLevel lv[KC_BOT_MAXLEV];
+  St9 st[KC_BOT_MAXLEV];
   double* gv;        // entry-level v in HBM (padded, pitch gP): read unless v_zero, always written
   const double* gf;  // entry-level f in HBM
   int gP;
-  int v_zero;    // entry-level v is the zero guess
-  int nk;        // number of consecutive kappa_cycle calls at the entry level (1 or 2)
-  int kap[2];    // their counters (kappa, kappa-1)
+  int v_zero;        // entry-level v is the zero guess
+  const unsigned* sched;  // host-built phase list (bot_schedule), device memory
+  int nsched;
+  int final_cur;     // buffer holding the entry level's v after the schedule
 };
 
-__device__ __forceinline__ double* bl_v(double* sm, const BotLevel& L, int cur) { return sm + L.ov[cur] + L.S + 1; }
-__device__ __forceinline__ double* bl_f(double* sm, const BotLevel& L) { return sm + L.of + L.S + 1; }
+// smem geometry of level d (entry side m0): side m_d = ((m0+1) >> d) - 1,
+// stride S = m+2, three (m+2)^2 arrays v0, v1, f.
+__host__ __device__ __forceinline__ int bot_m(int m0, int d) { return ((m0 + 1) >> d) - 1; }
+__host__ __device__ __forceinline__ int bot_off(int m0, int d) {
+  int off = 0;
+  for (int j = 0; j < d; ++j) {
+    const int s = bot_m(m0, j) + 2;
+    off += 3 * s * s;
+  }
+  return off;
+}
+__host__ __device__ __forceinline__ int bot_smem_doubles(int m0, int nlev) { return bot_off(m0, nlev); }
+__host__ __device__ __forceinline__ int bot_warps(int m) {
+  return m >= 31 ? KC_BOT_WARPS : (m >= 15 ? 8 : 1);  // 2 warps at m = 7 measured slower
+}
 
-__global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp) {
+__device__ __forceinline__ void bot_sync(int g) {
+  if (g == KC_BOT_WARPS) __syncthreads();
+  else if (g == 1) __syncwarp();
+  else if (g == 8) asm volatile("bar.sync 1, 256;" ::: "memory");
+  else asm volatile("bar.sync 2, 64;" ::: "memory");
+}
+
+#ifdef KC_BOT_TRACE
+__device__ long long kc_bot_trace[KC_BOT_TRACE];
+__device__ int kc_bot_trace_op[KC_BOT_TRACE];
+__device__ int kc_bot_trace_n;
+__device__ long long kc_bot_trace_end[KC_BOT_TRACE];
+#endif
+
+// Phase descriptor (host-built by bot_schedule in kc_engine.cu):
+//  bits 0-2 op (PH_*), 3-5 level d, 6 src buffer, 7 zero guess, 8 child buffer
+//  (prolong), 9 child is the 1x1 coarsest (restrict), 10-11 warp group code.
+enum BotOp { PH_JACOBI = 0, PH_RESID = 1, PH_RESTRICT = 2, PH_PROLONG = 3, PH_JOIN = 4 };
+__host__ __device__ __forceinline__ unsigned bot_desc(int op, int d, int src, int zero, int cbuf, int cc, int g) {
+  const unsigned gc = g >= KC_BOT_WARPS ? 3u : (g >= 8 ? 2u : (g >= 2 ? 1u : 0u));
+  return (unsigned)op | ((unsigned)d << 3) | ((unsigned)src << 6) | ((unsigned)zero << 7) | ((unsigned)cbuf << 8) |
+         ((unsigned)cc << 9) | (gc << 10);
+}
+__device__ __forceinline__ int bot_desc_g(unsigned e) {
+  const unsigned gc = (e >> 10) & 3u;
+  return gc == 3u ? KC_BOT_WARPS : (gc == 2u ? 8 : (gc == 1u ? 2 : 1));
+}
+
+#include <vector>
+// Flatten kappa_cycle over the smem-resident levels (cycle.py:204-220) into
+// the bottom kernel's phase list (kc_bottom.cuh), tracking ping-pong buffers
+// and zero guesses exactly like the executor does for the HBM levels.
+struct BotBuilder {  // host side
+  int m0, nlev, nu1, nu2;
+  unsigned cur = 0, vz = 0;
+  int gprev = KC_BOT_WARPS;
+  std::vector<unsigned> out;
+  void emit(int op, int d, int src, int zero, int cbuf, int cc) {
+    const int g = bot_warps(bot_m(m0, d));
+    if (g > gprev) out.push_back(bot_desc(PH_JOIN, 0, 0, 0, 0, 0, g));
+    gprev = g;
+    out.push_back(bot_desc(op, d, src, zero, cbuf, cc, g));
+  }
+  void relax(int d, int count) {
+    for (int i = 0; i < count; ++i) {
+      emit(PH_JACOBI, d, (cur >> d) & 1u, (vz >> d) & 1u, 0, 0);
+      vz &= ~(1u << d);
+      cur ^= 1u << d;
+    }
+  }
+  void rec(int d, int kap) {
+    relax(d, nu1);
+    const int c = (cur >> d) & 1u;
+    const int z = (vz >> d) & 1u;
+    if (!z) emit(PH_RESID, d, c, 0, 0, 0);  // residual into buffer c^1
+    const int cc = (d + 1 == nlev - 1);
+    emit(PH_RESTRICT, d, c ^ 1, z, 0, cc);
+    cur &= ~(1u << (d + 1));
+    if (cc) {
+      vz &= ~(1u << (d + 1));  // both coarsest calls: one f/center inside the restriction
+    } else {
+      vz |= 1u << (d + 1);
+      rec(d + 1, kap);
+      if (kap > 1) rec(d + 1, kap - 1);
+    }
+    emit(PH_PROLONG, d, (cur >> d) & 1u, (vz >> d) & 1u, (cur >> (d + 1)) & 1u, 0);
+    vz &= ~(1u << d);
+    relax(d, nu2);
+  }
+};
+
+
+// y = i / m for i < 2^12, m <= 64: float reciprocal, exact for these ranges
+__device__ __forceinline__ int bot_div(int i, float inv) { return (int)(((float)i + 0.5f) * inv); }
+
+// Jacobi sweep (zero guess folded) or residual on an m x m smem level.
+// RB rows per thread share their loads (3 new loads per row).
+template <int RB>
+__device__ __forceinline__ void bot_stencil(bool jac, bool zero, const double* __restrict__ u, double* __restrict__ o,
+                                            const double* __restrict__ f, int m, int S, float inv, const St9& st,
+                                            int tid, int nth, int nitems) {
+  for (int it = tid; it < nitems; it += nth) {
+    const int rb = bot_div(it, inv);  // it / m
+    const int x = it - rb * m;
+    const int y0 = rb * RB;
+    if (jac && zero) {
+#pragma unroll
+      for (int k = 0; k < RB; ++k)
+        if (y0 + k < m) o[(y0 + k) * S + x] = kc_jacobi_zero(f[(y0 + k) * S + x], st.c);
+      continue;
+    }
+    const double* pu = u + y0 * S + x;
+    double a0 = pu[-S - 1], a1 = pu[-S], a2 = pu[-S + 1];
+    double b0 = pu[-1], b1 = pu[0], b2 = pu[1];
+#pragma unroll
+    for (int k = 0; k < RB; ++k) {
+      if (y0 + k < m) {
+        const double* pn = pu + (k + 1) * S;
+        const double c0 = pn[-1], c1 = pn[0], c2 = pn[1];
+        const int i = (y0 + k) * S + x;
+        const double au = kc_sum9(st, a0, a1, a2, b0, b1, b2, c0, c1, c2);
+        o[i] = jac ? kc_jacobi_pt(b1, f[i], au, st.c) : DSUB(f[i], au);
+        a0 = b0; a1 = b1; a2 = b2;
+        b0 = c0; b1 = c1; b2 = c2;
+      }
+    }
+  }
+}
+
+// per-level constants precomputed once per launch (keeps the per-phase
+// dependent integer chain short: one LDS.128 pair instead of address math)
+struct BotLv {
+  int m, S, vo0, vo1;  // side, stride, smem offsets of v buffers (interior origin)
+  int fo, nitem1, nitem4, pad;  // f offset, items for RB=1 / RB=4 stencil loops
+  float inv, invc, invn, padf;  // 1/m, 1/m_child, 1/(m_child+1)
+};
+
+__global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp, int m0) {
   extern __shared__ double sm[];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < bp.total; i += KC_BOT_THREADS) sm[i] = 0.0;
-  __syncthreads();
-  {
-    const BotLevel& L = bp.lv[0];
-    double* v = bl_v(sm, L, 0);
-    double* f = bl_f(sm, L);
-    for (int y = ty; y < L.m; y += 32)
-      for (int x = tx; x < L.m; x += 32) {
-        const size_t gi = kc_idx(bp.gP, y, x);
-        f[y * L.S + x] = bp.gf[gi];
-        if (!bp.v_zero) v[y * L.S + x] = bp.gv[gi];
-      }
-  }
-  __syncthreads();
-
-  unsigned cur = 0u;                          // bit l: current v buffer of level l
-  unsigned vz = bp.v_zero ? 1u : 0u;          // bit l: v of level l is the zero guess
+  __shared__ St9 tab[KC_BOT_MAXLEV];
+  __shared__ BotLv lv[KC_BOT_MAXLEV];
+  __shared__ unsigned sched[KC_BOT_MAXPH];
   const int nlev = bp.nlev;
-
-  // relax `count` damped-Jacobi sweeps on level l (smoother.py:138-148)
-  auto relax = [&](int l, int count) {
-    const BotLevel& L = bp.lv[l];
-    const double* f = bl_f(sm, L);
-    for (int it = 0; it < count; ++it) {
-      const int c = (cur >> l) & 1u;
-      const double* u = bl_v(sm, L, c);
-      double* o = bl_v(sm, L, c ^ 1);
-      if ((vz >> l) & 1u) {
-        for (int y = ty; y < L.m; y += 32)
-          for (int x = tx; x < L.m; x += 32) o[y * L.S + x] = kc_jacobi_zero(f[y * L.S + x], L.s.c);
-        vz &= ~(1u << l);
-      } else {
-        for (int y = ty; y < L.m; y += 32)
-          for (int x = tx; x < L.m; x += 32) {
-            const int i = y * L.S + x;
-            o[i] = kc_jacobi_pt(u[i], f[i], kc_apply9(u + i, L.S, L.s), L.s.c);
-          }
-      }
-      cur ^= (1u << l);
-      __syncthreads();
-    }
-  };
-
-  // f[l+1] = restrict(f[l] - A v[l]) (cycle.py:165-168); r staged in the free buffer
-  auto restrict_residual = [&](int l) {
-    const BotLevel& L = bp.lv[l];
-    const BotLevel& C = bp.lv[l + 1];
-    const double* f = bl_f(sm, L);
-    const double* r = f;  // zero guess: r = f - (+0) = f exactly
-    if (!((vz >> l) & 1u)) {
-      const int c = (cur >> l) & 1u;
-      const double* u = bl_v(sm, L, c);
-      double* t = bl_v(sm, L, c ^ 1);
-      for (int y = ty; y < L.m; y += 32)
-        for (int x = tx; x < L.m; x += 32) {
-          const int i = y * L.S + x;
-          t[i] = DSUB(f[i], kc_apply9(u + i, L.S, L.s));
-        }
-      __syncthreads();
-      r = t;
-    }
-    double* fc = bl_f(sm, C);
-    for (int q = ty; q < C.m; q += 32)
-      for (int p = tx; p < C.m; p += 32) {
-        const double* rc = r + (2 * q + 1) * L.S + (2 * p + 1);
-        const double* rs = rc - L.S;
-        const double* rn = rc + L.S;
-        fc[q * C.S + p] = kc_fw(rs[-1], rs[0], rs[1], rc[-1], rc[0], rc[1], rn[-1], rn[0], rn[1]);
-      }
-    __syncthreads();
-  };
-
-  // v[l] += prolong(v[l+1]) (cycle.py:174-176)
-  auto prolong_add = [&](int l) {
-    const BotLevel& L = bp.lv[l];
-    const BotLevel& C = bp.lv[l + 1];
-    double* v = bl_v(sm, L, (cur >> l) & 1u);
-    const double* vc = bl_v(sm, C, (cur >> (l + 1)) & 1u);
-    const bool z = (vz >> l) & 1u;
-    auto cp = [&](int q, int p) { return vc[q * C.S + p]; };
-    for (int y = ty; y < L.m; y += 32)
-      for (int x = tx; x < L.m; x += 32) {
-        const int i = y * L.S + x;
-        v[i] = DADD(z ? 0.0 : v[i], kc_prolong_val(y, x, cp));
-      }
-    vz &= ~(1u << l);
-    __syncthreads();
-  };
-
-  for (int kk = 0; kk < bp.nk; ++kk) {
-    // explicit stack: depth d == level offset; 4 bits kappa + 2 bits phase per depth
-    int kap[KC_BOT_MAXLEV];
-    int ph[KC_BOT_MAXLEV];
-    int d = 0;
-    kap[0] = bp.kap[kk];
-    ph[0] = 0;
-    bool skip_coarsest = false;
-    while (d >= 0) {
-      if (d == nlev - 1) {  // coarsest: exact 1x1 solve (cycle.py:182-190)
-        if (!skip_coarsest) {
-          const BotLevel& L = bp.lv[d];
-          if (threadIdx.x == 0) {
-            double* v = bl_v(sm, L, (cur >> d) & 1u);
-            v[0] = __ddiv_rn(bl_f(sm, L)[0], L.s.center);
-          }
-          vz &= ~(1u << d);
-          __syncthreads();
-        }
-        skip_coarsest = false;
-        --d;
-        continue;
-      }
-      if (ph[d] == 0) {  // kappa_cycle lines: relax nu1, restrict, zero guess, first call
-        relax(d, bp.nu1);
-        restrict_residual(d);
-        vz |= (1u << (d + 1));
-        cur &= ~(1u << (d + 1));
-        ph[d] = 1;
-        kap[d + 1] = kap[d];
-        ph[d + 1] = 0;
-        ++d;
-        continue;
-      }
-      if (ph[d] == 1) {
-        ph[d] = 2;
-        if (kap[d] > 1) {  // second call with kappa-1, continuing from v[l+1]
-          kap[d + 1] = kap[d] - 1;
-          ph[d + 1] = 0;
-          ++d;
-          skip_coarsest = (d == nlev - 1);
-          continue;
-        }
-      }
-      prolong_add(d);
-      relax(d, bp.nu2);
-      --d;
+  const int total = bot_smem_doubles(m0, nlev);
+  for (int i = threadIdx.x; i < total; i += KC_BOT_THREADS) sm[i] = 0.0;
+  for (int i = threadIdx.x; i < bp.nsched; i += KC_BOT_THREADS) sched[i] = bp.sched[i];
+  if (threadIdx.x < nlev) {
+    const int d = threadIdx.x;
+    tab[d] = bp.st[d];
+    const int m = bot_m(m0, d), S = m + 2, base = bot_off(m0, d);
+    const int mc = d + 1 < nlev ? bot_m(m0, d + 1) : 1;
+    BotLv L;
+    L.m = m;
+    L.S = S;
+    L.vo0 = base + S + 1;
+    L.vo1 = base + S * S + S + 1;
+    L.fo = base + 2 * S * S + S + 1;
+    L.nitem1 = m * m;
+    L.nitem4 = m * ((m + 3) / 4);
+    L.pad = 0;
+    L.inv = 1.0f / (float)m;
+    L.invc = 1.0f / (float)mc;
+    L.invn = 1.0f / (float)(mc + 1);
+    L.padf = 0.f;
+    lv[d] = L;
+  }
+  __syncthreads();
+  {
+    const int S = m0 + 2;
+    double* v = sm + S + 1;
+    double* f = sm + 2 * S * S + S + 1;
+    for (int i = threadIdx.x; i < m0 * m0; i += KC_BOT_THREADS) {
+      const int y = i / m0, x = i - y * m0;
+      const size_t gi = kc_idx(bp.gP, y, x);
+      f[y * S + x] = bp.gf[gi];
+      if (!bp.v_zero) v[y * S + x] = bp.gv[gi];
     }
   }
+  __syncthreads();
 
+  const int warp = threadIdx.x >> 5;
+  const int tid = threadIdx.x;
+#ifdef KC_BOT_TRACE
+  int tr_n = 0;
+#endif
+  if (nlev == 1) {  // the entry level is the coarsest (n == 1): f / center
+    if (threadIdx.x == 0) sm[4] = __ddiv_rn(sm[2 * 9 + 4], tab[0].center);
+  }
+  // replay the schedule: a warp takes part in the phases of its group only;
+  // JOIN entries gather a larger group before it resumes work
+  unsigned e_next = bp.nsched > 0 ? sched[0] : 0u;
+  for (int k = 0; k < bp.nsched; ++k) {
+    const unsigned e = e_next;
+    if (k + 1 < bp.nsched) e_next = sched[k + 1];
+    const int g = bot_desc_g(e);
+    if (warp >= g) continue;
+    const int op = e & 7u;
+    if (op == PH_JOIN) {
+      bot_sync(g);
+      continue;
+    }
+    const int d = (e >> 3) & 7u;
+    const int src = (e >> 6) & 1u;
+    const bool zero = (e >> 7) & 1u;
+    const BotLv L = lv[d];
+    const int m = L.m, S = L.S;
+    const int nth = g * 32;
+    const double* f = sm + L.fo;
+    double* u = sm + (src ? L.vo1 : L.vo0);
+#ifdef KC_BOT_TRACE
+    if (threadIdx.x == 0 && tr_n < KC_BOT_TRACE) {
+      kc_bot_trace[tr_n] = clock64();
+      kc_bot_trace_op[tr_n] = op * 16 + d;
+      kc_bot_trace_n = ++tr_n;
+    }
+#endif
+    if (op <= PH_RESID) {
+      double* o = sm + (src ? L.vo0 : L.vo1);
+      const St9 st = tab[d];
+      if (m >= 31) bot_stencil<4>(op == PH_JACOBI, zero, u, o, f, m, S, L.inv, st, tid, nth, L.nitem4);
+      else bot_stencil<1>(op == PH_JACOBI, zero, u, o, f, m, S, L.inv, st, tid, nth, L.nitem1);
+    } else if (op == PH_RESTRICT) {  // fc = FW(r); r in buffer src, or f itself on a zero guess
+      const BotLv C = lv[d + 1];
+      const int mc = C.m, SC = C.S;
+      double* fc = sm + C.fo;
+      double* vc = sm + C.vo0;  // buffer 0
+      const double* r = zero ? f : u;
+      const bool cc = (e >> 9) & 1u;
+      for (int i = tid; i < C.nitem1; i += nth) {
+        const int q = bot_div(i, L.invc), p = i - q * mc;
+        const double* rc = r + (2 * q + 1) * S + (2 * p + 1);
+        const double* rs = rc - S;
+        const double* rn = rc + S;
+        const double fv = kc_fw(rs[-1], rs[0], rs[1], rc[-1], rc[0], rc[1], rn[-1], rn[0], rn[1]);
+        fc[q * SC + p] = fv;
+        if (cc) vc[0] = __ddiv_rn(fv, tab[d + 1].center);  // coarsest_solve, cycle.py:182-190
+      }
+    } else {  // PH_PROLONG: v += P vc, one coarse cell (2x2 fine points) per item
+      const BotLv C = lv[d + 1];
+      const int mc = C.m, SC = C.S;
+      const int cbuf = (e >> 8) & 1u;
+      const double* vc = sm + (cbuf ? C.vo1 : C.vo0);
+      const int nc = mc + 1;
+      for (int i = tid; i < nc * nc; i += nth) {
+        const int q = bot_div(i, L.invn), p = i - q * nc;
+        const double c00 = vc[(q - 1) * SC + p - 1], c01 = vc[(q - 1) * SC + p];
+        const double c10 = vc[q * SC + p - 1], c11 = vc[q * SC + p];
+        double* pv = u + 2 * q * S + 2 * p;
+        // (even, even): fine[0::2, 0::2] = 0.25 (((c00 + c01) + c10) + c11)   (transfer.py:57)
+        pv[0] = DADD(zero ? 0.0 : pv[0], DMUL(0.25, DADD(DADD(DADD(c00, c01), c10), c11)));
+        if (p < mc)  // (even, odd): fine[0::2, 1::2] = 0.5 (c01 + c11)   (transfer.py:56)
+          pv[1] = DADD(zero ? 0.0 : pv[1], DMUL(0.5, DADD(c01, c11)));
+        if (q < mc) {
+          pv[S] = DADD(zero ? 0.0 : pv[S], DMUL(0.5, DADD(c10, c11)));  // (odd, even), transfer.py:55
+          if (p < mc) pv[S + 1] = DADD(zero ? 0.0 : pv[S + 1], c11);     // (odd, odd), transfer.py:54
+        }
+      }
+    }
+    bot_sync(g);
+  }
+  __syncthreads();
   {
-    const BotLevel& L = bp.lv[0];
-    const double* v = bl_v(sm, L, cur & 1u);
-    for (int y = ty; y < L.m; y += 32)
-      for (int x = tx; x < L.m; x += 32) bp.gv[kc_idx(bp.gP, y, x)] = v[y * L.S + x];
+    const int S = m0 + 2;
+    const double* v = sm + bp.final_cur * S * S + S + 1;
+    for (int i = threadIdx.x; i < m0 * m0; i += KC_BOT_THREADS) {
+      const int y = i / m0, x = i - y * m0;
+      bp.gv[kc_idx(bp.gP, y, x)] = v[y * S + x];
+    }
   }
 }

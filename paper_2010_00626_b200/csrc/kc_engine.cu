@@ -61,6 +61,9 @@ struct kc_handle {
   int Lb = -1;  // 0-based first smem-resident (bottom) level, or -1 if none
   BotParams bot_base{};
   size_t bot_smem = 0;
+  int bot_m0 = 0;
+  // host-built bottom phase schedules, keyed by (kappa1, kappa2, v_zero)
+  std::map<std::tuple<int, int, int>, std::tuple<unsigned*, int, int>> bot_sched;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double* d_part = nullptr;     // reduction partials
@@ -244,6 +247,34 @@ int ex_coarsest(kc_handle* h) {
   return KC_OK;
 }
 
+int get_bot_sched(kc_handle* h, int k1, int k2, int vzero, const unsigned** dev, int* n, int* final_cur) {
+  auto key = std::make_tuple(k1, k2, vzero);
+  auto it = h->bot_sched.find(key);
+  if (it == h->bot_sched.end()) {
+    BotBuilder b;
+    b.m0 = h->bot_m0;
+    b.nlev = h->bot_base.nlev;
+    b.nu1 = h->nu1;
+    b.nu2 = h->nu2;
+    b.vz = vzero ? 1u : 0u;
+    if (b.nlev > 1) {
+      b.rec(0, k1);
+      if (k2 > 0) b.rec(0, k2);
+    }
+    if ((int)b.out.size() > KC_BOT_MAXPH)
+      KC_FAIL(h, KC_EINVAL, "bottom schedule of %zu phases exceeds %d", b.out.size(), KC_BOT_MAXPH);
+    unsigned* d = nullptr;
+    const size_t bytes = sizeof(unsigned) * (b.out.empty() ? 1 : b.out.size());
+    KC_CUDA(h, cudaMalloc(&d, bytes));
+    if (!b.out.empty()) KC_CUDA(h, cudaMemcpy(d, b.out.data(), sizeof(unsigned) * b.out.size(), cudaMemcpyHostToDevice));
+    it = h->bot_sched.emplace(key, std::make_tuple(d, (int)b.out.size(), (int)(b.cur & 1u))).first;
+  }
+  *dev = std::get<0>(it->second);
+  *n = std::get<1>(it->second);
+  *final_cur = std::get<2>(it->second);
+  return KC_OK;
+}
+
 int ex_bottom(kc_handle* h, int l, int k1, int k2) {
   Level& L = h->L[l];
   BotParams bp = h->bot_base;
@@ -251,10 +282,10 @@ int ex_bottom(kc_handle* h, int l, int k1, int k2) {
   bp.gf = L.f;
   bp.gP = L.P;
   bp.v_zero = L.vzero ? 1 : 0;
-  bp.nk = k2 > 0 ? 2 : 1;
-  bp.kap[0] = k1;
-  bp.kap[1] = k2;
-  k_bottom<<<1, KC_BOT_THREADS, h->bot_smem, h->stream>>>(bp);
+  int rc = get_bot_sched(h, k1, k2, bp.v_zero, &bp.sched, &bp.nsched, &bp.final_cur);
+  if (rc) return rc;
+  if (h->L[h->n - 1].st.center == 0.0) KC_FAIL(h, KC_ESINGULAR, "singular coarsest operator");
+  k_bottom<<<1, KC_BOT_THREADS, h->bot_smem, h->stream>>>(bp, h->bot_m0);
   KC_LAUNCH_CHECK(h);
   ++h->launches;
   L.vzero = false;
@@ -323,6 +354,14 @@ int get_cycle_graph(kc_handle* h, int kappa, GraphEntry** out) {
     save_vz[j] = h->L[j].vzero;
   }
   for (int j = 1; j < h->n; ++j) h->L[j].cur = 0;
+  // bottom schedules live in device memory: build them before capturing
+  for (const Op& op : ops)
+    if (op.kind == OP_BOTTOM) {
+      const unsigned* dv;
+      int nn, fc, rc0;
+      for (int vz = 0; vz < 2; ++vz)
+        if ((rc0 = get_bot_sched(h, op.a, op.b, vz, &dv, &nn, &fc))) return rc0;
+    }
   GraphEntry g;
   const int l0 = h->launches;
   KC_CUDA(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
@@ -499,27 +538,13 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
       lb = l;
       break;
     }
-  if (lb >= 0 && n - lb <= KC_BOT_MAXLEV) {
+  if (lb >= 0) {
     BotParams& bp = h->bot_base;
     memset(&bp, 0, sizeof(bp));
     bp.nlev = n - lb;
-    bp.nu1 = nu1;
-    bp.nu2 = nu2;
-    int off = 0;
-    for (int j = 0; j < bp.nlev; ++j) {
-      const Level& L = h->L[lb + j];
-      BotLevel& B = bp.lv[j];
-      B.m = L.m;
-      B.S = L.m + 2;
-      const int sz = B.S * B.S;
-      B.ov[0] = off;
-      B.ov[1] = off + sz;
-      B.of = off + 2 * sz;
-      off += 3 * sz;
-      B.s = L.st;
-    }
-    bp.total = off;
-    h->bot_smem = sizeof(double) * (size_t)off;
+    for (int j = 0; j < bp.nlev; ++j) bp.st[j] = h->L[lb + j].st;
+    h->bot_m0 = h->L[lb].m;
+    h->bot_smem = sizeof(double) * (size_t)bot_smem_doubles(h->bot_m0, bp.nlev);
     if (cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->bot_smem) != cudaSuccess) {
       h->err = "cudaFuncSetAttribute(k_bottom) failed";
       return fail(KC_ECUDA);
@@ -547,6 +572,7 @@ int kc_destroy(kc_handle* h) {
   cudaFree(h->ap);
   cudaFree(h->fb);
   cudaFree(h->snap);
+  for (auto& kv : h->bot_sched) cudaFree(std::get<0>(kv.second));
   cudaFree(h->d_part);
   cudaFree(h->d_scal);
   if (h->h_scal) cudaFreeHost(h->h_scal);

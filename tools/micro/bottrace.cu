@@ -1,0 +1,54 @@
+// Per-phase cycle trace of the bottom kernel on a synthetic 63^2..1 hierarchy.
+#define KC_BOT_TRACE 8192
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <cuda_runtime.h>
+#include "../../paper_2010_00626_b200/csrc/kc_bottom.cuh"
+
+int main(int argc, char** argv) {
+  int kappa = argc > 1 ? atoi(argv[1]) : 3;
+  const int m0 = 63, nlev = 6, P = kc_pitch(m0);
+  size_t el = (size_t)(m0 + 2) * P;
+  std::vector<double> hf(el, 0.0);
+  for (int y = 0; y < m0; ++y) for (int x = 0; x < m0; ++x) hf[kc_idx(P, y, x)] = ((y * 7 + x * 3) % 11) * 0.1;
+  double *gv, *gf;
+  cudaMalloc(&gv, el * 8); cudaMalloc(&gf, el * 8);
+  cudaMemset(gv, 0, el * 8);
+  cudaMemcpy(gf, hf.data(), el * 8, cudaMemcpyHostToDevice);
+  BotParams bp{};
+  bp.nlev = nlev;
+  for (int d = 0; d < nlev; ++d) {
+    for (int k = 0; k < 9; ++k) bp.st[d].w[k] = -0.1;
+    bp.st[d].w[4] = 1.0; bp.st[d].center = 1.0; bp.st[d].c = 0.8;
+  }
+  BotBuilder b; b.m0 = m0; b.nlev = nlev; b.nu1 = 2; b.nu2 = 2; b.vz = 1;
+  b.rec(0, kappa); if (kappa > 1) b.rec(0, kappa - 1);
+  unsigned* ds; cudaMalloc(&ds, b.out.size() * 4);
+  cudaMemcpy(ds, b.out.data(), b.out.size() * 4, cudaMemcpyHostToDevice);
+  bp.gv = gv; bp.gf = gf; bp.gP = P; bp.v_zero = 1; bp.sched = ds; bp.nsched = (int)b.out.size(); bp.final_cur = b.cur & 1;
+  size_t smem = sizeof(double) * bot_smem_doubles(m0, nlev);
+  cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int zero = 0;
+  for (int rep = 0; rep < 2; ++rep) {
+    cudaMemcpyToSymbol(kc_bot_trace_n, &zero, sizeof(int));
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    k_bottom<<<1, KC_BOT_THREADS, smem>>>(bp, m0);
+    cudaEventRecord(e1);
+    cudaError_t err = cudaDeviceSynchronize();
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    if (rep == 1) printf("kappa=%d+%d: %.1f us, %zu phases %s\n", kappa, kappa - 1, ms * 1e3, b.out.size(), cudaGetErrorString(err));
+  }
+  int n; cudaMemcpyFromSymbol(&n, kc_bot_trace_n, sizeof(int));
+  std::vector<long long> t(n); std::vector<int> op(n);
+  cudaMemcpyFromSymbol(t.data(), kc_bot_trace, n * 8);
+  cudaMemcpyFromSymbol(op.data(), kc_bot_trace_op, n * 4);
+  double sum[4][8] = {}; int cnt[4][8] = {};
+  for (int i = 0; i + 1 < n; ++i) { int o = op[i] / 16, d = op[i] % 16; sum[o][d] += t[i + 1] - t[i]; cnt[o][d]++; }
+  const char* nm[4] = {"jacobi", "resid", "restrict", "prolong"};
+  for (int o = 0; o < 4; ++o) for (int d = 0; d < nlev; ++d) if (cnt[o][d])
+    printf("  %-9s level %d (m=%2d): %5d phases, %7.0f cycles avg, %9.0f total\n", nm[o], d, bot_m(m0, d), cnt[o][d], sum[o][d] / cnt[o][d], sum[o][d]);
+  printf("phases traced: %d, total cycles %lld\n", n, n > 1 ? t[n - 1] - t[0] : 0);
+  return 0;
+}
