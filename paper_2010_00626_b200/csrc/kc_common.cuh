@@ -8,6 +8,7 @@
 // implicit zeros" (mesh.py:3-5, stencil.py:108-113, transfer.py:49-52), so
 // no kernel carries boundary branches.  KC_OX = 16 puts x = 0 on a 128-byte
 // line; P is a multiple of 16 doubles so every row starts 128-B aligned.
+// Rows also carry >= 127 columns of zero padding past the ghost column.
 #pragma once
 #include <cstddef>
 #include <cstdint>
@@ -20,7 +21,10 @@ __host__ __device__ __forceinline__ size_t kc_idx(int P, int y, int x) {
 }
 
 __host__ __device__ __forceinline__ int kc_pitch(int m) {
-  int need = KC_OX + m + 1;  // columns -1 .. m live at KC_OX-1 .. KC_OX+m
+  // columns -1 .. m live at KC_OX-1 .. KC_OX+m; the streaming kernels read
+  // 128-column bands that may run up to 127 columns past m (masked), so rows
+  // carry that much zero padding
+  int need = KC_OX + m + 128;
   return (need + 15) & ~15;
 }
 

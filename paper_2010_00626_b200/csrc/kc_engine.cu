@@ -25,6 +25,7 @@
 #include "kc_common.cuh"
 #include "kc_grid_kernels.cuh"
 #include "kc_pcg.cuh"
+#include "kc_stream.cuh"
 
 namespace {
 
@@ -40,7 +41,9 @@ struct Level {
   St9 st{};
 };
 
-enum OpKind : int { OP_RELAX, OP_RESTRICT, OP_ZERO, OP_PROLONG, OP_COARSEST, OP_BOTTOM };
+enum OpKind : int { OP_RELAX, OP_RESTRICT, OP_ZERO, OP_PROLONG, OP_COARSEST, OP_BOTTOM, OP_PRE, OP_POST };
+#define KC_FUSE_MAXNU 4      // fused streaming kernels exist for nu <= 4
+#define KC_FUSE_MIN_M 127    // HBM levels handled by the streaming kernels
 struct Op {
   int kind, level, a, b;
 };
@@ -69,7 +72,12 @@ struct kc_handle {
   double* d_part = nullptr;     // reduction partials
   double* d_scal = nullptr;     // device scalars
   double* h_scal = nullptr;     // pinned host mirror
-  std::map<std::tuple<int, int, int>, GraphEntry> graphs;
+  std::map<std::tuple<int, int, int, int>, GraphEntry> graphs;  // (kappa, cur0, vzero0, norms)
+  double* d_npart = nullptr;  // per-warp norm partials of the fused level-1 post kernel
+  int npart_cap = 0;
+  bool fuse = true;           // use the fused streaming kernels in native cycles
+  int num_sms = 148;
+  std::map<const void*, int> ks_occ;  // warp slots per streaming kernel (one wave)
   int launches = 0;             // kernel launches issued by the executor (for capture counting)
   std::string err;
   // PCG vectors (lazily allocated), finest padded layout
@@ -294,8 +302,126 @@ int ex_bottom(kc_handle* h, int l, int k1, int k2) {
   return KC_OK;
 }
 
+// ---------------------------------------------------------------------------
+// fused streaming kernels (kc_stream.cuh)
+// ---------------------------------------------------------------------------
+inline int ks_npb(int D) { return (KS_BAND - 1 - D - 2 * ((D + 2) / 2)) / 2; }  // KsGeom<D>::NPB
+
+// One wave of warps: every band gets K = slots / nbands warps, each streaming
+// a contiguous run of ceil((mc+1)/K) coarse rows, so all warps finish
+// together and the per-warp warm-up stays a small fraction of its rows.
+int ks_choose_nq(int mc, int nbands, int slots) {
+  const int k = slots / nbands > 1 ? slots / nbands : 1;
+  const int nq = (mc + 1 + k - 1) / k;
+  return nq > 2 ? nq : 2;
+}
+
+typedef void (*KsFn)(StreamParams);
+KsFn ks_pre_fn(int nu, bool zero) {
+#define KS_PRE(N) return zero ? k_pre<N, true> : k_pre<N, false>
+  switch (nu) {
+    case 0: KS_PRE(0);
+    case 1: KS_PRE(1);
+    case 2: KS_PRE(2);
+    case 3: KS_PRE(3);
+    case 4: KS_PRE(4);
+  }
+#undef KS_PRE
+  return nullptr;
+}
+KsFn ks_post_fn(int nu, bool vz, bool norms) {
+#define KS_POST(N) \
+  return vz ? (norms ? k_post<N, true, true> : k_post<N, true, false>) : (norms ? k_post<N, false, true> : k_post<N, false, false>)
+  switch (nu) {
+    case 0: KS_POST(0);
+    case 1: KS_POST(1);
+    case 2: KS_POST(2);
+    case 3: KS_POST(3);
+    case 4: KS_POST(4);
+  }
+#undef KS_POST
+  return nullptr;
+}
+
+int ks_slots(kc_handle* h, const void* fn) {
+  auto it = h->ks_occ.find(fn);
+  if (it != h->ks_occ.end()) return it->second;
+  int blocks = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, 128, 0) != cudaSuccess || blocks < 1) blocks = 1;
+  const int slots = blocks * 4 * h->num_sms;
+  h->ks_occ[fn] = slots;
+  return slots;
+}
+
+StreamParams ks_params(kc_handle* h, int l, int D, int* nwarps, const void* fn) {
+  Level& L = h->L[l];
+  Level& C = h->L[l + 1];
+  StreamParams p{};
+  p.u = L.v[L.cur];
+  p.f = L.f;
+  p.uo = L.v[L.cur ^ 1];
+  p.fc = C.f;
+  p.vc = C.v[C.cur];
+  p.m = L.m;
+  p.P = L.P;
+  p.mc = C.m;
+  p.Pc = C.P;
+  p.s = L.st;
+  p.nbands = (C.m + 1 + ks_npb(D) - 1) / ks_npb(D);
+  p.nq = ks_choose_nq(C.m, p.nbands, fn ? ks_slots(h, fn) : 148 * 12);
+  *nwarps = p.nbands * ((C.m + 1 + p.nq - 1) / p.nq);
+  return p;
+}
+
+// relax(nu1) + restrict_residual (cycle.py:211-213) in one pass
+int ex_pre(kc_handle* h, int l) {
+  Level& L = h->L[l];
+  int nw = 0;
+  KsFn fn = ks_pre_fn(h->nu1, L.vzero);
+  StreamParams p = ks_params(h, l, h->nu1 + 1, &nw, (const void*)fn);
+  fn<<<(nw + 3) / 4, 128, 0, h->stream>>>(p);
+  KC_LAUNCH_CHECK(h);
+  ++h->launches;
+  if (h->nu1 > 0) {
+    L.cur ^= 1;
+    L.vzero = false;
+  }
+  return KC_OK;
+}
+
+// prolong_add + relax(nu2) (cycle.py:219-220), optionally with the norms of
+// the result (||v||, ||f - A v|| into d_scal[0], d_scal[1])
+int ex_post(kc_handle* h, int l, bool norms) {
+  Level& L = h->L[l];
+  Level& C = h->L[l + 1];
+  int rc = ex_materialize(h, l + 1);
+  if (rc) return rc;
+  int nw = 0;
+  const int D = h->nu2 + (norms ? 1 : 0);
+  KsFn fn = ks_post_fn(h->nu2, L.vzero, norms);
+  StreamParams p = ks_params(h, l, D > 0 ? D : 1, &nw, (const void*)fn);
+  p.vc = C.v[C.cur];
+  if (norms) {
+    if (nw > h->npart_cap) KC_FAIL(h, KC_EINVAL, "norm partial buffer too small (%d < %d)", h->npart_cap, nw);
+    p.part = h->d_npart;
+  }
+  fn<<<(nw + 3) / 4, 128, 0, h->stream>>>(p);
+  KC_LAUNCH_CHECK(h);
+  ++h->launches;
+  if (norms) {
+    k_norms_final<<<1, 256, 0, h->stream>>>(h->d_npart, nw, h->d_scal);
+    KC_LAUNCH_CHECK(h);
+    ++h->launches;
+  }
+  L.cur ^= 1;
+  L.vzero = false;
+  return KC_OK;
+}
+
 int ex_op(kc_handle* h, const Op& op) {
   switch (op.kind) {
+    case OP_PRE: return ex_pre(h, op.level);
+    case OP_POST: return ex_post(h, op.level, op.b != 0);
     case OP_RELAX: return ex_relax(h, op.level, op.a);
     case OP_RESTRICT: return ex_restrict(h, op.level);
     case OP_ZERO: h->L[op.level].vzero = true; return KC_OK;
@@ -306,8 +432,14 @@ int ex_op(kc_handle* h, const Op& op) {
   return KC_EINVAL;
 }
 
-// Flatten kappa_cycle(level, kappa) (cycle.py:204-220) into ops.
-void flatten(const kc_handle* h, int l, int kappa, std::vector<Op>& ops) {
+bool fusable(const kc_handle* h, int l) {
+  return h->fuse && h->nu1 <= KC_FUSE_MAXNU && h->nu2 <= KC_FUSE_MAXNU && l < h->n - 1 && h->L[l].m >= KC_FUSE_MIN_M;
+}
+
+// Flatten kappa_cycle(level, kappa) (cycle.py:204-220) into ops.  `norms`
+// asks the level-0 post-smoothing of this call to also produce ||v|| and
+// ||f - A v|| (the stand-alone stopping test) inside the cycle.
+void flatten(const kc_handle* h, int l, int kappa, std::vector<Op>& ops, bool norms = false) {
   const int n = h->n;
   if (l == h->Lb) {
     ops.push_back({OP_BOTTOM, l, kappa, 0});
@@ -317,8 +449,13 @@ void flatten(const kc_handle* h, int l, int kappa, std::vector<Op>& ops) {
     ops.push_back({OP_COARSEST, l, 0, 0});
     return;
   }
-  ops.push_back({OP_RELAX, l, h->nu1, 0});
-  ops.push_back({OP_RESTRICT, l, 0, 0});
+  const bool fu = fusable(h, l);
+  if (fu) {
+    ops.push_back({OP_PRE, l, 0, 0});
+  } else {
+    ops.push_back({OP_RELAX, l, h->nu1, 0});
+    ops.push_back({OP_RESTRICT, l, 0, 0});
+  }
   ops.push_back({OP_ZERO, l + 1, 0, 0});
   if (l + 1 == h->Lb) {
     ops.push_back({OP_BOTTOM, l + 1, kappa, kappa > 1 ? kappa - 1 : 0});
@@ -332,20 +469,28 @@ void flatten(const kc_handle* h, int l, int kappa, std::vector<Op>& ops) {
       }
     }
   }
-  ops.push_back({OP_PROLONG, l, 0, 0});
-  ops.push_back({OP_RELAX, l, h->nu2, 0});
+  if (fu) {
+    ops.push_back({OP_POST, l, 0, norms ? 1 : 0});
+  } else {
+    ops.push_back({OP_PROLONG, l, 0, 0});
+    ops.push_back({OP_RELAX, l, h->nu2, 0});
+  }
 }
 
-int get_cycle_graph(kc_handle* h, int kappa, GraphEntry** out) {
+// true when flatten(norms=true) leaves ||v||, ||f-Av|| in d_scal[0..1]
+bool cycle_has_norms(const kc_handle* h) { return h->Lb != 0 && fusable(h, 0); }
+
+int get_cycle_graph(kc_handle* h, int kappa, GraphEntry** out, bool norms = false) {
   Level& L0 = h->L[0];
-  auto key = std::make_tuple(kappa, L0.cur, L0.vzero ? 1 : 0);
+  norms = norms && cycle_has_norms(h);
+  auto key = std::make_tuple(kappa, L0.cur, L0.vzero ? 1 : 0, norms ? 1 : 0);
   auto it = h->graphs.find(key);
   if (it != h->graphs.end()) {
     *out = &it->second;
     return KC_OK;
   }
   std::vector<Op> ops;
-  flatten(h, 0, kappa, ops);
+  flatten(h, 0, kappa, ops, norms);
   // coarse levels start every cycle logically overwritten (zero_guess precedes use)
   std::vector<int> save_cur(h->n);
   std::vector<char> save_vz(h->n);
@@ -388,9 +533,9 @@ int get_cycle_graph(kc_handle* h, int kappa, GraphEntry** out) {
   return KC_OK;
 }
 
-int run_cycle_graph(kc_handle* h, int kappa) {
+int run_cycle_graph(kc_handle* h, int kappa, bool norms = false) {
   GraphEntry* g = nullptr;
-  int rc = get_cycle_graph(h, kappa, &g);
+  int rc = get_cycle_graph(h, kappa, &g, norms);
   if (rc) return rc;
   KC_CUDA(h, cudaGraphLaunch(g->exec, h->stream));
   h->L[0].cur = g->end_cur0;
@@ -477,6 +622,7 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
   KC_CUDA(none, cudaSetDevice(device));
 
   kc_handle* h = new kc_handle();
+  h->num_sms = prop.multiProcessorCount;
   h->n = n;
   h->coarsening = coarsening;
   h->smoother = smoother_kind;
@@ -551,6 +697,20 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
     }
     h->Lb = lb;
   }
+  if (n >= 2 && h->L[0].m >= KC_FUSE_MIN_M) {  // per-warp partials of the fused level-1 norms
+    int nw = 0;
+    const int D = nu2 + 1;
+    StreamParams p = ks_params(h, 0, D, &nw, (const void*)ks_post_fn(nu2, true, true));
+    int nw2 = 0;
+    ks_params(h, 0, D, &nw2, (const void*)ks_post_fn(nu2, false, true));
+    nw = nw > nw2 ? nw : nw2;
+    (void)p;
+    h->npart_cap = nw;
+    if (cudaMalloc(&h->d_npart, sizeof(double) * 2 * (size_t)nw) != cudaSuccess) {
+      h->err = "cudaMalloc norm partials failed";
+      return fail(KC_ENOMEM);
+    }
+  }
   *out = h;
   return KC_OK;
 }
@@ -572,6 +732,7 @@ int kc_destroy(kc_handle* h) {
   cudaFree(h->ap);
   cudaFree(h->fb);
   cudaFree(h->snap);
+  cudaFree(h->d_npart);
   for (auto& kv : h->bot_sched) cudaFree(std::get<0>(kv.second));
   cudaFree(h->d_part);
   cudaFree(h->d_scal);
@@ -841,8 +1002,9 @@ int kc_solve(kc_handle* h, int kappa, int stop_mode, double target_reduction, in
   int rc;
   if ((rc = ex_materialize(h, 0))) return rc;
   // build the graph before timing (setup, like build_state)
+  const bool fused_norms = cycle_has_norms(h);
   GraphEntry* g = nullptr;
-  if ((rc = get_cycle_graph(h, kappa, &g))) return rc;
+  if ((rc = get_cycle_graph(h, kappa, &g, fused_norms))) return rc;
   KC_CUDA(h, cudaStreamSynchronize(h->stream));
   Level& L0 = h->L[0];
   KC_CUDA(h, cudaEventRecord(h->ev0, h->stream));
@@ -860,9 +1022,11 @@ int kc_solve(kc_handle* h, int kappa, int stop_mode, double target_reduction, in
     st = KC_STATUS_CONVERGED;
   } else {
     for (it = 1; it <= max_cycles; ++it) {
-      if ((rc = run_cycle_graph(h, kappa))) return rc;
-      if ((rc = red_dot(h, L0.v[L0.cur], L0.v[L0.cur], 0, 0, true))) return rc;
-      if ((rc = red_resnorm(h, L0.v[L0.cur], L0.f, 0, 1))) return rc;
+      if ((rc = run_cycle_graph(h, kappa, fused_norms))) return rc;
+      if (!fused_norms) {
+        if ((rc = red_dot(h, L0.v[L0.cur], L0.v[L0.cur], 0, 0, true))) return rc;
+        if ((rc = red_resnorm(h, L0.v[L0.cur], L0.f, 0, 1))) return rc;
+      }
       if ((rc = fetch_scalars(h, 2))) return rc;
       if (err_hist) err_hist[it] = h->h_scal[0];
       if (res_hist) res_hist[it] = h->h_scal[1];

@@ -1,0 +1,316 @@
+// kc_stream.cuh — fused streaming kernels for the HBM-resident levels.
+//
+//   k_pre<NU, ZERO>        NU damped-Jacobi sweeps + residual + full-weighting
+//                          restriction in one pass (SURVEY.md §2.3 K1+K2+K8):
+//                          reads v, f; writes v' and the coarse f.
+//   k_post<NU, VZ, NORMS>  v + P vc, then NU sweeps (K3+K1), optionally with
+//                          ||v'||^2 and ||f - A v'||^2 partial sums fused in
+//                          (the stand-alone stopping test, cycle.py:345).
+//
+// Each warp streams down a band of 64 fine columns (2 per lane), one input
+// row per step.  Stage t (t = 1..D) computes row yin - 2t from the last three
+// rows of stage t-1, so the stages of one step are independent (ILP); the
+// x-neighbours come from warp shuffles.  Every stage loses one column of
+// validity per side, so a band owns NPB coarse columns (2*NPB fine columns)
+// and recomputes a thin halo; rows stream without recomputation apart from a
+// short warm-up per chunk, and the chunks are sized so all warps of a launch
+// form one wave (kc_engine.cu ks_choose_nq).  Loads of rows outside [-1, m]
+// are clamped onto the all-zero ghost rows, so the hot loop has no branches.
+//
+// Per-point arithmetic is the reference's (kc_common.cuh), bit-identical to
+// the per-op kernels and to scipy/numpy.  Points outside the interior are
+// forced to +0.0 at every stage (the Dirichlet ghost values).
+#pragma once
+#include "kc_common.cuh"
+
+#define KS_BAND 64  // fine columns per warp band (2 per lane)
+
+struct StreamParams {
+  const double* u;   // input v (current buffer); unused on a zero guess
+  const double* f;   // level f
+  double* uo;        // output v (the other buffer)
+  double* fc;        // PRE: coarse f (output)
+  const double* vc;  // POST: coarse v (input)
+  int m, P, mc, Pc;
+  int nbands, nq;    // bands across x; coarse rows per chunk
+  St9 s;
+  double* part;      // POST+NORMS: 2 partial sums per warp
+};
+
+__device__ __forceinline__ double kc_shfl_up1(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+__device__ __forceinline__ double kc_shfl_dn1(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+
+// Jacobi (JAC) or residual at the lane's two columns from three rows
+// (r0 = south, r1 = centre, r2 = north), own values and shuffled edges.
+template <bool JAC>
+__device__ __forceinline__ void ks_stencil2(const St9& s, double2 r0, double2 r1, double2 r2, double2 fv,
+                                            double& ox, double& oy) {
+  const double l0 = kc_shfl_up1(r0.y), l1 = kc_shfl_up1(r1.y), l2 = kc_shfl_up1(r2.y);
+  const double e0 = kc_shfl_dn1(r0.x), e1 = kc_shfl_dn1(r1.x), e2 = kc_shfl_dn1(r2.x);
+  const double ax = kc_sum9(s, l0, r0.x, r0.y, l1, r1.x, r1.y, l2, r2.x, r2.y);
+  const double ay = kc_sum9(s, r0.x, r0.y, e0, r1.x, r1.y, e1, r2.x, r2.y, e2);
+  if (JAC) {
+    ox = kc_jacobi_pt(r1.x, fv.x, ax, s.c);
+    oy = kc_jacobi_pt(r1.y, fv.y, ay, s.c);
+  } else {
+    ox = DSUB(fv.x, ax);
+    oy = DSUB(fv.y, ay);
+  }
+}
+
+// Left halo HL >= D+1 (even) and the coarse columns owned per 64-column band.
+template <int D>
+struct KsGeom {
+  static constexpr int HL = 2 * ((D + 2) / 2);
+  static constexpr int NPB = (KS_BAND - 1 - D - HL) / 2;
+};
+
+__device__ __forceinline__ double2 ks_ld2(const double* __restrict__ a, size_t i) {
+  return __ldg(reinterpret_cast<const double2*>(a + i));
+}
+
+// ---------------------------------------------------------------------------
+// PRE: NU sweeps + residual + restriction
+// ---------------------------------------------------------------------------
+template <int NU, bool ZERO>
+__global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
+  constexpr int D = NU + 1;
+  using G = KsGeom<D>;
+  const int lane = threadIdx.x & 31;
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int band = wg % p.nbands, chunk = wg / p.nbands;
+  const int P0 = band * G::NPB, Q0 = chunk * p.nq;
+  if (Q0 > p.mc) return;  // whole warp
+  const int m = p.m, P = p.P;
+  const int XS = 2 * P0 - G::HL;
+  const int c0 = XS + 2 * lane;
+  const bool colx_in = c0 >= 0 && c0 < m, coly_in = c0 + 1 >= 0 && c0 + 1 < m;
+  const int pcol = c0 >> 1;  // coarse column of this lane (c0 even)
+  const bool own_lane = lane >= G::HL / 2 && lane < G::HL / 2 + G::NPB;
+  const St9 s = p.s;
+
+  double2 W[D][3];       // last three rows of stages 0..NU (W[NU] feeds the residual)
+  double2 R[3];          // last three residual rows
+  double2 F[2 * D + 1];  // f rows yin .. yin-2D (own columns)
+#pragma unroll
+  for (int t = 0; t < D; ++t) W[t][0] = W[t][1] = W[t][2] = make_double2(0.0, 0.0);
+  R[0] = R[1] = R[2] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int k = 0; k < 2 * D + 1; ++k) F[k] = make_double2(0.0, 0.0);
+
+  const int ys = 2 * Q0 - D;
+  const int ye = 2 * Q0 + 2 * p.nq + 2 * D + 1;  // inclusive
+  // rows outside [-1, m] read the all-zero ghost rows: branch-free
+  auto rp = [&](int y) -> size_t { return kc_idx(P, min(max(y, -1), m), c0); };
+  double2 pu0 = ZERO ? make_double2(0.0, 0.0) : ks_ld2(p.u, rp(ys));
+  double2 pf0 = ks_ld2(p.f, rp(ys));
+  double2 pu1 = ZERO ? make_double2(0.0, 0.0) : ks_ld2(p.u, rp(ys + 1));
+  double2 pf1 = ks_ld2(p.f, rp(ys + 1));
+  for (int yin = ys; yin <= ye; ++yin) {
+    double2 u0 = pu0;
+    const double2 f0 = pf0;
+    pu0 = pu1;
+    pf0 = pf1;
+    if (!ZERO) pu1 = ks_ld2(p.u, rp(yin + 2));
+    pf1 = ks_ld2(p.f, rp(yin + 2));
+    const bool row_in = yin >= 0 && yin < m;
+    u0.x = (row_in && colx_in) ? u0.x : 0.0;
+    u0.y = (row_in && coly_in) ? u0.y : 0.0;
+#pragma unroll
+    for (int k = 2 * D; k > 0; --k) F[k] = F[k - 1];  // F[k] = f row (yin - k)
+    F[0] = f0;
+
+    // ---- all stages from the pre-step windows (independent) -------------
+    double2 nw[D + 1];
+    nw[0] = u0;
+#pragma unroll
+    for (int t = 1; t <= D; ++t) {
+      const int y = yin - 2 * t;
+      double ox, oy;
+      if (t <= NU) {
+        if (ZERO && t == 1) {  // first sweep on the zero guess: 0 + c f
+          ox = kc_jacobi_zero(F[2].x, s.c);
+          oy = kc_jacobi_zero(F[2].y, s.c);
+        } else {
+          ks_stencil2<true>(s, W[t - 1][0], W[t - 1][1], W[t - 1][2], F[2 * t], ox, oy);
+        }
+      } else if (ZERO && NU == 0) {  // residual of the zero guess: f exactly
+        ox = F[2 * t].x;
+        oy = F[2 * t].y;
+      } else {
+        ks_stencil2<false>(s, W[t - 1][0], W[t - 1][1], W[t - 1][2], F[2 * t], ox, oy);
+      }
+      const bool in = y >= 0 && y < m;
+      nw[t] = make_double2((in && colx_in) ? ox : 0.0, (in && coly_in) ? oy : 0.0);
+    }
+
+    // ---- restriction from the residual rows of earlier steps ------------
+    {
+      const int yr = yin - 1 - 2 * D;  // newest residual row in R[2]
+      const double e0 = kc_shfl_dn1(R[0].x), e1 = kc_shfl_dn1(R[1].x), e2 = kc_shfl_dn1(R[2].x);
+      const int q = (yr >> 1) - 1;
+      if (!(yr & 1) && own_lane && q >= Q0 && q < Q0 + p.nq && q < p.mc && q >= 0 && pcol < p.mc)
+        p.fc[kc_idx(p.Pc, q, pcol)] = kc_fw(R[0].x, R[0].y, e0, R[1].x, R[1].y, e1, R[2].x, R[2].y, e2);
+    }
+    // ---- output v after NU sweeps ----------------------------------------
+    if (NU > 0) {
+      const int y = yin - 2 * NU;
+      if (own_lane && y >= 2 * Q0 && y < 2 * Q0 + 2 * p.nq && y >= 0 && y < m)
+        *reinterpret_cast<double2*>(p.uo + kc_idx(P, y, c0)) = nw[NU];
+    }
+    // ---- shift windows ----------------------------------------------------
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+      W[t][0] = W[t][1];
+      W[t][1] = W[t][2];
+      W[t][2] = nw[t];
+    }
+    R[0] = R[1];
+    R[1] = R[2];
+    R[2] = nw[D];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// POST: v + P vc, NU sweeps, optional fused norms of the result
+// ---------------------------------------------------------------------------
+template <int NU, bool VZ, bool NORMS>
+__global__ void __launch_bounds__(128, 4) k_post(const StreamParams p) {
+  constexpr int D = NU + (NORMS ? 1 : 0);
+  constexpr int DD = D > 0 ? D : 1;
+  using G = KsGeom<DD>;
+  const int lane = threadIdx.x & 31;
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int band = wg % p.nbands, chunk = wg / p.nbands;
+  const int P0 = band * G::NPB, Q0 = chunk * p.nq;
+  double acc_e = 0.0, acc_r = 0.0;
+  const bool active = Q0 <= p.mc;
+  const int m = p.m, P = p.P;
+  const int XS = 2 * P0 - G::HL;
+  const int c0 = XS + 2 * lane;
+  const bool colx_in = c0 >= 0 && c0 < m, coly_in = c0 + 1 >= 0 && c0 + 1 < m;
+  const int pc = c0 >> 1;
+  const bool own_lane = lane >= G::HL / 2 && lane < G::HL / 2 + G::NPB;
+  const St9 s = p.s;
+
+  if (active) {
+    double2 W[DD][3];
+    double2 F[2 * DD + 1];
+#pragma unroll
+    for (int t = 0; t < DD; ++t) W[t][0] = W[t][1] = W[t][2] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < 2 * DD + 1; ++k) F[k] = make_double2(0.0, 0.0);
+    const int ys = 2 * Q0 - D;
+    const int ye = 2 * Q0 + 2 * p.nq - 1 + 2 * D;
+    auto rp = [&](int y) -> size_t { return kc_idx(P, min(max(y, -1), m), c0); };
+    auto ldc = [&](int q) -> double { return __ldg(p.vc + kc_idx(p.Pc, min(max(q, -1), p.mc), pc)); };
+    // coarse rows around the input row: vcp = row q-1, vcc = row q (q = floor(yin/2))
+    int qcur = ys >> 1;  // arithmetic shift: floor
+    double vcp = ldc(qcur - 1), vcc = ldc(qcur), vcn = ldc(qcur + 1);
+    double2 pu0 = VZ ? make_double2(0.0, 0.0) : ks_ld2(p.u, rp(ys));
+    double2 pf0 = ks_ld2(p.f, rp(ys));
+    double2 pu1 = VZ ? make_double2(0.0, 0.0) : ks_ld2(p.u, rp(ys + 1));
+    double2 pf1 = ks_ld2(p.f, rp(ys + 1));
+    for (int yin = ys; yin <= ye; ++yin) {
+      const double2 u0 = pu0, f0 = pf0;
+      pu0 = pu1;
+      pf0 = pf1;
+      if (!VZ) pu1 = ks_ld2(p.u, rp(yin + 2));
+      pf1 = ks_ld2(p.f, rp(yin + 2));
+      const int q = yin >> 1;
+      if (q != qcur) {  // advance the coarse window by one row (yin even); warp-uniform
+        vcp = vcc;
+        vcc = vcn;
+        qcur = q;
+        vcn = ldc(q + 1);
+      }
+      // prolongation + correction (transfer.py:50-58, cycle.py:174-176)
+      const double lp = kc_shfl_up1(vcp), lc = kc_shfl_up1(vcc);  // coarse column pc-1
+      double ex, ey;
+      if (yin & 1) {  // fine row 2q+1
+        ex = DMUL(0.5, DADD(lc, vcc));
+        ey = vcc;
+      } else {        // fine row 2q
+        ex = DMUL(0.25, DADD(DADD(DADD(lp, vcp), lc), vcc));
+        ey = DMUL(0.5, DADD(vcp, vcc));
+      }
+      const bool row_in = yin >= 0 && yin < m;
+      double2 s0;
+      s0.x = (row_in && colx_in) ? DADD(VZ ? 0.0 : u0.x, ex) : 0.0;
+      s0.y = (row_in && coly_in) ? DADD(VZ ? 0.0 : u0.y, ey) : 0.0;
+#pragma unroll
+      for (int k = 2 * DD; k > 0; --k) F[k] = F[k - 1];
+      F[0] = f0;
+
+      double2 nw[DD + 1];
+      nw[0] = s0;
+#pragma unroll
+      for (int t = 1; t <= D; ++t) {
+        const int y = yin - 2 * t;
+        double ox, oy;
+        if (t <= NU) ks_stencil2<true>(s, W[t - 1][0], W[t - 1][1], W[t - 1][2], F[2 * t], ox, oy);
+        else ks_stencil2<false>(s, W[t - 1][0], W[t - 1][1], W[t - 1][2], F[2 * t], ox, oy);
+        const bool in = y >= 0 && y < m;
+        nw[t] = make_double2((in && colx_in) ? ox : 0.0, (in && coly_in) ? oy : 0.0);
+      }
+      // output after NU sweeps (stage NU; NU = 0 writes the corrected v)
+      {
+        const int y = yin - 2 * NU;
+        if (own_lane && y >= 2 * Q0 && y < 2 * Q0 + 2 * p.nq && y >= 0 && y < m) {
+          *reinterpret_cast<double2*>(p.uo + kc_idx(P, y, c0)) = nw[NU];
+          if (NORMS) acc_e = fma(nw[NU].y, nw[NU].y, fma(nw[NU].x, nw[NU].x, acc_e));
+        }
+      }
+      if (NORMS) {
+        const int y = yin - 2 * D;
+        if (own_lane && y >= 2 * Q0 && y < 2 * Q0 + 2 * p.nq && y >= 0 && y < m)
+          acc_r = fma(nw[D].y, nw[D].y, fma(nw[D].x, nw[D].x, acc_r));
+      }
+#pragma unroll
+      for (int t = 0; t < DD; ++t) {
+        W[t][0] = W[t][1];
+        W[t][1] = W[t][2];
+        W[t][2] = nw[t];
+      }
+    }
+  }
+  if (NORMS) {
+    for (int o = 16; o > 0; o >>= 1) {
+      acc_e += __shfl_down_sync(0xffffffffu, acc_e, o);
+      acc_r += __shfl_down_sync(0xffffffffu, acc_r, o);
+    }
+    if (lane == 0) {
+      p.part[2 * wg] = acc_e;
+      p.part[2 * wg + 1] = acc_r;
+    }
+  }
+}
+
+// deterministic final sum of the per-warp partials: out[0] = sqrt(sum e), out[1] = sqrt(sum r)
+__global__ void __launch_bounds__(256) k_norms_final(const double* __restrict__ part, int nw, double* __restrict__ out) {
+  __shared__ double sh[2][8];
+  double e = 0.0, r = 0.0;
+  for (int i = threadIdx.x; i < nw; i += 256) {
+    e += part[2 * i];
+    r += part[2 * i + 1];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    e += __shfl_down_sync(0xffffffffu, e, o);
+    r += __shfl_down_sync(0xffffffffu, r, o);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+    sh[0][w] = e;
+    sh[1][w] = r;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double te = 0.0, tr = 0.0;
+    for (int k = 0; k < 8; ++k) {
+      te += sh[0][k];
+      tr += sh[1][k];
+    }
+    out[0] = sqrt(te);
+    out[1] = sqrt(tr);
+  }
+}

@@ -323,7 +323,7 @@ class CudaGridState:
     def fill_zero(self, level: int = 1, which: str = "f"):
         N.check(N.lib.kc_fill_zero(self._h, level, N.KC_WHICH_F if which == "f" else N.KC_WHICH_V), self._h)
 
-    OP_NAMES = ("relax", "restrict_residual", "zero_guess", "prolong_add", "coarsest", "bottom")
+    OP_NAMES = ("relax", "restrict_residual", "zero_guess", "prolong_add", "coarsest", "bottom", "pre", "post")
 
     def profile_cycle(self, kappa: int) -> list[dict]:
         """One eager cycle with CUDA events around every scheduled op."""
