@@ -31,6 +31,40 @@ namespace {
 
 thread_local std::string g_create_err;
 
+// Device-resident stand-alone loop state (cycle.py:332-353), advanced by
+// k_stop_check at the end of every cycle inside a conditional WHILE graph.
+struct SolveState {
+  double target, prev;
+  int it, max_it, streak, status, stop_mode, pad;
+  double* err_hist;
+  double* res_hist;
+};
+
+__global__ void k_stop_check(cudaGraphConditionalHandle hnd, SolveState* st, const double* __restrict__ scal) {
+  if (threadIdx.x != 0) return;
+  const int it = st->it + 1;
+  st->it = it;
+  const double e = scal[0], r = scal[1];
+  st->err_hist[it] = e;
+  st->res_hist[it] = r;
+  const double cur = st->stop_mode == KC_STOP_ERROR ? e : r;
+  unsigned go = 1u;
+  if (cur <= st->target) {  // cycle.py:347
+    st->status = KC_STATUS_CONVERGED;
+    go = 0u;
+  } else {  // cycle.py:350-353: five consecutive growth steps
+    const int streak = cur > st->prev ? st->streak + 1 : 0;
+    st->streak = streak;
+    if (streak >= 5) {
+      st->status = KC_STATUS_DIVERGED;
+      go = 0u;
+    }
+  }
+  st->prev = cur;
+  if (go && it >= st->max_it) go = 0u;  // status stays MAX_CYCLES
+  cudaGraphSetConditional(hnd, go);
+}
+
 struct Level {
   int m = 0, P = 0;
   size_t elems = 0;
@@ -53,6 +87,9 @@ struct GraphEntry {
   cudaGraph_t graph = nullptr;
   int end_cur0 = 0;
   int kernels = 0;
+  // whole stand-alone loop: WHILE(cycle; k_stop_check), built on demand
+  cudaGraphExec_t loop_exec = nullptr;
+  cudaGraph_t loop_graph = nullptr;
 };
 
 }  // namespace
@@ -77,6 +114,9 @@ struct kc_handle {
   int npart_cap = 0;
   bool fuse = true;           // use the fused streaming kernels in native cycles
   int num_sms = 148;
+  SolveState* d_solve = nullptr;   // device loop state
+  double* d_hist = nullptr;        // err | res histories for the device loop
+  int hist_cap = 0;
   std::map<const void*, int> ks_occ;  // warp slots per streaming kernel (one wave)
   int launches = 0;             // kernel launches issued by the executor (for capture counting)
   std::string err;
@@ -547,6 +587,40 @@ int run_cycle_graph(kc_handle* h, int kappa, bool norms = false) {
   return KC_OK;
 }
 
+// WHILE(cond) { cycle graph (child, norms fused); k_stop_check } — the whole
+// stand-alone loop in one graph launch, no host round trip per cycle.
+int get_loop_graph(kc_handle* h, GraphEntry* g) {
+  if (g->loop_exec) return KC_OK;
+  if (!h->d_solve) KC_CUDA(h, cudaMalloc(&h->d_solve, sizeof(SolveState)));
+  cudaGraph_t cg = nullptr;
+  KC_CUDA(h, cudaGraphCreate(&cg, 0));
+  cudaGraphConditionalHandle hnd;
+  KC_CUDA(h, cudaGraphConditionalHandleCreate(&hnd, cg, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams np{};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = hnd;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t cn;
+  KC_CUDA(h, cudaGraphAddNode(&cn, cg, nullptr, 0, &np));
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  cudaGraphNode_t child;
+  KC_CUDA(h, cudaGraphAddChildGraphNode(&child, body, nullptr, 0, g->graph));
+  SolveState* st = h->d_solve;
+  const double* scal = h->d_scal;
+  void* args[] = {&hnd, &st, &scal};
+  cudaKernelNodeParams kp{};
+  kp.func = (void*)k_stop_check;
+  kp.gridDim = dim3(1);
+  kp.blockDim = dim3(32);
+  kp.kernelParams = args;
+  cudaGraphNode_t kn;
+  KC_CUDA(h, cudaGraphAddKernelNode(&kn, body, &child, 1, &kp));
+  KC_CUDA(h, cudaGraphInstantiate(&g->loop_exec, cg, 0));
+  g->loop_graph = cg;
+  return KC_OK;
+}
+
 // async reductions into h->d_scal[slot]
 int red_dot(kc_handle* h, const double* a, const double* b, int l, int slot, bool sq) {
   Level& L = h->L[l];
@@ -721,7 +795,11 @@ int kc_destroy(kc_handle* h) {
   for (auto& kv : h->graphs) {
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+    if (kv.second.loop_exec) cudaGraphExecDestroy(kv.second.loop_exec);
+    if (kv.second.loop_graph) cudaGraphDestroy(kv.second.loop_graph);
   }
+  cudaFree(h->d_solve);
+  cudaFree(h->d_hist);
   for (Level& L : h->L) {
     cudaFree(L.v[0]);
     cudaFree(L.v[1]);
@@ -1005,8 +1083,20 @@ int kc_solve(kc_handle* h, int kappa, int stop_mode, double target_reduction, in
   const bool fused_norms = cycle_has_norms(h);
   GraphEntry* g = nullptr;
   if ((rc = get_cycle_graph(h, kappa, &g, fused_norms))) return rc;
-  KC_CUDA(h, cudaStreamSynchronize(h->stream));
   Level& L0 = h->L[0];
+  // the device loop needs a cycle graph that leaves the finest buffer where it
+  // found it (true whenever nu1 > 0 with the fused kernels)
+  const bool device_loop = fused_norms && g->end_cur0 == L0.cur && max_cycles > 0;
+  if (device_loop) {  // setup outside the timed span
+    if (max_cycles + 1 > h->hist_cap) {
+      cudaFree(h->d_hist);
+      h->d_hist = nullptr;
+      KC_CUDA(h, cudaMalloc(&h->d_hist, sizeof(double) * 2 * (size_t)(max_cycles + 1)));
+      h->hist_cap = max_cycles + 1;
+    }
+    if ((rc = get_loop_graph(h, g))) return rc;
+  }
+  KC_CUDA(h, cudaStreamSynchronize(h->stream));
   KC_CUDA(h, cudaEventRecord(h->ev0, h->stream));
   if ((rc = red_dot(h, L0.v[L0.cur], L0.v[L0.cur], 0, 0, true))) return rc;
   if ((rc = red_resnorm(h, L0.v[L0.cur], L0.f, 0, 1))) return rc;
@@ -1020,6 +1110,32 @@ int kc_solve(kc_handle* h, int kappa, int stop_mode, double target_reduction, in
   double cur = m0;
   if (m0 <= target) {
     st = KC_STATUS_CONVERGED;
+  } else if (device_loop) {
+    SolveState ss{};
+    ss.target = target;
+    ss.prev = m0;
+    ss.it = 0;
+    ss.max_it = max_cycles;
+    ss.streak = 0;
+    ss.status = KC_STATUS_MAX_CYCLES;
+    ss.stop_mode = stop_mode;
+    ss.err_hist = h->d_hist;
+    ss.res_hist = h->d_hist + h->hist_cap;
+    KC_CUDA(h, cudaMemcpyAsync(h->d_solve, &ss, sizeof(ss), cudaMemcpyHostToDevice, h->stream));
+    KC_CUDA(h, cudaGraphLaunch(g->loop_exec, h->stream));
+    KC_CUDA(h, cudaMemcpyAsync(&ss, h->d_solve, sizeof(ss), cudaMemcpyDeviceToHost, h->stream));
+    KC_CUDA(h, cudaStreamSynchronize(h->stream));
+    it = ss.it;
+    st = ss.status;
+    if (err_hist) KC_CUDA(h, cudaMemcpy(err_hist + 1, h->d_hist + 1, sizeof(double) * it, cudaMemcpyDeviceToHost));
+    if (res_hist)
+      KC_CUDA(h, cudaMemcpy(res_hist + 1, h->d_hist + h->hist_cap + 1, sizeof(double) * it, cudaMemcpyDeviceToHost));
+    // level-state bookkeeping after it cycles of the graph
+    L0.vzero = false;
+    for (int j = 1; j < h->n; ++j) {
+      h->L[j].vzero = true;
+      h->L[j].cur = 0;
+    }
   } else {
     for (it = 1; it <= max_cycles; ++it) {
       if ((rc = run_cycle_graph(h, kappa, fused_norms))) return rc;
