@@ -142,6 +142,11 @@ int kc_profile_cycle(kc_handle* h, int kappa, int max_ops, int* op_kind, int* op
  * harness can record its own events on the stream the kernels run on */
 int kc_stream(kc_handle* h, void** stream);
 
+/* engine options: "fuse" (1: fused streaming kernels in native cycles, the
+ * default; 0: the per-op kernels), for A/B parity tests and profiling.
+ * Changing an option drops the captured graphs. */
+int kc_set_option(kc_handle* h, const char* name, int value);
+
 /* keep a device-resident copy of the finest v (kc_snapshot) and copy it back
  * (kc_restore): re-running a solve from the same start without host traffic */
 int kc_snapshot(kc_handle* h);

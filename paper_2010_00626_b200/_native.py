@@ -78,6 +78,7 @@ _SIGS = {
     "kc_stream": (C.c_int, [_h, C.POINTER(C.c_void_p)]),
     "kc_fill_zero": (C.c_int, [_h, C.c_int, C.c_int]),
     "kc_snapshot": (C.c_int, [_h]),
+    "kc_set_option": (C.c_int, [_h, C.c_char_p, C.c_int]),
     "kc_restore": (C.c_int, [_h]),
 }
 

@@ -383,11 +383,15 @@ KsFn ks_post_fn(int nu, bool vz, bool norms) {
   return nullptr;
 }
 
+#define KS_SMEM_BYTES (4 * KS_WARP_SMEM_DOUBLES * (int)sizeof(double))
+
 int ks_slots(kc_handle* h, const void* fn) {
   auto it = h->ks_occ.find(fn);
   if (it != h->ks_occ.end()) return it->second;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, KS_SMEM_BYTES);
   int blocks = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, 128, 0) != cudaSuccess || blocks < 1) blocks = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, 128, KS_SMEM_BYTES) != cudaSuccess || blocks < 1)
+    blocks = 1;
   const int slots = blocks * 4 * h->num_sms;
   h->ks_occ[fn] = slots;
   return slots;
@@ -419,7 +423,7 @@ int ex_pre(kc_handle* h, int l) {
   int nw = 0;
   KsFn fn = ks_pre_fn(h->nu1, L.vzero);
   StreamParams p = ks_params(h, l, h->nu1 + 1, &nw, (const void*)fn);
-  fn<<<(nw + 3) / 4, 128, 0, h->stream>>>(p);
+  fn<<<(nw + 3) / 4, 128, KS_SMEM_BYTES, h->stream>>>(p);
   KC_LAUNCH_CHECK(h);
   ++h->launches;
   if (h->nu1 > 0) {
@@ -445,7 +449,7 @@ int ex_post(kc_handle* h, int l, bool norms) {
     if (nw > h->npart_cap) KC_FAIL(h, KC_EINVAL, "norm partial buffer too small (%d < %d)", h->npart_cap, nw);
     p.part = h->d_npart;
   }
-  fn<<<(nw + 3) / 4, 128, 0, h->stream>>>(p);
+  fn<<<(nw + 3) / 4, 128, KS_SMEM_BYTES, h->stream>>>(p);
   KC_LAUNCH_CHECK(h);
   ++h->launches;
   if (norms) {
@@ -1015,6 +1019,23 @@ int kc_profile_cycle(kc_handle* h, int kappa, int max_ops, int* op_kind, int* op
   if (se != cudaSuccess) KC_FAIL(h, KC_ECUDA, "profile cycle: %s", cudaGetErrorString(se));
   *n_ops = (int)ops.size();
   return KC_OK;
+}
+
+int kc_set_option(kc_handle* h, const char* name, int value) {
+  if (!h || !name) return KC_EINVAL;
+  if (strcmp(name, "fuse") == 0) {
+    KC_CUDA(h, cudaStreamSynchronize(h->stream));
+    h->fuse = value != 0;
+    for (auto& kv : h->graphs) {
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+      if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+      if (kv.second.loop_exec) cudaGraphExecDestroy(kv.second.loop_exec);
+      if (kv.second.loop_graph) cudaGraphDestroy(kv.second.loop_graph);
+    }
+    h->graphs.clear();
+    return KC_OK;
+  }
+  KC_FAIL(h, KC_EINVAL, "unknown option '%s'", name);
 }
 
 int kc_snapshot(kc_handle* h) {

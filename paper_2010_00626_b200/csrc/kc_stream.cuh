@@ -69,6 +69,22 @@ __device__ __forceinline__ double2 ks_ld2(const double* __restrict__ a, size_t i
   return __ldg(reinterpret_cast<const double2*>(a + i));
 }
 
+// Input rows stream through per-warp shared-memory rings filled with
+// cp.async (LDGSTS): each lane copies and later reads back only its own 16
+// bytes, so no warp synchronisation is needed, and a load in flight never
+// holds a register (a register queue would make every shift wait for it).
+#define KS_PF 4       // prefetch distance (rows)
+#define KS_URING 8    // u ring slots (> KS_PF)
+#define KS_FRING 16   // f ring slots (> 2*D + KS_PF)
+#define KS_WARP_SMEM_DOUBLES ((KS_URING + KS_FRING) * KS_BAND)
+__device__ __forceinline__ void ks_cp16(double* smem, const double* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void ks_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void ks_cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(KS_PF) : "memory"); }
+__device__ __forceinline__ double2 ks_lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+
 // ---------------------------------------------------------------------------
 // PRE: NU sweeps + residual + restriction
 // ---------------------------------------------------------------------------
@@ -89,59 +105,71 @@ __global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
   const bool own_lane = lane >= G::HL / 2 && lane < G::HL / 2 + G::NPB;
   const St9 s = p.s;
 
-  double2 W[D][3];       // last three rows of stages 0..NU (W[NU] feeds the residual)
-  double2 R[3];          // last three residual rows
-  double2 F[2 * D + 1];  // f rows yin .. yin-2D (own columns)
+  double2 W[D][3];  // last three rows of stages 0..NU (W[NU] feeds the residual)
+  double2 R[3];     // last three residual rows
 #pragma unroll
   for (int t = 0; t < D; ++t) W[t][0] = W[t][1] = W[t][2] = make_double2(0.0, 0.0);
   R[0] = R[1] = R[2] = make_double2(0.0, 0.0);
-#pragma unroll
-  for (int k = 0; k < 2 * D + 1; ++k) F[k] = make_double2(0.0, 0.0);
 
   const int ys = 2 * Q0 - D;
   const int ye = 2 * Q0 + 2 * p.nq + 2 * D + 1;  // inclusive
+  // only warps touching the domain boundary need masks / row clamping
+  const bool edge = XS < 0 || XS + KS_BAND - 1 >= m || ys - 2 * D < 0 || ye + 2 >= m;
   // rows outside [-1, m] read the all-zero ghost rows: branch-free
   auto rp = [&](int y) -> size_t { return kc_idx(P, min(max(y, -1), m), c0); };
-  double2 pu0 = ZERO ? make_double2(0.0, 0.0) : ks_ld2(p.u, rp(ys));
-  double2 pf0 = ks_ld2(p.f, rp(ys));
-  double2 pu1 = ZERO ? make_double2(0.0, 0.0) : ks_ld2(p.u, rp(ys + 1));
-  double2 pf1 = ks_ld2(p.f, rp(ys + 1));
+  // shared-memory rings (this warp's slice): u rows and f rows
+  extern __shared__ double ks_smem[];
+  double* ring = ks_smem + (threadIdx.x >> 5) * KS_WARP_SMEM_DOUBLES + 2 * lane;
+  double* uring = ring;
+  double* fring = ring + KS_URING * KS_BAND;
+  // one commit group per row: f(y) and, for rows the loop consumes, u(y).
+  // No two copies in flight may target the same slot (their completion
+  // order is not defined), hence u only from row ys on.
+  auto fetch = [&](int y, bool with_u) {
+    const size_t i = rp(y);
+    if (!ZERO && with_u) ks_cp16(uring + (y & (KS_URING - 1)) * KS_BAND, p.u + i);
+    ks_cp16(fring + (y & (KS_FRING - 1)) * KS_BAND, p.f + i);
+    ks_cp_commit();
+  };
+  // f rows from ys-2D (stage D's first row) up to ys+KS_PF-1 before the first step
+  for (int y = ys - 2 * D; y < ys + KS_PF; ++y) fetch(y, y >= ys);
   for (int yin = ys; yin <= ye; ++yin) {
-    double2 u0 = pu0;
-    const double2 f0 = pf0;
-    pu0 = pu1;
-    pf0 = pf1;
-    if (!ZERO) pu1 = ks_ld2(p.u, rp(yin + 2));
-    pf1 = ks_ld2(p.f, rp(yin + 2));
-    const bool row_in = yin >= 0 && yin < m;
-    u0.x = (row_in && colx_in) ? u0.x : 0.0;
-    u0.y = (row_in && coly_in) ? u0.y : 0.0;
+    fetch(yin + KS_PF, true);
+    ks_cp_wait();  // all but the newest KS_PF groups done: rows <= yin have landed
+    const double2 u0 = ZERO ? make_double2(0.0, 0.0) : ks_lds2(uring + (yin & (KS_URING - 1)) * KS_BAND);
+    double2 fr[D + 1];  // f of the row each stage computes
 #pragma unroll
-    for (int k = 2 * D; k > 0; --k) F[k] = F[k - 1];  // F[k] = f row (yin - k)
-    F[0] = f0;
+    for (int t = 1; t <= D; ++t) fr[t] = ks_lds2(fring + ((yin - 2 * t) & (KS_FRING - 1)) * KS_BAND);
 
     // ---- all stages from the pre-step windows (independent) -------------
     double2 nw[D + 1];
     nw[0] = u0;
 #pragma unroll
     for (int t = 1; t <= D; ++t) {
-      const int y = yin - 2 * t;
       double ox, oy;
       if (t <= NU) {
         if (ZERO && t == 1) {  // first sweep on the zero guess: 0 + c f
-          ox = kc_jacobi_zero(F[2].x, s.c);
-          oy = kc_jacobi_zero(F[2].y, s.c);
+          ox = kc_jacobi_zero(fr[1].x, s.c);
+          oy = kc_jacobi_zero(fr[1].y, s.c);
         } else {
-          ks_stencil2<true>(s, W[t - 1][0], W[t - 1][1], W[t - 1][2], F[2 * t], ox, oy);
+          ks_stencil2<true>(s, W[t - 1][0], W[t - 1][1], W[t - 1][2], fr[t], ox, oy);
         }
       } else if (ZERO && NU == 0) {  // residual of the zero guess: f exactly
-        ox = F[2 * t].x;
-        oy = F[2 * t].y;
+        ox = fr[t].x;
+        oy = fr[t].y;
       } else {
-        ks_stencil2<false>(s, W[t - 1][0], W[t - 1][1], W[t - 1][2], F[2 * t], ox, oy);
+        ks_stencil2<false>(s, W[t - 1][0], W[t - 1][1], W[t - 1][2], fr[t], ox, oy);
       }
-      const bool in = y >= 0 && y < m;
-      nw[t] = make_double2((in && colx_in) ? ox : 0.0, (in && coly_in) ? oy : 0.0);
+      nw[t] = make_double2(ox, oy);
+    }
+    if (edge) {  // Dirichlet: every stage is +0.0 outside the interior
+#pragma unroll
+      for (int t = 0; t <= D; ++t) {
+        const int y = yin - 2 * t;
+        const bool in = y >= 0 && y < m;
+        nw[t].x = (in && colx_in) ? nw[t].x : 0.0;
+        nw[t].y = (in && coly_in) ? nw[t].y : 0.0;
+      }
     }
 
     // ---- restriction from the residual rows of earlier steps ------------
@@ -195,28 +223,34 @@ __global__ void __launch_bounds__(128, 4) k_post(const StreamParams p) {
 
   if (active) {
     double2 W[DD][3];
-    double2 F[2 * DD + 1];
 #pragma unroll
     for (int t = 0; t < DD; ++t) W[t][0] = W[t][1] = W[t][2] = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int k = 0; k < 2 * DD + 1; ++k) F[k] = make_double2(0.0, 0.0);
     const int ys = 2 * Q0 - D;
     const int ye = 2 * Q0 + 2 * p.nq - 1 + 2 * D;
+    const bool edge = XS < 0 || XS + KS_BAND - 1 >= m || ys - 2 * D - 2 < 0 || ye + 4 >= m;
     auto rp = [&](int y) -> size_t { return kc_idx(P, min(max(y, -1), m), c0); };
     auto ldc = [&](int q) -> double { return __ldg(p.vc + kc_idx(p.Pc, min(max(q, -1), p.mc), pc)); };
     // coarse rows around the input row: vcp = row q-1, vcc = row q (q = floor(yin/2))
     int qcur = ys >> 1;  // arithmetic shift: floor
     double vcp = ldc(qcur - 1), vcc = ldc(qcur), vcn = ldc(qcur + 1);
-    double2 pu0 = VZ ? make_double2(0.0, 0.0) : ks_ld2(p.u, rp(ys));
-    double2 pf0 = ks_ld2(p.f, rp(ys));
-    double2 pu1 = VZ ? make_double2(0.0, 0.0) : ks_ld2(p.u, rp(ys + 1));
-    double2 pf1 = ks_ld2(p.f, rp(ys + 1));
+    extern __shared__ double ks_smem[];
+    double* ring = ks_smem + (threadIdx.x >> 5) * KS_WARP_SMEM_DOUBLES + 2 * lane;
+    double* uring = ring;
+    double* fring = ring + KS_URING * KS_BAND;
+    auto fetch = [&](int y, bool with_u) {  // see k_pre: u only from row ys on
+      const size_t i = rp(y);
+      if (!VZ && with_u) ks_cp16(uring + (y & (KS_URING - 1)) * KS_BAND, p.u + i);
+      ks_cp16(fring + (y & (KS_FRING - 1)) * KS_BAND, p.f + i);
+      ks_cp_commit();
+    };
+    for (int y = ys - 2 * D; y < ys + KS_PF; ++y) fetch(y, y >= ys);
     for (int yin = ys; yin <= ye; ++yin) {
-      const double2 u0 = pu0, f0 = pf0;
-      pu0 = pu1;
-      pf0 = pf1;
-      if (!VZ) pu1 = ks_ld2(p.u, rp(yin + 2));
-      pf1 = ks_ld2(p.f, rp(yin + 2));
+      fetch(yin + KS_PF, true);
+      ks_cp_wait();
+      const double2 u0 = VZ ? make_double2(0.0, 0.0) : ks_lds2(uring + (yin & (KS_URING - 1)) * KS_BAND);
+      double2 fr[DD + 1];
+#pragma unroll
+      for (int t = 1; t <= D; ++t) fr[t] = ks_lds2(fring + ((yin - 2 * t) & (KS_FRING - 1)) * KS_BAND);
       const int q = yin >> 1;
       if (q != qcur) {  // advance the coarse window by one row (yin even); warp-uniform
         vcp = vcc;
@@ -234,24 +268,23 @@ __global__ void __launch_bounds__(128, 4) k_post(const StreamParams p) {
         ex = DMUL(0.25, DADD(DADD(DADD(lp, vcp), lc), vcc));
         ey = DMUL(0.5, DADD(vcp, vcc));
       }
-      const bool row_in = yin >= 0 && yin < m;
-      double2 s0;
-      s0.x = (row_in && colx_in) ? DADD(VZ ? 0.0 : u0.x, ex) : 0.0;
-      s0.y = (row_in && coly_in) ? DADD(VZ ? 0.0 : u0.y, ey) : 0.0;
-#pragma unroll
-      for (int k = 2 * DD; k > 0; --k) F[k] = F[k - 1];
-      F[0] = f0;
-
       double2 nw[DD + 1];
-      nw[0] = s0;
+      nw[0] = make_double2(DADD(VZ ? 0.0 : u0.x, ex), DADD(VZ ? 0.0 : u0.y, ey));
 #pragma unroll
       for (int t = 1; t <= D; ++t) {
-        const int y = yin - 2 * t;
         double ox, oy;
-        if (t <= NU) ks_stencil2<true>(s, W[t - 1][0], W[t - 1][1], W[t - 1][2], F[2 * t], ox, oy);
-        else ks_stencil2<false>(s, W[t - 1][0], W[t - 1][1], W[t - 1][2], F[2 * t], ox, oy);
-        const bool in = y >= 0 && y < m;
-        nw[t] = make_double2((in && colx_in) ? ox : 0.0, (in && coly_in) ? oy : 0.0);
+        if (t <= NU) ks_stencil2<true>(s, W[t - 1][0], W[t - 1][1], W[t - 1][2], fr[t], ox, oy);
+        else ks_stencil2<false>(s, W[t - 1][0], W[t - 1][1], W[t - 1][2], fr[t], ox, oy);
+        nw[t] = make_double2(ox, oy);
+      }
+      if (edge) {  // Dirichlet: every stage is +0.0 outside the interior
+#pragma unroll
+        for (int t = 0; t <= D; ++t) {
+          const int y = yin - 2 * t;
+          const bool in = y >= 0 && y < m;
+          nw[t].x = (in && colx_in) ? nw[t].x : 0.0;
+          nw[t].y = (in && coly_in) ? nw[t].y : 0.0;
+        }
       }
       // output after NU sweeps (stage NU; NU = 0 writes the corrected v)
       {

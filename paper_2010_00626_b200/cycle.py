@@ -313,6 +313,10 @@ class CudaGridState:
         k = it.value
         return k, N.STATUS_NAMES[st.value], dms.value, err[: k + 1].tolist(), res[: k + 1].tolist()
 
+    def set_option(self, name: str, value: int):
+        """Engine option (kc_set_option): "fuse" = 0 runs native cycles on the per-op kernels."""
+        N.check(N.lib.kc_set_option(self._h, name.encode(), int(value)), self._h)
+
     def snapshot(self):
         """Keep a device copy of the finest v (restore() puts it back)."""
         N.check(N.lib.kc_snapshot(self._h), self._h)

@@ -447,3 +447,36 @@ def test_validation_errors_map_to_reference_types():
         st.v[5]
     with pytest.raises(ValueError):
         solve_standalone(ProblemSpec(1e-4, 45.0), CycleConfig(n=3), 1.0)
+
+
+# ---------------------------------------------------------------------------
+# fused streaming kernels vs per-op kernels vs the oracle, across sizes and nu
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [6, 7, 8, 9, 10])
+@pytest.mark.parametrize("nu1,nu2", [(2, 2), (1, 1), (2, 0), (0, 2), (3, 1), (4, 4)])
+def test_fused_matches_per_op_and_oracle(n, nu1, nu2):
+    """Native cycles run k_pre/k_post on every HBM level (side >= 127); with
+    fuse=0 they run the per-op kernels.  Both must equal the oracle bit-for-bit
+    for non-zero f, over two cycles (the second starts from a non-zero v and
+    exercises the buffer parity after the first)."""
+    m = 2 ** n - 1
+    rng = np.random.default_rng(100 * n + 10 * nu1 + nu2)
+    v0, f0 = rng.random((m, m)), rng.standard_normal((m, m))
+    problem = ProblemSpec(1e-3, 30.0)
+    for kappa in (1, 2):
+        cfg = CycleConfig(n=n, kappa=kappa, nu1=nu1, nu2=nu2)
+        h = O.Hierarchy(O.hierarchy(1e-3, 30.0, n), nu1=nu1, nu2=nu2)
+        h.v[0], h.f[0] = v0.copy(), f0.copy()
+        ref = []
+        for _ in range(2):
+            h.cycle(kappa)
+            ref.append(h.v[0].copy())
+        for fuse in (1, 0):
+            st = build_state(problem, cfg)
+            st.set_option("fuse", fuse)
+            st.v[0], st.f[0] = v0, f0
+            for c in range(2):
+                run_cycle(st, cfg, CycleStats.for_levels(n))
+                assert np.array_equal(st.v[0], ref[c]), (n, nu1, nu2, kappa, fuse, c)
+            st.close()
