@@ -142,8 +142,10 @@ int kc_profile_cycle(kc_handle* h, int kappa, int max_ops, int* op_kind, int* op
  * harness can record its own events on the stream the kernels run on */
 int kc_stream(kc_handle* h, void** stream);
 
-/* engine options: "fuse" (1: fused streaming kernels in native cycles, the
- * default; 0: the per-op kernels), for A/B parity tests and profiling.
+/* engine options: "fuse" (1: fused kernels in native cycles, the default;
+ * 0: the per-op kernels) and "tile" (1: overlapped-tile kernels on sides
+ * <= 511, the default; 0: streaming kernels there too), for A/B parity tests
+ * and profiling.
  * Changing an option drops the captured graphs. */
 int kc_set_option(kc_handle* h, const char* name, int value);
 

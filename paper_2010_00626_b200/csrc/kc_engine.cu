@@ -26,6 +26,7 @@
 #include "kc_grid_kernels.cuh"
 #include "kc_pcg.cuh"
 #include "kc_stream.cuh"
+#include "kc_tile.cuh"
 
 namespace {
 
@@ -77,7 +78,8 @@ struct Level {
 
 enum OpKind : int { OP_RELAX, OP_RESTRICT, OP_ZERO, OP_PROLONG, OP_COARSEST, OP_BOTTOM, OP_PRE, OP_POST };
 #define KC_FUSE_MAXNU 4      // fused streaming kernels exist for nu <= 4
-#define KC_FUSE_MIN_M 127    // HBM levels handled by the streaming kernels
+#define KC_FUSE_MIN_M 127    // HBM levels handled by the fused kernels
+#define KC_TILE_MAX_M 511    // up to this side the overlapped-tile kernels beat streaming
 struct Op {
   int kind, level, a, b;
 };
@@ -113,6 +115,7 @@ struct kc_handle {
   double* d_npart = nullptr;  // per-warp norm partials of the fused level-1 post kernel
   int npart_cap = 0;
   bool fuse = true;           // use the fused streaming kernels in native cycles
+  bool tile = true;           // overlapped-tile kernels on the mid-size levels
   int num_sms = 148;
   SolveState* d_solve = nullptr;   // device loop state
   double* d_hist = nullptr;        // err | res histories for the device loop
@@ -417,9 +420,67 @@ StreamParams ks_params(kc_handle* h, int l, int D, int* nwarps, const void* fn) 
   return p;
 }
 
+typedef void (*KtFn)(TileParams);
+KtFn kt_pre_fn(int nu, bool zero) {
+#define KT_PRE(N) return zero ? k_tile_pre<N, true> : k_tile_pre<N, false>
+  switch (nu) {
+    case 0: KT_PRE(0);
+    case 1: KT_PRE(1);
+    case 2: KT_PRE(2);
+    case 3: KT_PRE(3);
+    case 4: KT_PRE(4);
+  }
+#undef KT_PRE
+  return nullptr;
+}
+KtFn kt_post_fn(int nu, bool vz) {
+#define KT_POST(N) return vz ? k_tile_post<N, true> : k_tile_post<N, false>
+  switch (nu) {
+    case 0: KT_POST(0);
+    case 1: KT_POST(1);
+    case 2: KT_POST(2);
+    case 3: KT_POST(3);
+    case 4: KT_POST(4);
+  }
+#undef KT_POST
+  return nullptr;
+}
+
+int ex_tile(kc_handle* h, int l, bool pre) {
+  Level& L = h->L[l];
+  Level& C = h->L[l + 1];
+  TileParams p{};
+  p.u = L.v[L.cur];
+  p.f = L.f;
+  p.uo = L.v[L.cur ^ 1];
+  p.fc = C.f;
+  p.vc = C.v[C.cur];
+  p.m = L.m;
+  p.P = L.P;
+  p.mc = C.m;
+  p.Pc = C.P;
+  p.s = L.st;
+  p.tiles_x = (L.m + KT_TX - 1) / KT_TX;
+  const int tiles = p.tiles_x * ((L.m + KT_TY - 1) / KT_TY);
+  const int nu = pre ? h->nu1 : h->nu2;
+  const int D = pre ? nu + 1 : (nu > 0 ? nu : 1);
+  const size_t smem = sizeof(double) * (size_t)kt_smem_doubles(D);
+  KtFn fn = pre ? kt_pre_fn(nu, L.vzero) : kt_post_fn(nu, L.vzero);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  fn<<<tiles, KT_THREADS, smem, h->stream>>>(p);
+  KC_LAUNCH_CHECK(h);
+  ++h->launches;
+  if (!pre || nu > 0) {
+    L.cur ^= 1;
+    L.vzero = false;
+  }
+  return KC_OK;
+}
+
 // relax(nu1) + restrict_residual (cycle.py:211-213) in one pass
 int ex_pre(kc_handle* h, int l) {
   Level& L = h->L[l];
+  if (L.m <= KC_TILE_MAX_M && h->tile) return ex_tile(h, l, true);
   int nw = 0;
   KsFn fn = ks_pre_fn(h->nu1, L.vzero);
   StreamParams p = ks_params(h, l, h->nu1 + 1, &nw, (const void*)fn);
@@ -440,6 +501,7 @@ int ex_post(kc_handle* h, int l, bool norms) {
   Level& C = h->L[l + 1];
   int rc = ex_materialize(h, l + 1);
   if (rc) return rc;
+  if (L.m <= KC_TILE_MAX_M && h->tile && !norms) return ex_tile(h, l, false);
   int nw = 0;
   const int D = h->nu2 + (norms ? 1 : 0);
   KsFn fn = ks_post_fn(h->nu2, L.vzero, norms);
@@ -1023,9 +1085,10 @@ int kc_profile_cycle(kc_handle* h, int kappa, int max_ops, int* op_kind, int* op
 
 int kc_set_option(kc_handle* h, const char* name, int value) {
   if (!h || !name) return KC_EINVAL;
-  if (strcmp(name, "fuse") == 0) {
+  if (strcmp(name, "fuse") == 0 || strcmp(name, "tile") == 0) {
     KC_CUDA(h, cudaStreamSynchronize(h->stream));
-    h->fuse = value != 0;
+    if (name[0] == 'f') h->fuse = value != 0;
+    else h->tile = value != 0;
     for (auto& kv : h->graphs) {
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
       if (kv.second.graph) cudaGraphDestroy(kv.second.graph);

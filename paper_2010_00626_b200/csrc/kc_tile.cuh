@@ -1,0 +1,178 @@
+// kc_tile.cuh — fused overlapped-tile kernels for the mid-size HBM levels.
+//
+// Same operations as k_pre / k_post (kc_stream.cuh) but for levels whose
+// cost is latency, not bandwidth (sides 127 .. 511 here): a streaming warp
+// spends most of its life warming up its stage pipeline there.  Instead each
+// CTA stages one 2D tile plus a D-deep halo in shared memory and runs the
+// stages one after another with a CTA barrier between them (halo points are
+// recomputed by neighbouring tiles).  Per launch: one global load phase, D
+// short compute phases, one store phase.
+//
+//   k_tile_pre<NU, ZERO>   NU sweeps + residual + full weighting
+//   k_tile_post<NU, VZ>    v + P vc + NU sweeps
+//
+// Arithmetic is the reference's (kc_common.cuh): bit-identical results.
+#pragma once
+#include "kc_common.cuh"
+
+#define KT_TY 16        // fine rows owned per tile (even)
+#define KT_TX 32        // fine columns owned per tile (even)
+#define KT_THREADS 256
+
+struct TileParams {
+  const double* u;
+  const double* f;
+  double* uo;
+  double* fc;
+  const double* vc;
+  int m, P, mc, Pc;
+  int tiles_x;
+  St9 s;
+};
+
+// shared-memory footprint (doubles) of a tile kernel with D stencil stages
+__host__ __device__ constexpr int kt_region(int D) { return (KT_TY + 1 + 2 * D) * (KT_TX + 1 + 2 * D); }
+#define KT_CM 4  // coarse-patch margin (covers halos D <= 5)
+#define KT_CH (KT_TY / 2 + 2 * KT_CM + 1)
+#define KT_CW (KT_TX / 2 + 2 * KT_CM + 1)
+__host__ __device__ constexpr int kt_smem_doubles(int D) { return 3 * kt_region(D) + KT_CH * KT_CW; }
+
+// Stage t buffer covers rows [y0 - (D - t), y0 + TY + (D - t)] and likewise
+// columns, stored with the full stage-0 stride so all stages share indexing:
+// element (y, x) at (y - y0 + D) * W + (x - x0 + D), W = TX + 1 + 2D.
+template <int D>
+struct KtGeom {
+  static constexpr int W = KT_TX + 1 + 2 * D;
+  static constexpr int H = KT_TY + 1 + 2 * D;
+};
+
+template <int NU, bool ZERO>
+__global__ void __launch_bounds__(KT_THREADS) k_tile_pre(const TileParams p) {
+  constexpr int D = NU + 1;
+  using G = KtGeom<D>;
+  extern __shared__ double sm[];
+  double* buf[2] = {sm, sm + G::H * G::W};
+  double* fs = sm + 2 * G::H * G::W;
+  const int tx = blockIdx.x % p.tiles_x, ty = blockIdx.x / p.tiles_x;
+  const int y0 = ty * KT_TY, x0 = tx * KT_TX;
+  const int m = p.m, P = p.P;
+  const St9 s = p.s;
+  // load u (stage 0) and f on the full region; outside [-1, m] read ghost zeros
+  for (int i = threadIdx.x; i < G::H * G::W; i += KT_THREADS) {
+    const int ry = i / G::W, rx = i - ry * G::W;
+    const int y = y0 - D + ry, x = x0 - D + rx;
+    const bool in = y >= 0 && y < m && x >= 0 && x < m;
+    const size_t gi = kc_idx(P, min(max(y, -1), m), min(max(x, -1), m));
+    fs[i] = __ldg(p.f + gi);
+    buf[0][i] = (ZERO || !in) ? 0.0 : __ldg(p.u + gi);
+  }
+  __syncthreads();
+  int cur = 0;
+#pragma unroll 1
+  for (int t = 1; t <= D; ++t) {
+    const int h = D - t;  // halo of this stage
+    const int rh = KT_TY + 1 + 2 * h, rw = KT_TX + 1 + 2 * h;
+    const double* src = buf[cur];
+    double* dst = buf[cur ^ 1];
+    const bool zero_sweep = ZERO && t == 1;
+    for (int i = threadIdx.x; i < rh * rw; i += KT_THREADS) {
+      const int ry = i / rw, rx = i - ry * rw;
+      const int y = y0 - h + ry, x = x0 - h + rx;
+      const int k = (ry + t) * G::W + (rx + t);
+      double v = 0.0;
+      if (y >= 0 && y < m && x >= 0 && x < m) {
+        if (t <= NU) {
+          v = zero_sweep ? kc_jacobi_zero(fs[k], s.c) : kc_jacobi_pt(src[k], fs[k], kc_apply9(src + k, G::W, s), s.c);
+        } else {
+          v = (ZERO && NU == 0) ? fs[k] : DSUB(fs[k], kc_apply9(src + k, G::W, s));
+        }
+      }
+      dst[k] = v;
+    }
+    __syncthreads();
+    if (t == NU) {  // v after NU sweeps: owned points
+      for (int i = threadIdx.x; i < KT_TY * KT_TX; i += KT_THREADS) {
+        const int ry = i / KT_TX, rx = i - ry * KT_TX;
+        const int y = y0 + ry, x = x0 + rx;
+        if (y < m && x < m) p.uo[kc_idx(P, y, x)] = dst[(ry + D) * G::W + (rx + D)];
+      }
+    }
+    cur ^= 1;
+  }
+  // full weighting of the residual (buffer cur) for the tile's coarse nodes
+  const double* r = buf[cur];
+  for (int i = threadIdx.x; i < (KT_TY / 2) * (KT_TX / 2); i += KT_THREADS) {
+    const int qy = i / (KT_TX / 2), qx = i - qy * (KT_TX / 2);
+    const int q = y0 / 2 + qy, pc = x0 / 2 + qx;
+    if (q < p.mc && pc < p.mc) {
+      const double* rc = r + (2 * qy + 1 + D) * G::W + (2 * qx + 1 + D);
+      const double* rs = rc - G::W;
+      const double* rn = rc + G::W;
+      p.fc[kc_idx(p.Pc, q, pc)] = kc_fw(rs[-1], rs[0], rs[1], rc[-1], rc[0], rc[1], rn[-1], rn[0], rn[1]);
+    }
+  }
+}
+
+template <int NU, bool VZ>
+__global__ void __launch_bounds__(KT_THREADS) k_tile_post(const TileParams p) {
+  constexpr int D = NU > 0 ? NU : 1;
+  using G = KtGeom<D>;
+  extern __shared__ double sm[];
+  double* buf[2] = {sm, sm + G::H * G::W};
+  double* fs = sm + 2 * G::H * G::W;
+  double* cs = sm + 3 * G::H * G::W;  // coarse v patch
+  constexpr int CW = KT_CW;
+  constexpr int CH = KT_CH;
+  const int tx = blockIdx.x % p.tiles_x, ty = blockIdx.x / p.tiles_x;
+  const int y0 = ty * KT_TY, x0 = tx * KT_TX;
+  const int m = p.m, P = p.P;
+  const St9 s = p.s;
+  // coarse patch rows/cols q in [y0/2 - CM, y0/2 + TY/2 + CM], clamped onto the ghost ring
+  const int qy0 = y0 / 2 - KT_CM, qx0 = x0 / 2 - KT_CM;
+  for (int i = threadIdx.x; i < CH * CW; i += KT_THREADS) {
+    const int cy = i / CW, cx = i - cy * CW;
+    const int q = min(max(qy0 + cy, -1), p.mc), pc = min(max(qx0 + cx, -1), p.mc);
+    cs[i] = __ldg(p.vc + kc_idx(p.Pc, q, pc));
+  }
+  for (int i = threadIdx.x; i < G::H * G::W; i += KT_THREADS) {
+    const int ry = i / G::W, rx = i - ry * G::W;
+    const int y = y0 - D + ry, x = x0 - D + rx;
+    const size_t gi = kc_idx(P, min(max(y, -1), m), min(max(x, -1), m));
+    fs[i] = __ldg(p.f + gi);
+    if (!VZ) buf[1][i] = __ldg(p.u + gi);
+  }
+  __syncthreads();
+  // stage 0: v + P vc on the full region (zero outside the interior)
+  auto cp = [&](int q, int pc) { return cs[(q - qy0) * CW + (pc - qx0)]; };
+  for (int i = threadIdx.x; i < G::H * G::W; i += KT_THREADS) {
+    const int ry = i / G::W, rx = i - ry * G::W;
+    const int y = y0 - D + ry, x = x0 - D + rx;
+    double v = 0.0;
+    if (y >= 0 && y < m && x >= 0 && x < m) v = DADD(VZ ? 0.0 : buf[1][i], kc_prolong_val(y, x, cp));
+    buf[0][i] = v;
+  }
+  __syncthreads();
+  int cur = 0;
+#pragma unroll 1
+  for (int t = 1; t <= NU; ++t) {
+    const int h = D - t;
+    const int rh = KT_TY + 1 + 2 * h, rw = KT_TX + 1 + 2 * h;
+    const double* src = buf[cur];
+    double* dst = buf[cur ^ 1];
+    for (int i = threadIdx.x; i < rh * rw; i += KT_THREADS) {
+      const int ry = i / rw, rx = i - ry * rw;
+      const int y = y0 - h + ry, x = x0 - h + rx;
+      const int k = (ry + t) * G::W + (rx + t);
+      dst[k] = (y >= 0 && y < m && x >= 0 && x < m) ? kc_jacobi_pt(src[k], fs[k], kc_apply9(src + k, G::W, s), s.c)
+                                                     : 0.0;
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+  const double* o = buf[cur];
+  for (int i = threadIdx.x; i < KT_TY * KT_TX; i += KT_THREADS) {
+    const int ry = i / KT_TX, rx = i - ry * KT_TX;
+    const int y = y0 + ry, x = x0 + rx;
+    if (y < m && x < m) p.uo[kc_idx(P, y, x)] = o[(ry + D) * G::W + (rx + D)];
+  }
+}

@@ -472,11 +472,12 @@ def test_fused_matches_per_op_and_oracle(n, nu1, nu2):
         for _ in range(2):
             h.cycle(kappa)
             ref.append(h.v[0].copy())
-        for fuse in (1, 0):
+        for fuse, tile in ((1, 1), (1, 0), (0, 0)):
             st = build_state(problem, cfg)
             st.set_option("fuse", fuse)
+            st.set_option("tile", tile)
             st.v[0], st.f[0] = v0, f0
             for c in range(2):
                 run_cycle(st, cfg, CycleStats.for_levels(n))
-                assert np.array_equal(st.v[0], ref[c]), (n, nu1, nu2, kappa, fuse, c)
+                assert np.array_equal(st.v[0], ref[c]), (n, nu1, nu2, kappa, fuse, tile, c)
             st.close()
