@@ -313,6 +313,17 @@ class CudaGridState:
         k = it.value
         return k, N.STATUS_NAMES[st.value], dms.value, err[: k + 1].tolist(), res[: k + 1].tolist()
 
+    def get_level(self, level: int = 1, which: str = "v", out: np.ndarray | None = None) -> np.ndarray:
+        """Copy v or f of `level` to the host (into `out` when given)."""
+        nx, ny = self.spec.dims[level - 1]
+        if out is None:
+            out = np.empty((ny, nx))
+        elif out.shape != (ny, nx) or out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float64 array of the level shape")
+        w = N.KC_WHICH_V if which == "v" else N.KC_WHICH_F
+        N.check(N.lib.kc_get(self._h, level, w, N.dptr(out), ny, nx), self._h)
+        return out
+
     def set_option(self, name: str, value: int):
         """Engine option (kc_set_option): "fuse" = 0 runs native cycles on the per-op kernels."""
         N.check(N.lib.kc_set_option(self._h, name.encode(), int(value)), self._h)
@@ -464,6 +475,7 @@ def solve_standalone(
     stop: str = "error",
     device: int = 0,
     state: CudaGridState | None = None,
+    solution_out: np.ndarray | None = None,
 ) -> SolveReport:
     """Repeated cycles on the zero-solution problem (cycle.py:303-366), on the device.
 
@@ -471,7 +483,9 @@ def solve_standalone(
     cycle.py:332-347); `stop="residual"` stops on the true relative residual
     ||f - A v_k|| <= ||f - A v_0|| / target (BASELINE headline).  Both
     histories are recorded every cycle either way.  `state` lets a caller
-    reuse an already built hierarchy (it must match `config`).
+    reuse an already built hierarchy (it must match `config`);
+    `solution_out` (a C-contiguous float64 array of the finest shape, e.g.
+    in pinned memory) receives the solution instead of a new array.
     """
     if target_reduction <= 1.0:
         raise ValueError(f"target reduction must exceed 1, got {target_reduction}")
@@ -508,7 +522,7 @@ def solve_standalone(
         asymptotic_factor=_asymptotic_factor(reductions),
         stats=stats,
         wall_time_ms=wall_ms,
-        solution=state.v[0],
+        solution=state.get_level(1, "v", solution_out),
         error_history=err_hist,
         residual_history=res_hist,
         stop=stop,
