@@ -82,7 +82,19 @@ __device__ long long kc_bot_trace_end[KC_BOT_TRACE];
 // Phase descriptor (host-built by bot_schedule in kc_engine.cu):
 //  bits 0-2 op (PH_*), 3-5 level d, 6 src buffer, 7 zero guess, 8 child buffer
 //  (prolong), 9 child is the 1x1 coarsest (restrict), 10-11 warp group code.
-enum BotOp { PH_JACOBI = 0, PH_RESID = 1, PH_RESTRICT = 2, PH_PROLONG = 3, PH_JOIN = 4 };
+// Fused phases cut the dependent phases of a routine call from 7 to 4:
+//   PH_J2Z  two sweeps from the zero guess: u1 = 0 + c f is pointwise, so the
+//           second sweep recomputes it at its 3x3 neighbours from f (+0.0 on
+//           the ghost ring, exactly the Dirichlet value);
+//   PH_RR   residual + full weighting, each coarse node forming its 3x3 fine
+//           residuals (small levels);
+//   PH_PJ   prolong-correct + first post sweep, each point forming the
+//           corrected v at its 3x3 neighbours (small levels).
+// Same per-point arithmetic, so results stay bit-identical.
+enum BotOp {
+  PH_JACOBI = 0, PH_RESID = 1, PH_RESTRICT = 2, PH_PROLONG = 3, PH_JOIN = 4, PH_J2Z = 5, PH_RR = 6, PH_PJ = 7
+};
+#define KC_BOT_FUSE_M 15  // PH_RR / PH_PJ on sides <= this (latency-bound levels)
 __host__ __device__ __forceinline__ unsigned bot_desc(int op, int d, int src, int zero, int cbuf, int cc, int g) {
   const unsigned gc = g >= KC_BOT_WARPS ? 3u : (g >= 8 ? 2u : (g >= 2 ? 1u : 0u));
   return (unsigned)op | ((unsigned)d << 3) | ((unsigned)src << 6) | ((unsigned)zero << 7) | ((unsigned)cbuf << 8) |
@@ -108,8 +120,16 @@ struct BotBuilder {  // host side
     gprev = g;
     out.push_back(bot_desc(op, d, src, zero, cbuf, cc, g));
   }
+  bool fuse = true;         // emit PH_J2Z
+  bool fuse_small = false;  // emit PH_RR / PH_PJ (measured slower: larger kernel, longer chains)
   void relax(int d, int count) {
-    for (int i = 0; i < count; ++i) {
+    int i = 0;
+    if (fuse && count >= 2 && ((vz >> d) & 1u)) {  // two sweeps from the zero guess: result in buffer cur
+      emit(PH_J2Z, d, (cur >> d) & 1u, 1, 0, 0);
+      vz &= ~(1u << d);
+      i = 2;
+    }
+    for (; i < count; ++i) {
       emit(PH_JACOBI, d, (cur >> d) & 1u, (vz >> d) & 1u, 0, 0);
       vz &= ~(1u << d);
       cur ^= 1u << d;
@@ -119,9 +139,14 @@ struct BotBuilder {  // host side
     relax(d, nu1);
     const int c = (cur >> d) & 1u;
     const int z = (vz >> d) & 1u;
-    if (!z) emit(PH_RESID, d, c, 0, 0, 0);  // residual into buffer c^1
     const int cc = (d + 1 == nlev - 1);
-    emit(PH_RESTRICT, d, c ^ 1, z, 0, cc);
+    const bool small = fuse && fuse_small && bot_m(m0, d) <= KC_BOT_FUSE_M;
+    if (small && !z) {
+      emit(PH_RR, d, c, 0, 0, cc);
+    } else {
+      if (!z) emit(PH_RESID, d, c, 0, 0, 0);  // residual into buffer c^1
+      emit(PH_RESTRICT, d, c ^ 1, z, 0, cc);
+    }
     cur &= ~(1u << (d + 1));
     if (cc) {
       vz &= ~(1u << (d + 1));  // both coarsest calls: one f/center inside the restriction
@@ -130,9 +155,16 @@ struct BotBuilder {  // host side
       rec(d + 1, kap);
       if (kap > 1) rec(d + 1, kap - 1);
     }
-    emit(PH_PROLONG, d, (cur >> d) & 1u, (vz >> d) & 1u, (cur >> (d + 1)) & 1u, 0);
-    vz &= ~(1u << d);
-    relax(d, nu2);
+    if (small && nu2 > 0) {  // prolong-correct fused with the first post sweep
+      emit(PH_PJ, d, (cur >> d) & 1u, (vz >> d) & 1u, (cur >> (d + 1)) & 1u, 0);
+      vz &= ~(1u << d);
+      cur ^= 1u << d;
+      relax(d, nu2 - 1);
+    } else {
+      emit(PH_PROLONG, d, (cur >> d) & 1u, (vz >> d) & 1u, (cur >> (d + 1)) & 1u, 0);
+      vz &= ~(1u << d);
+      relax(d, nu2);
+    }
   }
 };
 
@@ -261,7 +293,20 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
       kc_bot_trace_n = ++tr_n;
     }
 #endif
-    if (op <= PH_RESID) {
+    if (op == PH_J2Z) {  // u2 = J(J(0)) with u1 = 0 + c f recomputed at the neighbours
+      const St9 st = tab[d];
+      for (int i = tid; i < L.nitem1; i += nth) {
+        const int y = bot_div(i, L.inv), x = i - y * m;
+        const double* pf = f + y * S + x;
+        double n1[9];
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx) n1[dy * 3 + dx] = kc_jacobi_zero(pf[(dy - 1) * S + (dx - 1)], st.c);
+        const double au = kc_sum9(st, n1[0], n1[1], n1[2], n1[3], n1[4], n1[5], n1[6], n1[7], n1[8]);
+        u[y * S + x] = kc_jacobi_pt(n1[4], pf[0], au, st.c);
+      }
+    } else if (op <= PH_RESID) {
       double* o = sm + (src ? L.vo0 : L.vo1);
       const St9 st = tab[d];
       if (m >= 31) bot_stencil<4>(op == PH_JACOBI, zero, u, o, f, m, S, L.inv, st, tid, nth, L.nitem4);
