@@ -17,7 +17,7 @@
 
 #define KT_TY 16        // fine rows owned per tile (even)
 #define KT_TX 32        // fine columns owned per tile (even)
-#define KT_THREADS 256
+#define KT_THREADS 512
 
 struct TileParams {
   const double* u;
