@@ -364,6 +364,30 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                "api": "paper_2010_00626_b200.solve_standalone(initial_guess=pinned host v0, stop='residual', "
                       "solution_out=pinned host array)"}
 
+    # ---- config C3: the kappa-cycle as PCG preconditioner (MGCG), same problem
+    pcg = None
+    if not args.quick:
+        pcg = {}
+        zeros = np.zeros((m, m))
+        for pk in cands:
+            k = n if pk == "W" else int(pk)
+            cfgk = kc.CycleConfig(n=n, kappa=math.inf if pk == "W" else k)
+            pc = kc.PcgConfig(cycle=cfgk, target_reduction=args.target, stop="residual", max_iterations=2000)
+            kc.pcg_solve(state, zeros, pc, x0=v0)  # warm (captures the graphs)
+            reps = [kc.pcg_solve(state, zeros, pc, x0=v0) for _ in range(2)]
+            gp = os.path.join(ROOT, "tests", "golden", f"pcg_n{n}_k{pk}.json")
+            ref_it = None
+            if os.path.exists(gp):
+                with open(gp) as fh:
+                    ref_it = json.load(fh)["iters"]["residual_1e10"]
+            pcg[pk] = {"iterations": reps[-1].iterations, "reference_iterations": ref_it,
+                          "status": reps[-1].status,
+                          "ms_to_solution": min(r.device_time_ms for r in reps),
+                          "ms_per_iteration": min(r.device_time_ms for r in reps) / max(1, reps[-1].iterations)}
+        pbest = min(pcg, key=lambda kk: pcg[kk]["ms_to_solution"])
+        pcg = {"best_kappa": pbest, "best_ms": pcg[pbest]["ms_to_solution"], "stop": "recursive residual 1e-10 "
+               "(PcgConfig default, krylov.py:51)", "sweep": pcg}
+
     # ---- CPU baseline (oracle, rank 0, N = 1 only) ---------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -397,6 +421,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "gpu_launches": gpu_launches,
             "clocks": clocks,
             "sweep": sweep,
+            "pcg": pcg,
             "cycle_profile": {"eager_cycle_ms": cycle_ms_eager, "bottom_kernel_ms": bottom_ms,
                               "per_level_ms": per_level},
         }

@@ -481,3 +481,29 @@ def test_fused_matches_per_op_and_oracle(n, nu1, nu2):
                 run_cycle(st, cfg, CycleStats.for_levels(n))
                 assert np.array_equal(st.v[0], ref[c]), (n, nu1, nu2, kappa, fuse, tile, c)
             st.close()
+
+
+@pytest.mark.parametrize("kname", ["1", "2", "3", "4", "W"])
+def test_n12_pcg_vs_reference(kname):
+    """Config C3: the kappa-cycle as PCG preconditioner at
+    4097^2 -- identical iteration counts to the reference under the CLI rule
+    (stop="error", 1e8) and the PcgConfig default (recursive residual, 1e10)."""
+    name = f"pcg_n12_k{kname}.json"
+    if not golden_exists(name):
+        pytest.skip(f"{name} not generated")
+    g = load_json(name)
+    n, m = 12, 4095
+    kappa = INF if kname == "W" else int(kname)
+    cfg = CycleConfig(n=n, kappa=kappa)
+    problem = ProblemSpec(1e-4, 45.0, seed=0)
+    x0 = np.random.default_rng(0).random((m, m))
+    f = np.zeros((m, m))
+    state = build_state(problem, cfg)
+    for stop, tgt, key, hist_key in (("error", 1e8, "error_1e8", "x_hist"), ("residual", 1e10, "residual_1e10", "r_hist")):
+        rep = pcg_solve(state, f, PcgConfig(cycle=cfg, target_reduction=tgt, stop=stop), x0=x0)
+        assert rep.status == "converged"
+        assert rep.iterations == g["iters"][key], (stop, rep.iterations, g["iters"][key])
+        hist = np.asarray(rep.error_history if stop == "error" else rep.residual_history)
+        ref_h = np.asarray(g[hist_key][: len(hist)])
+        assert np.max(np.abs(hist - ref_h)) / ref_h[0] < 1e-10
+    state.close()
