@@ -31,6 +31,7 @@ from .cycle import (
     run_cycle,
     solve_standalone,
 )
+from . import costmodel
 from .krylov import PcgConfig, pcg_solve
 from .mesh import Coarsening, HierarchySpec, build_hierarchy
 from .smoother import SmootherKind, SmootherSpec

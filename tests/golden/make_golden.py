@@ -378,14 +378,54 @@ def gen_dry():
     dump("dry_stats.json", out)
 
 
+def gen_costmodel():
+    """Closed forms, model predictions, fits and turning points (costmodel.py)."""
+    from kcycle import costmodel as cm
+    out = {"cells": [], "f_factor": [], "n_ops": [], "turning_points": [], "fit": None}
+    for kappa in (1, 2, 3, 4, 5, 6, INF):
+        for n in range(1, 15):
+            cell = {"kappa": kname(kappa), "n": n,
+                    "level_calls": [cm.level_calls(kappa, l) for l in range(1, n + 1)],
+                    "total_calls": cm.total_calls(kappa, n),
+                    "n_gpu_calls": {str(nu): cm.n_gpu_calls(kappa, n, nu) for nu in (0, 2, 4)},
+                    "ops_per_unknown": cm.ops_per_unknown(kappa),
+                    "predicted_ms_paper": cm.predict_runtime(cm.CostModelParams(2.48e-3, 1.18e-6, 4), kappa, n)}
+            if kappa != INF:
+                cell["histogram"] = {str(k): v for k, v in cm.coarse_counter_histogram(kappa, n).items()}
+            out["cells"].append(cell)
+    for kappa in (1, 2, 3, 7, INF):
+        for c in (0.2, 0.25, 0.3, 0.45, 0.5):
+            try:
+                v = cm.f_factor(kappa, c)
+            except ValueError:
+                v = None
+            out["f_factor"].append({"kappa": kname(kappa), "c": c, "value": v})
+    spec = cm.OpCountSpec(C=1.3, Ctilde=2.7, N1=1.0)
+    for kappa in (1, 2, 3, 5, INF):
+        for c in (0.2, 0.25, 0.3):
+            for n in (1, 3, 7, 12):
+                out["n_ops"].append({"kappa": kname(kappa), "c": c, "n": n, "value": cm.n_ops_model(kappa, c, n, spec)})
+    for kappa in (1, 2, 3, 4, INF):
+        tp = cm.turning_point(cm.CostModelParams(2.48e-3, 1.18e-6, 4), kappa)
+        out["turning_points"].append({"kappa": kname(kappa), "n_tp": tp.n_tp, "N_tp": tp.N_tp, "converged": tp.converged})
+    rows = [(k, n, 0.01 * cm.n_gpu_calls(k, n, 4) + 3e-7 * (2 ** n - 1) ** 2 * cm.ops_per_unknown(k) * (1 + 0.01 * ((n * 7 + int(k if k != INF else 9)) % 5 - 2)))
+            for k in (1, 2, 3, 4, INF) for n in range(4, 14)]
+    a, b = cm.fit_params(rows, nu=4)
+    out["fit"] = {"rows": [[kname(k), n, t] for k, n, t in rows], "alpha": a, "beta": b}
+    dump("costmodel.json", out)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["small", "solve", "pcg"])
+    ap.add_argument("what", choices=["small", "solve", "pcg", "costmodel"])
     ap.add_argument("--n", type=int, default=12)
     ap.add_argument("--kappa", default="1")
     ap.add_argument("--cap", type=int, default=20000)
     a = ap.parse_args()
     print("reference kcycle", kcycle.__version__, "numpy", np.__version__, flush=True)
+    if a.what == "costmodel":
+        gen_costmodel()
+        return
     if a.what == "small":
         gen_stencils()
         gen_kernels()

@@ -1,0 +1,118 @@
+"""Config C5: refit the paper's run-time model T = alpha*N_launch + beta*N_ops
+ to B200 measurements over the paper's grid
+kappa in {1,2,3,4,inf} x n in 4..13, and fit a per-level cost
+model from CUDA-event timings of every scheduled op.
+
+  python tools/refit_cost_model.py [--reps 50] [--out profiles/r01_costmodel_fit.json]
+
+Writes the reference `kcycle bench` CSV schema (cli.py:291-321:
+kappa,levels,mean_ms,launches,op_units) plus the engine's own launch count,
+the two fits (reference launch accounting n_gpu_calls; the engine's kernels
+per captured cycle graph), per-cell relative prediction errors (cf. paper
+Table 2) and the turning points (cf. Table 1).
+"""
+
+import argparse
+import json
+import math
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+
+import paper_2010_00626_b200 as kc  # noqa: E402
+from paper_2010_00626_b200 import costmodel as cm  # noqa: E402
+
+KAPPAS = (1, 2, 3, 4, math.inf)
+
+
+def kname(k):
+    return "inf" if k == math.inf else str(k)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=50)
+    ap.add_argument("--nmin", type=int, default=4)
+    ap.add_argument("--nmax", type=int, default=13)
+    ap.add_argument("--out", default="profiles/r01_costmodel_fit.json")
+    a = ap.parse_args()
+    nu = 4
+    problem = kc.ProblemSpec(1e-4, 45.0, seed=0)
+    rows, per_level = [], {}
+    print("kappa,levels,mean_ms,launches,op_units,engine_launches")
+    for n in range(a.nmin, a.nmax + 1):
+        st = kc.build_state(problem, kc.CycleConfig(n=n, kappa=1))
+        m = 2 ** n - 1
+        st.v[0] = np.random.default_rng(0).random((m, m))
+        for k in KAPPAS:
+            ke = n if k == math.inf else k
+            st.run_cycles(ke, 3)  # warm-up, graph capture
+            ms = st.time_cycles(ke, a.reps) / a.reps
+            launches = cm.n_gpu_calls(k, n, nu)
+            ops = (2 ** n - 1) ** 2 * cm.ops_per_unknown(k)
+            eng = st.launches_per_cycle(ke)
+            rows.append({"kappa": kname(k), "levels": n, "mean_ms": ms, "launches": launches,
+                         "op_units": ops, "engine_launches": eng})
+            print(f"{kname(k)},{n},{ms:.6g},{launches},{ops:.6g},{eng}", flush=True)
+            if n == a.nmax:  # per-level costs of one eager cycle, largest size
+                prof = st.profile_cycle(ke)
+                for p in prof:
+                    key = (p["level"], p["op"])
+                    per_level.setdefault(key, []).append(p["ms"])
+        st.close()
+
+    def kv(s):
+        return math.inf if s == "inf" else int(s)
+
+    obs = [(kv(r["kappa"]), r["levels"], r["mean_ms"]) for r in rows]
+    alpha, beta = cm.fit_params(obs, nu=nu)
+    params = cm.CostModelParams(alpha=max(alpha, 0.0), beta=max(beta, 0.0), nu=nu)
+    # the engine's own cost structure: graph kernels, routine calls executed
+    # inside the persistent bottom kernel (sides <= 63), and op units
+    for r in rows:
+        k, n = kv(r["kappa"]), r["levels"]
+        r["bottom_calls"] = sum(cm.level_calls(k, l) for l in range(1, n + 1) if 2 ** (n - l + 1) - 1 <= 63)
+    A = np.array([[r["engine_launches"], r["bottom_calls"], r["op_units"]] for r in rows], float)
+    y = np.array([r["mean_ms"] for r in rows], float)
+    (alpha_e, gamma_e, beta_e), *_ = np.linalg.lstsq(A, y, rcond=None)
+    for r in rows:
+        k, n = kv(r["kappa"]), r["levels"]
+        r["predicted_ms"] = cm.predict_runtime(params, k, n)
+        r["rel_error"] = (r["predicted_ms"] - r["mean_ms"]) / r["mean_ms"]
+        r["predicted_ms_engine"] = alpha_e * r["engine_launches"] + gamma_e * r["bottom_calls"] + beta_e * r["op_units"]
+        r["rel_error_engine"] = (r["predicted_ms_engine"] - r["mean_ms"]) / r["mean_ms"]
+    tps = {}
+    for k in KAPPAS:
+        try:
+            tp = cm.turning_point(params, k)
+            tps[kname(k)] = {"n_tp": tp.n_tp, "N_tp": tp.N_tp, "converged": tp.converged, "degenerate": tp.degenerate}
+        except ValueError as exc:
+            tps[kname(k)] = {"error": str(exc)}
+    levels = {}
+    for (lev, op), ts in per_level.items():
+        levels.setdefault(str(lev), {})[op] = {"calls": len(ts), "mean_us": 1e3 * float(np.mean(ts))}
+    out = {
+        "grid": "kappa in {1,2,3,4,inf} x n in %d..%d, nu=(2,2), eps=1e-4 phi=45, %d back-to-back cycles per cell"
+                % (a.nmin, a.nmax, a.reps),
+        "fit_reference_accounting": {"alpha_ms_per_launch": alpha, "beta_ms_per_op_unit": beta,
+                                     "max_abs_rel_error": max(abs(r["rel_error"]) for r in rows)},
+        "fit_engine_accounting": {"model": "T = a*graph_kernels + g*bottom_routine_calls + b*op_units",
+                                  "a_ms_per_kernel": float(alpha_e), "g_ms_per_bottom_call": float(gamma_e),
+                                  "b_ms_per_op_unit": float(beta_e),
+                                  "max_abs_rel_error": max(abs(r["rel_error_engine"]) for r in rows)},
+        "paper_gtx1060": {"alpha": 2.48e-3, "beta": 1.18e-6},
+        "turning_points": tps,
+        "cells": rows,
+        "per_level_eager_us_at_nmax": levels,
+    }
+    os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
+    with open(a.out, "w") as fh:
+        json.dump(out, fh, indent=1)
+    print(json.dumps({k: out[k] for k in ("fit_reference_accounting", "fit_engine_accounting", "turning_points")}))
+
+
+if __name__ == "__main__":
+    main()
