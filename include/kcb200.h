@@ -157,6 +157,30 @@ int kc_restore(kc_handle* h);
 /* v[level] (which = KC_WHICH_V) or f[level] = 0 on the device */
 int kc_fill_zero(kc_handle* h, int level, int which);
 
+/* ---------------------------------------------------------------------
+ * Row-strip kernels for the multi-GPU decomposition.
+ * Device pointers address the strip's interior origin (local row 0,
+ * column 0); rows -2..-1 and ny..ny+1 are halo / zero ghost rows owned by
+ * the caller; `stream` is a cudaStream_t (NULL = legacy stream).  Each call
+ * is one reference operation on the strip, bit-identical to the
+ * single-domain kernels.  w9 is the level stencil (host array of 9).
+ * --------------------------------------------------------------------- */
+int kc_strip_jacobi(const double* u, const double* f, double* out, int ny, int nx, int pitch, const double* w9,
+                    double omega, int zero_u, void* stream);                        /* smoother.py:95-100 */
+int kc_strip_resid_restrict(const double* u, const double* f, double* fc, int ncy, int ncx, int pitch,
+                            int pitch_c, const double* w9, int zero_u, void* stream);  /* cycle.py:165-168 */
+int kc_strip_prolong_add(double* v, const double* vc, int ny, int nx, int pitch, int pitch_c, int v_zero,
+                         void* stream);                                                /* cycle.py:174-176 */
+/* out (device, 2 doubles) = { sum v^2, sum (f - A v)^2 } over the strip's own rows */
+int kc_strip_norms(const double* v, const double* f, int ny, int nx, int pitch, const double* w9, double* out,
+                   void* stream);
+
+/* level data from / to device memory with an explicit row pitch (doubles):
+ * agglomeration of distributed levels onto the native engine */
+int kc_set_device(kc_handle* h, int level, int which, const double* dev, long long ny, long long nx,
+                  long long pitch);
+int kc_get_device(kc_handle* h, int level, int which, double* dev, long long ny, long long nx, long long pitch);
+
 #ifdef __cplusplus
 }
 #endif

@@ -79,6 +79,15 @@ _SIGS = {
     "kc_fill_zero": (C.c_int, [_h, C.c_int, C.c_int]),
     "kc_snapshot": (C.c_int, [_h]),
     "kc_set_option": (C.c_int, [_h, C.c_char_p, C.c_int]),
+    "kc_strip_jacobi": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, _dp, C.c_double,
+                                  C.c_int, C.c_void_p]),
+    "kc_strip_resid_restrict": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                          _dp, C.c_int, C.c_void_p]),
+    "kc_strip_prolong_add": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.c_void_p]),
+    "kc_strip_norms": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, _dp, C.c_void_p, C.c_void_p]),
+    "kc_set_device": (C.c_int, [_h, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_longlong, C.c_longlong]),
+    "kc_get_device": (C.c_int, [_h, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_longlong, C.c_longlong]),
     "kc_restore": (C.c_int, [_h]),
 }
 

@@ -27,6 +27,7 @@
 #include "kc_pcg.cuh"
 #include "kc_stream.cuh"
 #include "kc_tile.cuh"
+#include "kc_strip.cuh"
 
 namespace {
 
@@ -1408,5 +1409,97 @@ extern "C" int kc_pcg(kc_handle* h, int kappa, const double* f, const double* x0
   *iterations = it;
   *status = st;
   if (n_precond) *n_precond = napp;
+  return KC_OK;
+}
+
+// ===========================================================================
+// row-strip kernels (multi-GPU decomposition)
+// ===========================================================================
+namespace {
+St9 strip_stencil(const double* w9, double omega) {
+  St9 s{};
+  for (int k = 0; k < 9; ++k) s.w[k] = std::fabs(w9[k]) <= DBL_EPSILON ? 0.0 : w9[k];  // ndimage tap drop
+  s.center = w9[4];
+  s.c = omega / s.center;
+  return s;
+}
+int strip_err(cudaError_t e) {
+  if (e == cudaSuccess) return KC_OK;
+  g_create_err = cudaGetErrorString(e);
+  return KC_ECUDA;
+}
+}  // namespace
+
+extern "C" int kc_strip_jacobi(const double* u, const double* f, double* out, int ny, int nx, int pitch,
+                               const double* w9, double omega, int zero_u, void* stream) {
+  if (!f || !out || !w9 || ny < 0 || nx < 0) return KC_EINVAL;
+  if (w9[4] == 0.0) return KC_EINVAL;
+  if (ny == 0 || nx == 0) return KC_OK;
+  dim3 g((nx + KSTR_BX - 1) / KSTR_BX, (ny + KSTR_BY - 1) / KSTR_BY);
+  k_strip_jacobi<<<g, dim3(KSTR_BX, KSTR_BY), 0, (cudaStream_t)stream>>>(u, f, out, ny, nx, pitch,
+                                                                        strip_stencil(w9, omega), zero_u);
+  return strip_err(cudaGetLastError());
+}
+
+extern "C" int kc_strip_resid_restrict(const double* u, const double* f, double* fc, int ncy, int ncx, int pitch,
+                                       int pitch_c, const double* w9, int zero_u, void* stream) {
+  if (!f || !fc || !w9 || ncy < 0 || ncx < 0) return KC_EINVAL;
+  if (ncy == 0 || ncx == 0) return KC_OK;
+  dim3 g((ncx + KSTR_BX - 1) / KSTR_BX, (ncy + KSTR_BY - 1) / KSTR_BY);
+  k_strip_resid_restrict<<<g, dim3(KSTR_BX, KSTR_BY), 0, (cudaStream_t)stream>>>(
+      u, f, fc, ncy, ncx, pitch, pitch_c, strip_stencil(w9, 1.0), zero_u);
+  return strip_err(cudaGetLastError());
+}
+
+extern "C" int kc_strip_prolong_add(double* v, const double* vc, int ny, int nx, int pitch, int pitch_c,
+                                    int v_zero, void* stream) {
+  if (!v || !vc || ny < 0 || nx < 0) return KC_EINVAL;
+  if (ny == 0 || nx == 0) return KC_OK;
+  dim3 g((nx + KSTR_BX - 1) / KSTR_BX, (ny + KSTR_BY - 1) / KSTR_BY);
+  k_strip_prolong_add<<<g, dim3(KSTR_BX, KSTR_BY), 0, (cudaStream_t)stream>>>(v, vc, ny, nx, pitch, pitch_c, v_zero);
+  return strip_err(cudaGetLastError());
+}
+
+extern "C" int kc_strip_norms(const double* v, const double* f, int ny, int nx, int pitch, const double* w9,
+                              double* out, void* stream) {
+  if (!v || !f || !out || !w9) return KC_EINVAL;
+  static thread_local double* part = nullptr;  // per-thread scratch for the block partials
+  const int nb = 256;
+  if (!part) {
+    cudaError_t e = cudaMalloc(&part, sizeof(double) * 2 * nb);
+    if (e != cudaSuccess) return strip_err(e);
+  }
+  k_strip_norms<<<nb, 256, 0, (cudaStream_t)stream>>>(v, f, ny, nx, pitch, strip_stencil(w9, 1.0), part);
+  k_strip_norms_final<<<1, 32, 0, (cudaStream_t)stream>>>(part, nb, out);
+  return strip_err(cudaGetLastError());
+}
+
+extern "C" int kc_set_device(kc_handle* h, int level, int which, const double* dev, long long ny, long long nx,
+                             long long pitch) {
+  if (!h || !dev) return KC_EINVAL;
+  int rc = check_level(h, level);
+  if (rc) return rc;
+  Level& L = h->L[level - 1];
+  if (ny != L.m || nx != L.m) KC_FAIL(h, KC_EINVAL, "shape (%lld, %lld) != level %d shape (%d, %d)", ny, nx, level, L.m, L.m);
+  double* dst = which == KC_WHICH_F ? L.f : L.v[L.cur];
+  KC_CUDA(h, cudaMemcpy2DAsync(dst + kc_idx(L.P, 0, 0), sizeof(double) * L.P, dev, sizeof(double) * pitch,
+                               sizeof(double) * L.m, L.m, cudaMemcpyDeviceToDevice, h->stream));
+  KC_CUDA(h, cudaStreamSynchronize(h->stream));
+  if (which != KC_WHICH_F) L.vzero = false;
+  return KC_OK;
+}
+
+extern "C" int kc_get_device(kc_handle* h, int level, int which, double* dev, long long ny, long long nx,
+                             long long pitch) {
+  if (!h || !dev) return KC_EINVAL;
+  int rc = check_level(h, level);
+  if (rc) return rc;
+  Level& L = h->L[level - 1];
+  if (ny != L.m || nx != L.m) KC_FAIL(h, KC_EINVAL, "shape (%lld, %lld) != level %d shape (%d, %d)", ny, nx, level, L.m, L.m);
+  if (which != KC_WHICH_F && (rc = ex_materialize(h, level - 1))) return rc;
+  const double* src = which == KC_WHICH_F ? L.f : L.v[L.cur];
+  KC_CUDA(h, cudaMemcpy2DAsync(dev, sizeof(double) * pitch, src + kc_idx(L.P, 0, 0), sizeof(double) * L.P,
+                               sizeof(double) * L.m, L.m, cudaMemcpyDeviceToDevice, h->stream));
+  KC_CUDA(h, cudaStreamSynchronize(h->stream));
   return KC_OK;
 }

@@ -1,0 +1,197 @@
+"""Multi-rank kappa-cycles — host logic on the CPU.
+
+The distributed driver (paper_2010_00626_b200.distributed) runs here with the
+test-only numpy strip backend, first with in-process thread ranks, then as
+world_size-2 torch.distributed/gloo processes.  Bar: iterates bit-identical
+to the single-domain oracle (which is pinned to the reference), identical
+iteration counts.  The same driver with the CUDA strip kernels is covered by
+tests/test_gpu_parity.py (thread ranks on one B200).
+"""
+
+import math
+import os
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+from dist_numpy_backend import NumpyCoarse, NumpyStripOps
+from oracle import kcycle_oracle as O
+from paper_2010_00626_b200 import CycleConfig, ProblemSpec
+from paper_2010_00626_b200.distributed import DistributedKappaSolver, ThreadComm, plan_partition
+
+
+def test_plan_partition_properties():
+    for n in (5, 7, 9, 12, 14):
+        for world in (2, 3, 4, 8):
+            plan = plan_partition(n, world, min_rows=16)
+            if plan.n_dist == 0:
+                continue
+            for l in range(1, plan.n_dist + 1):
+                m = plan.side(l)
+                rows = plan.rows[l - 1]
+                assert rows[0][0] == 0 and rows[-1][1] == m
+                for r in range(world):
+                    a, b = rows[r]
+                    assert a % 2 == 0 and a <= b
+                    if r + 1 < world:
+                        assert rows[r + 1][0] == b
+                if l > 1:  # nesting: fine strip = 2 x coarse strip
+                    for (a, b), (ac, bc) in zip(plan.rows[l - 1], plan.rows[l - 2]):
+                        assert ac == 2 * a
+            assert plan.side(plan.n_dist) >= 2 * world + 1
+
+
+def _run_threads(world, fn):
+    comms = ThreadComm.group(world)
+    out = [None] * world
+    err = []
+
+    def body(r):
+        try:
+            out[r] = fn(comms[r])
+        except BaseException as exc:  # pragma: no cover - surfaced below
+            err.append(exc)
+            raise
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if err:
+        raise err[0]
+    return out
+
+
+def _solver(comm, n, kappa, eps, phi, nu1=2, nu2=2, min_rows=8):
+    problem = ProblemSpec(eps, phi, seed=0)
+    cfg = CycleConfig(n=n, kappa=kappa, nu1=nu1, nu2=nu2)
+    ws = O.hierarchy(eps, phi, n)
+
+    def make_coarse(levels, wsub):
+        return NumpyCoarse(ws[n - levels:], 0.8, nu1, nu2)
+
+    return DistributedKappaSolver(problem, cfg, comm, ops=NumpyStripOps(), make_coarse=make_coarse,
+                                  min_rows=min_rows)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("kappa", [1, 2, 3])
+def test_thread_ranks_bit_exact_vs_single_domain(world, kappa):
+    n, eps, phi = 7, 1e-3, 30.0
+    m = 2 ** n - 1
+    rng = np.random.default_rng(world * 10 + kappa)
+    v0, f0 = rng.random((m, m)), rng.standard_normal((m, m))
+    h = O.Hierarchy(O.hierarchy(eps, phi, n))
+    h.v[0], h.f[0] = v0.copy(), f0.copy()
+    ref = []
+    for _ in range(2):
+        h.cycle(kappa)
+        ref.append(h.v[0].copy())
+
+    def fn(comm):
+        s = _solver(comm, n, kappa, eps, phi)
+        assert s.plan.n_dist >= 2  # several distributed levels + agglomeration
+        s.set_level1("v", v0)
+        s.set_level1("f", f0)
+        got = []
+        for _ in range(2):
+            s.cycle()
+            got.append(s.gather_level1())
+        return got
+
+    for got in _run_threads(world, fn):
+        for c in range(2):
+            assert np.array_equal(got[c], ref[c]), (world, kappa, c)
+
+
+@pytest.mark.parametrize("nu1,nu2", [(1, 1), (2, 0), (0, 2), (3, 1)])
+def test_thread_ranks_nu_variants(nu1, nu2):
+    n, eps, phi, world, kappa = 6, 1e-4, 45.0, 2, 2
+    m = 2 ** n - 1
+    rng = np.random.default_rng(nu1 * 7 + nu2)
+    v0, f0 = rng.random((m, m)), rng.random((m, m))
+    h = O.Hierarchy(O.hierarchy(eps, phi, n), nu1=nu1, nu2=nu2)
+    h.v[0], h.f[0] = v0.copy(), f0.copy()
+    h.cycle(kappa)
+
+    def fn(comm):
+        s = _solver(comm, n, kappa, eps, phi, nu1, nu2, min_rows=4)
+        s.set_level1("v", v0)
+        s.set_level1("f", f0)
+        s.cycle()
+        return s.gather_level1()
+
+    for got in _run_threads(world, fn):
+        assert np.array_equal(got, h.v[0])
+
+
+def test_thread_ranks_solve_counts():
+    n, eps, phi, kappa = 6, 1e-4, 45.0, 2
+    ref = O.standalone(eps, phi, n, kappa, target=1e8, stop="residual")
+
+    def fn(comm):
+        s = _solver(comm, n, kappa, eps, phi, min_rows=4)
+        return s.solve_standalone(1e8, max_cycles=500, stop="residual")
+
+    for rep in _run_threads(3, fn):
+        assert rep["status"] == ref["status"]
+        assert rep["iterations"] == ref["iterations"]
+        rr = np.asarray(ref["res_hist"])
+        assert np.max(np.abs(np.asarray(rep["res_hist"]) - rr) / rr) < 1e-12
+        assert rep["stats"].visits == [O.level_calls(kappa, n)[l] * rep["iterations"] for l in range(n)]
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2010_00626_b200.distributed import TorchComm
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, kappa = 6, 3
+        m = 2 ** n - 1
+        rng = np.random.default_rng(5)
+        v0, f0 = rng.random((m, m)), rng.standard_normal((m, m))
+        s = _solver(TorchComm(), n, kappa, 0.1, 45.0, min_rows=4)
+        s.set_level1("v", v0)
+        s.set_level1("f", f0)
+        s.cycle()
+        got = s.gather_level1()
+        e, r = s.norms()
+        q.put((rank, got, e, r))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_bit_exact():
+    import socket
+
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n, kappa = 6, 3
+    m = 2 ** n - 1
+    rng = np.random.default_rng(5)
+    v0, f0 = rng.random((m, m)), rng.standard_normal((m, m))
+    h = O.Hierarchy(O.hierarchy(0.1, 45.0, n))
+    h.v[0], h.f[0] = v0.copy(), f0.copy()
+    h.cycle(kappa)
+    e_ref = O.norm2(h.v[0])
+    r_ref = O.norm2(O.residual(h.ws[0], h.v[0], h.f[0]))
+    for rank, got, e, r in res:
+        assert np.array_equal(got, h.v[0]), rank
+        assert e == pytest.approx(e_ref, rel=1e-13) and r == pytest.approx(r_ref, rel=1e-13)

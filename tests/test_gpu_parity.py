@@ -507,3 +507,53 @@ def test_n12_pcg_vs_reference(kname):
         ref_h = np.asarray(g[hist_key][: len(hist)])
         assert np.max(np.abs(hist - ref_h)) / ref_h[0] < 1e-10
     state.close()
+
+
+# ---------------------------------------------------------------------------
+# multi-rank decomposition with the CUDA strip kernels (thread ranks on one GPU)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("kappa", [1, 3])
+def test_distributed_cuda_strips_bit_exact(world, kappa):
+    import threading
+
+    from paper_2010_00626_b200.distributed import DistributedKappaSolver, ThreadComm
+    n, eps, phi = 9, 1e-4, 45.0
+    m = 2 ** n - 1
+    rng = np.random.default_rng(world + 10 * kappa)
+    v0, f0 = rng.random((m, m)), rng.standard_normal((m, m))
+    h = O.Hierarchy(O.hierarchy(eps, phi, n))
+    h.v[0], h.f[0] = v0.copy(), f0.copy()
+    ref = []
+    for _ in range(2):
+        h.cycle(kappa)
+        ref.append(h.v[0].copy())
+    comms = ThreadComm.group(world)
+    out, err = [None] * world, []
+
+    def body(r):
+        try:
+            s = DistributedKappaSolver(ProblemSpec(eps, phi), CycleConfig(n=n, kappa=kappa), comms[r], min_rows=32)
+            assert s.plan.n_dist >= 2
+            s.set_level1("v", v0)
+            s.set_level1("f", f0)
+            got = []
+            for _ in range(2):
+                s.cycle()
+                got.append(s.gather_level1())
+            out[r] = (got, s.norms())
+        except BaseException as exc:
+            err.append(exc)
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not err, err
+    e_ref = O.norm2(ref[1])
+    for got, (e, r) in out:
+        for c in range(2):
+            assert np.array_equal(got[c], ref[c]), c
+        assert e == pytest.approx(e_ref, rel=1e-13)
