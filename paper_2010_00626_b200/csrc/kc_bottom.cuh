@@ -47,6 +47,7 @@ struct BotParams {
   const unsigned* sched;  // host-built phase list (bot_schedule), device memory
   int nsched;
   int final_cur;     // buffer holding the entry level's v after the schedule
+  int nu1, nu2;      // sweeps inside PH_TINY frames
 };
 
 // smem geometry of level d (entry side m0): side m_d = ((m0+1) >> d) - 1,
@@ -91,19 +92,35 @@ __device__ long long kc_bot_trace_end[KC_BOT_TRACE];
 //   PH_PJ   prolong-correct + first post sweep, each point forming the
 //           corrected v at its 3x3 neighbours (small levels).
 // Same per-point arithmetic, so results stay bit-identical.
+//   PH_TINY a whole kappa_cycle frame on a level of side <= 7 (with its
+//           children) executed by warp 0 with the fused phases and no
+//           interpreter overhead between them (bot_tiny below).
 enum BotOp {
-  PH_JACOBI = 0, PH_RESID = 1, PH_RESTRICT = 2, PH_PROLONG = 3, PH_JOIN = 4, PH_J2Z = 5, PH_RR = 6, PH_PJ = 7
+  PH_JACOBI = 0, PH_RESID = 1, PH_RESTRICT = 2, PH_PROLONG = 3, PH_JOIN = 4, PH_J2Z = 5, PH_RR = 6, PH_PJ = 7,
+  PH_TINY = 8
 };
+#define KC_BOT_TINY_M 7  // frames on sides <= this run as PH_TINY
 #define KC_BOT_FUSE_M 15  // PH_RR / PH_PJ on sides <= this (latency-bound levels)
-__host__ __device__ __forceinline__ unsigned bot_desc(int op, int d, int src, int zero, int cbuf, int cc, int g) {
+// Descriptor: bits 0-3 op, 4-6 level d, 7 src buffer, 8 zero guess, 9 child
+// buffer (prolong), 10 child is the 1x1 coarsest (restrict), 11-12 warp
+// group code, 13-16 cycle counter (PH_TINY).
+__host__ __device__ __forceinline__ unsigned bot_desc(int op, int d, int src, int zero, int cbuf, int cc, int g,
+                                                      int kap = 0) {
   const unsigned gc = g >= KC_BOT_WARPS ? 3u : (g >= 8 ? 2u : (g >= 2 ? 1u : 0u));
-  return (unsigned)op | ((unsigned)d << 3) | ((unsigned)src << 6) | ((unsigned)zero << 7) | ((unsigned)cbuf << 8) |
-         ((unsigned)cc << 9) | (gc << 10);
+  return (unsigned)op | ((unsigned)d << 4) | ((unsigned)src << 7) | ((unsigned)zero << 8) | ((unsigned)cbuf << 9) |
+         ((unsigned)cc << 10) | (gc << 11) | ((unsigned)(kap > 15 ? 15 : kap) << 13);
 }
 __device__ __forceinline__ int bot_desc_g(unsigned e) {
-  const unsigned gc = (e >> 10) & 3u;
+  const unsigned gc = (e >> 11) & 3u;
   return gc == 3u ? KC_BOT_WARPS : (gc == 2u ? 8 : (gc == 1u ? 2 : 1));
 }
+#define BD_OP(e) ((int)((e) & 15u))
+#define BD_D(e) ((int)(((e) >> 4) & 7u))
+#define BD_SRC(e) ((int)(((e) >> 7) & 1u))
+#define BD_ZERO(e) ((int)(((e) >> 8) & 1u))
+#define BD_CBUF(e) ((int)(((e) >> 9) & 1u))
+#define BD_CC(e) ((int)(((e) >> 10) & 1u))
+#define BD_KAP(e) ((int)(((e) >> 13) & 15u))
 
 #include <vector>
 // Flatten kappa_cycle over the smem-resident levels (cycle.py:204-220) into
@@ -113,15 +130,18 @@ struct BotBuilder {  // host side
   int m0, nlev, nu1, nu2;
   unsigned cur = 0, vz = 0;
   int gprev = KC_BOT_WARPS;
+  bool fuse = true;         // emit PH_J2Z
+  bool fuse_small = false;  // emit PH_RR / PH_PJ (measured slower: larger kernel, longer chains)
+  bool tiny = true;         // whole frames on sides <= KC_BOT_TINY_M as PH_TINY
+  bool dry = false;         // track buffers only (inside a PH_TINY frame)
   std::vector<unsigned> out;
-  void emit(int op, int d, int src, int zero, int cbuf, int cc) {
+  void emit(int op, int d, int src, int zero, int cbuf, int cc, int kap = 0) {
+    if (dry) return;
     const int g = bot_warps(bot_m(m0, d));
     if (g > gprev) out.push_back(bot_desc(PH_JOIN, 0, 0, 0, 0, 0, g));
     gprev = g;
-    out.push_back(bot_desc(op, d, src, zero, cbuf, cc, g));
+    out.push_back(bot_desc(op, d, src, zero, cbuf, cc, g, kap));
   }
-  bool fuse = true;         // emit PH_J2Z
-  bool fuse_small = false;  // emit PH_RR / PH_PJ (measured slower: larger kernel, longer chains)
   void relax(int d, int count) {
     int i = 0;
     if (fuse && count >= 2 && ((vz >> d) & 1u)) {  // two sweeps from the zero guess: result in buffer cur
@@ -136,11 +156,20 @@ struct BotBuilder {  // host side
     }
   }
   void rec(int d, int kap) {
+    if (tiny && fuse && !dry && bot_m(m0, d) <= KC_BOT_TINY_M && d < nlev - 1 && kap <= 15) {
+      // one descriptor; bot_tiny follows the rules below (J2Z on), so
+      // replay them dry to track the buffers of level d
+      emit(PH_TINY, d, (cur >> d) & 1u, (vz >> d) & 1u, 0, 0, kap);
+      dry = true;
+      rec(d, kap);
+      dry = false;
+      return;
+    }
     relax(d, nu1);
     const int c = (cur >> d) & 1u;
     const int z = (vz >> d) & 1u;
     const int cc = (d + 1 == nlev - 1);
-    const bool small = fuse && fuse_small && bot_m(m0, d) <= KC_BOT_FUSE_M;
+    const bool small = fuse && fuse_small && bot_m(m0, d) <= KC_BOT_FUSE_M;  // RR / PJ
     if (small && !z) {
       emit(PH_RR, d, c, 0, 0, cc);
     } else {
@@ -214,6 +243,130 @@ struct BotLv {
   float inv, invc, invn, padf;  // 1/m, 1/m_child, 1/(m_child+1)
 };
 
+// u2 = J(J(0)) into u, with u1 = 0 + c f recomputed at the neighbours (PH_J2Z)
+__device__ __forceinline__ void bot_j2z(double* __restrict__ u, const double* __restrict__ f, const BotLv& L,
+                                        const St9& st, int tid, int nth) {
+  const int m = L.m, S = L.S;
+  for (int i = tid; i < L.nitem1; i += nth) {
+    const int y = bot_div(i, L.inv), x = i - y * m;
+    const double* pf = f + y * S + x;
+    double n1[9];
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) n1[dy * 3 + dx] = kc_jacobi_zero(pf[(dy - 1) * S + (dx - 1)], st.c);
+    const double au = kc_sum9(st, n1[0], n1[1], n1[2], n1[3], n1[4], n1[5], n1[6], n1[7], n1[8]);
+    u[y * S + x] = kc_jacobi_pt(n1[4], pf[0], au, st.c);
+  }
+}
+
+// fc = FW(r) on level d+1; with cc the child is the 1x1 coarsest and its
+// solve f/center is folded in (coarsest_solve, cycle.py:182-190)
+__device__ __forceinline__ void bot_restrict(const double* __restrict__ r, const BotLv& L, const BotLv& C,
+                                             double* __restrict__ sm, double ccenter, bool cc, int tid, int nth) {
+  const int S = L.S, mc = C.m, SC = C.S;
+  double* fc = sm + C.fo;
+  double* vc = sm + C.vo0;  // buffer 0
+  for (int i = tid; i < C.nitem1; i += nth) {
+    const int q = bot_div(i, L.invc), p = i - q * mc;
+    const double* rc = r + (2 * q + 1) * S + (2 * p + 1);
+    const double* rs = rc - S;
+    const double* rn = rc + S;
+    const double fv = kc_fw(rs[-1], rs[0], rs[1], rc[-1], rc[0], rc[1], rn[-1], rn[0], rn[1]);
+    fc[q * SC + p] = fv;
+    if (cc) vc[0] = __ddiv_rn(fv, ccenter);
+  }
+}
+
+// u += P vc (zero: u = 0 + P vc), one coarse cell (2x2 fine points) per item
+__device__ __forceinline__ void bot_prolong(double* __restrict__ u, const double* __restrict__ vc, const BotLv& L,
+                                            const BotLv& C, bool zero, int tid, int nth) {
+  const int S = L.S, mc = C.m, SC = C.S;
+  const int nc = mc + 1;
+  for (int i = tid; i < nc * nc; i += nth) {
+    const int q = bot_div(i, L.invn), p = i - q * nc;
+    const double c00 = vc[(q - 1) * SC + p - 1], c01 = vc[(q - 1) * SC + p];
+    const double c10 = vc[q * SC + p - 1], c11 = vc[q * SC + p];
+    double* pv = u + 2 * q * S + 2 * p;
+    // (even, even): fine[0::2, 0::2] = 0.25 (((c00 + c01) + c10) + c11)   (transfer.py:57)
+    pv[0] = DADD(zero ? 0.0 : pv[0], DMUL(0.25, DADD(DADD(DADD(c00, c01), c10), c11)));
+    if (p < mc)  // (even, odd): fine[0::2, 1::2] = 0.5 (c01 + c11)   (transfer.py:56)
+      pv[1] = DADD(zero ? 0.0 : pv[1], DMUL(0.5, DADD(c01, c11)));
+    if (q < mc) {
+      pv[S] = DADD(zero ? 0.0 : pv[S], DMUL(0.5, DADD(c10, c11)));  // (odd, even), transfer.py:55
+      if (p < mc) pv[S + 1] = DADD(zero ? 0.0 : pv[S + 1], c11);     // (odd, odd), transfer.py:54
+    }
+  }
+}
+
+// PH_TINY: whole kappa_cycle frames on sides <= KC_BOT_TINY_M, run by warp 0
+// alone (one __syncwarp per phase, no descriptor decode).  Follows
+// BotBuilder::rec with J2Z on, so the host's dry replay of the same rules
+// knows the buffer each level ends in.
+struct BotTiny {
+  double* sm;
+  const BotLv* lv;
+  const St9* tab;
+  int nu1, nu2, lane;
+  __device__ __forceinline__ double* buf(const BotLv& L, int b) const { return sm + (b ? L.vo1 : L.vo0); }
+  __device__ __forceinline__ void relax(const BotLv& L, const St9& st, int count, int& cur, int& vz) const {
+    int i = 0;
+    const double* f = sm + L.fo;
+    if (count >= 2 && vz) {
+      bot_j2z(buf(L, cur), f, L, st, lane, 32);
+      __syncwarp();
+      vz = 0;
+      i = 2;
+    }
+    for (; i < count; ++i) {
+      bot_stencil<1>(true, vz, buf(L, cur), buf(L, cur ^ 1), f, L.m, L.S, L.inv, st, lane, 32, L.nitem1);
+      __syncwarp();
+      vz = 0;
+      cur ^= 1;
+    }
+  }
+  // pre-smooth + residual + restriction of level d into d+1
+  __device__ __forceinline__ void down(int d, const BotLv& L, const St9& st, int& cur, int& vz, bool cc) const {
+    relax(L, st, nu1, cur, vz);
+    const double* f = sm + L.fo;
+    if (!vz) {
+      bot_stencil<1>(false, false, buf(L, cur), buf(L, cur ^ 1), f, L.m, L.S, L.inv, st, lane, 32, L.nitem1);
+      __syncwarp();
+    }
+    bot_restrict(vz ? f : buf(L, cur ^ 1), L, lv[d + 1], sm, tab[d + 1].center, cc, lane, 32);
+    __syncwarp();
+  }
+  // prolongation of child buffer cb + post-smoothing
+  __device__ __forceinline__ void up(int d, const BotLv& L, const St9& st, int& cur, int& vz, int cb) const {
+    const BotLv C = lv[d + 1];
+    bot_prolong(buf(L, cur), buf(C, cb), L, C, vz, lane, 32);
+    __syncwarp();
+    vz = 0;
+    relax(L, st, nu2, cur, vz);
+  }
+  // a frame whose child is the coarsest (both coarsest calls folded)
+  __device__ __forceinline__ void leaf(int d, int& cur, int& vz) const {
+    const BotLv L = lv[d];
+    const St9 st = tab[d];
+    down(d, L, st, cur, vz, true);
+    up(d, L, st, cur, vz, 0);
+  }
+  __device__ void frame(int d, int kap, int nlev, int& cur, int& vz) const {
+    if (d + 2 == nlev) {
+      leaf(d, cur, vz);
+      return;
+    }
+    // side 7: children are side-3 leaves (kappa only sets how many)
+    const BotLv L = lv[d];
+    const St9 st = tab[d];
+    down(d, L, st, cur, vz, false);
+    int cc = 0, cz = 1;
+    leaf(d + 1, cc, cz);
+    if (kap > 1) leaf(d + 1, cc, cz);
+    up(d, L, st, cur, vz, cc);
+  }
+};
+
 __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp, int m0) {
   extern __shared__ double sm[];
   __shared__ St9 tab[KC_BOT_MAXLEV];
@@ -273,14 +426,14 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
     if (k + 1 < bp.nsched) e_next = sched[k + 1];
     const int g = bot_desc_g(e);
     if (warp >= g) continue;
-    const int op = e & 7u;
+    const int op = BD_OP(e);
     if (op == PH_JOIN) {
       bot_sync(g);
       continue;
     }
-    const int d = (e >> 3) & 7u;
-    const int src = (e >> 6) & 1u;
-    const bool zero = (e >> 7) & 1u;
+    const int d = BD_D(e);
+    const int src = BD_SRC(e);
+    const bool zero = BD_ZERO(e);
     const BotLv L = lv[d];
     const int m = L.m, S = L.S;
     const int nth = g * 32;
@@ -293,60 +446,22 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
       kc_bot_trace_n = ++tr_n;
     }
 #endif
-    if (op == PH_J2Z) {  // u2 = J(J(0)) with u1 = 0 + c f recomputed at the neighbours
-      const St9 st = tab[d];
-      for (int i = tid; i < L.nitem1; i += nth) {
-        const int y = bot_div(i, L.inv), x = i - y * m;
-        const double* pf = f + y * S + x;
-        double n1[9];
-#pragma unroll
-        for (int dy = 0; dy < 3; ++dy)
-#pragma unroll
-          for (int dx = 0; dx < 3; ++dx) n1[dy * 3 + dx] = kc_jacobi_zero(pf[(dy - 1) * S + (dx - 1)], st.c);
-        const double au = kc_sum9(st, n1[0], n1[1], n1[2], n1[3], n1[4], n1[5], n1[6], n1[7], n1[8]);
-        u[y * S + x] = kc_jacobi_pt(n1[4], pf[0], au, st.c);
-      }
+    if (op == PH_J2Z) {
+      bot_j2z(u, f, L, tab[d], tid, nth);
     } else if (op <= PH_RESID) {
       double* o = sm + (src ? L.vo0 : L.vo1);
       const St9 st = tab[d];
       if (m >= 31) bot_stencil<4>(op == PH_JACOBI, zero, u, o, f, m, S, L.inv, st, tid, nth, L.nitem4);
       else bot_stencil<1>(op == PH_JACOBI, zero, u, o, f, m, S, L.inv, st, tid, nth, L.nitem1);
-    } else if (op == PH_RESTRICT) {  // fc = FW(r); r in buffer src, or f itself on a zero guess
+    } else if (op == PH_RESTRICT) {  // r in buffer src, or f itself on a zero guess
+      bot_restrict(zero ? f : u, L, lv[d + 1], sm, tab[d + 1].center, BD_CC(e), tid, nth);
+    } else if (op == PH_PROLONG) {
       const BotLv C = lv[d + 1];
-      const int mc = C.m, SC = C.S;
-      double* fc = sm + C.fo;
-      double* vc = sm + C.vo0;  // buffer 0
-      const double* r = zero ? f : u;
-      const bool cc = (e >> 9) & 1u;
-      for (int i = tid; i < C.nitem1; i += nth) {
-        const int q = bot_div(i, L.invc), p = i - q * mc;
-        const double* rc = r + (2 * q + 1) * S + (2 * p + 1);
-        const double* rs = rc - S;
-        const double* rn = rc + S;
-        const double fv = kc_fw(rs[-1], rs[0], rs[1], rc[-1], rc[0], rc[1], rn[-1], rn[0], rn[1]);
-        fc[q * SC + p] = fv;
-        if (cc) vc[0] = __ddiv_rn(fv, tab[d + 1].center);  // coarsest_solve, cycle.py:182-190
-      }
-    } else {  // PH_PROLONG: v += P vc, one coarse cell (2x2 fine points) per item
-      const BotLv C = lv[d + 1];
-      const int mc = C.m, SC = C.S;
-      const int cbuf = (e >> 8) & 1u;
-      const double* vc = sm + (cbuf ? C.vo1 : C.vo0);
-      const int nc = mc + 1;
-      for (int i = tid; i < nc * nc; i += nth) {
-        const int q = bot_div(i, L.invn), p = i - q * nc;
-        const double c00 = vc[(q - 1) * SC + p - 1], c01 = vc[(q - 1) * SC + p];
-        const double c10 = vc[q * SC + p - 1], c11 = vc[q * SC + p];
-        double* pv = u + 2 * q * S + 2 * p;
-        // (even, even): fine[0::2, 0::2] = 0.25 (((c00 + c01) + c10) + c11)   (transfer.py:57)
-        pv[0] = DADD(zero ? 0.0 : pv[0], DMUL(0.25, DADD(DADD(DADD(c00, c01), c10), c11)));
-        if (p < mc)  // (even, odd): fine[0::2, 1::2] = 0.5 (c01 + c11)   (transfer.py:56)
-          pv[1] = DADD(zero ? 0.0 : pv[1], DMUL(0.5, DADD(c01, c11)));
-        if (q < mc) {
-          pv[S] = DADD(zero ? 0.0 : pv[S], DMUL(0.5, DADD(c10, c11)));  // (odd, even), transfer.py:55
-          if (p < mc) pv[S + 1] = DADD(zero ? 0.0 : pv[S + 1], c11);     // (odd, odd), transfer.py:54
-        }
-      }
+      bot_prolong(u, sm + (BD_CBUF(e) ? C.vo1 : C.vo0), L, C, zero, tid, nth);
+    } else {  // PH_TINY (warp 0)
+      const BotTiny t{sm, lv, tab, bp.nu1, bp.nu2, tid};
+      int cur = src, vz = zero;
+      t.frame(d, BD_KAP(e), nlev, cur, vz);
     }
     bot_sync(g);
   }

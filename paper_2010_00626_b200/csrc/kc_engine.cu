@@ -829,6 +829,8 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
     BotParams& bp = h->bot_base;
     memset(&bp, 0, sizeof(bp));
     bp.nlev = n - lb;
+    bp.nu1 = nu1;
+    bp.nu2 = nu2;
     for (int j = 0; j < bp.nlev; ++j) bp.st[j] = h->L[lb + j].st;
     h->bot_m0 = h->L[lb].m;
     h->bot_smem = sizeof(double) * (size_t)bot_smem_doubles(h->bot_m0, bp.nlev);

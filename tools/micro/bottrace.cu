@@ -23,10 +23,12 @@ int main(int argc, char** argv) {
     bp.st[d].w[4] = 1.0; bp.st[d].center = 1.0; bp.st[d].c = 0.8;
   }
   BotBuilder b; b.m0 = m0; b.nlev = nlev; b.nu1 = 2; b.nu2 = 2; b.vz = 1;
+  b.tiny = argc > 2 ? atoi(argv[2]) != 0 : true;
   b.rec(0, kappa); if (kappa > 1) b.rec(0, kappa - 1);
   unsigned* ds; cudaMalloc(&ds, b.out.size() * 4);
   cudaMemcpy(ds, b.out.data(), b.out.size() * 4, cudaMemcpyHostToDevice);
   bp.gv = gv; bp.gf = gf; bp.gP = P; bp.v_zero = 1; bp.sched = ds; bp.nsched = (int)b.out.size(); bp.final_cur = b.cur & 1;
+  bp.nu1 = 2; bp.nu2 = 2;
   size_t smem = sizeof(double) * bot_smem_doubles(m0, nlev);
   cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int zero = 0;
@@ -44,10 +46,10 @@ int main(int argc, char** argv) {
   std::vector<long long> t(n); std::vector<int> op(n);
   cudaMemcpyFromSymbol(t.data(), kc_bot_trace, n * 8);
   cudaMemcpyFromSymbol(op.data(), kc_bot_trace_op, n * 4);
-  double sum[4][8] = {}; int cnt[4][8] = {};
+  double sum[16][8] = {}; int cnt[16][8] = {};
   for (int i = 0; i + 1 < n; ++i) { int o = op[i] / 16, d = op[i] % 16; sum[o][d] += t[i + 1] - t[i]; cnt[o][d]++; }
-  const char* nm[4] = {"jacobi", "resid", "restrict", "prolong"};
-  for (int o = 0; o < 4; ++o) for (int d = 0; d < nlev; ++d) if (cnt[o][d])
+  const char* nm[9] = {"jacobi", "resid", "restrict", "prolong", "join", "j2z", "rr", "pj", "tiny"};
+  for (int o = 0; o < 9; ++o) for (int d = 0; d < nlev; ++d) if (cnt[o][d])
     printf("  %-9s level %d (m=%2d): %5d phases, %7.0f cycles avg, %9.0f total\n", nm[o], d, bot_m(m0, d), cnt[o][d], sum[o][d] / cnt[o][d], sum[o][d]);
   printf("phases traced: %d, total cycles %lld\n", n, n > 1 ? t[n - 1] - t[0] : 0);
   return 0;
