@@ -363,10 +363,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     assert all(r[1] == "converged" and r[0] == cycles for r in results), "non-deterministic solve"
     clocks = clk.summary()
 
-    # kernels launched per solve: cycle graph kernels + 4 reduction kernels per
-    # cycle (error norm, residual norm: partial + final each) + 4 initial
+    # kernels launched per solve by the device loop (kc_engine.cu
+    # get_solve_graph): every iteration runs the level-1 pre kernel with the
+    # input norms, k_norms_lanes and k_stop_check, then the remaining
+    # launches_per_cycle - 1 kernels of the cycle; the final iteration stops
+    # after the check (cycles + 1 iterations)
     launches_per_cycle = state.launches_per_cycle(kbest)
-    gpu_launches = args.steps * (cycles * (launches_per_cycle + 4) + 4)
+    gpu_launches = args.steps * (cycles * (launches_per_cycle + 2) + 3)
 
     # ---- roofline: level-1 Jacobi sweep, eager profile on the same stream ---
     state.restore()

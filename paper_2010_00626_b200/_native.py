@@ -19,7 +19,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkcb200.so")
+LIB_PATH = os.environ.get("KCB200_LIB") or os.path.join(_HERE, "libkcb200.so")  # override: experiments only
 
 KC_OK, KC_EINVAL, KC_ESINGULAR, KC_ECUDA, KC_ENOMEM = 0, 1, 2, 3, 4
 KC_COARSEN_FULL, KC_COARSEN_SEMI_Y = 0, 1

@@ -34,27 +34,31 @@ namespace {
 thread_local std::string g_create_err;
 
 // Device-resident stand-alone loop state (cycle.py:332-353), advanced by
-// k_stop_check at the end of every cycle inside a conditional WHILE graph.
+// k_stop_check inside the conditional WHILE graph of the stand-alone solve:
+// it runs after the level-0 pre kernel has produced the norms of the
+// current iterate v_it (cycle.py:338-353) and decides whether the rest of
+// the cycle (an IF node) and the next iteration run.
 struct SolveState {
-  double target, prev;
+  double target, prev, reduction;
   int it, max_it, streak, status, stop_mode, pad;
   double* err_hist;
   double* res_hist;
 };
 
-__global__ void k_stop_check(cudaGraphConditionalHandle hnd, SolveState* st, const double* __restrict__ scal) {
+__global__ void k_stop_check(cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_rest, SolveState* st,
+                             const double* __restrict__ scal) {
   if (threadIdx.x != 0) return;
-  const int it = st->it + 1;
-  st->it = it;
+  const int it = st->it;  // cycles completed
   const double e = scal[0], r = scal[1];
   st->err_hist[it] = e;
   st->res_hist[it] = r;
   const double cur = st->stop_mode == KC_STOP_ERROR ? e : r;
+  if (it == 0) st->target = cur / st->reduction;  // cycle.py:338-341
   unsigned go = 1u;
   if (cur <= st->target) {  // cycle.py:347
     st->status = KC_STATUS_CONVERGED;
     go = 0u;
-  } else {  // cycle.py:350-353: five consecutive growth steps
+  } else if (it > 0) {  // cycle.py:350-353: five consecutive growth steps
     const int streak = cur > st->prev ? st->streak + 1 : 0;
     st->streak = streak;
     if (streak >= 5) {
@@ -64,7 +68,9 @@ __global__ void k_stop_check(cudaGraphConditionalHandle hnd, SolveState* st, con
   }
   st->prev = cur;
   if (go && it >= st->max_it) go = 0u;  // status stays MAX_CYCLES
-  cudaGraphSetConditional(hnd, go);
+  if (go) st->it = it + 1;
+  cudaGraphSetConditional(h_loop, go);
+  cudaGraphSetConditional(h_rest, go);
 }
 
 struct Level {
@@ -90,9 +96,14 @@ struct GraphEntry {
   cudaGraph_t graph = nullptr;
   int end_cur0 = 0;
   int kernels = 0;
-  // whole stand-alone loop: WHILE(cycle; k_stop_check), built on demand
-  cudaGraphExec_t loop_exec = nullptr;
-  cudaGraph_t loop_graph = nullptr;
+};
+
+// the whole stand-alone loop in one graph:
+//   WHILE { pre (level 0, input norms) ; k_stop_check ; IF { rest of the cycle } }
+struct SolveGraph {
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr, pre = nullptr, rest = nullptr;
+  int end_cur0 = 0, kernels_pre = 0, kernels_rest = 0;
 };
 
 }  // namespace
@@ -113,7 +124,10 @@ struct kc_handle {
   double* d_scal = nullptr;     // device scalars
   double* h_scal = nullptr;     // pinned host mirror
   std::map<std::tuple<int, int, int, int>, GraphEntry> graphs;  // (kappa, cur0, vzero0, norms)
-  double* d_npart = nullptr;  // per-warp norm partials of the fused level-1 post kernel
+  std::map<std::pair<int, int>, SolveGraph> solve_graphs;       // (kappa, cur0)
+  double* d_npart = nullptr;  // norm partials of the fused level-1 kernels (per warp: post; per lane: pre)
+  double* d_nblk = nullptr;    // block sums of k_norms_lanes
+  unsigned* d_ncount = nullptr;
   int npart_cap = 0;
   bool fuse = true;           // use the fused streaming kernels in native cycles
   bool tile = true;           // overlapped-tile kernels on the mid-size levels
@@ -361,8 +375,8 @@ int ks_choose_nq(int mc, int nbands, int slots) {
 }
 
 typedef void (*KsFn)(StreamParams);
-KsFn ks_pre_fn(int nu, bool zero) {
-#define KS_PRE(N) return zero ? k_pre<N, true> : k_pre<N, false>
+KsFn ks_pre_fn(int nu, bool zero, bool norms = false) {
+#define KS_PRE(N) return zero ? k_pre<N, true> : (norms ? k_pre<N, false, true> : k_pre<N, false>)
   switch (nu) {
     case 0: KS_PRE(0);
     case 1: KS_PRE(1);
@@ -478,16 +492,28 @@ int ex_tile(kc_handle* h, int l, bool pre) {
   return KC_OK;
 }
 
-// relax(nu1) + restrict_residual (cycle.py:211-213) in one pass
-int ex_pre(kc_handle* h, int l) {
+// relax(nu1) + restrict_residual (cycle.py:211-213) in one pass; with norms
+// also ||v||, ||f - A v|| of the input v into d_scal[0], d_scal[1]
+int ex_pre(kc_handle* h, int l, bool norms = false) {
   Level& L = h->L[l];
-  if (L.m <= KC_TILE_MAX_M && h->tile) return ex_tile(h, l, true);
+  if (norms && L.vzero) KC_FAIL(h, KC_EINVAL, "fused input norms need a materialized level");
+  if (L.m <= KC_TILE_MAX_M && h->tile && !norms) return ex_tile(h, l, true);
   int nw = 0;
-  KsFn fn = ks_pre_fn(h->nu1, L.vzero);
+  KsFn fn = ks_pre_fn(h->nu1, L.vzero, norms);
   StreamParams p = ks_params(h, l, h->nu1 + 1, &nw, (const void*)fn);
+  if (norms) {
+    if (32 * nw > h->npart_cap) KC_FAIL(h, KC_EINVAL, "norm partial buffer too small (%d < %d)", h->npart_cap, 32 * nw);
+    p.part = h->d_npart;
+  }
   fn<<<(nw + 3) / 4, 128, KS_SMEM_BYTES, h->stream>>>(p);
   KC_LAUNCH_CHECK(h);
   ++h->launches;
+  if (norms) {
+    k_norms_lanes<<<KS_NB, 256, 0, h->stream>>>(reinterpret_cast<const double2*>(h->d_npart), nw * 32,
+                                                 reinterpret_cast<double2*>(h->d_nblk), h->d_ncount, h->d_scal);
+    KC_LAUNCH_CHECK(h);
+    ++h->launches;
+  }
   if (h->nu1 > 0) {
     L.cur ^= 1;
     L.vzero = false;
@@ -527,7 +553,7 @@ int ex_post(kc_handle* h, int l, bool norms) {
 
 int ex_op(kc_handle* h, const Op& op) {
   switch (op.kind) {
-    case OP_PRE: return ex_pre(h, op.level);
+    case OP_PRE: return ex_pre(h, op.level, op.b != 0);
     case OP_POST: return ex_post(h, op.level, op.b != 0);
     case OP_RELAX: return ex_relax(h, op.level, op.a);
     case OP_RESTRICT: return ex_restrict(h, op.level);
@@ -546,7 +572,9 @@ bool fusable(const kc_handle* h, int l) {
 // Flatten kappa_cycle(level, kappa) (cycle.py:204-220) into ops.  `norms`
 // asks the level-0 post-smoothing of this call to also produce ||v|| and
 // ||f - A v|| (the stand-alone stopping test) inside the cycle.
-void flatten(const kc_handle* h, int l, int kappa, std::vector<Op>& ops, bool norms = false) {
+// norms: 0 none, 1 after the cycle (fused into the level-0 post), 2 of the
+// cycle's input (fused into the level-0 pre; the device solve loop).
+void flatten(const kc_handle* h, int l, int kappa, std::vector<Op>& ops, int norms = 0) {
   const int n = h->n;
   if (l == h->Lb) {
     ops.push_back({OP_BOTTOM, l, kappa, 0});
@@ -558,7 +586,7 @@ void flatten(const kc_handle* h, int l, int kappa, std::vector<Op>& ops, bool no
   }
   const bool fu = fusable(h, l);
   if (fu) {
-    ops.push_back({OP_PRE, l, 0, 0});
+    ops.push_back({OP_PRE, l, 0, norms == 2 ? 1 : 0});
   } else {
     ops.push_back({OP_RELAX, l, h->nu1, 0});
     ops.push_back({OP_RESTRICT, l, 0, 0});
@@ -577,7 +605,7 @@ void flatten(const kc_handle* h, int l, int kappa, std::vector<Op>& ops, bool no
     }
   }
   if (fu) {
-    ops.push_back({OP_POST, l, 0, norms ? 1 : 0});
+    ops.push_back({OP_POST, l, 0, norms == 1 ? 1 : 0});
   } else {
     ops.push_back({OP_PROLONG, l, 0, 0});
     ops.push_back({OP_RELAX, l, h->nu2, 0});
@@ -597,7 +625,7 @@ int get_cycle_graph(kc_handle* h, int kappa, GraphEntry** out, bool norms = fals
     return KC_OK;
   }
   std::vector<Op> ops;
-  flatten(h, 0, kappa, ops, norms);
+  flatten(h, 0, kappa, ops, norms ? 1 : 0);
   // coarse levels start every cycle logically overwritten (zero_guess precedes use)
   std::vector<int> save_cur(h->n);
   std::vector<char> save_vz(h->n);
@@ -654,37 +682,115 @@ int run_cycle_graph(kc_handle* h, int kappa, bool norms = false) {
   return KC_OK;
 }
 
-// WHILE(cond) { cycle graph (child, norms fused); k_stop_check } — the whole
-// stand-alone loop in one graph launch, no host round trip per cycle.
-int get_loop_graph(kc_handle* h, GraphEntry* g) {
-  if (g->loop_exec) return KC_OK;
+void drop_graphs(kc_handle* h) {
+  for (auto& kv : h->graphs) {
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+  }
+  h->graphs.clear();
+  for (auto& kv : h->solve_graphs) {
+    SolveGraph& g = kv.second;
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+    if (g.pre) cudaGraphDestroy(g.pre);
+    if (g.rest) cudaGraphDestroy(g.rest);
+  }
+  h->solve_graphs.clear();
+}
+
+int capture_ops(kc_handle* h, const std::vector<Op>& ops, size_t i0, size_t i1, cudaGraph_t* out, int* kernels) {
+  const int l0 = h->launches;
+  KC_CUDA(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = KC_OK;
+  for (size_t i = i0; i < i1 && rc == KC_OK; ++i) rc = ex_op(h, ops[i]);
+  cudaGraph_t graph = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(h->stream, &graph);
+  *kernels = h->launches - l0;
+  h->launches = l0;
+  if (rc != KC_OK || ce != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    if (rc) return rc;
+    KC_FAIL(h, KC_ECUDA, "cudaStreamEndCapture: %s", cudaGetErrorString(ce));
+  }
+  *out = graph;
+  return KC_OK;
+}
+
+// Build (once per kappa and finest buffer) the stand-alone loop graph.  The
+// norms of iterate v_k come out of the level-0 pre kernel of cycle k+1
+// (its first stencil stage computes f - A v_k anyway); when the stop test
+// fires the remainder of that cycle is skipped and v_k, still in its buffer
+// (the pre kernel writes the other one), is the result.
+int get_solve_graph(kc_handle* h, int kappa, SolveGraph** out) {
+  Level& L0 = h->L[0];
+  const auto key = std::make_pair(kappa, L0.cur);
+  auto it = h->solve_graphs.find(key);
+  if (it != h->solve_graphs.end()) {
+    *out = &it->second;
+    return KC_OK;
+  }
+  std::vector<Op> ops;
+  flatten(h, 0, kappa, ops, 2);
+  if (ops.empty() || ops[0].kind != OP_PRE || ops[0].b != 1) KC_FAIL(h, KC_EINVAL, "no fused level-0 pre kernel");
+  for (const Op& op : ops)
+    if (op.kind == OP_BOTTOM) {
+      const unsigned* dv;
+      int nn, fc, rc0;
+      for (int vz = 0; vz < 2; ++vz)
+        if ((rc0 = get_bot_sched(h, op.a, op.b, vz, &dv, &nn, &fc))) return rc0;
+    }
+  std::vector<int> save_cur(h->n);
+  std::vector<char> save_vz(h->n);
+  for (int j = 0; j < h->n; ++j) {
+    save_cur[j] = h->L[j].cur;
+    save_vz[j] = h->L[j].vzero;
+  }
+  for (int j = 1; j < h->n; ++j) h->L[j].cur = 0;
+  SolveGraph sg;
+  int rc = capture_ops(h, ops, 0, 1, &sg.pre, &sg.kernels_pre);
+  if (rc == KC_OK) rc = capture_ops(h, ops, 1, ops.size(), &sg.rest, &sg.kernels_rest);
+  sg.end_cur0 = L0.cur;
+  for (int j = 0; j < h->n; ++j) {
+    h->L[j].cur = save_cur[j];
+    h->L[j].vzero = save_vz[j];
+  }
+  if (rc) return rc;
   if (!h->d_solve) KC_CUDA(h, cudaMalloc(&h->d_solve, sizeof(SolveState)));
   cudaGraph_t cg = nullptr;
   KC_CUDA(h, cudaGraphCreate(&cg, 0));
-  cudaGraphConditionalHandle hnd;
-  KC_CUDA(h, cudaGraphConditionalHandleCreate(&hnd, cg, 1, cudaGraphCondAssignDefault));
-  cudaGraphNodeParams np{};
-  np.type = cudaGraphNodeTypeConditional;
-  np.conditional.handle = hnd;
-  np.conditional.type = cudaGraphCondTypeWhile;
-  np.conditional.size = 1;
-  cudaGraphNode_t cn;
-  KC_CUDA(h, cudaGraphAddNode(&cn, cg, nullptr, 0, &np));
-  cudaGraph_t body = np.conditional.phGraph_out[0];
-  cudaGraphNode_t child;
-  KC_CUDA(h, cudaGraphAddChildGraphNode(&child, body, nullptr, 0, g->graph));
+  cudaGraphConditionalHandle h_loop, h_rest;
+  KC_CUDA(h, cudaGraphConditionalHandleCreate(&h_loop, cg, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams wp{};
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = h_loop;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  cudaGraphNode_t wn;
+  KC_CUDA(h, cudaGraphAddNode(&wn, cg, nullptr, 0, &wp));
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+  KC_CUDA(h, cudaGraphConditionalHandleCreate(&h_rest, body, 0, cudaGraphCondAssignDefault));
+  cudaGraphNode_t pre_node, chk_node, if_node, rest_node;
+  KC_CUDA(h, cudaGraphAddChildGraphNode(&pre_node, body, nullptr, 0, sg.pre));
   SolveState* st = h->d_solve;
   const double* scal = h->d_scal;
-  void* args[] = {&hnd, &st, &scal};
+  void* args[] = {&h_loop, &h_rest, &st, &scal};
   cudaKernelNodeParams kp{};
   kp.func = (void*)k_stop_check;
   kp.gridDim = dim3(1);
   kp.blockDim = dim3(32);
   kp.kernelParams = args;
-  cudaGraphNode_t kn;
-  KC_CUDA(h, cudaGraphAddKernelNode(&kn, body, &child, 1, &kp));
-  KC_CUDA(h, cudaGraphInstantiate(&g->loop_exec, cg, 0));
-  g->loop_graph = cg;
+  KC_CUDA(h, cudaGraphAddKernelNode(&chk_node, body, &pre_node, 1, &kp));
+  cudaGraphNodeParams ip{};
+  ip.type = cudaGraphNodeTypeConditional;
+  ip.conditional.handle = h_rest;
+  ip.conditional.type = cudaGraphCondTypeIf;
+  ip.conditional.size = 1;
+  KC_CUDA(h, cudaGraphAddNode(&if_node, body, &chk_node, 1, &ip));
+  KC_CUDA(h, cudaGraphAddChildGraphNode(&rest_node, ip.conditional.phGraph_out[0], nullptr, 0, sg.rest));
+  KC_CUDA(h, cudaGraphInstantiate(&sg.exec, cg, 0));
+  sg.graph = cg;
+  auto ins = h->solve_graphs.emplace(key, sg);
+  *out = &ins.first->second;
   return KC_OK;
 }
 
@@ -847,9 +953,14 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
     int nw2 = 0;
     ks_params(h, 0, D, &nw2, (const void*)ks_post_fn(nu2, false, true));
     nw = nw > nw2 ? nw : nw2;
+    ks_params(h, 0, nu1 + 1, &nw2, (const void*)ks_pre_fn(nu1, false, true));
+    nw = nw > 32 * nw2 ? nw : 32 * nw2;  // the pre kernel leaves per-lane partials
     (void)p;
     h->npart_cap = nw;
-    if (cudaMalloc(&h->d_npart, sizeof(double) * 2 * (size_t)nw) != cudaSuccess) {
+    if (cudaMalloc(&h->d_nblk, sizeof(double) * 2 * KS_NB) != cudaSuccess ||
+        cudaMalloc(&h->d_ncount, sizeof(unsigned)) != cudaSuccess ||
+        cudaMemset(h->d_ncount, 0, sizeof(unsigned)) != cudaSuccess ||
+        cudaMalloc(&h->d_npart, sizeof(double) * 2 * (size_t)nw) != cudaSuccess) {
       h->err = "cudaMalloc norm partials failed";
       return fail(KC_ENOMEM);
     }
@@ -861,12 +972,7 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
 int kc_destroy(kc_handle* h) {
   if (!h) return KC_OK;
   if (h->stream) cudaStreamSynchronize(h->stream);
-  for (auto& kv : h->graphs) {
-    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-    if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
-    if (kv.second.loop_exec) cudaGraphExecDestroy(kv.second.loop_exec);
-    if (kv.second.loop_graph) cudaGraphDestroy(kv.second.loop_graph);
-  }
+  drop_graphs(h);
   cudaFree(h->d_solve);
   cudaFree(h->d_hist);
   for (Level& L : h->L) {
@@ -880,6 +986,8 @@ int kc_destroy(kc_handle* h) {
   cudaFree(h->fb);
   cudaFree(h->snap);
   cudaFree(h->d_npart);
+  cudaFree(h->d_nblk);
+  cudaFree(h->d_ncount);
   for (auto& kv : h->bot_sched) cudaFree(std::get<0>(kv.second));
   cudaFree(h->d_part);
   cudaFree(h->d_scal);
@@ -1092,13 +1200,7 @@ int kc_set_option(kc_handle* h, const char* name, int value) {
     KC_CUDA(h, cudaStreamSynchronize(h->stream));
     if (name[0] == 'f') h->fuse = value != 0;
     else h->tile = value != 0;
-    for (auto& kv : h->graphs) {
-      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-      if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
-      if (kv.second.loop_exec) cudaGraphExecDestroy(kv.second.loop_exec);
-      if (kv.second.loop_graph) cudaGraphDestroy(kv.second.loop_graph);
-    }
-    h->graphs.clear();
+    drop_graphs(h);
     return KC_OK;
   }
   KC_FAIL(h, KC_EINVAL, "unknown option '%s'", name);
@@ -1166,41 +1268,28 @@ int kc_solve(kc_handle* h, int kappa, int stop_mode, double target_reduction, in
   if (kappa > h->n) kappa = h->n;
   int rc;
   if ((rc = ex_materialize(h, 0))) return rc;
-  // build the graph before timing (setup, like build_state)
+  // build the graphs before timing (setup, like build_state)
   const bool fused_norms = cycle_has_norms(h);
-  GraphEntry* g = nullptr;
-  if ((rc = get_cycle_graph(h, kappa, &g, fused_norms))) return rc;
   Level& L0 = h->L[0];
-  // the device loop needs a cycle graph that leaves the finest buffer where it
-  // found it (true whenever nu1 > 0 with the fused kernels)
-  const bool device_loop = fused_norms && g->end_cur0 == L0.cur && max_cycles > 0;
-  if (device_loop) {  // setup outside the timed span
-    if (max_cycles + 1 > h->hist_cap) {
-      cudaFree(h->d_hist);
-      h->d_hist = nullptr;
-      KC_CUDA(h, cudaMalloc(&h->d_hist, sizeof(double) * 2 * (size_t)(max_cycles + 1)));
-      h->hist_cap = max_cycles + 1;
-    }
-    if ((rc = get_loop_graph(h, g))) return rc;
+  SolveGraph* sg = nullptr;
+  if (fused_norms && max_cycles > 0 && (rc = get_solve_graph(h, kappa, &sg))) return rc;
+  // the device loop needs a cycle that leaves the finest buffer where it
+  // found it (always true with the fused kernels: pre and post flip once each)
+  const bool device_loop = sg && sg->end_cur0 == L0.cur;
+  GraphEntry* g = nullptr;
+  if (!device_loop && (rc = get_cycle_graph(h, kappa, &g, fused_norms))) return rc;
+  if (device_loop && max_cycles + 1 > h->hist_cap) {  // setup outside the timed span
+    cudaFree(h->d_hist);
+    h->d_hist = nullptr;
+    KC_CUDA(h, cudaMalloc(&h->d_hist, sizeof(double) * 2 * (size_t)(max_cycles + 1)));
+    h->hist_cap = max_cycles + 1;
   }
   KC_CUDA(h, cudaStreamSynchronize(h->stream));
   KC_CUDA(h, cudaEventRecord(h->ev0, h->stream));
-  if ((rc = red_dot(h, L0.v[L0.cur], L0.v[L0.cur], 0, 0, true))) return rc;
-  if ((rc = red_resnorm(h, L0.v[L0.cur], L0.f, 0, 1))) return rc;
-  if ((rc = fetch_scalars(h, 2))) return rc;
-  const double e0 = h->h_scal[0], r0 = h->h_scal[1];
-  if (err_hist) err_hist[0] = e0;
-  if (res_hist) res_hist[0] = r0;
-  const double m0 = stop_mode == KC_STOP_ERROR ? e0 : r0;
-  const double target = m0 / target_reduction;
   int st = KC_STATUS_MAX_CYCLES, it = 0, streak = 0;
-  double cur = m0;
-  if (m0 <= target) {
-    st = KC_STATUS_CONVERGED;
-  } else if (device_loop) {
+  if (device_loop) {
     SolveState ss{};
-    ss.target = target;
-    ss.prev = m0;
+    ss.reduction = target_reduction;
     ss.it = 0;
     ss.max_it = max_cycles;
     ss.streak = 0;
@@ -1209,21 +1298,34 @@ int kc_solve(kc_handle* h, int kappa, int stop_mode, double target_reduction, in
     ss.err_hist = h->d_hist;
     ss.res_hist = h->d_hist + h->hist_cap;
     KC_CUDA(h, cudaMemcpyAsync(h->d_solve, &ss, sizeof(ss), cudaMemcpyHostToDevice, h->stream));
-    KC_CUDA(h, cudaGraphLaunch(g->loop_exec, h->stream));
+    KC_CUDA(h, cudaGraphLaunch(sg->exec, h->stream));
     KC_CUDA(h, cudaMemcpyAsync(&ss, h->d_solve, sizeof(ss), cudaMemcpyDeviceToHost, h->stream));
     KC_CUDA(h, cudaStreamSynchronize(h->stream));
     it = ss.it;
     st = ss.status;
-    if (err_hist) KC_CUDA(h, cudaMemcpy(err_hist + 1, h->d_hist + 1, sizeof(double) * it, cudaMemcpyDeviceToHost));
+    if (err_hist) KC_CUDA(h, cudaMemcpy(err_hist, h->d_hist, sizeof(double) * (it + 1), cudaMemcpyDeviceToHost));
     if (res_hist)
-      KC_CUDA(h, cudaMemcpy(res_hist + 1, h->d_hist + h->hist_cap + 1, sizeof(double) * it, cudaMemcpyDeviceToHost));
-    // level-state bookkeeping after it cycles of the graph
+      KC_CUDA(h, cudaMemcpy(res_hist, h->d_hist + h->hist_cap, sizeof(double) * (it + 1), cudaMemcpyDeviceToHost));
+    // level-state bookkeeping after it cycles (the finest buffer is unchanged)
     L0.vzero = false;
     for (int j = 1; j < h->n; ++j) {
       h->L[j].vzero = true;
       h->L[j].cur = 0;
     }
   } else {
+    if ((rc = red_dot(h, L0.v[L0.cur], L0.v[L0.cur], 0, 0, true))) return rc;
+    if ((rc = red_resnorm(h, L0.v[L0.cur], L0.f, 0, 1))) return rc;
+    if ((rc = fetch_scalars(h, 2))) return rc;
+    const double e0 = h->h_scal[0], r0 = h->h_scal[1];
+    if (err_hist) err_hist[0] = e0;
+    if (res_hist) res_hist[0] = r0;
+    const double m0 = stop_mode == KC_STOP_ERROR ? e0 : r0;
+    const double target = m0 / target_reduction;
+    double cur = m0;
+    if (m0 <= target) {
+      st = KC_STATUS_CONVERGED;
+      max_cycles = 0;
+    }
     for (it = 1; it <= max_cycles; ++it) {
       if ((rc = run_cycle_graph(h, kappa, fused_norms))) return rc;
       if (!fused_norms) {

@@ -42,19 +42,41 @@ __device__ __forceinline__ double kc_shfl_dn1(double v) { return __shfl_down_syn
 
 // Jacobi (JAC) or residual at the lane's two columns from three rows
 // (r0 = south, r1 = centre, r2 = north), own values and shuffled edges.
+// rx, ry receive the residual f - A u at the two points (the Jacobi update is
+// u + c (f - A u) with that very difference, kc_jacobi_pt).
 template <bool JAC>
 __device__ __forceinline__ void ks_stencil2(const St9& s, double2 r0, double2 r1, double2 r2, double2 fv,
-                                            double& ox, double& oy) {
+                                            double& ox, double& oy, double& rx, double& ry) {
   const double l0 = kc_shfl_up1(r0.y), l1 = kc_shfl_up1(r1.y), l2 = kc_shfl_up1(r2.y);
   const double e0 = kc_shfl_dn1(r0.x), e1 = kc_shfl_dn1(r1.x), e2 = kc_shfl_dn1(r2.x);
   const double ax = kc_sum9(s, l0, r0.x, r0.y, l1, r1.x, r1.y, l2, r2.x, r2.y);
   const double ay = kc_sum9(s, r0.x, r0.y, e0, r1.x, r1.y, e1, r2.x, r2.y, e2);
+  rx = DSUB(fv.x, ax);
+  ry = DSUB(fv.y, ay);
   if (JAC) {
-    ox = kc_jacobi_pt(r1.x, fv.x, ax, s.c);
-    oy = kc_jacobi_pt(r1.y, fv.y, ay, s.c);
+    ox = DADD(r1.x, DMUL(s.c, rx));
+    oy = DADD(r1.y, DMUL(s.c, ry));
   } else {
-    ox = DSUB(fv.x, ax);
-    oy = DSUB(fv.y, ay);
+    ox = rx;
+    oy = ry;
+  }
+}
+template <bool JAC>
+__device__ __forceinline__ void ks_stencil2(const St9& s, double2 r0, double2 r1, double2 r2, double2 fv,
+                                            double& ox, double& oy) {
+  double rx, ry;
+  ks_stencil2<JAC>(s, r0, r1, r2, fv, ox, oy, rx, ry);
+}
+
+// per-warp partial sums (a, b) -> part[2 wg], part[2 wg + 1]
+__device__ __forceinline__ void ks_warp_partials(double a, double b, double* __restrict__ part, int wg, int lane) {
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_down_sync(0xffffffffu, a, o);
+    b += __shfl_down_sync(0xffffffffu, b, o);
+  }
+  if (lane == 0) {
+    part[2 * wg] = a;
+    part[2 * wg + 1] = b;
   }
 }
 
@@ -86,9 +108,12 @@ __device__ __forceinline__ void ks_cp_wait() { asm volatile("cp.async.wait_group
 __device__ __forceinline__ double2 ks_lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 
 // ---------------------------------------------------------------------------
-// PRE: NU sweeps + residual + restriction
+// PRE: NU sweeps + residual + restriction.  NORMS: also ||u||^2 of the input
+// and ||f - A u||^2 (the first stage's residual) as per-warp partials: the
+// stand-alone stopping test of the previous cycle's result (cycle.py:345)
+// at no extra stencil work.
 // ---------------------------------------------------------------------------
-template <int NU, bool ZERO>
+template <int NU, bool ZERO, bool NORMS = false>
 __global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
   constexpr int D = NU + 1;
   using G = KsGeom<D>;
@@ -96,9 +121,13 @@ __global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
   const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int band = wg % p.nbands, chunk = wg / p.nbands;
   const int P0 = band * G::NPB, Q0 = chunk * p.nq;
-  if (Q0 > p.mc) return;  // whole warp
+  if (Q0 > p.mc) {  // whole warp
+    if (NORMS) reinterpret_cast<double2*>(p.part)[wg * 32 + lane] = make_double2(0.0, 0.0);
+    return;
+  }
   const int m = p.m, P = p.P;
   const int XS = 2 * P0 - G::HL;
+  double acc_e = 0.0, acc_r = 0.0;
   const int c0 = XS + 2 * lane;
   const bool colx_in = c0 >= 0 && c0 < m, coly_in = c0 + 1 >= 0 && c0 + 1 < m;
   const int pcol = c0 >> 1;  // coarse column of this lane (c0 even)
@@ -144,6 +173,12 @@ __global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
     // ---- all stages from the pre-step windows (independent) -------------
     double2 nw[D + 1];
     nw[0] = u0;
+    // NORMS: rows owned by this chunk, interior columns owned by this lane;
+    // the input's residual is the first stage's f - A u at row yin - 2
+    const int y1 = yin - 2;
+    const bool own_e = NORMS && own_lane && yin >= 2 * Q0 && yin < 2 * Q0 + 2 * p.nq && yin < m;
+    const bool own_r = NORMS && own_lane && y1 >= 2 * Q0 && y1 < 2 * Q0 + 2 * p.nq && y1 >= 0 && y1 < m;
+    if (own_e) acc_e = fma(u0.y, u0.y, fma(u0.x, u0.x, acc_e));
 #pragma unroll
     for (int t = 1; t <= D; ++t) {
       double ox, oy;
@@ -151,6 +186,10 @@ __global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
         if (ZERO && t == 1) {  // first sweep on the zero guess: 0 + c f
           ox = kc_jacobi_zero(fr[1].x, s.c);
           oy = kc_jacobi_zero(fr[1].y, s.c);
+        } else if (NORMS && t == 1) {
+          double rx, ry;
+          ks_stencil2<true>(s, W[0][0], W[0][1], W[0][2], fr[1], ox, oy, rx, ry);
+          if (own_r) acc_r = fma(colx_in ? rx : 0.0, rx, fma(coly_in ? ry : 0.0, ry, acc_r));
         } else {
           ks_stencil2<true>(s, W[t - 1][0], W[t - 1][1], W[t - 1][2], fr[t], ox, oy);
         }
@@ -159,6 +198,7 @@ __global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
         oy = fr[t].y;
       } else {
         ks_stencil2<false>(s, W[t - 1][0], W[t - 1][1], W[t - 1][2], fr[t], ox, oy);
+        if (NORMS && t == 1 && own_r) acc_r = fma(colx_in ? ox : 0.0, ox, fma(coly_in ? oy : 0.0, oy, acc_r));
       }
       nw[t] = make_double2(ox, oy);
     }
@@ -196,6 +236,10 @@ __global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
     R[0] = R[1];
     R[1] = R[2];
     R[2] = nw[D];
+    // per-lane partials, stored from inside the loop: any code after it (a
+    // warp reduction, even a store) makes the compiler wrap the hot loop in
+    // a reconvergence region with divergence checks at every shuffle
+    if (NORMS && yin == ye) reinterpret_cast<double2*>(p.part)[wg * 32 + lane] = make_double2(acc_e, acc_r);
   }
 }
 
@@ -307,16 +351,7 @@ __global__ void __launch_bounds__(128, 4) k_post(const StreamParams p) {
       }
     }
   }
-  if (NORMS) {
-    for (int o = 16; o > 0; o >>= 1) {
-      acc_e += __shfl_down_sync(0xffffffffu, acc_e, o);
-      acc_r += __shfl_down_sync(0xffffffffu, acc_r, o);
-    }
-    if (lane == 0) {
-      p.part[2 * wg] = acc_e;
-      p.part[2 * wg + 1] = acc_r;
-    }
-  }
+  if (NORMS) ks_warp_partials(acc_e, acc_r, p.part, wg, lane);
 }
 
 // deterministic final sum of the per-warp partials: out[0] = sqrt(sum e), out[1] = sqrt(sum r)
@@ -345,5 +380,55 @@ __global__ void __launch_bounds__(256) k_norms_final(const double* __restrict__ 
     }
     out[0] = sqrt(te);
     out[1] = sqrt(tr);
+  }
+}
+
+// Deterministic sum of n (a, b) pairs over KS_NB blocks; the last block to
+// finish adds the block sums in order: out[0] = sqrt(sum a), out[1] = sqrt(sum b).
+#define KS_NB 32
+__global__ void __launch_bounds__(256) k_norms_lanes(const double2* __restrict__ part, int n, double2* __restrict__ bsum,
+                                                     unsigned* __restrict__ counter, double* __restrict__ out) {
+  __shared__ double sh[2][8];
+  __shared__ bool last;
+  const int per = (n + KS_NB - 1) / KS_NB;
+  const int i0 = blockIdx.x * per, i1 = min(n, i0 + per);
+  double a = 0.0, b = 0.0;
+  for (int i = i0 + threadIdx.x; i < i1; i += 256) {
+    const double2 v = part[i];
+    a += v.x;
+    b += v.y;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_down_sync(0xffffffffu, a, o);
+    b += __shfl_down_sync(0xffffffffu, b, o);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+    sh[0][w] = a;
+    sh[1][w] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ta = 0.0, tb = 0.0;
+    for (int k = 0; k < 8; ++k) {
+      ta += sh[0][k];
+      tb += sh[1][k];
+    }
+    bsum[blockIdx.x] = make_double2(ta, tb);
+    __threadfence();
+    last = atomicAdd(counter, 1u) == KS_NB - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double ta = 0.0, tb = 0.0;
+    for (int k = 0; k < KS_NB; ++k) {
+      const double2 v = __ldcg(bsum + k);  // L2: written by other blocks
+      ta += v.x;
+      tb += v.y;
+    }
+    out[0] = sqrt(ta);
+    out[1] = sqrt(tb);
+    *counter = 0u;
   }
 }
