@@ -27,9 +27,32 @@
 // coarsest solve under level n-1 (cycle.py:7-10) recomputes the identical
 // f/center and is skipped; CycleStats still counts it.
 #pragma once
+#include <cooperative_groups.h>
 #include "kc_common.cuh"
 
+// Two launch shapes, one kernel:
+//  * single CTA (entry side <= KC_BOT_MAX_M): every level in its shared
+//    memory, as described above;
+//  * thread-block cluster of cs CTAs (16, non-portable; 8 as a fallback)
+//    entering at a side <= KC_CLU_MAX_M (255): the levels with side >=
+//    KC_CLU_MIN_STRIP (31) are split into row strips of R = (m+1)/cs rows,
+//    one per CTA, each with one halo row above and below.  A strip phase is
+//    run by every CTA on its own rows; outputs on a strip's first/last row
+//    are also stored into the neighbour's halo row through distributed
+//    shared memory (st to a mapa'd address), and the phase ends with a
+//    cluster barrier (release/acquire), so the next phase sees them.
+//    Coarser levels live in CTA 0 only and run as in the single-CTA case
+//    while the other CTAs wait at the next cluster barrier (PH_CSYNC);
+//    the restriction into them and the prolongation out of them read and
+//    write CTA 0's shared memory remotely.  The full-coarsening strips nest
+//    (coarse strip = fine strip / 2), so every transfer is strip-local.
+// Measured (tools/micro/clsync): a 16-CTA cluster barrier costs ~490
+// cycles, ~940 with remote stores outstanding — cheaper than one graph
+// kernel node (~1.1 us) and far cheaper than the 255^2 / 127^2 levels on
+// the graph's tile kernels.
 #define KC_BOT_MAX_M 63
+#define KC_CLU_MAX_M 255
+#define KC_CLU_MIN_STRIP 31
 #define KC_BOT_MAXLEV 8
 #define KC_BOT_THREADS 512
 #define KC_BOT_WARPS (KC_BOT_THREADS / 32)
@@ -48,20 +71,28 @@ struct BotParams {
   int nsched;
   int final_cur;     // buffer holding the entry level's v after the schedule
   int nu1, nu2;      // sweeps inside PH_TINY frames
+  int nstrip;        // leading levels split into row strips over the cluster (0: single CTA)
 };
 
 // smem geometry of level d (entry side m0): side m_d = ((m0+1) >> d) - 1,
-// stride S = m+2, three (m+2)^2 arrays v0, v1, f.
+// stride S = m+2, three arrays v0, v1, f of (rows+2) x S, rows = m, or the
+// strip height R = (m+1)/cs for the first nstrip levels (same on every CTA,
+// so a local address maps to the same array on any rank).
 __host__ __device__ __forceinline__ int bot_m(int m0, int d) { return ((m0 + 1) >> d) - 1; }
-__host__ __device__ __forceinline__ int bot_off(int m0, int d) {
+__host__ __device__ __forceinline__ int bot_rows(int m0, int d, int nstrip, int cs) {
+  return d < nstrip ? (bot_m(m0, d) + 1) / cs : bot_m(m0, d);
+}
+__host__ __device__ __forceinline__ int bot_off(int m0, int d, int nstrip = 0, int cs = 1) {
   int off = 0;
   for (int j = 0; j < d; ++j) {
     const int s = bot_m(m0, j) + 2;
-    off += 3 * s * s;
+    off += 3 * (bot_rows(m0, j, nstrip, cs) + 2) * s;
   }
   return off;
 }
-__host__ __device__ __forceinline__ int bot_smem_doubles(int m0, int nlev) { return bot_off(m0, nlev); }
+__host__ __device__ __forceinline__ int bot_smem_doubles(int m0, int nlev, int nstrip = 0, int cs = 1) {
+  return bot_off(m0, nlev, nstrip, cs);
+}
 __host__ __device__ __forceinline__ int bot_warps(int m) {
   return m >= 31 ? KC_BOT_WARPS : (m >= 15 ? 8 : 1);  // 2 warps at m = 7 measured slower
 }
@@ -71,6 +102,10 @@ __device__ __forceinline__ void bot_sync(int g) {
   else if (g == 1) __syncwarp();
   else if (g == 8) asm volatile("bar.sync 1, 256;" ::: "memory");
   else asm volatile("bar.sync 2, 64;" ::: "memory");
+}
+// every thread of every CTA of the cluster; orders the DSMEM stores before it
+__device__ __forceinline__ void clu_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 #ifdef KC_BOT_TRACE
@@ -97,13 +132,14 @@ __device__ long long kc_bot_trace_end[KC_BOT_TRACE];
 //           interpreter overhead between them (bot_tiny below).
 enum BotOp {
   PH_JACOBI = 0, PH_RESID = 1, PH_RESTRICT = 2, PH_PROLONG = 3, PH_JOIN = 4, PH_J2Z = 5, PH_RR = 6, PH_PJ = 7,
-  PH_TINY = 8
+  PH_TINY = 8, PH_CSYNC = 9
 };
 #define KC_BOT_TINY_M 7  // frames on sides <= this run as PH_TINY
 #define KC_BOT_FUSE_M 15  // PH_RR / PH_PJ on sides <= this (latency-bound levels)
 // Descriptor: bits 0-3 op, 4-6 level d, 7 src buffer, 8 zero guess, 9 child
 // buffer (prolong), 10 child is the 1x1 coarsest (restrict), 11-12 warp
-// group code, 13-16 cycle counter (PH_TINY).
+// group code, 13-16 cycle counter (PH_TINY), 17 strip phase (all CTAs).
+//   PH_CSYNC  cluster barrier before a strip phase that follows CTA-0 work.
 __host__ __device__ __forceinline__ unsigned bot_desc(int op, int d, int src, int zero, int cbuf, int cc, int g,
                                                       int kap = 0) {
   const unsigned gc = g >= KC_BOT_WARPS ? 3u : (g >= 8 ? 2u : (g >= 2 ? 1u : 0u));
@@ -121,6 +157,7 @@ __device__ __forceinline__ int bot_desc_g(unsigned e) {
 #define BD_CBUF(e) ((int)(((e) >> 9) & 1u))
 #define BD_CC(e) ((int)(((e) >> 10) & 1u))
 #define BD_KAP(e) ((int)(((e) >> 13) & 15u))
+#define BD_STRIP_BIT (1u << 17)
 
 #include <vector>
 // Flatten kappa_cycle over the smem-resident levels (cycle.py:204-220) into
@@ -128,8 +165,10 @@ __device__ __forceinline__ int bot_desc_g(unsigned e) {
 // and zero guesses exactly like the executor does for the HBM levels.
 struct BotBuilder {  // host side
   int m0, nlev, nu1, nu2;
+  int nstrip = 0;           // levels d < nstrip are strip phases (all CTAs of the cluster)
   unsigned cur = 0, vz = 0;
   int gprev = KC_BOT_WARPS;
+  bool local_run = false;   // the last emitted phase ran on CTA 0 only
   bool fuse = true;         // emit PH_J2Z
   bool fuse_small = false;  // emit PH_RR / PH_PJ (measured slower: larger kernel, longer chains)
   bool tiny = true;         // whole frames on sides <= KC_BOT_TINY_M as PH_TINY
@@ -137,9 +176,17 @@ struct BotBuilder {  // host side
   std::vector<unsigned> out;
   void emit(int op, int d, int src, int zero, int cbuf, int cc, int kap = 0) {
     if (dry) return;
+    if (d < nstrip) {
+      if (local_run) out.push_back(bot_desc(PH_CSYNC, 0, 0, 0, 0, 0, KC_BOT_WARPS));
+      local_run = false;
+      gprev = KC_BOT_WARPS;  // a strip phase ends with a cluster barrier
+      out.push_back(bot_desc(op, d, src, zero, cbuf, cc, KC_BOT_WARPS, kap) | BD_STRIP_BIT);
+      return;
+    }
     const int g = bot_warps(bot_m(m0, d));
     if (g > gprev) out.push_back(bot_desc(PH_JOIN, 0, 0, 0, 0, 0, g));
     gprev = g;
+    local_run = true;
     out.push_back(bot_desc(op, d, src, zero, cbuf, cc, g, kap));
   }
   void relax(int d, int count) {
@@ -156,7 +203,7 @@ struct BotBuilder {  // host side
     }
   }
   void rec(int d, int kap) {
-    if (tiny && fuse && !dry && bot_m(m0, d) <= KC_BOT_TINY_M && d < nlev - 1 && kap <= 15) {
+    if (tiny && fuse && !dry && d >= nstrip && bot_m(m0, d) <= KC_BOT_TINY_M && d < nlev - 1 && kap <= 15) {
       // one descriptor; bot_tiny follows the rules below (J2Z on), so
       // replay them dry to track the buffers of level d
       emit(PH_TINY, d, (cur >> d) & 1u, (vz >> d) & 1u, 0, 0, kap);
@@ -201,12 +248,46 @@ struct BotBuilder {  // host side
 // y = i / m for i < 2^12, m <= 64: float reciprocal, exact for these ranges
 __device__ __forceinline__ int bot_div(int i, float inv) { return (int)(((float)i + 0.5f) * inv); }
 
-// Jacobi sweep (zero guess folded) or residual on an m x m smem level.
-// RB rows per thread share their loads (3 new loads per row).
+// per-level constants precomputed once per launch (keeps the per-phase
+// dependent integer chain short: a few LDS.128 instead of address math)
+struct BotLv {
+  int m, S, vo0, vo1;           // side, stride, smem offsets of the v buffers (interior origin)
+  int fo, nitem1, nitem4, rows;  // f offset, stencil items for RB = 1 / 4, own interior rows
+  int a, R, rb4, crows;          // first global row, strip height, RB = 4?, own rows of the child
+  float inv, invc, invn, padf;   // 1/m, 1/m_child, 1/(m_child+1)
+};
+
+// Halo pushes of a strip phase: values on own row 0 also go to the upper
+// neighbour's row R (its halo below), values on own row R-1 to the lower
+// neighbour's row -1.  Null for CTA-local levels and at the strip ends.
+struct BotPush {
+  double* up;
+  double* dn;
+  int last;
+  __device__ __forceinline__ void put(double* o, int S, int y, int x, double v) const {
+    o[y * S + x] = v;
+    if (up && y == 0) up[x] = v;
+    if (dn && y == last) dn[x] = v;
+  }
+};
+__device__ __forceinline__ BotPush bot_push(double* origin, const BotLv& L, bool strip, int rank, int cs) {
+  BotPush p{nullptr, nullptr, -1};
+  if (strip) {
+    cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+    if (rank > 0) p.up = cl.map_shared_rank(origin, rank - 1) + L.R * L.S;
+    if (rank + 1 < cs) p.dn = cl.map_shared_rank(origin, rank + 1) - L.S;
+    p.last = L.R - 1;
+  }
+  return p;
+}
+
+// Jacobi sweep (zero guess folded) or residual on the rows x m block of a
+// level (all of it, or this CTA's strip).  RB rows per item share their
+// loads (3 new loads per row).
 template <int RB>
 __device__ __forceinline__ void bot_stencil(bool jac, bool zero, const double* __restrict__ u, double* __restrict__ o,
-                                            const double* __restrict__ f, int m, int S, float inv, const St9& st,
-                                            int tid, int nth, int nitems) {
+                                            const double* __restrict__ f, int m, int rows, int S, float inv,
+                                            const St9& st, int tid, int nth, int nitems, const BotPush& ps) {
   for (int it = tid; it < nitems; it += nth) {
     const int rb = bot_div(it, inv);  // it / m
     const int x = it - rb * m;
@@ -214,7 +295,7 @@ __device__ __forceinline__ void bot_stencil(bool jac, bool zero, const double* _
     if (jac && zero) {
 #pragma unroll
       for (int k = 0; k < RB; ++k)
-        if (y0 + k < m) o[(y0 + k) * S + x] = kc_jacobi_zero(f[(y0 + k) * S + x], st.c);
+        if (y0 + k < rows) ps.put(o, S, y0 + k, x, kc_jacobi_zero(f[(y0 + k) * S + x], st.c));
       continue;
     }
     const double* pu = u + y0 * S + x;
@@ -222,12 +303,12 @@ __device__ __forceinline__ void bot_stencil(bool jac, bool zero, const double* _
     double b0 = pu[-1], b1 = pu[0], b2 = pu[1];
 #pragma unroll
     for (int k = 0; k < RB; ++k) {
-      if (y0 + k < m) {
+      if (y0 + k < rows) {
         const double* pn = pu + (k + 1) * S;
         const double c0 = pn[-1], c1 = pn[0], c2 = pn[1];
         const int i = (y0 + k) * S + x;
         const double au = kc_sum9(st, a0, a1, a2, b0, b1, b2, c0, c1, c2);
-        o[i] = jac ? kc_jacobi_pt(b1, f[i], au, st.c) : DSUB(f[i], au);
+        ps.put(o, S, y0 + k, x, jac ? kc_jacobi_pt(b1, f[i], au, st.c) : DSUB(f[i], au));
         a0 = b0; a1 = b1; a2 = b2;
         b0 = c0; b1 = c1; b2 = c2;
       }
@@ -235,17 +316,9 @@ __device__ __forceinline__ void bot_stencil(bool jac, bool zero, const double* _
   }
 }
 
-// per-level constants precomputed once per launch (keeps the per-phase
-// dependent integer chain short: one LDS.128 pair instead of address math)
-struct BotLv {
-  int m, S, vo0, vo1;  // side, stride, smem offsets of v buffers (interior origin)
-  int fo, nitem1, nitem4, pad;  // f offset, items for RB=1 / RB=4 stencil loops
-  float inv, invc, invn, padf;  // 1/m, 1/m_child, 1/(m_child+1)
-};
-
 // u2 = J(J(0)) into u, with u1 = 0 + c f recomputed at the neighbours (PH_J2Z)
 __device__ __forceinline__ void bot_j2z(double* __restrict__ u, const double* __restrict__ f, const BotLv& L,
-                                        const St9& st, int tid, int nth) {
+                                        const St9& st, int tid, int nth, const BotPush& ps) {
   const int m = L.m, S = L.S;
   for (int i = tid; i < L.nitem1; i += nth) {
     const int y = bot_div(i, L.inv), x = i - y * m;
@@ -256,45 +329,48 @@ __device__ __forceinline__ void bot_j2z(double* __restrict__ u, const double* __
 #pragma unroll
       for (int dx = 0; dx < 3; ++dx) n1[dy * 3 + dx] = kc_jacobi_zero(pf[(dy - 1) * S + (dx - 1)], st.c);
     const double au = kc_sum9(st, n1[0], n1[1], n1[2], n1[3], n1[4], n1[5], n1[6], n1[7], n1[8]);
-    u[y * S + x] = kc_jacobi_pt(n1[4], pf[0], au, st.c);
+    ps.put(u, S, y, x, kc_jacobi_pt(n1[4], pf[0], au, st.c));
   }
 }
 
-// fc = FW(r) on level d+1; with cc the child is the 1x1 coarsest and its
-// solve f/center is folded in (coarsest_solve, cycle.py:182-190)
-__device__ __forceinline__ void bot_restrict(const double* __restrict__ r, const BotLv& L, const BotLv& C,
-                                             double* __restrict__ sm, double ccenter, bool cc, int tid, int nth) {
-  const int S = L.S, mc = C.m, SC = C.S;
-  double* fc = sm + C.fo;
-  double* vc = sm + C.vo0;  // buffer 0
-  for (int i = tid; i < C.nitem1; i += nth) {
+// fc = FW(r) on the crows x mc coarse block of this CTA (fc: its row 0);
+// with cc the child is the 1x1 coarsest and its solve f/center is folded in
+// (coarsest_solve, cycle.py:182-190)
+__device__ __forceinline__ void bot_restrict(const double* __restrict__ r, const BotLv& L, double* __restrict__ fc,
+                                             int mc, int SC, double* __restrict__ vc, double ccenter, bool cc,
+                                             int tid, int nth, const BotPush& ps) {
+  const int S = L.S;
+  const int n = L.crows * mc;
+  for (int i = tid; i < n; i += nth) {
     const int q = bot_div(i, L.invc), p = i - q * mc;
     const double* rc = r + (2 * q + 1) * S + (2 * p + 1);
     const double* rs = rc - S;
     const double* rn = rc + S;
     const double fv = kc_fw(rs[-1], rs[0], rs[1], rc[-1], rc[0], rc[1], rn[-1], rn[0], rn[1]);
-    fc[q * SC + p] = fv;
+    ps.put(fc, SC, q, p, fv);
     if (cc) vc[0] = __ddiv_rn(fv, ccenter);
   }
 }
 
-// u += P vc (zero: u = 0 + P vc), one coarse cell (2x2 fine points) per item
+// u += P vc (zero: u = 0 + P vc) on this CTA's rows, one coarse cell (2x2
+// fine points) per item; vc points at the child row matching fine row 0 / 2
 __device__ __forceinline__ void bot_prolong(double* __restrict__ u, const double* __restrict__ vc, const BotLv& L,
-                                            const BotLv& C, bool zero, int tid, int nth) {
-  const int S = L.S, mc = C.m, SC = C.S;
+                                            int mc, int SC, bool zero, int tid, int nth, const BotPush& ps) {
+  const int S = L.S;
   const int nc = mc + 1;
-  for (int i = tid; i < nc * nc; i += nth) {
+  const int n = ((L.rows + 1) >> 1) * nc;
+  for (int i = tid; i < n; i += nth) {
     const int q = bot_div(i, L.invn), p = i - q * nc;
     const double c00 = vc[(q - 1) * SC + p - 1], c01 = vc[(q - 1) * SC + p];
     const double c10 = vc[q * SC + p - 1], c11 = vc[q * SC + p];
-    double* pv = u + 2 * q * S + 2 * p;
+    const int y = 2 * q, x = 2 * p;
     // (even, even): fine[0::2, 0::2] = 0.25 (((c00 + c01) + c10) + c11)   (transfer.py:57)
-    pv[0] = DADD(zero ? 0.0 : pv[0], DMUL(0.25, DADD(DADD(DADD(c00, c01), c10), c11)));
+    ps.put(u, S, y, x, DADD(zero ? 0.0 : u[y * S + x], DMUL(0.25, DADD(DADD(DADD(c00, c01), c10), c11))));
     if (p < mc)  // (even, odd): fine[0::2, 1::2] = 0.5 (c01 + c11)   (transfer.py:56)
-      pv[1] = DADD(zero ? 0.0 : pv[1], DMUL(0.5, DADD(c01, c11)));
-    if (q < mc) {
-      pv[S] = DADD(zero ? 0.0 : pv[S], DMUL(0.5, DADD(c10, c11)));  // (odd, even), transfer.py:55
-      if (p < mc) pv[S + 1] = DADD(zero ? 0.0 : pv[S + 1], c11);     // (odd, odd), transfer.py:54
+      ps.put(u, S, y, x + 1, DADD(zero ? 0.0 : u[y * S + x + 1], DMUL(0.5, DADD(c01, c11))));
+    if (y + 1 < L.rows) {
+      ps.put(u, S, y + 1, x, DADD(zero ? 0.0 : u[(y + 1) * S + x], DMUL(0.5, DADD(c10, c11))));  // transfer.py:55
+      if (p < mc) ps.put(u, S, y + 1, x + 1, DADD(zero ? 0.0 : u[(y + 1) * S + x + 1], c11));   // transfer.py:54
     }
   }
 }
@@ -313,13 +389,14 @@ struct BotTiny {
     int i = 0;
     const double* f = sm + L.fo;
     if (count >= 2 && vz) {
-      bot_j2z(buf(L, cur), f, L, st, lane, 32);
+      bot_j2z(buf(L, cur), f, L, st, lane, 32, BotPush{nullptr, nullptr, -1});
       __syncwarp();
       vz = 0;
       i = 2;
     }
     for (; i < count; ++i) {
-      bot_stencil<1>(true, vz, buf(L, cur), buf(L, cur ^ 1), f, L.m, L.S, L.inv, st, lane, 32, L.nitem1);
+      bot_stencil<1>(true, vz, buf(L, cur), buf(L, cur ^ 1), f, L.m, L.m, L.S, L.inv, st, lane, 32, L.nitem1,
+                     BotPush{nullptr, nullptr, -1});
       __syncwarp();
       vz = 0;
       cur ^= 1;
@@ -330,16 +407,19 @@ struct BotTiny {
     relax(L, st, nu1, cur, vz);
     const double* f = sm + L.fo;
     if (!vz) {
-      bot_stencil<1>(false, false, buf(L, cur), buf(L, cur ^ 1), f, L.m, L.S, L.inv, st, lane, 32, L.nitem1);
+      bot_stencil<1>(false, false, buf(L, cur), buf(L, cur ^ 1), f, L.m, L.m, L.S, L.inv, st, lane, 32, L.nitem1,
+                     BotPush{nullptr, nullptr, -1});
       __syncwarp();
     }
-    bot_restrict(vz ? f : buf(L, cur ^ 1), L, lv[d + 1], sm, tab[d + 1].center, cc, lane, 32);
+    const BotLv C = lv[d + 1];
+    bot_restrict(vz ? f : buf(L, cur ^ 1), L, sm + C.fo, C.m, C.S, sm + C.vo0, tab[d + 1].center, cc, lane, 32,
+                 BotPush{nullptr, nullptr, -1});
     __syncwarp();
   }
   // prolongation of child buffer cb + post-smoothing
   __device__ __forceinline__ void up(int d, const BotLv& L, const St9& st, int& cur, int& vz, int cb) const {
     const BotLv C = lv[d + 1];
-    bot_prolong(buf(L, cur), buf(C, cb), L, C, vz, lane, 32);
+    bot_prolong(buf(L, cur), buf(C, cb), L, C.m, C.S, vz, lane, 32, BotPush{nullptr, nullptr, -1});
     __syncwarp();
     vz = 0;
     relax(L, st, nu2, cur, vz);
@@ -372,24 +452,33 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
   __shared__ St9 tab[KC_BOT_MAXLEV];
   __shared__ BotLv lv[KC_BOT_MAXLEV];
   __shared__ unsigned sched[KC_BOT_MAXPH];
-  const int nlev = bp.nlev;
-  const int total = bot_smem_doubles(m0, nlev);
+  cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+  const int rank = (int)cl.block_rank(), cs = (int)cl.num_blocks();
+  const int nlev = bp.nlev, nstrip = bp.nstrip;
+  const int total = bot_smem_doubles(m0, nlev, nstrip, cs);
   for (int i = threadIdx.x; i < total; i += KC_BOT_THREADS) sm[i] = 0.0;
   for (int i = threadIdx.x; i < bp.nsched; i += KC_BOT_THREADS) sched[i] = bp.sched[i];
   if (threadIdx.x < nlev) {
     const int d = threadIdx.x;
     tab[d] = bp.st[d];
-    const int m = bot_m(m0, d), S = m + 2, base = bot_off(m0, d);
+    const bool strip = d < nstrip;
+    const int m = bot_m(m0, d), S = m + 2, base = bot_off(m0, d, nstrip, cs);
+    const int R = bot_rows(m0, d, nstrip, cs);
     const int mc = d + 1 < nlev ? bot_m(m0, d + 1) : 1;
     BotLv L;
     L.m = m;
     L.S = S;
+    L.R = R;
+    L.a = strip ? rank * R : 0;
+    L.rows = strip ? min(R, m - L.a) : m;
     L.vo0 = base + S + 1;
-    L.vo1 = base + S * S + S + 1;
-    L.fo = base + 2 * S * S + S + 1;
-    L.nitem1 = m * m;
-    L.nitem4 = m * ((m + 3) / 4);
-    L.pad = 0;
+    L.vo1 = base + (R + 2) * S + S + 1;
+    L.fo = base + 2 * (R + 2) * S + S + 1;
+    L.nitem1 = L.rows * m;
+    L.nitem4 = m * ((L.rows + 3) / 4);
+    L.rb4 = strip ? (L.nitem4 >= KC_BOT_THREADS) : (m >= 31);
+    // coarse rows whose centre fine row 2q+1 lies in this CTA's rows
+    L.crows = strip ? min(mc, (L.a + L.rows) / 2) - L.a / 2 : mc;
     L.inv = 1.0f / (float)m;
     L.invc = 1.0f / (float)mc;
     L.invn = 1.0f / (float)(mc + 1);
@@ -397,7 +486,22 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
     lv[d] = L;
   }
   __syncthreads();
-  {
+  if (nstrip > 0) {  // strip entry: own rows plus one halo row each side, ghost columns included
+    const BotLv L = lv[0];
+    const int S = L.S;
+    double* v = sm + L.vo0 - 1;  // row 0, column -1
+    double* f = sm + L.fo - 1;
+    const int y0 = L.a - 1, y1 = min(L.a + L.R, m0);  // rows -1 .. m0 exist in HBM (ghost rows zero)
+    const int n = (y1 - y0 + 1) * S;
+    for (int i = threadIdx.x; i < n; i += KC_BOT_THREADS) {
+      const int r = i / S, c = i - r * S;
+      const int y = y0 + r;
+      const size_t gi = kc_idx(bp.gP, y, c - 1);
+      f[(y - L.a) * S + c] = bp.gf[gi];
+      if (!bp.v_zero) v[(y - L.a) * S + c] = bp.gv[gi];
+    }
+    clu_sync();  // every CTA initialised before any halo push lands
+  } else {
     const int S = m0 + 2;
     double* v = sm + S + 1;
     double* f = sm + 2 * S * S + S + 1;
@@ -407,8 +511,8 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
       f[y * S + x] = bp.gf[gi];
       if (!bp.v_zero) v[y * S + x] = bp.gv[gi];
     }
+    __syncthreads();
   }
-  __syncthreads();
 
   const int warp = threadIdx.x >> 5;
   const int tid = threadIdx.x;
@@ -418,15 +522,21 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
   if (nlev == 1) {  // the entry level is the coarsest (n == 1): f / center
     if (threadIdx.x == 0) sm[4] = __ddiv_rn(sm[2 * 9 + 4], tab[0].center);
   }
-  // replay the schedule: a warp takes part in the phases of its group only;
-  // JOIN entries gather a larger group before it resumes work
+  // replay the schedule: strip phases run on every CTA and end with a
+  // cluster barrier; the others run on CTA 0, where a warp takes part in the
+  // phases of its group only and JOIN entries gather a larger group
   unsigned e_next = bp.nsched > 0 ? sched[0] : 0u;
   for (int k = 0; k < bp.nsched; ++k) {
     const unsigned e = e_next;
     if (k + 1 < bp.nsched) e_next = sched[k + 1];
-    const int g = bot_desc_g(e);
-    if (warp >= g) continue;
     const int op = BD_OP(e);
+    if (op == PH_CSYNC) {
+      clu_sync();
+      continue;
+    }
+    const bool strip = (e & BD_STRIP_BIT) != 0u;
+    const int g = bot_desc_g(e);
+    if (!strip && (rank != 0 || warp >= g)) continue;
     if (op == PH_JOIN) {
       bot_sync(g);
       continue;
@@ -440,38 +550,55 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
     const double* f = sm + L.fo;
     double* u = sm + (src ? L.vo1 : L.vo0);
 #ifdef KC_BOT_TRACE
-    if (threadIdx.x == 0 && tr_n < KC_BOT_TRACE) {
+    if (threadIdx.x == 0 && rank == 0 && tr_n < KC_BOT_TRACE) {
       kc_bot_trace[tr_n] = clock64();
       kc_bot_trace_op[tr_n] = op * 16 + d;
       kc_bot_trace_n = ++tr_n;
     }
 #endif
     if (op == PH_J2Z) {
-      bot_j2z(u, f, L, tab[d], tid, nth);
+      bot_j2z(u, f, L, tab[d], tid, nth, bot_push(u, L, strip, rank, cs));
     } else if (op <= PH_RESID) {
       double* o = sm + (src ? L.vo0 : L.vo1);
       const St9 st = tab[d];
-      if (m >= 31) bot_stencil<4>(op == PH_JACOBI, zero, u, o, f, m, S, L.inv, st, tid, nth, L.nitem4);
-      else bot_stencil<1>(op == PH_JACOBI, zero, u, o, f, m, S, L.inv, st, tid, nth, L.nitem1);
+      const BotPush ps = bot_push(o, L, strip, rank, cs);
+      if (L.rb4) bot_stencil<4>(op == PH_JACOBI, zero, u, o, f, m, L.rows, S, L.inv, st, tid, nth, L.nitem4, ps);
+      else bot_stencil<1>(op == PH_JACOBI, zero, u, o, f, m, L.rows, S, L.inv, st, tid, nth, L.nitem1, ps);
     } else if (op == PH_RESTRICT) {  // r in buffer src, or f itself on a zero guess
-      bot_restrict(zero ? f : u, L, lv[d + 1], sm, tab[d + 1].center, BD_CC(e), tid, nth);
+      const BotLv C = lv[d + 1];
+      double* fc = sm + C.fo;
+      double* vc = sm + C.vo0;
+      BotPush ps{nullptr, nullptr, -1};
+      if (strip && d + 1 < nstrip) {
+        ps = bot_push(fc, C, true, rank, cs);
+      } else if (strip) {  // into CTA 0's level, at this strip's first coarse row
+        fc = cl.map_shared_rank(fc, 0) + (L.a / 2) * C.S;
+        vc = cl.map_shared_rank(vc, 0);
+      }
+      bot_restrict(zero ? f : u, L, fc, C.m, C.S, vc, tab[d + 1].center, BD_CC(e), tid, nth, ps);
     } else if (op == PH_PROLONG) {
       const BotLv C = lv[d + 1];
-      bot_prolong(u, sm + (BD_CBUF(e) ? C.vo1 : C.vo0), L, C, zero, tid, nth);
-    } else {  // PH_TINY (warp 0)
+      const double* vc = sm + (BD_CBUF(e) ? C.vo1 : C.vo0);
+      if (strip && d + 1 >= nstrip)  // from CTA 0's level, at this strip's first coarse row
+        vc = cl.map_shared_rank(const_cast<double*>(vc), 0) + (L.a / 2) * C.S;
+      bot_prolong(u, vc, L, C.m, C.S, zero, tid, nth, bot_push(u, L, strip, rank, cs));
+    } else {  // PH_TINY (warp 0 of CTA 0)
       const BotTiny t{sm, lv, tab, bp.nu1, bp.nu2, tid};
       int cur = src, vz = zero;
       t.frame(d, BD_KAP(e), nlev, cur, vz);
     }
-    bot_sync(g);
+    if (strip) clu_sync();
+    else bot_sync(g);
   }
   __syncthreads();
   {
-    const int S = m0 + 2;
-    const double* v = sm + bp.final_cur * S * S + S + 1;
-    for (int i = threadIdx.x; i < m0 * m0; i += KC_BOT_THREADS) {
+    const BotLv L = lv[0];
+    const int S = L.S;
+    const double* v = sm + (bp.final_cur ? L.vo1 : L.vo0);
+    const int n = L.rows * m0;
+    for (int i = threadIdx.x; i < n; i += KC_BOT_THREADS) {
       const int y = i / m0, x = i - y * m0;
-      bp.gv[kc_idx(bp.gP, y, x)] = v[y * S + x];
+      bp.gv[kc_idx(bp.gP, L.a + y, x)] = v[y * S + x];
     }
   }
 }

@@ -116,6 +116,7 @@ struct kc_handle {
   BotParams bot_base{};
   size_t bot_smem = 0;
   int bot_m0 = 0;
+  int bot_cs = 1;  // CTAs per bottom launch (thread-block cluster when > 1)
   // host-built bottom phase schedules, keyed by (kappa1, kappa2, v_zero)
   std::map<std::tuple<int, int, int>, std::tuple<unsigned*, int, int>> bot_sched;
   cudaStream_t stream = nullptr;
@@ -323,6 +324,7 @@ int get_bot_sched(kc_handle* h, int k1, int k2, int vzero, const unsigned** dev,
     b.nu1 = h->nu1;
     b.nu2 = h->nu2;
     b.vz = vzero ? 1u : 0u;
+    b.nstrip = h->bot_base.nstrip;
     if (b.nlev > 1) {
       b.rec(0, k1);
       if (k2 > 0) b.rec(0, k2);
@@ -351,7 +353,23 @@ int ex_bottom(kc_handle* h, int l, int k1, int k2) {
   int rc = get_bot_sched(h, k1, k2, bp.v_zero, &bp.sched, &bp.nsched, &bp.final_cur);
   if (rc) return rc;
   if (h->L[h->n - 1].st.center == 0.0) KC_FAIL(h, KC_ESINGULAR, "singular coarsest operator");
-  k_bottom<<<1, KC_BOT_THREADS, h->bot_smem, h->stream>>>(bp, h->bot_m0);
+  if (h->bot_cs > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(h->bot_cs);
+    cfg.blockDim = dim3(KC_BOT_THREADS);
+    cfg.dynamicSmemBytes = h->bot_smem;
+    cfg.stream = h->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = h->bot_cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    KC_CUDA(h, cudaLaunchKernelEx(&cfg, k_bottom, bp, h->bot_m0));
+  } else {
+    k_bottom<<<1, KC_BOT_THREADS, h->bot_smem, h->stream>>>(bp, h->bot_m0);
+  }
   KC_LAUNCH_CHECK(h);
   ++h->launches;
   L.vzero = false;
@@ -924,22 +942,76 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
   }
   cudaMemset(h->d_scal, 0, sizeof(double) * 64);
 
-  // bottom (smem-resident) levels
-  int lb = -1;
-  for (int l = 0; l < n; ++l)
-    if (h->L[l].m <= KC_BOT_MAX_M) {
-      lb = l;
-      break;
+  // bottom (smem-resident) levels: a cluster of 16 (else 8) CTAs entering
+  // at side <= 255 with the sides >= 31 in row strips, else one CTA
+  // entering at side <= 63 (kc_bottom.cuh); KC_BOT_CLUSTER=0 forces one CTA
+  int lb = -1, cs = 1, nstrip = 0;
+  size_t smem = 0;
+  {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k_bottom);
+    const size_t smem_max = prop.sharedMemPerBlockOptin - fa.sharedSizeBytes;
+    const char* env = getenv("KC_BOT_CLUSTER");
+    const bool allow = !(env && env[0] == '0');
+    cudaFuncSetAttribute(k_bottom, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (int csz : {16, 8}) {
+      if (!allow || lb >= 0) break;
+      for (int e = 0; e < n && lb < 0; ++e) {
+        if (h->L[e].m > KC_CLU_MAX_M) continue;
+        const int m0 = h->L[e].m, nl = n - e;
+        int ns = 0;
+        while (ns < nl) {
+          const int m = bot_m(m0, ns);
+          if (m < KC_CLU_MIN_STRIP || (m + 1) % csz != 0 || ((m + 1) / csz) % 2 != 0) break;
+          ++ns;
+        }
+        if (ns == 0) break;  // coarser entries have no strips either
+        const size_t bytes = sizeof(double) * (size_t)bot_smem_doubles(m0, nl, ns, csz);
+        if (bytes > smem_max) continue;
+        if (cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) continue;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(csz);
+        cfg.blockDim = dim3(KC_BOT_THREADS);
+        cfg.dynamicSmemBytes = bytes;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = csz;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, k_bottom, &cfg) != cudaSuccess || ncl < 1) {
+          cudaGetLastError();
+          break;
+        }
+        lb = e;
+        cs = csz;
+        nstrip = ns;
+        smem = bytes;
+      }
     }
+    cudaGetLastError();
+    if (lb < 0) {
+      for (int l = 0; l < n; ++l)
+        if (h->L[l].m <= KC_BOT_MAX_M) {
+          lb = l;
+          break;
+        }
+      if (lb >= 0) smem = sizeof(double) * (size_t)bot_smem_doubles(h->L[lb].m, n - lb);
+    }
+  }
   if (lb >= 0) {
     BotParams& bp = h->bot_base;
     memset(&bp, 0, sizeof(bp));
     bp.nlev = n - lb;
     bp.nu1 = nu1;
     bp.nu2 = nu2;
+    bp.nstrip = nstrip;
     for (int j = 0; j < bp.nlev; ++j) bp.st[j] = h->L[lb + j].st;
     h->bot_m0 = h->L[lb].m;
-    h->bot_smem = sizeof(double) * (size_t)bot_smem_doubles(h->bot_m0, bp.nlev);
+    h->bot_cs = cs;
+    h->bot_smem = smem;
     if (cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->bot_smem) != cudaSuccess) {
       h->err = "cudaFuncSetAttribute(k_bottom) failed";
       return fail(KC_ECUDA);

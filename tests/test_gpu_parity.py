@@ -483,6 +483,35 @@ def test_fused_matches_per_op_and_oracle(n, nu1, nu2):
             st.close()
 
 
+@pytest.mark.parametrize("n", [3, 4, 5, 6, 7, 8, 9, 10])
+@pytest.mark.parametrize("nu1,nu2", [(2, 2), (1, 1), (0, 2), (3, 0)])
+def test_bottom_cluster_and_single_cta(n, nu1, nu2, monkeypatch):
+    """The bottom kernel runs as a 16-CTA cluster (levels >= 31^2 in row
+    strips with DSMEM halos, entry <= 255^2) or, with KC_BOT_CLUSTER=0, as one
+    CTA (entry <= 63^2).  Both must equal the oracle bit-for-bit for every
+    kappa, including W (long schedules, many CTA-0 <-> strip transitions)."""
+    m = 2 ** n - 1
+    rng = np.random.default_rng(7 * n + nu1)
+    v0, f0 = rng.random((m, m)), rng.standard_normal((m, m))
+    for kappa in (1, 2, 3, INF):
+        cfg = CycleConfig(n=n, kappa=kappa, nu1=nu1, nu2=nu2)
+        h = O.Hierarchy(O.hierarchy(1e-4, 45.0, n), nu1=nu1, nu2=nu2)
+        h.v[0], h.f[0] = v0.copy(), f0.copy()
+        ke = n if kappa == INF else kappa
+        ref = []
+        for _ in range(2):
+            h.cycle(ke)
+            ref.append(h.v[0].copy())
+        for mode in ("1", "0"):
+            monkeypatch.setenv("KC_BOT_CLUSTER", mode)
+            st = build_state(ProblemSpec(1e-4, 45.0), cfg)
+            st.v[0], st.f[0] = v0, f0
+            for c in range(2):
+                run_cycle(st, cfg, CycleStats.for_levels(n))
+                assert np.array_equal(st.v[0], ref[c]), (n, nu1, nu2, kappa, mode, c)
+            st.close()
+
+
 @pytest.mark.parametrize("kname", ["1", "2", "3", "4", "W"])
 def test_n12_pcg_vs_reference(kname):
     """Config C3: the kappa-cycle as PCG preconditioner at

@@ -8,7 +8,10 @@
 
 int main(int argc, char** argv) {
   int kappa = argc > 1 ? atoi(argv[1]) : 3;
-  const int m0 = 63, nlev = 6, P = kc_pitch(m0);
+  const int cs = argc > 3 ? atoi(argv[3]) : 1;  // cluster size (16: entry 255^2, strips down to 31^2)
+  const int m0 = cs > 1 ? 255 : 63, nlev = cs > 1 ? 8 : 6, P = kc_pitch(m0);
+  int nstrip = 0;
+  while (cs > 1 && nstrip < nlev && bot_m(m0, nstrip) >= KC_CLU_MIN_STRIP) ++nstrip;
   size_t el = (size_t)(m0 + 2) * P;
   std::vector<double> hf(el, 0.0);
   for (int y = 0; y < m0; ++y) for (int x = 0; x < m0; ++x) hf[kc_idx(P, y, x)] = ((y * 7 + x * 3) % 11) * 0.1;
@@ -24,19 +27,29 @@ int main(int argc, char** argv) {
   }
   BotBuilder b; b.m0 = m0; b.nlev = nlev; b.nu1 = 2; b.nu2 = 2; b.vz = 1;
   b.tiny = argc > 2 ? atoi(argv[2]) != 0 : true;
+  b.nstrip = nstrip;
   b.rec(0, kappa); if (kappa > 1) b.rec(0, kappa - 1);
   unsigned* ds; cudaMalloc(&ds, b.out.size() * 4);
   cudaMemcpy(ds, b.out.data(), b.out.size() * 4, cudaMemcpyHostToDevice);
   bp.gv = gv; bp.gf = gf; bp.gP = P; bp.v_zero = 1; bp.sched = ds; bp.nsched = (int)b.out.size(); bp.final_cur = b.cur & 1;
-  bp.nu1 = 2; bp.nu2 = 2;
-  size_t smem = sizeof(double) * bot_smem_doubles(m0, nlev);
+  bp.nu1 = 2; bp.nu2 = 2; bp.nstrip = nstrip;
+  size_t smem = sizeof(double) * bot_smem_doubles(m0, nlev, nstrip, cs);
   cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_bottom, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs);
+  cfg.blockDim = dim3(KC_BOT_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at; cfg.numAttrs = 1;
   int zero = 0;
   for (int rep = 0; rep < 2; ++rep) {
     cudaMemcpyToSymbol(kc_bot_trace_n, &zero, sizeof(int));
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    k_bottom<<<1, KC_BOT_THREADS, smem>>>(bp, m0);
+    cudaLaunchKernelEx(&cfg, k_bottom, bp, m0);
     cudaEventRecord(e1);
     cudaError_t err = cudaDeviceSynchronize();
     float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -48,8 +61,8 @@ int main(int argc, char** argv) {
   cudaMemcpyFromSymbol(op.data(), kc_bot_trace_op, n * 4);
   double sum[16][8] = {}; int cnt[16][8] = {};
   for (int i = 0; i + 1 < n; ++i) { int o = op[i] / 16, d = op[i] % 16; sum[o][d] += t[i + 1] - t[i]; cnt[o][d]++; }
-  const char* nm[9] = {"jacobi", "resid", "restrict", "prolong", "join", "j2z", "rr", "pj", "tiny"};
-  for (int o = 0; o < 9; ++o) for (int d = 0; d < nlev; ++d) if (cnt[o][d])
+  const char* nm[10] = {"jacobi", "resid", "restrict", "prolong", "join", "j2z", "rr", "pj", "tiny", "csync"};
+  for (int o = 0; o < 10; ++o) for (int d = 0; d < nlev; ++d) if (cnt[o][d])
     printf("  %-9s level %d (m=%2d): %5d phases, %7.0f cycles avg, %9.0f total\n", nm[o], d, bot_m(m0, d), cnt[o][d], sum[o][d] / cnt[o][d], sum[o][d]);
   printf("phases traced: %d, total cycles %lld\n", n, n > 1 ? t[n - 1] - t[0] : 0);
   return 0;
