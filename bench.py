@@ -402,7 +402,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
-            traffic = json.load(fh).get("k_jacobi_level1_bytes_per_launch")
+            traffic = json.load(fh).get("k_pre_level1_bytes_per_launch")
     per_level = {}
     for p in prof:
         per_level.setdefault(str(p["level"]), 0.0)

@@ -52,7 +52,9 @@
 // the graph's tile kernels.
 #define KC_BOT_MAX_M 63
 #define KC_CLU_MAX_M 255
+#ifndef KC_CLU_MIN_STRIP
 #define KC_CLU_MIN_STRIP 31
+#endif
 #define KC_BOT_MAXLEV 8
 #define KC_BOT_THREADS 512
 #define KC_BOT_WARPS (KC_BOT_THREADS / 32)
@@ -134,7 +136,9 @@ enum BotOp {
   PH_JACOBI = 0, PH_RESID = 1, PH_RESTRICT = 2, PH_PROLONG = 3, PH_JOIN = 4, PH_J2Z = 5, PH_RR = 6, PH_PJ = 7,
   PH_TINY = 8, PH_CSYNC = 9
 };
-#define KC_BOT_TINY_M 7  // frames on sides <= this run as PH_TINY
+#ifndef KC_BOT_TINY_M
+#define KC_BOT_TINY_M 7  // frames on sides <= this run as PH_TINY (one warp; 15 measured slower)
+#endif
 #define KC_BOT_FUSE_M 15  // PH_RR / PH_PJ on sides <= this (latency-bound levels)
 // Descriptor: bits 0-3 op, 4-6 level d, 7 src buffer, 8 zero guess, 9 child
 // buffer (prolong), 10 child is the 1x1 coarsest (restrict), 11-12 warp
@@ -431,18 +435,32 @@ struct BotTiny {
     down(d, L, st, cur, vz, true);
     up(d, L, st, cur, vz, 0);
   }
-  __device__ void frame(int d, int kap, int nlev, int& cur, int& vz) const {
-    if (d + 2 == nlev) {
-      leaf(d, cur, vz);
-      return;
-    }
-    // side 7: children are side-3 leaves (kappa only sets how many)
+  // side 7: children are side-3 leaves (kappa only sets how many)
+  __device__ __forceinline__ void frame7(int d, int kap, int& cur, int& vz) const {
     const BotLv L = lv[d];
     const St9 st = tab[d];
     down(d, L, st, cur, vz, false);
     int cc = 0, cz = 1;
     leaf(d + 1, cc, cz);
     if (kap > 1) leaf(d + 1, cc, cz);
+    up(d, L, st, cur, vz, cc);
+  }
+  __device__ void frame(int d, int kap, int nlev, int& cur, int& vz) const {
+    if (d + 2 == nlev) {
+      leaf(d, cur, vz);
+      return;
+    }
+    if (d + 3 == nlev) {
+      frame7(d, kap, cur, vz);
+      return;
+    }
+    // side 15: children are side-7 frames with kappa and kappa - 1 (cycle.py:215-218)
+    const BotLv L = lv[d];
+    const St9 st = tab[d];
+    down(d, L, st, cur, vz, false);
+    int cc = 0, cz = 1;
+    frame7(d + 1, kap, cc, cz);
+    if (kap > 1) frame7(d + 1, kap - 1, cc, cz);
     up(d, L, st, cur, vz, cc);
   }
 };

@@ -70,19 +70,26 @@ def main():
     obs = [(kv(r["kappa"]), r["levels"], r["mean_ms"]) for r in rows]
     alpha, beta = cm.fit_params(obs, nu=nu)
     params = cm.CostModelParams(alpha=max(alpha, 0.0), beta=max(beta, 0.0), nu=nu)
-    # the engine's own cost structure: graph kernels, routine calls executed
-    # inside the persistent bottom kernel (sides <= 63), and op units
+    # the engine's own cost structure: graph kernels; routine calls executed
+    # inside the persistent bottom kernel, split into the cluster-strip levels
+    # (sides 31..255: cluster barriers) and the CTA-0 levels (sides <= 15);
+    # and op units (HBM work)
     for r in rows:
         k, n = kv(r["kappa"]), r["levels"]
-        r["bottom_calls"] = sum(cm.level_calls(k, l) for l in range(1, n + 1) if 2 ** (n - l + 1) - 1 <= 63)
-    A = np.array([[r["engine_launches"], r["bottom_calls"], r["op_units"]] for r in rows], float)
+        side = lambda l: 2 ** (n - l + 1) - 1  # noqa: E731
+        r["bottom_strip_calls"] = sum(cm.level_calls(k, l) for l in range(1, n + 1) if 31 <= side(l) <= 255)
+        r["bottom_local_calls"] = sum(cm.level_calls(k, l) for l in range(1, n + 1) if 1 < side(l) <= 15)
+    A = np.array([[r["engine_launches"], r["bottom_strip_calls"], r["bottom_local_calls"], r["op_units"]] for r in rows],
+                 float)
     y = np.array([r["mean_ms"] for r in rows], float)
-    (alpha_e, gamma_e, beta_e), *_ = np.linalg.lstsq(A, y, rcond=None)
+    # relative least squares (cells span 4 decades of time)
+    (alpha_e, gs_e, gl_e, beta_e), *_ = np.linalg.lstsq(A / y[:, None], np.ones_like(y), rcond=None)
     for r in rows:
         k, n = kv(r["kappa"]), r["levels"]
         r["predicted_ms"] = cm.predict_runtime(params, k, n)
         r["rel_error"] = (r["predicted_ms"] - r["mean_ms"]) / r["mean_ms"]
-        r["predicted_ms_engine"] = alpha_e * r["engine_launches"] + gamma_e * r["bottom_calls"] + beta_e * r["op_units"]
+        r["predicted_ms_engine"] = (alpha_e * r["engine_launches"] + gs_e * r["bottom_strip_calls"]
+                                    + gl_e * r["bottom_local_calls"] + beta_e * r["op_units"])
         r["rel_error_engine"] = (r["predicted_ms_engine"] - r["mean_ms"]) / r["mean_ms"]
     tps = {}
     for k in KAPPAS:
@@ -99,9 +106,10 @@ def main():
                 % (a.nmin, a.nmax, a.reps),
         "fit_reference_accounting": {"alpha_ms_per_launch": alpha, "beta_ms_per_op_unit": beta,
                                      "max_abs_rel_error": max(abs(r["rel_error"]) for r in rows)},
-        "fit_engine_accounting": {"model": "T = a*graph_kernels + g*bottom_routine_calls + b*op_units",
-                                  "a_ms_per_kernel": float(alpha_e), "g_ms_per_bottom_call": float(gamma_e),
-                                  "b_ms_per_op_unit": float(beta_e),
+        "fit_engine_accounting": {"model": "T = a*graph_kernels + gs*strip_level_calls + gl*cta0_level_calls"
+                                           " + b*op_units (relative least squares)",
+                                  "a_ms_per_kernel": float(alpha_e), "gs_ms_per_strip_call": float(gs_e),
+                                  "gl_ms_per_cta0_call": float(gl_e), "b_ms_per_op_unit": float(beta_e),
                                   "max_abs_rel_error": max(abs(r["rel_error_engine"]) for r in rows)},
         "paper_gtx1060": {"alpha": 2.48e-3, "beta": 1.18e-6},
         "turning_points": tps,
