@@ -415,9 +415,62 @@ def gen_costmodel():
     dump("costmodel.json", out)
 
 
+CLI_CASES = [
+    ["calls", "--kappa", "3", "--levels", "5"],
+    ["calls", "--kappa", "inf", "--levels", "12"],
+    ["predict", "--alpha", "0.00248", "--beta", "1.18e-6", "--kappa", "2", "--levels", "10"],
+    ["predict", "--alpha", "0.00028", "--beta", "2e-8", "--kappa", "inf", "--levels", "12", "--nu", "2"],
+    ["turning-point", "--alpha", "0.00248", "--beta", "1.18e-6", "--kappa", "inf"],
+    ["turning-point", "--alpha", "0.0", "--beta", "1.18e-6", "--kappa", "2"],
+    ["bench", "--kappa", "1,2,inf", "--levels", "4-6", "--reps", "0"],
+    ["solve", "--levels", "7", "--kappa", "1", "--eps", "1e-4", "--phi", "45"],
+    ["solve", "--levels", "6", "--kappa", "2", "--eps", "1e-4", "--phi", "45", "--solver", "pcg"],
+    ["solve", "--levels", "5", "--kappa", "inf", "--eps", "0.1", "--phi", "30", "--out", "csv"],
+    ["solve", "--levels", "5", "--kappa", "2", "--eps", "1e-4", "--phi", "45", "--max-cycles", "3"],
+]
+CLI_FIT_INPUT = "kappa,levels,ms\n1,4,0.1\n2,5,0.3\n3,6,0.9\ninf,7,2.5\n"
+
+
+def gen_cli():
+    """The reference CLI (cli.py) on fixed argument lists: stdout and exit
+    code; solve records without the run-dependent fields (wall_ms,
+    timestamp, version)."""
+    import contextlib
+    import io
+    from kcycle import cli
+    out = []
+    cases = [(c, None) for c in CLI_CASES] + [(["fit"], CLI_FIT_INPUT)]
+    for argv, stdin in cases:
+        buf = io.StringIO()
+        old_in = sys.stdin
+        if stdin is not None:
+            sys.stdin = io.StringIO(stdin)
+        try:
+            with contextlib.redirect_stdout(buf):
+                rc = cli.main(argv)
+        finally:
+            sys.stdin = old_in
+        text = buf.getvalue()
+        rec = {"argv": argv, "stdin": stdin, "exit": rc}
+        if argv[0] == "solve" and "--out" not in argv:
+            d = json.loads(text)
+            d["result"].pop("wall_ms")
+            rec["record"] = {"config": d["config"], "result": d["result"]}
+        elif argv[0] == "solve":
+            hdr, row = [line.split(",") for line in text.strip().splitlines()]
+            rec["csv_header"] = hdr
+            rec["csv_row"] = dict(zip(hdr, row))
+            rec["csv_row"].pop("wall_ms")
+        else:
+            rec["stdout"] = text
+        out.append(rec)
+        print(argv, rc, flush=True)
+    dump("cli.json", out)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["small", "solve", "pcg", "costmodel"])
+    ap.add_argument("what", choices=["small", "solve", "pcg", "costmodel", "cli"])
     ap.add_argument("--n", type=int, default=12)
     ap.add_argument("--kappa", default="1")
     ap.add_argument("--cap", type=int, default=20000)
@@ -425,6 +478,9 @@ def main():
     print("reference kcycle", kcycle.__version__, "numpy", np.__version__, flush=True)
     if a.what == "costmodel":
         gen_costmodel()
+        return
+    if a.what == "cli":
+        gen_cli()
         return
     if a.what == "small":
         gen_stencils()
