@@ -126,6 +126,8 @@ struct kc_handle {
   double* h_scal = nullptr;     // pinned host mirror
   std::map<std::tuple<int, int, int, int>, GraphEntry> graphs;  // (kappa, cur0, vzero0, norms)
   std::map<std::pair<int, int>, SolveGraph> solve_graphs;       // (kappa, cur0)
+  std::map<std::tuple<int, int, int>, SolveGraph> pcg_graphs;   // (kappa, measure x, cur0)
+  PcgState* d_pcg = nullptr;
   double* d_npart = nullptr;  // norm partials of the fused level-1 kernels (per warp: post; per lane: pre)
   double* d_nblk = nullptr;    // block sums of k_norms_lanes
   unsigned* d_ncount = nullptr;
@@ -405,9 +407,10 @@ KsFn ks_pre_fn(int nu, bool zero, bool norms = false) {
 #undef KS_PRE
   return nullptr;
 }
-KsFn ks_post_fn(int nu, bool vz, bool norms) {
-#define KS_POST(N) \
-  return vz ? (norms ? k_post<N, true, true> : k_post<N, true, false>) : (norms ? k_post<N, false, true> : k_post<N, false, false>)
+KsFn ks_post_fn(int nu, bool vz, int nm) {
+#define KS_POST(N)                                                                            \
+  return vz ? (nm == 1 ? k_post<N, true, 1> : nm == 2 ? k_post<N, true, (N > 0 ? 2 : 0)> : k_post<N, true, 0>) \
+            : (nm == 1 ? k_post<N, false, 1> : nm == 2 ? k_post<N, false, (N > 0 ? 2 : 0)> : k_post<N, false, 0>)
   switch (nu) {
     case 0: KS_POST(0);
     case 1: KS_POST(1);
@@ -527,7 +530,7 @@ int ex_pre(kc_handle* h, int l, bool norms = false) {
   KC_LAUNCH_CHECK(h);
   ++h->launches;
   if (norms) {
-    k_norms_lanes<<<KS_NB, 256, 0, h->stream>>>(reinterpret_cast<const double2*>(h->d_npart), nw * 32,
+    k_norms_lanes<true><<<KS_NB, 256, 0, h->stream>>>(reinterpret_cast<const double2*>(h->d_npart), nw * 32,
                                                  reinterpret_cast<double2*>(h->d_nblk), h->d_ncount, h->d_scal);
     KC_LAUNCH_CHECK(h);
     ++h->launches;
@@ -539,28 +542,38 @@ int ex_pre(kc_handle* h, int l, bool norms = false) {
   return KC_OK;
 }
 
-// prolong_add + relax(nu2) (cycle.py:219-220), optionally with the norms of
-// the result (||v||, ||f - A v|| into d_scal[0], d_scal[1])
-int ex_post(kc_handle* h, int l, bool norms) {
+// prolong_add + relax(nu2) (cycle.py:219-220); nm = 1: with the norms of
+// the result (||v||, ||f - A v|| into d_scal[0], d_scal[1]); nm = 2: with
+// f . v into d_scal[S_RZN] (PCG rz of a preconditioning cycle, nu2 >= 1)
+enum { S_RZ = 2, S_PAP = 3, S_MEAS = 4, S_RZN = 5 };
+int ex_post(kc_handle* h, int l, int nm) {
   Level& L = h->L[l];
   Level& C = h->L[l + 1];
   int rc = ex_materialize(h, l + 1);
   if (rc) return rc;
-  if (L.m <= KC_TILE_MAX_M && h->tile && !norms) return ex_tile(h, l, false);
+  if (nm == 2 && h->nu2 < 1) KC_FAIL(h, KC_EINVAL, "fused r.z needs nu2 >= 1");
+  if (L.m <= KC_TILE_MAX_M && h->tile && !nm) return ex_tile(h, l, false);
   int nw = 0;
-  const int D = h->nu2 + (norms ? 1 : 0);
-  KsFn fn = ks_post_fn(h->nu2, L.vzero, norms);
+  const int D = h->nu2 + (nm == 1 ? 1 : 0);
+  KsFn fn = ks_post_fn(h->nu2, L.vzero, nm);
   StreamParams p = ks_params(h, l, D > 0 ? D : 1, &nw, (const void*)fn);
   p.vc = C.v[C.cur];
-  if (norms) {
-    if (nw > h->npart_cap) KC_FAIL(h, KC_EINVAL, "norm partial buffer too small (%d < %d)", h->npart_cap, nw);
+  if (nm) {
+    const int need = nm == 2 ? 32 * nw : nw;
+    if (need > h->npart_cap) KC_FAIL(h, KC_EINVAL, "norm partial buffer too small (%d < %d)", h->npart_cap, need);
     p.part = h->d_npart;
   }
   fn<<<(nw + 3) / 4, 128, KS_SMEM_BYTES, h->stream>>>(p);
   KC_LAUNCH_CHECK(h);
   ++h->launches;
-  if (norms) {
+  if (nm == 1) {
     k_norms_final<<<1, 256, 0, h->stream>>>(h->d_npart, nw, h->d_scal);
+    KC_LAUNCH_CHECK(h);
+    ++h->launches;
+  } else if (nm == 2) {
+    k_norms_lanes<false><<<KS_NB, 256, 0, h->stream>>>(reinterpret_cast<const double2*>(h->d_npart), nw * 32,
+                                                        reinterpret_cast<double2*>(h->d_nblk), h->d_ncount,
+                                                        h->d_scal + S_RZN);
     KC_LAUNCH_CHECK(h);
     ++h->launches;
   }
@@ -572,7 +585,7 @@ int ex_post(kc_handle* h, int l, bool norms) {
 int ex_op(kc_handle* h, const Op& op) {
   switch (op.kind) {
     case OP_PRE: return ex_pre(h, op.level, op.b != 0);
-    case OP_POST: return ex_post(h, op.level, op.b != 0);
+    case OP_POST: return ex_post(h, op.level, op.b);
     case OP_RELAX: return ex_relax(h, op.level, op.a);
     case OP_RESTRICT: return ex_restrict(h, op.level);
     case OP_ZERO: h->L[op.level].vzero = true; return KC_OK;
@@ -591,7 +604,8 @@ bool fusable(const kc_handle* h, int l) {
 // asks the level-0 post-smoothing of this call to also produce ||v|| and
 // ||f - A v|| (the stand-alone stopping test) inside the cycle.
 // norms: 0 none, 1 after the cycle (fused into the level-0 post), 2 of the
-// cycle's input (fused into the level-0 pre; the device solve loop).
+// cycle's input (fused into the level-0 pre; the device solve loop), 3 the
+// PCG r . z of a preconditioning cycle (fused into the level-0 post).
 void flatten(const kc_handle* h, int l, int kappa, std::vector<Op>& ops, int norms = 0) {
   const int n = h->n;
   if (l == h->Lb) {
@@ -623,7 +637,7 @@ void flatten(const kc_handle* h, int l, int kappa, std::vector<Op>& ops, int nor
     }
   }
   if (fu) {
-    ops.push_back({OP_POST, l, 0, norms == 1 ? 1 : 0});
+    ops.push_back({OP_POST, l, 0, norms == 1 ? 1 : (norms == 3 ? 2 : 0)});
   } else {
     ops.push_back({OP_PROLONG, l, 0, 0});
     ops.push_back({OP_RELAX, l, h->nu2, 0});
@@ -633,17 +647,19 @@ void flatten(const kc_handle* h, int l, int kappa, std::vector<Op>& ops, int nor
 // true when flatten(norms=true) leaves ||v||, ||f-Av|| in d_scal[0..1]
 bool cycle_has_norms(const kc_handle* h) { return h->Lb != 0 && fusable(h, 0); }
 
-int get_cycle_graph(kc_handle* h, int kappa, GraphEntry** out, bool norms = false) {
+// norms: 0 plain, 1 with the result's norms, 3 with the PCG r . z (flatten)
+int get_cycle_graph(kc_handle* h, int kappa, GraphEntry** out, int norms = 0) {
   Level& L0 = h->L[0];
-  norms = norms && cycle_has_norms(h);
-  auto key = std::make_tuple(kappa, L0.cur, L0.vzero ? 1 : 0, norms ? 1 : 0);
+  if (norms && !cycle_has_norms(h)) norms = 0;
+  if (norms == 3 && h->nu2 < 1) norms = 0;
+  auto key = std::make_tuple(kappa, L0.cur, L0.vzero ? 1 : 0, norms);
   auto it = h->graphs.find(key);
   if (it != h->graphs.end()) {
     *out = &it->second;
     return KC_OK;
   }
   std::vector<Op> ops;
-  flatten(h, 0, kappa, ops, norms ? 1 : 0);
+  flatten(h, 0, kappa, ops, norms);
   // coarse levels start every cycle logically overwritten (zero_guess precedes use)
   std::vector<int> save_cur(h->n);
   std::vector<char> save_vz(h->n);
@@ -686,7 +702,7 @@ int get_cycle_graph(kc_handle* h, int kappa, GraphEntry** out, bool norms = fals
   return KC_OK;
 }
 
-int run_cycle_graph(kc_handle* h, int kappa, bool norms = false) {
+int run_cycle_graph(kc_handle* h, int kappa, int norms = 0) {
   GraphEntry* g = nullptr;
   int rc = get_cycle_graph(h, kappa, &g, norms);
   if (rc) return rc;
@@ -714,6 +730,14 @@ void drop_graphs(kc_handle* h) {
     if (g.rest) cudaGraphDestroy(g.rest);
   }
   h->solve_graphs.clear();
+  for (auto& kv : h->pcg_graphs) {
+    SolveGraph& g = kv.second;
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+    if (g.pre) cudaGraphDestroy(g.pre);
+    if (g.rest) cudaGraphDestroy(g.rest);
+  }
+  h->pcg_graphs.clear();
 }
 
 int capture_ops(kc_handle* h, const std::vector<Op>& ops, size_t i0, size_t i1, cudaGraph_t* out, int* kernels) {
@@ -1021,12 +1045,16 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
   if (n >= 2 && h->L[0].m >= KC_FUSE_MIN_M) {  // per-warp partials of the fused level-1 norms
     int nw = 0;
     const int D = nu2 + 1;
-    StreamParams p = ks_params(h, 0, D, &nw, (const void*)ks_post_fn(nu2, true, true));
+    StreamParams p = ks_params(h, 0, D, &nw, (const void*)ks_post_fn(nu2, true, 1));
     int nw2 = 0;
-    ks_params(h, 0, D, &nw2, (const void*)ks_post_fn(nu2, false, true));
+    ks_params(h, 0, D, &nw2, (const void*)ks_post_fn(nu2, false, 1));
     nw = nw > nw2 ? nw : nw2;
     ks_params(h, 0, nu1 + 1, &nw2, (const void*)ks_pre_fn(nu1, false, true));
     nw = nw > 32 * nw2 ? nw : 32 * nw2;  // the pre kernel leaves per-lane partials
+    if (nu2 >= 1) {
+      ks_params(h, 0, nu2, &nw2, (const void*)ks_post_fn(nu2, false, 2));
+      nw = nw > 32 * nw2 ? nw : 32 * nw2;
+    }
     (void)p;
     h->npart_cap = nw;
     if (cudaMalloc(&h->d_nblk, sizeof(double) * 2 * KS_NB) != cudaSuccess ||
@@ -1047,6 +1075,7 @@ int kc_destroy(kc_handle* h) {
   drop_graphs(h);
   cudaFree(h->d_solve);
   cudaFree(h->d_hist);
+  cudaFree(h->d_pcg);
   for (Level& L : h->L) {
     cudaFree(L.v[0]);
     cudaFree(L.v[1]);
@@ -1460,8 +1489,6 @@ int download_interior(kc_handle* h, double* host, const double* src) {
   return KC_OK;
 }
 
-enum { S_RZ = 2, S_PAP = 3, S_MEAS = 4, S_RZN = 5 };
-
 // z = M^-1 r into L0.v[cur]; r lives in L0.f (krylov.py:81-86)
 int pcg_precondition(kc_handle* h, int kappa, kc_precond_fn fn, void* ctx, std::vector<double>& hr,
                      std::vector<double>& hz) {
@@ -1480,6 +1507,98 @@ int pcg_precondition(kc_handle* h, int kappa, kc_precond_fn fn, void* ctx, std::
 }
 }  // namespace
 
+namespace {
+// The whole PCG loop of krylov.py:100-130 in one graph launch:
+//   WHILE { Ap = A p, pAp ; x += alpha p, r -= alpha Ap, measure ; k_pcg_check ;
+//           IF { z = M r (the cycle graph, r . z fused into its last kernel) ;
+//                p = z + beta p ; rz = rz_next } }
+// r lives in L0.f and z in the finest v buffer, as in the host loop.
+int get_pcg_graph(kc_handle* h, int kappa, bool mx, SolveGraph** out) {
+  Level& L0 = h->L[0];
+  const auto key = std::make_tuple(kappa, mx ? 1 : 0, L0.cur);
+  auto it = h->pcg_graphs.find(key);
+  if (it != h->pcg_graphs.end()) {
+    *out = &it->second;
+    return KC_OK;
+  }
+  const int m = L0.m, P = L0.P;
+  if (!h->d_pcg) KC_CUDA(h, cudaMalloc(&h->d_pcg, sizeof(PcgState)));
+  // the preconditioning cycle (z = M r from a zero guess, r . z fused)
+  const int cur0 = L0.cur;
+  const bool vz0 = L0.vzero;
+  L0.vzero = true;
+  GraphEntry* g = nullptr;
+  int rc = get_cycle_graph(h, kappa, &g, 3);
+  L0.vzero = vz0;
+  if (rc) return rc;
+  if (g->end_cur0 != cur0) KC_FAIL(h, KC_EINVAL, "preconditioning cycle does not return to its buffer");
+  const double* z = L0.v[cur0];
+  double* r = L0.f;
+  PcgState* st = h->d_pcg;
+  SolveGraph sg;
+  // A: Ap, pAp, x/r update, measure
+  KC_CUDA(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  k_pcg_apply_dot<<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(h->p, h->ap, m, P, L0.st, h->d_part);
+  k_red_final<false><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_part, KC_RED_BLOCKS, h->d_scal + S_PAP);
+  if (mx)
+    k_pcg_update_xr<true><<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(h->x, r, h->p, h->ap, m, P, h->d_scal, S_RZ,
+                                                                            S_PAP, h->d_part, st);
+  else
+    k_pcg_update_xr<false><<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(h->x, r, h->p, h->ap, m, P, h->d_scal,
+                                                                             S_RZ, S_PAP, h->d_part, st);
+  k_red_final<true><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_part, KC_RED_BLOCKS, h->d_scal + S_MEAS);
+  cudaError_t ce = cudaStreamEndCapture(h->stream, &sg.pre);
+  if (ce != cudaSuccess) KC_FAIL(h, KC_ECUDA, "PCG capture: %s", cudaGetErrorString(ce));
+  // tail of the body: p = z + beta p ; rz = rz_next
+  KC_CUDA(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  k_pcg_update_p<<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(h->p, z, m, P, h->d_scal, S_RZN, S_RZ);
+  k_copy_scalar<<<1, 32, 0, h->stream>>>(h->d_scal, S_RZ, S_RZN);
+  ce = cudaStreamEndCapture(h->stream, &sg.rest);
+  if (ce != cudaSuccess) KC_FAIL(h, KC_ECUDA, "PCG capture: %s", cudaGetErrorString(ce));
+  sg.kernels_pre = 4;
+  sg.kernels_rest = g->kernels + 2;
+  cudaGraph_t cg = nullptr;
+  KC_CUDA(h, cudaGraphCreate(&cg, 0));
+  cudaGraphConditionalHandle h_loop, h_body;
+  KC_CUDA(h, cudaGraphConditionalHandleCreate(&h_loop, cg, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams wp{};
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = h_loop;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  cudaGraphNode_t wn;
+  KC_CUDA(h, cudaGraphAddNode(&wn, cg, nullptr, 0, &wp));
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+  KC_CUDA(h, cudaGraphConditionalHandleCreate(&h_body, body, 0, cudaGraphCondAssignDefault));
+  cudaGraphNode_t a_node, chk_node, if_node, cyc_node, tail_node;
+  KC_CUDA(h, cudaGraphAddChildGraphNode(&a_node, body, nullptr, 0, sg.pre));
+  const double* scal = h->d_scal;
+  int s_rz = S_RZ, s_pap = S_PAP, s_meas = S_MEAS;
+  void* args[] = {&h_loop, &h_body, &st, &scal, &s_rz, &s_pap, &s_meas};
+  cudaKernelNodeParams kp{};
+  kp.func = (void*)k_pcg_check;
+  kp.gridDim = dim3(1);
+  kp.blockDim = dim3(32);
+  kp.kernelParams = args;
+  KC_CUDA(h, cudaGraphAddKernelNode(&chk_node, body, &a_node, 1, &kp));
+  cudaGraphNodeParams ip{};
+  ip.type = cudaGraphNodeTypeConditional;
+  ip.conditional.handle = h_body;
+  ip.conditional.type = cudaGraphCondTypeIf;
+  ip.conditional.size = 1;
+  KC_CUDA(h, cudaGraphAddNode(&if_node, body, &chk_node, 1, &ip));
+  cudaGraph_t ifb = ip.conditional.phGraph_out[0];
+  KC_CUDA(h, cudaGraphAddChildGraphNode(&cyc_node, ifb, nullptr, 0, g->graph));
+  KC_CUDA(h, cudaGraphAddChildGraphNode(&tail_node, ifb, &cyc_node, 1, sg.rest));
+  KC_CUDA(h, cudaGraphInstantiate(&sg.exec, cg, 0));
+  sg.graph = cg;
+  sg.end_cur0 = cur0;
+  auto ins = h->pcg_graphs.emplace(key, sg);
+  *out = &ins.first->second;
+  return KC_OK;
+}
+}  // namespace
+
 extern "C" int kc_pcg(kc_handle* h, int kappa, const double* f, const double* x0, int stop_mode,
                       double target_reduction, int max_it, kc_precond_fn precond, void* ctx, double* hist,
                       int* iterations, int* status, int* n_precond, double* x_out, double* device_ms) {
@@ -1493,9 +1612,22 @@ extern "C" int kc_pcg(kc_handle* h, int kappa, const double* f, const double* x0
   Level& L0 = h->L[0];
   const int m = L0.m, P = L0.P;
   std::vector<double> hr, hz;
+  const bool mx = stop_mode == KC_STOP_ERROR;
+  // the whole loop on the device when the preconditioner is the native cycle
+  // and the fused kernels apply (r . z fused into the cycle's last kernel)
+  const bool device_loop = !precond && cycle_has_norms(h) && h->nu2 >= 1 && max_it > 0;
+  SolveGraph* pg = nullptr;
   if (precond) {
     hr.resize((size_t)m * m);
     hz.resize((size_t)m * m);
+  } else if (device_loop) {  // setup outside the timed span
+    if ((rc = get_pcg_graph(h, kappa, mx, &pg))) return rc;
+    if (max_it + 1 > h->hist_cap) {
+      cudaFree(h->d_hist);
+      h->d_hist = nullptr;
+      KC_CUDA(h, cudaMalloc(&h->d_hist, sizeof(double) * 2 * (size_t)(max_it + 1)));
+      h->hist_cap = max_it + 1;
+    }
   } else {
     GraphEntry* g = nullptr;  // capture both level-1 states up front (setup)
     if ((rc = get_cycle_graph(h, kappa, &g))) return rc;
@@ -1507,7 +1639,6 @@ extern "C" int kc_pcg(kc_handle* h, int kappa, const double* f, const double* x0
     KC_CUDA(h, cudaMemsetAsync(h->x, 0, L0.elems * sizeof(double), h->stream));
   }
   KC_CUDA(h, cudaStreamSynchronize(h->stream));
-  const bool mx = stop_mode == KC_STOP_ERROR;
   double* r = L0.f;
   int napp = 0;
   KC_CUDA(h, cudaEventRecord(h->ev0, h->stream));
@@ -1522,6 +1653,30 @@ extern "C" int kc_pcg(kc_handle* h, int kappa, const double* f, const double* x0
   double cur = norm0;
   if (norm0 <= target) {
     st = KC_STATUS_CONVERGED;
+  } else if (device_loop) {
+    L0.vzero = true;  // z = M r from the zero guess, r . z into S_RZN
+    if ((rc = run_cycle_graph(h, kappa, 3))) return rc;
+    KC_CUDA(h, cudaMemcpyAsync(h->p, L0.v[L0.cur], L0.elems * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    k_copy_scalar<<<1, 32, 0, h->stream>>>(h->d_scal, S_RZ, S_RZN);
+    KC_LAUNCH_CHECK(h);
+    PcgState ps{};
+    ps.target = target;
+    ps.max_it = max_it;
+    ps.status = KC_STATUS_MAX_CYCLES;
+    ps.napp = 1;
+    ps.hist = h->d_hist;
+    KC_CUDA(h, cudaMemcpyAsync(h->d_pcg, &ps, sizeof(ps), cudaMemcpyHostToDevice, h->stream));
+    KC_CUDA(h, cudaGraphLaunch(pg->exec, h->stream));
+    KC_CUDA(h, cudaMemcpyAsync(&ps, h->d_pcg, sizeof(ps), cudaMemcpyDeviceToHost, h->stream));
+    KC_CUDA(h, cudaStreamSynchronize(h->stream));
+    it = ps.it;
+    st = ps.status;
+    napp = ps.napp;
+    if (hist && it > 0) KC_CUDA(h, cudaMemcpy(hist + 1, h->d_hist + 1, sizeof(double) * it, cudaMemcpyDeviceToHost));
+    for (int j = 1; j < h->n; ++j) {  // coarse levels are scratch after the cycles
+      h->L[j].vzero = true;
+      h->L[j].cur = 0;
+    }
   } else {
     if ((rc = pcg_precondition(h, kappa, precond, ctx, hr, hz))) return rc;
     ++napp;
@@ -1538,10 +1693,11 @@ extern "C" int kc_pcg(kc_handle* h, int kappa, const double* f, const double* x0
         KC_LAUNCH_CHECK(h);
         if (mx)
           k_pcg_update_xr<true><<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(h->x, r, h->p, h->ap, m, P, h->d_scal,
-                                                                                  S_RZ, S_PAP, h->d_part);
+                                                                                  S_RZ, S_PAP, h->d_part, nullptr);
         else
           k_pcg_update_xr<false><<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(h->x, r, h->p, h->ap, m, P,
-                                                                                   h->d_scal, S_RZ, S_PAP, h->d_part);
+                                                                                   h->d_scal, S_RZ, S_PAP, h->d_part,
+                                                                                   nullptr);
         KC_LAUNCH_CHECK(h);
         k_red_final<true><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_part, KC_RED_BLOCKS, h->d_scal + S_MEAS);
         KC_LAUNCH_CHECK(h);

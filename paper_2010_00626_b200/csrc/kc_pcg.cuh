@@ -41,15 +41,26 @@ __global__ void __launch_bounds__(KC_RED_THREADS)
   if (threadIdx.x == 0) part[blockIdx.x] = t;
 }
 
+// Device-resident PCG loop state (kc_engine.cu get_pcg_graph): iterations
+// completed, limits, outcome, history of the stopping measure.
+struct PcgState {
+  double target;
+  int it, max_it, status, napp;
+  double* hist;
+};
+
 // x += alpha p ; r -= alpha ap ; partial = sum (x^2 | r^2)  (krylov.py:114-117)
+// With a loop state the update also waits for the previous iteration's
+// checks to pass (rz > 0, budget left), which k_pcg_check evaluates after it.
 template <bool MEASURE_X>
 __global__ void __launch_bounds__(KC_RED_THREADS)
     k_pcg_update_xr(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
                     const double* __restrict__ ap, int m, int P, const double* __restrict__ scal, int s_rz,
-                    int s_pap, double* __restrict__ part) {
+                    int s_pap, double* __restrict__ part, const PcgState* __restrict__ st) {
   const double pap = scal[s_pap];
   double acc = 0.0;
-  if (pap > 0.0) {
+  const bool go = pap > 0.0 && (!st || (scal[s_rz] > 0.0 && st->it < st->max_it));
+  if (go) {
     const double alpha = __ddiv_rn(scal[s_rz], pap);
     for (int y = blockIdx.x; y < m; y += gridDim.x)
       for (int xx = threadIdx.x; xx < m; xx += KC_RED_THREADS) {
@@ -81,4 +92,37 @@ __global__ void __launch_bounds__(KC_RED_THREADS)
 
 __global__ void k_copy_scalar(double* __restrict__ scal, int dst, int src) {
   if (threadIdx.x == 0) scal[dst] = scal[src];
+}
+
+// Stopping logic of one device PCG iteration (krylov.py:100-130), run after
+// the x/r update: rz (from the previous preconditioning) must be positive,
+// the budget not exhausted, pAp positive; then the measure is recorded and
+// compared with the target.  Sets the loop and body conditions.
+__global__ void k_pcg_check(cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_body,
+                            PcgState* __restrict__ st, const double* __restrict__ scal, int s_rz, int s_pap,
+                            int s_meas) {
+  if (threadIdx.x != 0) return;
+  unsigned go = 0u;
+  if (!(scal[s_rz] > 0.0)) {
+    st->status = KC_STATUS_BREAKDOWN;
+  } else if (st->it >= st->max_it) {
+    st->status = KC_STATUS_MAX_CYCLES;
+  } else {
+    const int it = st->it + 1;
+    st->it = it;
+    if (!(scal[s_pap] > 0.0)) {
+      st->status = KC_STATUS_BREAKDOWN;
+    } else {
+      const double meas = scal[s_meas];
+      st->hist[it] = meas;
+      if (meas <= st->target) {
+        st->status = KC_STATUS_CONVERGED;
+      } else {
+        go = 1u;
+        st->napp += 1;
+      }
+    }
+  }
+  cudaGraphSetConditional(h_loop, go);
+  cudaGraphSetConditional(h_body, go);
 }

@@ -246,8 +246,13 @@ __global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
 // ---------------------------------------------------------------------------
 // POST: v + P vc, NU sweeps, optional fused norms of the result
 // ---------------------------------------------------------------------------
-template <int NU, bool VZ, bool NORMS>
+// NM = 0: plain; 1: ||v'||^2 and ||f - A v'||^2 (one extra residual stage,
+// per-warp partials); 2: f . v' (the PCG rz = r . z of a preconditioning
+// cycle, whose f is r and whose result is z; per-lane partials, NU >= 1).
+template <int NU, bool VZ, int NM>
 __global__ void __launch_bounds__(128, 4) k_post(const StreamParams p) {
+  constexpr bool NORMS = NM == 1, DOT = NM == 2;
+  static_assert(!DOT || NU >= 1, "the f . v partials use the f row of the last sweep");
   constexpr int D = NU + (NORMS ? 1 : 0);
   constexpr int DD = D > 0 ? D : 1;
   using G = KsGeom<DD>;
@@ -257,6 +262,7 @@ __global__ void __launch_bounds__(128, 4) k_post(const StreamParams p) {
   const int P0 = band * G::NPB, Q0 = chunk * p.nq;
   double acc_e = 0.0, acc_r = 0.0;
   const bool active = Q0 <= p.mc;
+  if (DOT && !active) reinterpret_cast<double2*>(p.part)[wg * 32 + lane] = make_double2(0.0, 0.0);
   const int m = p.m, P = p.P;
   const int XS = 2 * P0 - G::HL;
   const int c0 = XS + 2 * lane;
@@ -336,6 +342,7 @@ __global__ void __launch_bounds__(128, 4) k_post(const StreamParams p) {
         if (own_lane && y >= 2 * Q0 && y < 2 * Q0 + 2 * p.nq && y >= 0 && y < m) {
           *reinterpret_cast<double2*>(p.uo + kc_idx(P, y, c0)) = nw[NU];
           if (NORMS) acc_e = fma(nw[NU].y, nw[NU].y, fma(nw[NU].x, nw[NU].x, acc_e));
+          if (DOT) acc_e = fma(fr[NU > 0 ? NU : 1].y, nw[NU].y, fma(fr[NU > 0 ? NU : 1].x, nw[NU].x, acc_e));
         }
       }
       if (NORMS) {
@@ -349,6 +356,7 @@ __global__ void __launch_bounds__(128, 4) k_post(const StreamParams p) {
         W[t][1] = W[t][2];
         W[t][2] = nw[t];
       }
+      if (DOT && yin == ye) reinterpret_cast<double2*>(p.part)[wg * 32 + lane] = make_double2(acc_e, 0.0);
     }
   }
   if (NORMS) ks_warp_partials(acc_e, acc_r, p.part, wg, lane);
@@ -384,8 +392,10 @@ __global__ void __launch_bounds__(256) k_norms_final(const double* __restrict__ 
 }
 
 // Deterministic sum of n (a, b) pairs over KS_NB blocks; the last block to
-// finish adds the block sums in order: out[0] = sqrt(sum a), out[1] = sqrt(sum b).
+// finish adds the block sums in order: out = (sum a, sum b), square roots
+// taken when SQRT.
 #define KS_NB 32
+template <bool SQRT>
 __global__ void __launch_bounds__(256) k_norms_lanes(const double2* __restrict__ part, int n, double2* __restrict__ bsum,
                                                      unsigned* __restrict__ counter, double* __restrict__ out) {
   __shared__ double sh[2][8];
@@ -427,8 +437,8 @@ __global__ void __launch_bounds__(256) k_norms_lanes(const double2* __restrict__
       ta += v.x;
       tb += v.y;
     }
-    out[0] = sqrt(ta);
-    out[1] = sqrt(tb);
+    out[0] = SQRT ? sqrt(ta) : ta;
+    out[1] = SQRT ? sqrt(tb) : tb;
     *counter = 0u;
   }
 }
