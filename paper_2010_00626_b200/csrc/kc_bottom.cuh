@@ -379,6 +379,38 @@ __device__ __forceinline__ void bot_prolong(double* __restrict__ u, const double
   }
 }
 
+// Strip prolongation from a strip child without any exchange: the corrected
+// v is formed on the CTA's own rows AND its two halo rows (-1, R) from the
+// local copies of the pre-smoothed v and of the child's rows -1 .. R/2 —
+// the same arithmetic the neighbour applies to those rows, so the copies stay
+// bit-identical and the phase ends with a CTA barrier instead of a cluster
+// barrier.  Cells q = -1 .. R/2 cover fine rows 2q (from child rows q-1, q)
+// and 2q+1 (from child row q); rows outside -1 .. R or the domain are skipped.
+__device__ __forceinline__ void bot_prolong_ext(double* __restrict__ u, const double* __restrict__ vc,
+                                                const BotLv& L, int mc, int SC, bool zero, int tid, int nth) {
+  const int S = L.S;
+  const int nc = mc + 1;
+  const int n = (L.R / 2 + 2) * nc;
+  const int glo = -L.a, ghi = L.m - L.a;  // local rows inside the domain: [glo, ghi)
+  for (int i = tid; i < n; i += nth) {
+    const int qq = bot_div(i, L.invn), p = i - qq * nc;
+    const int q = qq - 1;
+    const double c10 = vc[q * SC + p - 1], c11 = vc[q * SC + p];
+    const int y = 2 * q, x = 2 * p;
+    if (q >= 0 && y <= L.R && y >= glo && y < ghi) {  // even row, transfer.py:56-57
+      const double c00 = vc[(q - 1) * SC + p - 1], c01 = vc[(q - 1) * SC + p];
+      double* pv = u + y * S + x;
+      pv[0] = DADD(zero ? 0.0 : pv[0], DMUL(0.25, DADD(DADD(DADD(c00, c01), c10), c11)));
+      if (p < mc) pv[1] = DADD(zero ? 0.0 : pv[1], DMUL(0.5, DADD(c01, c11)));
+    }
+    if (y + 1 <= L.R && y + 1 >= glo && y + 1 < ghi) {  // odd row, transfer.py:54-55
+      double* pv = u + (y + 1) * S + x;
+      pv[0] = DADD(zero ? 0.0 : pv[0], DMUL(0.5, DADD(c10, c11)));
+      if (p < mc) pv[1] = DADD(zero ? 0.0 : pv[1], c11);
+    }
+  }
+}
+
 // PH_TINY: whole kappa_cycle frames on sides <= KC_BOT_TINY_M, run by warp 0
 // alone (one __syncwarp per phase, no descriptor decode).  Follows
 // BotBuilder::rec with J2Z on, so the host's dry replay of the same rules
@@ -597,7 +629,12 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
     } else if (op == PH_PROLONG) {
       const BotLv C = lv[d + 1];
       const double* vc = sm + (BD_CBUF(e) ? C.vo1 : C.vo0);
-      if (strip && d + 1 >= nstrip)  // from CTA 0's level, at this strip's first coarse row
+      if (strip && d + 1 < nstrip) {  // halo rows formed locally: no exchange (CTA barrier below)
+        bot_prolong_ext(u, vc, L, C.m, C.S, zero, tid, nth);
+        __syncthreads();
+        continue;
+      }
+      if (strip)  // from CTA 0's level, at this strip's first coarse row
         vc = cl.map_shared_rank(const_cast<double*>(vc), 0) + (L.a / 2) * C.S;
       bot_prolong(u, vc, L, C.m, C.S, zero, tid, nth, bot_push(u, L, strip, rank, cs));
     } else {  // PH_TINY (warp 0 of CTA 0)
