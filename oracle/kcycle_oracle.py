@@ -22,6 +22,12 @@ Arithmetic contract, restated from the reference:
   * Jacobi u + (omega/center)*(f - Au)       smoother.py:95-100
   * full weighting / bilinear in numpy order  transfer.py:46-87
   * norm2 = np.linalg.norm (OpenBLAS ddot)    mesh.py:93-95
+  * zebra line relaxation (smoother.py:107-135): even lines, then odd lines,
+    each a tridiagonal solve of scipy.linalg.solve_banded((1,1)) = LAPACK
+    dgtsv (Gaussian elimination with partial pivoting), restated in `gtsv`
+    and pinned bit-exact against scipy itself (tests/test_oracle.py);
+  * y-semi-coarsening transfers and the single-line coarsest solve
+    (transfer.py:59-66, 84-86; cycle.py:191-200; smoother.py:71-92).
 """
 
 from __future__ import annotations
@@ -91,11 +97,35 @@ def restrict(r: np.ndarray) -> np.ndarray:
     return (4.0 * c + 2.0 * (s + n + wv + e) + (sw + se + nw + ne)) / 16.0
 
 
-def galerkin(w: np.ndarray) -> np.ndarray:
+def prolong_semi(c: np.ndarray) -> np.ndarray:
+    """Linear prolongation in y, y-semi-coarsening (transfer.py:59-66)."""
+    nyc, nx = c.shape
+    cp = np.zeros((nyc + 2, nx))
+    cp[1:-1, :] = c
+    out = np.zeros((2 * nyc + 1, nx))
+    out[1::2, :] = c
+    out[0::2, :] = 0.5 * (cp[:-1, :] + cp[1:, :])
+    return out
+
+
+def restrict_semi(r: np.ndarray) -> np.ndarray:
+    """Full weighting in y (transfer.py:84-86): 0.25 (S + 2 C + N)."""
+    return 0.25 * (r[0:-1:2, :] + 2.0 * r[1::2, :] + r[2::2, :])
+
+
+FULL, SEMI_Y = "full", "semi-y"
+
+
+def transfer(coarsening):
+    return (prolong, restrict) if coarsening == FULL else (prolong_semi, restrict_semi)
+
+
+def galerkin(w: np.ndarray, coarsening: str = FULL) -> np.ndarray:
     """R A P read off a 7x7 auxiliary coarse impulse (stencil.py:126-148)."""
+    pro, res = transfer(coarsening)
     imp = np.zeros((7, 7))
     imp[3, 3] = 1.0
-    resp = restrict(apply(w, prolong(imp)))
+    resp = res(apply(w, pro(imp)))
     out = np.empty((3, 3))
     for dy in (-1, 0, 1):
         for dx in (-1, 0, 1):
@@ -103,12 +133,20 @@ def galerkin(w: np.ndarray) -> np.ndarray:
     return out
 
 
-def hierarchy(epsilon: float, phi: float, n: int, coarse_op: str = "galerkin") -> list[np.ndarray]:
-    """stencil.py:151-176 (full coarsening)."""
+def hierarchy(epsilon: float, phi: float, n: int, coarse_op: str = "galerkin", coarsening: str = FULL
+              ) -> list[np.ndarray]:
+    """stencil.py:151-176."""
     ws = [fine_stencil(epsilon, phi)]
     for l in range(1, n):
-        ws.append(galerkin(ws[-1]) if coarse_op == "galerkin" else ws[0] * 0.25 ** l)
+        ws.append(galerkin(ws[-1], coarsening) if coarse_op == "galerkin" else ws[0] * 0.25 ** l)
     return ws
+
+
+def dims(n: int, coarsening: str = FULL) -> list[tuple[int, int]]:
+    """(ny, nx) per level, finest first (mesh.py:56-73)."""
+    if coarsening == FULL:
+        return [(2 ** (n - l) - 1, 2 ** (n - l) - 1) for l in range(n)]
+    return [(2 ** (n - l) - 1, 2 ** n - 1) for l in range(n)]
 
 
 # ---------------------------------------------------------------------------
@@ -122,17 +160,116 @@ def jacobi(w, u, f, omega):
     return u + (omega / center) * (f - apply(w, u))
 
 
-def relax(w, u, f, omega, count):
-    for _ in range(count):
-        u = jacobi(w, u, f, omega)
+def gtsv(dl, d, du, b):
+    """LAPACK dgtsv (scipy.linalg.solve_banded with l = u = 1): Gaussian
+    elimination with partial pivoting, then back substitution; b is (n, k)."""
+    dl, d, du, b = (np.array(a, dtype=float) for a in (dl, d, du, b))
+    n = len(d)
+    for i in range(n - 1):
+        if abs(d[i]) >= abs(dl[i]):
+            if d[i] == 0.0:
+                raise np.linalg.LinAlgError("singular tridiagonal system")
+            fact = dl[i] / d[i]
+            d[i + 1] = d[i + 1] - fact * du[i]
+            b[i + 1] = b[i + 1] - fact * b[i]
+            if i < n - 2:
+                dl[i] = 0.0
+        else:  # interchange rows i and i+1
+            fact = d[i] / dl[i]
+            d[i] = dl[i]
+            temp = d[i + 1]
+            d[i + 1] = du[i] - fact * temp
+            if i < n - 2:
+                dl[i] = du[i + 1]
+                du[i + 1] = -fact * dl[i]
+            du[i] = temp
+            temp = b[i].copy()
+            b[i] = b[i + 1]
+            b[i + 1] = temp - fact * b[i + 1]
+    if d[n - 1] == 0.0:
+        raise np.linalg.LinAlgError("singular tridiagonal system")
+    b[n - 1] = b[n - 1] / d[n - 1]
+    if n > 1:
+        b[n - 2] = (b[n - 2] - du[n - 2] * b[n - 1]) / d[n - 2]
+    for i in range(n - 3, -1, -1):
+        b[i] = (b[i] - du[i] * b[i + 1] - dl[i] * b[i + 2]) / d[i]
+    return b
+
+
+def zebra(w, u, f, axis):
+    """One zebra sweep with lines along `axis` (smoother.py:107-135): even
+    lines then odd lines, rhs = f - (north/south part of A) u, each line a
+    constant-coefficient tridiagonal solve.  y-lines run on the transposes."""
+    if axis == "y":
+        return zebra(np.ascontiguousarray(w.T), u.T, f.T, "x").T
+    ny, nx = u.shape
+    woff = w.copy()
+    woff[1, :] = 0.0
+    out = u.copy()
+    for start in (0, 1):
+        if start >= ny:
+            break
+        rhs = (f - apply(woff, out))[start::2]
+        sol = gtsv(np.full(nx - 1, w[1, 0]), np.full(nx, w[1, 1]), np.full(nx - 1, w[1, 2]), rhs.T)
+        out[start::2] = sol.T
+    return out
+
+
+JACOBI, ZEBRA_X, ZEBRA_Y, ZEBRA_XY = "jacobi", "zebra-x", "zebra-y", "zebra-xy"
+
+
+def relax(w, u, f, omega, count, kind=JACOBI):
+    """smoother.py:138-163."""
+    if kind == JACOBI:
+        for _ in range(count):
+            u = jacobi(w, u, f, omega)
+    elif kind in (ZEBRA_X, ZEBRA_Y):
+        for _ in range(count):
+            u = zebra(w, u, f, kind[-1])
+    elif kind == ZEBRA_XY:
+        if count % 2:
+            raise ValueError("alternating zebra needs an even relaxation count")
+        for _ in range(count // 2):
+            u = zebra(w, u, f, "x")
+            u = zebra(w, u, f, "y")
+    else:
+        raise ValueError(kind)
     return u
 
 
-def coarsest(w, f):
-    center = float(w[1, 1])
-    if center == 0.0:
-        raise np.linalg.LinAlgError("singular coarsest operator")
-    return f / center
+def thomas(lower, diag, upper, rhs):
+    """smoother.py:71-92: forward elimination without pivoting."""
+    m = len(diag)
+    cp, dp = np.empty(m), np.empty(m)
+    piv = diag[0]
+    if piv == 0.0:
+        raise np.linalg.LinAlgError("zero pivot in tridiagonal elimination")
+    cp[0] = upper[0] / piv
+    dp[0] = rhs[0] / piv
+    for i in range(1, m):
+        piv = diag[i] - lower[i] * cp[i - 1]
+        if piv == 0.0:
+            raise np.linalg.LinAlgError("zero pivot in tridiagonal elimination")
+        cp[i] = upper[i] / piv
+        dp[i] = (rhs[i] - lower[i] * dp[i - 1]) / piv
+    x = np.empty(m)
+    x[m - 1] = dp[m - 1]
+    for i in range(m - 2, -1, -1):
+        x[i] = dp[i] - cp[i] * x[i + 1]
+    return x
+
+
+def coarsest(w, f, coarsening=FULL):
+    """cycle.py:182-200: 1x1 division, or one x-line Thomas solve (semi-y)."""
+    ny, nx = f.shape
+    if ny == 1 and nx == 1:
+        center = float(w[1, 1])
+        if center == 0.0:
+            raise np.linalg.LinAlgError("singular coarsest operator")
+        return f / center
+    if coarsening == SEMI_Y and ny == 1:
+        return thomas(np.full(nx, w[1, 0]), np.full(nx, w[1, 1]), np.full(nx, w[1, 2]), f[0].copy()).reshape(1, nx)
+    raise ValueError(f"not a coarsest grid: {f.shape}")
 
 
 def norm2(a) -> float:
@@ -150,28 +287,32 @@ def dot(a, b) -> float:
 class Hierarchy:
     """Per-level v, f and stencils; level index 0 = finest (cycle.py:144-179)."""
 
-    def __init__(self, ws, omega=0.8, nu1=2, nu2=2):
+    def __init__(self, ws, omega=0.8, nu1=2, nu2=2, smoother=JACOBI, coarsening=FULL):
         self.ws = ws
         self.n = len(ws)
         self.omega, self.nu1, self.nu2 = omega, nu1, nu2
-        sides = [2 ** (self.n - l) - 1 for l in range(self.n)]
-        self.v = [np.zeros((m, m)) for m in sides]
-        self.f = [np.zeros((m, m)) for m in sides]
+        self.smoother, self.coarsening = smoother, coarsening
+        self.pro, self.res = transfer(coarsening)
+        self.v = [np.zeros(d) for d in dims(self.n, coarsening)]
+        self.f = [np.zeros(d) for d in dims(self.n, coarsening)]
         self.trace: list[tuple[int, int]] = []
+
+    def _relax(self, l, count):
+        self.v[l] = relax(self.ws[l], self.v[l], self.f[l], self.omega, count, self.smoother)
 
     def cycle(self, kappa: int, l: int = 0):
         self.trace.append((l + 1, kappa))
         if l == self.n - 1:
-            self.v[l] = coarsest(self.ws[l], self.f[l])
+            self.v[l] = coarsest(self.ws[l], self.f[l], self.coarsening)
             return
-        self.v[l] = relax(self.ws[l], self.v[l], self.f[l], self.omega, self.nu1)
-        self.f[l + 1] = restrict(residual(self.ws[l], self.v[l], self.f[l]))
+        self._relax(l, self.nu1)
+        self.f[l + 1] = self.res(residual(self.ws[l], self.v[l], self.f[l]))
         self.v[l + 1] = np.zeros_like(self.v[l + 1])
         self.cycle(kappa, l + 1)
         if kappa > 1:
             self.cycle(kappa - 1, l + 1)
-        self.v[l] = self.v[l] + prolong(self.v[l + 1])
-        self.v[l] = relax(self.ws[l], self.v[l], self.f[l], self.omega, self.nu2)
+        self.v[l] = self.v[l] + self.pro(self.v[l + 1])
+        self._relax(l, self.nu2)
 
 
 def eff_kappa(kappa, n):
@@ -185,10 +326,10 @@ def level_calls(kappa, n):
 
 
 def standalone(epsilon, phi, n, kappa, target=1e10, max_cycles=10000, seed=0, v0=None,
-               stop="error", omega=0.8, nu1=2, nu2=2, track_residual=True):
+               stop="error", omega=0.8, nu1=2, nu2=2, track_residual=True, smoother=JACOBI, coarsening=FULL):
     """solve_standalone loop (cycle.py:320-353) with per-cycle error and true
     residual histories; `stop` picks the stopping measure."""
-    h = Hierarchy(hierarchy(epsilon, phi, n), omega, nu1, nu2)
+    h = Hierarchy(hierarchy(epsilon, phi, n, coarsening=coarsening), omega, nu1, nu2, smoother, coarsening)
     m = 2 ** n - 1
     h.v[0] = np.random.default_rng(seed).random((m, m)) if v0 is None else np.array(v0, dtype=float)
     k = eff_kappa(kappa, n)

@@ -415,6 +415,84 @@ def gen_costmodel():
     dump("costmodel.json", out)
 
 
+ZEBRA_CONFIGS = [  # (smoother, coarsening) pairs of the paper's solvers 3-6
+    ("zebra-xy", "full"), ("zebra-x", "semi-y"), ("zebra-y", "full"), ("jacobi", "semi-y"), ("zebra-x", "full"),
+]
+_SK = {"jacobi": None, "zebra-x": "ZEBRA_X", "zebra-y": "ZEBRA_Y", "zebra-xy": "ZEBRA_ALTERNATING"}
+
+
+def _smoother(name):
+    return ksm.SmootherSpec(ksm.SmootherKind.DAMPED_JACOBI if name == "jacobi" else getattr(ksm.SmootherKind, _SK[name]),
+                            0.8)
+
+
+def _coarsening(name):
+    return km.Coarsening.FULL_STANDARD if name == "full" else km.Coarsening.SEMI_Y
+
+
+def gen_zebra():
+    """Zebra line relaxation, y-semi-coarsening and the line coarsest solve
+    (smoother.py:71-163, transfer.py:46-87, cycle.py:182-200): kernel KATs,
+    semi-y Galerkin hierarchies, cycle iterates and small solves."""
+    rng = np.random.default_rng(4)
+    arrays, meta = {}, {"kernels": [], "cycles": {}, "solves": {}, "hierarchies": []}
+    full = kst.operator_hierarchy(kst.ProblemSpec(1e-4, 45.0), km.build_hierarchy(6, km.Coarsening.FULL_STANDARD))
+    semi = kst.operator_hierarchy(kst.ProblemSpec(1e-4, 45.0), km.build_hierarchy(6, km.Coarsening.SEMI_Y))
+    pivot = kst.Stencil9(np.array([[0.1, -0.3, 0.05], [2.5, 0.7, -1.9], [0.2, 0.4, -0.1]]))  # forces row interchanges
+    for ny, nx in ((1, 1), (1, 7), (3, 3), (7, 7), (15, 7), (7, 31), (31, 31)):
+        for tag, op in (("f0", full[0]), ("f3", full[3]), ("s2", semi[2]), ("piv", pivot)):
+            key = f"z{ny}x{nx}_{tag}"
+            u = rng.random((ny, nx))
+            f = rng.standard_normal((ny, nx))
+            arrays[key + "_u"], arrays[key + "_f"], arrays[key + "_w"] = u, f, op.w
+            arrays[key + "_zx"] = ksm.zebra_line_sweep(op, u, f, "x")
+            arrays[key + "_zy"] = ksm.zebra_line_sweep(op, u, f, "y")
+            arrays[key + "_zxy2"] = ksm.relax(op, u, f, ksm.SmootherSpec(ksm.SmootherKind.ZEBRA_ALTERNATING), 2)
+            if ny >= 3:
+                arrays[key + "_rsemi"] = ktr.restrict(f, km.Coarsening.SEMI_Y)
+            arrays[key + "_psemi"] = ktr.prolong(u, km.Coarsening.SEMI_Y)
+            if ny == 1 and tag != "piv":
+                arrays[key + "_coarsest"] = kc.coarsest_solve(op, f, km.Coarsening.SEMI_Y)
+            meta["kernels"].append(key)
+    for eps, phi in STENCIL_CASES:
+        ops = kst.operator_hierarchy(kst.ProblemSpec(epsilon=eps, phi=phi), km.build_hierarchy(12, km.Coarsening.SEMI_Y))
+        meta["hierarchies"].append({"epsilon": eps, "phi": phi, "n": 12,
+                                    "w_hex": [[float(x).hex() for x in op.w.ravel()] for op in ops]})
+    for sm, co in ZEBRA_CONFIGS:
+        for n in (3, 5):
+            for kappa in (1, 2, INF):
+                problem = kst.ProblemSpec(epsilon=0.5, phi=30.0)
+                cfg = kc.CycleConfig(n=n, kappa=kappa, smoother=_smoother(sm), coarsening=_coarsening(co))
+                state = kc.build_state(problem, cfg)
+                r2 = np.random.default_rng(7 + n)
+                state.v[0] = r2.random(state.v[0].shape)
+                state.f[0] = r2.random(state.f[0].shape)
+                key = f"{sm}_{co}_n{n}_k{kname(kappa)}"
+                arrays[key + "_v0"], arrays[key + "_f0"] = state.v[0].copy(), state.f[0].copy()
+                stats = kc.CycleStats.for_levels(n)
+                for c in range(1, 3):
+                    kc.run_cycle(state, cfg, stats)
+                    arrays[f"{key}_c{c}"] = state.v[0].copy()
+                meta["cycles"][key] = {"smoother": sm, "coarsening": co, "n": n, "kappa": kname(kappa),
+                                       "visits": stats.visits, "kernel_launches": stats.kernel_launches,
+                                       "unknown_touches": stats.unknown_touches}
+        for n in (5, 7):
+            for kappa in (1, 2):
+                problem, cfg = problem_config(n, kappa, smoother=_smoother(sm), coarsening=_coarsening(co))
+                rep = kc.solve_standalone(problem, cfg, 1e8, max_cycles=2000)
+                h = [1.0]
+                for red in rep.per_cycle_reduction:
+                    h.append(h[-1] * red)
+                meta["solves"][f"{sm}_{co}_n{n}_k{kname(kappa)}"] = {
+                    "smoother": sm, "coarsening": co, "n": n, "kappa": kname(kappa), "status": rep.status,
+                    "iterations": rep.iterations, "initial_error_norm": rep.initial_error_norm,
+                    "final_error_norm": rep.final_error_norm, "per_cycle_reduction": rep.per_cycle_reduction,
+                    "kernel_launches": rep.stats.kernel_launches, "unknown_touches": rep.stats.unknown_touches}
+                print(sm, co, n, kname(kappa), rep.status, rep.iterations, flush=True)
+    np.savez_compressed(os.path.join(HERE, "zebra.npz"), **arrays)
+    dump("zebra_meta.json", meta)
+
+
 CLI_CASES = [
     ["calls", "--kappa", "3", "--levels", "5"],
     ["calls", "--kappa", "inf", "--levels", "12"],
@@ -470,7 +548,7 @@ def gen_cli():
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["small", "solve", "pcg", "costmodel", "cli"])
+    ap.add_argument("what", choices=["small", "solve", "pcg", "costmodel", "cli", "zebra"])
     ap.add_argument("--n", type=int, default=12)
     ap.add_argument("--kappa", default="1")
     ap.add_argument("--cap", type=int, default=20000)
@@ -481,6 +559,9 @@ def main():
         return
     if a.what == "cli":
         gen_cli()
+        return
+    if a.what == "zebra":
+        gen_zebra()
         return
     if a.what == "small":
         gen_stencils()

@@ -129,3 +129,69 @@ def test_n12_first_cycle_sha():
     assert O.norm2(h.v[0]) == pytest.approx(g["err_hist"][0], rel=1e-14)
     h.cycle(4)
     assert sha(h.v[0]) == g["sha256"]["1"]
+
+
+# ---------------------------------------------------------------------------
+# zebra line relaxation, y-semi-coarsening, line coarsest solve (§8(f)1)
+# ---------------------------------------------------------------------------
+
+def test_gtsv_restatement_matches_scipy_solve_banded():
+    """The oracle's dgtsv restatement is bit-identical to scipy's
+    solve_banded((1,1)) -- the call inside zebra_line_sweep (smoother.py:133)
+    -- with and without row interchanges."""
+    import scipy.linalg as sl
+    rng = np.random.default_rng(0)
+    for trial in range(200):
+        n = int(rng.integers(1, 50))
+        lo, di, up = rng.standard_normal(3) * (1.0 if trial % 2 else np.array([0.3, 2.0, 0.4]))
+        ab = np.zeros((3, n))
+        ab[0, 1:], ab[1, :], ab[2, :-1] = up, di, lo
+        b = rng.standard_normal((n, 3))
+        ref = sl.solve_banded((1, 1), ab, b)
+        got = O.gtsv(np.full(n - 1, lo), np.full(n, di), np.full(n - 1, up), b)
+        assert np.array_equal(ref, got), trial
+
+
+def test_zebra_kernels_vs_reference():
+    z = load_npz("zebra.npz")
+    meta = load_json("zebra_meta.json")
+    for key in meta["kernels"]:
+        u, f, w = z[key + "_u"], z[key + "_f"], z[key + "_w"]
+        assert np.array_equal(O.zebra(w, u, f, "x"), z[key + "_zx"]), key
+        assert np.array_equal(O.zebra(w, u, f, "y"), z[key + "_zy"]), key
+        assert np.array_equal(O.relax(w, u, f, 0.8, 2, O.ZEBRA_XY), z[key + "_zxy2"]), key
+        if key + "_rsemi" in z:
+            assert np.array_equal(O.restrict_semi(f), z[key + "_rsemi"]), key
+        assert np.array_equal(O.prolong_semi(u), z[key + "_psemi"]), key
+        if key + "_coarsest" in z:
+            assert np.array_equal(O.coarsest(w, f, O.SEMI_Y), z[key + "_coarsest"]), key
+
+
+def test_semi_hierarchies_vs_reference():
+    for rec in load_json("zebra_meta.json")["hierarchies"]:
+        ws = O.hierarchy(rec["epsilon"], rec["phi"], rec["n"], coarsening=O.SEMI_Y)
+        for w, ref in zip(ws, rec["w_hex"]):
+            assert [float(x).hex() for x in w.ravel()] == ref, (rec["epsilon"], rec["phi"])
+
+
+def test_zebra_cycles_vs_reference():
+    z = load_npz("zebra.npz")
+    for key, rec in load_json("zebra_meta.json")["cycles"].items():
+        n = rec["n"]
+        ws = O.hierarchy(0.5, 30.0, n, coarsening=rec["coarsening"])
+        h = O.Hierarchy(ws, smoother=rec["smoother"], coarsening=rec["coarsening"])
+        h.v[0], h.f[0] = z[key + "_v0"].copy(), z[key + "_f0"].copy()
+        k = O.eff_kappa(O.INF if rec["kappa"] == "W" else int(rec["kappa"]), n)
+        for c in (1, 2):
+            h.cycle(k)
+            assert np.array_equal(h.v[0], z[f"{key}_c{c}"]), (key, c)
+
+
+def test_zebra_solves_vs_reference():
+    for key, rec in load_json("zebra_meta.json")["solves"].items():
+        if rec["n"] > 5:
+            continue  # n = 7 cases are covered on the GPU
+        out = O.standalone(1e-4, 45.0, rec["n"], int(rec["kappa"]), target=1e8, max_cycles=2000,
+                           smoother=rec["smoother"], coarsening=rec["coarsening"], track_residual=False)
+        assert out["status"] == rec["status"] and out["iterations"] == rec["iterations"], key
+        assert out["err_hist"][-1] == pytest.approx(rec["final_error_norm"], rel=1e-12)
