@@ -44,8 +44,11 @@ extern "C" {
 
 /* enums mirrored from the reference */
 #define KC_COARSEN_FULL 0        /* Coarsening.FULL_STANDARD, mesh.py:38 */
-#define KC_COARSEN_SEMI_Y 1      /* Coarsening.SEMI_Y, mesh.py:39 (not yet supported: KC_EINVAL) */
+#define KC_COARSEN_SEMI_Y 1      /* Coarsening.SEMI_Y, mesh.py:39 (per-op kernels, kc_zebra.cuh) */
 #define KC_SMOOTH_JACOBI 0       /* SmootherKind.DAMPED_JACOBI, smoother.py:37 */
+#define KC_SMOOTH_ZEBRA_X 1      /* SmootherKind.ZEBRA_X, smoother.py:39 */
+#define KC_SMOOTH_ZEBRA_Y 2      /* SmootherKind.ZEBRA_Y, smoother.py:40 */
+#define KC_SMOOTH_ZEBRA_XY 3     /* SmootherKind.ZEBRA_ALTERNATING, smoother.py:41 */
 #define KC_WHICH_V 0             /* GridState.v[level-1], cycle.py:155 */
 #define KC_WHICH_F 1             /* GridState.f[level-1], cycle.py:156 */
 #define KC_STOP_ERROR 0          /* ||v_k|| <= ||v_0||/target (cycle.py:332-347) */

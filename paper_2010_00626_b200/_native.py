@@ -23,7 +23,10 @@ LIB_PATH = os.environ.get("KCB200_LIB") or os.path.join(_HERE, "libkcb200.so")  
 
 KC_OK, KC_EINVAL, KC_ESINGULAR, KC_ECUDA, KC_ENOMEM = 0, 1, 2, 3, 4
 KC_COARSEN_FULL, KC_COARSEN_SEMI_Y = 0, 1
-KC_SMOOTH_JACOBI = 0
+KC_SMOOTH_JACOBI, KC_SMOOTH_ZEBRA_X, KC_SMOOTH_ZEBRA_Y, KC_SMOOTH_ZEBRA_XY = 0, 1, 2, 3
+COARSENING_KIND = {"full": KC_COARSEN_FULL, "semi-y": KC_COARSEN_SEMI_Y}  # Coarsening values (mesh.py:38-39)
+SMOOTHER_KIND = {"jacobi": KC_SMOOTH_JACOBI, "zebra-x": KC_SMOOTH_ZEBRA_X, "zebra-y": KC_SMOOTH_ZEBRA_Y,
+                 "zebra-xy": KC_SMOOTH_ZEBRA_XY}  # SmootherKind values (smoother.py:37-41)
 KC_WHICH_V, KC_WHICH_F = 0, 1
 KC_STOP_ERROR, KC_STOP_RESIDUAL = 0, 1
 STATUS_NAMES = {0: "converged", 1: "diverged", 2: "max_cycles", 3: "breakdown"}

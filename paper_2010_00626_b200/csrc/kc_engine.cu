@@ -25,6 +25,7 @@
 #include "kc_common.cuh"
 #include "kc_grid_kernels.cuh"
 #include "kc_pcg.cuh"
+#include "kc_zebra.cuh"
 #include "kc_stream.cuh"
 #include "kc_tile.cuh"
 #include "kc_strip.cuh"
@@ -74,7 +75,14 @@ __global__ void k_stop_check(cudaGraphConditionalHandle h_loop, cudaGraphConditi
 }
 
 struct Level {
-  int m = 0, P = 0;
+  int m = 0, P = 0;  // m: columns (nx); rows ny == m except under y-semi-coarsening
+  int ny = 0;
+  // zebra (kc_zebra.cuh): dgtsv plans of the x- and y-line systems, the
+  // cross-line stencils (line row / column zeroed; the y one transposed)
+  ZPlan zp[2]{};
+  void* zmem[2] = {nullptr, nullptr};
+  bool zsing[2] = {false, false};
+  St9 zoff[2]{};
   size_t elems = 0;
   double* v[2] = {nullptr, nullptr};
   double* f = nullptr;
@@ -117,6 +125,8 @@ struct kc_handle {
   size_t bot_smem = 0;
   int bot_m0 = 0;
   int bot_cs = 1;  // CTAs per bottom launch (thread-block cluster when > 1)
+  double line_w[3] = {0, 0, 0};  // semi-y coarsest line: lower, diag, upper (raw w[1][:])
+  bool line_singular = false;
   // host-built bottom phase schedules, keyed by (kappa1, kappa2, v_zero)
   std::map<std::tuple<int, int, int>, std::tuple<unsigned*, int, int>> bot_sched;
   cudaStream_t stream = nullptr;
@@ -256,20 +266,158 @@ const dim3 kBlock(KC_BX, KC_BY);
 int ex_materialize(kc_handle* h, int l) {
   Level& L = h->L[l];
   if (!L.vzero) return KC_OK;
-  k_zero<<<grid2(L.m, L.m), kBlock, 0, h->stream>>>(L.v[L.cur], L.m, L.P);
+  k_zero<<<grid2(L.m, L.ny), kBlock, 0, h->stream>>>(L.v[L.cur], L.ny, L.m, L.P);
   KC_LAUNCH_CHECK(h);
   ++h->launches;
   L.vzero = false;
   return KC_OK;
 }
 
+// LAPACK dgtsv elimination of a constant-coefficient tridiagonal system of
+// order n (what scipy.linalg.solve_banded((1,1)) runs, smoother.py:133),
+// recorded as a plan: everything but the right-hand-side updates is data
+// independent.  Host fp64 without contraction (-ffp-contract=off).
+struct HostZPlan {
+  std::vector<double> fact, d, du, dl;
+  std::vector<unsigned char> piv;
+  bool singular = false;
+};
+HostZPlan gtsv_plan(double lo, double di, double up, int n) {
+  HostZPlan p;
+  std::vector<double> dl(n > 1 ? n - 1 : 0, lo), d(n, di), du(n > 1 ? n - 1 : 0, up);
+  p.fact.assign(n > 1 ? n - 1 : 0, 0.0);
+  p.piv.assign(n > 1 ? n - 1 : 0, 0);
+  for (int i = 0; i < n - 1; ++i) {
+    if (std::fabs(d[i]) >= std::fabs(dl[i])) {
+      if (d[i] == 0.0) p.singular = true;
+      const double fact = dl[i] / d[i];
+      p.fact[i] = fact;
+      d[i + 1] = d[i + 1] - fact * du[i];
+      if (i < n - 2) dl[i] = 0.0;
+    } else {
+      const double fact = d[i] / dl[i];
+      p.fact[i] = fact;
+      p.piv[i] = 1;
+      d[i] = dl[i];
+      const double temp = d[i + 1];
+      d[i + 1] = du[i] - fact * temp;
+      if (i < n - 2) {
+        dl[i] = du[i + 1];
+        du[i + 1] = -fact * dl[i];
+      }
+      du[i] = temp;
+    }
+  }
+  if (d[n - 1] == 0.0) p.singular = true;
+  p.d = d;
+  p.du = du;
+  p.dl.assign(dl.begin(), dl.begin() + (n > 2 ? n - 2 : 0));
+  return p;
+}
+
+int zebra_setup(kc_handle* h, const double* w) {
+  for (int l = 0; l < h->n; ++l) {
+    Level& L = h->L[l];
+    const double* wl = w + 9 * l;  // raw (un-dropped) coefficients build the line systems
+    for (int axis = 0; axis < 2; ++axis) {
+      const bool need = (axis == 0 && (h->smoother == KC_SMOOTH_ZEBRA_X || h->smoother == KC_SMOOTH_ZEBRA_XY)) ||
+                        (axis == 1 && (h->smoother == KC_SMOOTH_ZEBRA_Y || h->smoother == KC_SMOOTH_ZEBRA_XY));
+      if (!need) continue;
+      const int n = axis == 0 ? L.m : L.ny;
+      const HostZPlan hp = axis == 0 ? gtsv_plan(wl[3], wl[4], wl[5], n) : gtsv_plan(wl[1], wl[4], wl[7], n);
+      L.zsing[axis] = hp.singular;
+      const size_t nd = hp.fact.size() + hp.d.size() + hp.du.size() + hp.dl.size();
+      const size_t bytes = sizeof(double) * (nd + 1) + hp.piv.size() + 16;
+      KC_CUDA(h, cudaMalloc(&L.zmem[axis], bytes));
+      std::vector<char> host(bytes, 0);
+      double* hd = reinterpret_cast<double*>(host.data());
+      size_t o = 0;
+      auto put = [&](const std::vector<double>& v) {
+        const size_t at = o;
+        for (double x : v) hd[o++] = x;
+        return at;
+      };
+      const size_t of = put(hp.fact), od = put(hp.d), odu = put(hp.du), odl = put(hp.dl);
+      unsigned char* hpv = reinterpret_cast<unsigned char*>(hd + nd + 1);
+      for (size_t i = 0; i < hp.piv.size(); ++i) hpv[i] = hp.piv[i];
+      KC_CUDA(h, cudaMemcpy(L.zmem[axis], host.data(), bytes, cudaMemcpyHostToDevice));
+      const double* dd = reinterpret_cast<const double*>(L.zmem[axis]);
+      L.zp[axis] = ZPlan{dd + of, dd + od, dd + odu, dd + odl,
+                         reinterpret_cast<const unsigned char*>(dd + nd + 1), n};
+      // cross-line stencil: the line's row (x-lines) or column (y-lines) of
+      // taps zeroed; y-lines accumulate in the transposed C order
+      St9 off{};
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) off.w[a * 3 + b] = axis == 0 ? L.st.w[a * 3 + b] : L.st.w[b * 3 + a];
+      off.w[3] = off.w[4] = off.w[5] = 0.0;
+      L.zoff[axis] = off;
+    }
+  }
+  if (h->coarsening == KC_COARSEN_SEMI_Y) {  // Thomas pivots of the coarsest line (smoother.py:77-85)
+    const double* wl = w + 9 * (h->n - 1);
+    h->line_w[0] = wl[3];
+    h->line_w[1] = wl[4];
+    h->line_w[2] = wl[5];
+    double piv = wl[4];
+    bool sing = piv == 0.0;
+    double cp = sing ? 0.0 : wl[5] / piv;
+    for (int i = 1; i < h->L[h->n - 1].m && !sing; ++i) {
+      piv = wl[4] - wl[3] * cp;
+      if (piv == 0.0) sing = true;
+      else cp = wl[5] / piv;
+    }
+    h->line_singular = sing;
+  }
+  return KC_OK;
+}
+
+// One zebra sweep with lines along x (axis 0) or y (axis 1), in place:
+// even lines, then odd lines with the updated even ones (smoother.py:107-135)
+int ex_zebra(kc_handle* h, int l, int axis) {
+  Level& L = h->L[l];
+  if (L.zsing[axis]) KC_FAIL(h, KC_ESINGULAR, "singular tridiagonal line system");
+  int rc = ex_materialize(h, l);
+  if (rc) return rc;
+  double* u = L.v[L.cur];
+  for (int par = 0; par < 2; ++par) {
+    if (axis == 0) {
+      if (par >= L.ny) break;
+      const int nl = (L.ny - par + 1) / 2;
+      k_zebra_rhs_x<<<dim3((L.m + 31) / 32, (nl + 7) / 8), dim3(32, 8), 0, h->stream>>>(u, L.f, L.ny, L.m, L.P,
+                                                                                       L.zoff[0], par);
+      k_zebra_solve_x<<<(nl + 63) / 64, 64, 0, h->stream>>>(u, L.ny, L.P, L.zp[0], par);
+    } else {
+      if (par >= L.m) break;
+      const int nl = (L.m - par + 1) / 2;
+      k_zebra_rhs_y<<<dim3((nl + 31) / 32, (L.ny + 7) / 8), dim3(32, 8), 0, h->stream>>>(u, L.f, L.ny, L.m, L.P,
+                                                                                        L.zoff[1], par);
+      k_zebra_solve_y<<<(nl + 63) / 64, 64, 0, h->stream>>>(u, L.m, L.P, L.zp[1], par);
+    }
+    KC_LAUNCH_CHECK(h);
+    h->launches += 2;
+  }
+  return KC_OK;
+}
+
+int ex_zebra(kc_handle* h, int l, int axis);
 int ex_relax(kc_handle* h, int l, int count) {
   Level& L = h->L[l];
+  if (h->smoother != KC_SMOOTH_JACOBI) {  // relax(), smoother.py:138-163
+    if (h->smoother == KC_SMOOTH_ZEBRA_XY && count % 2)
+      KC_FAIL(h, KC_EINVAL, "alternating zebra needs an even relaxation count");
+    const int reps = h->smoother == KC_SMOOTH_ZEBRA_XY ? count / 2 : count;
+    for (int it = 0; it < reps; ++it) {
+      int rc;
+      if (h->smoother != KC_SMOOTH_ZEBRA_Y && (rc = ex_zebra(h, l, 0))) return rc;
+      if (h->smoother != KC_SMOOTH_ZEBRA_X && (rc = ex_zebra(h, l, 1))) return rc;
+    }
+    return KC_OK;
+  }
   for (int it = 0; it < count; ++it) {
     double* u = L.v[L.cur];
     double* o = L.v[L.cur ^ 1];
-    if (L.vzero) k_jacobi<true><<<grid2(L.m, L.m, KC_RY), kBlock, 0, h->stream>>>(u, L.f, o, L.m, L.P, L.st);
-    else k_jacobi<false><<<grid2(L.m, L.m, KC_RY), kBlock, 0, h->stream>>>(u, L.f, o, L.m, L.P, L.st);
+    if (L.vzero) k_jacobi<true><<<grid2(L.m, L.ny, KC_RY), kBlock, 0, h->stream>>>(u, L.f, o, L.ny, L.m, L.P, L.st);
+    else k_jacobi<false><<<grid2(L.m, L.ny, KC_RY), kBlock, 0, h->stream>>>(u, L.f, o, L.ny, L.m, L.P, L.st);
     KC_LAUNCH_CHECK(h);
     ++h->launches;
     L.vzero = false;
@@ -281,10 +429,20 @@ int ex_relax(kc_handle* h, int l, int count) {
 int ex_restrict(kc_handle* h, int l) {
   Level& L = h->L[l];
   Level& C = h->L[l + 1];
-  if (L.vzero)
-    k_resid_restrict<true><<<grid2(C.m, C.m), kBlock, 0, h->stream>>>(L.v[L.cur], L.f, C.f, C.m, L.P, C.P, L.st);
-  else
-    k_resid_restrict<false><<<grid2(C.m, C.m), kBlock, 0, h->stream>>>(L.v[L.cur], L.f, C.f, C.m, L.P, C.P, L.st);
+  if (h->coarsening == KC_COARSEN_SEMI_Y) {  // transfer.py:84-86
+    if (L.vzero)
+      k_resid_restrict_semi<true><<<grid2(C.m, C.ny), kBlock, 0, h->stream>>>(L.v[L.cur], L.f, C.f, C.ny, C.m, L.P,
+                                                                            C.P, L.st);
+    else
+      k_resid_restrict_semi<false><<<grid2(C.m, C.ny), kBlock, 0, h->stream>>>(L.v[L.cur], L.f, C.f, C.ny, C.m, L.P,
+                                                                             C.P, L.st);
+  } else if (L.vzero) {
+    k_resid_restrict<true><<<grid2(C.m, C.ny), kBlock, 0, h->stream>>>(L.v[L.cur], L.f, C.f, C.ny, C.m, L.P, C.P,
+                                                                     L.st);
+  } else {
+    k_resid_restrict<false><<<grid2(C.m, C.ny), kBlock, 0, h->stream>>>(L.v[L.cur], L.f, C.f, C.ny, C.m, L.P, C.P,
+                                                                      L.st);
+  }
   KC_LAUNCH_CHECK(h);
   ++h->launches;
   return KC_OK;
@@ -295,10 +453,17 @@ int ex_prolong(kc_handle* h, int l) {
   Level& C = h->L[l + 1];
   int rc = ex_materialize(h, l + 1);
   if (rc) return rc;
-  if (L.vzero)
-    k_prolong_add<true><<<grid2(L.m, L.m), kBlock, 0, h->stream>>>(L.v[L.cur], C.v[C.cur], L.m, L.P, C.P);
-  else
-    k_prolong_add<false><<<grid2(L.m, L.m), kBlock, 0, h->stream>>>(L.v[L.cur], C.v[C.cur], L.m, L.P, C.P);
+  if (h->coarsening == KC_COARSEN_SEMI_Y) {  // transfer.py:59-66
+    if (L.vzero)
+      k_prolong_add_semi<true><<<grid2(L.m, L.ny), kBlock, 0, h->stream>>>(L.v[L.cur], C.v[C.cur], L.ny, L.m, L.P, C.P);
+    else
+      k_prolong_add_semi<false><<<grid2(L.m, L.ny), kBlock, 0, h->stream>>>(L.v[L.cur], C.v[C.cur], L.ny, L.m, L.P,
+                                                                          C.P);
+  } else if (L.vzero) {
+    k_prolong_add<true><<<grid2(L.m, L.ny), kBlock, 0, h->stream>>>(L.v[L.cur], C.v[C.cur], L.ny, L.m, L.P, C.P);
+  } else {
+    k_prolong_add<false><<<grid2(L.m, L.ny), kBlock, 0, h->stream>>>(L.v[L.cur], C.v[C.cur], L.ny, L.m, L.P, C.P);
+  }
   KC_LAUNCH_CHECK(h);
   ++h->launches;
   L.vzero = false;
@@ -307,7 +472,16 @@ int ex_prolong(kc_handle* h, int l) {
 
 int ex_coarsest(kc_handle* h) {
   Level& L = h->L[h->n - 1];
-  if (L.m != 1) KC_FAIL(h, KC_EINVAL, "not a coarsest grid: side %d", L.m);
+  if (L.ny == 1 && L.m > 1 && h->coarsening == KC_COARSEN_SEMI_Y) {  // one x-line, cycle.py:191-200
+    if (h->line_singular) KC_FAIL(h, KC_ESINGULAR, "zero pivot in tridiagonal elimination");
+    k_coarsest_line<<<1, 32, 0, h->stream>>>(L.v[L.cur], L.f, L.v[L.cur ^ 1], L.m, L.P, h->line_w[0], h->line_w[1],
+                                             h->line_w[2]);
+    KC_LAUNCH_CHECK(h);
+    ++h->launches;
+    L.vzero = false;
+    return KC_OK;
+  }
+  if (L.m != 1 || L.ny != 1) KC_FAIL(h, KC_EINVAL, "not a coarsest grid: shape (%d, %d)", L.ny, L.m);
   if (L.st.center == 0.0) KC_FAIL(h, KC_ESINGULAR, "singular coarsest operator");
   k_coarsest<<<1, 32, 0, h->stream>>>(L.v[L.cur], L.f, L.P, L.st.center);
   KC_LAUNCH_CHECK(h);
@@ -597,7 +771,8 @@ int ex_op(kc_handle* h, const Op& op) {
 }
 
 bool fusable(const kc_handle* h, int l) {
-  return h->fuse && h->nu1 <= KC_FUSE_MAXNU && h->nu2 <= KC_FUSE_MAXNU && l < h->n - 1 && h->L[l].m >= KC_FUSE_MIN_M;
+  return h->fuse && h->smoother == KC_SMOOTH_JACOBI && h->coarsening == KC_COARSEN_FULL && h->nu1 <= KC_FUSE_MAXNU &&
+         h->nu2 <= KC_FUSE_MAXNU && l < h->n - 1 && h->L[l].m >= KC_FUSE_MIN_M;
 }
 
 // Flatten kappa_cycle(level, kappa) (cycle.py:204-220) into ops.  `norms`
@@ -839,7 +1014,7 @@ int get_solve_graph(kc_handle* h, int kappa, SolveGraph** out) {
 // async reductions into h->d_scal[slot]
 int red_dot(kc_handle* h, const double* a, const double* b, int l, int slot, bool sq) {
   Level& L = h->L[l];
-  k_red_partial<0><<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(a, b, L.m, L.P, L.st, h->d_part);
+  k_red_partial<0><<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(a, b, L.ny, L.m, L.P, L.st, h->d_part);
   KC_LAUNCH_CHECK(h);
   if (sq) k_red_final<true><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_part, KC_RED_BLOCKS, h->d_scal + slot);
   else k_red_final<false><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_part, KC_RED_BLOCKS, h->d_scal + slot);
@@ -849,7 +1024,7 @@ int red_dot(kc_handle* h, const double* a, const double* b, int l, int slot, boo
 
 int red_resnorm(kc_handle* h, const double* u, const double* f, int l, int slot) {
   Level& L = h->L[l];
-  k_red_partial<1><<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(u, f, L.m, L.P, L.st, h->d_part);
+  k_red_partial<1><<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(u, f, L.ny, L.m, L.P, L.st, h->d_part);
   KC_LAUNCH_CHECK(h);
   k_red_final<true><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_part, KC_RED_BLOCKS, h->d_scal + slot);
   KC_LAUNCH_CHECK(h);
@@ -893,11 +1068,12 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
   *out = nullptr;
   if (n < 1) KC_FAIL(none, KC_EINVAL, "level count must be >= 1, got %d", n);
   if (n > 15) KC_FAIL(none, KC_EINVAL, "level count %d exceeds the engine limit 15", n);
-  if (coarsening != KC_COARSEN_FULL)
-    KC_FAIL(none, KC_EINVAL, "only full coarsening is implemented on the device (got %d)", coarsening);
-  if (smoother_kind != KC_SMOOTH_JACOBI)
-    KC_FAIL(none, KC_EINVAL, "only damped Jacobi is implemented on the device (got %d)", smoother_kind);
-  if (!(omega > 0.0 && omega <= 1.0)) KC_FAIL(none, KC_EINVAL, "jacobi damping must lie in (0, 1], got %g", omega);
+  if (coarsening != KC_COARSEN_FULL && coarsening != KC_COARSEN_SEMI_Y)
+    KC_FAIL(none, KC_EINVAL, "unknown coarsening kind %d", coarsening);
+  if (smoother_kind < KC_SMOOTH_JACOBI || smoother_kind > KC_SMOOTH_ZEBRA_XY)
+    KC_FAIL(none, KC_EINVAL, "unknown smoother kind %d", smoother_kind);
+  if (smoother_kind == KC_SMOOTH_JACOBI && !(omega > 0.0 && omega <= 1.0))
+    KC_FAIL(none, KC_EINVAL, "jacobi damping must lie in (0, 1], got %g", omega);
   if (nu1 < 0 || nu2 < 0) KC_FAIL(none, KC_EINVAL, "relaxation counts must be >= 0");
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -925,17 +1101,18 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
     kc_destroy(h);
     return code;
   };
-  for (int l = 0; l < n; ++l) {
+  for (int l = 0; l < n; ++l) {  // mesh.py:56-73
     Level& L = h->L[l];
-    L.m = (1 << (n - l)) - 1;
+    L.ny = (1 << (n - l)) - 1;
+    L.m = coarsening == KC_COARSEN_SEMI_Y ? (1 << n) - 1 : L.ny;
     L.P = kc_pitch(L.m);
-    L.elems = (size_t)(L.m + 2) * L.P;
+    L.elems = (size_t)(L.ny + 2) * L.P;
     for (int k = 0; k < 9; ++k) {
       double wk = w[9 * l + k];
       L.st.w[k] = (std::fabs(wk) <= DBL_EPSILON) ? 0.0 : wk;  // ndimage tap drop (F3)
     }
     L.st.center = w[9 * l + 4];
-    if (L.m > 1 && (nu1 + nu2) > 0 && L.st.center == 0.0) {
+    if (smoother_kind == KC_SMOOTH_JACOBI && (L.m > 1 || L.ny > 1) && (nu1 + nu2) > 0 && L.st.center == 0.0) {
       h->err = "zero center coefficient";
       return fail(KC_EINVAL);
     }
@@ -966,12 +1143,18 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
   }
   cudaMemset(h->d_scal, 0, sizeof(double) * 64);
 
+  // zebra line-solve plans and the semi-y coarsest line (data independent)
+  if (smoother_kind != KC_SMOOTH_JACOBI || coarsening == KC_COARSEN_SEMI_Y) {
+    int rc = zebra_setup(h, w);
+    if (rc) return fail(rc);
+  }
   // bottom (smem-resident) levels: a cluster of 16 (else 8) CTAs entering
   // at side <= 255 with the sides >= 31 in row strips, else one CTA
-  // entering at side <= 63 (kc_bottom.cuh); KC_BOT_CLUSTER=0 forces one CTA
+  // entering at side <= 63 (kc_bottom.cuh); KC_BOT_CLUSTER=0 forces one CTA.
+  // Only the Jacobi / full-coarsening path has fused kernels.
   int lb = -1, cs = 1, nstrip = 0;
   size_t smem = 0;
-  {
+  if (smoother_kind == KC_SMOOTH_JACOBI && coarsening == KC_COARSEN_FULL) {
     cudaFuncAttributes fa{};
     cudaFuncGetAttributes(&fa, k_bottom);
     const size_t smem_max = prop.sharedMemPerBlockOptin - fa.sharedSizeBytes;
@@ -1080,6 +1263,8 @@ int kc_destroy(kc_handle* h) {
     cudaFree(L.v[0]);
     cudaFree(L.v[1]);
     cudaFree(L.f);
+    cudaFree(L.zmem[0]);
+    cudaFree(L.zmem[1]);
   }
   cudaFree(h->x);
   cudaFree(h->p);
@@ -1110,7 +1295,8 @@ int kc_level_dims(kc_handle* h, int level, int* nx, int* ny) {
   if (!h) return KC_EINVAL;
   int rc = check_level(h, level);
   if (rc) return rc;
-  *nx = *ny = h->L[level - 1].m;
+  *nx = h->L[level - 1].m;
+  *ny = h->L[level - 1].ny;
   return KC_OK;
 }
 
@@ -1119,10 +1305,10 @@ int kc_set(kc_handle* h, int level, int which, const double* host, long long ny,
   int rc = check_level(h, level);
   if (rc) return rc;
   Level& L = h->L[level - 1];
-  if (ny != L.m || nx != L.m) KC_FAIL(h, KC_EINVAL, "shape (%lld, %lld) != level %d shape (%d, %d)", ny, nx, level, L.m, L.m);
+  if (ny != L.ny || nx != L.m) KC_FAIL(h, KC_EINVAL, "shape (%lld, %lld) != level %d shape (%d, %d)", ny, nx, level, L.ny, L.m);
   double* dst = which == KC_WHICH_F ? L.f : L.v[L.cur];
   KC_CUDA(h, cudaMemcpy2DAsync(dst + kc_idx(L.P, 0, 0), sizeof(double) * L.P, host, sizeof(double) * L.m,
-                               sizeof(double) * L.m, L.m, cudaMemcpyHostToDevice, h->stream));
+                               sizeof(double) * L.m, L.ny, cudaMemcpyHostToDevice, h->stream));
   KC_CUDA(h, cudaStreamSynchronize(h->stream));
   if (which != KC_WHICH_F) L.vzero = false;
   return KC_OK;
@@ -1133,14 +1319,14 @@ int kc_get(kc_handle* h, int level, int which, double* host, long long ny, long 
   int rc = check_level(h, level);
   if (rc) return rc;
   Level& L = h->L[level - 1];
-  if (ny != L.m || nx != L.m) KC_FAIL(h, KC_EINVAL, "shape (%lld, %lld) != level %d shape (%d, %d)", ny, nx, level, L.m, L.m);
+  if (ny != L.ny || nx != L.m) KC_FAIL(h, KC_EINVAL, "shape (%lld, %lld) != level %d shape (%d, %d)", ny, nx, level, L.ny, L.m);
   if (which != KC_WHICH_F) {
     rc = ex_materialize(h, level - 1);
     if (rc) return rc;
   }
   const double* src = which == KC_WHICH_F ? L.f : L.v[L.cur];
   KC_CUDA(h, cudaMemcpy2DAsync(host, sizeof(double) * L.m, src + kc_idx(L.P, 0, 0), sizeof(double) * L.P,
-                               sizeof(double) * L.m, L.m, cudaMemcpyDeviceToHost, h->stream));
+                               sizeof(double) * L.m, L.ny, cudaMemcpyDeviceToHost, h->stream));
   KC_CUDA(h, cudaStreamSynchronize(h->stream));
   return KC_OK;
 }
@@ -1158,8 +1344,8 @@ int kc_restrict_residual(kc_handle* h, int level) {
   if (!h) return KC_EINVAL;
   int rc = check_level(h, level);
   if (rc) return rc;
-  if (level == h->n || h->L[level - 1].m < 3)
-    KC_FAIL(h, KC_EINVAL, "fine ny must be odd and >= 3, got %d", h->L[level - 1].m);
+  if (level == h->n || h->L[level - 1].ny < 3)
+    KC_FAIL(h, KC_EINVAL, "fine ny must be odd and >= 3, got %d", h->L[level - 1].ny);
   return ex_restrict(h, level - 1);
 }
 
@@ -1189,14 +1375,14 @@ int kc_apply(kc_handle* h, int level, int residual, double* out, long long ny, l
   int rc = check_level(h, level);
   if (rc) return rc;
   Level& L = h->L[level - 1];
-  if (ny != L.m || nx != L.m) KC_FAIL(h, KC_EINVAL, "shape (%lld, %lld) != level %d shape (%d, %d)", ny, nx, level, L.m, L.m);
+  if (ny != L.ny || nx != L.m) KC_FAIL(h, KC_EINVAL, "shape (%lld, %lld) != level %d shape (%d, %d)", ny, nx, level, L.ny, L.m);
   if ((rc = ex_materialize(h, level - 1))) return rc;
   double* t = L.v[L.cur ^ 1];
-  if (residual) k_apply<true><<<grid2(L.m, L.m), kBlock, 0, h->stream>>>(L.v[L.cur], L.f, t, L.m, L.P, L.st);
-  else k_apply<false><<<grid2(L.m, L.m), kBlock, 0, h->stream>>>(L.v[L.cur], L.f, t, L.m, L.P, L.st);
+  if (residual) k_apply<true><<<grid2(L.m, L.ny), kBlock, 0, h->stream>>>(L.v[L.cur], L.f, t, L.ny, L.m, L.P, L.st);
+  else k_apply<false><<<grid2(L.m, L.ny), kBlock, 0, h->stream>>>(L.v[L.cur], L.f, t, L.ny, L.m, L.P, L.st);
   KC_LAUNCH_CHECK(h);
   KC_CUDA(h, cudaMemcpy2DAsync(out, sizeof(double) * L.m, t + kc_idx(L.P, 0, 0), sizeof(double) * L.P,
-                               sizeof(double) * L.m, L.m, cudaMemcpyDeviceToHost, h->stream));
+                               sizeof(double) * L.m, L.ny, cudaMemcpyDeviceToHost, h->stream));
   KC_CUDA(h, cudaStreamSynchronize(h->stream));
   return KC_OK;
 }
@@ -1341,7 +1527,7 @@ int kc_fill_zero(kc_handle* h, int level, int which) {
   if (rc) return rc;
   Level& L = h->L[level - 1];
   if (which == KC_WHICH_F) {
-    k_zero<<<grid2(L.m, L.m), kBlock, 0, h->stream>>>(L.f, L.m, L.P);
+    k_zero<<<grid2(L.m, L.ny), kBlock, 0, h->stream>>>(L.f, L.ny, L.m, L.P);
     KC_LAUNCH_CHECK(h);
   } else {
     L.vzero = true;
@@ -1478,14 +1664,14 @@ int ensure_pcg_buffers(kc_handle* h) {
 int upload_interior(kc_handle* h, double* dst, const double* host) {
   const Level& L = h->L[0];
   KC_CUDA(h, cudaMemcpy2DAsync(dst + kc_idx(L.P, 0, 0), sizeof(double) * L.P, host, sizeof(double) * L.m,
-                               sizeof(double) * L.m, L.m, cudaMemcpyHostToDevice, h->stream));
+                               sizeof(double) * L.m, L.ny, cudaMemcpyHostToDevice, h->stream));
   return KC_OK;
 }
 
 int download_interior(kc_handle* h, double* host, const double* src) {
   const Level& L = h->L[0];
   KC_CUDA(h, cudaMemcpy2DAsync(host, sizeof(double) * L.m, src + kc_idx(L.P, 0, 0), sizeof(double) * L.P,
-                               sizeof(double) * L.m, L.m, cudaMemcpyDeviceToHost, h->stream));
+                               sizeof(double) * L.m, L.ny, cudaMemcpyDeviceToHost, h->stream));
   return KC_OK;
 }
 
@@ -1812,10 +1998,10 @@ extern "C" int kc_set_device(kc_handle* h, int level, int which, const double* d
   int rc = check_level(h, level);
   if (rc) return rc;
   Level& L = h->L[level - 1];
-  if (ny != L.m || nx != L.m) KC_FAIL(h, KC_EINVAL, "shape (%lld, %lld) != level %d shape (%d, %d)", ny, nx, level, L.m, L.m);
+  if (ny != L.ny || nx != L.m) KC_FAIL(h, KC_EINVAL, "shape (%lld, %lld) != level %d shape (%d, %d)", ny, nx, level, L.ny, L.m);
   double* dst = which == KC_WHICH_F ? L.f : L.v[L.cur];
   KC_CUDA(h, cudaMemcpy2DAsync(dst + kc_idx(L.P, 0, 0), sizeof(double) * L.P, dev, sizeof(double) * pitch,
-                               sizeof(double) * L.m, L.m, cudaMemcpyDeviceToDevice, h->stream));
+                               sizeof(double) * L.m, L.ny, cudaMemcpyDeviceToDevice, h->stream));
   KC_CUDA(h, cudaStreamSynchronize(h->stream));
   if (which != KC_WHICH_F) L.vzero = false;
   return KC_OK;
@@ -1827,11 +2013,11 @@ extern "C" int kc_get_device(kc_handle* h, int level, int which, double* dev, lo
   int rc = check_level(h, level);
   if (rc) return rc;
   Level& L = h->L[level - 1];
-  if (ny != L.m || nx != L.m) KC_FAIL(h, KC_EINVAL, "shape (%lld, %lld) != level %d shape (%d, %d)", ny, nx, level, L.m, L.m);
+  if (ny != L.ny || nx != L.m) KC_FAIL(h, KC_EINVAL, "shape (%lld, %lld) != level %d shape (%d, %d)", ny, nx, level, L.ny, L.m);
   if (which != KC_WHICH_F && (rc = ex_materialize(h, level - 1))) return rc;
   const double* src = which == KC_WHICH_F ? L.f : L.v[L.cur];
   KC_CUDA(h, cudaMemcpy2DAsync(dev, sizeof(double) * pitch, src + kc_idx(L.P, 0, 0), sizeof(double) * L.P,
-                               sizeof(double) * L.m, L.m, cudaMemcpyDeviceToDevice, h->stream));
+                               sizeof(double) * L.m, L.ny, cudaMemcpyDeviceToDevice, h->stream));
   KC_CUDA(h, cudaStreamSynchronize(h->stream));
   return KC_OK;
 }

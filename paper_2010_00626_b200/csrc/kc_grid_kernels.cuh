@@ -18,10 +18,10 @@
 template <bool ZERO_U>
 __global__ void __launch_bounds__(KC_BX* KC_BY)
     k_jacobi(const double* __restrict__ u, const double* __restrict__ f, double* __restrict__ out,
-             int m, int P, St9 s) {
+             int m, int nx, int P, St9 s) {  // m rows, nx columns
   const int x = blockIdx.x * KC_BX + threadIdx.x;
   const int y0 = (blockIdx.y * KC_BY + threadIdx.y) * KC_RY;
-  if (x >= m || y0 >= m) return;
+  if (x >= nx || y0 >= m) return;
   const size_t i0 = kc_idx(P, y0, x);
   if (ZERO_U) {
 #pragma unroll
@@ -54,10 +54,10 @@ __global__ void __launch_bounds__(KC_BX* KC_BY)
 template <bool ZERO_U>
 __global__ void __launch_bounds__(KC_BX* KC_BY)
     k_resid_restrict(const double* __restrict__ u, const double* __restrict__ f,
-                     double* __restrict__ fc, int mc, int P, int Pc, St9 s) {
+                     double* __restrict__ fc, int mc, int mcx, int P, int Pc, St9 s) {  // mc x mcx coarse
   const int p = blockIdx.x * KC_BX + threadIdx.x;
   const int q = blockIdx.y * KC_BY + threadIdx.y;
-  if (p >= mc || q >= mc) return;
+  if (p >= mcx || q >= mc) return;
   const int y = 2 * q + 1, x = 2 * p + 1;
   double r[3][3];
 #pragma unroll
@@ -80,10 +80,10 @@ __global__ void __launch_bounds__(KC_BX* KC_BY)
 // v += P vc (in place).  V_ZERO: v is the all-zero guess -> v = 0.0 + e.
 template <bool V_ZERO>
 __global__ void __launch_bounds__(KC_BX* KC_BY)
-    k_prolong_add(double* __restrict__ v, const double* __restrict__ vc, int m, int P, int Pc) {
+    k_prolong_add(double* __restrict__ v, const double* __restrict__ vc, int m, int nx, int P, int Pc) {
   const int x = blockIdx.x * KC_BX + threadIdx.x;
   const int y = blockIdx.y * KC_BY + threadIdx.y;
-  if (x >= m || y >= m) return;
+  if (x >= nx || y >= m) return;
   auto cp = [&](int q, int p) { return __ldg(vc + kc_idx(Pc, q, p)); };
   const double e = kc_prolong_val(y, x, cp);
   const size_t i = kc_idx(P, y, x);
@@ -93,11 +93,11 @@ __global__ void __launch_bounds__(KC_BX* KC_BY)
 // out = A u (stencil.py:108-113) or f - A u (stencil.py:116-120)
 template <bool RES>
 __global__ void __launch_bounds__(KC_BX* KC_BY)
-    k_apply(const double* __restrict__ u, const double* __restrict__ f, double* __restrict__ out, int m, int P,
-            St9 s) {
+    k_apply(const double* __restrict__ u, const double* __restrict__ f, double* __restrict__ out, int m, int nx,
+            int P, St9 s) {
   const int x = blockIdx.x * KC_BX + threadIdx.x;
   const int y = blockIdx.y * KC_BY + threadIdx.y;
-  if (x >= m || y >= m) return;
+  if (x >= nx || y >= m) return;
   const size_t i = kc_idx(P, y, x);
   const double a = kc_apply9(u + i, P, s);
   out[i] = RES ? DSUB(__ldg(f + i), a) : a;
@@ -111,10 +111,10 @@ __global__ void k_coarsest(double* __restrict__ v, const double* __restrict__ f,
 }
 
 // Zero the interior of a level (ghost ring is already zero).
-__global__ void k_zero(double* __restrict__ v, int m, int P) {
+__global__ void k_zero(double* __restrict__ v, int m, int nx, int P) {
   const int x = blockIdx.x * KC_BX + threadIdx.x;
   const int y = blockIdx.y * KC_BY + threadIdx.y;
-  if (x >= m || y >= m) return;
+  if (x >= nx || y >= m) return;
   v[kc_idx(P, y, x)] = 0.0;
 }
 
@@ -145,11 +145,11 @@ __device__ __forceinline__ double kc_block_sum(double v) {
 // kind 0: sum a*b ; kind 1: sum (f - A a)^2 (b = f)
 template <int KIND>
 __global__ void __launch_bounds__(KC_RED_THREADS)
-    k_red_partial(const double* __restrict__ a, const double* __restrict__ b, int m, int P, St9 s,
+    k_red_partial(const double* __restrict__ a, const double* __restrict__ b, int m, int nx, int P, St9 s,
                   double* __restrict__ part) {
   double acc = 0.0;
   for (int y = blockIdx.x; y < m; y += gridDim.x) {
-    for (int x = threadIdx.x; x < m; x += KC_RED_THREADS) {
+    for (int x = threadIdx.x; x < nx; x += KC_RED_THREADS) {
       const size_t i = kc_idx(P, y, x);
       if (KIND == 0) {
         acc = fma(__ldg(a + i), __ldg(b + i), acc);

@@ -197,10 +197,6 @@ class CudaGridState:
 
     def __init__(self, spec: HierarchySpec, ops: list[Stencil9], smoother: SmootherSpec,
                  nu1: int, nu2: int, device: int = 0):
-        if spec.coarsening is not Coarsening.FULL_STANDARD:
-            raise ValueError("the B200 engine implements full coarsening only (semi-y is SURVEY.md §8(f) row 1)")
-        if smoother.kind is not SmootherKind.DAMPED_JACOBI:
-            raise ValueError("the B200 engine implements damped Jacobi only (zebra is SURVEY.md §8(f) row 1)")
         if len(ops) != spec.n:
             raise ValueError(f"need {spec.n} operators, got {len(ops)}")
         self.spec = spec
@@ -213,8 +209,9 @@ class CudaGridState:
         self._h = None
         w = np.ascontiguousarray(np.concatenate([op.w.ravel() for op in ops]), dtype=np.float64)
         h = C.c_void_p()
-        N.check(N.lib.kc_create(spec.n, N.KC_COARSEN_FULL, N.dptr(w), N.KC_SMOOTH_JACOBI,
-                                float(smoother.omega), nu1, nu2, device, C.byref(h)), None)
+        N.check(N.lib.kc_create(spec.n, N.COARSENING_KIND[spec.coarsening.value], N.dptr(w),
+                                N.SMOOTHER_KIND[smoother.kind.value], float(smoother.omega), nu1, nu2, device,
+                                C.byref(h)), None)
         self._h = h
         self.v = _LevelData(self, N.KC_WHICH_V)
         self.f = _LevelData(self, N.KC_WHICH_F)

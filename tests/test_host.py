@@ -143,12 +143,17 @@ def test_no_gpu_fails_loudly():
         build_state(ProblemSpec(1e-4, 45.0), CycleConfig(n=3))
 
 
-def test_unsupported_variants_rejected_before_device():
+def test_zebra_and_semi_coarsening_reach_the_engine():
+    """Zebra smoothers and y-semi-coarsening are engine paths now (§8(f)1): the
+    Python layer passes them to kc_create, which without a GPU fails with
+    CudaUnavailableError (never a silent CPU fallback) and on a B200 builds."""
+    from paper_2010_00626_b200 import CudaUnavailableError
     from paper_2010_00626_b200.cycle import CudaGridState
-    spec = build_hierarchy(3, Coarsening.SEMI_Y)
-    ops = [Stencil9(np.eye(3))] * 3
-    with pytest.raises(ValueError):
-        CudaGridState(spec, ops, SmootherSpec(SmootherKind.DAMPED_JACOBI), 2, 2)
-    spec = build_hierarchy(3, Coarsening.FULL_STANDARD)
-    with pytest.raises(ValueError):
-        CudaGridState(spec, ops, SmootherSpec(SmootherKind.ZEBRA_X), 2, 2)
+    w = np.array([[0.1, -0.5, 0.1], [-0.5, 2.0, -0.5], [0.1, -0.5, 0.1]])
+    for co, kind in ((Coarsening.SEMI_Y, SmootherKind.DAMPED_JACOBI), (Coarsening.FULL_STANDARD, SmootherKind.ZEBRA_X),
+                     (Coarsening.SEMI_Y, SmootherKind.ZEBRA_ALTERNATING)):
+        spec = build_hierarchy(3, co)
+        try:
+            CudaGridState(spec, [Stencil9(w)] * 3, SmootherSpec(kind), 2, 2).close()
+        except CudaUnavailableError:
+            pass
