@@ -47,6 +47,11 @@ struct St9 {
 #define DADD(a, b) __dadd_rn((a), (b))
 #define DSUB(a, b) __dsub_rn((a), (b))
 #define DMUL(a, b) __dmul_rn((a), (b))
+// 0.0 + a*b with the product rounded first, as one instruction: fma rounds
+// the exact a*b + 0.0 once, which equals the rounded product for every
+// nonzero result, and -0 + +0 = +0 covers the zero case -- bit-identical to
+// DADD(0.0, DMUL(a, b)), one fp64 issue instead of two.
+#define DMUL0(a, b) __fma_rn((a), (b), 0.0)
 
 // 9-point correlation at p (pointer to u(y,x)), rows at p -/+ S.
 // Accumulation order = scipy.ndimage.correlate's C order: acc = 0, then
@@ -55,8 +60,7 @@ template <typename T>
 __device__ __forceinline__ double kc_apply9(const T* __restrict__ p, int S, const St9& s) {
   const T* ps = p - S;
   const T* pn = p + S;
-  double acc = 0.0;
-  acc = DADD(acc, DMUL(s.w[0], ps[-1]));
+  double acc = DMUL0(s.w[0], ps[-1]);  // 0.0 + w0 u
   acc = DADD(acc, DMUL(s.w[1], ps[0]));
   acc = DADD(acc, DMUL(s.w[2], ps[1]));
   acc = DADD(acc, DMUL(s.w[3], p[-1]));
@@ -71,8 +75,7 @@ __device__ __forceinline__ double kc_apply9(const T* __restrict__ p, int S, cons
 // Same sum from nine register values (a = south row, b = centre row, c = north row).
 __device__ __forceinline__ double kc_sum9(const St9& s, double a0, double a1, double a2, double b0,
                                           double b1, double b2, double c0, double c1, double c2) {
-  double acc = 0.0;
-  acc = DADD(acc, DMUL(s.w[0], a0));
+  double acc = DMUL0(s.w[0], a0);  // 0.0 + w0 a0
   acc = DADD(acc, DMUL(s.w[1], a1));
   acc = DADD(acc, DMUL(s.w[2], a2));
   acc = DADD(acc, DMUL(s.w[3], b0));
@@ -92,7 +95,7 @@ __device__ __forceinline__ double kc_jacobi_pt(double u, double f, double au, do
 // First sweep on an all-zero guess: A*0 == +0 exactly, f - (+0) == f, so the
 // update is 0.0 + c*f (the +0.0 add keeps the sign of zero identical).
 __device__ __forceinline__ double kc_jacobi_zero(double f, double c) {
-  return DADD(0.0, DMUL(c, f));
+  return DMUL0(c, f);
 }
 
 // Full weighting (transfer.py:78-83): numpy evaluates
