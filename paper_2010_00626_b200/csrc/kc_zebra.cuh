@@ -62,35 +62,95 @@ __global__ void k_zebra_rhs_y(double* __restrict__ u, const double* __restrict__
   u[i] = DSUB(__ldg(f + i), acc);
 }
 
-// dgtsv on one line whose right-hand side b(i) = line[i * stride] (in place)
+// dgtsv on one line whose right-hand side b(i) = line[i * stride] (in place).
+// A line solve is one thread's serial recurrence, and a zebra half-sweep has
+// few lines (ny/2, or a handful on semi-coarsened levels), so the SMs hold
+// few warps: every line value and plan entry is fetched KZ_CH steps ahead
+// (software pipelining over two register chunks) instead of one dependent
+// memory round trip per step.
+#define KZ_CH 8
 __device__ __forceinline__ void kz_gtsv_line(double* __restrict__ line, size_t stride, const ZPlan& pl) {
   const int n = pl.n;
-  // forward elimination, carrying the current row
+  // ---- forward elimination over steps i = 0 .. n-2, carrying row i ----
   double cur = line[0];
-  for (int i = 0; i < n - 1; ++i) {
-    const double nxt = line[(size_t)(i + 1) * stride];
-    const double fact = __ldg(pl.fact + i);
-    if (!__ldg(pl.piv + i)) {  // B(i+1) = B(i+1) - FACT*B(i)
-      line[(size_t)i * stride] = cur;
-      cur = DSUB(nxt, DMUL(fact, cur));
-    } else {  // interchange: B(i) = B(i+1); B(i+1) = B(i) - FACT*B(i+1)
-      line[(size_t)i * stride] = nxt;
-      cur = DSUB(cur, DMUL(fact, nxt));
+  {
+    double nv[2][KZ_CH], fa[2][KZ_CH];
+    unsigned char pv[2][KZ_CH];
+    auto fetch = [&](int buf, int i0) {
+#pragma unroll
+      for (int k = 0; k < KZ_CH; ++k) {
+        const int i = i0 + k;
+        if (i < n - 1) {
+          nv[buf][k] = line[(size_t)(i + 1) * stride];
+          fa[buf][k] = __ldg(pl.fact + i);
+          pv[buf][k] = __ldg(pl.piv + i);
+        }
+      }
+    };
+    fetch(0, 0);
+    for (int i0 = 0; i0 < n - 1; i0 += 2 * KZ_CH) {
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int ib = i0 + half * KZ_CH;
+        if (ib >= n - 1) break;
+        fetch(half ^ 1, ib + KZ_CH);  // next chunk in flight while this one is eliminated
+#pragma unroll
+        for (int k = 0; k < KZ_CH; ++k) {
+          const int i = ib + k;
+          if (i < n - 1) {
+            if (!pv[half][k]) {  // B(i+1) = B(i+1) - FACT*B(i)
+              line[(size_t)i * stride] = cur;
+              cur = DSUB(nv[half][k], DMUL(fa[half][k], cur));
+            } else {  // interchange: B(i) = B(i+1); B(i+1) = B(i) - FACT*B(i+1)
+              line[(size_t)i * stride] = nv[half][k];
+              cur = DSUB(cur, DMUL(fa[half][k], nv[half][k]));
+            }
+          }
+        }
+      }
     }
   }
-  // back substitution: B(i) = (B(i) - DU(i) B(i+1) - DL(i) B(i+2)) / D(i)
+  // ---- back substitution: B(i) = (B(i) - DU(i) B(i+1) - DL(i) B(i+2)) / D(i) ----
   double b1 = __ddiv_rn(cur, __ldg(pl.d + n - 1));
   line[(size_t)(n - 1) * stride] = b1;
   if (n < 2) return;
+  // row n-2 was stored by the forward pass; it is re-read here
   double b0 = __ddiv_rn(DSUB(line[(size_t)(n - 2) * stride], DMUL(__ldg(pl.du + n - 2), b1)), __ldg(pl.d + n - 2));
   line[(size_t)(n - 2) * stride] = b0;
-  for (int i = n - 3; i >= 0; --i) {
-    const double v = __ddiv_rn(
-        DSUB(DSUB(line[(size_t)i * stride], DMUL(__ldg(pl.du + i), b0)), DMUL(__ldg(pl.dl + i), b1)),
-        __ldg(pl.d + i));
-    line[(size_t)i * stride] = v;
-    b1 = b0;
-    b0 = v;
+  {
+    double bv[2][KZ_CH], dv[2][KZ_CH], uv[2][KZ_CH], lv2[2][KZ_CH];
+    auto fetch = [&](int buf, int i0) {  // rows i0, i0-1, ..., i0-KZ_CH+1
+#pragma unroll
+      for (int k = 0; k < KZ_CH; ++k) {
+        const int i = i0 - k;
+        if (i >= 0) {
+          bv[buf][k] = line[(size_t)i * stride];
+          dv[buf][k] = __ldg(pl.d + i);
+          uv[buf][k] = __ldg(pl.du + i);
+          lv2[buf][k] = __ldg(pl.dl + i);
+        }
+      }
+    };
+    fetch(0, n - 3);
+    for (int i0 = n - 3; i0 >= 0; i0 -= 2 * KZ_CH) {
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int ib = i0 - half * KZ_CH;
+        if (ib < 0) break;
+        fetch(half ^ 1, ib - KZ_CH);
+#pragma unroll
+        for (int k = 0; k < KZ_CH; ++k) {
+          const int i = ib - k;
+          if (i >= 0) {
+            const double v = __ddiv_rn(DSUB(DSUB(bv[half][k], DMUL(uv[half][k], b0)), DMUL(lv2[half][k], b1)),
+                                       dv[half][k]);
+            line[(size_t)i * stride] = v;
+            b1 = b0;
+            b0 = v;
+          }
+        }
+      }
+    }
   }
 }
 
