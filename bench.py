@@ -409,6 +409,16 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         per_level[str(p["level"])] += p["ms"]
     cycle_ms_eager = sum(p["ms"] for p in prof)
     bottom_ms = sum(p["ms"] for p in prof if p["op"] == "bottom")
+    # SURVEY.md §8(d) reported metrics: coarse-level fraction of the cycle
+    # (levels of side <= 511, i.e. the tile kernels and the cluster bottom
+    # kernel, from the eager per-op profile) and the cycle's achieved GB/s
+    # over the algorithmic bytes B(kappa, n) of the fused decomposition
+    side = lambda lev: 2 ** (n - lev + 1) - 1  # noqa: E731
+    coarse_ms = sum(p["ms"] for p in prof if side(p["level"]) <= 511)
+    nu = 4
+    calls = [kc.costmodel.level_calls(math.inf if best == "W" else kbest, lev) for lev in range(1, n + 1)]
+    b_cycle = sum(calls[lev - 1] * ((24 * nu + 16) * side(lev) ** 2 + 16 * side(lev + 1) ** 2)
+                  for lev in range(1, n)) + 16 * calls[n - 1]
 
     # ---- e2e through the public API (pinned host v0, solution back) --------
     e2e = None
@@ -497,7 +507,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "sweep": sweep,
             "pcg": pcg,
             "cycle_profile": {"eager_cycle_ms": cycle_ms_eager, "bottom_kernel_ms": bottom_ms,
-                              "per_level_ms": per_level},
+                              "per_level_ms": per_level,
+                              "coarse_fraction_le511": coarse_ms / cycle_ms_eager if cycle_ms_eager else None,
+                              "algorithmic_bytes_per_cycle": b_cycle,
+                              "cycle_gbs": b_cycle / (ms_per_step / cycles * 1e-3) / 1e9 if cycles else None,
+                              "cycle_frac_of_hbm_peak": (b_cycle / (ms_per_step / cycles * 1e-3) / 1e9 / peak
+                                                         if cycles else None)},
         }
         print(json.dumps(line), flush=True)
     state.close()
