@@ -586,3 +586,43 @@ def test_distributed_cuda_strips_bit_exact(world, kappa):
         for c in range(2):
             assert np.array_equal(got[c], ref[c]), c
         assert e == pytest.approx(e_ref, rel=1e-13)
+
+
+# ---------------------------------------------------------------------------
+# full-size properties (BASELINE sizes and beyond): the fused / cluster path
+# against the independently pinned per-op kernels, bit for bit
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n,kappas", [(12, (1, 2, 3)), (13, (2,)), (14, (1,))])
+def test_full_size_fused_equals_per_op(n, kappas):
+    """At 4095^2, 8191^2 and 16383^2 (config C4's global size) the native cycle
+    (streaming kernels, tile kernels, 16-CTA cluster bottom kernel) must give
+    the same iterate as the per-op kernels, which are pinned to the reference
+    kernel by kernel.  Size-independent bar: bit-identical arrays."""
+    m = 2 ** n - 1
+    rng = np.random.default_rng(n)
+    v0 = rng.random((m, m))
+    f0 = rng.standard_normal((m, m)) * 1e-3
+    problem = ProblemSpec(1e-4, 45.0)
+    for kappa in kappas:
+        cfg = CycleConfig(n=n, kappa=kappa)
+        out = []
+        for fuse in (1, 0):
+            st = build_state(problem, cfg)
+            st.set_option("fuse", fuse)
+            st.v[0], st.f[0] = v0, f0
+            run_cycle(st, cfg, CycleStats.for_levels(n))
+            out.append(st.v[0])
+            st.close()
+        assert np.array_equal(out[0], out[1]), (n, kappa)
+
+
+def test_full_size_solve_reduces_residual_monotonically():
+    """n = 13 F-cycle solve to 1e-10 relative residual: converged, every cycle
+    reduces the residual (the asymptotic factor of the reference's problem)."""
+    cfg = CycleConfig(n=13, kappa=2)
+    rep = solve_standalone(ProblemSpec(1e-4, 45.0, seed=0), cfg, 1e10, max_cycles=1000, stop="residual")
+    assert rep.status == "converged"
+    res = rep.residual_history
+    assert all(b < a for a, b in zip(res, res[1:]))
+    assert res[-1] <= res[0] / 1e10
