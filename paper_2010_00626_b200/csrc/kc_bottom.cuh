@@ -137,7 +137,7 @@ enum BotOp {
   PH_TINY = 8, PH_CSYNC = 9
 };
 #ifndef KC_BOT_TINY_M
-#define KC_BOT_TINY_M 7  // frames on sides <= this run as PH_TINY (one warp; 15 measured slower)
+#define KC_BOT_TINY_M 15  // frames on sides <= this run as PH_TINY (side 15 on 8 warps)
 #endif
 #define KC_BOT_FUSE_M 15  // PH_RR / PH_PJ on sides <= this (latency-bound levels)
 // Descriptor: bits 0-3 op, 4-6 level d, 7 src buffer, 8 zero guess, 9 child
@@ -419,21 +419,25 @@ struct BotTiny {
   double* sm;
   const BotLv* lv;
   const St9* tab;
-  int nu1, nu2, lane;
+  int nu1, nu2, tid, nth;  // nth = 32: one warp (__syncwarp); 256: warps 0-7 (named barrier 1)
+  __device__ __forceinline__ void sync() const {
+    if (nth == 32) __syncwarp();
+    else asm volatile("bar.sync 1, 256;" ::: "memory");
+  }
   __device__ __forceinline__ double* buf(const BotLv& L, int b) const { return sm + (b ? L.vo1 : L.vo0); }
   __device__ __forceinline__ void relax(const BotLv& L, const St9& st, int count, int& cur, int& vz) const {
     int i = 0;
     const double* f = sm + L.fo;
     if (count >= 2 && vz) {
-      bot_j2z(buf(L, cur), f, L, st, lane, 32, BotPush{nullptr, nullptr, -1});
-      __syncwarp();
+      bot_j2z(buf(L, cur), f, L, st, tid, nth, BotPush{nullptr, nullptr, -1});
+      sync();
       vz = 0;
       i = 2;
     }
     for (; i < count; ++i) {
-      bot_stencil<1>(true, vz, buf(L, cur), buf(L, cur ^ 1), f, L.m, L.m, L.S, L.inv, st, lane, 32, L.nitem1,
+      bot_stencil<1>(true, vz, buf(L, cur), buf(L, cur ^ 1), f, L.m, L.m, L.S, L.inv, st, tid, nth, L.nitem1,
                      BotPush{nullptr, nullptr, -1});
-      __syncwarp();
+      sync();
       vz = 0;
       cur ^= 1;
     }
@@ -443,20 +447,20 @@ struct BotTiny {
     relax(L, st, nu1, cur, vz);
     const double* f = sm + L.fo;
     if (!vz) {
-      bot_stencil<1>(false, false, buf(L, cur), buf(L, cur ^ 1), f, L.m, L.m, L.S, L.inv, st, lane, 32, L.nitem1,
+      bot_stencil<1>(false, false, buf(L, cur), buf(L, cur ^ 1), f, L.m, L.m, L.S, L.inv, st, tid, nth, L.nitem1,
                      BotPush{nullptr, nullptr, -1});
-      __syncwarp();
+      sync();
     }
     const BotLv C = lv[d + 1];
-    bot_restrict(vz ? f : buf(L, cur ^ 1), L, sm + C.fo, C.m, C.S, sm + C.vo0, tab[d + 1].center, cc, lane, 32,
+    bot_restrict(vz ? f : buf(L, cur ^ 1), L, sm + C.fo, C.m, C.S, sm + C.vo0, tab[d + 1].center, cc, tid, nth,
                  BotPush{nullptr, nullptr, -1});
-    __syncwarp();
+    sync();
   }
   // prolongation of child buffer cb + post-smoothing
   __device__ __forceinline__ void up(int d, const BotLv& L, const St9& st, int& cur, int& vz, int cb) const {
     const BotLv C = lv[d + 1];
-    bot_prolong(buf(L, cur), buf(C, cb), L, C.m, C.S, vz, lane, 32, BotPush{nullptr, nullptr, -1});
-    __syncwarp();
+    bot_prolong(buf(L, cur), buf(C, cb), L, C.m, C.S, vz, tid, nth, BotPush{nullptr, nullptr, -1});
+    sync();
     vz = 0;
     relax(L, st, nu2, cur, vz);
   }
@@ -477,7 +481,9 @@ struct BotTiny {
     if (kap > 1) leaf(d + 1, cc, cz);
     up(d, L, st, cur, vz, cc);
   }
-  __device__ void frame(int d, int kap, int nlev, int& cur, int& vz) const {
+  // side 15 on warps 0-7; its side-7 children (kappa, kappa - 1;
+  // cycle.py:215-218) on warp 0 while warps 1-7 wait at the named barrier
+  __device__ void frame(int d, int kap, int nlev, int& cur, int& vz, int* child_buf) const {
     if (d + 2 == nlev) {
       leaf(d, cur, vz);
       return;
@@ -486,14 +492,18 @@ struct BotTiny {
       frame7(d, kap, cur, vz);
       return;
     }
-    // side 15: children are side-7 frames with kappa and kappa - 1 (cycle.py:215-218)
     const BotLv L = lv[d];
     const St9 st = tab[d];
     down(d, L, st, cur, vz, false);
-    int cc = 0, cz = 1;
-    frame7(d + 1, kap, cc, cz);
-    if (kap > 1) frame7(d + 1, kap - 1, cc, cz);
-    up(d, L, st, cur, vz, cc);
+    if (tid < 32) {
+      const BotTiny w{sm, lv, tab, nu1, nu2, tid, 32};
+      int cc = 0, cz = 1;
+      w.frame7(d + 1, kap, cc, cz);
+      if (kap > 1) w.frame7(d + 1, kap - 1, cc, cz);
+      if (tid == 0) *child_buf = cc;
+    }
+    sync();
+    up(d, L, st, cur, vz, *child_buf);
   }
 };
 
@@ -502,6 +512,7 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
   __shared__ St9 tab[KC_BOT_MAXLEV];
   __shared__ BotLv lv[KC_BOT_MAXLEV];
   __shared__ unsigned sched[KC_BOT_MAXPH];
+  __shared__ int tiny_child;
   cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
   const int rank = (int)cl.block_rank(), cs = (int)cl.num_blocks();
   const int nlev = bp.nlev, nstrip = bp.nstrip;
@@ -637,10 +648,10 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
       if (strip)  // from CTA 0's level, at this strip's first coarse row
         vc = cl.map_shared_rank(const_cast<double*>(vc), 0) + (L.a / 2) * C.S;
       bot_prolong(u, vc, L, C.m, C.S, zero, tid, nth, bot_push(u, L, strip, rank, cs));
-    } else {  // PH_TINY (warp 0 of CTA 0)
-      const BotTiny t{sm, lv, tab, bp.nu1, bp.nu2, tid};
+    } else {  // PH_TINY (CTA 0: warp 0 for sides <= 7, warps 0-7 for side 15)
+      const BotTiny t{sm, lv, tab, bp.nu1, bp.nu2, tid, nth};
       int cur = src, vz = zero;
-      t.frame(d, BD_KAP(e), nlev, cur, vz);
+      t.frame(d, BD_KAP(e), nlev, cur, vz, &tiny_child);
     }
     if (strip) clu_sync();
     else bot_sync(g);
