@@ -94,7 +94,9 @@ struct Level {
 enum OpKind : int { OP_RELAX, OP_RESTRICT, OP_ZERO, OP_PROLONG, OP_COARSEST, OP_BOTTOM, OP_PRE, OP_POST };
 #define KC_FUSE_MAXNU 4      // fused streaming kernels exist for nu <= 4
 #define KC_FUSE_MIN_M 127    // HBM levels handled by the fused kernels
+#ifndef KC_TILE_MAX_M
 #define KC_TILE_MAX_M 511    // up to this side the overlapped-tile kernels beat streaming
+#endif
 struct Op {
   int kind, level, a, b;
 };
@@ -563,9 +565,10 @@ inline int ks_npb(int D) { return (KS_BAND - 1 - D - 2 * ((D + 2) / 2)) / 2; }  
 // a contiguous run of ceil((mc+1)/K) coarse rows, so all warps finish
 // together and the per-warp warm-up stays a small fraction of its rows.
 int ks_choose_nq(int mc, int nbands, int slots) {
+  const int minnq = 2;
   const int k = slots / nbands > 1 ? slots / nbands : 1;
   const int nq = (mc + 1 + k - 1) / k;
-  return nq > 2 ? nq : 2;
+  return nq > minnq ? nq : minnq;
 }
 
 typedef void (*KsFn)(StreamParams);
