@@ -140,6 +140,7 @@ struct kc_handle {
   std::map<std::pair<int, int>, SolveGraph> solve_graphs;       // (kappa, cur0)
   std::map<std::tuple<int, int, int>, SolveGraph> pcg_graphs;   // (kappa, measure x, cur0)
   PcgState* d_pcg = nullptr;
+  double* d_pcgpart = nullptr;  // per-block partials of k_pcg_apply_dot
   double* d_npart = nullptr;  // norm partials of the fused level-1 kernels (per warp: post; per lane: pre)
   double* d_nblk = nullptr;    // block sums of k_norms_lanes
   unsigned* d_ncount = nullptr;
@@ -1262,6 +1263,7 @@ int kc_destroy(kc_handle* h) {
   cudaFree(h->d_solve);
   cudaFree(h->d_hist);
   cudaFree(h->d_pcg);
+  cudaFree(h->d_pcgpart);
   for (Level& L : h->L) {
     cudaFree(L.v[0]);
     cudaFree(L.v[1]);
@@ -1654,6 +1656,7 @@ int kc_solve(kc_handle* h, int kappa, int stop_mode, double target_reduction, in
 namespace {
 int ensure_pcg_buffers(kc_handle* h) {
   const size_t bytes = h->L[0].elems * sizeof(double);
+  if (!h->d_pcgpart) KC_CUDA(h, cudaMalloc(&h->d_pcgpart, sizeof(double) * (size_t)KC_PCG_BLOCKS(h->L[0].m)));
   double** bufs[4] = {&h->x, &h->p, &h->ap, &h->fb};
   for (double** b : bufs) {
     if (*b) continue;
@@ -1727,8 +1730,8 @@ int get_pcg_graph(kc_handle* h, int kappa, bool mx, SolveGraph** out) {
   SolveGraph sg;
   // A: Ap, pAp, x/r update, measure
   KC_CUDA(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-  k_pcg_apply_dot<<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(h->p, h->ap, m, P, L0.st, h->d_part);
-  k_red_final<false><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_part, KC_RED_BLOCKS, h->d_scal + S_PAP);
+  k_pcg_apply_dot<<<grid2(m, m, KC_RY), kBlock, 0, h->stream>>>(h->p, h->ap, m, P, L0.st, h->d_pcgpart);
+  k_red_final<false><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_pcgpart, KC_PCG_BLOCKS(m), h->d_scal + S_PAP);
   if (mx)
     k_pcg_update_xr<true><<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(h->x, r, h->p, h->ap, m, P, h->d_scal, S_RZ,
                                                                             S_PAP, h->d_part, st);
@@ -1876,9 +1879,9 @@ extern "C" int kc_pcg(kc_handle* h, int kappa, const double* f, const double* x0
       st = KC_STATUS_BREAKDOWN;
     } else {
       for (it = 1; it <= max_it; ++it) {
-        k_pcg_apply_dot<<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(h->p, h->ap, m, P, L0.st, h->d_part);
+        k_pcg_apply_dot<<<grid2(m, m, KC_RY), kBlock, 0, h->stream>>>(h->p, h->ap, m, P, L0.st, h->d_pcgpart);
         KC_LAUNCH_CHECK(h);
-        k_red_final<false><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_part, KC_RED_BLOCKS, h->d_scal + S_PAP);
+        k_red_final<false><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_pcgpart, KC_PCG_BLOCKS(m), h->d_scal + S_PAP);
         KC_LAUNCH_CHECK(h);
         if (mx)
           k_pcg_update_xr<true><<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(h->x, r, h->p, h->ap, m, P, h->d_scal,

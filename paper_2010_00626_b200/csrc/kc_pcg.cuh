@@ -24,21 +24,44 @@ __global__ void __launch_bounds__(KC_RED_THREADS)
     }
 }
 
-// ap = A p ; partial[b] = sum p*ap (krylov.py:109-110)
-__global__ void __launch_bounds__(KC_RED_THREADS)
+// ap = A p ; partial[block] = sum p*ap (krylov.py:109-110).  A thread owns
+// one column and slides a 3x3 register window down KC_RY rows (3 new loads
+// per row instead of 9), like k_jacobi; blocks of KC_BX x KC_BY threads,
+// one deterministic partial per block.
+#define KC_PCG_BLOCKS(m) (((m) + KC_BX - 1) / KC_BX * (((m) + KC_BY * KC_RY - 1) / (KC_BY * KC_RY)))
+__global__ void __launch_bounds__(KC_BX* KC_BY)
     k_pcg_apply_dot(const double* __restrict__ p, double* __restrict__ ap, int m, int P, St9 s,
                     double* __restrict__ part) {
+  const int x = blockIdx.x * KC_BX + threadIdx.x;
+  const int y0 = (blockIdx.y * KC_BY + threadIdx.y) * KC_RY;
   double acc = 0.0;
-  for (int y = blockIdx.x; y < m; y += gridDim.x)
-    for (int xx = threadIdx.x; xx < m; xx += KC_RED_THREADS) {
-      const size_t i = kc_idx(P, y, xx);
-      const double pv = __ldg(p + i);
-      const double a = kc_apply9(p + i, P, s);
-      ap[i] = a;
-      acc = fma(pv, a, acc);
+  if (x < m && y0 < m) {
+    const double* pu = p + kc_idx(P, y0, x);
+    double a0 = __ldg(pu - P - 1), a1 = __ldg(pu - P), a2 = __ldg(pu - P + 1);
+    double b0 = __ldg(pu - 1), b1 = __ldg(pu), b2 = __ldg(pu + 1);
+#pragma unroll
+    for (int k = 0; k < KC_RY; ++k) {
+      if (y0 + k >= m) break;
+      const double* pn = pu + (size_t)(k + 1) * P;
+      const double c0 = __ldg(pn - 1), c1 = __ldg(pn), c2 = __ldg(pn + 1);
+      const double a = kc_sum9(s, a0, a1, a2, b0, b1, b2, c0, c1, c2);
+      ap[kc_idx(P, y0 + k, x)] = a;
+      acc = fma(b1, a, acc);
+      a0 = b0; a1 = b1; a2 = b2;
+      b0 = c0; b1 = c1; b2 = c2;
     }
-  const double t = kc_block_sum(acc);
-  if (threadIdx.x == 0) part[blockIdx.x] = t;
+  }
+  // block tree: warps, then warp 0
+  __shared__ double sh[KC_BX * KC_BY / 32];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  const int t = threadIdx.y * KC_BX + threadIdx.x;
+  if ((t & 31) == 0) sh[t >> 5] = acc;
+  __syncthreads();
+  if (t == 0) {
+    double b = 0.0;
+    for (int w = 0; w < KC_BX * KC_BY / 32; ++w) b += sh[w];
+    part[blockIdx.y * gridDim.x + blockIdx.x] = b;
+  }
 }
 
 // Device-resident PCG loop state (kc_engine.cu get_pcg_graph): iterations
