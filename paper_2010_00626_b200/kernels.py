@@ -11,7 +11,8 @@ per-kernel parity tests and drop-in convenience; the solvers never call them.
   relax                  smoother.py:138-163     k_jacobi x count
   restrict               transfer.py:70-83       k_resid_restrict (zero u)
   prolong                transfer.py:46-58       k_prolong_add (zero v)
-  coarsest_solve         cycle.py:182-190        k_coarsest
+  coarsest_solve         cycle.py:182-200        k_coarsest / k_coarsest_line (semi-y)
+  zebra_line_sweep       smoother.py:107-135     k_zebra_rhs_* + k_zebra_solve_*
   norm2 / dot-free norm  mesh.py:93-95           k_red_partial + k_red_final
 """
 
@@ -25,7 +26,7 @@ from .smoother import SmootherKind, SmootherSpec
 from .stencil import Stencil9
 
 __all__ = ["apply", "residual", "damped_jacobi_sweep", "relax", "restrict", "prolong",
-           "coarsest_solve", "norm2"]
+           "coarsest_solve", "zebra_line_sweep", "norm2"]
 
 _ID = Stencil9([[0.0, 0.0, 0.0], [0.0, 1.0, 0.0], [0.0, 0.0, 0.0]])
 
@@ -37,11 +38,12 @@ def _levels_for(side: int) -> int:
     return n
 
 
-def _state(side: int, ops_top: list[Stencil9], omega: float = 0.8) -> CudaGridState:
+def _state(side: int, ops_top: list[Stencil9], omega: float = 0.8,
+           kind: SmootherKind = SmootherKind.DAMPED_JACOBI) -> CudaGridState:
     n = _levels_for(side)
     ops = list(ops_top) + [_ID] * (n - len(ops_top))
     return CudaGridState(build_hierarchy(n, Coarsening.FULL_STANDARD), ops[:n],
-                         SmootherSpec(SmootherKind.DAMPED_JACOBI, omega if 0 < omega <= 1 else 0.8), 0, 0)
+                         SmootherSpec(kind, omega if 0 < omega <= 1 else 0.8), 0, 0)
 
 
 def _square(a) -> np.ndarray:
@@ -75,14 +77,14 @@ def residual(op: Stencil9, u, f) -> np.ndarray:
 def relax(op: Stencil9, u, f, spec: SmootherSpec, count: int) -> np.ndarray:
     if count < 0:
         raise ValueError(f"relaxation count must be >= 0, got {count}")
-    if spec.kind is not SmootherKind.DAMPED_JACOBI:
-        raise ValueError("the B200 engine implements damped Jacobi only")
-    if op.center == 0.0 and count > 0:
+    if spec.kind is SmootherKind.ZEBRA_ALTERNATING and count % 2:
+        raise ValueError("alternating zebra needs an even relaxation count")
+    if spec.kind is SmootherKind.DAMPED_JACOBI and op.center == 0.0 and count > 0:
         raise ValueError("zero center coefficient")
     u, f = _square(u), _square(f)
     if u.shape != f.shape:
         raise ValueError(f"dimension mismatch: {u.shape} vs {f.shape}")
-    s = _state(u.shape[0], [op], spec.omega)
+    s = _state(u.shape[0], [op], spec.omega, spec.kind)
     s.v[0] = u
     s.f[0] = f
     s.relax_level(1, count)
@@ -133,6 +135,14 @@ def coarsest_solve(op: Stencil9, f, coarsening: Coarsening = Coarsening.FULL_STA
     out = s.v[0]
     s.close()
     return out
+
+
+def zebra_line_sweep(op: Stencil9, u, f, axis: str) -> np.ndarray:
+    """One zebra sweep with lines along `axis` (smoother.py:107-135)."""
+    if axis not in ("x", "y"):
+        raise ValueError(f"axis must be 'x' or 'y', got {axis!r}")
+    kind = SmootherKind.ZEBRA_X if axis == "x" else SmootherKind.ZEBRA_Y
+    return relax(op, u, f, SmootherSpec(kind), 1)
 
 
 def norm2(g) -> float:

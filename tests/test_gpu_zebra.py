@@ -111,3 +111,17 @@ def test_zebra_solves_match_reference(key):
     assert rep.final_error_norm == pytest.approx(rec["final_error_norm"], rel=1e-10)
     assert rep.stats.kernel_launches == rec["kernel_launches"]
     assert rep.stats.unknown_touches == rec["unknown_touches"]
+
+
+def test_pure_function_zebra_sweep_matches_reference():
+    """kernels.zebra_line_sweep / relax (the reference's pure-function
+    signatures) on square grids."""
+    from paper_2010_00626_b200 import kernels as K
+    for key in META["kernels"]:
+        u = Z[key + "_u"]
+        if u.shape[0] != u.shape[1]:
+            continue
+        f, op = Z[key + "_f"], Stencil9(Z[key + "_w"])
+        assert np.array_equal(K.zebra_line_sweep(op, u, f, "x"), Z[key + "_zx"]), key
+        assert np.array_equal(K.zebra_line_sweep(op, u, f, "y"), Z[key + "_zy"]), key
+        assert np.array_equal(K.relax(op, u, f, SmootherSpec(SmootherKind.ZEBRA_ALTERNATING), 2), Z[key + "_zxy2"])
