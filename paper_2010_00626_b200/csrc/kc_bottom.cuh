@@ -187,7 +187,7 @@ struct BotBuilder {  // host side
       out.push_back(bot_desc(op, d, src, zero, cbuf, cc, KC_BOT_WARPS, kap) | BD_STRIP_BIT);
       return;
     }
-    const int g = bot_warps(bot_m(m0, d));
+    const int g = (op == PH_TINY && bot_m(m0, d) == 7) ? 2 : bot_warps(bot_m(m0, d));
     if (g > gprev) out.push_back(bot_desc(PH_JOIN, 0, 0, 0, 0, 0, g));
     gprev = g;
     local_run = true;
@@ -419,9 +419,10 @@ struct BotTiny {
   double* sm;
   const BotLv* lv;
   const St9* tab;
-  int nu1, nu2, tid, nth;  // nth = 32: one warp (__syncwarp); 256: warps 0-7 (named barrier 1)
+  int nu1, nu2, tid, nth;  // 32: warp 0 (__syncwarp); 64: warps 0-1 (barrier 2); 256: warps 0-7 (barrier 1)
   __device__ __forceinline__ void sync() const {
     if (nth == 32) __syncwarp();
+    else if (nth == 64) asm volatile("bar.sync 2, 64;" ::: "memory");
     else asm volatile("bar.sync 1, 256;" ::: "memory");
   }
   __device__ __forceinline__ double* buf(const BotLv& L, int b) const { return sm + (b ? L.vo1 : L.vo0); }
@@ -471,39 +472,50 @@ struct BotTiny {
     down(d, L, st, cur, vz, true);
     up(d, L, st, cur, vz, 0);
   }
-  // side 7: children are side-3 leaves (kappa only sets how many)
-  __device__ __forceinline__ void frame7(int d, int kap, int& cur, int& vz) const {
+  // side 7 (on warps 0-1: one point per thread): children are side-3 leaves
+  // on warp 0 (kappa only sets how many); slot passes their final buffer
+  __device__ __forceinline__ void frame7(int d, int kap, int& cur, int& vz, int* slot) const {
     const BotLv L = lv[d];
     const St9 st = tab[d];
     down(d, L, st, cur, vz, false);
-    int cc = 0, cz = 1;
-    leaf(d + 1, cc, cz);
-    if (kap > 1) leaf(d + 1, cc, cz);
+    int cc = 0;
+    if (tid < 32) {
+      const BotTiny w{sm, lv, tab, nu1, nu2, tid, 32};
+      int cz = 1;
+      w.leaf(d + 1, cc, cz);
+      if (kap > 1) w.leaf(d + 1, cc, cz);
+      if (nth > 32 && tid == 0) *slot = cc;
+    }
+    if (nth > 32) {
+      sync();
+      cc = *slot;
+    }
     up(d, L, st, cur, vz, cc);
   }
   // side 15 on warps 0-7; its side-7 children (kappa, kappa - 1;
   // cycle.py:215-218) on warp 0 while warps 1-7 wait at the named barrier
+  // child_buf[0]: the side-15 frame's child buffer, child_buf[1]: the side-7 frames'
   __device__ void frame(int d, int kap, int nlev, int& cur, int& vz, int* child_buf) const {
     if (d + 2 == nlev) {
       leaf(d, cur, vz);
       return;
     }
     if (d + 3 == nlev) {
-      frame7(d, kap, cur, vz);
+      frame7(d, kap, cur, vz, child_buf + 1);
       return;
     }
     const BotLv L = lv[d];
     const St9 st = tab[d];
     down(d, L, st, cur, vz, false);
-    if (tid < 32) {
-      const BotTiny w{sm, lv, tab, nu1, nu2, tid, 32};
+    if (tid < 64) {
+      const BotTiny w{sm, lv, tab, nu1, nu2, tid, 64};
       int cc = 0, cz = 1;
-      w.frame7(d + 1, kap, cc, cz);
-      if (kap > 1) w.frame7(d + 1, kap - 1, cc, cz);
-      if (tid == 0) *child_buf = cc;
+      w.frame7(d + 1, kap, cc, cz, child_buf + 1);
+      if (kap > 1) w.frame7(d + 1, kap - 1, cc, cz, child_buf + 1);
+      if (tid == 0) child_buf[0] = cc;
     }
     sync();
-    up(d, L, st, cur, vz, *child_buf);
+    up(d, L, st, cur, vz, child_buf[0]);
   }
 };
 
@@ -512,7 +524,7 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
   __shared__ St9 tab[KC_BOT_MAXLEV];
   __shared__ BotLv lv[KC_BOT_MAXLEV];
   __shared__ unsigned sched[KC_BOT_MAXPH];
-  __shared__ int tiny_child;
+  __shared__ int tiny_child[2];
   cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
   const int rank = (int)cl.block_rank(), cs = (int)cl.num_blocks();
   const int nlev = bp.nlev, nstrip = bp.nstrip;
@@ -651,7 +663,7 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
     } else {  // PH_TINY (CTA 0: warp 0 for sides <= 7, warps 0-7 for side 15)
       const BotTiny t{sm, lv, tab, bp.nu1, bp.nu2, tid, nth};
       int cur = src, vz = zero;
-      t.frame(d, BD_KAP(e), nlev, cur, vz, &tiny_child);
+      t.frame(d, BD_KAP(e), nlev, cur, vz, tiny_child);
     }
     if (strip) clu_sync();
     else bot_sync(g);
