@@ -56,7 +56,9 @@
 #define KC_CLU_MIN_STRIP 31
 #endif
 #define KC_BOT_MAXLEV 8
-#define KC_BOT_THREADS 512
+#ifndef KC_BOT_THREADS
+#define KC_BOT_THREADS 384  // 12 warps: 147 registers without spills (512 spills at the 128 cap)
+#endif
 #define KC_BOT_WARPS (KC_BOT_THREADS / 32)
 #define KC_BOT_RB 4  // rows per thread in stencil phases
 
