@@ -626,3 +626,24 @@ def test_full_size_solve_reduces_residual_monotonically():
     res = rep.residual_history
     assert all(b < a for a, b in zip(res, res[1:]))
     assert res[-1] <= res[0] / 1e10
+
+
+@pytest.mark.parametrize("nu1,nu2", [(5, 3), (6, 0), (0, 5)])
+def test_large_nu_native_cycles_bit_exact(nu1, nu2):
+    """nu > 4 leaves the fused streaming kernels (per-op kernels on the HBM
+    levels) while the bottom kernel's schedule and tiny frames take any nu;
+    the native cycle must still equal the oracle bit for bit."""
+    n = 9
+    m = 2 ** n - 1
+    rng = np.random.default_rng(nu1 * 10 + nu2)
+    v0, f0 = rng.random((m, m)), rng.standard_normal((m, m))
+    for kappa in (2, 3):
+        cfg = CycleConfig(n=n, kappa=kappa, nu1=nu1, nu2=nu2)
+        h = O.Hierarchy(O.hierarchy(1e-4, 45.0, n), nu1=nu1, nu2=nu2)
+        h.v[0], h.f[0] = v0.copy(), f0.copy()
+        h.cycle(kappa)
+        st = build_state(ProblemSpec(1e-4, 45.0), cfg)
+        st.v[0], st.f[0] = v0, f0
+        run_cycle(st, cfg, CycleStats.for_levels(n))
+        assert np.array_equal(st.v[0], h.v[0]), (nu1, nu2, kappa)
+        st.close()
