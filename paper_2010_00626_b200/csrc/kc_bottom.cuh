@@ -1,26 +1,27 @@
-// kc_bottom.cuh — persistent one-CTA kernel for the latency-bound bottom of
-// the hierarchy.
+// kc_bottom.cuh — persistent kernel for the latency-bound bottom of the
+// hierarchy: a 16-CTA thread-block cluster entering at
+// side <= 255 (see below), or one CTA entering at side <= 63.
 //
-// Below a side of KC_BOT_MAX_M (63) every remaining level (v ping-pong pair
-// and f, each with its zero ghost ring) fits in shared memory (~137 KB for
-// 63^2 .. 1^2).  One CTA loads f (and v unless it is the zero guess) of the
-// entry level from HBM, runs the reference's kappa_cycle recursion
-// (cycle.py:204-220) as a device-side state machine, and writes v back.
-// Every routine call of the bottom levels costs barriers instead of kernel
-// launches, so host-visible launches per cycle no longer grow with kappa's
-// polynomial call count.
+// Every remaining level (v ping-pong pair and f, each with its zero ghost
+// ring) lives in shared memory.  The kernel loads f (and v unless it is the
+// zero guess) of the entry level from HBM, replays the reference's
+// kappa_cycle recursion (cycle.py:204-220) from a host-built phase list, and
+// writes v back.  Every routine call of the bottom levels costs barriers
+// instead of kernel launches, so host-visible launches per cycle no longer
+// grow with kappa's polynomial call count.
 //
 // Design for latency (measured on B200, tools/micro: fp64 dependent op 8
-// cycles, __syncthreads 47-115, __syncwarp 31, a bare 3x3 Jacobi phase ~340):
-//  * one control loop yields one phase per iteration and executes it at a
-//    single inlined site, so the kernel is small (instruction-cache
-//    resident) and has no calls; the recursion stack is bit-packed in a
-//    register (stage, counter and sweep count per level);
-//  * the warps that work on a level scale with its size: 16 warps for
-//    sides >= 31 (CTA barrier), 8 warps for 15 (named barrier), 1 warp for
-//    sides <= 7 (__syncwarp), and idle warps skip the phase;
+// cycles, __syncthreads 47-115, __syncwarp 31, a bare 3x3 Jacobi phase ~340,
+// cluster barrier ~490 / ~940 with remote stores outstanding):
+//  * one control loop replays one phase descriptor per iteration at a single
+//    inlined site, so the kernel stays small; 384 threads per CTA leave 170
+//    registers per thread (the loop is register-bound: 512 threads spilled);
+//  * the warps that work on a level scale with its size: all 12 for sides
+//    >= 31 (CTA or cluster barrier), 8 for 15 (named barrier), 1-2 for the
+//    smallest (__syncwarp / named barrier), and idle warps skip the phase;
+//    whole frames on sides <= 15 run as one descriptor (PH_TINY);
 //  * stencil phases are register-blocked 4 rows per thread (3 new loads per
-//    row instead of 9), halving shared-memory traffic on the 63^2/31^2 levels;
+//    row instead of 9) where there are enough rows;
 //  * the coarsest 1x1 solve is folded into its parent's restriction.
 // Per-point arithmetic is identical to the HBM kernels (kc_common.cuh), so
 // iterates stay bit-identical to the reference.  The redundant second
@@ -119,29 +120,25 @@ __device__ int kc_bot_trace_n;
 __device__ long long kc_bot_trace_end[KC_BOT_TRACE];
 #endif
 
-// Phase descriptor (host-built by bot_schedule in kc_engine.cu):
-//  bits 0-2 op (PH_*), 3-5 level d, 6 src buffer, 7 zero guess, 8 child buffer
-//  (prolong), 9 child is the 1x1 coarsest (restrict), 10-11 warp group code.
-// Fused phases cut the dependent phases of a routine call from 7 to 4:
+// Phase kinds (host-built list, BotBuilder below):
+//   PH_JACOBI / PH_RESID / PH_RESTRICT / PH_PROLONG  one protocol routine;
 //   PH_J2Z  two sweeps from the zero guess: u1 = 0 + c f is pointwise, so the
 //           second sweep recomputes it at its 3x3 neighbours from f (+0.0 on
-//           the ghost ring, exactly the Dirichlet value);
-//   PH_RR   residual + full weighting, each coarse node forming its 3x3 fine
-//           residuals (small levels);
-//   PH_PJ   prolong-correct + first post sweep, each point forming the
-//           corrected v at its 3x3 neighbours (small levels).
-// Same per-point arithmetic, so results stay bit-identical.
-//   PH_TINY a whole kappa_cycle frame on a level of side <= 7 (with its
-//           children) executed by warp 0 with the fused phases and no
-//           interpreter overhead between them (bot_tiny below).
+//           the ghost ring, exactly the Dirichlet value) -- same per-point
+//           arithmetic, so results stay bit-identical;
+//   PH_TINY a whole kappa_cycle frame on a level of side <= 15 (with its
+//           children) run without interpreter overhead between its phases
+//           (BotTiny below);
+//   PH_JOIN gather a larger warp group; PH_CSYNC cluster barrier.
+// (Residual+restriction and prolongation+sweep fusions for the small levels
+// were measured slower -- larger kernel, longer dependent chains -- and the
+// tiny frames replaced them.)
 enum BotOp {
-  PH_JACOBI = 0, PH_RESID = 1, PH_RESTRICT = 2, PH_PROLONG = 3, PH_JOIN = 4, PH_J2Z = 5, PH_RR = 6, PH_PJ = 7,
-  PH_TINY = 8, PH_CSYNC = 9
+  PH_JACOBI = 0, PH_RESID = 1, PH_RESTRICT = 2, PH_PROLONG = 3, PH_JOIN = 4, PH_J2Z = 5, PH_TINY = 8, PH_CSYNC = 9
 };
 #ifndef KC_BOT_TINY_M
 #define KC_BOT_TINY_M 15  // frames on sides <= this run as PH_TINY (side 15 on 8 warps)
 #endif
-#define KC_BOT_FUSE_M 15  // PH_RR / PH_PJ on sides <= this (latency-bound levels)
 // Descriptor: bits 0-3 op, 4-6 level d, 7 src buffer, 8 zero guess, 9 child
 // buffer (prolong), 10 child is the 1x1 coarsest (restrict), 11-12 warp
 // group code, 13-16 cycle counter (PH_TINY), 17 strip phase (all CTAs).
@@ -176,7 +173,6 @@ struct BotBuilder {  // host side
   int gprev = KC_BOT_WARPS;
   bool local_run = false;   // the last emitted phase ran on CTA 0 only
   bool fuse = true;         // emit PH_J2Z
-  bool fuse_small = false;  // emit PH_RR / PH_PJ (measured slower: larger kernel, longer chains)
   bool tiny = true;         // whole frames on sides <= KC_BOT_TINY_M as PH_TINY
   bool dry = false;         // track buffers only (inside a PH_TINY frame)
   std::vector<unsigned> out;
@@ -222,13 +218,8 @@ struct BotBuilder {  // host side
     const int c = (cur >> d) & 1u;
     const int z = (vz >> d) & 1u;
     const int cc = (d + 1 == nlev - 1);
-    const bool small = fuse && fuse_small && bot_m(m0, d) <= KC_BOT_FUSE_M;  // RR / PJ
-    if (small && !z) {
-      emit(PH_RR, d, c, 0, 0, cc);
-    } else {
-      if (!z) emit(PH_RESID, d, c, 0, 0, 0);  // residual into buffer c^1
-      emit(PH_RESTRICT, d, c ^ 1, z, 0, cc);
-    }
+    if (!z) emit(PH_RESID, d, c, 0, 0, 0);  // residual into buffer c^1
+    emit(PH_RESTRICT, d, c ^ 1, z, 0, cc);
     cur &= ~(1u << (d + 1));
     if (cc) {
       vz &= ~(1u << (d + 1));  // both coarsest calls: one f/center inside the restriction
@@ -237,16 +228,9 @@ struct BotBuilder {  // host side
       rec(d + 1, kap);
       if (kap > 1) rec(d + 1, kap - 1);
     }
-    if (small && nu2 > 0) {  // prolong-correct fused with the first post sweep
-      emit(PH_PJ, d, (cur >> d) & 1u, (vz >> d) & 1u, (cur >> (d + 1)) & 1u, 0);
-      vz &= ~(1u << d);
-      cur ^= 1u << d;
-      relax(d, nu2 - 1);
-    } else {
-      emit(PH_PROLONG, d, (cur >> d) & 1u, (vz >> d) & 1u, (cur >> (d + 1)) & 1u, 0);
-      vz &= ~(1u << d);
-      relax(d, nu2);
-    }
+    emit(PH_PROLONG, d, (cur >> d) & 1u, (vz >> d) & 1u, (cur >> (d + 1)) & 1u, 0);
+    vz &= ~(1u << d);
+    relax(d, nu2);
   }
 };
 
