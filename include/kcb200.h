@@ -178,6 +178,20 @@ int kc_strip_prolong_add(double* v, const double* vc, int ny, int nx, int pitch,
 int kc_strip_norms(const double* v, const double* f, int ny, int nx, int pitch, const double* w9, double* out,
                    void* stream);
 
+/* Fused strip passes (the single-GPU k_pre / k_post on a strip): rows local
+ * fine rows from global row gy0 (even) of mg, hb halo rows valid in the
+ * buffers (>= nu1+2 for pre, >= nu2 for post; the caller exchanges them).
+ * pre: nu1 sweeps of u (out in uo; nu1 = 0: uo untouched) + residual + full
+ * weighting into fc for crows local coarse rows (cycle.py:211-213);
+ * post: uo = relax^nu2(u + P vc) with vc's local row 0 at global coarse row
+ * gy0/2, crows coarse rows and hbc (>= nu2/2 + 1) halo rows (cycle.py:219-220). */
+int kc_strip_pre(const double* u, const double* f, double* uo, double* fc, int rows, int nx, int pitch, int pitch_c,
+                 int crows, int gy0, int mg, int hb, const double* w9, double omega, int nu1, int zero_u,
+                 void* stream);
+int kc_strip_post(const double* u, const double* f, double* uo, const double* vc, int rows, int nx, int pitch,
+                  int pitch_c, int crows, int gy0, int mg, int hb, int hbc, const double* w9, double omega, int nu2,
+                  int v_zero, void* stream);
+
 /* level data from / to device memory with an explicit row pitch (doubles):
  * agglomeration of distributed levels onto the native engine */
 int kc_set_device(kc_handle* h, int level, int which, const double* dev, long long ny, long long nx,

@@ -89,6 +89,10 @@ _SIGS = {
     "kc_strip_prolong_add": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                        C.c_void_p]),
     "kc_strip_norms": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, _dp, C.c_void_p, C.c_void_p]),
+    "kc_strip_pre": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p] + [C.c_int] * 8
+                     + [_dp, C.c_double, C.c_int, C.c_int, C.c_void_p]),
+    "kc_strip_post": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p] + [C.c_int] * 9
+                      + [_dp, C.c_double, C.c_int, C.c_int, C.c_void_p]),
     "kc_set_device": (C.c_int, [_h, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_longlong, C.c_longlong]),
     "kc_get_device": (C.c_int, [_h, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_longlong, C.c_longlong]),
     "kc_restore": (C.c_int, [_h]),

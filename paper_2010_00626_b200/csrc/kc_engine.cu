@@ -628,6 +628,12 @@ StreamParams ks_params(kc_handle* h, int l, int D, int* nwarps, const void* fn) 
   p.mc = C.m;
   p.Pc = C.P;
   p.s = L.st;
+  p.rows = L.m;
+  p.gy0 = 0;
+  p.mg = L.m;
+  p.hb = 1;
+  p.mcr = C.m;
+  p.hbc = 1;
   p.nbands = (C.m + 1 + ks_npb(D) - 1) / ks_npb(D);
   p.nq = ks_choose_nq(C.m, p.nbands, fn ? ks_slots(h, fn) : 148 * 12);
   *nwarps = p.nbands * ((C.m + 1 + p.nq - 1) / p.nq);
@@ -1995,6 +2001,114 @@ extern "C" int kc_strip_norms(const double* v, const double* f, int ny, int nx, 
   }
   k_strip_norms<<<nb, 256, 0, (cudaStream_t)stream>>>(v, f, ny, nx, pitch, strip_stencil(w9, 1.0), part);
   k_strip_norms_final<<<1, 32, 0, (cudaStream_t)stream>>>(part, nb, out);
+  return strip_err(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// fused strip passes: k_pre / k_post (kc_stream.cuh) on a row strip whose
+// buffers carry `hb` halo rows (exchanged by the caller, depth >= nu+1 for
+// the pre pass, >= nu for the post pass) -- two launches per routine call
+// instead of nu + 2 per-op kernels, and two halo exchanges
+// ---------------------------------------------------------------------------
+namespace {
+int strip_slots(const void* fn) {
+  static std::map<const void*, int> cache;
+  static int sms = 0;
+  auto it = cache.find(fn);
+  if (it != cache.end()) return it->second;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, KS_SMEM_BYTES);
+  int blocks = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, 128, KS_SMEM_BYTES) != cudaSuccess || blocks < 1)
+    blocks = 1;
+  return cache[fn] = blocks * 4 * sms;
+}
+KsFn strip_pre_fn(int nu, bool zero) {
+#define KS_SPRE(N) return zero ? k_pre<N, true, false, true> : k_pre<N, false, false, true>
+  switch (nu) {
+    case 0: KS_SPRE(0);
+    case 1: KS_SPRE(1);
+    case 2: KS_SPRE(2);
+    case 3: KS_SPRE(3);
+    case 4: KS_SPRE(4);
+  }
+#undef KS_SPRE
+  return nullptr;
+}
+KsFn strip_post_fn(int nu, bool vz) {
+#define KS_SPOST(N) return vz ? k_post<N, true, 0, true> : k_post<N, false, 0, true>
+  switch (nu) {
+    case 0: KS_SPOST(0);
+    case 1: KS_SPOST(1);
+    case 2: KS_SPOST(2);
+    case 3: KS_SPOST(3);
+    case 4: KS_SPOST(4);
+  }
+#undef KS_SPOST
+  return nullptr;
+}
+StreamParams strip_params(int rows, int nx, int pitch, int pitch_c, int crows, int gy0, int mg, int hb, int hbc,
+                          const double* w9, double omega, int D, const void* fn, int* nwarps) {
+  StreamParams p{};
+  p.m = nx;
+  p.P = pitch;
+  p.mc = (nx - 1) / 2;
+  p.Pc = pitch_c;
+  p.s = strip_stencil(w9, omega);
+  p.rows = rows;
+  p.gy0 = gy0;
+  p.mg = mg;
+  p.hb = hb;
+  p.mcr = crows;
+  p.hbc = hbc;
+  p.nbands = (p.mc + 1 + ks_npb(D) - 1) / ks_npb(D);
+  p.nq = ks_choose_nq(crows, p.nbands, strip_slots(fn));
+  *nwarps = p.nbands * ((crows + 1 + p.nq - 1) / p.nq);
+  return p;
+}
+}  // namespace
+
+extern "C" int kc_strip_pre(const double* u, const double* f, double* uo, double* fc, int rows, int nx, int pitch,
+                            int pitch_c, int crows, int gy0, int mg, int hb, const double* w9, double omega, int nu1,
+                            int zero_u, void* stream) {
+  if (!f || !uo || !fc || !w9 || rows < 1 || nx < 3 || crows < 0 || hb < nu1 + 2 || gy0 < 0 || gy0 % 2) return KC_EINVAL;
+  if (!zero_u && !u) return KC_EINVAL;
+  if (nu1 < 0 || nu1 > 4 || (nu1 > 0 && w9[4] == 0.0)) return KC_EINVAL;
+  int nw = 0;
+  KsFn fn = strip_pre_fn(nu1, zero_u != 0);
+  StreamParams p = strip_params(rows, nx, pitch, pitch_c, crows, gy0, mg, hb, 1, w9, omega, nu1 + 1, (const void*)fn, &nw);
+  // the kernels index from the padded-array base: kc_idx(P, 0, 0) = P + KC_OX
+  const ptrdiff_t ob = (ptrdiff_t)pitch + KC_OX, obc = (ptrdiff_t)pitch_c + KC_OX;
+  p.u = u ? u - ob : nullptr;
+  p.f = f - ob;
+  p.uo = uo - ob;
+  p.fc = fc - obc;
+  fn<<<(nw + 3) / 4, 128, KS_SMEM_BYTES, (cudaStream_t)stream>>>(p);
+  return strip_err(cudaGetLastError());
+}
+
+extern "C" int kc_strip_post(const double* u, const double* f, double* uo, const double* vc, int rows, int nx,
+                             int pitch, int pitch_c, int crows, int gy0, int mg, int hb, int hbc, const double* w9,
+                             double omega, int nu2, int v_zero, void* stream) {
+  if (!f || !uo || !vc || !w9 || rows < 1 || nx < 3 || crows < 0 || hb < nu2 || hbc < nu2 / 2 + 1 || gy0 < 0 ||
+      gy0 % 2)
+    return KC_EINVAL;
+  if (!v_zero && !u) return KC_EINVAL;
+  if (nu2 < 0 || nu2 > 4 || (nu2 > 0 && w9[4] == 0.0)) return KC_EINVAL;
+  int nw = 0;
+  KsFn fn = strip_post_fn(nu2, v_zero != 0);
+  StreamParams p = strip_params(rows, nx, pitch, pitch_c, crows, gy0, mg, hb, hbc, w9, omega, nu2 > 0 ? nu2 : 1,
+                                (const void*)fn, &nw);
+  const ptrdiff_t ob = (ptrdiff_t)pitch + KC_OX, obc = (ptrdiff_t)pitch_c + KC_OX;  // see kc_strip_pre
+  p.u = u ? u - ob : nullptr;
+  p.f = f - ob;
+  p.uo = uo - ob;
+  p.vc = vc - obc;
+  fn<<<(nw + 3) / 4, 128, KS_SMEM_BYTES, (cudaStream_t)stream>>>(p);
   return strip_err(cudaGetLastError());
 }
 

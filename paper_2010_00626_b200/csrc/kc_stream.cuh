@@ -35,6 +35,12 @@ struct StreamParams {
   int nbands, nq;    // bands across x; coarse rows per chunk
   St9 s;
   double* part;      // POST+NORMS: 2 partial sums per warp
+  // row geometry: a whole level (rows = mg = m, gy0 = 0, hb = hbc = 1,
+  // mcr = mc), or a row strip of a distributed level (multi-GPU): `rows`
+  // local fine rows starting at global row gy0 (even) of mg, with hb valid
+  // halo rows above and below in the buffer; mcr local coarse rows with hbc
+  // coarse halo rows.  Masks use global rows, memory stays in the buffer.
+  int rows, gy0, mg, hb, mcr, hbc;
 };
 
 __device__ __forceinline__ double kc_shfl_up1(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
@@ -113,15 +119,18 @@ __device__ __forceinline__ double2 ks_lds2(const double* p) { return *reinterpre
 // stand-alone stopping test of the previous cycle's result (cycle.py:345)
 // at no extra stencil work.
 // ---------------------------------------------------------------------------
-template <int NU, bool ZERO, bool NORMS = false>
+template <int NU, bool ZERO, bool NORMS = false, bool STRIP = false>
 __global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
   constexpr int D = NU + 1;
+  // row geometry (StreamParams): compile-time whole-level values unless STRIP
+  const int g_rows = STRIP ? p.rows : p.m, g_y0 = STRIP ? p.gy0 : 0, g_mg = STRIP ? p.mg : p.m;
+  const int g_hb = STRIP ? p.hb : 1, g_mcr = STRIP ? p.mcr : p.mc;
   using G = KsGeom<D>;
   const int lane = threadIdx.x & 31;
   const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int band = wg % p.nbands, chunk = wg / p.nbands;
   const int P0 = band * G::NPB, Q0 = chunk * p.nq;
-  if (Q0 > p.mc) {  // whole warp
+  if (Q0 > g_mcr) {  // whole warp
     if (NORMS) reinterpret_cast<double2*>(p.part)[wg * 32 + lane] = make_double2(0.0, 0.0);
     return;
   }
@@ -143,9 +152,10 @@ __global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
   const int ys = 2 * Q0 - D;
   const int ye = 2 * Q0 + 2 * p.nq + 2 * D + 1;  // inclusive
   // only warps touching the domain boundary need masks / row clamping
-  const bool edge = XS < 0 || XS + KS_BAND - 1 >= m || ys - 2 * D < 0 || ye + 2 >= m;
-  // rows outside [-1, m] read the all-zero ghost rows: branch-free
-  auto rp = [&](int y) -> size_t { return kc_idx(P, min(max(y, -1), m), c0); };
+  const bool edge = XS < 0 || XS + KS_BAND - 1 >= m || g_y0 + ys - 2 * D < 0 || g_y0 + ye + 2 >= g_mg;
+  // rows outside the buffer read its edge rows (the all-zero ghost rows of a
+  // whole level): branch-free
+  auto rp = [&](int y) -> size_t { return kc_idx(P, min(max(y, -g_hb), g_rows + g_hb - 1), c0); };
   // shared-memory rings (this warp's slice): u rows and f rows
   extern __shared__ double ks_smem[];
   double* ring = ks_smem + (threadIdx.x >> 5) * KS_WARP_SMEM_DOUBLES + 2 * lane;
@@ -176,8 +186,8 @@ __global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
     // NORMS: rows owned by this chunk, interior columns owned by this lane;
     // the input's residual is the first stage's f - A u at row yin - 2
     const int y1 = yin - 2;
-    const bool own_e = NORMS && own_lane && yin >= 2 * Q0 && yin < 2 * Q0 + 2 * p.nq && yin < m;
-    const bool own_r = NORMS && own_lane && y1 >= 2 * Q0 && y1 < 2 * Q0 + 2 * p.nq && y1 >= 0 && y1 < m;
+    const bool own_e = NORMS && own_lane && yin >= 2 * Q0 && yin < 2 * Q0 + 2 * p.nq && yin < g_rows;
+    const bool own_r = NORMS && own_lane && y1 >= 2 * Q0 && y1 < 2 * Q0 + 2 * p.nq && y1 >= 0 && y1 < g_rows;
     if (own_e) acc_e = fma(u0.y, u0.y, fma(u0.x, u0.x, acc_e));
 #pragma unroll
     for (int t = 1; t <= D; ++t) {
@@ -205,8 +215,8 @@ __global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
     if (edge) {  // Dirichlet: every stage is +0.0 outside the interior
 #pragma unroll
       for (int t = 0; t <= D; ++t) {
-        const int y = yin - 2 * t;
-        const bool in = y >= 0 && y < m;
+        const int y = yin - 2 * t + g_y0;  // global row
+        const bool in = y >= 0 && y < g_mg;
         nw[t].x = (in && colx_in) ? nw[t].x : 0.0;
         nw[t].y = (in && coly_in) ? nw[t].y : 0.0;
       }
@@ -217,13 +227,13 @@ __global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
       const int yr = yin - 1 - 2 * D;  // newest residual row in R[2]
       const double e0 = kc_shfl_dn1(R[0].x), e1 = kc_shfl_dn1(R[1].x), e2 = kc_shfl_dn1(R[2].x);
       const int q = (yr >> 1) - 1;
-      if (!(yr & 1) && own_lane && q >= Q0 && q < Q0 + p.nq && q < p.mc && q >= 0 && pcol < p.mc)
+      if (!(yr & 1) && own_lane && q >= Q0 && q < Q0 + p.nq && q < g_mcr && q >= 0 && pcol < p.mc)
         p.fc[kc_idx(p.Pc, q, pcol)] = kc_fw(R[0].x, R[0].y, e0, R[1].x, R[1].y, e1, R[2].x, R[2].y, e2);
     }
     // ---- output v after NU sweeps ----------------------------------------
     if (NU > 0) {
       const int y = yin - 2 * NU;
-      if (own_lane && y >= 2 * Q0 && y < 2 * Q0 + 2 * p.nq && y >= 0 && y < m)
+      if (own_lane && y >= 2 * Q0 && y < 2 * Q0 + 2 * p.nq && y >= 0 && y < g_rows)
         *reinterpret_cast<double2*>(p.uo + kc_idx(P, y, c0)) = nw[NU];
     }
     // ---- shift windows ----------------------------------------------------
@@ -249,9 +259,11 @@ __global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
 // NM = 0: plain; 1: ||v'||^2 and ||f - A v'||^2 (one extra residual stage,
 // per-warp partials); 2: f . v' (the PCG rz = r . z of a preconditioning
 // cycle, whose f is r and whose result is z; per-lane partials, NU >= 1).
-template <int NU, bool VZ, int NM>
+template <int NU, bool VZ, int NM, bool STRIP = false>
 __global__ void __launch_bounds__(128, 4) k_post(const StreamParams p) {
   constexpr bool NORMS = NM == 1, DOT = NM == 2;
+  const int g_rows = STRIP ? p.rows : p.m, g_y0 = STRIP ? p.gy0 : 0, g_mg = STRIP ? p.mg : p.m;
+  const int g_hb = STRIP ? p.hb : 1, g_mcr = STRIP ? p.mcr : p.mc, g_hbc = STRIP ? p.hbc : 1;
   static_assert(!DOT || NU >= 1, "the f . v partials use the f row of the last sweep");
   constexpr int D = NU + (NORMS ? 1 : 0);
   constexpr int DD = D > 0 ? D : 1;
@@ -261,7 +273,7 @@ __global__ void __launch_bounds__(128, 4) k_post(const StreamParams p) {
   const int band = wg % p.nbands, chunk = wg / p.nbands;
   const int P0 = band * G::NPB, Q0 = chunk * p.nq;
   double acc_e = 0.0, acc_r = 0.0;
-  const bool active = Q0 <= p.mc;
+  const bool active = Q0 <= g_mcr;
   if (DOT && !active) reinterpret_cast<double2*>(p.part)[wg * 32 + lane] = make_double2(0.0, 0.0);
   const int m = p.m, P = p.P;
   const int XS = 2 * P0 - G::HL;
@@ -277,9 +289,12 @@ __global__ void __launch_bounds__(128, 4) k_post(const StreamParams p) {
     for (int t = 0; t < DD; ++t) W[t][0] = W[t][1] = W[t][2] = make_double2(0.0, 0.0);
     const int ys = 2 * Q0 - D;
     const int ye = 2 * Q0 + 2 * p.nq - 1 + 2 * D;
-    const bool edge = XS < 0 || XS + KS_BAND - 1 >= m || ys - 2 * D - 2 < 0 || ye + 4 >= m;
-    auto rp = [&](int y) -> size_t { return kc_idx(P, min(max(y, -1), m), c0); };
-    auto ldc = [&](int q) -> double { return __ldg(p.vc + kc_idx(p.Pc, min(max(q, -1), p.mc), pc)); };
+    const bool edge =
+        XS < 0 || XS + KS_BAND - 1 >= m || g_y0 + ys - 2 * D - 2 < 0 || g_y0 + ye + 4 >= g_mg;
+    auto rp = [&](int y) -> size_t { return kc_idx(P, min(max(y, -g_hb), g_rows + g_hb - 1), c0); };
+    auto ldc = [&](int q) -> double {
+      return __ldg(p.vc + kc_idx(p.Pc, min(max(q, -g_hbc), g_mcr + g_hbc - 1), pc));
+    };
     // coarse rows around the input row: vcp = row q-1, vcc = row q (q = floor(yin/2))
     int qcur = ys >> 1;  // arithmetic shift: floor
     double vcp = ldc(qcur - 1), vcc = ldc(qcur), vcn = ldc(qcur + 1);
@@ -330,8 +345,8 @@ __global__ void __launch_bounds__(128, 4) k_post(const StreamParams p) {
       if (edge) {  // Dirichlet: every stage is +0.0 outside the interior
 #pragma unroll
         for (int t = 0; t <= D; ++t) {
-          const int y = yin - 2 * t;
-          const bool in = y >= 0 && y < m;
+          const int y = yin - 2 * t + g_y0;  // global row
+          const bool in = y >= 0 && y < g_mg;
           nw[t].x = (in && colx_in) ? nw[t].x : 0.0;
           nw[t].y = (in && coly_in) ? nw[t].y : 0.0;
         }
@@ -339,7 +354,7 @@ __global__ void __launch_bounds__(128, 4) k_post(const StreamParams p) {
       // output after NU sweeps (stage NU; NU = 0 writes the corrected v)
       {
         const int y = yin - 2 * NU;
-        if (own_lane && y >= 2 * Q0 && y < 2 * Q0 + 2 * p.nq && y >= 0 && y < m) {
+        if (own_lane && y >= 2 * Q0 && y < 2 * Q0 + 2 * p.nq && y >= 0 && y < g_rows) {
           *reinterpret_cast<double2*>(p.uo + kc_idx(P, y, c0)) = nw[NU];
           if (NORMS) acc_e = fma(nw[NU].y, nw[NU].y, fma(nw[NU].x, nw[NU].x, acc_e));
           if (DOT) acc_e = fma(fr[NU > 0 ? NU : 1].y, nw[NU].y, fma(fr[NU > 0 ? NU : 1].x, nw[NU].x, acc_e));
@@ -347,7 +362,7 @@ __global__ void __launch_bounds__(128, 4) k_post(const StreamParams p) {
       }
       if (NORMS) {
         const int y = yin - 2 * D;
-        if (own_lane && y >= 2 * Q0 && y < 2 * Q0 + 2 * p.nq && y >= 0 && y < m)
+        if (own_lane && y >= 2 * Q0 && y < 2 * Q0 + 2 * p.nq && y >= 0 && y < g_rows)
           acc_r = fma(nw[D].y, nw[D].y, fma(nw[D].x, nw[D].x, acc_r));
       }
 #pragma unroll

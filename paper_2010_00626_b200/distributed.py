@@ -44,8 +44,9 @@ from .cycle import CycleConfig, CycleStats, DryState, kappa_cycle
 from .mesh import Coarsening, build_hierarchy
 from .stencil import ProblemSpec, operator_hierarchy
 
-HALO = 2
+HALO = 6  # halo rows per strip buffer: the fused passes need nu1 + 2 (pre) and nu2 (post)
 KC_OX = 16
+FUSE_MIN_M = 127  # narrower levels keep the per-op strip kernels (kc_engine.cu KC_FUSE_MIN_M)
 
 
 def kc_pitch(m: int) -> int:
@@ -222,6 +223,17 @@ class CudaStripOps:
         self.N.check(self.N.lib.kc_strip_prolong_add(self._p(v, HALO), self._p(vc, HALO), ny, nx, v.shape[1],
                                                      vc.shape[1], int(zero), self._stream()))
 
+    # fused passes (kc_strip_pre / kc_strip_post): the single-GPU streaming kernels on the strip
+    def pre(self, u, f, uo, fc, ny, nx, crows, gy0, mg, w, omega, nu1, zero):
+        self.N.check(self.N.lib.kc_strip_pre(self._p(u, HALO), self._p(f, HALO), self._p(uo, HALO), self._p(fc, HALO),
+                                             ny, nx, u.shape[1], fc.shape[1], crows, gy0, mg, HALO, self._w(w),
+                                             omega, nu1, int(zero), self._stream()))
+
+    def post(self, u, f, uo, vc, ny, nx, crows, gy0, mg, w, omega, nu2, zero):
+        self.N.check(self.N.lib.kc_strip_post(self._p(u, HALO), self._p(f, HALO), self._p(uo, HALO),
+                                              self._p(vc, HALO), ny, nx, u.shape[1], vc.shape[1], crows, gy0, mg,
+                                              HALO, HALO, self._w(w), omega, nu2, int(zero), self._stream()))
+
     def norms(self, v, f, ny, nx, w):
         out = self.torch.zeros(2, dtype=self.torch.float64, device=self.device)
         if ny > 0:
@@ -323,7 +335,7 @@ class DistributedKappaSolver:
         if which == "v":
             s.vzero = False
         else:
-            self._halo(s, s.f, 1)
+            self._halo(s, s.f, HALO)
 
     def gather_level1(self) -> np.ndarray:
         """All-gather the finest v (every rank receives the full array)."""
@@ -372,28 +384,54 @@ class DistributedKappaSolver:
             s.vzero = False
             s.cur ^= 1
 
+    def _fused(self, l: int) -> bool:
+        """Fused strip passes at distributed level l: wide enough, nu within the
+        buffers' halo, every rank's strip at least HALO rows deep."""
+        return (hasattr(self.ops, "pre") and self.plan.side(l) >= FUSE_MIN_M and self.nu1 <= 4 and self.nu2 <= 4
+                and self.nu1 + 2 <= HALO and self.nu2 + 1 <= HALO
+                and min(b - a for a, b in self.plan.rows[l - 1]) >= HALO)
+
     def _cycle(self, l: int, kappa: int):
         s = self.strips[l - 1]
         nd = self.plan.n_dist
-        self._relax(l, self.nu1)
-        if not s.vzero:
-            self._halo(s, s.v[s.cur], HALO)
+        fused = self._fused(l)
+        if fused:  # nu1 sweeps + residual + full weighting in one pass (cycle.py:211-213)
+            if not s.vzero:  # the last owned coarse row reaches nu1 + 2 fine rows below the strip
+                self._halo(s, s.v[s.cur], self.nu1 + 2)
+        else:
+            self._relax(l, self.nu1)
+            if not s.vzero:
+                self._halo(s, s.v[s.cur], 2)
         if l < nd:  # restrict into the next distributed strip
             c = self.strips[l]
-            self.ops.resid_restrict(s.v[s.cur], s.f, c.f, c.ny, c.m, self.w[l - 1], s.vzero)
-            self._halo(c, c.f, 1)
+            if fused:
+                self.ops.pre(s.v[s.cur], s.f, s.v[s.cur ^ 1], c.f, s.ny, s.m, c.ny, s.a, s.m, self.w[l - 1],
+                             self.omega, self.nu1, s.vzero)
+                if self.nu1 > 0:
+                    s.cur ^= 1
+                    s.vzero = False
+            else:
+                self.ops.resid_restrict(s.v[s.cur], s.f, c.f, c.ny, c.m, self.w[l - 1], s.vzero)
+            self._halo(c, c.f, HALO)
             c.vzero = True
             self._cycle(l + 1, kappa)
             if kappa > 1:
                 self._cycle(l + 1, kappa - 1)
-            self._halo(c, c.v[c.cur], 1)
-            vc = c.v[c.cur]
+            self._halo(c, c.v[c.cur], self.nu2 // 2 + 2)
+            vc, vc_rows = c.v[c.cur], c.ny
         else:  # agglomerate: all-gather the coarse rows, replicated sub-cycle
             mc = self.plan.side(l + 1)
             q0, q1 = s.a // 2, (s.b // 2 if self.rank < self.world - 1 else mc)
             maxq = max((b // 2 if r < self.world - 1 else mc) - a // 2 for r, (a, b) in enumerate(self.plan.rows[l - 1]))
             part = self.ops.zeros(maxq + 2 * HALO, self.cfull.shape[1])
-            self.ops.resid_restrict(s.v[s.cur], s.f, part, q1 - q0, mc, self.w[l - 1], s.vzero)
+            if fused:
+                self.ops.pre(s.v[s.cur], s.f, s.v[s.cur ^ 1], part, s.ny, s.m, q1 - q0, s.a, s.m, self.w[l - 1],
+                             self.omega, self.nu1, s.vzero)
+                if self.nu1 > 0:
+                    s.cur ^= 1
+                    s.vzero = False
+            else:
+                self.ops.resid_restrict(s.v[s.cur], s.f, part, q1 - q0, mc, self.w[l - 1], s.vzero)
             parts = self.comm.allgather(part)
             for r, (a, b) in enumerate(self.plan.rows[l - 1]):
                 ra, rb = a // 2, (b // 2 if r < self.world - 1 else mc)
@@ -406,9 +444,18 @@ class DistributedKappaSolver:
             self.coarse.get_v(self.vfull)
             vc = self.vfull[q0:]  # local coarse row 0 <-> global row q0 (ghost rows above)
             # view whose interior origin (row HALO) is coarse row q0: vfull row HALO + q0
-        self.ops.prolong_add(s.v[s.cur], vc, s.ny, s.m, s.vzero)
-        s.vzero = False
-        self._relax(l, self.nu2)
+            vc_rows = q1 - q0
+        if fused:  # v + P vc and nu2 sweeps in one pass (cycle.py:219-220)
+            if not s.vzero:
+                self._halo(s, s.v[s.cur], max(self.nu2, 1))
+            self.ops.post(s.v[s.cur], s.f, s.v[s.cur ^ 1], vc, s.ny, s.m, vc_rows, s.a, s.m, self.w[l - 1],
+                          self.omega, self.nu2, s.vzero)
+            s.cur ^= 1
+            s.vzero = False
+        else:
+            self.ops.prolong_add(s.v[s.cur], vc, s.ny, s.m, s.vzero)
+            s.vzero = False
+            self._relax(l, self.nu2)
 
     def cycle(self, kappa: int | None = None, stats: CycleStats | None = None):
         """One kappa-cycle (run_cycle, cycle.py:261-263) over the decomposed hierarchy."""

@@ -542,17 +542,21 @@ def test_n12_pcg_vs_reference(kname):
 # multi-rank decomposition with the CUDA strip kernels (thread ranks on one GPU)
 # ---------------------------------------------------------------------------
 
-@pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("kappa", [1, 3])
-def test_distributed_cuda_strips_bit_exact(world, kappa):
+@pytest.mark.parametrize("world,kappa,nu", [(2, 1, (2, 2)), (2, 3, (2, 2)), (3, 1, (2, 2)), (3, 3, (2, 2)),
+                                             (2, 2, (1, 1)), (2, 2, (3, 0)), (3, 2, (0, 3)), (2, 2, (4, 4))])
+def test_distributed_cuda_strips_bit_exact(world, kappa, nu):
+    """Thread ranks on one GPU: the fused strip passes (kc_strip_pre/post with
+    deep halos) on the distributed levels >= 127 wide, per-op strip kernels
+    below and for nu1 > 3, agglomeration onto the native engine."""
     import threading
 
     from paper_2010_00626_b200.distributed import DistributedKappaSolver, ThreadComm
     n, eps, phi = 9, 1e-4, 45.0
+    nu1, nu2 = nu
     m = 2 ** n - 1
-    rng = np.random.default_rng(world + 10 * kappa)
+    rng = np.random.default_rng(world + 10 * kappa + nu1)
     v0, f0 = rng.random((m, m)), rng.standard_normal((m, m))
-    h = O.Hierarchy(O.hierarchy(eps, phi, n))
+    h = O.Hierarchy(O.hierarchy(eps, phi, n), nu1=nu1, nu2=nu2)
     h.v[0], h.f[0] = v0.copy(), f0.copy()
     ref = []
     for _ in range(2):
@@ -563,7 +567,8 @@ def test_distributed_cuda_strips_bit_exact(world, kappa):
 
     def body(r):
         try:
-            s = DistributedKappaSolver(ProblemSpec(eps, phi), CycleConfig(n=n, kappa=kappa), comms[r], min_rows=32)
+            s = DistributedKappaSolver(ProblemSpec(eps, phi), CycleConfig(n=n, kappa=kappa, nu1=nu1, nu2=nu2),
+                                       comms[r], min_rows=32)
             assert s.plan.n_dist >= 2
             s.set_level1("v", v0)
             s.set_level1("f", f0)
