@@ -600,14 +600,12 @@ KsFn ks_post_fn(int nu, bool vz, int nm) {
   return nullptr;
 }
 
-#define KS_SMEM_BYTES (4 * KS_WARP_SMEM_DOUBLES * (int)sizeof(double))
-
-int ks_slots(kc_handle* h, const void* fn) {
+int ks_slots(kc_handle* h, const void* fn, int D) {
   auto it = h->ks_occ.find(fn);
   if (it != h->ks_occ.end()) return it->second;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, KS_SMEM_BYTES);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ks_smem_bytes(D));
   int blocks = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, 128, KS_SMEM_BYTES) != cudaSuccess || blocks < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, 128, ks_smem_bytes(D)) != cudaSuccess || blocks < 1)
     blocks = 1;
   const int slots = blocks * 4 * h->num_sms;
   h->ks_occ[fn] = slots;
@@ -635,7 +633,11 @@ StreamParams ks_params(kc_handle* h, int l, int D, int* nwarps, const void* fn) 
   p.mcr = C.m;
   p.hbc = 1;
   p.nbands = (C.m + 1 + ks_npb(D) - 1) / ks_npb(D);
-  p.nq = ks_choose_nq(C.m, p.nbands, fn ? ks_slots(h, fn) : 148 * 12);
+  const int slots = fn ? ks_slots(h, fn, D) : 148 * 12;
+  p.nq = ks_choose_nq(C.m, p.nbands, slots);
+  // more than 16 warps per SM only where the chunks stay long enough that
+  // the extra warm-up rows (2D+1 per chunk) cost < 10 % of the streamed rows
+  if (10 * (2 * D + 1) > 2 * p.nq) p.nq = ks_choose_nq(C.m, p.nbands, std::min(slots, 16 * h->num_sms));
   *nwarps = p.nbands * ((C.m + 1 + p.nq - 1) / p.nq);
   return p;
 }
@@ -710,7 +712,7 @@ int ex_pre(kc_handle* h, int l, bool norms = false) {
     if (32 * nw > h->npart_cap) KC_FAIL(h, KC_EINVAL, "norm partial buffer too small (%d < %d)", h->npart_cap, 32 * nw);
     p.part = h->d_npart;
   }
-  fn<<<(nw + 3) / 4, 128, KS_SMEM_BYTES, h->stream>>>(p);
+  fn<<<(nw + 3) / 4, 128, ks_smem_bytes(h->nu1 + 1), h->stream>>>(p);
   KC_LAUNCH_CHECK(h);
   ++h->launches;
   if (norms) {
@@ -747,7 +749,7 @@ int ex_post(kc_handle* h, int l, int nm) {
     if (need > h->npart_cap) KC_FAIL(h, KC_EINVAL, "norm partial buffer too small (%d < %d)", h->npart_cap, need);
     p.part = h->d_npart;
   }
-  fn<<<(nw + 3) / 4, 128, KS_SMEM_BYTES, h->stream>>>(p);
+  fn<<<(nw + 3) / 4, 128, ks_smem_bytes(D > 0 ? D : 1), h->stream>>>(p);
   KC_LAUNCH_CHECK(h);
   ++h->launches;
   if (nm == 1) {
@@ -2011,7 +2013,7 @@ extern "C" int kc_strip_norms(const double* v, const double* f, int ny, int nx, 
 // instead of nu + 2 per-op kernels, and two halo exchanges
 // ---------------------------------------------------------------------------
 namespace {
-int strip_slots(const void* fn) {
+int strip_slots(const void* fn, int D) {
   static std::map<const void*, int> cache;
   static int sms = 0;
   auto it = cache.find(fn);
@@ -2021,9 +2023,9 @@ int strip_slots(const void* fn) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, KS_SMEM_BYTES);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ks_smem_bytes(D));
   int blocks = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, 128, KS_SMEM_BYTES) != cudaSuccess || blocks < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, 128, ks_smem_bytes(D)) != cudaSuccess || blocks < 1)
     blocks = 1;
   return cache[fn] = blocks * 4 * sms;
 }
@@ -2066,7 +2068,7 @@ StreamParams strip_params(int rows, int nx, int pitch, int pitch_c, int crows, i
   p.mcr = crows;
   p.hbc = hbc;
   p.nbands = (p.mc + 1 + ks_npb(D) - 1) / ks_npb(D);
-  p.nq = ks_choose_nq(crows, p.nbands, strip_slots(fn));
+  p.nq = ks_choose_nq(crows, p.nbands, strip_slots(fn, D));
   *nwarps = p.nbands * ((crows + 1 + p.nq - 1) / p.nq);
   return p;
 }
@@ -2087,7 +2089,7 @@ extern "C" int kc_strip_pre(const double* u, const double* f, double* uo, double
   p.f = f - ob;
   p.uo = uo - ob;
   p.fc = fc - obc;
-  fn<<<(nw + 3) / 4, 128, KS_SMEM_BYTES, (cudaStream_t)stream>>>(p);
+  fn<<<(nw + 3) / 4, 128, ks_smem_bytes(nu1 + 1), (cudaStream_t)stream>>>(p);
   return strip_err(cudaGetLastError());
 }
 
@@ -2108,7 +2110,7 @@ extern "C" int kc_strip_post(const double* u, const double* f, double* uo, const
   p.f = f - ob;
   p.uo = uo - ob;
   p.vc = vc - obc;
-  fn<<<(nw + 3) / 4, 128, KS_SMEM_BYTES, (cudaStream_t)stream>>>(p);
+  fn<<<(nw + 3) / 4, 128, ks_smem_bytes(nu2 > 0 ? nu2 : 1), (cudaStream_t)stream>>>(p);
   return strip_err(cudaGetLastError());
 }
 

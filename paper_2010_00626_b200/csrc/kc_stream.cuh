@@ -8,9 +8,12 @@
 //                          (the stand-alone stopping test, cycle.py:345).
 //
 // Each warp streams down a band of 64 fine columns (2 per lane), one input
-// row per step.  Stage t (t = 1..D) computes row yin - 2t from the last three
-// rows of stage t-1, so the stages of one step are independent (ILP); the
-// x-neighbours come from warp shuffles.  Every stage loses one column of
+// row per step.  Stage t (t = 1..D) takes the row stage t-1 produced in the
+// same step and completes its own row yin - t: the 9-point sum of an output
+// row is accumulated over the three steps that deliver its south, centre and
+// north input rows (ks_step; the reference's C order is kept), so each row
+// is shuffled once for its x-neighbours and the dependent chain per stage
+// and step is three taps plus the update.  Every stage loses one column of
 // validity per side, so a band owns NPB coarse columns (2*NPB fine columns)
 // and recomputes a thin halo; rows stream without recomputation apart from a
 // short warm-up per chunk, and the chunks are sized so all warps of a launch
@@ -46,34 +49,6 @@ struct StreamParams {
 __device__ __forceinline__ double kc_shfl_up1(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
 __device__ __forceinline__ double kc_shfl_dn1(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 
-// Jacobi (JAC) or residual at the lane's two columns from three rows
-// (r0 = south, r1 = centre, r2 = north), own values and shuffled edges.
-// rx, ry receive the residual f - A u at the two points (the Jacobi update is
-// u + c (f - A u) with that very difference, kc_jacobi_pt).
-template <bool JAC>
-__device__ __forceinline__ void ks_stencil2(const St9& s, double2 r0, double2 r1, double2 r2, double2 fv,
-                                            double& ox, double& oy, double& rx, double& ry) {
-  const double l0 = kc_shfl_up1(r0.y), l1 = kc_shfl_up1(r1.y), l2 = kc_shfl_up1(r2.y);
-  const double e0 = kc_shfl_dn1(r0.x), e1 = kc_shfl_dn1(r1.x), e2 = kc_shfl_dn1(r2.x);
-  const double ax = kc_sum9(s, l0, r0.x, r0.y, l1, r1.x, r1.y, l2, r2.x, r2.y);
-  const double ay = kc_sum9(s, r0.x, r0.y, e0, r1.x, r1.y, e1, r2.x, r2.y, e2);
-  rx = DSUB(fv.x, ax);
-  ry = DSUB(fv.y, ay);
-  if (JAC) {
-    ox = DADD(r1.x, DMUL(s.c, rx));
-    oy = DADD(r1.y, DMUL(s.c, ry));
-  } else {
-    ox = rx;
-    oy = ry;
-  }
-}
-template <bool JAC>
-__device__ __forceinline__ void ks_stencil2(const St9& s, double2 r0, double2 r1, double2 r2, double2 fv,
-                                            double& ox, double& oy) {
-  double rx, ry;
-  ks_stencil2<JAC>(s, r0, r1, r2, fv, ox, oy, rx, ry);
-}
-
 // per-warp partial sums (a, b) -> part[2 wg], part[2 wg + 1]
 __device__ __forceinline__ void ks_warp_partials(double a, double b, double* __restrict__ part, int wg, int lane) {
   for (int o = 16; o > 0; o >>= 1) {
@@ -103,8 +78,11 @@ __device__ __forceinline__ double2 ks_ld2(const double* __restrict__ a, size_t i
 // holds a register (a register queue would make every shift wait for it).
 #define KS_PF 4       // prefetch distance (rows)
 #define KS_URING 8    // u ring slots (> KS_PF)
-#define KS_FRING 16   // f ring slots (> 2*D + KS_PF)
-#define KS_WARP_SMEM_DOUBLES ((KS_URING + KS_FRING) * KS_BAND)
+// f ring: stage t reads row yin - t, so rows yin - D .. yin + KS_PF are live
+__host__ __device__ constexpr int ks_fring(int D) { return D + KS_PF + 1 <= 8 ? 8 : 16; }
+__host__ __device__ constexpr int ks_warp_smem_doubles(int D) { return (KS_URING + ks_fring(D)) * KS_BAND; }
+// dynamic shared memory of a 128-thread streaming block with D stages
+__host__ __device__ constexpr int ks_smem_bytes(int D) { return 4 * ks_warp_smem_doubles(D) * (int)sizeof(double); }
 __device__ __forceinline__ void ks_cp16(double* smem, const double* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
@@ -113,12 +91,44 @@ __device__ __forceinline__ void ks_cp_commit() { asm volatile("cp.async.commit_g
 __device__ __forceinline__ void ks_cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(KS_PF) : "memory"); }
 __device__ __forceinline__ double2 ks_lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 
+// Lag-1 stage state of the lane's two columns (x: column c0, y: c0 + 1).
+// The 9-point sum of an output row runs in the reference's C order (south
+// row, centre row, north row; kc_sum9), split over the three steps in which
+// those input rows arrive: b holds the south taps of the row after next, c
+// the south + centre taps of the next output, cen that output's own value.
+// Each input row is shuffled once (its west and east neighbours), not once
+// per use.
+struct KsAcc {
+  double2 b, c, cen;
+};
+__device__ __forceinline__ void ks_step(const St9& s, KsAcc& a, double2 n, double& aux, double& auy,
+                                        double2& cen) {
+  const double l = kc_shfl_up1(n.y), e = kc_shfl_dn1(n.x);
+  aux = DADD(DADD(DADD(a.c.x, DMUL(s.w[6], l)), DMUL(s.w[7], n.x)), DMUL(s.w[8], n.y));
+  auy = DADD(DADD(DADD(a.c.y, DMUL(s.w[6], n.x)), DMUL(s.w[7], n.y)), DMUL(s.w[8], e));
+  cen = a.cen;
+  a.c.x = DADD(DADD(DADD(a.b.x, DMUL(s.w[3], l)), DMUL(s.w[4], n.x)), DMUL(s.w[5], n.y));
+  a.c.y = DADD(DADD(DADD(a.b.y, DMUL(s.w[3], n.x)), DMUL(s.w[4], n.y)), DMUL(s.w[5], e));
+  a.b.x = DADD(DADD(DMUL0(s.w[0], l), DMUL(s.w[1], n.x)), DMUL(s.w[2], n.y));
+  a.b.y = DADD(DADD(DMUL0(s.w[0], n.x), DMUL(s.w[1], n.y)), DMUL(s.w[2], e));
+  a.cen = n;
+}
+// Dirichlet: +0.0 outside the interior (global row y)
+__device__ __forceinline__ void ks_mask(double2& v, int y, int mg, bool colx_in, bool coly_in) {
+  const bool in = y >= 0 && y < mg;
+  v.x = (in && colx_in) ? v.x : 0.0;
+  v.y = (in && coly_in) ? v.y : 0.0;
+}
+
 // ---------------------------------------------------------------------------
 // PRE: NU sweeps + residual + restriction.  NORMS: also ||u||^2 of the input
 // and ||f - A u||^2 (the first stage's residual) as per-warp partials: the
 // stand-alone stopping test of the previous cycle's result (cycle.py:345)
 // at no extra stencil work.
 // ---------------------------------------------------------------------------
+// Stage t (1..D) consumes the row stage t-1 produced in the same step and
+// completes its own output one row behind it (ks_step), so stage t emits row
+// yin - t and a chunk needs only D warm-up rows per side.
 template <int NU, bool ZERO, bool NORMS = false, bool STRIP = false>
 __global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
   constexpr int D = NU + 1;
@@ -143,22 +153,23 @@ __global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
   const bool own_lane = lane >= G::HL / 2 && lane < G::HL / 2 + G::NPB;
   const St9 s = p.s;
 
-  double2 W[D][3];  // last three rows of stages 0..NU (W[NU] feeds the residual)
-  double2 R[3];     // last three residual rows
+  KsAcc A[D + 1];  // pending sums of stages 1..D
 #pragma unroll
-  for (int t = 0; t < D; ++t) W[t][0] = W[t][1] = W[t][2] = make_double2(0.0, 0.0);
-  R[0] = R[1] = R[2] = make_double2(0.0, 0.0);
+  for (int t = 0; t <= D; ++t) A[t].b = A[t].c = A[t].cen = make_double2(0.0, 0.0);
+  double2 R[3] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};  // residual rows
+  double RE[3] = {0.0, 0.0, 0.0};  // their values one column east of the lane's pair
 
   const int ys = 2 * Q0 - D;
-  const int ye = 2 * Q0 + 2 * p.nq + 2 * D + 1;  // inclusive
+  const int ye = 2 * Q0 + 2 * p.nq + D;  // inclusive: residual row 2 (Q0 + nq)
   // only warps touching the domain boundary need masks / row clamping
-  const bool edge = XS < 0 || XS + KS_BAND - 1 >= m || g_y0 + ys - 2 * D < 0 || g_y0 + ye + 2 >= g_mg;
+  const bool edge = XS < 0 || XS + KS_BAND - 1 >= m || g_y0 + ys - D - 1 < 0 || g_y0 + ye + 1 >= g_mg;
   // rows outside the buffer read its edge rows (the all-zero ghost rows of a
   // whole level): branch-free
   auto rp = [&](int y) -> size_t { return kc_idx(P, min(max(y, -g_hb), g_rows + g_hb - 1), c0); };
   // shared-memory rings (this warp's slice): u rows and f rows
   extern __shared__ double ks_smem[];
-  double* ring = ks_smem + (threadIdx.x >> 5) * KS_WARP_SMEM_DOUBLES + 2 * lane;
+  constexpr int FR = ks_fring(D);
+  double* ring = ks_smem + (threadIdx.x >> 5) * ks_warp_smem_doubles(D) + 2 * lane;
   double* uring = ring;
   double* fring = ring + KS_URING * KS_BAND;
   // one commit group per row: f(y) and, for rows the loop consumes, u(y).
@@ -167,85 +178,71 @@ __global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
   auto fetch = [&](int y, bool with_u) {
     const size_t i = rp(y);
     if (!ZERO && with_u) ks_cp16(uring + (y & (KS_URING - 1)) * KS_BAND, p.u + i);
-    ks_cp16(fring + (y & (KS_FRING - 1)) * KS_BAND, p.f + i);
+    ks_cp16(fring + (y & (FR - 1)) * KS_BAND, p.f + i);
     ks_cp_commit();
   };
-  // f rows from ys-2D (stage D's first row) up to ys+KS_PF-1 before the first step
-  for (int y = ys - 2 * D; y < ys + KS_PF; ++y) fetch(y, y >= ys);
+  // f rows from ys-D (stage D's row in the first step) up to ys+KS_PF-1
+  for (int y = ys - D; y < ys + KS_PF; ++y) fetch(y, y >= ys);
   for (int yin = ys; yin <= ye; ++yin) {
     fetch(yin + KS_PF, true);
     ks_cp_wait();  // all but the newest KS_PF groups done: rows <= yin have landed
     const double2 u0 = ZERO ? make_double2(0.0, 0.0) : ks_lds2(uring + (yin & (KS_URING - 1)) * KS_BAND);
-    double2 fr[D + 1];  // f of the row each stage computes
+    double2 fr[D + 1];  // f of the row each stage completes (yin - t)
 #pragma unroll
-    for (int t = 1; t <= D; ++t) fr[t] = ks_lds2(fring + ((yin - 2 * t) & (KS_FRING - 1)) * KS_BAND);
+    for (int t = 1; t <= D; ++t) fr[t] = ks_lds2(fring + ((yin - t) & (FR - 1)) * KS_BAND);
 
-    // ---- all stages from the pre-step windows (independent) -------------
-    double2 nw[D + 1];
-    nw[0] = u0;
     // NORMS: rows owned by this chunk, interior columns owned by this lane;
-    // the input's residual is the first stage's f - A u at row yin - 2
-    const int y1 = yin - 2;
+    // the input's residual is the first stage's f - A u at row yin - 1
+    const int y1 = yin - 1;
     const bool own_e = NORMS && own_lane && yin >= 2 * Q0 && yin < 2 * Q0 + 2 * p.nq && yin < g_rows;
     const bool own_r = NORMS && own_lane && y1 >= 2 * Q0 && y1 < 2 * Q0 + 2 * p.nq && y1 >= 0 && y1 < g_rows;
     if (own_e) acc_e = fma(u0.y, u0.y, fma(u0.x, u0.x, acc_e));
+    double2 nw[D + 1];
+    nw[0] = u0;
+    if (edge) ks_mask(nw[0], yin + g_y0, g_mg, colx_in, coly_in);  // Dirichlet: +0.0 outside the interior
 #pragma unroll
     for (int t = 1; t <= D; ++t) {
       double ox, oy;
-      if (t <= NU) {
-        if (ZERO && t == 1) {  // first sweep on the zero guess: 0 + c f
-          ox = kc_jacobi_zero(fr[1].x, s.c);
-          oy = kc_jacobi_zero(fr[1].y, s.c);
-        } else if (NORMS && t == 1) {
-          double rx, ry;
-          ks_stencil2<true>(s, W[0][0], W[0][1], W[0][2], fr[1], ox, oy, rx, ry);
-          if (own_r) acc_r = fma(colx_in ? rx : 0.0, rx, fma(coly_in ? ry : 0.0, ry, acc_r));
-        } else {
-          ks_stencil2<true>(s, W[t - 1][0], W[t - 1][1], W[t - 1][2], fr[t], ox, oy);
-        }
-      } else if (ZERO && NU == 0) {  // residual of the zero guess: f exactly
-        ox = fr[t].x;
-        oy = fr[t].y;
+      if (ZERO && t == 1) {  // first sweep on the zero guess: 0 + c f (NU = 0: the residual is f)
+        ox = NU > 0 ? kc_jacobi_zero(fr[1].x, s.c) : fr[1].x;
+        oy = NU > 0 ? kc_jacobi_zero(fr[1].y, s.c) : fr[1].y;
       } else {
-        ks_stencil2<false>(s, W[t - 1][0], W[t - 1][1], W[t - 1][2], fr[t], ox, oy);
-        if (NORMS && t == 1 && own_r) acc_r = fma(colx_in ? ox : 0.0, ox, fma(coly_in ? oy : 0.0, oy, acc_r));
+        double ax, ay;
+        double2 cen;
+        ks_step(s, A[t], nw[t - 1], ax, ay, cen);
+        const double rx = DSUB(fr[t].x, ax), ry = DSUB(fr[t].y, ay);
+        if (t <= NU) {
+          ox = DADD(cen.x, DMUL(s.c, rx));  // kc_jacobi_pt
+          oy = DADD(cen.y, DMUL(s.c, ry));
+        } else {
+          ox = rx;
+          oy = ry;
+        }
+        if (NORMS && t == 1 && own_r) acc_r = fma(colx_in ? rx : 0.0, rx, fma(coly_in ? ry : 0.0, ry, acc_r));
       }
       nw[t] = make_double2(ox, oy);
-    }
-    if (edge) {  // Dirichlet: every stage is +0.0 outside the interior
-#pragma unroll
-      for (int t = 0; t <= D; ++t) {
-        const int y = yin - 2 * t + g_y0;  // global row
-        const bool in = y >= 0 && y < g_mg;
-        nw[t].x = (in && colx_in) ? nw[t].x : 0.0;
-        nw[t].y = (in && coly_in) ? nw[t].y : 0.0;
-      }
+      if (edge) ks_mask(nw[t], yin - t + g_y0, g_mg, colx_in, coly_in);
     }
 
-    // ---- restriction from the residual rows of earlier steps ------------
-    {
-      const int yr = yin - 1 - 2 * D;  // newest residual row in R[2]
-      const double e0 = kc_shfl_dn1(R[0].x), e1 = kc_shfl_dn1(R[1].x), e2 = kc_shfl_dn1(R[2].x);
-      const int q = (yr >> 1) - 1;
-      if (!(yr & 1) && own_lane && q >= Q0 && q < Q0 + p.nq && q < g_mcr && q >= 0 && pcol < p.mc)
-        p.fc[kc_idx(p.Pc, q, pcol)] = kc_fw(R[0].x, R[0].y, e0, R[1].x, R[1].y, e1, R[2].x, R[2].y, e2);
-    }
-    // ---- output v after NU sweeps ----------------------------------------
-    if (NU > 0) {
-      const int y = yin - 2 * NU;
-      if (own_lane && y >= 2 * Q0 && y < 2 * Q0 + 2 * p.nq && y >= 0 && y < g_rows)
-        *reinterpret_cast<double2*>(p.uo + kc_idx(P, y, c0)) = nw[NU];
-    }
-    // ---- shift windows ----------------------------------------------------
-#pragma unroll
-    for (int t = 0; t < D; ++t) {
-      W[t][0] = W[t][1];
-      W[t][1] = W[t][2];
-      W[t][2] = nw[t];
-    }
+    // ---- restriction: residual rows yr-2, yr-1, yr (yr = yin - D, newest) --
     R[0] = R[1];
     R[1] = R[2];
     R[2] = nw[D];
+    RE[0] = RE[1];
+    RE[1] = RE[2];
+    RE[2] = kc_shfl_dn1(nw[D].x);
+    {
+      const int yr = yin - D;
+      const int q = (yr >> 1) - 1;
+      if (!(yr & 1) && own_lane && q >= Q0 && q < Q0 + p.nq && q < g_mcr && q >= 0 && pcol < p.mc)
+        p.fc[kc_idx(p.Pc, q, pcol)] = kc_fw(R[0].x, R[0].y, RE[0], R[1].x, R[1].y, RE[1], R[2].x, R[2].y, RE[2]);
+    }
+    // ---- output v after NU sweeps ----------------------------------------
+    if (NU > 0) {
+      const int y = yin - NU;
+      if (own_lane && y >= 2 * Q0 && y < 2 * Q0 + 2 * p.nq && y >= 0 && y < g_rows)
+        *reinterpret_cast<double2*>(p.uo + kc_idx(P, y, c0)) = nw[NU];
+    }
     // per-lane partials, stored from inside the loop: any code after it (a
     // warp reduction, even a store) makes the compiler wrap the hot loop in
     // a reconvergence region with divergence checks at every shuffle
@@ -284,13 +281,12 @@ __global__ void __launch_bounds__(128, 4) k_post(const StreamParams p) {
   const St9 s = p.s;
 
   if (active) {
-    double2 W[DD][3];
+    KsAcc A[DD + 1];
 #pragma unroll
-    for (int t = 0; t < DD; ++t) W[t][0] = W[t][1] = W[t][2] = make_double2(0.0, 0.0);
+    for (int t = 0; t <= DD; ++t) A[t].b = A[t].c = A[t].cen = make_double2(0.0, 0.0);
     const int ys = 2 * Q0 - D;
-    const int ye = 2 * Q0 + 2 * p.nq - 1 + 2 * D;
-    const bool edge =
-        XS < 0 || XS + KS_BAND - 1 >= m || g_y0 + ys - 2 * D - 2 < 0 || g_y0 + ye + 4 >= g_mg;
+    const int ye = 2 * Q0 + 2 * p.nq - 1 + D;
+    const bool edge = XS < 0 || XS + KS_BAND - 1 >= m || g_y0 + ys - D - 2 < 0 || g_y0 + ye + 2 >= g_mg;
     auto rp = [&](int y) -> size_t { return kc_idx(P, min(max(y, -g_hb), g_rows + g_hb - 1), c0); };
     auto ldc = [&](int q) -> double {
       return __ldg(p.vc + kc_idx(p.Pc, min(max(q, -g_hbc), g_mcr + g_hbc - 1), pc));
@@ -299,23 +295,24 @@ __global__ void __launch_bounds__(128, 4) k_post(const StreamParams p) {
     int qcur = ys >> 1;  // arithmetic shift: floor
     double vcp = ldc(qcur - 1), vcc = ldc(qcur), vcn = ldc(qcur + 1);
     extern __shared__ double ks_smem[];
-    double* ring = ks_smem + (threadIdx.x >> 5) * KS_WARP_SMEM_DOUBLES + 2 * lane;
+    constexpr int FR = ks_fring(DD);
+    double* ring = ks_smem + (threadIdx.x >> 5) * ks_warp_smem_doubles(DD) + 2 * lane;
     double* uring = ring;
     double* fring = ring + KS_URING * KS_BAND;
     auto fetch = [&](int y, bool with_u) {  // see k_pre: u only from row ys on
       const size_t i = rp(y);
       if (!VZ && with_u) ks_cp16(uring + (y & (KS_URING - 1)) * KS_BAND, p.u + i);
-      ks_cp16(fring + (y & (KS_FRING - 1)) * KS_BAND, p.f + i);
+      ks_cp16(fring + (y & (FR - 1)) * KS_BAND, p.f + i);
       ks_cp_commit();
     };
-    for (int y = ys - 2 * D; y < ys + KS_PF; ++y) fetch(y, y >= ys);
+    for (int y = ys - D; y < ys + KS_PF; ++y) fetch(y, y >= ys);
     for (int yin = ys; yin <= ye; ++yin) {
       fetch(yin + KS_PF, true);
       ks_cp_wait();
       const double2 u0 = VZ ? make_double2(0.0, 0.0) : ks_lds2(uring + (yin & (KS_URING - 1)) * KS_BAND);
-      double2 fr[DD + 1];
+      double2 fr[DD + 1];  // f of row yin - t
 #pragma unroll
-      for (int t = 1; t <= D; ++t) fr[t] = ks_lds2(fring + ((yin - 2 * t) & (KS_FRING - 1)) * KS_BAND);
+      for (int t = 1; t <= D; ++t) fr[t] = ks_lds2(fring + ((yin - t) & (FR - 1)) * KS_BAND);
       const int q = yin >> 1;
       if (q != qcur) {  // advance the coarse window by one row (yin even); warp-uniform
         vcp = vcc;
@@ -335,25 +332,20 @@ __global__ void __launch_bounds__(128, 4) k_post(const StreamParams p) {
       }
       double2 nw[DD + 1];
       nw[0] = make_double2(DADD(VZ ? 0.0 : u0.x, ex), DADD(VZ ? 0.0 : u0.y, ey));
+      if (edge) ks_mask(nw[0], yin + g_y0, g_mg, colx_in, coly_in);
 #pragma unroll
       for (int t = 1; t <= D; ++t) {
-        double ox, oy;
-        if (t <= NU) ks_stencil2<true>(s, W[t - 1][0], W[t - 1][1], W[t - 1][2], fr[t], ox, oy);
-        else ks_stencil2<false>(s, W[t - 1][0], W[t - 1][1], W[t - 1][2], fr[t], ox, oy);
-        nw[t] = make_double2(ox, oy);
-      }
-      if (edge) {  // Dirichlet: every stage is +0.0 outside the interior
-#pragma unroll
-        for (int t = 0; t <= D; ++t) {
-          const int y = yin - 2 * t + g_y0;  // global row
-          const bool in = y >= 0 && y < g_mg;
-          nw[t].x = (in && colx_in) ? nw[t].x : 0.0;
-          nw[t].y = (in && coly_in) ? nw[t].y : 0.0;
-        }
+        double ax, ay;
+        double2 cen;
+        ks_step(s, A[t], nw[t - 1], ax, ay, cen);
+        const double rx = DSUB(fr[t].x, ax), ry = DSUB(fr[t].y, ay);
+        if (t <= NU) nw[t] = make_double2(DADD(cen.x, DMUL(s.c, rx)), DADD(cen.y, DMUL(s.c, ry)));
+        else nw[t] = make_double2(rx, ry);
+        if (edge) ks_mask(nw[t], yin - t + g_y0, g_mg, colx_in, coly_in);
       }
       // output after NU sweeps (stage NU; NU = 0 writes the corrected v)
       {
-        const int y = yin - 2 * NU;
+        const int y = yin - NU;
         if (own_lane && y >= 2 * Q0 && y < 2 * Q0 + 2 * p.nq && y >= 0 && y < g_rows) {
           *reinterpret_cast<double2*>(p.uo + kc_idx(P, y, c0)) = nw[NU];
           if (NORMS) acc_e = fma(nw[NU].y, nw[NU].y, fma(nw[NU].x, nw[NU].x, acc_e));
@@ -361,15 +353,9 @@ __global__ void __launch_bounds__(128, 4) k_post(const StreamParams p) {
         }
       }
       if (NORMS) {
-        const int y = yin - 2 * D;
+        const int y = yin - D;
         if (own_lane && y >= 2 * Q0 && y < 2 * Q0 + 2 * p.nq && y >= 0 && y < g_rows)
           acc_r = fma(nw[D].y, nw[D].y, fma(nw[D].x, nw[D].x, acc_r));
-      }
-#pragma unroll
-      for (int t = 0; t < DD; ++t) {
-        W[t][0] = W[t][1];
-        W[t][1] = W[t][2];
-        W[t][2] = nw[t];
       }
       if (DOT && yin == ye) reinterpret_cast<double2*>(p.part)[wg * 32 + lane] = make_double2(acc_e, 0.0);
     }
