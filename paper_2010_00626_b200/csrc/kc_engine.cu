@@ -95,7 +95,10 @@ enum OpKind : int { OP_RELAX, OP_RESTRICT, OP_ZERO, OP_PROLONG, OP_COARSEST, OP_
 #define KC_FUSE_MAXNU 4      // fused streaming kernels exist for nu <= 4
 #define KC_FUSE_MIN_M 127    // HBM levels handled by the fused kernels
 #ifndef KC_TILE_MAX_M
-#define KC_TILE_MAX_M 511    // up to this side the overlapped-tile kernels beat streaming
+#define KC_TILE_MAX_M 511    // up to this side the overlapped-tile pre kernel beats streaming
+#endif
+#ifndef KC_TILE_POST_MAX_M
+#define KC_TILE_POST_MAX_M 255  // the lag-1 streaming post pass wins from 511 up (measured 10.3 vs 12.2 us)
 #endif
 struct Op {
   int kind, level, a, b;
@@ -738,7 +741,7 @@ int ex_post(kc_handle* h, int l, int nm) {
   int rc = ex_materialize(h, l + 1);
   if (rc) return rc;
   if (nm == 2 && h->nu2 < 1) KC_FAIL(h, KC_EINVAL, "fused r.z needs nu2 >= 1");
-  if (L.m <= KC_TILE_MAX_M && h->tile && !nm) return ex_tile(h, l, false);
+  if (L.m <= KC_TILE_POST_MAX_M && h->tile && !nm) return ex_tile(h, l, false);
   int nw = 0;
   const int D = h->nu2 + (nm == 1 ? 1 : 0);
   KsFn fn = ks_post_fn(h->nu2, L.vzero, nm);
