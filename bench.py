@@ -242,9 +242,10 @@ def run_ours_distributed(args, rank: int, world: int, local_rank: int):
     solver = DistributedKappaSolver(problem, kc.CycleConfig(n=n, kappa=kappa), TorchComm(), device=local_rank,
                                     min_rows=64)
     v0 = np.random.default_rng(0).random((m, m))
-    rep = solver.solve_standalone(args.target, 20000, initial_guess=v0, stop="residual")
-    solver.snapshot()
-    for _ in range(args.warmup):
+    solver.set_level1("v", v0)
+    solver.set_level1("f", np.zeros((m, m)))
+    solver.snapshot()  # the initial guess, restored before every solve
+    for _ in range(max(1, args.warmup)):
         solver.restore()
         rep = solver.solve_standalone(args.target, 20000, stop="residual", resident=True)
     stream = torch.cuda.current_stream()
@@ -541,18 +542,23 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if world > 1:
+    # KC_BENCH_FORCE_DIST=1: the N > 1 code path (NCCL process group, strip
+    # solver) on a single GPU, to exercise it where only one GPU is available
+    dist_path = world > 1 or os.environ.get("KC_BENCH_FORCE_DIST") == "1"
+    if dist_path:
         import torch
         import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"), rank=rank, world_size=world)
     try:
-        if world > 1:
+        if dist_path:
             run_ours_distributed(args, rank, world, local_rank)
         else:
             run_ours(args, rank, world, local_rank)
     finally:
-        if world > 1:
+        if dist_path:
             import torch.distributed as dist
             dist.destroy_process_group()
 

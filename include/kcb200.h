@@ -197,6 +197,22 @@ int kc_strip_post(const double* u, const double* f, double* uo, const double* vc
 int kc_set_device(kc_handle* h, int level, int which, const double* dev, long long ny, long long nx,
                   long long pitch);
 int kc_get_device(kc_handle* h, int level, int which, double* dev, long long ny, long long nx, long long pitch);
+/* the same without waiting for the copy (ordered on the handle's stream) */
+int kc_set_device_async(kc_handle* h, int level, int which, const double* dev, long long ny, long long nx,
+                        long long pitch);
+int kc_get_device_async(kc_handle* h, int level, int which, double* dev, long long ny, long long nx,
+                        long long pitch);
+
+/* issue all further work of the handle on `stream` (a cudaStream_t, NULL =
+ * CUDA's stream 0; (void*)-1 = the handle's own stream again), e.g. a
+ * framework's current stream, so the engine orders with the caller's kernels
+ * and collectives */
+int kc_set_stream(kc_handle* h, void* stream);
+
+/* one kappa-cycle (kappa_cycle from level 1, cycle.py:204-220) issued op by op
+ * on the handle's stream without waiting: capturable into the caller's CUDA
+ * graph once the same cycle has run outside a capture */
+int kc_cycle_enqueue(kc_handle* h, int kappa);
 
 #ifdef __cplusplus
 }

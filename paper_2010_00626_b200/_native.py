@@ -95,6 +95,10 @@ _SIGS = {
                       + [_dp, C.c_double, C.c_int, C.c_int, C.c_void_p]),
     "kc_set_device": (C.c_int, [_h, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_longlong, C.c_longlong]),
     "kc_get_device": (C.c_int, [_h, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_longlong, C.c_longlong]),
+    "kc_set_device_async": (C.c_int, [_h, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_longlong, C.c_longlong]),
+    "kc_get_device_async": (C.c_int, [_h, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_longlong, C.c_longlong]),
+    "kc_set_stream": (C.c_int, [_h, C.c_void_p]),
+    "kc_cycle_enqueue": (C.c_int, [_h, C.c_int]),
     "kc_restore": (C.c_int, [_h]),
 }
 

@@ -134,7 +134,8 @@ struct kc_handle {
   bool line_singular = false;
   // host-built bottom phase schedules, keyed by (kappa1, kappa2, v_zero)
   std::map<std::tuple<int, int, int>, std::tuple<unsigned*, int, int>> bot_sched;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;      // the stream every operation is issued on
+  cudaStream_t own_stream = nullptr;  // created by kc_create (kc_set_stream may redirect `stream`)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double* d_part = nullptr;     // reduction partials
   double* d_scal = nullptr;     // device scalars
@@ -1148,7 +1149,7 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
       else L.f = ptr;
     }
   }
-  if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
+  if (cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&h->ev0) != cudaSuccess || cudaEventCreate(&h->ev1) != cudaSuccess ||
       cudaMalloc(&h->d_part, sizeof(double) * KC_RED_BLOCKS) != cudaSuccess ||
       cudaMalloc(&h->d_scal, sizeof(double) * 64) != cudaSuccess ||
@@ -1156,6 +1157,7 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
     h->err = "stream/event/scratch allocation failed";
     return fail(KC_ECUDA);
   }
+  h->stream = h->own_stream;
   cudaMemset(h->d_scal, 0, sizeof(double) * 64);
 
   // zebra line-solve plans and the semi-y coarsest line (data independent)
@@ -1296,7 +1298,7 @@ int kc_destroy(kc_handle* h) {
   if (h->h_scal) cudaFreeHost(h->h_scal);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
-  if (h->stream) cudaStreamDestroy(h->stream);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
   return KC_OK;
 }
@@ -1999,13 +2001,13 @@ extern "C" int kc_strip_norms(const double* v, const double* f, int ny, int nx, 
                               double* out, void* stream) {
   if (!v || !f || !out || !w9) return KC_EINVAL;
   static thread_local double* part = nullptr;  // per-thread scratch for the block partials
-  const int nb = 256;
+  const int nb = 1184;  // 8 blocks per SM: enough rows in flight to stream v and f
   if (!part) {
     cudaError_t e = cudaMalloc(&part, sizeof(double) * 2 * nb);
     if (e != cudaSuccess) return strip_err(e);
   }
   k_strip_norms<<<nb, 256, 0, (cudaStream_t)stream>>>(v, f, ny, nx, pitch, strip_stencil(w9, 1.0), part);
-  k_strip_norms_final<<<1, 32, 0, (cudaStream_t)stream>>>(part, nb, out);
+  k_strip_norms_final<<<1, 256, 0, (cudaStream_t)stream>>>(part, nb, out);
   return strip_err(cudaGetLastError());
 }
 
@@ -2117,8 +2119,8 @@ extern "C" int kc_strip_post(const double* u, const double* f, double* uo, const
   return strip_err(cudaGetLastError());
 }
 
-extern "C" int kc_set_device(kc_handle* h, int level, int which, const double* dev, long long ny, long long nx,
-                             long long pitch) {
+static int set_device(kc_handle* h, int level, int which, const double* dev, long long ny, long long nx,
+                      long long pitch, bool sync) {
   if (!h || !dev) return KC_EINVAL;
   int rc = check_level(h, level);
   if (rc) return rc;
@@ -2127,13 +2129,13 @@ extern "C" int kc_set_device(kc_handle* h, int level, int which, const double* d
   double* dst = which == KC_WHICH_F ? L.f : L.v[L.cur];
   KC_CUDA(h, cudaMemcpy2DAsync(dst + kc_idx(L.P, 0, 0), sizeof(double) * L.P, dev, sizeof(double) * pitch,
                                sizeof(double) * L.m, L.ny, cudaMemcpyDeviceToDevice, h->stream));
-  KC_CUDA(h, cudaStreamSynchronize(h->stream));
+  if (sync) KC_CUDA(h, cudaStreamSynchronize(h->stream));
   if (which != KC_WHICH_F) L.vzero = false;
   return KC_OK;
 }
 
-extern "C" int kc_get_device(kc_handle* h, int level, int which, double* dev, long long ny, long long nx,
-                             long long pitch) {
+static int get_device(kc_handle* h, int level, int which, double* dev, long long ny, long long nx, long long pitch,
+                      bool sync) {
   if (!h || !dev) return KC_EINVAL;
   int rc = check_level(h, level);
   if (rc) return rc;
@@ -2143,6 +2145,49 @@ extern "C" int kc_get_device(kc_handle* h, int level, int which, double* dev, lo
   const double* src = which == KC_WHICH_F ? L.f : L.v[L.cur];
   KC_CUDA(h, cudaMemcpy2DAsync(dev, sizeof(double) * pitch, src + kc_idx(L.P, 0, 0), sizeof(double) * L.P,
                                sizeof(double) * L.m, L.ny, cudaMemcpyDeviceToDevice, h->stream));
-  KC_CUDA(h, cudaStreamSynchronize(h->stream));
+  if (sync) KC_CUDA(h, cudaStreamSynchronize(h->stream));
+  return KC_OK;
+}
+
+extern "C" int kc_set_device(kc_handle* h, int level, int which, const double* dev, long long ny, long long nx,
+                             long long pitch) {
+  return set_device(h, level, which, dev, ny, nx, pitch, true);
+}
+
+extern "C" int kc_get_device(kc_handle* h, int level, int which, double* dev, long long ny, long long nx,
+                             long long pitch) {
+  return get_device(h, level, which, dev, ny, nx, pitch, true);
+}
+
+extern "C" int kc_set_device_async(kc_handle* h, int level, int which, const double* dev, long long ny,
+                                   long long nx, long long pitch) {
+  return set_device(h, level, which, dev, ny, nx, pitch, false);
+}
+
+extern "C" int kc_get_device_async(kc_handle* h, int level, int which, double* dev, long long ny, long long nx,
+                                   long long pitch) {
+  return get_device(h, level, which, dev, ny, nx, pitch, false);
+}
+
+extern "C" int kc_set_stream(kc_handle* h, void* stream) {
+  if (!h) return KC_EINVAL;
+  // NULL is CUDA's stream 0 (the legacy default stream), (void*)-1 the handle's own
+  h->stream = stream == (void*)-1 ? h->own_stream : (cudaStream_t)stream;
+  return KC_OK;
+}
+
+// One kappa-cycle issued op by op on the handle's stream, nothing awaited:
+// capturable into a caller's CUDA graph (the bottom schedules and occupancy
+// tables are built on first use, so run it once outside a capture first).
+extern "C" int kc_cycle_enqueue(kc_handle* h, int kappa) {
+  if (!h) return KC_EINVAL;
+  if (kappa < 1) KC_FAIL(h, KC_EINVAL, "cycle counter must be >= 1, got %d", kappa);
+  if (kappa > h->n) kappa = h->n;
+  std::vector<Op> ops;
+  flatten(h, 0, kappa, ops);
+  for (const Op& op : ops) {
+    const int rc = ex_op(h, op);
+    if (rc) return rc;
+  }
   return KC_OK;
 }

@@ -89,13 +89,31 @@ __global__ void __launch_bounds__(256) k_strip_norms(const double* __restrict__ 
   }
 }
 
-__global__ void k_strip_norms_final(const double* __restrict__ part, int nb, double* __restrict__ out) {
-  if (threadIdx.x != 0) return;
+__global__ void __launch_bounds__(256) k_strip_norms_final(const double* __restrict__ part, int nb,
+                                                          double* __restrict__ out) {
+  // fixed-order tree over the block partials (deterministic)
   double e = 0.0, r = 0.0;
-  for (int b = 0; b < nb; ++b) {
+  for (int b = threadIdx.x; b < nb; b += 256) {
     e += part[2 * b];
     r += part[2 * b + 1];
   }
-  out[0] = e;
-  out[1] = r;
+  __shared__ double sh[2][8];
+  for (int o = 16; o > 0; o >>= 1) {
+    e += __shfl_down_sync(0xffffffffu, e, o);
+    r += __shfl_down_sync(0xffffffffu, r, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sh[0][threadIdx.x >> 5] = e;
+    sh[1][threadIdx.x >> 5] = r;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double te = 0.0, tr = 0.0;
+    for (int k = 0; k < 8; ++k) {
+      te += sh[0][k];
+      tr += sh[1][k];
+    }
+    out[0] = te;
+    out[1] = tr;
+  }
 }

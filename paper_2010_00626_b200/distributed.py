@@ -71,10 +71,10 @@ class Plan:
 
 def plan_partition(n: int, world: int, min_rows: int = 64) -> Plan:
     """Distributed levels: side >= world * min_rows (at least the finest level
-    when world > 1 and n >= 2); strips even-aligned so coarse rows nest."""
+    when n >= 2); strips even-aligned so coarse rows nest."""
     sides = [2 ** (n - l + 1) - 1 for l in range(1, n + 1)]
     n_dist = 0
-    if world > 1:
+    if world >= 1:  # world 1: one strip per level (the N > 1 code path on one device)
         for l in range(1, n):  # the coarsest level is never distributed
             if sides[l - 1] >= world * min_rows:
                 n_dist = l
@@ -243,7 +243,10 @@ class CudaStripOps:
 
 
 class CudaCoarse:
-    """The agglomerated levels as one native engine hierarchy (replicated per rank)."""
+    """The agglomerated levels as one native engine hierarchy (replicated per
+    rank), issued on the caller's current stream without host waits (the
+    engine follows torch's stream, so a distributed cycle can be captured
+    into one CUDA graph)."""
 
     def __init__(self, problem: ProblemSpec, n_levels: int, ops, smoother, nu1, nu2, device=0):
         from .cycle import CudaGridState
@@ -251,22 +254,30 @@ class CudaCoarse:
         self.state = CudaGridState(spec, ops, smoother, nu1, nu2, device=device)
         self.m = spec.dims[0][0]
 
+    def _bind_stream(self):
+        import torch
+
+        from . import _native as N
+        N.check(N.lib.kc_set_stream(self.state._h, torch.cuda.current_stream().cuda_stream), self.state._h)
+
     def set_f(self, full):  # full: (m + 2*HALO, pitch) tensor with interior at (HALO, KC_OX)
         from . import _native as N
+        self._bind_stream()
         ptr = full.data_ptr() + 8 * (HALO * full.shape[1] + KC_OX)
-        N.check(N.lib.kc_set_device(self.state._h, 1, N.KC_WHICH_F, ptr, self.m, self.m, full.shape[1]),
+        N.check(N.lib.kc_set_device_async(self.state._h, 1, N.KC_WHICH_F, ptr, self.m, self.m, full.shape[1]),
                 self.state._h)
 
     def zero_guess(self):
         self.state.zero_guess(1)
 
     def run(self, kappa):
-        self.state.run_cycles(kappa, 1)
+        from . import _native as N
+        N.check(N.lib.kc_cycle_enqueue(self.state._h, int(kappa)), self.state._h)
 
     def get_v(self, full):
         from . import _native as N
         ptr = full.data_ptr() + 8 * (HALO * full.shape[1] + KC_OX)
-        N.check(N.lib.kc_get_device(self.state._h, 1, N.KC_WHICH_V, ptr, self.m, self.m, full.shape[1]),
+        N.check(N.lib.kc_get_device_async(self.state._h, 1, N.KC_WHICH_V, ptr, self.m, self.m, full.shape[1]),
                 self.state._h)
 
 
@@ -293,7 +304,7 @@ class DistributedKappaSolver:
     """
 
     def __init__(self, problem: ProblemSpec, config: CycleConfig, comm, ops=None, make_coarse=None,
-                 min_rows: int = 64, device: int = 0):
+                 min_rows: int = 64, device: int = 0, graphs: bool = True):
         if config.coarsening is not Coarsening.FULL_STANDARD:
             raise ValueError("distributed cycles support full coarsening only")
         self.problem, self.config, self.comm = problem, config, comm
@@ -322,6 +333,15 @@ class DistributedKappaSolver:
         self.cfull = self.ops.zeros(mc + 2 * HALO, kc_pitch(mc))   # replicated level n_dist+1 (f, then v)
         self.vfull = self.ops.zeros(mc + 2 * HALO, kc_pitch(mc))
         self._stats_cache = {}
+        # one CUDA graph per cycle counter (CUDA strips + NCCL + the native
+        # coarse engine all on torch's stream); captured on the second call
+        self._graphs_ok = (graphs and isinstance(self.ops, CudaStripOps) and isinstance(comm, TorchComm)
+                           and isinstance(self.coarse, CudaCoarse))
+        self._graphs = {}
+        self._warm = set()
+        if self._graphs_ok:
+            import torch
+            self._nrm = torch.zeros(2, dtype=torch.float64, device=self.ops.device)
 
     # -- data in/out -------------------------------------------------------
     def set_level1(self, which: str, full: np.ndarray):
@@ -457,18 +477,67 @@ class DistributedKappaSolver:
             s.vzero = False
             self._relax(l, self.nu2)
 
-    def cycle(self, kappa: int | None = None, stats: CycleStats | None = None):
+    def cycle(self, kappa: int | None = None, stats: CycleStats | None = None, with_norms: bool = False):
         """One kappa-cycle (run_cycle, cycle.py:261-263) over the decomposed hierarchy."""
         k = self.config.effective_kappa if kappa is None else min(kappa, self.n)
         if self.plan.n_dist == 0:
             raise ValueError("nothing to distribute: use the single-GPU engine (run_cycle)")
-        self._cycle(1, k)
+        self._run(k, with_norms and self._graphs_ok)
         if stats is not None:
             if k not in self._stats_cache:
                 st = CycleStats.for_levels(self.n)
                 kappa_cycle(DryState(self.n, self.nu1, self.nu2), 1, k, st)
                 self._stats_cache[k] = st
             stats.absorb(self._stats_cache[k])
+
+    def _host_state(self):
+        return tuple((st.cur, st.vzero) for st in self.strips)
+
+    def _body(self, k: int, with_norms: bool):
+        self._cycle(1, k)
+        if with_norms:  # ||v||^2, ||f - A v||^2 of the result into self._nrm (allreduced)
+            s = self.strips[0]
+            self._halo(s, s.v[s.cur], 1)
+            t = self.ops.norms(s.v[s.cur], s.f, s.ny, s.m, self.w[0])
+            self.comm.allreduce_sum(t)
+            self._nrm.copy_(t)
+
+    def _run(self, k: int, with_norms: bool = False):
+        """One cycle (and optionally the norms of its result): eager on the
+        first call per key, then captured once and replayed as a CUDA graph."""
+        key = (k, with_norms)
+        if self._graphs_ok and key in self._warm:
+            g = self._graphs.get(key)
+            if g is None:
+                g = self._capture(key)
+            if g is not None:
+                g.replay()
+                return
+        self._body(k, with_norms)
+        self._warm.add(key)
+
+    def _capture(self, key):
+        """Capture _body(*key) into a CUDA graph; None (eager from then on)
+        when the cycle does not return the strips to their buffer parity (a
+        replayed graph would read the wrong buffers) or cannot be captured."""
+        import torch
+        state0 = self._host_state()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.graph(g):
+                self._body(*key)
+        except Exception:  # a backend that cannot be captured: stay eager
+            ok = False
+        else:
+            ok = self._host_state() == state0
+        if not ok:
+            for st, (cur, vz) in zip(self.strips, state0):
+                st.cur, st.vzero = cur, vz
+            self._graphs_ok = False
+            return None
+        self._graphs[key] = g
+        return g
 
     def norms(self) -> tuple[float, float]:
         """(||v||, ||f - A v||) of the finest level: partial sums + allreduce."""
@@ -511,9 +580,15 @@ class DistributedKappaSolver:
         if meas[0] <= target:
             status = "converged"
         else:
+            k = self.config.effective_kappa
             for it in range(1, max_cycles + 1):
-                self.cycle(stats=stats)
-                e, r = self.norms()
+                if self._graphs_ok:  # cycle + norms as one graph, one host read
+                    self.cycle(k, stats=stats, with_norms=True)
+                    e2, r2 = self._nrm.tolist()
+                    e, r = math.sqrt(e2), math.sqrt(r2)
+                else:
+                    self.cycle(stats=stats)
+                    e, r = self.norms()
                 err.append(e)
                 res.append(r)
                 if meas[-1] <= target:

@@ -24,7 +24,7 @@ from paper_2010_00626_b200.distributed import DistributedKappaSolver, ThreadComm
 
 def test_plan_partition_properties():
     for n in (5, 7, 9, 12, 14):
-        for world in (2, 3, 4, 8):
+        for world in (1, 2, 3, 4, 8):
             plan = plan_partition(n, world, min_rows=16)
             if plan.n_dist == 0:
                 continue
@@ -77,7 +77,7 @@ def _solver(comm, n, kappa, eps, phi, nu1=2, nu2=2, min_rows=8):
                                   min_rows=min_rows)
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
 @pytest.mark.parametrize("kappa", [1, 2, 3])
 def test_thread_ranks_bit_exact_vs_single_domain(world, kappa):
     n, eps, phi = 7, 1e-3, 30.0

@@ -542,7 +542,8 @@ def test_n12_pcg_vs_reference(kname):
 # multi-rank decomposition with the CUDA strip kernels (thread ranks on one GPU)
 # ---------------------------------------------------------------------------
 
-@pytest.mark.parametrize("world,kappa,nu", [(2, 1, (2, 2)), (2, 3, (2, 2)), (3, 1, (2, 2)), (3, 3, (2, 2)),
+@pytest.mark.parametrize("world,kappa,nu", [(1, 2, (2, 2)), (2, 1, (2, 2)), (2, 3, (2, 2)), (3, 1, (2, 2)),
+                                             (3, 3, (2, 2)),
                                              (2, 2, (1, 1)), (2, 2, (3, 0)), (3, 2, (0, 3)), (2, 2, (4, 4))])
 def test_distributed_cuda_strips_bit_exact(world, kappa, nu):
     """Thread ranks on one GPU: the fused strip passes (kc_strip_pre/post with
@@ -652,3 +653,41 @@ def test_large_nu_native_cycles_bit_exact(nu1, nu2):
         run_cycle(st, cfg, CycleStats.for_levels(n))
         assert np.array_equal(st.v[0], h.v[0]), (nu1, nu2, kappa)
         st.close()
+
+
+def test_distributed_nccl_world1_graph_replay_bit_exact():
+    """The N > 1 production path on one GPU: an NCCL process group of one
+    rank, CUDA strips, the native coarse engine on torch's stream, and the
+    cycle captured into one CUDA graph (first call eager, then capture and
+    replays) -- bit-identical to the oracle cycle by cycle."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2010_00626_b200.distributed import DistributedKappaSolver, TorchComm
+    n, eps, phi, kappa = 9, 1e-4, 45.0, 2
+    m = 2 ** n - 1
+    rng = np.random.default_rng(7)
+    v0, f0 = rng.random((m, m)), rng.standard_normal((m, m))
+    h = O.Hierarchy(O.hierarchy(eps, phi, n))
+    h.v[0], h.f[0] = v0.copy(), f0.copy()
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", device_id=torch.device("cuda:0"), rank=0, world_size=1)
+    try:
+        s = DistributedKappaSolver(ProblemSpec(eps, phi), CycleConfig(n=n, kappa=kappa), TorchComm(), min_rows=32)
+        assert s.plan.n_dist >= 2 and s._graphs_ok
+        s.set_level1("v", v0)
+        s.set_level1("f", f0)
+        for c in range(4):
+            h.cycle(kappa)
+            s.cycle()
+            assert np.array_equal(s.gather_level1(), h.v[0]), c
+        assert (kappa, False) in s._graphs  # cycles 2.. ran as graph replays
+    finally:
+        dist.destroy_process_group()
