@@ -383,11 +383,9 @@ class DistributedKappaSolver:
             if down < self.world:
                 sends[down] = t[HALO + s.ny - depth:HALO + s.ny]
                 recvs[down] = t[HALO + s.ny:HALO + s.ny + depth]
-            # receive into scratch, then copy (views of t must not be written while sent)
-            scratch = {p: self.ops.zeros(depth, t.shape[1]) for p in recvs}
-            self.comm.sendrecv(sends, scratch)
-            for p, dst in recvs.items():
-                dst.copy_(scratch[p])
+            # sent rows and ghost rows are disjoint row blocks (contiguous
+            # views): receive straight into the ghost rows
+            self.comm.sendrecv(sends, recvs)
 
     def _materialize(self, s: _Strip):
         if s.vzero:
