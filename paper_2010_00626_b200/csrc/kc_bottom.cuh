@@ -65,6 +65,17 @@
 
 #define KC_BOT_MAXPH 4096  // phase descriptors per launch (host-checked)
 
+// per-level constants, computed on the host (bot_geometry; the strip rows
+// of each rank are finished on the device) and kept in shared memory: each
+// phase reads a few LDS.128 instead of doing address math
+struct BotLv {
+  int m, S, vo0, vo1;           // side, stride, smem offsets of the v buffers (interior origin)
+  int fo, nitem1, nitem4, rows;  // f offset, stencil items for RB = 1 / 4, own interior rows
+  int a, R, rb4, crows;          // first global row, strip height, RB = 4?, own rows of the child
+  float inv, invc, invn;         // 1/m, 1/m_child, 1/(m_child+1)
+  int mc;                        // child side
+};
+
 struct BotParams {
   int nlev;  // levels resident in smem: entry level .. coarsest
   St9 st[KC_BOT_MAXLEV];
@@ -77,6 +88,8 @@ struct BotParams {
   int final_cur;     // buffer holding the entry level's v after the schedule
   int nu1, nu2;      // sweeps inside PH_TINY frames
   int nstrip;        // leading levels split into row strips over the cluster (0: single CTA)
+  int total;         // shared-memory doubles of all levels (bot_smem_doubles)
+  BotLv lv[KC_BOT_MAXLEV];  // bot_geometry (rank 0's strip rows)
 };
 
 // smem geometry of level d (entry side m0): side m_d = ((m0+1) >> d) - 1,
@@ -102,6 +115,37 @@ __host__ __device__ __forceinline__ int bot_warps(int m) {
   return m >= 31 ? KC_BOT_WARPS : (m >= 15 ? 8 : 1);  // 2 warps at m = 7 measured slower
 }
 
+// Per-level geometry of a launch (host; m0 = entry side, cs = cluster size):
+// what the kernel used to derive with integer divisions in its prologue.
+inline void bot_geometry(BotParams& bp, int m0, int cs) {
+  const int nlev = bp.nlev, nstrip = bp.nstrip;
+  bp.total = bot_smem_doubles(m0, nlev, nstrip, cs);
+  for (int d = 0; d < nlev; ++d) {
+    const bool strip = d < nstrip;
+    const int m = bot_m(m0, d), S = m + 2, base = bot_off(m0, d, nstrip, cs);
+    const int R = bot_rows(m0, d, nstrip, cs);
+    const int mc = d + 1 < nlev ? bot_m(m0, d + 1) : 1;
+    BotLv L{};
+    L.m = m;
+    L.S = S;
+    L.R = R;
+    L.mc = mc;
+    L.a = 0;
+    L.rows = strip ? (R < m ? R : m) : m;
+    L.vo0 = base + S + 1;
+    L.vo1 = base + (R + 2) * S + S + 1;
+    L.fo = base + 2 * (R + 2) * S + S + 1;
+    L.nitem1 = L.rows * m;
+    L.nitem4 = m * ((L.rows + 3) / 4);
+    L.rb4 = strip ? (L.nitem4 >= KC_BOT_THREADS) : (m >= 31);
+    L.crows = strip ? ((mc < L.rows / 2) ? mc : L.rows / 2) : mc;
+    L.inv = 1.0f / (float)m;
+    L.invc = 1.0f / (float)mc;
+    L.invn = 1.0f / (float)(mc + 1);
+    bp.lv[d] = L;
+  }
+}
+
 __device__ __forceinline__ void bot_sync(int g) {
   if (g == KC_BOT_WARPS) __syncthreads();
   else if (g == 1) __syncwarp();
@@ -118,6 +162,17 @@ __device__ long long kc_bot_trace[KC_BOT_TRACE];
 __device__ int kc_bot_trace_op[KC_BOT_TRACE];
 __device__ int kc_bot_trace_n;
 __device__ long long kc_bot_trace_end[KC_BOT_TRACE];
+__device__ unsigned long long kc_bot_stamp[8];  // globaltimer: start, init, entry, phases, end (CTA 0)
+__device__ __forceinline__ void kc_bot_mark(int k) {
+  if (threadIdx.x == 0 && cooperative_groups::this_cluster().block_rank() == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    kc_bot_stamp[k] = t;
+  }
+}
+#define KC_BOT_MARK(k) kc_bot_mark(k)
+#else
+#define KC_BOT_MARK(k)
 #endif
 
 // Phase kinds (host-built list, BotBuilder below):
@@ -237,15 +292,6 @@ struct BotBuilder {  // host side
 
 // y = i / m for i < 2^12, m <= 64: float reciprocal, exact for these ranges
 __device__ __forceinline__ int bot_div(int i, float inv) { return (int)(((float)i + 0.5f) * inv); }
-
-// per-level constants precomputed once per launch (keeps the per-phase
-// dependent integer chain short: a few LDS.128 instead of address math)
-struct BotLv {
-  int m, S, vo0, vo1;           // side, stride, smem offsets of the v buffers (interior origin)
-  int fo, nitem1, nitem4, rows;  // f offset, stencil items for RB = 1 / 4, own interior rows
-  int a, R, rb4, crows;          // first global row, strip height, RB = 4?, own rows of the child
-  float inv, invc, invn, padf;   // 1/m, 1/m_child, 1/(m_child+1)
-};
 
 // Halo pushes of a strip phase: values on own row 0 also go to the upper
 // neighbour's row R (its halo below), values on own row R-1 to the lower
@@ -514,65 +560,106 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
   cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
   const int rank = (int)cl.block_rank(), cs = (int)cl.num_blocks();
   const int nlev = bp.nlev, nstrip = bp.nstrip;
-  const int total = bot_smem_doubles(m0, nlev, nstrip, cs);
-  for (int i = threadIdx.x; i < total; i += KC_BOT_THREADS) sm[i] = 0.0;
-  for (int i = threadIdx.x; i < bp.nsched; i += KC_BOT_THREADS) sched[i] = bp.sched[i];
+  KC_BOT_MARK(0);
+  // Prologue, ordered so the global latencies overlap: schedule and level
+  // constants into registers, the entry level's rows as 8-byte cp.async
+  // copies straight into shared memory, then zero everything those copies
+  // do not cover (ghost rings, halos, coarser levels), then publish.
+  constexpr int SCHED_PER_THREAD = (KC_BOT_MAXPH + KC_BOT_THREADS - 1) / KC_BOT_THREADS;
+  unsigned sreg[SCHED_PER_THREAD];
+#pragma unroll
+  for (int k = 0; k < SCHED_PER_THREAD; ++k) {
+    const int i = threadIdx.x + k * KC_BOT_THREADS;
+    sreg[k] = i < bp.nsched ? __ldg(bp.sched + i) : 0u;
+  }
+  const int dl = threadIdx.x < nlev ? threadIdx.x : 0;
+  const St9 st_d = bp.st[dl];
+  const BotLv lv_d = bp.lv[dl];
+  const int total = bp.total;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  auto cp8 = [](double* dst, const double* src) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src) : "memory");
+  };
+  auto zero = [&](int lo, int hi) {  // sm[lo, hi)
+    if (lo >= hi) return;
+    if ((lo & 1) && threadIdx.x == 0) sm[lo] = 0.0;
+    const int l2 = (lo + 1) >> 1, h2 = hi >> 1;
+    double2* z2 = reinterpret_cast<double2*>(sm);  // dynamic smem is 16-byte aligned
+    for (int i = l2 + threadIdx.x; i < h2; i += KC_BOT_THREADS) z2[i] = make_double2(0.0, 0.0);
+    if ((hi & 1) && hi - 1 >= lo && threadIdx.x == KC_BOT_THREADS - 1) sm[hi - 1] = 0.0;
+  };
+  if (nstrip > 0) {
+    // strip entry: own rows plus one halo row each side (rows -1 .. m0
+    // exist in HBM, ghost rows zero), ghost columns included; level 0 is
+    // the first block: v0 rows at [0, (R+2) S), f rows at [2 (R+2) S, ...)
+    const int S = bp.lv[0].S, R = bp.lv[0].R, a = rank * R;
+    const int y0 = a - 1, y1 = min(a + R, m0);
+    const int w0 = (y0 - a + 1) * S, w1 = (y1 - a + 2) * S;  // loaded storage rows, as an offset range
+    const int fbase = 2 * (R + 2) * S;
+    for (int y = y0 + wid; y <= y1; y += KC_BOT_WARPS) {
+      const double* gfr = bp.gf + kc_idx(bp.gP, y, -1);
+      const double* gvr = bp.gv + kc_idx(bp.gP, y, -1);
+      const int o = (y - a + 1) * S;
+      for (int c = lane; c < S; c += 32) {
+        cp8(sm + fbase + o + c, gfr + c);
+        if (!bp.v_zero) cp8(sm + o + c, gvr + c);
+      }
+    }
+    if (bp.v_zero) zero(0, fbase + w0);
+    else {
+      zero(0, w0);
+      zero(w1, fbase + w0);
+    }
+    zero(fbase + w1, total);
+  } else {
+    zero(0, total);
+  }
+  KC_BOT_MARK(5);
+#pragma unroll
+  for (int k = 0; k < SCHED_PER_THREAD; ++k) {
+    const int i = threadIdx.x + k * KC_BOT_THREADS;
+    if (i < bp.nsched) sched[i] = sreg[k];
+  }
+  KC_BOT_MARK(6);
   if (threadIdx.x < nlev) {
     const int d = threadIdx.x;
-    tab[d] = bp.st[d];
-    const bool strip = d < nstrip;
-    const int m = bot_m(m0, d), S = m + 2, base = bot_off(m0, d, nstrip, cs);
-    const int R = bot_rows(m0, d, nstrip, cs);
-    const int mc = d + 1 < nlev ? bot_m(m0, d + 1) : 1;
-    BotLv L;
-    L.m = m;
-    L.S = S;
-    L.R = R;
-    L.a = strip ? rank * R : 0;
-    L.rows = strip ? min(R, m - L.a) : m;
-    L.vo0 = base + S + 1;
-    L.vo1 = base + (R + 2) * S + S + 1;
-    L.fo = base + 2 * (R + 2) * S + S + 1;
-    L.nitem1 = L.rows * m;
-    L.nitem4 = m * ((L.rows + 3) / 4);
-    L.rb4 = strip ? (L.nitem4 >= KC_BOT_THREADS) : (m >= 31);
-    // coarse rows whose centre fine row 2q+1 lies in this CTA's rows
-    L.crows = strip ? min(mc, (L.a + L.rows) / 2) - L.a / 2 : mc;
-    L.inv = 1.0f / (float)m;
-    L.invc = 1.0f / (float)mc;
-    L.invn = 1.0f / (float)(mc + 1);
-    L.padf = 0.f;
+    tab[d] = st_d;
+    BotLv L = lv_d;
+    if (d < nstrip) {  // this rank's rows of the strip level
+      L.a = rank * L.R;
+      L.rows = min(L.R, L.m - L.a);
+      L.nitem1 = L.rows * L.m;
+      L.nitem4 = L.m * ((L.rows + 3) / 4);
+      L.rb4 = L.nitem4 >= KC_BOT_THREADS;
+      // coarse rows whose centre fine row 2q+1 lies in this CTA's rows
+      L.crows = min(L.mc, (L.a + L.rows) / 2) - L.a / 2;
+    }
     lv[d] = L;
   }
-  __syncthreads();
-  if (nstrip > 0) {  // strip entry: own rows plus one halo row each side, ghost columns included
-    const BotLv L = lv[0];
-    const int S = L.S;
-    double* v = sm + L.vo0 - 1;  // row 0, column -1
-    double* f = sm + L.fo - 1;
-    const int y0 = L.a - 1, y1 = min(L.a + L.R, m0);  // rows -1 .. m0 exist in HBM (ghost rows zero)
-    const int n = (y1 - y0 + 1) * S;
-    for (int i = threadIdx.x; i < n; i += KC_BOT_THREADS) {
-      const int r = i / S, c = i - r * S;
-      const int y = y0 + r;
-      const size_t gi = kc_idx(bp.gP, y, c - 1);
-      f[(y - L.a) * S + c] = bp.gf[gi];
-      if (!bp.v_zero) v[(y - L.a) * S + c] = bp.gv[gi];
-    }
+  if (nstrip > 0) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    KC_BOT_MARK(1);
     clu_sync();  // every CTA initialised before any halo push lands
   } else {
+    __syncthreads();
+    KC_BOT_MARK(1);
     const int S = m0 + 2;
     double* v = sm + S + 1;
     double* f = sm + 2 * S * S + S + 1;
-    for (int i = threadIdx.x; i < m0 * m0; i += KC_BOT_THREADS) {
-      const int y = i / m0, x = i - y * m0;
-      const size_t gi = kc_idx(bp.gP, y, x);
-      f[y * S + x] = bp.gf[gi];
-      if (!bp.v_zero) v[y * S + x] = bp.gv[gi];
+    for (int y = wid; y < m0; y += KC_BOT_WARPS) {
+      const double* gfr = bp.gf + kc_idx(bp.gP, y, 0);
+      const double* gvr = bp.gv + kc_idx(bp.gP, y, 0);
+      for (int x = lane; x < m0; x += 32) {
+        cp8(f + y * S + x, gfr + x);
+        if (!bp.v_zero) cp8(v + y * S + x, gvr + x);
+      }
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
   }
 
+  KC_BOT_MARK(2);
   const int warp = threadIdx.x >> 5;
   const int tid = threadIdx.x;
 #ifdef KC_BOT_TRACE
@@ -655,14 +742,15 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
     else bot_sync(g);
   }
   __syncthreads();
+  KC_BOT_MARK(3);
   {
     const BotLv L = lv[0];
     const int S = L.S;
     const double* v = sm + (bp.final_cur ? L.vo1 : L.vo0);
-    const int n = L.rows * m0;
-    for (int i = threadIdx.x; i < n; i += KC_BOT_THREADS) {
-      const int y = i / m0, x = i - y * m0;
-      bp.gv[kc_idx(bp.gP, L.a + y, x)] = v[y * S + x];
+    for (int y = threadIdx.x >> 5; y < L.rows; y += KC_BOT_WARPS) {
+      double* g = bp.gv + kc_idx(bp.gP, L.a + y, 0);
+      for (int x = threadIdx.x & 31; x < m0; x += 32) g[x] = v[y * S + x];
     }
   }
+  KC_BOT_MARK(4);
 }

@@ -1235,6 +1235,7 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
     for (int j = 0; j < bp.nlev; ++j) bp.st[j] = h->L[lb + j].st;
     h->bot_m0 = h->L[lb].m;
     h->bot_cs = cs;
+    bot_geometry(bp, h->bot_m0, cs);
     h->bot_smem = smem;
     if (cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->bot_smem) != cudaSuccess) {
       h->err = "cudaFuncSetAttribute(k_bottom) failed";

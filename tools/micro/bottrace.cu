@@ -32,7 +32,7 @@ int main(int argc, char** argv) {
   unsigned* ds; cudaMalloc(&ds, b.out.size() * 4);
   cudaMemcpy(ds, b.out.data(), b.out.size() * 4, cudaMemcpyHostToDevice);
   bp.gv = gv; bp.gf = gf; bp.gP = P; bp.v_zero = 1; bp.sched = ds; bp.nsched = (int)b.out.size(); bp.final_cur = b.cur & 1;
-  bp.nu1 = 2; bp.nu2 = 2; bp.nstrip = nstrip;
+  bp.nu1 = 2; bp.nu2 = 2; bp.nstrip = nstrip; bot_geometry(bp, m0, cs);
   size_t smem = sizeof(double) * bot_smem_doubles(m0, nlev, nstrip, cs);
   cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_bottom, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -54,6 +54,28 @@ int main(int argc, char** argv) {
     cudaError_t err = cudaDeviceSynchronize();
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     if (rep == 1) printf("kappa=%d+%d: %.1f us, %zu phases %s\n", kappa, kappa - 1, ms * 1e3, b.out.size(), cudaGetErrorString(err));
+  }
+  {
+    unsigned long long st[8];
+    cudaMemcpyFromSymbol(st, kc_bot_stamp, sizeof(st));
+    printf("  CTA-0 timeline (us): init %.2f, entry load %.2f, phases %.2f, write-back %.2f; kernel body %.2f\n",
+           (st[1] - st[0]) * 1e-3, (st[2] - st[1]) * 1e-3, (st[3] - st[2]) * 1e-3, (st[4] - st[3]) * 1e-3,
+           (st[4] - st[0]) * 1e-3);
+    printf("  init: zero %.2f, sched %.2f, setup %.2f\n", (st[5] - st[0]) * 1e-3, (st[6] - st[5]) * 1e-3, (st[1] - st[6]) * 1e-3);
+    // in-graph: 20 back-to-back launches
+    cudaStream_t s; cudaStreamCreate(&s);
+    cudaGraph_t g; cudaGraphExec_t ge;
+    cfg.stream = s;
+    cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal);
+    for (int i = 0; i < 20; ++i) cudaLaunchKernelEx(&cfg, k_bottom, bp, m0);
+    cudaStreamEndCapture(s, &g);
+    cudaGraphInstantiate(&ge, g, 0);
+    cudaGraphLaunch(ge, s); cudaStreamSynchronize(s);
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    cudaEventRecord(a, s); cudaGraphLaunch(ge, s); cudaEventRecord(b, s); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    printf("  in-graph: %.2f us per launch\n", ms * 1e3 / 20);
+    cfg.stream = 0;
   }
   int n; cudaMemcpyFromSymbol(&n, kc_bot_trace_n, sizeof(int));
   std::vector<long long> t(n); std::vector<int> op(n);
