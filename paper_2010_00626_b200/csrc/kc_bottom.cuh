@@ -137,7 +137,9 @@ inline void bot_geometry(BotParams& bp, int m0, int cs) {
     L.fo = base + 2 * (R + 2) * S + S + 1;
     L.nitem1 = L.rows * m;
     L.nitem4 = m * ((L.rows + 3) / 4);
-    L.rb4 = strip ? (L.nitem4 >= KC_BOT_THREADS) : (m >= 31);
+    // RB = 4 where a thread would otherwise run more than one item: a full
+    // 4-row item is four independent chains, little longer than one
+    L.rb4 = strip ? (L.nitem1 > KC_BOT_THREADS) : (m >= 31);
     L.crows = strip ? ((mc < L.rows / 2) ? mc : L.rows / 2) : mc;
     L.inv = 1.0f / (float)m;
     L.invc = 1.0f / (float)mc;
@@ -335,6 +337,26 @@ __device__ __forceinline__ void bot_stencil(bool jac, bool zero, const double* _
       continue;
     }
     const double* pu = u + y0 * S + x;
+    if (RB > 1 && y0 + RB <= rows) {
+      // full item: every load first, then RB independent chains (the
+      // guarded loop below keeps the compiler from overlapping its rows)
+      double w[RB + 2][3], fv[RB], out[RB];
+#pragma unroll
+      for (int k = 0; k < RB + 2; ++k)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) w[k][dx] = pu[(k - 1) * S + dx - 1];
+#pragma unroll
+      for (int k = 0; k < RB; ++k) fv[k] = f[(y0 + k) * S + x];
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        const double au = kc_sum9(st, w[k][0], w[k][1], w[k][2], w[k + 1][0], w[k + 1][1], w[k + 1][2],
+                                  w[k + 2][0], w[k + 2][1], w[k + 2][2]);
+        out[k] = jac ? kc_jacobi_pt(w[k + 1][1], fv[k], au, st.c) : DSUB(fv[k], au);
+      }
+#pragma unroll
+      for (int k = 0; k < RB; ++k) ps.put(o, S, y0 + k, x, out[k]);
+      continue;
+    }
     double a0 = pu[-S - 1], a1 = pu[-S], a2 = pu[-S + 1];
     double b0 = pu[-1], b1 = pu[0], b2 = pu[1];
 #pragma unroll
@@ -353,19 +375,48 @@ __device__ __forceinline__ void bot_stencil(bool jac, bool zero, const double* _
 }
 
 // u2 = J(J(0)) into u, with u1 = 0 + c f recomputed at the neighbours (PH_J2Z)
+__device__ __forceinline__ double bot_j2z_pt(const double* __restrict__ pf, int S, const St9& st) {
+  double n1[9];
+#pragma unroll
+  for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+    for (int dx = 0; dx < 3; ++dx) n1[dy * 3 + dx] = kc_jacobi_zero(pf[(dy - 1) * S + (dx - 1)], st.c);
+  const double au = kc_sum9(st, n1[0], n1[1], n1[2], n1[3], n1[4], n1[5], n1[6], n1[7], n1[8]);
+  return kc_jacobi_pt(n1[4], pf[0], au, st.c);
+}
 __device__ __forceinline__ void bot_j2z(double* __restrict__ u, const double* __restrict__ f, const BotLv& L,
                                         const St9& st, int tid, int nth, const BotPush& ps) {
   const int m = L.m, S = L.S;
-  for (int i = tid; i < L.nitem1; i += nth) {
-    const int y = bot_div(i, L.inv), x = i - y * m;
-    const double* pf = f + y * S + x;
-    double n1[9];
+  if (!L.rb4) {
+    for (int i = tid; i < L.nitem1; i += nth) {
+      const int y = bot_div(i, L.inv), x = i - y * m;
+      ps.put(u, S, y, x, bot_j2z_pt(f + y * S + x, S, st));
+    }
+    return;
+  }
+  // 2-row items (several items per thread): the u1 = 0 + c f values of rows
+  // y0-1 .. y0+2 are shared by both outputs (the same rounded product
+  // wherever used), and the two chains run side by side
+  const int n2 = m * ((L.rows + 1) >> 1);
+  for (int it = tid; it < n2; it += nth) {
+    const int rb = bot_div(it, L.inv), x = it - rb * m, y0 = 2 * rb;
+    const double* pf = f + y0 * S + x;
+    if (y0 + 2 <= L.rows) {
+      double n1[4][3];
 #pragma unroll
-    for (int dy = 0; dy < 3; ++dy)
+      for (int k = 0; k < 4; ++k)
 #pragma unroll
-      for (int dx = 0; dx < 3; ++dx) n1[dy * 3 + dx] = kc_jacobi_zero(pf[(dy - 1) * S + (dx - 1)], st.c);
-    const double au = kc_sum9(st, n1[0], n1[1], n1[2], n1[3], n1[4], n1[5], n1[6], n1[7], n1[8]);
-    ps.put(u, S, y, x, kc_jacobi_pt(n1[4], pf[0], au, st.c));
+        for (int dx = 0; dx < 3; ++dx) n1[k][dx] = kc_jacobi_zero(pf[(k - 1) * S + dx - 1], st.c);
+      const double a0 = kc_sum9(st, n1[0][0], n1[0][1], n1[0][2], n1[1][0], n1[1][1], n1[1][2], n1[2][0], n1[2][1],
+                                n1[2][2]);
+      const double a1 = kc_sum9(st, n1[1][0], n1[1][1], n1[1][2], n1[2][0], n1[2][1], n1[2][2], n1[3][0], n1[3][1],
+                                n1[3][2]);
+      const double o0 = kc_jacobi_pt(n1[1][1], pf[0], a0, st.c), o1 = kc_jacobi_pt(n1[2][1], pf[S], a1, st.c);
+      ps.put(u, S, y0, x, o0);
+      ps.put(u, S, y0 + 1, x, o1);
+    } else {
+      ps.put(u, S, y0, x, bot_j2z_pt(pf, S, st));
+    }
   }
 }
 
@@ -631,7 +682,7 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
       L.rows = min(L.R, L.m - L.a);
       L.nitem1 = L.rows * L.m;
       L.nitem4 = L.m * ((L.rows + 3) / 4);
-      L.rb4 = L.nitem4 >= KC_BOT_THREADS;
+      L.rb4 = L.nitem1 > KC_BOT_THREADS;
       // coarse rows whose centre fine row 2q+1 lies in this CTA's rows
       L.crows = min(L.mc, (L.a + L.rows) / 2) - L.a / 2;
     }
