@@ -703,11 +703,48 @@ int ex_tile(kc_handle* h, int l, bool pre) {
   return KC_OK;
 }
 
+// the same pre pass on column tiles (k_ctile_pre, nu1 <= 2)
+#ifndef KC_CTILE_MAX_M
+#define KC_CTILE_MAX_M 1023  // measured faster than the streaming pass up to here (tools/micro/midlev.cu)
+#endif
+#define KC_CTILE_TY 32
+int ex_ctile_pre(kc_handle* h, int l) {
+  Level& L = h->L[l];
+  Level& C = h->L[l + 1];
+  TileParams p{};
+  p.u = L.v[L.cur];
+  p.f = L.f;
+  p.uo = L.v[L.cur ^ 1];
+  p.fc = C.f;
+  p.vc = C.v[C.cur];
+  p.m = L.m;
+  p.P = L.P;
+  p.mc = C.m;
+  p.Pc = C.P;
+  p.s = L.st;
+  p.tiles_x = (L.m + KC_CT_TX - 1) / KC_CT_TX;
+  const int tiles = p.tiles_x * ((L.m + KC_CTILE_TY - 1) / KC_CTILE_TY);
+  const int nu = h->nu1;
+  const bool z = L.vzero;
+  auto fn = nu == 0 ? (z ? k_ctile_pre<0, true, KC_CTILE_TY> : k_ctile_pre<0, false, KC_CTILE_TY>)
+          : nu == 1 ? (z ? k_ctile_pre<1, true, KC_CTILE_TY> : k_ctile_pre<1, false, KC_CTILE_TY>)
+                    : (z ? k_ctile_pre<2, true, KC_CTILE_TY> : k_ctile_pre<2, false, KC_CTILE_TY>);
+  fn<<<tiles, KC_CT_NW * 32, 0, h->stream>>>(p);
+  KC_LAUNCH_CHECK(h);
+  ++h->launches;
+  if (nu > 0) {
+    L.cur ^= 1;
+    L.vzero = false;
+  }
+  return KC_OK;
+}
+
 // relax(nu1) + restrict_residual (cycle.py:211-213) in one pass; with norms
 // also ||v||, ||f - A v|| of the input v into d_scal[0], d_scal[1]
 int ex_pre(kc_handle* h, int l, bool norms = false) {
   Level& L = h->L[l];
   if (norms && L.vzero) KC_FAIL(h, KC_EINVAL, "fused input norms need a materialized level");
+  if (L.m <= KC_CTILE_MAX_M && h->tile && !norms && h->nu1 <= 2) return ex_ctile_pre(h, l);
   if (L.m <= KC_TILE_MAX_M && h->tile && !norms) return ex_tile(h, l, true);
   int nw = 0;
   KsFn fn = ks_pre_fn(h->nu1, L.vzero, norms);

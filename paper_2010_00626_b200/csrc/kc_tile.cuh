@@ -176,3 +176,115 @@ __global__ void __launch_bounds__(KT_THREADS) k_tile_post(const TileParams p) {
     if (y < m && x < m) p.uo[kc_idx(P, y, x)] = o[(ry + D) * G::W + (rx + D)];
   }
 }
+
+// ---------------------------------------------------------------------------
+// Column tiles (k_ctile_pre): the same pass with one lane per region column
+// and each warp owning a block of RB rows, so every stage is RB independent
+// chains per thread with 3 shared-memory loads per row and no index
+// division.  Region W = TX + 1 + 2D <= 32 columns (TX = 24 owned at D = 3),
+// H = TY + 1 + 2D rows; rows and columns outside the interior are +0.0 at
+// every stage (Dirichlet), as in k_tile_pre.
+// ---------------------------------------------------------------------------
+#define KC_CT_TX 24
+#define KC_CT_NW 8
+__device__ __forceinline__ void kt_cp8(double* smem, const double* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+template <int NU, bool ZERO, int TY, int NW = KC_CT_NW>
+__global__ void __launch_bounds__(NW * 32) k_ctile_pre(const TileParams p) {
+  constexpr int D = NU + 1;
+  constexpr int TX = KC_CT_TX;
+  constexpr int W = TX + 1 + 2 * D;
+  constexpr int H = TY + 1 + 2 * D;
+  constexpr int RB = (H - 2 + NW - 1) / NW;  // rows per warp (stage 1)
+  static_assert(W <= 32, "one lane per region column");
+  __shared__ double su[2][H][32];
+  __shared__ double sf[H][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tx = blockIdx.x % p.tiles_x, ty = blockIdx.x / p.tiles_x;
+  const int y0 = ty * TY, x0 = tx * TX;
+  const int m = p.m, P = p.P;
+  const St9 s = p.s;
+  const int gx = x0 - D + lane;  // global column of this lane
+  const bool xin = gx >= 0 && gx < m;
+  // load f (and u) of the region: lane = column, rows strided over warps;
+  // coordinates outside [-1, m] read the all-zero ghost ring
+  {
+    const int cx = min(max(gx, -1), m);
+    for (int r = w; r < H; r += NW) {
+      const int cy = min(max(y0 - D + r, -1), m);
+      if (lane < W) {
+        const size_t gi = kc_idx(P, cy, cx);
+        kt_cp8(&sf[r][lane], p.f + gi);
+        if (!ZERO) kt_cp8(&su[0][r][lane], p.u + gi);
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+  __syncthreads();
+#pragma unroll
+  for (int t = 1; t <= D; ++t) {
+    const double(*src)[32] = su[(t - 1) & 1];
+    double(*dst)[32] = su[t & 1];
+    const bool lane_on = lane >= t && lane < W - t;
+    const int r0 = t + w * RB, r1 = min(r0 + RB, H - t);
+    if (lane_on && r0 < r1) {
+      double out[RB];
+      if (ZERO && t == 1) {
+#pragma unroll
+        for (int k = 0; k < RB; ++k)
+          if (r0 + k < r1) out[k] = NU > 0 ? kc_jacobi_zero(sf[r0 + k][lane], s.c) : sf[r0 + k][lane];
+      } else if (r1 - r0 == RB) {  // full block: every load first, RB independent chains
+        double v[RB + 2][3], fv[RB];
+#pragma unroll
+        for (int k = 0; k < RB + 2; ++k)
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx) v[k][dx] = src[r0 - 1 + k][lane - 1 + dx];
+#pragma unroll
+        for (int k = 0; k < RB; ++k) fv[k] = sf[r0 + k][lane];
+#pragma unroll
+        for (int k = 0; k < RB; ++k) {
+          const double au = kc_sum9(s, v[k][0], v[k][1], v[k][2], v[k + 1][0], v[k + 1][1], v[k + 1][2], v[k + 2][0],
+                                    v[k + 2][1], v[k + 2][2]);
+          out[k] = t <= NU ? kc_jacobi_pt(v[k + 1][1], fv[k], au, s.c) : DSUB(fv[k], au);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < RB; ++k)
+          if (r0 + k < r1) {
+            const int r = r0 + k;
+            const double au = kc_sum9(s, src[r - 1][lane - 1], src[r - 1][lane], src[r - 1][lane + 1], src[r][lane - 1],
+                                      src[r][lane], src[r][lane + 1], src[r + 1][lane - 1], src[r + 1][lane],
+                                      src[r + 1][lane + 1]);
+            out[k] = t <= NU ? kc_jacobi_pt(src[r][lane], sf[r][lane], au, s.c) : DSUB(sf[r][lane], au);
+          }
+      }
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        const int r = r0 + k;
+        if (r < r1) {
+          const int gy = y0 - D + r;
+          const double v = (xin && gy >= 0 && gy < m) ? out[k] : 0.0;
+          dst[r][lane] = v;
+          // v after NU sweeps: owned points straight to HBM
+          if (t == NU && r >= D && r < D + TY && lane >= D && lane < D + TX && xin && gy >= 0 && gy < m)
+            p.uo[kc_idx(P, gy, gx)] = v;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // full weighting of the residual rows y0 .. y0+TY, columns x0 .. x0+TX
+  const double(*r)[32] = su[D & 1];
+  for (int i = threadIdx.x; i < (TY / 2) * (TX / 2); i += NW * 32) {
+    const int qy = i / (TX / 2), qx = i - qy * (TX / 2);
+    const int q = y0 / 2 + qy, pc = x0 / 2 + qx;
+    if (q < p.mc && pc < p.mc) {
+      const int cy = D + 2 * qy + 1, cx = D + 2 * qx + 1;
+      p.fc[kc_idx(p.Pc, q, pc)] = kc_fw(r[cy - 1][cx - 1], r[cy - 1][cx], r[cy - 1][cx + 1], r[cy][cx - 1], r[cy][cx],
+                                        r[cy][cx + 1], r[cy + 1][cx - 1], r[cy + 1][cx], r[cy + 1][cx + 1]);
+    }
+  }
+}

@@ -4,6 +4,7 @@
 // variant is captured N times back to back into one graph; us per pass.
 //   ./midlev [nu]
 #include <algorithm>
+#include <cstring>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -66,6 +67,29 @@ int main(int argc, char** argv) {
     cudaFuncSetAttribute(k_tile_pre<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smp);
     cudaFuncSetAttribute(k_tile_post<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smq);
     const double t_tpre = time_graph([&] { k_tile_pre<2, false><<<tiles, KT_THREADS, smp, s>>>(tp); });
+    // column tiles: bit-exact against k_tile_pre, then timed
+    auto ctile = [&](auto kern, int ty, const char* name, int nwarp = KC_CT_NW) {
+      TileParams cp = tp;
+      cp.tiles_x = (m + KC_CT_TX - 1) / KC_CT_TX;
+      const int nt = cp.tiles_x * ((m + ty - 1) / ty);
+      std::vector<double> a(el), b(el), ac(elc), bc(elc);
+      CK(cudaMemset(uo, 0, el * 8)); CK(cudaMemset(fc, 0, elc * 8));
+      k_tile_pre<2, false><<<tiles, KT_THREADS, smp, s>>>(tp);
+      CK(cudaStreamSynchronize(s));
+      CK(cudaMemcpy(a.data(), uo, el * 8, cudaMemcpyDeviceToHost)); CK(cudaMemcpy(ac.data(), fc, elc * 8, cudaMemcpyDeviceToHost));
+      CK(cudaMemset(uo, 0, el * 8)); CK(cudaMemset(fc, 0, elc * 8));
+      kern<<<nt, nwarp * 32, 0, s>>>(cp);
+      CK(cudaStreamSynchronize(s));
+      CK(cudaMemcpy(b.data(), uo, el * 8, cudaMemcpyDeviceToHost)); CK(cudaMemcpy(bc.data(), fc, elc * 8, cudaMemcpyDeviceToHost));
+      const bool same = memcmp(a.data(), b.data(), el * 8) == 0 && memcmp(ac.data(), bc.data(), elc * 8) == 0;
+      const double t = time_graph([&] { kern<<<nt, nwarp * 32, 0, s>>>(cp); });
+      printf("   m=%4d ctile pre %s: %6.2f us (%d blocks) %s\n", m, name, t, nt, same ? "bit-exact" : "MISMATCH");
+    };
+    ctile(k_ctile_pre<2, false, 16>, 16, "TY=16");
+    ctile(k_ctile_pre<2, false, 32>, 32, "TY=32");
+    ctile(k_ctile_pre<2, false, 48>, 48, "TY=48");
+    ctile(k_ctile_pre<2, false, 32, 16>, 32, "TY=32 16w", 16);
+    ctile(k_ctile_pre<2, false, 16, 4>, 16, "TY=16 4w", 4);
     const double t_tpost = time_graph([&] { k_tile_post<2, false><<<tiles, KT_THREADS, smq, s>>>(tp); });
     // streaming (kc_engine.cu ks_params / ks_choose_nq)
     auto sparams = [&](int D, const void* fn, int* nw) {
