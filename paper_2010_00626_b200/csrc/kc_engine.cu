@@ -739,6 +739,45 @@ int ex_ctile_pre(kc_handle* h, int l) {
   return KC_OK;
 }
 
+// prolong_add + relax(nu2) on column tiles (k_ctile_post, nu2 <= 4)
+#ifndef KC_CTILE_POST_MAX_M
+#define KC_CTILE_POST_MAX_M 511  // faster than the streaming post pass up to here (tools/micro/midlev.cu)
+#endif
+#define KC_CTILE_POST_TY 16
+int ex_ctile_post(kc_handle* h, int l) {
+  Level& L = h->L[l];
+  Level& C = h->L[l + 1];
+  TileParams p{};
+  p.u = L.v[L.cur];
+  p.f = L.f;
+  p.uo = L.v[L.cur ^ 1];
+  p.vc = C.v[C.cur];
+  p.m = L.m;
+  p.P = L.P;
+  p.mc = C.m;
+  p.Pc = C.P;
+  p.s = L.st;
+  p.tiles_x = (L.m + KC_CT_TX - 1) / KC_CT_TX;
+  const int tiles = p.tiles_x * ((L.m + KC_CTILE_POST_TY - 1) / KC_CTILE_POST_TY);
+  const bool z = L.vzero;
+#define KCT_POST(N) (z ? k_ctile_post<N, true, KC_CTILE_POST_TY> : k_ctile_post<N, false, KC_CTILE_POST_TY>)
+  void (*fn)(TileParams) = nullptr;
+  switch (h->nu2) {
+    case 0: fn = KCT_POST(0); break;
+    case 1: fn = KCT_POST(1); break;
+    case 2: fn = KCT_POST(2); break;
+    case 3: fn = KCT_POST(3); break;
+    default: fn = KCT_POST(4); break;
+  }
+#undef KCT_POST
+  fn<<<tiles, KC_CT_NW * 32, 0, h->stream>>>(p);
+  KC_LAUNCH_CHECK(h);
+  ++h->launches;
+  L.cur ^= 1;
+  L.vzero = false;
+  return KC_OK;
+}
+
 // relax(nu1) + restrict_residual (cycle.py:211-213) in one pass; with norms
 // also ||v||, ||f - A v|| of the input v into d_scal[0], d_scal[1]
 int ex_pre(kc_handle* h, int l, bool norms = false) {
@@ -779,6 +818,7 @@ int ex_post(kc_handle* h, int l, int nm) {
   int rc = ex_materialize(h, l + 1);
   if (rc) return rc;
   if (nm == 2 && h->nu2 < 1) KC_FAIL(h, KC_EINVAL, "fused r.z needs nu2 >= 1");
+  if (L.m <= KC_CTILE_POST_MAX_M && h->tile && !nm && h->nu2 <= 4) return ex_ctile_post(h, l);
   if (L.m <= KC_TILE_POST_MAX_M && h->tile && !nm) return ex_tile(h, l, false);
   int nw = 0;
   const int D = h->nu2 + (nm == 1 ? 1 : 0);

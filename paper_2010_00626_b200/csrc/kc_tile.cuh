@@ -288,3 +288,110 @@ __global__ void __launch_bounds__(NW * 32) k_ctile_pre(const TileParams p) {
     }
   }
 }
+
+// v + P vc, then NU sweeps, on column tiles (region W = TX + 2 NU <= 32
+// columns, H = TY + 2 NU rows; the coarse patch under it in shared memory)
+template <int NU, bool VZ, int TY, int NW = KC_CT_NW>
+__global__ void __launch_bounds__(NW * 32) k_ctile_post(const TileParams p) {
+  constexpr int D = NU;
+  constexpr int TX = KC_CT_TX;
+  constexpr int W = TX + 2 * D;
+  constexpr int H = TY + 2 * D;
+  constexpr int RB = (H - 2 > 0 ? H - 2 + NW - 1 : NW) / NW;  // rows per warp in a sweep
+  constexpr int R0 = (H + NW - 1) / NW;                       // rows per warp in the prolongation
+  constexpr int CH = TY / 2 + D + 3;                          // coarse patch rows
+  static_assert(W <= 32, "one lane per region column");
+  __shared__ double su[2][H][32];
+  __shared__ double sf[H][32];
+  __shared__ double sc[CH][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tx = blockIdx.x % p.tiles_x, ty = blockIdx.x / p.tiles_x;
+  const int y0 = ty * TY, x0 = tx * TX;
+  const int m = p.m, P = p.P;
+  const St9 s = p.s;
+  const int gx = x0 - D + lane;
+  const bool xin = gx >= 0 && gx < m;
+  const int qy0 = ((y0 - D) >> 1) - 1, qx0 = ((x0 - D) >> 1) - 1;  // coarse patch origin
+  {
+    const int cx = min(max(gx, -1), m);
+    for (int r = w; r < H; r += NW) {
+      const int cy = min(max(y0 - D + r, -1), m);
+      if (lane < W) {
+        const size_t gi = kc_idx(P, cy, cx);
+        kt_cp8(&sf[r][lane], p.f + gi);
+        if (!VZ) kt_cp8(&su[1][r][lane], p.u + gi);
+      }
+    }
+    const int qx = min(max(qx0 + lane, -1), p.mc);
+    for (int r = w; r < CH; r += NW) {
+      const int qy = min(max(qy0 + r, -1), p.mc);
+      kt_cp8(&sc[r][lane], p.vc + kc_idx(p.Pc, qy, qx));
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+  __syncthreads();
+  // stage 0: v + P vc on the region (transfer.py:50-58, cycle.py:174-176)
+  if (lane < W) {
+    auto cp = [&](int q, int pc) { return sc[q - qy0][pc - qx0]; };
+#pragma unroll
+    for (int k = 0; k < R0; ++k) {
+      const int r = w * R0 + k;
+      if (r < H) {
+        const int gy = y0 - D + r;
+        double v = 0.0;
+        if (xin && gy >= 0 && gy < m) v = DADD(VZ ? 0.0 : su[1][r][lane], kc_prolong_val(gy, gx, cp));
+        su[0][r][lane] = v;
+        if (NU == 0 && r >= D && r < D + TY && lane >= D && lane < D + TX && xin && gy >= 0 && gy < m)
+          p.uo[kc_idx(P, gy, gx)] = v;
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int t = 1; t <= NU; ++t) {
+    const double(*src)[32] = su[(t - 1) & 1];
+    double(*dst)[32] = su[t & 1];
+    const bool lane_on = lane >= t && lane < W - t;
+    const int r0 = t + w * RB, r1 = min(r0 + RB, H - t);
+    if (lane_on && r0 < r1) {
+      double out[RB];
+      if (r1 - r0 == RB) {
+        double v[RB + 2][3], fv[RB];
+#pragma unroll
+        for (int k = 0; k < RB + 2; ++k)
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx) v[k][dx] = src[r0 - 1 + k][lane - 1 + dx];
+#pragma unroll
+        for (int k = 0; k < RB; ++k) fv[k] = sf[r0 + k][lane];
+#pragma unroll
+        for (int k = 0; k < RB; ++k) {
+          const double au = kc_sum9(s, v[k][0], v[k][1], v[k][2], v[k + 1][0], v[k + 1][1], v[k + 1][2], v[k + 2][0],
+                                    v[k + 2][1], v[k + 2][2]);
+          out[k] = kc_jacobi_pt(v[k + 1][1], fv[k], au, s.c);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < RB; ++k)
+          if (r0 + k < r1) {
+            const int r = r0 + k;
+            const double au = kc_sum9(s, src[r - 1][lane - 1], src[r - 1][lane], src[r - 1][lane + 1], src[r][lane - 1],
+                                      src[r][lane], src[r][lane + 1], src[r + 1][lane - 1], src[r + 1][lane],
+                                      src[r + 1][lane + 1]);
+            out[k] = kc_jacobi_pt(src[r][lane], sf[r][lane], au, s.c);
+          }
+      }
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        const int r = r0 + k;
+        if (r < r1) {
+          const int gy = y0 - D + r;
+          const bool in = xin && gy >= 0 && gy < m;
+          const double v = in ? out[k] : 0.0;
+          if (t < NU) dst[r][lane] = v;
+          else if (in && r >= D && r < D + TY && lane >= D && lane < D + TX) p.uo[kc_idx(P, gy, gx)] = v;
+        }
+      }
+    }
+    if (t < NU) __syncthreads();
+  }
+}

@@ -90,6 +90,26 @@ int main(int argc, char** argv) {
     ctile(k_ctile_pre<2, false, 48>, 48, "TY=48");
     ctile(k_ctile_pre<2, false, 32, 16>, 32, "TY=32 16w", 16);
     ctile(k_ctile_pre<2, false, 16, 4>, 16, "TY=16 4w", 4);
+    {  // column-tile post: bit-exact against k_tile_post, then timed
+      TileParams cp = tp;
+      cp.tiles_x = (m + KC_CT_TX - 1) / KC_CT_TX;
+      for (int ty : {16, 32}) {
+        const int nt = cp.tiles_x * ((m + ty - 1) / ty);
+        std::vector<double> a(el), b(el);
+        CK(cudaMemcpy(uo, h.data(), el * 8, cudaMemcpyHostToDevice));
+        k_tile_post<2, false><<<tiles, KT_THREADS, smq, s>>>(tp);
+        CK(cudaStreamSynchronize(s));
+        CK(cudaMemcpy(a.data(), uo, el * 8, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(uo, h.data(), el * 8, cudaMemcpyHostToDevice));
+        auto kern = ty == 16 ? k_ctile_post<2, false, 16> : k_ctile_post<2, false, 32>;
+        kern<<<nt, KC_CT_NW * 32, 0, s>>>(cp);
+        CK(cudaStreamSynchronize(s));
+        CK(cudaMemcpy(b.data(), uo, el * 8, cudaMemcpyDeviceToHost));
+        const bool same = memcmp(a.data(), b.data(), el * 8) == 0;
+        const double t = time_graph([&] { kern<<<nt, KC_CT_NW * 32, 0, s>>>(cp); });
+        printf("   m=%4d ctile post TY=%d: %6.2f us (%d blocks) %s\n", m, ty, t, nt, same ? "bit-exact" : "MISMATCH");
+      }
+    }
     const double t_tpost = time_graph([&] { k_tile_post<2, false><<<tiles, KT_THREADS, smq, s>>>(tp); });
     // streaming (kc_engine.cu ks_params / ks_choose_nq)
     auto sparams = [&](int D, const void* fn, int* nw) {
