@@ -38,7 +38,8 @@ thread_local std::string g_create_err;
 // k_stop_check inside the conditional WHILE graph of the stand-alone solve:
 // it runs after the level-0 pre kernel has produced the norms of the
 // current iterate v_it (cycle.py:338-353) and decides whether the rest of
-// the cycle (an IF node) and the next iteration run.
+// the cycle and the next iteration run (the WHILE condition; set_rest: also
+// an IF node's).
 struct SolveState {
   double target, prev, reduction;
   int it, max_it, streak, status, stop_mode, pad;
@@ -46,8 +47,8 @@ struct SolveState {
   double* res_hist;
 };
 
-__global__ void k_stop_check(cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_rest, SolveState* st,
-                             const double* __restrict__ scal) {
+__global__ void k_stop_check(cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_rest, int set_rest,
+                             SolveState* st, const double* __restrict__ scal) {
   if (threadIdx.x != 0) return;
   const int it = st->it;  // cycles completed
   const double e = scal[0], r = scal[1];
@@ -71,7 +72,7 @@ __global__ void k_stop_check(cudaGraphConditionalHandle h_loop, cudaGraphConditi
   if (go && it >= st->max_it) go = 0u;  // status stays MAX_CYCLES
   if (go) st->it = it + 1;
   cudaGraphSetConditional(h_loop, go);
-  cudaGraphSetConditional(h_rest, go);
+  if (set_rest) cudaGraphSetConditional(h_rest, go);
 }
 
 struct Level {
@@ -112,7 +113,7 @@ struct GraphEntry {
 };
 
 // the whole stand-alone loop in one graph:
-//   WHILE { pre (level 0, input norms) ; k_stop_check ; IF { rest of the cycle } }
+//   pre (level 0, input norms) ; k_stop_check ; WHILE(go) { rest of the cycle ; pre ; k_stop_check }
 struct SolveGraph {
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr, pre = nullptr, rest = nullptr;
@@ -1066,37 +1067,36 @@ int get_solve_graph(kc_handle* h, int kappa, SolveGraph** out) {
   }
   if (rc) return rc;
   if (!h->d_solve) KC_CUDA(h, cudaMalloc(&h->d_solve, sizeof(SolveState)));
+  // pre ; check ; WHILE(go) { rest ; pre ; check } -- the same sequence as
+  // WHILE { pre ; check ; IF(go) { rest } } without a conditional node per cycle
   cudaGraph_t cg = nullptr;
   KC_CUDA(h, cudaGraphCreate(&cg, 0));
-  cudaGraphConditionalHandle h_loop, h_rest;
+  cudaGraphConditionalHandle h_loop;
   KC_CUDA(h, cudaGraphConditionalHandleCreate(&h_loop, cg, 1, cudaGraphCondAssignDefault));
-  cudaGraphNodeParams wp{};
-  wp.type = cudaGraphNodeTypeConditional;
-  wp.conditional.handle = h_loop;
-  wp.conditional.type = cudaGraphCondTypeWhile;
-  wp.conditional.size = 1;
-  cudaGraphNode_t wn;
-  KC_CUDA(h, cudaGraphAddNode(&wn, cg, nullptr, 0, &wp));
-  cudaGraph_t body = wp.conditional.phGraph_out[0];
-  KC_CUDA(h, cudaGraphConditionalHandleCreate(&h_rest, body, 0, cudaGraphCondAssignDefault));
-  cudaGraphNode_t pre_node, chk_node, if_node, rest_node;
-  KC_CUDA(h, cudaGraphAddChildGraphNode(&pre_node, body, nullptr, 0, sg.pre));
   SolveState* st = h->d_solve;
   const double* scal = h->d_scal;
-  void* args[] = {&h_loop, &h_rest, &st, &scal};
+  cudaGraphConditionalHandle h_none = h_loop;
+  int set_rest = 0;
+  void* args[] = {&h_loop, &h_none, &set_rest, &st, &scal};
   cudaKernelNodeParams kp{};
   kp.func = (void*)k_stop_check;
   kp.gridDim = dim3(1);
   kp.blockDim = dim3(32);
   kp.kernelParams = args;
+  cudaGraphNode_t pre0, chk0, wn;
+  KC_CUDA(h, cudaGraphAddChildGraphNode(&pre0, cg, nullptr, 0, sg.pre));
+  KC_CUDA(h, cudaGraphAddKernelNode(&chk0, cg, &pre0, 1, &kp));
+  cudaGraphNodeParams wp{};
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = h_loop;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  KC_CUDA(h, cudaGraphAddNode(&wn, cg, &chk0, 1, &wp));
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+  cudaGraphNode_t rest_node, pre_node, chk_node;
+  KC_CUDA(h, cudaGraphAddChildGraphNode(&rest_node, body, nullptr, 0, sg.rest));
+  KC_CUDA(h, cudaGraphAddChildGraphNode(&pre_node, body, &rest_node, 1, sg.pre));
   KC_CUDA(h, cudaGraphAddKernelNode(&chk_node, body, &pre_node, 1, &kp));
-  cudaGraphNodeParams ip{};
-  ip.type = cudaGraphNodeTypeConditional;
-  ip.conditional.handle = h_rest;
-  ip.conditional.type = cudaGraphCondTypeIf;
-  ip.conditional.size = 1;
-  KC_CUDA(h, cudaGraphAddNode(&if_node, body, &chk_node, 1, &ip));
-  KC_CUDA(h, cudaGraphAddChildGraphNode(&rest_node, ip.conditional.phGraph_out[0], nullptr, 0, sg.rest));
   KC_CUDA(h, cudaGraphInstantiate(&sg.exec, cg, 0));
   sg.graph = cg;
   auto ins = h->solve_graphs.emplace(key, sg);
