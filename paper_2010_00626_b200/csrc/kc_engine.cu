@@ -1792,9 +1792,9 @@ int pcg_precondition(kc_handle* h, int kappa, kc_precond_fn fn, void* ctx, std::
 
 namespace {
 // The whole PCG loop of krylov.py:100-130 in one graph launch:
-//   WHILE { Ap = A p, pAp ; x += alpha p, r -= alpha Ap, measure ; k_pcg_check ;
-//           IF { z = M r (the cycle graph, r . z fused into its last kernel) ;
-//                p = z + beta p ; rz = rz_next } }
+//   A ; k_pcg_check ; WHILE(go) { z = M r (the cycle graph, r . z fused into
+//   its last kernel) ; p = z + beta p, rz = rz_next ; A ; k_pcg_check }
+// with A = { Ap = A p, pAp ; x += alpha p, r -= alpha Ap, measure }.
 // r lives in L0.f and z in the finest v buffer, as in the host loop.
 int get_pcg_graph(kc_handle* h, int kappa, bool mx, SolveGraph** out) {
   Level& L0 = h->L[0];
@@ -1840,39 +1840,36 @@ int get_pcg_graph(kc_handle* h, int kappa, bool mx, SolveGraph** out) {
   if (ce != cudaSuccess) KC_FAIL(h, KC_ECUDA, "PCG capture: %s", cudaGetErrorString(ce));
   sg.kernels_pre = 4;
   sg.kernels_rest = g->kernels + 2;
+  // A ; check ; WHILE(go) { cycle ; tail ; A ; check } -- the sequence of
+  // WHILE { A ; check ; IF(go) { cycle ; tail } } without the IF node
   cudaGraph_t cg = nullptr;
   KC_CUDA(h, cudaGraphCreate(&cg, 0));
-  cudaGraphConditionalHandle h_loop, h_body;
+  cudaGraphConditionalHandle h_loop;
   KC_CUDA(h, cudaGraphConditionalHandleCreate(&h_loop, cg, 1, cudaGraphCondAssignDefault));
-  cudaGraphNodeParams wp{};
-  wp.type = cudaGraphNodeTypeConditional;
-  wp.conditional.handle = h_loop;
-  wp.conditional.type = cudaGraphCondTypeWhile;
-  wp.conditional.size = 1;
-  cudaGraphNode_t wn;
-  KC_CUDA(h, cudaGraphAddNode(&wn, cg, nullptr, 0, &wp));
-  cudaGraph_t body = wp.conditional.phGraph_out[0];
-  KC_CUDA(h, cudaGraphConditionalHandleCreate(&h_body, body, 0, cudaGraphCondAssignDefault));
-  cudaGraphNode_t a_node, chk_node, if_node, cyc_node, tail_node;
-  KC_CUDA(h, cudaGraphAddChildGraphNode(&a_node, body, nullptr, 0, sg.pre));
   const double* scal = h->d_scal;
-  int s_rz = S_RZ, s_pap = S_PAP, s_meas = S_MEAS;
-  void* args[] = {&h_loop, &h_body, &st, &scal, &s_rz, &s_pap, &s_meas};
+  int s_rz = S_RZ, s_pap = S_PAP, s_meas = S_MEAS, set_body = 0;
+  cudaGraphConditionalHandle h_body = h_loop;
+  void* args[] = {&h_loop, &h_body, &set_body, &st, &scal, &s_rz, &s_pap, &s_meas};
   cudaKernelNodeParams kp{};
   kp.func = (void*)k_pcg_check;
   kp.gridDim = dim3(1);
   kp.blockDim = dim3(32);
   kp.kernelParams = args;
+  cudaGraphNode_t a0, chk0, wn;
+  KC_CUDA(h, cudaGraphAddChildGraphNode(&a0, cg, nullptr, 0, sg.pre));
+  KC_CUDA(h, cudaGraphAddKernelNode(&chk0, cg, &a0, 1, &kp));
+  cudaGraphNodeParams wp{};
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = h_loop;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  KC_CUDA(h, cudaGraphAddNode(&wn, cg, &chk0, 1, &wp));
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+  cudaGraphNode_t cyc_node, tail_node, a_node, chk_node;
+  KC_CUDA(h, cudaGraphAddChildGraphNode(&cyc_node, body, nullptr, 0, g->graph));
+  KC_CUDA(h, cudaGraphAddChildGraphNode(&tail_node, body, &cyc_node, 1, sg.rest));
+  KC_CUDA(h, cudaGraphAddChildGraphNode(&a_node, body, &tail_node, 1, sg.pre));
   KC_CUDA(h, cudaGraphAddKernelNode(&chk_node, body, &a_node, 1, &kp));
-  cudaGraphNodeParams ip{};
-  ip.type = cudaGraphNodeTypeConditional;
-  ip.conditional.handle = h_body;
-  ip.conditional.type = cudaGraphCondTypeIf;
-  ip.conditional.size = 1;
-  KC_CUDA(h, cudaGraphAddNode(&if_node, body, &chk_node, 1, &ip));
-  cudaGraph_t ifb = ip.conditional.phGraph_out[0];
-  KC_CUDA(h, cudaGraphAddChildGraphNode(&cyc_node, ifb, nullptr, 0, g->graph));
-  KC_CUDA(h, cudaGraphAddChildGraphNode(&tail_node, ifb, &cyc_node, 1, sg.rest));
   KC_CUDA(h, cudaGraphInstantiate(&sg.exec, cg, 0));
   sg.graph = cg;
   sg.end_cur0 = cur0;

@@ -120,8 +120,9 @@ __global__ void k_copy_scalar(double* __restrict__ scal, int dst, int src) {
 // Stopping logic of one device PCG iteration (krylov.py:100-130), run after
 // the x/r update: rz (from the previous preconditioning) must be positive,
 // the budget not exhausted, pAp positive; then the measure is recorded and
-// compared with the target.  Sets the loop and body conditions.
-__global__ void k_pcg_check(cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_body,
+// compared with the target.  Sets the loop condition (and the body's when
+// set_body).
+__global__ void k_pcg_check(cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_body, int set_body,
                             PcgState* __restrict__ st, const double* __restrict__ scal, int s_rz, int s_pap,
                             int s_meas) {
   if (threadIdx.x != 0) return;
@@ -147,5 +148,5 @@ __global__ void k_pcg_check(cudaGraphConditionalHandle h_loop, cudaGraphConditio
     }
   }
   cudaGraphSetConditional(h_loop, go);
-  cudaGraphSetConditional(h_body, go);
+  if (set_body) cudaGraphSetConditional(h_body, go);
 }
