@@ -53,6 +53,9 @@
 // the graph's tile kernels.
 #define KC_BOT_MAX_M 63
 #define KC_CLU_MAX_M 255
+#ifndef KC_CLU_ENTRY_M
+#define KC_CLU_ENTRY_M 127  // default entry (kc_engine.cu)
+#endif
 #ifndef KC_CLU_MIN_STRIP
 #define KC_CLU_MIN_STRIP 31
 #endif

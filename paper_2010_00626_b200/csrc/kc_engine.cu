@@ -1255,10 +1255,18 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
     const char* env = getenv("KC_BOT_CLUSTER");
     const bool allow = !(env && env[0] == '0');
     cudaFuncSetAttribute(k_bottom, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    // largest cluster entry side: 127 measured faster than 255 (the 255^2
+    // calls run as column-tile kernels on the whole GPU instead; F-cycle
+    // -3 %); KC_BOT_ENTRY overrides (<= KC_CLU_MAX_M), KC_BOT_CS=8 skips 16
+    const char* eenv = getenv("KC_BOT_ENTRY");
+    const int clu_max = eenv ? std::min(atoi(eenv), KC_CLU_MAX_M) : KC_CLU_ENTRY_M;
+    const char* csenv = getenv("KC_BOT_CS");
+    const int cs_first = csenv && atoi(csenv) == 8 ? 8 : 16;
     for (int csz : {16, 8}) {
+      if (csz > cs_first) continue;
       if (!allow || lb >= 0) break;
       for (int e = 0; e < n && lb < 0; ++e) {
-        if (h->L[e].m > KC_CLU_MAX_M) continue;
+        if (h->L[e].m > clu_max) continue;
         const int m0 = h->L[e].m, nl = n - e;
         int ns = 0;
         while (ns < nl) {

@@ -27,6 +27,9 @@
 #include "kc_common.cuh"
 
 #define KS_BAND 64  // fine columns per warp band (2 per lane)
+#ifndef KS_MINB
+#define KS_MINB 4   // __launch_bounds__ min blocks per SM of the streaming kernels
+#endif
 
 struct StreamParams {
   const double* u;   // input v (current buffer); unused on a zero guess
@@ -130,7 +133,7 @@ __device__ __forceinline__ void ks_mask(double2& v, int y, int mg, bool colx_in,
 // completes its own output one row behind it (ks_step), so stage t emits row
 // yin - t and a chunk needs only D warm-up rows per side.
 template <int NU, bool ZERO, bool NORMS = false, bool STRIP = false>
-__global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
+__global__ void __launch_bounds__(128, KS_MINB) k_pre(const StreamParams p) {
   constexpr int D = NU + 1;
   // row geometry (StreamParams): compile-time whole-level values unless STRIP
   const int g_rows = STRIP ? p.rows : p.m, g_y0 = STRIP ? p.gy0 : 0, g_mg = STRIP ? p.mg : p.m;
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(128, 4) k_pre(const StreamParams p) {
 // per-warp partials); 2: f . v' (the PCG rz = r . z of a preconditioning
 // cycle, whose f is r and whose result is z; per-lane partials, NU >= 1).
 template <int NU, bool VZ, int NM, bool STRIP = false>
-__global__ void __launch_bounds__(128, 4) k_post(const StreamParams p) {
+__global__ void __launch_bounds__(128, KS_MINB) k_post(const StreamParams p) {
   constexpr bool NORMS = NM == 1, DOT = NM == 2;
   const int g_rows = STRIP ? p.rows : p.m, g_y0 = STRIP ? p.gy0 : 0, g_mg = STRIP ? p.mg : p.m;
   const int g_hb = STRIP ? p.hb : 1, g_mcr = STRIP ? p.mcr : p.mc, g_hbc = STRIP ? p.hbc : 1;

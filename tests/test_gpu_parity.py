@@ -487,7 +487,8 @@ def test_fused_matches_per_op_and_oracle(n, nu1, nu2):
 @pytest.mark.parametrize("nu1,nu2", [(2, 2), (1, 1), (0, 2), (3, 0)])
 def test_bottom_cluster_and_single_cta(n, nu1, nu2, monkeypatch):
     """The bottom kernel runs as a 16-CTA cluster (levels >= 31^2 in row
-    strips with DSMEM halos, entry <= 255^2) or, with KC_BOT_CLUSTER=0, as one
+    strips with DSMEM halos, entry <= 127^2 by default, <= 255^2 with
+    KC_BOT_ENTRY=255) or, with KC_BOT_CLUSTER=0, as one
     CTA (entry <= 63^2).  Both must equal the oracle bit-for-bit for every
     kappa, including W (long schedules, many CTA-0 <-> strip transitions)."""
     m = 2 ** n - 1
@@ -502,8 +503,9 @@ def test_bottom_cluster_and_single_cta(n, nu1, nu2, monkeypatch):
         for _ in range(2):
             h.cycle(ke)
             ref.append(h.v[0].copy())
-        for mode in ("1", "0"):
-            monkeypatch.setenv("KC_BOT_CLUSTER", mode)
+        for mode in ("1", "0", "255"):
+            monkeypatch.setenv("KC_BOT_CLUSTER", "0" if mode == "0" else "1")
+            monkeypatch.setenv("KC_BOT_ENTRY", "255" if mode == "255" else "127")
             st = build_state(ProblemSpec(1e-4, 45.0), cfg)
             st.v[0], st.f[0] = v0, f0
             for c in range(2):
