@@ -792,6 +792,9 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
       int cur = src, vz = zero;
       t.frame(d, BD_KAP(e), nlev, cur, vz, tiny_child);
     }
+#ifdef KC_BOT_TRACE
+    if (threadIdx.x == 0 && rank == 0 && tr_n - 1 < KC_BOT_TRACE) kc_bot_trace_end[tr_n - 1] = clock64();
+#endif
     if (strip) clu_sync();
     else bot_sync(g);
   }

@@ -9,7 +9,9 @@
 int main(int argc, char** argv) {
   int kappa = argc > 1 ? atoi(argv[1]) : 3;
   const int cs = argc > 3 ? atoi(argv[3]) : 1;  // cluster size (16: entry 255^2, strips down to 31^2)
-  const int m0 = cs > 1 ? 255 : 63, nlev = cs > 1 ? 8 : 6, P = kc_pitch(m0);
+  const int m0 = argc > 4 ? atoi(argv[4]) : (cs > 1 ? 127 : 63), P = kc_pitch(m0);  // argv[4]: entry side
+  int nlev = 0;
+  while ((1 << nlev) - 1 < m0) ++nlev;
   int nstrip = 0;
   while (cs > 1 && nstrip < nlev && bot_m(m0, nstrip) >= KC_CLU_MIN_STRIP) ++nstrip;
   size_t el = (size_t)(m0 + 2) * P;
@@ -81,11 +83,17 @@ int main(int argc, char** argv) {
   std::vector<long long> t(n); std::vector<int> op(n);
   cudaMemcpyFromSymbol(t.data(), kc_bot_trace, n * 8);
   cudaMemcpyFromSymbol(op.data(), kc_bot_trace_op, n * 4);
-  double sum[16][8] = {}; int cnt[16][8] = {};
-  for (int i = 0; i + 1 < n; ++i) { int o = op[i] / 16, d = op[i] % 16; sum[o][d] += t[i + 1] - t[i]; cnt[o][d]++; }
+  std::vector<long long> te(n);
+  cudaMemcpyFromSymbol(te.data(), kc_bot_trace_end, n * 8);
+  double sum[16][8] = {}, cmp[16][8] = {}; int cnt[16][8] = {};
+  for (int i = 0; i + 1 < n; ++i) {
+    int o = op[i] / 16, d = op[i] % 16;
+    sum[o][d] += t[i + 1] - t[i]; cmp[o][d] += te[i] - t[i]; cnt[o][d]++;
+  }
   const char* nm[10] = {"jacobi", "resid", "restrict", "prolong", "join", "j2z", "rr", "pj", "tiny", "csync"};
   for (int o = 0; o < 10; ++o) for (int d = 0; d < nlev; ++d) if (cnt[o][d])
-    printf("  %-9s level %d (m=%2d): %5d phases, %7.0f cycles avg, %9.0f total\n", nm[o], d, bot_m(m0, d), cnt[o][d], sum[o][d] / cnt[o][d], sum[o][d]);
+    printf("  %-9s level %d (m=%3d): %5d phases, %7.0f cycles avg (thread 0 to its barrier %5.0f), %9.0f total\n", nm[o], d,
+           bot_m(m0, d), cnt[o][d], sum[o][d] / cnt[o][d], cmp[o][d] / cnt[o][d], sum[o][d]);
   printf("phases traced: %d, total cycles %lld\n", n, n > 1 ? t[n - 1] - t[0] : 0);
   return 0;
 }
