@@ -497,10 +497,65 @@ __device__ __forceinline__ void bot_prolong_ext(double* __restrict__ u, const do
   }
 }
 
-// PH_TINY: whole kappa_cycle frames on sides <= KC_BOT_TINY_M, run by warp 0
-// alone (one __syncwarp per phase, no descriptor decode).  Follows
-// BotBuilder::rec with J2Z on, so the host's dry replay of the same rules
-// knows the buffer each level ends in.
+// Phases of the tiny frames with the side M a compile-time constant: one
+// point (or coarse point / cell) per thread of the group (M*M <= its
+// threads), index math folded, no item loop.  Per-point arithmetic is that
+// of bot_stencil / bot_j2z / bot_restrict / bot_prolong.
+template <int M>
+__device__ __forceinline__ void bt_stencil(bool jac, bool zero, const double* __restrict__ u, double* __restrict__ o,
+                                           const double* __restrict__ f, const St9& st, int tid) {
+  constexpr int S = M + 2;
+  if (tid >= M * M) return;
+  const int y = tid / M, i = y * S + (tid - y * M);
+  if (jac && zero) {
+    o[i] = kc_jacobi_zero(f[i], st.c);
+    return;
+  }
+  const double* p = u + i;
+  const double au = kc_sum9(st, p[-S - 1], p[-S], p[-S + 1], p[-1], p[0], p[1], p[S - 1], p[S], p[S + 1]);
+  o[i] = jac ? kc_jacobi_pt(p[0], f[i], au, st.c) : DSUB(f[i], au);
+}
+template <int M>
+__device__ __forceinline__ void bt_j2z(double* __restrict__ u, const double* __restrict__ f, const St9& st, int tid) {
+  constexpr int S = M + 2;
+  if (tid >= M * M) return;
+  const int y = tid / M, i = y * S + (tid - y * M);
+  u[i] = bot_j2z_pt(f + i, S, st);
+}
+template <int M>
+__device__ __forceinline__ void bt_restrict(const double* __restrict__ r, double* __restrict__ fc,
+                                            double* __restrict__ vc, double ccenter, bool cc, int tid) {
+  constexpr int S = M + 2, MC = (M - 1) / 2, SC = MC + 2;
+  if (tid >= MC * MC) return;
+  const int q = tid / MC, p = tid - q * MC;
+  const double* rc = r + (2 * q + 1) * S + (2 * p + 1);
+  const double* rs = rc - S;
+  const double* rn = rc + S;
+  const double fv = kc_fw(rs[-1], rs[0], rs[1], rc[-1], rc[0], rc[1], rn[-1], rn[0], rn[1]);
+  fc[q * SC + p] = fv;
+  if (cc) vc[0] = __ddiv_rn(fv, ccenter);
+}
+template <int M>
+__device__ __forceinline__ void bt_prolong(double* __restrict__ u, const double* __restrict__ vc, bool zero, int tid) {
+  constexpr int S = M + 2, MC = (M - 1) / 2, SC = MC + 2, NC = MC + 1;
+  if (tid >= NC * NC) return;
+  const int q = tid / NC, p = tid - q * NC;
+  const double c00 = vc[(q - 1) * SC + p - 1], c01 = vc[(q - 1) * SC + p];
+  const double c10 = vc[q * SC + p - 1], c11 = vc[q * SC + p];
+  double* pu = u + (2 * q) * S + 2 * p;
+  // (even, even): fine[0::2, 0::2] = 0.25 (((c00 + c01) + c10) + c11)   (transfer.py:57)
+  pu[0] = DADD(zero ? 0.0 : pu[0], DMUL(0.25, DADD(DADD(DADD(c00, c01), c10), c11)));
+  if (p < MC) pu[1] = DADD(zero ? 0.0 : pu[1], DMUL(0.5, DADD(c01, c11)));  // transfer.py:56
+  if (q < MC) {
+    pu[S] = DADD(zero ? 0.0 : pu[S], DMUL(0.5, DADD(c10, c11)));        // transfer.py:55
+    if (p < MC) pu[S + 1] = DADD(zero ? 0.0 : pu[S + 1], c11);          // transfer.py:54
+  }
+}
+
+// PH_TINY: whole kappa_cycle frames on sides <= KC_BOT_TINY_M (15, 7, 3 with
+// the 1x1 folded into the 3x3 leaf), one named barrier / __syncwarp per
+// phase, no descriptor decode.  Follows BotBuilder::rec with J2Z on, so the
+// host's dry replay of the same rules knows the buffer each level ends in.
 struct BotTiny {
   double* sm;
   const BotLv* lv;
@@ -512,58 +567,58 @@ struct BotTiny {
     else asm volatile("bar.sync 1, 256;" ::: "memory");
   }
   __device__ __forceinline__ double* buf(const BotLv& L, int b) const { return sm + (b ? L.vo1 : L.vo0); }
+  template <int M>
   __device__ __forceinline__ void relax(const BotLv& L, const St9& st, int count, int& cur, int& vz) const {
     int i = 0;
     const double* f = sm + L.fo;
     if (count >= 2 && vz) {
-      bot_j2z(buf(L, cur), f, L, st, tid, nth, BotPush{nullptr, nullptr, -1});
+      bt_j2z<M>(buf(L, cur), f, st, tid);
       sync();
       vz = 0;
       i = 2;
     }
     for (; i < count; ++i) {
-      bot_stencil<1>(true, vz, buf(L, cur), buf(L, cur ^ 1), f, L.m, L.m, L.S, L.inv, st, tid, nth, L.nitem1,
-                     BotPush{nullptr, nullptr, -1});
+      bt_stencil<M>(true, vz, buf(L, cur), buf(L, cur ^ 1), f, st, tid);
       sync();
       vz = 0;
       cur ^= 1;
     }
   }
   // pre-smooth + residual + restriction of level d into d+1
+  template <int M>
   __device__ __forceinline__ void down(int d, const BotLv& L, const St9& st, int& cur, int& vz, bool cc) const {
-    relax(L, st, nu1, cur, vz);
+    relax<M>(L, st, nu1, cur, vz);
     const double* f = sm + L.fo;
     if (!vz) {
-      bot_stencil<1>(false, false, buf(L, cur), buf(L, cur ^ 1), f, L.m, L.m, L.S, L.inv, st, tid, nth, L.nitem1,
-                     BotPush{nullptr, nullptr, -1});
+      bt_stencil<M>(false, false, buf(L, cur), buf(L, cur ^ 1), f, st, tid);
       sync();
     }
     const BotLv C = lv[d + 1];
-    bot_restrict(vz ? f : buf(L, cur ^ 1), L, sm + C.fo, C.m, C.S, sm + C.vo0, tab[d + 1].center, cc, tid, nth,
-                 BotPush{nullptr, nullptr, -1});
+    bt_restrict<M>(vz ? f : buf(L, cur ^ 1), sm + C.fo, sm + C.vo0, tab[d + 1].center, cc, tid);
     sync();
   }
   // prolongation of child buffer cb + post-smoothing
+  template <int M>
   __device__ __forceinline__ void up(int d, const BotLv& L, const St9& st, int& cur, int& vz, int cb) const {
     const BotLv C = lv[d + 1];
-    bot_prolong(buf(L, cur), buf(C, cb), L, C.m, C.S, vz, tid, nth, BotPush{nullptr, nullptr, -1});
+    bt_prolong<M>(buf(L, cur), buf(C, cb), vz, tid);
     sync();
     vz = 0;
-    relax(L, st, nu2, cur, vz);
+    relax<M>(L, st, nu2, cur, vz);
   }
-  // a frame whose child is the coarsest (both coarsest calls folded)
+  // a 3x3 frame whose child is the coarsest (both coarsest calls folded)
   __device__ __forceinline__ void leaf(int d, int& cur, int& vz) const {
     const BotLv L = lv[d];
     const St9 st = tab[d];
-    down(d, L, st, cur, vz, true);
-    up(d, L, st, cur, vz, 0);
+    down<3>(d, L, st, cur, vz, true);
+    up<3>(d, L, st, cur, vz, 0);
   }
   // side 7 (on warps 0-1: one point per thread): children are side-3 leaves
   // on warp 0 (kappa only sets how many); slot passes their final buffer
   __device__ __forceinline__ void frame7(int d, int kap, int& cur, int& vz, int* slot) const {
     const BotLv L = lv[d];
     const St9 st = tab[d];
-    down(d, L, st, cur, vz, false);
+    down<7>(d, L, st, cur, vz, false);
     int cc = 0;
     if (tid < 32) {
       const BotTiny w{sm, lv, tab, nu1, nu2, tid, 32};
@@ -576,10 +631,10 @@ struct BotTiny {
       sync();
       cc = *slot;
     }
-    up(d, L, st, cur, vz, cc);
+    up<7>(d, L, st, cur, vz, cc);
   }
   // side 15 on warps 0-7; its side-7 children (kappa, kappa - 1;
-  // cycle.py:215-218) on warp 0 while warps 1-7 wait at the named barrier
+  // cycle.py:215-218) on warps 0-1 while warps 2-7 wait at the named barrier
   // child_buf[0]: the side-15 frame's child buffer, child_buf[1]: the side-7 frames'
   __device__ void frame(int d, int kap, int nlev, int& cur, int& vz, int* child_buf) const {
     if (d + 2 == nlev) {
@@ -592,7 +647,7 @@ struct BotTiny {
     }
     const BotLv L = lv[d];
     const St9 st = tab[d];
-    down(d, L, st, cur, vz, false);
+    down<15>(d, L, st, cur, vz, false);
     if (tid < 64) {
       const BotTiny w{sm, lv, tab, nu1, nu2, tid, 64};
       int cc = 0, cz = 1;
@@ -601,7 +656,7 @@ struct BotTiny {
       if (tid == 0) child_buf[0] = cc;
     }
     sync();
-    up(d, L, st, cur, vz, child_buf[0]);
+    up<15>(d, L, st, cur, vz, child_buf[0]);
   }
 };
 
