@@ -706,6 +706,18 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
     const int y0 = a - 1, y1 = min(a + R, m0);
     const int w0 = (y0 - a + 1) * S, w1 = (y1 - a + 2) * S;  // loaded storage rows, as an offset range
     const int fbase = 2 * (R + 2) * S;
+    if (bp.v_zero) zero(0, fbase + w0);
+    else {
+      zero(0, w0);
+      zero(w1, fbase + w0);
+    }
+    zero(fbase + w1, total);
+    // programmatic dependent launch: everything above touched only shared
+    // memory, parameters and the schedule; the entry level is the previous
+    // grid's output.  The successor (a column-tile post pass) may fetch its
+    // level's f and v from now on: they were final before that grid ended.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
     for (int y = y0 + wid; y <= y1; y += KC_BOT_WARPS) {
       const double* gfr = bp.gf + kc_idx(bp.gP, y, -1);
       const double* gvr = bp.gv + kc_idx(bp.gP, y, -1);
@@ -715,14 +727,10 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
         if (!bp.v_zero) cp8(sm + o + c, gvr + c);
       }
     }
-    if (bp.v_zero) zero(0, fbase + w0);
-    else {
-      zero(0, w0);
-      zero(w1, fbase + w0);
-    }
-    zero(fbase + w1, total);
   } else {
     zero(0, total);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
   }
   KC_BOT_MARK(5);
 #pragma unroll

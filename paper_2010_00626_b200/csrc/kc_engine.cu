@@ -152,6 +152,7 @@ struct kc_handle {
   int npart_cap = 0;
   bool fuse = true;           // use the fused streaming kernels in native cycles
   bool tile = true;           // overlapped-tile kernels on the mid-size levels
+  bool pdl = true;            // programmatic dependent launch around the bottom kernel (KC_PDL=0: off)
   int num_sms = 148;
   SolveState* d_solve = nullptr;   // device loop state
   double* d_hist = nullptr;        // err | res histories for the device loop
@@ -543,13 +544,18 @@ int ex_bottom(kc_handle* h, int l, int k1, int k2) {
     cfg.blockDim = dim3(KC_BOT_THREADS);
     cfg.dynamicSmemBytes = h->bot_smem;
     cfg.stream = h->stream;
-    cudaLaunchAttribute at[1];
+    // programmatic dependent launch: the cluster takes free SMs and runs its
+    // prologue while the previous pass (a column-tile pre pass, which
+    // triggers at its start) finishes; k_bottom waits before its entry load
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = h->bot_cs;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     KC_CUDA(h, cudaLaunchKernelEx(&cfg, k_bottom, bp, h->bot_m0));
   } else {
     k_bottom<<<1, KC_BOT_THREADS, h->bot_smem, h->stream>>>(bp, h->bot_m0);
@@ -771,7 +777,20 @@ int ex_ctile_post(kc_handle* h, int l) {
     default: fn = KCT_POST(4); break;
   }
 #undef KCT_POST
-  fn<<<tiles, KC_CT_NW * 32, 0, h->stream>>>(p);
+  // programmatic dependent launch: f and v of this level are final before
+  // the previous kernel (the child's last pass or the bottom kernel, which
+  // triggers only after its own wait) completes, so they are fetched before
+  // k_ctile_post waits for the coarse v
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tiles);
+  cfg.blockDim = dim3(KC_CT_NW * 32);
+  cfg.stream = h->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  KC_CUDA(h, cudaLaunchKernelEx(&cfg, fn, p));
   KC_LAUNCH_CHECK(h);
   ++h->launches;
   L.cur ^= 1;
@@ -1180,6 +1199,10 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
   KC_CUDA(none, cudaSetDevice(device));
 
   kc_handle* h = new kc_handle();
+  {
+    const char* penv = getenv("KC_PDL");
+    h->pdl = !(penv && penv[0] == '0');
+  }
   h->num_sms = prop.multiProcessorCount;
   h->n = n;
   h->coarsening = coarsening;

@@ -202,6 +202,9 @@ __global__ void __launch_bounds__(NW * 32) k_ctile_pre(const TileParams p) {
   static_assert(W <= 32, "one lane per region column");
   __shared__ double su[2][H][32];
   __shared__ double sf[H][32];
+  // a programmatically launched successor (the bottom kernel) may start its
+  // independent prologue on free SMs now; it waits for this grid itself
+  asm volatile("griddepcontrol.launch_dependents;");
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int tx = blockIdx.x % p.tiles_x, ty = blockIdx.x / p.tiles_x;
   const int y0 = ty * TY, x0 = tx * TX;
@@ -322,6 +325,9 @@ __global__ void __launch_bounds__(NW * 32) k_ctile_post(const TileParams p) {
         if (!VZ) kt_cp8(&su[1][r][lane], p.u + gi);
       }
     }
+    // f and v of this level are final already (ex_ctile_post); the coarse v
+    // is the previous grid's output
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int qx = min(max(qx0 + lane, -1), p.mc);
     for (int r = w; r < CH; r += NW) {
       const int qy = min(max(qy0 + r, -1), p.mc);
