@@ -30,6 +30,12 @@
 #ifndef KS_MINB
 #define KS_MINB 4   // __launch_bounds__ min blocks per SM of the streaming kernels
 #endif
+#ifndef KS_UNROLL
+#define KS_UNROLL 4  // row-step unroll of k_pre's loop (1 -> 4: level-1 pre 125 -> 116 us)
+#endif
+#ifndef KS_UNROLL_POST
+#define KS_UNROLL_POST 2  // row-step unroll of k_post's loop (3+ spills the norms variant)
+#endif
 
 struct StreamParams {
   const double* u;   // input v (current buffer); unused on a zero guess
@@ -186,6 +192,8 @@ __global__ void __launch_bounds__(128, KS_MINB) k_pre(const StreamParams p) {
   };
   // f rows from ys-D (stage D's row in the first step) up to ys+KS_PF-1
   for (int y = ys - D; y < ys + KS_PF; ++y) fetch(y, y >= ys);
+  constexpr int UR = NU <= 2 ? KS_UNROLL : 1;  // deeper stages spill when unrolled
+#pragma unroll UR
   for (int yin = ys; yin <= ye; ++yin) {
     fetch(yin + KS_PF, true);
     ks_cp_wait();  // all but the newest KS_PF groups done: rows <= yin have landed
@@ -309,6 +317,8 @@ __global__ void __launch_bounds__(128, KS_MINB) k_post(const StreamParams p) {
       ks_cp_commit();
     };
     for (int y = ys - D; y < ys + KS_PF; ++y) fetch(y, y >= ys);
+    constexpr int UR = (NU <= 2 || !NORMS) ? KS_UNROLL_POST : 1;  // deeper norm stages spill
+#pragma unroll UR
     for (int yin = ys; yin <= ye; ++yin) {
       fetch(yin + KS_PF, true);
       ks_cp_wait();
