@@ -153,6 +153,7 @@ struct kc_handle {
   bool fuse = true;           // use the fused streaming kernels in native cycles
   bool tile = true;           // overlapped-tile kernels on the mid-size levels
   bool pdl = true;            // programmatic dependent launch around the bottom kernel (KC_PDL=0: off)
+  bool ks_sym_on = true;      // shared w1/w7 products on symmetric levels (KC_SYM=0: off)
   int num_sms = 148;
   SolveState* d_solve = nullptr;   // device loop state
   double* d_hist = nullptr;        // err | res histories for the device loop
@@ -584,7 +585,11 @@ int ks_choose_nq(int mc, int nbands, int slots) {
 }
 
 typedef void (*KsFn)(StreamParams);
-KsFn ks_pre_fn(int nu, bool zero, bool norms = false) {
+// sym: the level's stencil has w7 == w1 bitwise (ks_step<SYM>); the shared
+// products are instantiated for the nu = 2 passes that stream level 1
+bool ks_sym(const St9& s) { return std::memcmp(&s.w[1], &s.w[7], sizeof(double)) == 0; }
+KsFn ks_pre_fn(int nu, bool zero, bool norms = false, bool sym = false) {
+  if (sym && nu == 2 && !zero) return norms ? k_pre<2, false, true, false, true> : k_pre<2, false, false, false, true>;
 #define KS_PRE(N) return zero ? k_pre<N, true> : (norms ? k_pre<N, false, true> : k_pre<N, false>)
   switch (nu) {
     case 0: KS_PRE(0);
@@ -596,7 +601,8 @@ KsFn ks_pre_fn(int nu, bool zero, bool norms = false) {
 #undef KS_PRE
   return nullptr;
 }
-KsFn ks_post_fn(int nu, bool vz, int nm) {
+KsFn ks_post_fn(int nu, bool vz, int nm, bool sym = false) {
+  if (sym && nu == 2 && nm == 0) return vz ? k_post<2, true, 0, false, true> : k_post<2, false, 0, false, true>;
 #define KS_POST(N)                                                                            \
   return vz ? (nm == 1 ? k_post<N, true, 1> : nm == 2 ? k_post<N, true, (N > 0 ? 2 : 0)> : k_post<N, true, 0>) \
             : (nm == 1 ? k_post<N, false, 1> : nm == 2 ? k_post<N, false, (N > 0 ? 2 : 0)> : k_post<N, false, 0>)
@@ -806,7 +812,7 @@ int ex_pre(kc_handle* h, int l, bool norms = false) {
   if (L.m <= KC_CTILE_MAX_M && h->tile && !norms && h->nu1 <= 2) return ex_ctile_pre(h, l);
   if (L.m <= KC_TILE_MAX_M && h->tile && !norms) return ex_tile(h, l, true);
   int nw = 0;
-  KsFn fn = ks_pre_fn(h->nu1, L.vzero, norms);
+  KsFn fn = ks_pre_fn(h->nu1, L.vzero, norms, h->ks_sym_on && ks_sym(L.st));
   StreamParams p = ks_params(h, l, h->nu1 + 1, &nw, (const void*)fn);
   if (norms) {
     if (32 * nw > h->npart_cap) KC_FAIL(h, KC_EINVAL, "norm partial buffer too small (%d < %d)", h->npart_cap, 32 * nw);
@@ -842,7 +848,7 @@ int ex_post(kc_handle* h, int l, int nm) {
   if (L.m <= KC_TILE_POST_MAX_M && h->tile && !nm) return ex_tile(h, l, false);
   int nw = 0;
   const int D = h->nu2 + (nm == 1 ? 1 : 0);
-  KsFn fn = ks_post_fn(h->nu2, L.vzero, nm);
+  KsFn fn = ks_post_fn(h->nu2, L.vzero, nm, h->ks_sym_on && ks_sym(L.st));
   StreamParams p = ks_params(h, l, D > 0 ? D : 1, &nw, (const void*)fn);
   p.vc = C.v[C.cur];
   if (nm) {
@@ -1202,6 +1208,8 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
   {
     const char* penv = getenv("KC_PDL");
     h->pdl = !(penv && penv[0] == '0');
+    const char* senv = getenv("KC_SYM");
+    h->ks_sym_on = !(senv && senv[0] == '0');
   }
   h->num_sms = prop.multiProcessorCount;
   h->n = n;
@@ -1358,8 +1366,10 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
     int nw2 = 0;
     ks_params(h, 0, D, &nw2, (const void*)ks_post_fn(nu2, false, 1));
     nw = nw > nw2 ? nw : nw2;
-    ks_params(h, 0, nu1 + 1, &nw2, (const void*)ks_pre_fn(nu1, false, true));
-    nw = nw > 32 * nw2 ? nw : 32 * nw2;  // the pre kernel leaves per-lane partials
+    for (int sym = 0; sym < 2; ++sym) {
+      ks_params(h, 0, nu1 + 1, &nw2, (const void*)ks_pre_fn(nu1, false, true, sym));
+      nw = nw > 32 * nw2 ? nw : 32 * nw2;  // the pre kernel leaves per-lane partials
+    }
     if (nu2 >= 1) {
       ks_params(h, 0, nu2, &nw2, (const void*)ks_post_fn(nu2, false, 2));
       nw = nw > 32 * nw2 ? nw : 32 * nw2;

@@ -110,16 +110,22 @@ __device__ __forceinline__ double2 ks_lds2(const double* p) { return *reinterpre
 struct KsAcc {
   double2 b, c, cen;
 };
+// SYM: the stencil's north and south centre taps are bitwise equal (w7 ==
+// w1, true of the finest level's stencil), so w7 * n and w1 * n are the same
+// rounded product and each is computed once: 2 fewer multiplies per stage.
+template <bool SYM = false>
 __device__ __forceinline__ void ks_step(const St9& s, KsAcc& a, double2 n, double& aux, double& auy,
                                         double2& cen) {
   const double l = kc_shfl_up1(n.y), e = kc_shfl_dn1(n.x);
-  aux = DADD(DADD(DADD(a.c.x, DMUL(s.w[6], l)), DMUL(s.w[7], n.x)), DMUL(s.w[8], n.y));
-  auy = DADD(DADD(DADD(a.c.y, DMUL(s.w[6], n.x)), DMUL(s.w[7], n.y)), DMUL(s.w[8], e));
+  const double p1x = DMUL(s.w[1], n.x), p1y = DMUL(s.w[1], n.y);
+  const double p7x = SYM ? p1x : DMUL(s.w[7], n.x), p7y = SYM ? p1y : DMUL(s.w[7], n.y);
+  aux = DADD(DADD(DADD(a.c.x, DMUL(s.w[6], l)), p7x), DMUL(s.w[8], n.y));
+  auy = DADD(DADD(DADD(a.c.y, DMUL(s.w[6], n.x)), p7y), DMUL(s.w[8], e));
   cen = a.cen;
   a.c.x = DADD(DADD(DADD(a.b.x, DMUL(s.w[3], l)), DMUL(s.w[4], n.x)), DMUL(s.w[5], n.y));
   a.c.y = DADD(DADD(DADD(a.b.y, DMUL(s.w[3], n.x)), DMUL(s.w[4], n.y)), DMUL(s.w[5], e));
-  a.b.x = DADD(DADD(DMUL0(s.w[0], l), DMUL(s.w[1], n.x)), DMUL(s.w[2], n.y));
-  a.b.y = DADD(DADD(DMUL0(s.w[0], n.x), DMUL(s.w[1], n.y)), DMUL(s.w[2], e));
+  a.b.x = DADD(DADD(DMUL0(s.w[0], l), p1x), DMUL(s.w[2], n.y));
+  a.b.y = DADD(DADD(DMUL0(s.w[0], n.x), p1y), DMUL(s.w[2], e));
   a.cen = n;
 }
 // Dirichlet: +0.0 outside the interior (global row y)
@@ -138,7 +144,7 @@ __device__ __forceinline__ void ks_mask(double2& v, int y, int mg, bool colx_in,
 // Stage t (1..D) consumes the row stage t-1 produced in the same step and
 // completes its own output one row behind it (ks_step), so stage t emits row
 // yin - t and a chunk needs only D warm-up rows per side.
-template <int NU, bool ZERO, bool NORMS = false, bool STRIP = false>
+template <int NU, bool ZERO, bool NORMS = false, bool STRIP = false, bool SYM = false>
 __global__ void __launch_bounds__(128, KS_MINB) k_pre(const StreamParams p) {
   constexpr int D = NU + 1;
   // row geometry (StreamParams): compile-time whole-level values unless STRIP
@@ -192,7 +198,8 @@ __global__ void __launch_bounds__(128, KS_MINB) k_pre(const StreamParams p) {
   };
   // f rows from ys-D (stage D's row in the first step) up to ys+KS_PF-1
   for (int y = ys - D; y < ys + KS_PF; ++y) fetch(y, y >= ys);
-  constexpr int UR = NU <= 2 ? KS_UNROLL : 1;  // deeper stages spill when unrolled
+  // deeper stages, and the shared-product norms pass, spill when unrolled x4
+  constexpr int UR = NU > 2 ? 1 : (SYM && NORMS && KS_UNROLL > 2) ? 2 : KS_UNROLL;
 #pragma unroll UR
   for (int yin = ys; yin <= ye; ++yin) {
     fetch(yin + KS_PF, true);
@@ -220,7 +227,7 @@ __global__ void __launch_bounds__(128, KS_MINB) k_pre(const StreamParams p) {
       } else {
         double ax, ay;
         double2 cen;
-        ks_step(s, A[t], nw[t - 1], ax, ay, cen);
+        ks_step<SYM>(s, A[t], nw[t - 1], ax, ay, cen);
         const double rx = DSUB(fr[t].x, ax), ry = DSUB(fr[t].y, ay);
         if (t <= NU) {
           ox = DADD(cen.x, DMUL(s.c, rx));  // kc_jacobi_pt
@@ -267,7 +274,7 @@ __global__ void __launch_bounds__(128, KS_MINB) k_pre(const StreamParams p) {
 // NM = 0: plain; 1: ||v'||^2 and ||f - A v'||^2 (one extra residual stage,
 // per-warp partials); 2: f . v' (the PCG rz = r . z of a preconditioning
 // cycle, whose f is r and whose result is z; per-lane partials, NU >= 1).
-template <int NU, bool VZ, int NM, bool STRIP = false>
+template <int NU, bool VZ, int NM, bool STRIP = false, bool SYM = false>
 __global__ void __launch_bounds__(128, KS_MINB) k_post(const StreamParams p) {
   constexpr bool NORMS = NM == 1, DOT = NM == 2;
   const int g_rows = STRIP ? p.rows : p.m, g_y0 = STRIP ? p.gy0 : 0, g_mg = STRIP ? p.mg : p.m;
@@ -350,7 +357,7 @@ __global__ void __launch_bounds__(128, KS_MINB) k_post(const StreamParams p) {
       for (int t = 1; t <= D; ++t) {
         double ax, ay;
         double2 cen;
-        ks_step(s, A[t], nw[t - 1], ax, ay, cen);
+        ks_step<SYM>(s, A[t], nw[t - 1], ax, ay, cen);
         const double rx = DSUB(fr[t].x, ax), ry = DSUB(fr[t].y, ay);
         if (t <= NU) nw[t] = make_double2(DADD(cen.x, DMUL(s.c, rx)), DADD(cen.y, DMUL(s.c, ry)));
         else nw[t] = make_double2(rx, ry);

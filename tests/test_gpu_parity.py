@@ -693,3 +693,33 @@ def test_distributed_nccl_world1_graph_replay_bit_exact():
         assert (kappa, False) in s._graphs  # cycles 2.. ran as graph replays
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_shared_product_passes_bit_exact(monkeypatch):
+    """The level-1 streaming passes with the shared w1/w7 products (KC_SYM,
+    ks_step<SYM>; the finest stencil is bitwise north/south symmetric) give the
+    oracle's iterates bit-for-bit, and the fused-norms pre pass used by the
+    solve loop gives the same histories and result as the plain passes."""
+    n, m = 11, 2047
+    rng = np.random.default_rng(11)
+    v0, f0 = rng.random((m, m)), rng.standard_normal((m, m))
+    cfg = CycleConfig(n=n, kappa=2)
+    h = O.Hierarchy(O.hierarchy(1e-4, 45.0, n), nu1=2, nu2=2)
+    h.v[0], h.f[0] = v0.copy(), f0.copy()
+    h.cycle(2)
+    ref = h.v[0].copy()
+    out = {}
+    for sym in ("1", "0"):
+        monkeypatch.setenv("KC_SYM", sym)
+        st = build_state(ProblemSpec(1e-4, 45.0), cfg)
+        st.v[0], st.f[0] = v0, f0
+        run_cycle(st, cfg, CycleStats.for_levels(n))
+        assert np.array_equal(st.v[0], ref), sym
+        st.v[0], st.f[0] = v0, f0
+        k, status, _, err, res = st.solve_device(2, stop="residual", target_reduction=1e10, max_cycles=12)
+        out[sym] = (k, status, err, res, np.asarray(st.v[0]).copy())
+        st.close()
+    a, b = out["1"], out["0"]
+    assert a[:4] == b[:4]
+    assert np.array_equal(a[4], b[4])
