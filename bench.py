@@ -23,10 +23,20 @@ norms computed on the device every cycle (the stopping test needs them).
            timed on a bounded sample (a few n = 12 cycles) and extrapolated
            by the reference's own cycle count (tests/golden).
 
-`--impl reference` times the reference's CPU algorithm (the oracle port; the
-reference is pure Python/numpy and cannot travel to the GPU box) on the same
-config: each step is one n = 12 cycle; value = mean cycle time x the
-reference's cycle count to the same target.
+Arithmetic: the engine ships two builds of the same sources, "exact"
+(libkcb200.so, iterates bit-identical to the reference) and "fast"
+(libkcb200_fast.so, FMA-contracted).  Both are swept; the fast build is
+eligible for the headline only where its solve takes exactly the
+reference's cycle count (the north star's parity bar; tests/test_gpu_fast.py
+checks the histories), and `config.arith` says which build the line used.
+
+`--impl reference` times the UNMODIFIED reference package `kcycle` (installed
+into baseline/_ref by tools/install_reference.sh, which travels to the GPU
+box; the numpy oracle port only if it is absent) on the same config through
+its own public API: each step is one `kcycle.cycle.run_cycle` at n = 12 on
+its `GridState` plus the two norms the stopping test needs; value = mean
+step time x the reference's cycle count to the same target (extrapolated:
+a full reference solve takes 7-40 minutes on one core).
 
 Multi-GPU (torchrun, N > 1): the same solve row-strip decomposed over the N
 GPUs (paper_2010_00626_b200.distributed: NCCL halos, coarse agglomeration,
@@ -62,6 +72,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=12)
     ap.add_argument("--kappa", default="best", help="1,2,3,4,W or best")
+    ap.add_argument("--arith", choices=["best", "exact", "fast"], default="best",
+                    help="engine build: exact (bit-identical), fast (FMA) or the faster one that passes the count gate")
     ap.add_argument("--target", type=float, default=1e10)
     ap.add_argument("--cpu-cycles", type=int, default=2, help="oracle cycles timed for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -181,28 +193,80 @@ def cpu_model():
     return "unknown"
 
 
+def import_reference():
+    """The unmodified reference package from baseline/_ref, or None."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "kcycle")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import kcycle
+        import kcycle.cycle  # noqa: F401
+        import kcycle.mesh  # noqa: F401
+        import kcycle.stencil  # noqa: F401
+    except Exception:
+        return None
+    return kcycle
+
+
+class ReferenceSolveStep:
+    """One step of the reference's own stand-alone loop at level count n:
+    kcycle.cycle.run_cycle on its GridState, then norm2(v) and
+    norm2(residual(A, v, f)) (the two norms the stopping rules need;
+    cycle.py:343-347, make_golden.py track_standalone)."""
+
+    def __init__(self, kcycle, n: int, kname: str):
+        import numpy as np
+        self.kc = kcycle
+        problem = kcycle.stencil.ProblemSpec(epsilon=EPS, phi=PHI, seed=0)
+        self.cfg = kcycle.cycle.CycleConfig(n=n, kappa=math.inf if kname == "W" else int(kname))
+        self.state = kcycle.cycle.build_state(problem, self.cfg)
+        self.state.v[0] = np.random.default_rng(0).random(self.state.v[0].shape)
+        self.stats = kcycle.cycle.CycleStats.for_levels(n)
+
+    def __call__(self) -> float:
+        t0 = time.perf_counter()
+        self.kc.cycle.run_cycle(self.state, self.cfg, self.stats)
+        self.kc.mesh.norm2(self.state.v[0])
+        self.kc.mesh.norm2(self.kc.stencil.residual(self.state.ops[0], self.state.v[0], self.state.f[0]))
+        return time.perf_counter() - t0
+
+
 def run_reference(args, rank: int, world: int):
-    """--impl reference: the reference's CPU algorithm (oracle port), 1 core."""
+    """--impl reference: the reference package itself (baseline/_ref), 1 core
+    (numpy / scipy.ndimage are single-threaded on this path)."""
     if rank != 0:
         return
     n = args.n
     counts = golden_counts(n)
     cands = KAPPAS if args.kappa == "best" else (args.kappa,)
-    # pick the CPU-best kappa from one timed cycle each (warm-up, untimed)
+    kcycle = import_reference()
+    kind = "reference" if kcycle is not None else "port"
+
+    def stepper(kname):
+        if kcycle is not None:
+            return ReferenceSolveStep(kcycle, n, kname)
+        return lambda: oracle_cycle_seconds(n, kname, 1)[0]
+
+    # pick the CPU-best kappa from one timed step each (golden count x step)
     est = {}
     for k in cands:
         c = counts.get(k, {}).get("residual_1e10")
         if c is None:
             continue
-        t = oracle_cycle_seconds(n, k, 1)[0]
-        est[k] = t * c
+        est[k] = stepper(k)() * c
     best = min(est, key=est.get) if est else cands[0]
     count = counts[best]["residual_1e10"]
-    for _ in range(max(0, args.warmup - 1)):
-        oracle_cycle_seconds(n, best, 1)
-    times = oracle_cycle_seconds(n, best, args.steps)
+    step = stepper(best)
+    for _ in range(args.warmup):
+        step()
+    times = [step() for _ in range(args.steps)]
     per_cycle_ms = 1e3 * statistics.mean(times)
     value = per_cycle_ms * count
+    what = ("kcycle.cycle.run_cycle on kcycle's GridState + norm2(v) + norm2(residual) (the unmodified "
+            f"reference {kcycle.__version__} from baseline/_ref)" if kcycle is not None else
+            "the numpy oracle port (baseline/_ref absent)")
     line = {
         "metric": METRIC, "value": value, "unit": "ms", "impl": "reference", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_cycle_ms, "higher_is_better": False,
@@ -210,9 +274,9 @@ def run_reference(args, rank: int, world: int):
         "config": {"workload": f"rotated anisotropic diffusion eps=1e-4 phi=45, {2**n+1}^2 (n={n}), "
                                f"stand-alone kappa-cycle to 1e-10 rel. residual, best kappa",
                    "kappa": best, "cycles_to_target": count, "n_levels": n},
-        "cpu_baseline": {"value": value, "unit": "ms", "cores": 1, "kind": "port",
-                         "sample": f"{args.steps} timed kappa={best} cycles of the numpy oracle at n={n} "
-                                   f"(4095^2), x {count} reference cycles to 1e-10 rel. residual (extrapolated)",
+        "cpu_baseline": {"value": value, "unit": "ms", "cores": 1, "kind": kind,
+                         "sample": f"{args.steps} timed kappa={best} steps at n={n} (4095^2), each one cycle of "
+                                   f"{what}; x {count} reference cycles to 1e-10 rel. residual (extrapolated)",
                          "cpu": cpu_model(), "per_kappa_estimate_ms": {k: 1e3 * v for k, v in est.items()}},
         "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -309,36 +373,51 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     m = 2 ** n - 1
     problem = kc.ProblemSpec(EPS, PHI, seed=0)
     base_cfg = kc.CycleConfig(n=n, kappa=1)
-    state = kc.build_state(problem, base_cfg, device=device)
-    stream = torch.cuda.ExternalStream(state.stream_ptr(), device=device)
     v0 = np.random.default_rng(0).random((m, m))
-    state.v[0] = v0
-    state.snapshot()
+    ariths = ("exact", "fast") if args.arith == "best" else (args.arith,)
+    states = {}
+    for a in ariths:
+        st = kc.build_state(problem, base_cfg, device=device, arith=a)
+        st.v[0] = v0
+        st.snapshot()
+        states[a] = st
+    counts = golden_counts(n)
 
-    def solve(kname):
+    def solve(arith, kname):
         k = n if kname == "W" else int(kname)
-        state.restore()
-        return state.solve_device(k, "residual", args.target, 20000)
+        states[arith].restore()
+        return states[arith].solve_device(k, "residual", args.target, 20000)
 
-    # kappa selection (untimed setup): one solve per candidate
+    # (arith, kappa) selection (untimed setup): one solve per candidate.  A
+    # candidate is eligible only if its cycle count equals the reference's
+    # (tests/golden), the north star's parity bar for the FMA build.
     cands = KAPPAS if args.kappa == "best" else (args.kappa,)
     sweep = {}
-    for kname in cands:
-        k = n if kname == "W" else int(kname)
-        L = state.launches_per_cycle(k)
-        it, status, dms, err, res = solve(kname)
-        sweep[kname] = {"cycles": it, "status": status, "ms_to_solution": dms,
-                        "ms_per_cycle": dms / max(1, it), "launches_per_cycle": L,
-                        "final_rel_residual": res[-1] / res[0]}
-    best = min(sweep, key=lambda kk: sweep[kk]["ms_to_solution"])
+    for a in ariths:
+        sweep[a] = {}
+        for kname in cands:
+            k = n if kname == "W" else int(kname)
+            L = states[a].launches_per_cycle(k)
+            it, status, dms, err, res = solve(a, kname)
+            ref_it = counts.get(kname, {}).get("residual_1e10")
+            sweep[a][kname] = {"cycles": it, "reference_cycles": ref_it, "status": status, "ms_to_solution": dms,
+                               "ms_per_cycle": dms / max(1, it), "launches_per_cycle": L,
+                               "final_rel_residual": res[-1] / res[0],
+                               "eligible": status == "converged" and (ref_it is None or it == ref_it)}
+    elig = [(a, kk) for a in ariths for kk in cands if sweep[a][kk]["eligible"]]
+    if not elig:
+        raise SystemExit("no (arith, kappa) candidate matched the reference cycle counts")
+    best_arith, best = min(elig, key=lambda ak: sweep[ak[0]][ak[1]]["ms_to_solution"])
     if world > 1:  # every rank must run the same kappa
-        t = torch.tensor([KAPPAS.index(best)], device=f"cuda:{device}")
+        t = torch.tensor([KAPPAS.index(best), ariths.index(best_arith)], device=f"cuda:{device}")
         dist.broadcast(t, 0)
-        best = KAPPAS[int(t.item())]
+        best, best_arith = KAPPAS[int(t[0].item())], ariths[int(t[1].item())]
+    state = states[best_arith]
+    stream = torch.cuda.ExternalStream(state.stream_ptr(), device=device)
     kbest = n if best == "W" else int(best)
-    cycles = sweep[best]["cycles"]
+    cycles = sweep[best_arith][best]["cycles"]
     for _ in range(args.warmup):
-        solve(best)
+        solve(best_arith, best)
 
     # ---- timed region: K solves, inputs resident in HBM ---------------------
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -350,7 +429,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         ev0.record(stream)
         results = []
         for _ in range(args.steps):
-            results.append(solve(best))
+            results.append(solve(best_arith, best))
         ev1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -463,37 +542,55 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if not args.quick:
         pcg = {}
         zeros = np.zeros((m, m))
-        for pk in cands:
-            k = n if pk == "W" else int(pk)
-            cfgk = kc.CycleConfig(n=n, kappa=math.inf if pk == "W" else k)
-            pc = kc.PcgConfig(cycle=cfgk, target_reduction=args.target, stop="residual", max_iterations=2000)
-            kc.pcg_solve(state, zeros, pc, x0=v0)  # warm (captures the graphs)
-            reps = [kc.pcg_solve(state, zeros, pc, x0=v0) for _ in range(2)]
-            gp = os.path.join(ROOT, "tests", "golden", f"pcg_n{n}_k{pk}.json")
-            ref_it = None
-            if os.path.exists(gp):
-                with open(gp) as fh:
-                    ref_it = json.load(fh)["iters"]["residual_1e10"]
-            pcg[pk] = {"iterations": reps[-1].iterations, "reference_iterations": ref_it,
-                          "status": reps[-1].status,
-                          "ms_to_solution": min(r.device_time_ms for r in reps),
-                          "ms_per_iteration": min(r.device_time_ms for r in reps) / max(1, reps[-1].iterations)}
-        pbest = min(pcg, key=lambda kk: pcg[kk]["ms_to_solution"])
-        pcg = {"best_kappa": pbest, "best_ms": pcg[pbest]["ms_to_solution"], "stop": "recursive residual 1e-10 "
+        for a in ariths:
+            for pk in cands:
+                k = n if pk == "W" else int(pk)
+                cfgk = kc.CycleConfig(n=n, kappa=math.inf if pk == "W" else k)
+                pc = kc.PcgConfig(cycle=cfgk, target_reduction=args.target, stop="residual", max_iterations=2000)
+                kc.pcg_solve(states[a], zeros, pc, x0=v0)  # warm (captures the graphs)
+                reps = [kc.pcg_solve(states[a], zeros, pc, x0=v0) for _ in range(2)]
+                gp = os.path.join(ROOT, "tests", "golden", f"pcg_n{n}_k{pk}.json")
+                ref_it = None
+                if os.path.exists(gp):
+                    with open(gp) as fh:
+                        ref_it = json.load(fh)["iters"]["residual_1e10"]
+                ms = min(r.device_time_ms for r in reps)
+                pcg[f"{a}:{pk}"] = {"arith": a, "kappa": pk, "iterations": reps[-1].iterations,
+                                    "reference_iterations": ref_it, "status": reps[-1].status,
+                                    "ms_to_solution": ms, "ms_per_iteration": ms / max(1, reps[-1].iterations),
+                                    "eligible": reps[-1].status == "converged" and ref_it in (None, reps[-1].iterations)}
+        pel = [kk for kk in pcg if pcg[kk]["eligible"]] or list(pcg)
+        pbest = min(pel, key=lambda kk: pcg[kk]["ms_to_solution"])
+        pcg = {"best": pbest, "best_ms": pcg[pbest]["ms_to_solution"], "stop": "recursive residual 1e-10 "
                "(PcgConfig default, krylov.py:51)", "sweep": pcg}
 
     # ---- CPU baseline (oracle, rank 0, N = 1 only) ---------------------------
+    # timed at the CPU's OWN best kappa: one oracle cycle per kappa x the
+    # reference's cycle count picks it, then cpu_cycles more cycles time it
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        counts = golden_counts(n)
-        ref_count = counts.get(best, {}).get("residual_1e10")
-        t = oracle_cycle_seconds(n, best, args.cpu_cycles, v0)
+        est = {}
+        for kk in cands:
+            c = counts.get(kk, {}).get("residual_1e10")
+            if c is not None:
+                est[kk] = oracle_cycle_seconds(n, kk, 1, v0)[0] * c
+        cbest = min(est, key=est.get) if est else best
+        count = counts.get(cbest, {}).get("residual_1e10") or cycles
+        t = oracle_cycle_seconds(n, cbest, args.cpu_cycles, v0)
         per_cycle = statistics.mean(t)
-        count = ref_count if ref_count is not None else cycles
         cpu = {"value": 1e3 * per_cycle * count, "unit": "ms", "cores": 1, "kind": "port",
-               "sample": f"{args.cpu_cycles} kappa={best} cycles of the numpy oracle at n={n} (4095^2), "
+               "sample": f"{args.cpu_cycles} kappa={cbest} cycles of the numpy oracle at n={n} (4095^2; kappa={cbest} "
+                         f"is the CPU's own best by one timed cycle per kappa x the reference's count), "
                          f"{1e3 * per_cycle:.0f} ms/cycle x {count} reference cycles to 1e-10 rel. residual "
-                         f"(extrapolated)", "cpu": cpu_model()}
+                         f"(extrapolated)", "cpu": cpu_model(), "kappa": cbest,
+               "per_kappa_estimate_ms": {kk: 1e3 * v for kk, v in est.items()}}
+
+    build_info = None
+    bpath = os.path.join(ROOT, "build", "build_info.json")
+    if os.path.exists(bpath):
+        with open(bpath) as fh:
+            build_info = json.load(fh)
+        build_info["this_host"] = os.uname().nodename
 
     if rank == 0:
         line = {
@@ -502,10 +599,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"rotated anisotropic diffusion eps=1e-4 phi=45, {2**n+1}^2 (n={n}), "
                                    f"stand-alone kappa-cycle to 1e-10 rel. residual, best kappa",
-                       "kappa": best, "cycles_to_target": cycles, "n_levels": n, "nu": [2, 2], "omega": OMEGA,
-                       "parallelism": "replicas" if world > 1 else "single",
+                       "kappa": best, "arith": best_arith, "cycles_to_target": cycles, "n_levels": n, "nu": [2, 2],
+                       "omega": OMEGA, "parallelism": "replicas" if world > 1 else "single",
                        "l2": f"inputs larger than L2 (3 x {8 * m * m / 1e6:.0f} MB finest arrays + hierarchy > 126 MB)",
-                       "reference_cycles_to_target": golden_counts(n).get(best, {}).get("residual_1e10")},
+                       "reference_cycles_to_target": counts.get(best, {}).get("residual_1e10")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": kname,
@@ -520,18 +617,23 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                               "per_level_ms": per_level,
                               "coarse_fraction_le511": coarse_ms / cycle_ms_eager if cycle_ms_eager else None,
                               "algorithmic_bytes_per_cycle": b_cycle,
-                              "cycle_gbs": b_cycle / (ms_per_step / cycles * 1e-3) / 1e9 if cycles else None,
-                              "cycle_frac_of_hbm_peak": (b_cycle / (ms_per_step / cycles * 1e-3) / 1e9 / peak
-                                                         if cycles else None),
+                              "survey_convention_gbs": (b_cycle / (ms_per_step / cycles * 1e-3) / 1e9
+                                                        if cycles else None),
                               "fused_bytes_per_cycle": b_fused,
                               "fused_cycle_gbs": b_fused / (ms_per_step / cycles * 1e-3) / 1e9 if cycles else None,
-                              "bytes_note": "algorithmic_bytes_per_cycle is SURVEY §8(d)'s convention (24 B per "
-                                            "Jacobi sweep, (24nu+16) N per call); the fused passes move "
-                                            "48 N_l + 16 N_l+1 per call (fused_bytes_per_cycle), so cycle_gbs "
-                                            "can exceed the HBM peak; levels <= 2047^2 are largely L2-resident"},
+                              "fused_cycle_frac_of_hbm_peak": (b_fused / (ms_per_step / cycles * 1e-3) / 1e9 / peak
+                                                               if cycles else None),
+                              "bytes_note": "algorithmic_bytes_per_cycle is SURVEY §8(d)'s per-op convention (24 B "
+                                            "per Jacobi sweep, (24nu+16) N per call), which the fused passes do "
+                                            "not move, so survey_convention_gbs is not a bandwidth; the engine "
+                                            "moves 48 N_l + 16 N_l+1 per call (fused_bytes_per_cycle), and "
+                                            "fused_cycle_frac_of_hbm_peak is the physical cycle utilisation "
+                                            "(levels <= 2047^2 are largely L2-resident)"},
+            "build": build_info,
         }
         print(json.dumps(line), flush=True)
-    state.close()
+    for st in states.values():
+        st.close()
 
 
 def main():

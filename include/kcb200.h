@@ -61,6 +61,15 @@ extern "C" {
 typedef struct kc_handle kc_handle;
 
 int kc_abi_version(void);
+
+/* Arithmetic of this build: KC_ARITH_EXACT (libkcb200.so: separately rounded
+ * products and sums in the reference's order, iterates bit-identical to
+ * kcycle) or KC_ARITH_FAST (libkcb200_fast.so: the same expressions with FMA
+ * contraction; histories within 1e-10 and identical iteration counts).  The
+ * reference has no such switch; both builds export the same entry points. */
+#define KC_ARITH_EXACT 0
+#define KC_ARITH_FAST 1
+int kc_arith_mode(void);
 const char* kc_last_error(const kc_handle* h);
 
 /* Galerkin coarse stencil R*A*P (stencil.py:129-148), bit-identical to the
@@ -121,7 +130,9 @@ int kc_solve(kc_handle* h, int kappa, int stop_mode, double target_reduction, in
  * krylov.py:65): it receives r and must fill z, both host (ny, nx) arrays.
  * x_out (may be NULL) receives the final iterate.  hist (may be NULL)
  * receives up to max_it+1 values of the stop measure (||x|| for
- * KC_STOP_ERROR, recursive ||r|| for KC_STOP_RESIDUAL, krylov.py:88-89).
+ * KC_STOP_ERROR, recursive ||r|| for KC_STOP_RESIDUAL, krylov.py:88-89):
+ * hist[0 .. iterations]; on a p.Ap breakdown (krylov.py:110-112) no measure
+ * is taken at that step and hist[iterations] is NaN.
  * n_precond receives the number of preconditioner applications. */
 typedef void (*kc_precond_fn)(const double* r, double* z, long long ny, long long nx, void* ctx);
 int kc_pcg(kc_handle* h, int kappa, const double* f, const double* x0, int stop_mode,

@@ -20,6 +20,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("KCB200_LIB") or os.path.join(_HERE, "libkcb200.so")  # override: experiments only
+# the FMA-contracted build of the same sources (kc_common.cuh KC_FAST)
+LIB_FAST_PATH = os.environ.get("KCB200_LIB_FAST") or os.path.join(_HERE, "libkcb200_fast.so")
+ARITH_MODES = ("exact", "fast")
 
 KC_OK, KC_EINVAL, KC_ESINGULAR, KC_ECUDA, KC_ENOMEM = 0, 1, 2, 3, 4
 KC_COARSEN_FULL, KC_COARSEN_SEMI_Y = 0, 1
@@ -39,13 +42,6 @@ class CudaError(RuntimeError):
 class CudaUnavailableError(CudaError):
     """No usable sm_100 device: the engine has no CPU fallback."""
 
-
-if not os.path.exists(LIB_PATH):
-    raise ImportError(
-        f"{LIB_PATH} is missing: build the CUDA engine first "
-        "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
-
-lib = C.CDLL(LIB_PATH)
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int)
@@ -102,25 +98,60 @@ _SIGS = {
     "kc_restore": (C.c_int, [_h]),
 }
 
-for _name, (_res, _args) in _SIGS.items():
-    _fn = getattr(lib, _name)
-    _fn.restype = _res
-    _fn.argtypes = _args
-
-if lib.kc_abi_version() != 1:
-    raise ImportError(f"libkcb200.so ABI version {lib.kc_abi_version()} != 1; rebuild")
+_SIGS["kc_arith_mode"] = (C.c_int, [])
 
 
-def last_error(handle) -> str:
-    msg = lib.kc_last_error(handle)
+def _load(path: str, arith: int):
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} is missing: build the CUDA engine first "
+            "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+    handle = C.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(handle, name)
+        fn.restype = res
+        fn.argtypes = args
+    if handle.kc_abi_version() != 1:
+        raise ImportError(f"{path} ABI version {handle.kc_abi_version()} != 1; rebuild")
+    if handle.kc_arith_mode() != arith:
+        raise ImportError(f"{path} reports arithmetic mode {handle.kc_arith_mode()}, expected {arith}")
+    return handle
+
+
+lib = _load(LIB_PATH, 0)  # the exact build: iterates bit-identical to the reference
+_libs = {"exact": lib}
+
+
+def default_arith() -> str:
+    """Arithmetic of new handles unless a caller says otherwise: KCB200_ARITH
+    ("exact" or "fast"), else "exact" (the bit-exact drop-in)."""
+    mode = os.environ.get("KCB200_ARITH", "exact")
+    if mode not in ARITH_MODES:
+        raise ValueError(f"KCB200_ARITH must be one of {ARITH_MODES}, got {mode!r}")
+    return mode
+
+
+def lib_for(arith: str | None = None):
+    """The engine library of an arithmetic mode ("exact" | "fast"; None: default_arith())."""
+    arith = default_arith() if arith is None else arith
+    if arith not in ARITH_MODES:
+        raise ValueError(f"arith must be one of {ARITH_MODES}, got {arith!r}")
+    if arith not in _libs:
+        _libs[arith] = _load(LIB_FAST_PATH, 1)
+    return _libs[arith]
+
+
+def last_error(handle, which=None) -> str:
+    msg = (which or lib).kc_last_error(handle)
     return msg.decode() if msg else ""
 
 
-def check(rc: int, handle=None) -> None:
-    """Raise the reference's exception type for a non-OK status."""
+def check(rc: int, handle=None, which=None) -> None:
+    """Raise the reference's exception type for a non-OK status (`which`:
+    the library that owns `handle`, default the exact build)."""
     if rc == KC_OK:
         return
-    msg = last_error(handle)
+    msg = last_error(handle, which)
     if rc == KC_EINVAL:
         raise ValueError(msg)
     if rc == KC_ESINGULAR:

@@ -1169,6 +1169,8 @@ extern "C" {
 
 int kc_abi_version(void) { return KC_ABI_VERSION; }
 
+int kc_arith_mode(void) { return KC_FAST ? KC_ARITH_FAST : KC_ARITH_EXACT; }
+
 const char* kc_last_error(const kc_handle* h) { return h ? h->err.c_str() : g_create_err.c_str(); }
 
 int kc_galerkin_coarsen(const double* w_fine9, int coarsening, double* w_coarse9) {
@@ -1209,7 +1211,9 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
     const char* penv = getenv("KC_PDL");
     h->pdl = !(penv && penv[0] == '0');
     const char* senv = getenv("KC_SYM");
-    h->ks_sym_on = !(senv && senv[0] == '0');
+    // the shared-product form only saves work when products are separately
+    // rounded; in the FMA build every product is fused into its sum
+    h->ks_sym_on = senv ? senv[0] != '0' : !KC_FAST;
   }
   h->num_sms = prop.multiProcessorCount;
   h->n = n;
@@ -2023,8 +2027,9 @@ extern "C" int kc_pcg(kc_handle* h, int kappa, const double* f, const double* x0
         k_red_final<true><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_part, KC_RED_BLOCKS, h->d_scal + S_MEAS);
         KC_LAUNCH_CHECK(h);
         if ((rc = fetch_scalars(h, S_MEAS + 1))) return rc;
-        if (!(h->h_scal[S_PAP] > 0.0)) {
+        if (!(h->h_scal[S_PAP] > 0.0)) {  // no measure at this step: NaN marks it
           st = KC_STATUS_BREAKDOWN;
+          if (hist) hist[it] = NAN;
           break;
         }
         cur = h->h_scal[S_MEAS];

@@ -134,8 +134,9 @@ __global__ void k_pcg_check(cudaGraphConditionalHandle h_loop, cudaGraphConditio
   } else {
     const int it = st->it + 1;
     st->it = it;
-    if (!(scal[s_pap] > 0.0)) {
+    if (!(scal[s_pap] > 0.0)) {  // no measure at this step (krylov.py:110-112)
       st->status = KC_STATUS_BREAKDOWN;
+      st->hist[it] = __longlong_as_double(0x7ff8000000000000LL);  // NaN marks it
     } else {
       const double meas = scal[s_meas];
       st->hist[it] = meas;

@@ -176,7 +176,7 @@ class _LevelData:
         level = self._level(i)
         nx, ny = self._s.spec.dims[level - 1]
         out = np.empty((ny, nx))
-        N.check(N.lib.kc_get(self._s._h, level, self._which, N.dptr(out), ny, nx), self._s._h)
+        self._s._check(self._s._lib.kc_get(self._s._h, level, self._which, N.dptr(out), ny, nx))
         return out
 
     def __setitem__(self, i: int, value) -> None:
@@ -185,7 +185,7 @@ class _LevelData:
         a = N.as_f64c(value)
         if a.shape != (ny, nx):
             raise ValueError(f"dimension mismatch: {a.shape} vs {(ny, nx)}")
-        N.check(N.lib.kc_set(self._s._h, level, self._which, N.dptr(a), ny, nx), self._s._h)
+        self._s._check(self._s._lib.kc_set(self._s._h, level, self._which, N.dptr(a), ny, nx))
 
 
 class CudaGridState:
@@ -196,7 +196,7 @@ class CudaGridState:
     """
 
     def __init__(self, spec: HierarchySpec, ops: list[Stencil9], smoother: SmootherSpec,
-                 nu1: int, nu2: int, device: int = 0):
+                 nu1: int, nu2: int, device: int = 0, arith: str | None = None):
         if len(ops) != spec.n:
             raise ValueError(f"need {spec.n} operators, got {len(ops)}")
         self.spec = spec
@@ -207,11 +207,16 @@ class CudaGridState:
         self.nu2 = nu2
         self.device = device
         self._h = None
+        # "exact": libkcb200.so, iterates bit-identical to the reference;
+        # "fast": libkcb200_fast.so, FMA-contracted (histories within 1e-10,
+        # identical iteration counts); default N.default_arith()
+        self.arith = N.default_arith() if arith is None else arith
+        self._lib = N.lib_for(self.arith)
         w = np.ascontiguousarray(np.concatenate([op.w.ravel() for op in ops]), dtype=np.float64)
         h = C.c_void_p()
-        N.check(N.lib.kc_create(spec.n, N.COARSENING_KIND[spec.coarsening.value], N.dptr(w),
+        N.check(self._lib.kc_create(spec.n, N.COARSENING_KIND[spec.coarsening.value], N.dptr(w),
                                 N.SMOOTHER_KIND[smoother.kind.value], float(smoother.omega), nu1, nu2, device,
-                                C.byref(h)), None)
+                                C.byref(h)), None, self._lib)
         self._h = h
         self.v = _LevelData(self, N.KC_WHICH_V)
         self.f = _LevelData(self, N.KC_WHICH_F)
@@ -220,7 +225,7 @@ class CudaGridState:
     # -- lifetime ---------------------------------------------------------
     def close(self):
         if self._h is not None:
-            N.lib.kc_destroy(self._h)
+            self._lib.kc_destroy(self._h)
             self._h = None
 
     def __del__(self):
@@ -229,41 +234,44 @@ class CudaGridState:
         except Exception:
             pass
 
+    def _check(self, rc: int) -> None:
+        N.check(rc, self._h, self._lib)
+
     # -- state protocol (cycle.py:158-179) ---------------------------------
     def unknowns(self, level: int) -> int:
         return self.spec.unknowns(level)
 
     def relax_level(self, level: int, count: int):
-        N.check(N.lib.kc_relax(self._h, level, count), self._h)
+        self._check(self._lib.kc_relax(self._h, level, count))
 
     def restrict_residual(self, level: int):
-        N.check(N.lib.kc_restrict_residual(self._h, level), self._h)
+        self._check(self._lib.kc_restrict_residual(self._h, level))
 
     def zero_guess(self, level: int):
-        N.check(N.lib.kc_zero_guess(self._h, level), self._h)
+        self._check(self._lib.kc_zero_guess(self._h, level))
 
     def prolong_add(self, level: int):
-        N.check(N.lib.kc_prolong_add(self._h, level), self._h)
+        self._check(self._lib.kc_prolong_add(self._h, level))
 
     def solve_coarsest(self):
-        N.check(N.lib.kc_solve_coarsest(self._h), self._h)
+        self._check(self._lib.kc_solve_coarsest(self._h))
 
     # -- device reductions / parity entry points ---------------------------
     def norm2(self, level: int = 1, which: str = "v") -> float:
         out = C.c_double()
         w = N.KC_WHICH_V if which == "v" else N.KC_WHICH_F
-        N.check(N.lib.kc_norm2(self._h, level, w, C.byref(out)), self._h)
+        self._check(self._lib.kc_norm2(self._h, level, w, C.byref(out)))
         return out.value
 
     def residual_norm(self, level: int = 1) -> float:
         out = C.c_double()
-        N.check(N.lib.kc_residual_norm(self._h, level, C.byref(out)), self._h)
+        self._check(self._lib.kc_residual_norm(self._h, level, C.byref(out)))
         return out.value
 
     def apply_level(self, level: int = 1, residual: bool = False) -> np.ndarray:
         nx, ny = self.spec.dims[level - 1]
         out = np.empty((ny, nx))
-        N.check(N.lib.kc_apply(self._h, level, 1 if residual else 0, N.dptr(out), ny, nx), self._h)
+        self._check(self._lib.kc_apply(self._h, level, 1 if residual else 0, N.dptr(out), ny, nx))
         return out
 
     # -- native cycle --------------------------------------------------------
@@ -277,25 +285,25 @@ class CudaGridState:
         return st
 
     def run_cycles(self, kappa: int, count: int = 1):
-        N.check(N.lib.kc_run_cycles(self._h, int(kappa), int(count)), self._h)
+        self._check(self._lib.kc_run_cycles(self._h, int(kappa), int(count)))
 
     def time_cycles(self, kappa: int, count: int = 1) -> float:
         ms = C.c_double()
-        N.check(N.lib.kc_time_cycles(self._h, int(kappa), int(count), C.byref(ms)), self._h)
+        self._check(self._lib.kc_time_cycles(self._h, int(kappa), int(count), C.byref(ms)))
         return ms.value
 
     def launches_per_cycle(self, kappa: int) -> int:
         k = C.c_int()
-        N.check(N.lib.kc_cycle_launches(self._h, int(kappa), C.byref(k)), self._h)
+        self._check(self._lib.kc_cycle_launches(self._h, int(kappa), C.byref(k)))
         return k.value
 
     def sync(self):
-        N.check(N.lib.kc_sync(self._h), self._h)
+        self._check(self._lib.kc_sync(self._h))
 
     def stream_ptr(self) -> int:
         """cudaStream_t of the handle (for torch.cuda.ExternalStream timing)."""
         p = C.c_void_p()
-        N.check(N.lib.kc_stream(self._h, C.byref(p)), self._h)
+        self._check(self._lib.kc_stream(self._h, C.byref(p)))
         return p.value or 0
 
     def solve_device(self, kappa: int, stop: str = "error", target_reduction: float = 1e8,
@@ -304,9 +312,9 @@ class CudaGridState:
         err = np.zeros(max_cycles + 1)
         res = np.zeros(max_cycles + 1)
         it, st, dms = C.c_int(), C.c_int(), C.c_double()
-        N.check(N.lib.kc_solve(self._h, int(kappa), N.KC_STOP_ERROR if stop == "error" else N.KC_STOP_RESIDUAL,
-                               float(target_reduction), int(max_cycles), N.dptr(err), N.dptr(res),
-                               C.byref(it), C.byref(st), C.byref(dms)), self._h)
+        self._check(self._lib.kc_solve(self._h, int(kappa), N.KC_STOP_ERROR if stop == "error" else N.KC_STOP_RESIDUAL,
+                                       float(target_reduction), int(max_cycles), N.dptr(err), N.dptr(res),
+                                       C.byref(it), C.byref(st), C.byref(dms)))
         k = it.value
         return k, N.STATUS_NAMES[st.value], dms.value, err[: k + 1].tolist(), res[: k + 1].tolist()
 
@@ -318,22 +326,22 @@ class CudaGridState:
         elif out.shape != (ny, nx) or out.dtype != np.float64 or not out.flags.c_contiguous:
             raise ValueError("out must be a C-contiguous float64 array of the level shape")
         w = N.KC_WHICH_V if which == "v" else N.KC_WHICH_F
-        N.check(N.lib.kc_get(self._h, level, w, N.dptr(out), ny, nx), self._h)
+        self._check(self._lib.kc_get(self._h, level, w, N.dptr(out), ny, nx))
         return out
 
     def set_option(self, name: str, value: int):
         """Engine option (kc_set_option): "fuse" = 0 runs native cycles on the per-op kernels."""
-        N.check(N.lib.kc_set_option(self._h, name.encode(), int(value)), self._h)
+        self._check(self._lib.kc_set_option(self._h, name.encode(), int(value)))
 
     def snapshot(self):
         """Keep a device copy of the finest v (restore() puts it back)."""
-        N.check(N.lib.kc_snapshot(self._h), self._h)
+        self._check(self._lib.kc_snapshot(self._h))
 
     def restore(self):
-        N.check(N.lib.kc_restore(self._h), self._h)
+        self._check(self._lib.kc_restore(self._h))
 
     def fill_zero(self, level: int = 1, which: str = "f"):
-        N.check(N.lib.kc_fill_zero(self._h, level, N.KC_WHICH_F if which == "f" else N.KC_WHICH_V), self._h)
+        self._check(self._lib.kc_fill_zero(self._h, level, N.KC_WHICH_F if which == "f" else N.KC_WHICH_V))
 
     OP_NAMES = ("relax", "restrict_residual", "zero_guess", "prolong_add", "coarsest", "bottom", "pre", "post")
 
@@ -345,7 +353,7 @@ class CudaGridState:
         arg = (C.c_int * cap)()
         ms = (C.c_double * cap)()
         nops = C.c_int()
-        N.check(N.lib.kc_profile_cycle(self._h, int(kappa), cap, kind, lev, arg, ms, C.byref(nops)), self._h)
+        self._check(self._lib.kc_profile_cycle(self._h, int(kappa), cap, kind, lev, arg, ms, C.byref(nops)))
         return [{"op": self.OP_NAMES[kind[i]], "level": lev[i], "arg": arg[i], "ms": ms[i]}
                 for i in range(min(nops.value, cap))]
 
@@ -353,11 +361,13 @@ class CudaGridState:
 GridState = CudaGridState
 
 
-def build_state(problem: ProblemSpec, config: CycleConfig, device: int = 0) -> CudaGridState:
-    """Hierarchy dims and per-level operators for one solve (cycle.py:266-270)."""
+def build_state(problem: ProblemSpec, config: CycleConfig, device: int = 0,
+                arith: str | None = None) -> CudaGridState:
+    """Hierarchy dims and per-level operators for one solve (cycle.py:266-270).
+    `arith`: "exact" (bit-identical) or "fast" (FMA); default N.default_arith()."""
     spec = build_hierarchy(config.n, config.coarsening)
     ops = operator_hierarchy(problem, spec, config.coarse_op)
-    return CudaGridState(spec, ops, config.smoother, config.nu1, config.nu2, device=device)
+    return CudaGridState(spec, ops, config.smoother, config.nu1, config.nu2, device=device, arith=arith)
 
 
 # ---------------------------------------------------------------------------
@@ -462,6 +472,23 @@ def _reductions(hist: list[float]) -> list[float]:
     return [hist[i] / hist[i - 1] if hist[i - 1] > 0.0 else 0.0 for i in range(1, len(hist))]
 
 
+def _check_state_matches(state: CudaGridState, problem: ProblemSpec, config: CycleConfig) -> None:
+    """A caller-supplied state must be the hierarchy build_state(problem,
+    config) would make; a mismatch would silently solve another system."""
+    if not isinstance(state, CudaGridState):
+        raise TypeError("state must be a CudaGridState")
+    if state.n != config.n or state.spec.coarsening != config.coarsening:
+        raise ValueError(f"state hierarchy (n={state.n}, {state.spec.coarsening}) does not match the config "
+                         f"(n={config.n}, {config.coarsening})")
+    if (state.nu1, state.nu2) != (config.nu1, config.nu2):
+        raise ValueError(f"state relaxation counts {(state.nu1, state.nu2)} != config {(config.nu1, config.nu2)}")
+    if state.smoother != config.smoother:
+        raise ValueError(f"state smoother {state.smoother} != config {config.smoother}")
+    want = operator_hierarchy(problem, state.spec, config.coarse_op)
+    if any(not np.array_equal(a.w, b.w) for a, b in zip(state.ops, want)):
+        raise ValueError("state operators do not match the problem (epsilon, phi, coarse_op)")
+
+
 def solve_standalone(
     problem: ProblemSpec,
     config: CycleConfig,
@@ -491,6 +518,8 @@ def solve_standalone(
     fresh = state is None
     if fresh:
         state = build_state(problem, config, device=device)
+    else:
+        _check_state_matches(state, problem, config)
     nx, ny = state.spec.dims[0]
     if initial_guess is None:
         v0 = np.random.default_rng(problem.seed).random((ny, nx))

@@ -11,6 +11,7 @@ reordered (deterministic tree instead of OpenBLAS ddot).
 from __future__ import annotations
 
 import ctypes as C
+import math
 import time
 from dataclasses import dataclass
 
@@ -70,24 +71,28 @@ def pcg_solve(state: CudaGridState, f: np.ndarray, config: PcgConfig, x0: np.nda
                 np.ctypeslib.as_array(z_ptr, shape=(ny_, nx_))[...] = z
             except BaseException as exc:  # surfaced after the call returns
                 errors.append(exc)
-                np.ctypeslib.as_array(z_ptr, shape=(ny_, nx_))[...] = -1.0  # forces breakdown
+                # NaN makes r . z fail the rz > 0 test at once (breakdown)
+                np.ctypeslib.as_array(z_ptr, shape=(ny_, nx_))[...] = np.nan
         cb = N.PRECOND_FN(_cb)
     else:
         state.launches_per_cycle(kappa)  # capture outside the timed span
 
     t0 = time.perf_counter()
-    rc = N.lib.kc_pcg(state._h, kappa, N.dptr(fa), None if xa is None else N.dptr(xa),
+    rc = state._lib.kc_pcg(state._h, kappa, N.dptr(fa), None if xa is None else N.dptr(xa),
                       N.KC_STOP_ERROR if config.stop == "error" else N.KC_STOP_RESIDUAL,
                       float(config.target_reduction), mi, cb, None, N.dptr(hist),
                       C.byref(it), C.byref(st), C.byref(napp), N.dptr(xout), C.byref(dms))
     wall_ms = (time.perf_counter() - t0) * 1e3
     if errors:
         raise errors[0]
-    N.check(rc, state._h)
+    N.check(rc, state._h, state._lib)
     k = it.value
     status = N.STATUS_NAMES[st.value]
-    # iterations that stopped on breakdown recorded no measure for that step
-    nh = k + 1 if status != "breakdown" else max(1, k)
+    # a p.Ap breakdown at step k took no measure there (krylov.py:110-112):
+    # the engine marks hist[k] NaN; an r.z breakdown came after measuring
+    nh = k + 1
+    if status == "breakdown" and k > 0 and math.isnan(hist[k]):
+        nh = k
     h = hist[:nh].tolist()
     stats = CycleStats.for_levels(state.n)
     if precondition is None:

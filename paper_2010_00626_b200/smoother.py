@@ -1,7 +1,7 @@
 """Relaxation configuration (mirror of kcycle.smoother's SmootherKind/SmootherSpec,
-smoother.py:36-53).  The sweeps themselves run on the device (damped Jacobi,
-kc_grid_kernels.cuh / kc_bottom.cuh).  Zebra line relaxation is the next
-row of SURVEY.md §8(f) and is rejected by the engine for now (ValueError)."""
+smoother.py:36-53).  The sweeps themselves run on the device: damped Jacobi
+in the fused streaming / tile / bottom kernels (kc_stream.cuh, kc_tile.cuh,
+kc_bottom.cuh), zebra x / y / alternating line relaxation in kc_zebra.cuh."""
 
 from __future__ import annotations
 

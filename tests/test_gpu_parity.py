@@ -7,9 +7,10 @@ Bars (SURVEY.md §8(c) parity protocol):
   * solve histories: per-cycle error and residual norms within 1e-10
     relative of the reference (norm reductions are reordered sums, so ~1e-15
     is expected), identical iteration counts;
-  * PCG: identical iteration counts, histories within 1e-10 relative... except
-    that non-symmetric kappa (1 < kappa < n) amplifies dot-product rounding, so
-    the history tolerance there is 1e-6 and counts must still match.
+  * PCG: identical iteration counts; histories within 1e-10 x the initial
+    measure AND entry by entry (conftest.check_pcg_hist: 1e-6 relative plus
+    a floor of 1e-13 of the initial measure; dot products are reordered
+    sums, so alpha/beta differ in the last bits).
 Every test calls through the C-ABI (libkcb200.so) via the package.
 """
 
@@ -19,7 +20,7 @@ import math
 import numpy as np
 import pytest
 
-from conftest import golden_exists, load_json, load_npz
+from conftest import check_pcg_hist as _check_pcg_hist, golden_exists, load_json, load_npz
 
 pytestmark = pytest.mark.gpu
 INF = math.inf
@@ -338,6 +339,59 @@ def test_n12_standalone_vs_reference(kname):
     state.close()
 
 
+@pytest.mark.parametrize("kname", ["1", "2", "3", "4", "W"])
+def test_n12_standalone_error_rule_vs_reference(kname):
+    """The reference's own stopping rule (||v_k|| <= ||v_0|| / target,
+    cycle.py:332-347) at the BASELINE size: identical counts to 1e8 and 1e10
+    (kappa=1: 3883 / 5617 cycles ... W: 226 / 318) and both per-cycle
+    histories within 1e-10 relative, entry by entry, over the whole solve."""
+    name = f"solve_n12_k{kname}.json"
+    if not golden_exists(name):
+        pytest.skip(f"{name} not generated")
+    g = load_json(name)
+    kappa = INF if kname == "W" else int(kname)
+    cfg = CycleConfig(n=12, kappa=kappa)
+    problem = ProblemSpec(1e-4, 45.0, seed=0)
+    state = build_state(problem, cfg)
+    rep = solve_standalone(problem, cfg, 1e10, max_cycles=20000, stop="error", state=state)
+    assert rep.status == "converged"
+    assert rep.iterations == g["iters_error_1e10"]
+    assert len(rep.error_history) == len(g["err_hist"])
+    _check_hist(rep.error_history, g["err_hist"], 1e-10)
+    _check_hist(rep.residual_history, g["res_hist"], 1e-10)
+    rep8 = solve_standalone(problem, cfg, 1e8, max_cycles=20000, stop="error", state=state)
+    assert rep8.iterations == g["iters_error_1e8"]
+    state.close()
+
+
+def test_n14_cycles_vs_reference_golden():
+    """Config C4's global size (16385^2, 268 M unknowns): the native kappa=3
+    cycle (streaming kernels, column tiles, cluster bottom kernel) against
+    the REAL reference's iterates (tests/golden/solve_n14_k3.json, made by
+    make_golden.py solve --n 14 --kappa 3 --cap 3): sha256 of v after cycles
+    1 and 2, and the error / residual norms of cycles 0..3 within 1e-10."""
+    name = "solve_n14_k3.json"
+    if not golden_exists(name):
+        pytest.skip(f"{name} not generated")
+    g = load_json(name)
+    n, m = 14, 16383
+    cfg = CycleConfig(n=n, kappa=3)
+    problem = ProblemSpec(1e-4, 45.0, seed=0)
+    state = build_state(problem, cfg)
+    cap = len(g["err_hist"]) - 1
+    rep = solve_standalone(problem, cfg, 1e10, max_cycles=cap, stop="residual", state=state)
+    assert rep.iterations == cap and rep.status == "max_cycles"
+    _check_hist(rep.error_history, g["err_hist"], 1e-10)
+    _check_hist(rep.residual_history, g["res_hist"], 1e-10)
+    state.v[0] = np.random.default_rng(0).random((m, m))
+    done = 0
+    for k in sorted(int(s) for s in g["sha256"]):
+        state.run_cycles(3, k - done)
+        done = k
+        assert sha(state.v[0]) == g["sha256"][str(k)], k
+    state.close()
+
+
 # ---------------------------------------------------------------------------
 # PCG vs the reference (krylov.py)
 # ---------------------------------------------------------------------------
@@ -362,9 +416,7 @@ def test_pcg_vs_reference(n, kname):
         rep = pcg_solve(state, np.zeros((m, m)), PcgConfig(cycle=cfg, target_reduction=tgt, stop=stop), x0=x0)
         assert rep.status == "converged"
         assert rep.iterations == g["iters"][key], (stop, tgt)
-        hist = np.asarray(rep.error_history if stop == "error" else rep.residual_history)
-        ref_h = np.asarray(g[hist_key][: len(hist)])
-        assert np.max(np.abs(hist - ref_h)) / ref_h[0] < 1e-10
+        _check_pcg_hist(rep.error_history if stop == "error" else rep.residual_history, g[hist_key])
         ref = g["reference_reports"][key]
         assert rep.stats.visits == ref["visits"]
         state.close()
@@ -534,9 +586,7 @@ def test_n12_pcg_vs_reference(kname):
         rep = pcg_solve(state, f, PcgConfig(cycle=cfg, target_reduction=tgt, stop=stop), x0=x0)
         assert rep.status == "converged"
         assert rep.iterations == g["iters"][key], (stop, rep.iterations, g["iters"][key])
-        hist = np.asarray(rep.error_history if stop == "error" else rep.residual_history)
-        ref_h = np.asarray(g[hist_key][: len(hist)])
-        assert np.max(np.abs(hist - ref_h)) / ref_h[0] < 1e-10
+        _check_pcg_hist(rep.error_history if stop == "error" else rep.residual_history, g[hist_key])
     state.close()
 
 

@@ -41,6 +41,40 @@ def test_abi_version():
     assert N.lib.kc_abi_version() == 1
 
 
+def test_fast_build_exports_the_same_abi():
+    """libkcb200_fast.so (the FMA build of the same sources) loads, reports
+    its arithmetic mode and exports every header symbol; the exact build
+    reports exact."""
+    fast = N.lib_for("fast")
+    assert fast is not N.lib
+    assert N.lib.kc_arith_mode() == 0 and fast.kc_arith_mode() == 1
+    assert fast.kc_abi_version() == 1
+    for s in header_symbols():
+        assert hasattr(fast, s), s
+
+
+def test_arith_selection(monkeypatch):
+    assert N.lib_for("exact") is N.lib
+    monkeypatch.setenv("KCB200_ARITH", "fast")
+    assert N.default_arith() == "fast" and N.lib_for() is N.lib_for("fast")
+    monkeypatch.setenv("KCB200_ARITH", "bogus")
+    with pytest.raises(ValueError):
+        N.default_arith()
+    with pytest.raises(ValueError):
+        N.lib_for("double")
+
+
+def test_create_without_gpu_fails_loudly_in_both_builds():
+    """No CPU fallback: without a device kc_create raises CudaUnavailableError
+    (the package never routes through the oracle or numpy)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    for arith in ("exact", "fast"):
+        with pytest.raises(kc.CudaUnavailableError):
+            kc.build_state(ProblemSpec(1e-4, 45.0), CycleConfig(n=3), arith=arith)
+
+
 def test_stencil_hand_values():
     """test_stencil.py:26-34: eps=0.1, phi=45 -> centre 2.2, edges -0.55, corners +-0.225."""
     w = rotated_anisotropic_stencil(0.1, 45.0).w
