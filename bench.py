@@ -70,7 +70,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=12)
+    ap.add_argument("--n", type=int, default=None, help="levels (default 12 at N = 1, config C4's 14 at N > 1)")
     ap.add_argument("--kappa", default="best", help="1,2,3,4,W or best")
     ap.add_argument("--arith", choices=["best", "exact", "fast"], default="best",
                     help="engine build: exact (bit-identical), fast (FMA) or the faster one that passes the count gate")
@@ -182,6 +182,15 @@ def oracle_cycle_seconds(n: int, kname: str, cycles: int, v0=None):
     return times
 
 
+def _peak():
+    """HBM peak GB/s: MEASURED_PEAKS.json (driver-written), else B200_PROFILING.md's fallback."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as fh:
@@ -238,7 +247,7 @@ def run_reference(args, rank: int, world: int):
     (numpy / scipy.ndimage are single-threaded on this path)."""
     if rank != 0:
         return
-    n = args.n
+    n = args.n if args.n is not None else 12
     counts = golden_counts(n)
     cands = KAPPAS if args.kappa == "best" else (args.kappa,)
     kcycle = import_reference()
@@ -288,57 +297,117 @@ def run_reference(args, rank: int, world: int):
 # ---------------------------------------------------------------------------
 
 def run_ours_distributed(args, rank: int, world: int, local_rank: int):
-    """N > 1: the same 4097^2 stand-alone solve, row-strip decomposed over the
-    N GPUs (paper_2010_00626_b200.distributed: NCCL halos / allgather /
-    allreduce), strong scaling; value = max over ranks of the device time."""
+    """N > 1: config C4 by default -- 16385^2 (n = 14) row-strip decomposed
+    over the N GPUs (paper_2010_00626_b200.distributed: NCCL halos, coarse
+    agglomeration, allreduced norms, the stop test on the device with one
+    host read per batch of cycles), strong scaling; kappa from a sweep;
+    value = max over ranks of the device time per solve."""
     import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_2010_00626_b200 as kc
-    from paper_2010_00626_b200.distributed import DistributedKappaSolver, TorchComm
+    from paper_2010_00626_b200.distributed import HALO, DistributedKappaSolver, TorchComm
 
-    n = args.n
+    n = args.n if args.n is not None else 14
     m = 2 ** n - 1
-    kname = "2" if args.kappa == "best" else args.kappa  # the single-GPU best (bench sweep)
-    kappa = n if kname == "W" else int(kname)
     problem = kc.ProblemSpec(EPS, PHI, seed=0)
-    solver = DistributedKappaSolver(problem, kc.CycleConfig(n=n, kappa=kappa), TorchComm(), device=local_rank,
-                                    min_rows=64)
     v0 = np.random.default_rng(0).random((m, m))
-    solver.set_level1("v", v0)
-    solver.set_level1("f", np.zeros((m, m)))
-    solver.snapshot()  # the initial guess, restored before every solve
-    for _ in range(max(1, args.warmup)):
-        solver.restore()
-        rep = solver.solve_standalone(args.target, 20000, stop="residual", resident=True)
     stream = torch.cuda.current_stream()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
+    arith = "exact" if args.arith == "best" else args.arith  # the strip kernels are the exact build
+    s = DistributedKappaSolver(problem, kc.CycleConfig(n=n, kappa=2), TorchComm(), device=local_rank, min_rows=64)
+    s.set_level1("v", v0)
+    s.set_level1("f", np.zeros((m, m)))
+    s.snapshot()  # the initial guess, restored before every solve
+
+    def kap(kname):
+        return n if kname == "W" else int(kname)
+
+    def solve(kname):
+        s.restore()
+        return s.solve_standalone(args.target, 20000, stop="residual", resident=True, kappa=kap(kname))
+
+    def device_ms(fn, reps=1):
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        torch.cuda.synchronize()
         ev0.record(stream)
-        for _ in range(args.steps):
-            solver.restore()
-            rep = solver.solve_standalone(args.target, 20000, stop="residual", resident=True)
+        out = [fn() for _ in range(reps)]
         ev1.record(stream)
         torch.cuda.synchronize()
-    dist.barrier()
-    t = torch.tensor([ev0.elapsed_time(ev1) / args.steps], device=f"cuda:{local_rank}", dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    # e2e: host v0 scattered, solution gathered, inside the timed region
+        t = torch.tensor([ev0.elapsed_time(ev1) / reps], device=f"cuda:{local_rank}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()), out[-1]
+
+    # kappa sweep (untimed selection; every rank runs the same solves, rank 0 decides)
+    cands = KAPPAS if args.kappa == "best" else (args.kappa,)
+    sweep = {}
+    for kname in cands:
+        solve(kname)  # warm: first call eager, graphs captured on the next
+        solve(kname)
+        ms, rep = device_ms(lambda: solve(kname))
+        sweep[kname] = {"cycles": rep["iterations"], "status": rep["status"], "ms_to_solution": ms,
+                        "ms_per_cycle": ms / max(1, rep["iterations"])}
+    best = min(sweep, key=lambda kk: sweep[kk]["ms_to_solution"])
+    t = torch.tensor([KAPPAS.index(best)], device=f"cuda:{local_rank}")
+    dist.broadcast(t, 0)
+    best = KAPPAS[int(t.item())]
+    for _ in range(max(0, args.warmup - 1)):
+        solve(best)
+    with ClockSampler(local_rank) as clk:
+        ms, rep = device_ms(lambda: solve(best), args.steps)
+    cycles = rep["iterations"]
+
+    # e2e through the solver API: host v0 scattered, solution gathered, inside the timed region
+    def e2e_step():
+        r = s.solve_standalone(args.target, 20000, initial_guess=v0, stop="residual", kappa=kap(best))
+        return r, s.gather_level1()
+
     t0 = time.perf_counter()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        rep2 = solver.solve_standalone(args.target, 20000, initial_guess=v0, stop="residual")
-        sol = solver.gather_level1()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    te = torch.tensor([e0.elapsed_time(e1) / args.steps], device=f"cuda:{local_rank}", dtype=torch.float64)
-    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    te, (rep2, sol) = device_ms(e2e_step, args.steps)
+    host_wall = 1e3 * (time.perf_counter() - t0) / args.steps
+
+    # roofline: this rank's level-1 fused pre pass (k_pre on the strip), CUDA events on torch's stream
+    st1 = s.strips[0]
+    c = s.strips[1] if len(s.strips) > 1 else None
+    pre_ms = None
+    if c is not None and s._fused(1):
+        fn = lambda: s.ops.pre(st1.v[st1.cur], st1.f, st1.v[st1.cur ^ 1], c.f, st1.ny, st1.m, c.ny,  # noqa: E731
+                               st1.a, st1.m, s.w[0], s.omega, s.nu1, False)
+        fn()
+        pre_ms, _ = device_ms(fn, 20)
+    peak = _peak()[0]
+    alg_bytes = 24.0 * st1.ny * st1.m + 8.0 * (c.ny if c is not None else 0) * ((m - 1) // 2)
+    roofline = None
+    if pre_ms:
+        achieved = alg_bytes / (pre_ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": None, "kernel": f"k_pre<2> strip pass (rank-local level 1: {st1.ny} x {st1.m}, "
+                    "24 B/fine + 8 B/coarse unknown), max over ranks", "kernel_ms": pre_ms,
+                    "algorithmic_bytes_per_launch": alg_bytes}
+
+    # config C3 at this size: the distributed PCG (3 allreduced dots per iteration)
+    pcg = None
+    if not args.quick:
+        x0 = v0
+        zeros = np.zeros((m, m))
+        s.pcg_solve(zeros, x0=x0, target_reduction=args.target, stop="residual", kappa=kap(best))  # warm
+        s.pcg_solve(zeros, x0=x0, target_reduction=args.target, stop="residual", kappa=kap(best))  # capture
+        pms, prep = device_ms(lambda: s.pcg_solve(None, target_reduction=args.target, stop="residual",
+                                                  kappa=kap(best), resident=True, gather=False))
+        pcg = {"kappa": best, "iterations": prep["iterations"], "status": prep["status"], "ms_to_solution": pms,
+               "allreduces_per_iteration": 3, "inputs": "f and x0 resident on the devices"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        # the oracle at n = 12 for this kappa, scaled by the unknown count to n = 14 and by the cycle count
+        tc = statistics.mean(oracle_cycle_seconds(12, best, 1))
+        scale = (m / 4095.0) ** 2
+        cpu = {"value": 1e3 * tc * scale * cycles, "unit": "ms", "cores": 1, "kind": "port",
+               "sample": f"one kappa={best} n=12 cycle of the numpy oracle ({1e3 * tc:.0f} ms) x {scale:.1f} "
+                         f"(unknowns {m}^2 / 4095^2) x {cycles} cycles (this run's count, which equals the "
+                         f"reference's wherever goldens exist) -- extrapolated", "cpu": cpu_model()}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
@@ -346,14 +415,16 @@ def run_ours_distributed(args, rank: int, world: int, local_rank: int):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"rotated anisotropic diffusion eps=1e-4 phi=45, {2**n+1}^2 (n={n}), "
                                    f"stand-alone kappa-cycle to 1e-10 rel. residual, row-strip decomposed",
-                       "kappa": kname, "cycles_to_target": rep["iterations"], "n_levels": n,
-                       "parallelism": f"rows{world} + agglomeration below level {solver.plan.n_dist}",
-                       "l2": "inputs larger than L2"},
-            "roofline": None, "cpu_baseline": None,
-            "e2e": {"value": float(te.item()), "unit": "ms", "h2d_bytes_per_step": 8 * m * m,
-                    "d2h_bytes_per_step": 8 * m * m, "host_wall_ms": 1e3 * (time.perf_counter() - t0) / args.steps},
-            "gpu_launches": None, "clocks": clk.summary(), "status": rep["status"],
-            "solution_checksum": float(np.sum(sol)),
+                       "kappa": best, "arith": arith, "cycles_to_target": cycles, "n_levels": n,
+                       "parallelism": f"rows{world} + agglomeration below level {s.plan.n_dist}",
+                       "agglomeration_amdahl_note": "levels below the agglomeration threshold run redundantly on "
+                                                    "every rank (DESIGN.md §8)",
+                       "l2": "inputs larger than L2", "stop_test": "device-side, one host read per 8 cycles"},
+            "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": {"value": te, "unit": "ms", "h2d_bytes_per_step": 8 * m * m,
+                    "d2h_bytes_per_step": 8 * m * m, "host_wall_ms": host_wall},
+            "gpu_launches": None, "clocks": clk.summary(), "status": rep["status"], "sweep": sweep, "pcg": pcg,
+            "solution_checksum": float(np.sum(sol)), "graph_fallback": s.graph_fallback,
         }
         print(json.dumps(line), flush=True)
 
@@ -369,7 +440,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         import torch.distributed as dist
     device = local_rank
     torch.cuda.set_device(device)
-    n = args.n
+    n = args.n if args.n is not None else 12
     m = 2 ** n - 1
     problem = kc.ProblemSpec(EPS, PHI, seed=0)
     base_cfg = kc.CycleConfig(n=n, kappa=1)
@@ -472,13 +543,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         sweep_ms = sum(p["ms"] for p in relax1) / max(1, sweeps)
         alg_bytes = 24.0 * m * m  # read u, f; write u'
         kname = "k_jacobi (level 1, 4095^2, 24 B/unknown algorithmic)"
-    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(peaks_path):
-        with open(peaks_path) as fh:
-            peak = float(json.load(fh)["hbm_gbs"])
-        peak_src = "measured"
-    else:
-        peak, peak_src = 6650.0, "fallback"
+    peak, peak_src = _peak()
     achieved = alg_bytes / (sweep_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")

@@ -225,6 +225,64 @@ int kc_set_stream(kc_handle* h, void* stream);
  * graph once the same cycle has run outside a capture */
 int kc_cycle_enqueue(kc_handle* h, int kappa);
 
+/* ---- device-side loops of the distributed solvers (distributed.py) ------
+ * Every scalar of the reference's PCG loop (krylov.py:91-128) and
+ * stand-alone loop (cycle.py:331-353) lives in a device array `scal` of
+ * KC_DS_SLOTS doubles.  Strip kernels write per-rank partial sums into a
+ * slot, the caller allreduces the slot in place (NCCL), and kc_dist_step
+ * applies the reference's decisions on the device, so an iteration needs no
+ * host read and a batch of iterations is one CUDA graph.  `part` is caller
+ * scratch of KC_DS_PART doubles.  Once scal[KC_DS_DONE] is set the vector
+ * updates are skipped. */
+#define KC_DS_RZ 0
+#define KC_DS_RZN 1
+#define KC_DS_PAP 2
+#define KC_DS_MEAS 3
+#define KC_DS_ALPHA 4
+#define KC_DS_BETA 5
+#define KC_DS_TARGET 6
+#define KC_DS_IT 7
+#define KC_DS_MAXIT 8
+#define KC_DS_STATUS 9        /* KC_STATUS_* once DONE */
+#define KC_DS_DONE 10
+#define KC_DS_JUST_DONE 11    /* set by the step that stopped the loop */
+#define KC_DS_E2 12           /* stand-alone: sum v^2 (allreduced) */
+#define KC_DS_R2 13           /* stand-alone: sum (f - A v)^2 (allreduced) */
+#define KC_DS_STOP_RESIDUAL 14
+#define KC_DS_STREAK 15
+#define KC_DS_PREV 16
+#define KC_DS_REDUCTION 17
+#define KC_DS_SLOTS 32
+#define KC_DS_PART 592
+/* step kinds */
+#define KC_DS_PCG_RZ0 0   /* rz = r.z of z = M r before the loop (krylov.py:100-104) */
+#define KC_DS_PCG_PAP 1   /* it += 1; pAp breakdown or alpha = rz/pAp (krylov.py:107-113) */
+#define KC_DS_PCG_MEAS 2  /* hist[it] = sqrt(meas); converged (krylov.py:116-120) */
+#define KC_DS_PCG_RZ 3    /* rz_next breakdown, max_iterations, or beta = rz_next/rz, rz = rz_next (krylov.py:121-126) */
+#define KC_DS_SOLVE 4     /* stand-alone norms of cycle it: stop / divergence rules (cycle.py:343-353) */
+
+/* Ap = A p on the strip (p: one halo row each side) and the partial p.Ap
+ * into scal[slot] (krylov.py:107-108, mesh.py:98-102) */
+int kc_strip_apply_dot(const double* p, double* ap, int ny, int nx, int pitch, const double* w9, double* part,
+                       double* scal, int slot, void* stream);
+/* partial a.b into scal[slot] (mesh.py:98-102) */
+int kc_strip_dot(const double* a, const double* b, int ny, int nx, int pitch, double* part, double* scal, int slot,
+                 void* stream);
+/* x += alpha p; r -= alpha ap (krylov.py:114-115) with alpha = scal[KC_DS_ALPHA];
+ * partial of x.x (measure_x) or r.r into scal[KC_DS_MEAS] (krylov.py:88-89) */
+int kc_strip_pcg_update_xr(double* x, double* r, const double* p, const double* ap, int ny, int nx, int pitch,
+                           int measure_x, double* part, double* scal, void* stream);
+/* p = z + beta p (krylov.py:125) with beta = scal[KC_DS_BETA] */
+int kc_strip_pcg_update_p(double* p, const double* z, int ny, int nx, int pitch, const double* scal, void* stream);
+/* r = f - A x (krylov.py:76); x carries one halo row each side */
+int kc_strip_residual(const double* x, const double* f, double* r, int ny, int nx, int pitch, const double* w9,
+                      void* stream);
+/* dst = src when scal[KC_DS_JUST_DONE] (the stand-alone solution at the stop) */
+int kc_strip_copy_if(const double* src, double* dst, int ny, int nx, int pitch, const double* scal, void* stream);
+/* one scalar step of the loops (KC_DS_PCG_* / KC_DS_SOLVE); hist: PCG
+ * measures hist[it], or stand-alone (error, residual) pairs hist[2it..2it+1] */
+int kc_dist_step(int kind, double* scal, double* hist, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

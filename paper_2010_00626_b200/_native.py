@@ -96,7 +96,23 @@ _SIGS = {
     "kc_set_stream": (C.c_int, [_h, C.c_void_p]),
     "kc_cycle_enqueue": (C.c_int, [_h, C.c_int]),
     "kc_restore": (C.c_int, [_h]),
+    # device-side loops of the distributed solvers (kc_dist.cuh)
+    "kc_strip_apply_dot": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, _dp, C.c_void_p, C.c_void_p,
+                                     C.c_int, C.c_void_p]),
+    "kc_strip_dot": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                               C.c_void_p]),
+    "kc_strip_pcg_update_xr": (C.c_int, [C.c_void_p] * 4 + [C.c_int] * 4 + [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "kc_strip_pcg_update_p": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    "kc_strip_residual": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, _dp, C.c_void_p]),
+    "kc_strip_copy_if": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    "kc_dist_step": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
 }
+
+# scalar slots / step kinds of the distributed device loops (include/kcb200.h KC_DS_*)
+DS = dict(RZ=0, RZN=1, PAP=2, MEAS=3, ALPHA=4, BETA=5, TARGET=6, IT=7, MAXIT=8, STATUS=9, DONE=10, JUST_DONE=11,
+          E2=12, R2=13, STOP_RESIDUAL=14, STREAK=15, PREV=16, REDUCTION=17)
+DS_SLOTS, DS_PART = 32, 592
+DS_PCG_RZ0, DS_PCG_PAP, DS_PCG_MEAS, DS_PCG_RZ, DS_SOLVE = 0, 1, 2, 3, 4
 
 _SIGS["kc_arith_mode"] = (C.c_int, [])
 

@@ -29,6 +29,7 @@
 #include "kc_stream.cuh"
 #include "kc_tile.cuh"
 #include "kc_strip.cuh"
+#include "kc_dist.cuh"
 
 namespace {
 
@@ -2129,6 +2130,63 @@ extern "C" int kc_strip_norms(const double* v, const double* f, int ny, int nx, 
   }
   k_strip_norms<<<nb, 256, 0, (cudaStream_t)stream>>>(v, f, ny, nx, pitch, strip_stencil(w9, 1.0), part);
   k_strip_norms_final<<<1, 256, 0, (cudaStream_t)stream>>>(part, nb, out);
+  return strip_err(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// device-side loops of the distributed solvers (kc_dist.cuh)
+// ---------------------------------------------------------------------------
+extern "C" int kc_strip_apply_dot(const double* p, double* ap, int ny, int nx, int pitch, const double* w9,
+                                  double* part, double* scal, int slot, void* stream) {
+  if (!p || !ap || !w9 || !part || !scal || ny < 0 || nx <= 0 || slot < 0 || slot >= KC_DS_SLOTS) return KC_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_strip_apply_dot<<<KDS_NB, 256, 0, s>>>(p, ap, ny, nx, pitch, strip_stencil(w9, 1.0), part, scal);
+  k_dist_final<<<1, 256, 0, s>>>(part, KDS_NB, scal, slot);
+  return strip_err(cudaGetLastError());
+}
+
+extern "C" int kc_strip_dot(const double* a, const double* b, int ny, int nx, int pitch, double* part, double* scal,
+                            int slot, void* stream) {
+  if (!a || !b || !part || !scal || ny < 0 || nx <= 0 || slot < 0 || slot >= KC_DS_SLOTS) return KC_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_strip_dot<<<KDS_NB, 256, 0, s>>>(a, b, ny, nx, pitch, part, scal);
+  k_dist_final<<<1, 256, 0, s>>>(part, KDS_NB, scal, slot);
+  return strip_err(cudaGetLastError());
+}
+
+extern "C" int kc_strip_pcg_update_xr(double* x, double* r, const double* p, const double* ap, int ny, int nx,
+                                      int pitch, int measure_x, double* part, double* scal, void* stream) {
+  if (!x || !r || !p || !ap || !part || !scal || ny < 0 || nx <= 0) return KC_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_strip_pcg_update_xr<<<KDS_NB, 256, 0, s>>>(x, r, p, ap, ny, nx, pitch, scal, measure_x, part);
+  k_dist_final<<<1, 256, 0, s>>>(part, KDS_NB, scal, KC_DS_MEAS);
+  return strip_err(cudaGetLastError());
+}
+
+extern "C" int kc_strip_pcg_update_p(double* p, const double* z, int ny, int nx, int pitch, const double* scal,
+                                     void* stream) {
+  if (!p || !z || !scal || ny < 0 || nx <= 0) return KC_EINVAL;
+  k_strip_pcg_update_p<<<KDS_NB, 256, 0, (cudaStream_t)stream>>>(p, z, ny, nx, pitch, scal);
+  return strip_err(cudaGetLastError());
+}
+
+extern "C" int kc_strip_residual(const double* x, const double* f, double* r, int ny, int nx, int pitch,
+                                 const double* w9, void* stream) {
+  if (!x || !f || !r || !w9 || ny < 0 || nx <= 0) return KC_EINVAL;
+  k_strip_residual<<<KDS_NB, 256, 0, (cudaStream_t)stream>>>(x, f, r, ny, nx, pitch, strip_stencil(w9, 1.0));
+  return strip_err(cudaGetLastError());
+}
+
+extern "C" int kc_strip_copy_if(const double* src, double* dst, int ny, int nx, int pitch, const double* scal,
+                                void* stream) {
+  if (!src || !dst || !scal || ny < 0 || nx <= 0) return KC_EINVAL;
+  k_strip_copy_if<<<KDS_NB, 256, 0, (cudaStream_t)stream>>>(src, dst, ny, nx, pitch, scal);
+  return strip_err(cudaGetLastError());
+}
+
+extern "C" int kc_dist_step(int kind, double* scal, double* hist, void* stream) {
+  if (!scal || !hist || kind < KC_DS_PCG_RZ0 || kind > KC_DS_SOLVE) return KC_EINVAL;
+  k_dist_step<<<1, 32, 0, (cudaStream_t)stream>>>(kind, scal, hist);
   return strip_err(cudaGetLastError());
 }
 

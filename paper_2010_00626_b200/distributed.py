@@ -39,6 +39,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from ._native import DS, DS_PART, DS_PCG_MEAS, DS_PCG_PAP, DS_PCG_RZ, DS_PCG_RZ0, DS_SLOTS, DS_SOLVE, STATUS_NAMES
 from .costmodel import level_calls  # noqa: F401  (re-exported for planners)
 from .cycle import CycleConfig, CycleStats, DryState, kappa_cycle
 from .mesh import Coarsening, build_hierarchy
@@ -234,12 +235,48 @@ class CudaStripOps:
                                               self._p(vc, HALO), ny, nx, u.shape[1], vc.shape[1], crows, gy0, mg,
                                               HALO, HALO, self._w(w), omega, nu2, int(zero), self._stream()))
 
-    def norms(self, v, f, ny, nx, w):
-        out = self.torch.zeros(2, dtype=self.torch.float64, device=self.device)
+    def norms(self, v, f, ny, nx, w, out=None):
+        """(sum v^2, sum (f - A v)^2) over the strip into `out` (2 doubles; new tensor if None)."""
+        if out is None:
+            out = self.torch.zeros(2, dtype=self.torch.float64, device=self.device)
         if ny > 0:
             self.N.check(self.N.lib.kc_strip_norms(self._p(v, HALO), self._p(f, HALO), ny, nx, v.shape[1],
                                                    self._w(w), out.data_ptr(), self._stream()))
+        else:
+            out.zero_()
         return out
+
+    # -- device-side loops (kc_dist.cuh): scalars in `scal`, KC_DS_* slots --
+    def vector(self, n):
+        return self.torch.zeros(n, dtype=self.torch.float64, device=self.device)
+
+    def apply_dot(self, p, ap, ny, nx, w, part, scal, slot):
+        self.N.check(self.N.lib.kc_strip_apply_dot(self._p(p, HALO), self._p(ap, HALO), ny, nx, p.shape[1], self._w(w),
+                                                   part.data_ptr(), scal.data_ptr(), slot, self._stream()))
+
+    def dot(self, a, b, ny, nx, part, scal, slot):
+        self.N.check(self.N.lib.kc_strip_dot(self._p(a, HALO), self._p(b, HALO), ny, nx, a.shape[1], part.data_ptr(),
+                                             scal.data_ptr(), slot, self._stream()))
+
+    def pcg_update_xr(self, x, r, p, ap, ny, nx, measure_x, part, scal):
+        self.N.check(self.N.lib.kc_strip_pcg_update_xr(self._p(x, HALO), self._p(r, HALO), self._p(p, HALO),
+                                                       self._p(ap, HALO), ny, nx, x.shape[1], int(measure_x),
+                                                       part.data_ptr(), scal.data_ptr(), self._stream()))
+
+    def pcg_update_p(self, p, z, ny, nx, scal):
+        self.N.check(self.N.lib.kc_strip_pcg_update_p(self._p(p, HALO), self._p(z, HALO), ny, nx, p.shape[1],
+                                                      scal.data_ptr(), self._stream()))
+
+    def residual(self, x, f, r, ny, nx, w):
+        self.N.check(self.N.lib.kc_strip_residual(self._p(x, HALO), self._p(f, HALO), self._p(r, HALO), ny, nx,
+                                                  x.shape[1], self._w(w), self._stream()))
+
+    def copy_if(self, src, dst, ny, nx, scal):
+        self.N.check(self.N.lib.kc_strip_copy_if(self._p(src, HALO), self._p(dst, HALO), ny, nx, src.shape[1],
+                                                 scal.data_ptr(), self._stream()))
+
+    def dist_step(self, kind, scal, hist):
+        self.N.check(self.N.lib.kc_dist_step(kind, scal.data_ptr(), hist.data_ptr(), self._stream()))
 
 
 class CudaCoarse:
@@ -339,6 +376,7 @@ class DistributedKappaSolver:
                            and isinstance(self.coarse, CudaCoarse))
         self._graphs = {}
         self._warm = set()
+        self.graph_fallback = None
         if self._graphs_ok:
             import torch
             self._nrm = torch.zeros(2, dtype=torch.float64, device=self.ops.device)
@@ -501,38 +539,48 @@ class DistributedKappaSolver:
             self._nrm.copy_(t)
 
     def _run(self, k: int, with_norms: bool = False):
-        """One cycle (and optionally the norms of its result): eager on the
-        first call per key, then captured once and replayed as a CUDA graph."""
-        key = (k, with_norms)
+        """One cycle (and optionally the norms of its result)."""
+        self._graphed((k, with_norms), lambda: self._body(k, with_norms))
+
+    def _graphed(self, key, fn):
+        """Run fn(): eager on the first call per key, then captured once into
+        a CUDA graph (CUDA strips, NCCL and the native coarse engine all on
+        torch's stream) and replayed."""
         if self._graphs_ok and key in self._warm:
             g = self._graphs.get(key)
             if g is None:
-                g = self._capture(key)
+                g = self._capture(key, fn)
             if g is not None:
                 g.replay()
                 return
-        self._body(k, with_norms)
+        fn()
         self._warm.add(key)
 
-    def _capture(self, key):
-        """Capture _body(*key) into a CUDA graph; None (eager from then on)
-        when the cycle does not return the strips to their buffer parity (a
-        replayed graph would read the wrong buffers) or cannot be captured."""
+    def _capture(self, key, fn):
+        """Capture fn() into a CUDA graph; None (eager from then on, with a
+        warning and `graph_fallback` set) when it does not return the strips
+        to their buffer parity (a replayed graph would read the wrong buffers)
+        or cannot be captured."""
         import torch
         state0 = self._host_state()
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
+        why = None
         try:
             with torch.cuda.graph(g):
-                self._body(*key)
-        except Exception:  # a backend that cannot be captured: stay eager
-            ok = False
+                fn()
+        except Exception as exc:  # a backend that cannot be captured: stay eager
+            why = f"capture failed: {exc!r}"
         else:
-            ok = self._host_state() == state0
-        if not ok:
+            if self._host_state() != state0:
+                why = "the captured work does not return the strips to their buffer parity"
+        if why is not None:
             for st, (cur, vz) in zip(self.strips, state0):
                 st.cur, st.vzero = cur, vz
             self._graphs_ok = False
+            self.graph_fallback = why
+            import warnings
+            warnings.warn(f"distributed solver: CUDA graphs off, running eagerly ({why})")
             return None
         self._graphs[key] = g
         return g
@@ -558,43 +606,220 @@ class DistributedKappaSolver:
         s.v[s.cur].copy_(self._snap)
         s.vzero = False
 
+    # -- device-side loops -------------------------------------------------
+    def _ds_buffers(self, hist_len: int):
+        """Scalars (KC_DS_* slots), reduction scratch and the history, once per
+        solver (the history grows when a longer loop asks for it)."""
+        if getattr(self, "_scal", None) is None:
+            self._scal = self.ops.vector(DS_SLOTS)
+            self._part = self.ops.vector(DS_PART)
+        if getattr(self, "_hist", None) is None or self._hist.numel() < hist_len:
+            self._hist = self.ops.vector(hist_len)
+        return self._scal, self._part, self._hist
+
+    def _allreduce_slots(self, scal, a: int, b: int):
+        """Allreduce scal[a:b] in place (a contiguous view: one NCCL call)."""
+        self.comm.allreduce_sum(scal[a:b])
+
+    def _read_scalars(self, scal) -> list[float]:
+        return [float(v) for v in scal.cpu().tolist()]
+
+    def _scatter(self, t, full):
+        """Own rows of a global finest-level host array into strip tensor t."""
+        s = self.strips[0]
+        rows = np.asarray(full, dtype=np.float64)[s.a:s.b]
+        host = np.zeros((s.ny, t.shape[1]))
+        host[:, KC_OX:KC_OX + s.m] = rows
+        t[HALO:HALO + s.ny].copy_(self.ops.torch.from_numpy(host) if hasattr(self.ops, "torch") else host)
+
+    def _gather(self, t) -> np.ndarray:
+        s = self.strips[0]
+        maxrows = max(b - a for a, b in self.plan.rows[0])
+        buf = self.ops.zeros(maxrows, t.shape[1])
+        buf[:s.ny].copy_(t[HALO:HALO + s.ny])
+        parts = self.comm.allgather(buf)
+        out = np.empty((s.m, s.m))
+        for r, (a, b) in enumerate(self.plan.rows[0]):
+            out[a:b] = parts[r][:b - a, KC_OX:KC_OX + s.m].cpu().numpy()
+        return out
+
+    def _precondition(self, k: int):
+        """z = M r (krylov.py:81-86): one kappa-cycle from the zero guess on
+        f = r, which lives in the finest strip's f; z is the finest v."""
+        s = self.strips[0]
+        self._halo(s, s.f, HALO)
+        s.vzero = True
+        self._cycle(1, k)
+        self._materialize(s)
+        return s.v[s.cur]
+
     def solve_standalone(self, target_reduction=1e8, max_cycles=10000, initial_guess=None, stop="error",
-                         resident=False):
-        """Distributed solve_standalone (cycle.py:303-366); every rank returns the same report.
-        resident=True solves from the finest v/f already on the devices."""
+                         resident=False, batch: int = 8, kappa=None):
+        """Distributed solve_standalone (cycle.py:303-366); every rank returns
+        the same report.  The stopping test runs on the device (KC_DS_SOLVE:
+        the reference's target, growth-streak and max_cycles rules): a batch
+        of `batch` cycles + norms + step is one graph replay and the host
+        reads the done flag once per batch; cycles a batch runs past the stop
+        are discarded (the iterate at the stop is saved on the device).
+        resident=True solves from the finest v/f already on the devices;
+        kappa overrides the config's cycle counter."""
+        if target_reduction <= 1.0:
+            raise ValueError(f"target reduction must exceed 1, got {target_reduction}")
+        if stop not in ("error", "residual"):
+            raise ValueError(f"stop must be 'error' or 'residual', got {stop!r}")
         m = self.plan.side(1)
+        s = self.strips[0]
         if not resident:
             v0 = (np.random.default_rng(self.problem.seed).random((m, m)) if initial_guess is None
                   else np.asarray(initial_guess, dtype=np.float64))
             self.set_level1("v", v0)
             self.set_level1("f", np.zeros((m, m)))
+        self._materialize(s)
+        scal, part, hist = self._ds_buffers(2 * (max_cycles + 1))
+        if getattr(self, "_sol", None) is None:
+            self._sol = self.ops.zeros(s.ny + 2 * HALO, s.f.shape[1])
+        scal.zero_()
+        init = np.zeros(DS_SLOTS)
+        init[DS["MAXIT"]] = max_cycles
+        init[DS["STOP_RESIDUAL"]] = 1.0 if stop == "residual" else 0.0
+        init[DS["REDUCTION"]] = target_reduction
+        scal.copy_(self.ops.torch.from_numpy(init))
+        k = self.config.effective_kappa if kappa is None else min(self.n, int(kappa) if kappa != math.inf else self.n)
+        e2 = DS["E2"]
+
+        def norms_step():
+            self._halo(s, s.v[s.cur], 1)
+            self.ops.norms(s.v[s.cur], s.f, s.ny, s.m, self.w[0], out=scal[e2:e2 + 2])
+            self._allreduce_slots(scal, e2, e2 + 2)
+            self.ops.dist_step(DS_SOLVE, scal, hist)
+            self.ops.copy_if(s.v[s.cur], self._sol, s.ny, s.m, scal)
+
+        def body():
+            for _ in range(batch):
+                self._cycle(1, k)
+                norms_step()
+
         stats = CycleStats.for_levels(self.n)
         t0 = time.perf_counter()
-        e, r = self.norms()
-        err, res = [e], [r]
-        meas = err if stop == "error" else res
-        target = meas[0] / target_reduction
-        status, it, streak = "max_cycles", 0, 0
-        if meas[0] <= target:
+        norms_step()  # cycle 0: the initial norms and target (cycle.py:333-341)
+        done = self._read_scalars(scal)[DS["DONE"]] != 0.0
+        while not done:
+            self._graphed(("solve", k, batch, stop, hist.data_ptr()), body)
+            done = self._read_scalars(scal)[DS["DONE"]] != 0.0
+        sc = self._read_scalars(scal)
+        it = int(sc[DS["IT"]])
+        status = STATUS_NAMES[int(sc[DS["STATUS"]])]
+        h = hist[: 2 * (it + 1)].cpu().numpy().reshape(-1, 2)
+        wall_ms = 1e3 * (time.perf_counter() - t0)
+        s.v[s.cur].copy_(self._sol)  # the iterate at the stop
+        if it:
+            if k not in self._stats_cache:
+                st = CycleStats.for_levels(self.n)
+                kappa_cycle(DryState(self.n, self.nu1, self.nu2), 1, k, st)
+                self._stats_cache[k] = st
+            stats.absorb(self._stats_cache[k], it)
+        return {"status": status, "iterations": it, "err_hist": h[:, 0].tolist(), "res_hist": h[:, 1].tolist(),
+                "stats": stats, "wall_ms": wall_ms}
+
+    def pcg_solve(self, f, x0=None, target_reduction=1e8, max_iterations=10000, stop="residual", batch: int = 4,
+                  kappa=None, resident: bool = False, gather: bool = True):
+        """Distributed pcg_solve (krylov.py:60-141) preconditioned by one
+        distributed kappa-cycle (krylov.py:81-86); every rank passes the same
+        host f / x0 and returns the same report.  Dot products are per-rank
+        partial sums + an in-place allreduce (NCCL): p.Ap, the stop measure
+        and r.z -- three per iteration.  alpha, beta, the breakdown and stop
+        tests run on the device (KC_DS_PCG_*), so `batch` iterations are one
+        graph replay with one host read of the done flag; iterations a batch
+        runs past the stop leave x, r, p untouched.  resident=True reuses the
+        f and x0 a previous call uploaded (kept on the devices; repeat solves
+        without host traffic); gather=False skips collecting the solution."""
+        if target_reduction <= 1.0:
+            raise ValueError(f"target reduction must exceed 1, got {target_reduction}")
+        if stop not in ("error", "residual"):
+            raise ValueError(f"stop must be 'error' or 'residual', got {stop!r}")
+        m = self.plan.side(1)
+        s = self.strips[0]
+        ops = self.ops
+        if getattr(self, "_pcgv", None) is None:
+            shape = (s.ny + 2 * HALO, s.f.shape[1])
+            self._pcgv = {name: ops.zeros(*shape) for name in ("x", "p", "ap", "b", "x0")}
+        V = self._pcgv
+        scal, part, hist = self._ds_buffers(max_iterations + 1)
+        measure_x = stop == "error"
+        if not resident:
+            self._scatter(V["b"], f)
+            self._scatter(V["x0"], np.zeros((m, m)) if x0 is None else x0)
+        V["x"].copy_(V["x0"])
+        self._halo(s, V["x"], 1)
+        ops.residual(V["x"], V["b"], s.f, s.ny, s.m, self.w[0])  # r = f - A x, kept in the finest f
+        scal.zero_()
+        meas = DS["MEAS"]
+        a, b = (V["x"], V["x"]) if measure_x else (s.f, s.f)
+        ops.dot(a, b, s.ny, s.m, part, scal, meas)
+        self._allreduce_slots(scal, meas, meas + 1)
+        stats = CycleStats.for_levels(self.n)
+        k = self.config.effective_kappa if kappa is None else min(self.n, int(kappa) if kappa != math.inf else self.n)
+        t0 = time.perf_counter()
+        norm0 = math.sqrt(self._read_scalars(scal)[meas])
+        target = norm0 / target_reduction
+        init = np.zeros(DS_SLOTS)
+        init[DS["TARGET"]], init[DS["MAXIT"]] = target, max_iterations
+        scal.copy_(ops.torch.from_numpy(init))
+        hist[:1].fill_(norm0)
+        napp = 0
+        status, it = "max_cycles", 0
+        if norm0 <= target:
             status = "converged"
         else:
-            k = self.config.effective_kappa
-            for it in range(1, max_cycles + 1):
-                if self._graphs_ok:  # cycle + norms as one graph, one host read
-                    self.cycle(k, stats=stats, with_norms=True)
-                    e2, r2 = self._nrm.tolist()
-                    e, r = math.sqrt(e2), math.sqrt(r2)
-                else:
-                    self.cycle(stats=stats)
-                    e, r = self.norms()
-                err.append(e)
-                res.append(r)
-                if meas[-1] <= target:
-                    status = "converged"
-                    break
-                streak = streak + 1 if meas[-1] > meas[-2] else 0
-                if streak >= 5:
-                    status = "diverged"
-                    break
-        return {"status": status, "iterations": it, "err_hist": err, "res_hist": res, "stats": stats,
-                "wall_ms": 1e3 * (time.perf_counter() - t0)}
+            z = self._precondition(k)
+            napp += 1
+            ops.dot(s.f, z, s.ny, s.m, part, scal, DS["RZN"])
+            self._allreduce_slots(scal, DS["RZN"], DS["RZN"] + 1)
+            ops.dist_step(DS_PCG_RZ0, scal, hist)
+            V["p"].copy_(z)
+            sc = self._read_scalars(scal)
+            if sc[DS["DONE"]] != 0.0:
+                status = STATUS_NAMES[int(sc[DS["STATUS"]])]
+            elif max_iterations > 0:
+                rzn = DS["RZN"]
+
+                def iteration():
+                    self._halo(s, V["p"], 1)
+                    ops.apply_dot(V["p"], V["ap"], s.ny, s.m, self.w[0], part, scal, DS["PAP"])
+                    self._allreduce_slots(scal, DS["PAP"], DS["PAP"] + 1)
+                    ops.dist_step(DS_PCG_PAP, scal, hist)
+                    ops.pcg_update_xr(V["x"], s.f, V["p"], V["ap"], s.ny, s.m, measure_x, part, scal)
+                    self._allreduce_slots(scal, meas, meas + 1)
+                    ops.dist_step(DS_PCG_MEAS, scal, hist)
+                    zz = self._precondition(k)
+                    ops.dot(s.f, zz, s.ny, s.m, part, scal, rzn)
+                    self._allreduce_slots(scal, rzn, rzn + 1)
+                    ops.dist_step(DS_PCG_RZ, scal, hist)
+                    ops.pcg_update_p(V["p"], zz, s.ny, s.m, scal)
+
+                def body():
+                    for _ in range(batch):
+                        iteration()
+
+                done = False
+                while not done:
+                    self._graphed(("pcg", k, batch, measure_x, hist.data_ptr()), body)
+                    done = self._read_scalars(scal)[DS["DONE"]] != 0.0
+                sc = self._read_scalars(scal)
+                it = int(sc[DS["IT"]])
+                status = STATUS_NAMES[int(sc[DS["STATUS"]])]
+                # applications that counted: one per iteration that reached its z = M r
+                napp += it if status != "converged" and not (status == "breakdown" and
+                                                              math.isnan(float(hist[it]))) else it - 1
+        wall_ms = 1e3 * (time.perf_counter() - t0)
+        hv = hist[: it + 1].cpu().numpy().tolist()
+        if status == "breakdown" and it > 0 and math.isnan(hv[it]):
+            hv = hv[:it]  # a p.Ap breakdown took no measure at that step
+        if napp:
+            if k not in self._stats_cache:
+                st = CycleStats.for_levels(self.n)
+                kappa_cycle(DryState(self.n, self.nu1, self.nu2), 1, k, st)
+                self._stats_cache[k] = st
+            stats.absorb(self._stats_cache[k], napp)
+        return {"status": status, "iterations": it, "hist": hv, "stats": stats, "wall_ms": wall_ms,
+                "solution": self._gather(V["x"]) if gather else None, "preconditioner_applications": napp}

@@ -107,3 +107,140 @@ class NumpyCoarse:
 
     def get_v(self, full):
         full.numpy()[HALO:HALO + self.m, KC_OX:KC_OX + self.m] = self.h.v[0]
+
+
+# ---------------------------------------------------------------------------
+# device-side loop ops (kc_dist.cuh) restated in numpy, same slot layout
+# ---------------------------------------------------------------------------
+from paper_2010_00626_b200._native import DS, DS_PCG_MEAS, DS_PCG_PAP, DS_PCG_RZ, DS_PCG_RZ0, DS_SOLVE  # noqa: E402
+
+_BREAKDOWN, _CONVERGED, _DIVERGED, _MAX = 3, 0, 1, 2
+
+
+def _loop_ops(cls):
+    def vector(self, n):
+        return torch.zeros(n, dtype=torch.float64)
+
+    def _own(self, t, ny, nx):
+        return self._view(t, 0, ny, 0, nx)
+
+    def apply_dot(self, p, ap, ny, nx, w, part, scal, slot):
+        if scal[DS["DONE"]] != 0:
+            return
+        w = np.asarray(w).reshape(3, 3)
+        a = _acc(w, self._view(p, -1, ny + 1, -1, nx + 1), ny, nx)
+        self._own(ap, ny, nx)[...] = a
+        scal[slot] = float(np.sum(self._own(p, ny, nx) * a))
+
+    def dot(self, a, b, ny, nx, part, scal, slot):
+        if scal[DS["DONE"]] != 0:
+            return
+        scal[slot] = float(np.sum(self._own(a, ny, nx) * self._own(b, ny, nx)))
+
+    def pcg_update_xr(self, x, r, p, ap, ny, nx, measure_x, part, scal):
+        if scal[DS["DONE"]] != 0:
+            return
+        alpha = float(scal[DS["ALPHA"]])
+        xv, rv = self._own(x, ny, nx), self._own(r, ny, nx)
+        xv[...] = xv + alpha * self._own(p, ny, nx)
+        rv[...] = rv - alpha * self._own(ap, ny, nx)
+        v = xv if measure_x else rv
+        scal[DS["MEAS"]] = float(np.sum(v * v))
+
+    def pcg_update_p(self, p, z, ny, nx, scal):
+        if scal[DS["DONE"]] != 0:
+            return
+        beta = float(scal[DS["BETA"]])
+        pv = self._own(p, ny, nx)
+        pv[...] = self._own(z, ny, nx) + beta * pv
+
+    def residual(self, x, f, r, ny, nx, w):
+        w = np.asarray(w).reshape(3, 3)
+        self._own(r, ny, nx)[...] = self._own(f, ny, nx) - _acc(w, self._view(x, -1, ny + 1, -1, nx + 1), ny, nx)
+
+    def copy_if(self, src, dst, ny, nx, scal):
+        if scal[DS["JUST_DONE"]] != 0:
+            self._own(dst, ny, nx)[...] = self._own(src, ny, nx)
+
+    def dist_step(self, kind, scal, hist):
+        """The reference's scalar decisions (the CUDA k_dist_step, restated)."""
+        sc = scal.numpy()
+        h = hist.numpy()
+        was_done = sc[DS["DONE"]] != 0
+        sc[DS["JUST_DONE"]] = 0.0
+        if was_done:
+            return
+
+        def finish(status):
+            sc[DS["STATUS"]], sc[DS["DONE"]], sc[DS["JUST_DONE"]] = status, 1.0, 1.0
+
+        if kind == DS_PCG_RZ0:
+            if not sc[DS["RZN"]] > 0.0:
+                finish(_BREAKDOWN)
+            else:
+                sc[DS["RZ"]] = sc[DS["RZN"]]
+        elif kind == DS_PCG_PAP:
+            it = int(sc[DS["IT"]]) + 1
+            sc[DS["IT"]] = it
+            if not sc[DS["PAP"]] > 0.0:
+                h[it] = np.nan
+                finish(_BREAKDOWN)
+            else:
+                sc[DS["ALPHA"]] = sc[DS["RZ"]] / sc[DS["PAP"]]
+        elif kind == DS_PCG_MEAS:
+            it = int(sc[DS["IT"]])
+            cur = float(np.sqrt(sc[DS["MEAS"]]))
+            h[it] = cur
+            if cur <= sc[DS["TARGET"]]:
+                finish(_CONVERGED)
+        elif kind == DS_PCG_RZ:
+            rzn = sc[DS["RZN"]]
+            if not rzn > 0.0:
+                finish(_BREAKDOWN)
+            elif int(sc[DS["IT"]]) >= int(sc[DS["MAXIT"]]):
+                finish(_MAX)
+            else:
+                sc[DS["BETA"]] = rzn / sc[DS["RZ"]]
+                sc[DS["RZ"]] = rzn
+        elif kind == DS_SOLVE:
+            it = int(sc[DS["IT"]])
+            e, r = float(np.sqrt(sc[DS["E2"]])), float(np.sqrt(sc[DS["R2"]]))
+            h[2 * it], h[2 * it + 1] = e, r
+            cur = r if sc[DS["STOP_RESIDUAL"]] != 0 else e
+            if it == 0:
+                sc[DS["TARGET"]] = cur / sc[DS["REDUCTION"]]
+            if cur <= sc[DS["TARGET"]]:
+                finish(_CONVERGED)
+            elif it > 0:
+                streak = sc[DS["STREAK"]] + 1.0 if cur > sc[DS["PREV"]] else 0.0
+                sc[DS["STREAK"]] = streak
+                if streak >= 5.0:
+                    finish(_DIVERGED)
+            sc[DS["PREV"]] = cur
+            if sc[DS["DONE"]] == 0:
+                if it >= int(sc[DS["MAXIT"]]):
+                    finish(_MAX)
+                else:
+                    sc[DS["IT"]] = it + 1
+
+    for fn in (vector, _own, apply_dot, dot, pcg_update_xr, pcg_update_p, residual, copy_if, dist_step):
+        setattr(cls, fn.__name__, fn)
+    return cls
+
+
+_loop_ops(NumpyStripOps)
+
+
+def _norms_out(self, v, f, ny, nx, w, out=None):
+    w = np.asarray(w).reshape(3, 3)
+    up = self._view(v, -1, ny + 1, -1, nx + 1)
+    r = self._view(f, 0, ny, 0, nx) - _acc(w, up, ny, nx)
+    vv = up[1:-1, 1:-1]
+    val = torch.tensor([float(np.sum(vv * vv)), float(np.sum(r * r))], dtype=torch.float64)
+    if out is None:
+        return val
+    out.copy_(val)
+    return out
+
+
+NumpyStripOps.norms = _norms_out

@@ -195,3 +195,153 @@ def test_gloo_two_ranks_bit_exact():
     for rank, got, e, r in res:
         assert np.array_equal(got, h.v[0]), rank
         assert e == pytest.approx(e_ref, rel=1e-13) and r == pytest.approx(r_ref, rel=1e-13)
+
+
+# ---------------------------------------------------------------------------
+# distributed PCG and the device-side (batched) stop loops (kc_dist.cuh logic)
+# ---------------------------------------------------------------------------
+
+def _golden_pcg(n, kname):
+    import json
+    with open(os.path.join(os.path.dirname(__file__), "golden", "solves_small.json")) as fh:
+        return json.load(fh)["pcg"][f"n{n}_k{kname}"]
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+@pytest.mark.parametrize("kname,stop,tgt", [("1", "error", 1e8), ("2", "residual", 1e10), ("3", "error", 1e10),
+                                            ("W", "residual", 1e10)])
+def test_thread_ranks_pcg_counts_vs_reference(world, kname, stop, tgt):
+    """Distributed pcg_solve (3 allreduced dots per iteration, alpha / beta /
+    stop on the 'device' scalars) against the REAL reference's counts and
+    histories (tests/golden/solves_small.json, made by make_golden.py)."""
+    from conftest import check_pcg_hist
+    n = 5
+    g = _golden_pcg(n, kname)
+    kappa = n if kname == "W" else int(kname)
+    m = 2 ** n - 1
+    x0 = np.random.default_rng(0).random((m, m))
+    key = {("error", 1e8): "error_1e8", ("error", 1e10): "error_1e10", ("residual", 1e10): "residual_1e10"}[(stop, tgt)]
+
+    def fn(comm):
+        s = _solver(comm, n, kappa, 1e-4, 45.0, min_rows=4)
+        return s.pcg_solve(np.zeros((m, m)), x0=x0, target_reduction=tgt, stop=stop, batch=3)
+
+    for rep in _run_threads(world, fn):
+        assert rep["status"] == "converged"
+        assert rep["iterations"] == g["iters"][key]
+        check_pcg_hist(rep["hist"], g["x_hist" if stop == "error" else "r_hist"])
+        ref_rep = g["reference_reports"].get(key)
+        if ref_rep is not None:
+            assert rep["stats"].visits == ref_rep["visits"]
+
+
+def test_thread_ranks_pcg_general_rhs_and_max_iterations():
+    n, kappa, m = 5, 2, 31
+    f = np.random.default_rng(12).random((m, m))
+    ref = O.pcg(1e-4, 45.0, n, kappa, target=1e10, stop="residual", x0=np.zeros((m, m)), f=f)
+
+    def fn(comm):
+        s = _solver(comm, n, kappa, 1e-4, 45.0, min_rows=4)
+        a = s.pcg_solve(f, target_reduction=1e10, stop="residual", batch=4)
+        b = s.pcg_solve(f, target_reduction=1e10, stop="residual", max_iterations=3, batch=2)
+        return a, b
+
+    for a, b in _run_threads(2, fn):
+        assert a["status"] == ref["status"] and a["iterations"] == ref["iterations"]
+        assert np.allclose(a["solution"], ref["solution"], rtol=0, atol=1e-12 * np.max(np.abs(ref["solution"])))
+        assert b["status"] == "max_cycles" and b["iterations"] == 3 and len(b["hist"]) == 4
+        assert b["preconditioner_applications"] == 4  # the initial one + one per iteration
+
+
+@pytest.mark.parametrize("batch", [1, 3, 8])
+def test_thread_ranks_device_stop_loop_batches(batch):
+    """The batched stand-alone loop: the stop fires inside a batch, the extra
+    cycles are discarded, and the report (count, histories, solution) is the
+    reference loop's, whatever the batch."""
+    n, eps, phi, kappa = 6, 1e-4, 45.0, 3
+    ref = O.standalone(eps, phi, n, kappa, target=1e8, stop="error")
+
+    def fn(comm):
+        s = _solver(comm, n, kappa, eps, phi, min_rows=4)
+        rep = s.solve_standalone(1e8, max_cycles=500, stop="error", batch=batch)
+        rep["solution"] = s.gather_level1()
+        return rep
+
+    for rep in _run_threads(2, fn):
+        assert rep["status"] == ref["status"] == "converged"
+        assert rep["iterations"] == ref["iterations"]
+        ee = np.asarray(ref["err_hist"])
+        assert len(rep["err_hist"]) == len(ee)
+        assert np.max(np.abs(np.asarray(rep["err_hist"]) - ee) / ee) < 1e-12
+        assert np.array_equal(rep["solution"], ref["solution"])
+
+
+def test_thread_ranks_device_stop_max_cycles_and_divergence():
+    n, kappa = 5, 2
+    ref = O.standalone(1e-4, 45.0, n, kappa, target=1e10, max_cycles=7, stop="residual")
+
+    def fn(comm):
+        s = _solver(comm, n, kappa, 1e-4, 45.0, min_rows=4)
+        return s.solve_standalone(1e10, max_cycles=7, stop="residual", batch=4)
+
+    for rep in _run_threads(2, fn):
+        assert rep["status"] == "max_cycles" and rep["iterations"] == 7 == ref["iterations"]
+    # pure coarse-grid correction without smoothing never converges (test_cycle.py:225-233)
+    ref = O.standalone(1.0, 0.0, 2, 1, target=1e8, max_cycles=40, seed=1, nu1=0, nu2=0)
+
+    def fn2(comm):
+        s = _solver(comm, 2, 1, 1.0, 0.0, nu1=0, nu2=0, min_rows=1)
+        s.problem = ProblemSpec(1.0, 0.0, seed=1)
+        return s.solve_standalone(1e8, max_cycles=40, batch=8)
+
+    for rep in _run_threads(1, fn2):
+        assert rep["status"] == ref["status"] and rep["iterations"] == ref["iterations"]
+
+
+def _gloo_pcg_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2010_00626_b200.distributed import TorchComm
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, kappa = 5, 2
+        m = 2 ** n - 1
+        x0 = np.random.default_rng(0).random((m, m))
+        s = _solver(TorchComm(), n, kappa, 1e-4, 45.0, min_rows=4)
+        rep = s.pcg_solve(np.zeros((m, m)), x0=x0, target_reduction=1e10, stop="residual", batch=4)
+        sol = s.solve_standalone(1e8, max_cycles=500, stop="residual", batch=5)
+        q.put((rank, rep["iterations"], rep["status"], rep["hist"], sol["iterations"], sol["status"]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_pcg_and_device_stop():
+    """world_size-2 torch.distributed/gloo processes: distributed PCG counts
+    and histories equal the reference's; the batched stand-alone loop's
+    count equals the oracle's."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from conftest import check_pcg_hist
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_pcg_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = _golden_pcg(5, "2")
+    for rank, it, status, hist, sit, sst in res:
+        assert status == "converged" and it == g["iters"]["residual_1e10"]
+        check_pcg_hist(hist, g["r_hist"])
+        assert sst == "converged"
+    n5 = O.standalone(1e-4, 45.0, 5, 2, target=1e8, stop="residual")
+    assert all(r[4] == n5["iterations"] for r in res), (res[0][4], n5["iterations"])
