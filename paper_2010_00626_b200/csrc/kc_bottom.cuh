@@ -93,7 +93,38 @@ struct BotParams {
   int nstrip;        // leading levels split into row strips over the cluster (0: single CTA)
   int total;         // shared-memory doubles of all levels (bot_smem_doubles)
   BotLv lv[KC_BOT_MAXLEV];  // bot_geometry (rank 0's strip rows)
+  // side-15 frame operators (KC_FAST cluster launches; see "Frame operators"
+  // below): blocks (kap - 1) * 2 + part of [A_kap | B_kap], 225 x KC_MV_LD
+  // rows in global memory; the blocks this launch uses (mv_copy, a subset
+  // of the handle's resident set) are copied row-sliced into every CTA's
+  // shared memory at mv_off, slot mv_slot[block].  mv_d: the side-15 level,
+  // replicated in every CTA when mv_rep (0: frame operators off).
+  const double* mv_mats;
+  int mv_copy, mv_off, mv_rows, mv_d, mv_rep, mv_xin;  // mv_xin: 2 x 225 doubles of packed inputs
+  int mv_slot[6];
 };
+
+// Frame operators (FMA build, cluster launches only).  A kappa_cycle frame on
+// the side-15 level (with its 7^2, 3^2 and 1x1 children; BotTiny below) is a
+// LINEAR map of its inputs: v_out = A_k v_in + B_k f (v_in = 0 on a zero
+// guess), A_k, B_k fixed 225 x 225 matrices for frame counter k (k >= 3 is
+// the W frame at this depth: kappa_cycle(15, k) recurses into 7^2 with
+// counters k, k - 1 >= 2, which are W there).  The engine builds the columns
+// on the device by running the very same frame code on unit inputs
+// (k_tiny_mats), each CTA of the 16-CTA cluster keeps a row slice of the
+// needed blocks in its shared memory, and a frame becomes one cluster-wide
+// matrix-vector phase (bot_mv_frame): ~2 k cycles instead of the ~10-12 k
+// of 30+ barrier-separated tiny phases on CTA 0.  The side-15 level itself
+// is then REPLICATED in every CTA: the restriction into it and the frame
+// outputs are stored into all CTAs (each CTA produces a slice), so a frame
+// reads its inputs and the prolongation out of it reads v locally -- no CTA
+// serves everybody's remote loads.  A frame whose blocks are not resident
+// runs the interpreter on CTA 0 and PH_BCAST then copies its result out.  The product rounds
+// differently from the frame's own operation sequence, so this is FAST-only
+// (the exact build keeps the frames); parity bar as for the FMA build.
+#define KC_MV_M 15
+#define KC_MV_N (KC_MV_M * KC_MV_M)  // 225 unknowns of a side-15 level
+#define KC_MV_LD 226                 // row stride (16-byte multiple: cp.async)
 
 // smem geometry of level d (entry side m0): side m_d = ((m0+1) >> d) - 1,
 // stride S = m+2, three arrays v0, v1, f of (rows+2) x S, rows = m, or the
@@ -194,7 +225,8 @@ __device__ __forceinline__ void kc_bot_mark(int k) {
 // were measured slower -- larger kernel, longer dependent chains -- and the
 // tiny frames replaced them.)
 enum BotOp {
-  PH_JACOBI = 0, PH_RESID = 1, PH_RESTRICT = 2, PH_PROLONG = 3, PH_JOIN = 4, PH_J2Z = 5, PH_TINY = 8, PH_CSYNC = 9
+  PH_JACOBI = 0, PH_RESID = 1, PH_RESTRICT = 2, PH_PROLONG = 3, PH_JOIN = 4, PH_J2Z = 5, PH_TINY = 8, PH_CSYNC = 9,
+  PH_BCAST = 10  // every CTA copies CTA 0's side-15 v (buffer src) into its replica
 };
 #ifndef KC_BOT_TINY_M
 #define KC_BOT_TINY_M 15  // frames on sides <= this run as PH_TINY (side 15 on 8 warps)
@@ -235,6 +267,8 @@ struct BotBuilder {  // host side
   bool fuse = true;         // emit PH_J2Z
   bool tiny = true;         // whole frames on sides <= KC_BOT_TINY_M as PH_TINY
   bool dry = false;         // track buffers only (inside a PH_TINY frame)
+  unsigned mv_mask = 0;     // resident frame-operator blocks (0: frame operators off)
+  unsigned mv_used = 0;     // blocks the emitted frames use (BotParams::mv_copy)
   std::vector<unsigned> out;
   void emit(int op, int d, int src, int zero, int cbuf, int cc, int kap = 0) {
     if (dry) return;
@@ -265,6 +299,33 @@ struct BotBuilder {  // host side
     }
   }
   void rec(int d, int kap) {
+    if (mv_mask && !dry && d >= nstrip && bot_m(m0, d) == KC_MV_M && d < nlev - 1) {
+      // frame operator: one cluster-wide phase (all CTAs, like a strip
+      // phase), output into the other buffer; children are scratch
+      const int k3 = kap < 3 ? kap : 3;
+      const int z = (vz >> d) & 1u;
+      const unsigned need = (1u << ((k3 - 1) * 2 + 1)) | (z ? 0u : (1u << ((k3 - 1) * 2)));
+      if ((mv_mask & need) == need) {
+        if (local_run) out.push_back(bot_desc(PH_CSYNC, 0, 0, 0, 0, 0, KC_BOT_WARPS));
+        local_run = false;
+        gprev = KC_BOT_WARPS;
+        out.push_back(bot_desc(PH_TINY, d, (cur >> d) & 1u, z, 0, 0, KC_BOT_WARPS, k3) | BD_STRIP_BIT);
+        mv_used |= need;
+        cur ^= 1u << d;
+        vz &= ~(1u << d);
+        return;
+      }
+      // interpreter frame on CTA 0, then its result into every replica
+      emit(PH_TINY, d, (cur >> d) & 1u, (vz >> d) & 1u, 0, 0, kap);
+      dry = true;
+      rec(d, kap);
+      dry = false;
+      out.push_back(bot_desc(PH_CSYNC, 0, 0, 0, 0, 0, KC_BOT_WARPS));
+      out.push_back(bot_desc(PH_BCAST, d, (cur >> d) & 1u, 0, 0, 0, KC_BOT_WARPS) | BD_STRIP_BIT);
+      local_run = false;
+      gprev = KC_BOT_WARPS;
+      return;
+    }
     if (tiny && fuse && !dry && d >= nstrip && bot_m(m0, d) <= KC_BOT_TINY_M && d < nlev - 1 && kap <= 15) {
       // one descriptor; bot_tiny follows the rules below (J2Z on), so
       // replay them dry to track the buffers of level d
@@ -439,6 +500,23 @@ __device__ __forceinline__ void bot_restrict(const double* __restrict__ r, const
     const double fv = kc_fw(rs[-1], rs[0], rs[1], rc[-1], rc[0], rc[1], rn[-1], rn[0], rn[1]);
     ps.put(fc, SC, q, p, fv);
     if (cc) vc[0] = __ddiv_rn(fv, ccenter);
+  }
+}
+
+// The same restriction into a level replicated in every CTA (the side-15
+// level under frame operators): each value goes to all cs CTAs' copies.
+__device__ __forceinline__ void bot_restrict_bcast(const double* __restrict__ r, const BotLv& L, double* fc, int mc,
+                                                   int SC, int tid, int nth, int cs) {
+  cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+  const int S = L.S;
+  const int n = L.crows * mc;
+  for (int i = tid; i < n; i += nth) {
+    const int q = bot_div(i, L.invc), p = i - q * mc;
+    const double* rc = r + (2 * q + 1) * S + (2 * p + 1);
+    const double* rs = rc - S;
+    const double* rn = rc + S;
+    const double fv = kc_fw(rs[-1], rs[0], rs[1], rc[-1], rc[0], rc[1], rn[-1], rn[0], rn[1]);
+    for (int k = 0; k < cs; ++k) *cl.map_shared_rank(fc + q * SC + p, k) = fv;
   }
 }
 
@@ -660,6 +738,91 @@ struct BotTiny {
   }
 };
 
+// One frame operator phase on every CTA of the cluster: this CTA's rows
+// i in [rank * R, rank * R + R) of v' = A_k v + B_k f (the A part skipped on
+// a zero guess), inputs gathered from CTA 0's side-15 level, outputs stored
+// into CTA 0's other v buffer (so no CTA overwrites an input another CTA may
+// still read); the caller ends the phase with a cluster barrier.
+__device__ __forceinline__ void bot_mv_frame(double* sm, const BotParams& bp, const BotLv& L, int src, bool zero,
+                                             int kap, int rank, int cs) {
+  cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+  const int R = bp.mv_rows;
+  asm volatile("cp.async.wait_all;" ::: "memory");  // the blocks (prologue copies)
+  __syncthreads();
+  const double* B = sm + bp.mv_off + bp.mv_slot[(kap - 1) * 2 + 1] * R * KC_MV_LD;
+  const double* A = sm + bp.mv_off + bp.mv_slot[(kap - 1) * 2] * R * KC_MV_LD;
+  const double* vin = sm + (src ? L.vo1 : L.vo0);  // this CTA's replica
+  const double* fin = sm + L.fo;
+  double* xv = sm + bp.mv_xin;  // inputs packed row-major: v (225), f (225)
+  double* xf = xv + KC_MV_N;
+  for (int i = threadIdx.x; i < KC_MV_N; i += KC_BOT_THREADS) {
+    const int y = i / KC_MV_M, o = y * L.S + (i - y * KC_MV_M);
+    xf[i] = fin[o];
+    if (!zero) xv[i] = vin[o];
+  }
+  __syncthreads();
+  double* out = sm + (src ? L.vo0 : L.vo1);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i0 = rank * R;
+  for (int r = warp; r < R && i0 + r < KC_MV_N; r += KC_BOT_WARPS) {
+    const double* br = B + r * KC_MV_LD;
+    const double* ar = A + r * KC_MV_LD;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // independent chains
+#pragma unroll
+    for (int k = 0; k < (KC_MV_N + 31) / 32; ++k) {
+      const int j = lane + 32 * k;
+      if (j < KC_MV_N) {
+        if (k & 1) a1 = fma(br[j], xf[j], a1);
+        else a0 = fma(br[j], xf[j], a0);
+        if (!zero) {
+          if (k & 1) a3 = fma(ar[j], xv[j], a3);
+          else a2 = fma(ar[j], xv[j], a2);
+        }
+      }
+    }
+    double acc = (a0 + a1) + (a2 + a3);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    // every lane holds the row's value: lane k stores it into CTA k's replica
+    const int i = i0 + r, y = i / KC_MV_M, x = i - y * KC_MV_M;
+    if (lane < cs) *cl.map_shared_rank(out + y * L.S + x, lane) = acc;
+  }
+}
+
+// Columns of the side-15 frame operators: CTA (j, k - 1) runs BotTiny::frame
+// (the bottom kernel's own frame code) with counter k on the unit input j
+// (j < 225: v = e_j; else f = e_(j-225)) and stores v_out as column j of
+// [A_k | B_k].  tp: the 4-level geometry of a side-15 entry.
+__global__ void __launch_bounds__(256) k_tiny_mats(const BotParams tp, double* __restrict__ mats) {
+  extern __shared__ double sm[];
+  __shared__ St9 tab[4];
+  __shared__ BotLv lv[4];
+  __shared__ int child[2];
+  const int j = blockIdx.x, kap = blockIdx.y + 1;
+  for (int i = threadIdx.x; i < tp.total; i += 256) sm[i] = 0.0;
+  if (threadIdx.x < 4) {
+    tab[threadIdx.x] = tp.st[threadIdx.x];
+    lv[threadIdx.x] = tp.lv[threadIdx.x];
+  }
+  __syncthreads();
+  const BotLv L0 = lv[0];
+  if (threadIdx.x == 0) {
+    const int jj = j % KC_MV_N, y = jj / KC_MV_M, x = jj - y * KC_MV_M;
+    sm[(j < KC_MV_N ? L0.vo0 : L0.fo) + y * L0.S + x] = 1.0;
+  }
+  __syncthreads();
+  const BotTiny t{sm, lv, tab, tp.nu1, tp.nu2, (int)threadIdx.x, 256};
+  int cur = 0, vz = 0;
+  t.frame(0, kap, 4, cur, vz, child);
+  __syncthreads();
+  const double* o = sm + (cur ? L0.vo1 : L0.vo0);
+  double* blk = mats + (size_t)((kap - 1) * 2 + (j < KC_MV_N ? 0 : 1)) * KC_MV_N * KC_MV_LD;
+  for (int i = threadIdx.x; i < KC_MV_N; i += 256) {
+    const int y = i / KC_MV_M, x = i - y * KC_MV_M;
+    blk[(size_t)i * KC_MV_LD + j % KC_MV_N] = o[y * L0.S + x];
+  }
+}
+
 __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp, int m0) {
   extern __shared__ double sm[];
   __shared__ St9 tab[KC_BOT_MAXLEV];
@@ -698,6 +861,23 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
     for (int i = l2 + threadIdx.x; i < h2; i += KC_BOT_THREADS) z2[i] = make_double2(0.0, 0.0);
     if ((hi & 1) && hi - 1 >= lo && threadIdx.x == KC_BOT_THREADS - 1) sm[hi - 1] = 0.0;
   };
+  if (bp.mv_copy) {
+    // this CTA's row slice of every resident frame-operator block (constant
+    // data: issued before the dependency wait, so it overlaps the previous
+    // grid; completed by the cp.async.wait_all below or in bot_mv_frame)
+    const int R = bp.mv_rows, i0 = rank * R;
+    const int rows = min(R, KC_MV_N - i0);
+    for (int b = 0; b < 6; ++b) {
+      if (!((bp.mv_copy >> b) & 1) || rows <= 0) continue;
+      const double* src = bp.mv_mats + ((size_t)b * KC_MV_N + i0) * KC_MV_LD;
+      double* dst = sm + bp.mv_off + bp.mv_slot[b] * R * KC_MV_LD;
+      for (int c = threadIdx.x; c < rows * KC_MV_LD / 2; c += KC_BOT_THREADS) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + 2 * c);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src + 2 * c) : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   if (nstrip > 0) {
     // strip entry: own rows plus one halo row each side (rows -1 .. m0
     // exist in HBM, ghost rows zero), ghost columns included; level 0 is
@@ -832,13 +1012,17 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
       double* fc = sm + C.fo;
       double* vc = sm + C.vo0;
       BotPush ps{nullptr, nullptr, -1};
-      if (strip && d + 1 < nstrip) {
-        ps = bot_push(fc, C, true, rank, cs);
-      } else if (strip) {  // into CTA 0's level, at this strip's first coarse row
-        fc = cl.map_shared_rank(fc, 0) + (L.a / 2) * C.S;
-        vc = cl.map_shared_rank(vc, 0);
+      if (strip && bp.mv_rep && d + 1 == bp.mv_d) {  // into every CTA's replica of the side-15 level
+        bot_restrict_bcast(zero ? f : u, L, fc + (L.a / 2) * C.S, C.m, C.S, tid, nth, cs);
+      } else {
+        if (strip && d + 1 < nstrip) {
+          ps = bot_push(fc, C, true, rank, cs);
+        } else if (strip) {  // into CTA 0's level, at this strip's first coarse row
+          fc = cl.map_shared_rank(fc, 0) + (L.a / 2) * C.S;
+          vc = cl.map_shared_rank(vc, 0);
+        }
+        bot_restrict(zero ? f : u, L, fc, C.m, C.S, vc, tab[d + 1].center, BD_CC(e), tid, nth, ps);
       }
-      bot_restrict(zero ? f : u, L, fc, C.m, C.S, vc, tab[d + 1].center, BD_CC(e), tid, nth, ps);
     } else if (op == PH_PROLONG) {
       const BotLv C = lv[d + 1];
       const double* vc = sm + (BD_CBUF(e) ? C.vo1 : C.vo0);
@@ -847,9 +1031,21 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
         __syncthreads();
         continue;
       }
-      if (strip)  // from CTA 0's level, at this strip's first coarse row
+      if (strip && bp.mv_rep && d + 1 == bp.mv_d)  // the local replica of the side-15 level
+        vc += (L.a / 2) * C.S;
+      else if (strip)  // from CTA 0's level, at this strip's first coarse row
         vc = cl.map_shared_rank(const_cast<double*>(vc), 0) + (L.a / 2) * C.S;
       bot_prolong(u, vc, L, C.m, C.S, zero, tid, nth, bot_push(u, L, strip, rank, cs));
+    } else if (op == PH_BCAST) {  // CTA 0's side-15 v (buffer src) into this CTA's replica
+      if (rank != 0) {
+        const double* v0 = cl.map_shared_rank(u, 0);
+        for (int i = tid; i < m * m; i += KC_BOT_THREADS) {
+          const int y = i / m, x = i - y * m;
+          u[y * S + x] = v0[y * S + x];
+        }
+      }
+    } else if (strip) {  // PH_TINY as a frame operator (all CTAs; FMA build)
+      bot_mv_frame(sm, bp, L, src, zero, BD_KAP(e), rank, cs);
     } else {  // PH_TINY (CTA 0: warp 0 for sides <= 7, warps 0-7 for side 15)
       const BotTiny t{sm, lv, tab, bp.nu1, bp.nu2, tid, nth};
       int cur = src, vz = zero;

@@ -132,10 +132,12 @@ struct kc_handle {
   size_t bot_smem = 0;
   int bot_m0 = 0;
   int bot_cs = 1;  // CTAs per bottom launch (thread-block cluster when > 1)
+  double* mv_mats = nullptr;  // side-15 frame operators (FMA build, kc_bottom.cuh)
+  int mv_resident = 0;        // blocks resident in the bottom kernel's shared memory
   double line_w[3] = {0, 0, 0};  // semi-y coarsest line: lower, diag, upper (raw w[1][:])
   bool line_singular = false;
   // host-built bottom phase schedules, keyed by (kappa1, kappa2, v_zero)
-  std::map<std::tuple<int, int, int>, std::tuple<unsigned*, int, int>> bot_sched;
+  std::map<std::tuple<int, int, int>, std::tuple<unsigned*, int, int, int>> bot_sched;  // dev, n, final cur, mv_used
   cudaStream_t stream = nullptr;      // the stream every operation is issued on
   cudaStream_t own_stream = nullptr;  // created by kc_create (kc_set_stream may redirect `stream`)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -501,7 +503,8 @@ int ex_coarsest(kc_handle* h) {
   return KC_OK;
 }
 
-int get_bot_sched(kc_handle* h, int k1, int k2, int vzero, const unsigned** dev, int* n, int* final_cur) {
+int get_bot_sched(kc_handle* h, int k1, int k2, int vzero, const unsigned** dev, int* n, int* final_cur,
+                  int* mv_used) {
   auto key = std::make_tuple(k1, k2, vzero);
   auto it = h->bot_sched.find(key);
   if (it == h->bot_sched.end()) {
@@ -512,6 +515,7 @@ int get_bot_sched(kc_handle* h, int k1, int k2, int vzero, const unsigned** dev,
     b.nu2 = h->nu2;
     b.vz = vzero ? 1u : 0u;
     b.nstrip = h->bot_base.nstrip;
+    b.mv_mask = h->bot_base.mv_rep ? (unsigned)h->mv_resident : 0u;
     if (b.nlev > 1) {
       b.rec(0, k1);
       if (k2 > 0) b.rec(0, k2);
@@ -522,11 +526,90 @@ int get_bot_sched(kc_handle* h, int k1, int k2, int vzero, const unsigned** dev,
     const size_t bytes = sizeof(unsigned) * (b.out.empty() ? 1 : b.out.size());
     KC_CUDA(h, cudaMalloc(&d, bytes));
     if (!b.out.empty()) KC_CUDA(h, cudaMemcpy(d, b.out.data(), sizeof(unsigned) * b.out.size(), cudaMemcpyHostToDevice));
-    it = h->bot_sched.emplace(key, std::make_tuple(d, (int)b.out.size(), (int)(b.cur & 1u))).first;
+    it = h->bot_sched.emplace(key, std::make_tuple(d, (int)b.out.size(), (int)(b.cur & 1u), (int)b.mv_used)).first;
   }
   *dev = std::get<0>(it->second);
   *n = std::get<1>(it->second);
   *final_cur = std::get<2>(it->second);
+  *mv_used = std::get<3>(it->second);
+  return KC_OK;
+}
+
+// k_bottom's dynamic shared-memory limit is a per-function attribute shared
+// by every handle of this library: only ever raise it (a smaller handle
+// created later must not break the launches or graphs of a larger one).
+cudaError_t bot_smem_attr(size_t bytes) {
+  static size_t cur = 0;
+  if (bytes <= cur) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
+
+// Side-15 frame operators of the FMA build (kc_bottom.cuh "Frame operators"):
+// columns computed on the device by k_tiny_mats, then as many blocks made
+// resident in every CTA of the cluster as its shared memory holds, in the
+// order the kappa-cycles use them (B1, B2, A1, B3, A2, A3).  Frames whose
+// blocks are not resident keep the interpreter path.
+int setup_frame_operators(kc_handle* h, const cudaDeviceProp& prop) {
+  BotParams& bp = h->bot_base;
+  int d15 = -1;
+  for (int d = 0; d < bp.nlev; ++d)
+    if (bot_m(h->bot_m0, d) == KC_MV_M) d15 = d;
+  if (d15 < bp.nstrip || d15 + 4 != bp.nlev) return KC_OK;
+  BotParams tp{};
+  tp.nlev = 4;
+  tp.nu1 = h->nu1;
+  tp.nu2 = h->nu2;
+  for (int j = 0; j < 4; ++j) tp.st[j] = bp.st[d15 + j];
+  bot_geometry(tp, KC_MV_M, 1);
+  const size_t mbytes = sizeof(double) * 6 * (size_t)KC_MV_N * KC_MV_LD;
+  KC_CUDA(h, cudaMalloc(&h->mv_mats, mbytes));
+  KC_CUDA(h, cudaMemset(h->mv_mats, 0, mbytes));
+  k_tiny_mats<<<dim3(2 * KC_MV_N, 3), 256, sizeof(double) * tp.total>>>(tp, h->mv_mats);
+  KC_LAUNCH_CHECK(h);
+  KC_CUDA(h, cudaDeviceSynchronize());
+  cudaFuncAttributes fa{};
+  KC_CUDA(h, cudaFuncGetAttributes(&fa, k_bottom));
+  const size_t smem_max = prop.sharedMemPerBlockOptin - fa.sharedSizeBytes;
+  const int R = (KC_MV_N + h->bot_cs - 1) / h->bot_cs;
+  const int off = (bp.total + 1) & ~1;
+  const size_t per = sizeof(double) * (size_t)R * KC_MV_LD;
+  const int order[6] = {1, 3, 0, 5, 2, 4};
+  int mask = 0, nres = 0;
+  for (int b : order) {
+    if (sizeof(double) * (size_t)(off + 2 * KC_MV_N) + per * (size_t)(nres + 1) > smem_max) break;
+    mask |= 1 << b;
+    bp.mv_slot[b] = nres++;
+  }
+  if (!mask) return KC_OK;
+  bp.mv_mats = h->mv_mats;
+  bp.mv_off = off;
+  bp.mv_rows = R;
+  bp.mv_d = d15;
+  bp.mv_xin = off + nres * R * KC_MV_LD;
+  const size_t bytes = sizeof(double) * (size_t)(bp.mv_xin + 2 * KC_MV_N);
+  // the cluster must still fit with the larger shared memory
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(h->bot_cs);
+  cfg.blockDim = dim3(KC_BOT_THREADS);
+  cfg.dynamicSmemBytes = bytes;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = h->bot_cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int ncl = 0;
+  if (bot_smem_attr(bytes) != cudaSuccess || cudaOccupancyMaxActiveClusters(&ncl, k_bottom, &cfg) != cudaSuccess ||
+      ncl < 1) {
+    cudaGetLastError();
+    return KC_OK;  // keep the interpreter frames
+  }
+  bp.mv_rep = 1;
+  h->mv_resident = mask;
+  h->bot_smem = bytes;
   return KC_OK;
 }
 
@@ -537,7 +620,7 @@ int ex_bottom(kc_handle* h, int l, int k1, int k2) {
   bp.gf = L.f;
   bp.gP = L.P;
   bp.v_zero = L.vzero ? 1 : 0;
-  int rc = get_bot_sched(h, k1, k2, bp.v_zero, &bp.sched, &bp.nsched, &bp.final_cur);
+  int rc = get_bot_sched(h, k1, k2, bp.v_zero, &bp.sched, &bp.nsched, &bp.final_cur, &bp.mv_copy);
   if (rc) return rc;
   if (h->L[h->n - 1].st.center == 0.0) KC_FAIL(h, KC_ESINGULAR, "singular coarsest operator");
   if (h->bot_cs > 1) {
@@ -967,9 +1050,9 @@ int get_cycle_graph(kc_handle* h, int kappa, GraphEntry** out, int norms = 0) {
   for (const Op& op : ops)
     if (op.kind == OP_BOTTOM) {
       const unsigned* dv;
-      int nn, fc, rc0;
+      int nn, fc, mu, rc0;
       for (int vz = 0; vz < 2; ++vz)
-        if ((rc0 = get_bot_sched(h, op.a, op.b, vz, &dv, &nn, &fc))) return rc0;
+        if ((rc0 = get_bot_sched(h, op.a, op.b, vz, &dv, &nn, &fc, &mu))) return rc0;
     }
   GraphEntry g;
   const int l0 = h->launches;
@@ -1072,9 +1155,9 @@ int get_solve_graph(kc_handle* h, int kappa, SolveGraph** out) {
   for (const Op& op : ops)
     if (op.kind == OP_BOTTOM) {
       const unsigned* dv;
-      int nn, fc, rc0;
+      int nn, fc, mu, rc0;
       for (int vz = 0; vz < 2; ++vz)
-        if ((rc0 = get_bot_sched(h, op.a, op.b, vz, &dv, &nn, &fc))) return rc0;
+        if ((rc0 = get_bot_sched(h, op.a, op.b, vz, &dv, &nn, &fc, &mu))) return rc0;
     }
   std::vector<int> save_cur(h->n);
   std::vector<char> save_vz(h->n);
@@ -1298,6 +1381,9 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
     const int clu_max = eenv ? std::min(atoi(eenv), KC_CLU_MAX_M) : KC_CLU_ENTRY_M;
     const char* csenv = getenv("KC_BOT_CS");
     const int cs_first = csenv && atoi(csenv) == 8 ? 8 : 16;
+    // smallest strip side (KC_BOT_MINSTRIP overrides): coarser levels live in CTA 0
+    const char* msenv = getenv("KC_BOT_MINSTRIP");
+    const int min_strip = msenv ? std::max(atoi(msenv), 31) : KC_CLU_MIN_STRIP;
     for (int csz : {16, 8}) {
       if (csz > cs_first) continue;
       if (!allow || lb >= 0) break;
@@ -1307,13 +1393,13 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
         int ns = 0;
         while (ns < nl) {
           const int m = bot_m(m0, ns);
-          if (m < KC_CLU_MIN_STRIP || (m + 1) % csz != 0 || ((m + 1) / csz) % 2 != 0) break;
+          if (m < min_strip || (m + 1) % csz != 0 || ((m + 1) / csz) % 2 != 0) break;
           ++ns;
         }
         if (ns == 0) break;  // coarser entries have no strips either
         const size_t bytes = sizeof(double) * (size_t)bot_smem_doubles(m0, nl, ns, csz);
         if (bytes > smem_max) continue;
-        if (cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) continue;
+        if (bot_smem_attr(bytes) != cudaSuccess) continue;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(csz);
         cfg.blockDim = dim3(KC_BOT_THREADS);
@@ -1358,11 +1444,18 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
     h->bot_cs = cs;
     bot_geometry(bp, h->bot_m0, cs);
     h->bot_smem = smem;
-    if (cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->bot_smem) != cudaSuccess) {
+    if (bot_smem_attr(h->bot_smem) != cudaSuccess) {
       h->err = "cudaFuncSetAttribute(k_bottom) failed";
       return fail(KC_ECUDA);
     }
     h->Lb = lb;
+#if KC_FAST
+    const char* mvenv = getenv("KC_TINY_MV");
+    if (cs > 1 && !(mvenv && mvenv[0] == '0')) {
+      int rc = setup_frame_operators(h, prop);
+      if (rc) return fail(rc);
+    }
+#endif
   }
   if (n >= 2 && h->L[0].m >= KC_FUSE_MIN_M) {  // per-warp partials of the fused level-1 norms
     int nw = 0;
@@ -1413,6 +1506,7 @@ int kc_destroy(kc_handle* h) {
   cudaFree(h->ap);
   cudaFree(h->fb);
   cudaFree(h->snap);
+  cudaFree(h->mv_mats);
   cudaFree(h->d_npart);
   cudaFree(h->d_nblk);
   cudaFree(h->d_ncount);

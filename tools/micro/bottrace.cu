@@ -30,12 +30,26 @@ int main(int argc, char** argv) {
   BotBuilder b; b.m0 = m0; b.nlev = nlev; b.nu1 = 2; b.nu2 = 2; b.vz = 1;
   b.tiny = argc > 2 ? atoi(argv[2]) != 0 : true;
   b.nstrip = nstrip;
+  // argv[5] = 1: side-15 frame operators (FMA build; dummy matrix values),
+  // the five blocks B1, B2, A1, B3, A2 resident
+  const bool mv = argc > 5 && atoi(argv[5]) != 0;
+  bp.nu1 = 2; bp.nu2 = 2; bp.nstrip = nstrip; bot_geometry(bp, m0, cs);
+  if (mv) {
+    double* mats; cudaMalloc(&mats, sizeof(double) * 6 * KC_MV_N * KC_MV_LD);
+    cudaMemset(mats, 0, sizeof(double) * 6 * KC_MV_N * KC_MV_LD);
+    const int R = (KC_MV_N + cs - 1) / cs, order[5] = {1, 3, 0, 5, 2};
+    bp.mv_mats = mats; bp.mv_rows = R; bp.mv_off = (bp.total + 1) & ~1;
+    for (int i = 0; i < 5; ++i) { b.mv_mask |= 1u << order[i]; bp.mv_slot[order[i]] = i; }
+    bp.mv_rep = 1;
+    for (int d = 0; d < nlev; ++d) if (bot_m(m0, d) == KC_MV_M) bp.mv_d = d;
+  }
   b.rec(0, kappa); if (kappa > 1) b.rec(0, kappa - 1);
+  bp.mv_copy = (int)b.mv_used;
   unsigned* ds; cudaMalloc(&ds, b.out.size() * 4);
   cudaMemcpy(ds, b.out.data(), b.out.size() * 4, cudaMemcpyHostToDevice);
   bp.gv = gv; bp.gf = gf; bp.gP = P; bp.v_zero = 1; bp.sched = ds; bp.nsched = (int)b.out.size(); bp.final_cur = b.cur & 1;
-  bp.nu1 = 2; bp.nu2 = 2; bp.nstrip = nstrip; bot_geometry(bp, m0, cs);
-  size_t smem = sizeof(double) * bot_smem_doubles(m0, nlev, nstrip, cs);
+  if (mv) bp.mv_xin = bp.mv_off + 5 * ((KC_MV_N + cs - 1) / cs) * KC_MV_LD;
+  size_t smem = sizeof(double) * (mv ? (size_t)(bp.mv_xin + 2 * KC_MV_N) : (size_t)bot_smem_doubles(m0, nlev, nstrip, cs));
   cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_bottom, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
