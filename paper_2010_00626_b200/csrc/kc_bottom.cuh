@@ -57,7 +57,7 @@
 #define KC_CLU_ENTRY_M 127  // default entry (kc_engine.cu)
 #endif
 #ifndef KC_CLU_MIN_STRIP
-#define KC_CLU_MIN_STRIP 31
+#define KC_CLU_MIN_STRIP 63  // coarser levels are replicated in every CTA (31^2: 1.1 k vs 1.9 k cycles per phase)
 #endif
 #define KC_BOT_MAXLEV 8
 #ifndef KC_BOT_THREADS
@@ -66,7 +66,7 @@
 #define KC_BOT_WARPS (KC_BOT_THREADS / 32)
 #define KC_BOT_RB 4  // rows per thread in stencil phases
 
-#define KC_BOT_MAXPH 4096  // phase descriptors per launch (host-checked)
+#define KC_BOT_MAXPH 1024  // phase descriptors per launch (host-checked; a W sub-cycle from 127^2 needs < 300)
 
 // per-level constants, computed on the host (bot_geometry; the strip rows
 // of each rank are finished on the device) and kept in shared memory: each
@@ -97,10 +97,9 @@ struct BotParams {
   // below): blocks (kap - 1) * 2 + part of [A_kap | B_kap], 225 x KC_MV_LD
   // rows in global memory; the blocks this launch uses (mv_copy, a subset
   // of the handle's resident set) are copied row-sliced into every CTA's
-  // shared memory at mv_off, slot mv_slot[block].  mv_d: the side-15 level,
-  // replicated in every CTA when mv_rep (0: frame operators off).
+  // shared memory at mv_off, slot mv_slot[block]
   const double* mv_mats;
-  int mv_copy, mv_off, mv_rows, mv_d, mv_rep, mv_xin;  // mv_xin: 2 x 225 doubles of packed inputs
+  int mv_copy, mv_off, mv_rows, mv_xin;  // mv_xin: 2 x 225 doubles of packed inputs
   int mv_slot[6];
 };
 
@@ -114,12 +113,10 @@ struct BotParams {
 // (k_tiny_mats), each CTA of the 16-CTA cluster keeps a row slice of the
 // needed blocks in its shared memory, and a frame becomes one cluster-wide
 // matrix-vector phase (bot_mv_frame): ~2 k cycles instead of the ~10-12 k
-// of 30+ barrier-separated tiny phases on CTA 0.  The side-15 level itself
-// is then REPLICATED in every CTA: the restriction into it and the frame
-// outputs are stored into all CTAs (each CTA produces a slice), so a frame
-// reads its inputs and the prolongation out of it reads v locally -- no CTA
-// serves everybody's remote loads.  A frame whose blocks are not resident
-// runs the interpreter on CTA 0 and PH_BCAST then copies its result out.  The product rounds
+// of 30+ barrier-separated tiny phases.  The side-15 level is replicated in
+// every CTA like all non-strip levels (BotBuilder), so a frame reads its
+// inputs locally and stores its rows into every CTA's copy.  A frame whose
+// blocks are not resident runs the interpreter on every CTA's copy.  The product rounds
 // differently from the frame's own operation sequence, so this is FAST-only
 // (the exact build keeps the frames); parity bar as for the FMA build.
 #define KC_MV_M 15
@@ -225,8 +222,7 @@ __device__ __forceinline__ void kc_bot_mark(int k) {
 // were measured slower -- larger kernel, longer dependent chains -- and the
 // tiny frames replaced them.)
 enum BotOp {
-  PH_JACOBI = 0, PH_RESID = 1, PH_RESTRICT = 2, PH_PROLONG = 3, PH_JOIN = 4, PH_J2Z = 5, PH_TINY = 8, PH_CSYNC = 9,
-  PH_BCAST = 10  // every CTA copies CTA 0's side-15 v (buffer src) into its replica
+  PH_JACOBI = 0, PH_RESID = 1, PH_RESTRICT = 2, PH_PROLONG = 3, PH_JOIN = 4, PH_J2Z = 5, PH_TINY = 8, PH_CSYNC = 9
 };
 #ifndef KC_BOT_TINY_M
 #define KC_BOT_TINY_M 15  // frames on sides <= this run as PH_TINY (side 15 on 8 warps)
@@ -263,18 +259,24 @@ struct BotBuilder {  // host side
   int nstrip = 0;           // levels d < nstrip are strip phases (all CTAs of the cluster)
   unsigned cur = 0, vz = 0;
   int gprev = KC_BOT_WARPS;
-  bool local_run = false;   // the last emitted phase ran on CTA 0 only
   bool fuse = true;         // emit PH_J2Z
   bool tiny = true;         // whole frames on sides <= KC_BOT_TINY_M as PH_TINY
   bool dry = false;         // track buffers only (inside a PH_TINY frame)
   unsigned mv_mask = 0;     // resident frame-operator blocks (0: frame operators off)
   unsigned mv_used = 0;     // blocks the emitted frames use (BotParams::mv_copy)
+  int mv_last = -1;         // buffer the previous frame operator wrote
+  bool mv_sync = false;     // an interpreter frame ran since: barrier before the next operator
   std::vector<unsigned> out;
+  // Strip phases run on every CTA on its rows and end with a cluster
+  // barrier.  Every coarser level is REPLICATED: each CTA holds all of it and
+  // runs its phases on its own copy (group barrier only), so no phase reads
+  // another CTA's copy and no cluster barrier is needed below the strips;
+  // data enters the replicas by broadcast stores (the restriction out of the
+  // last strip level, the frame operators' outputs), each followed by a
+  // cluster barrier.
   void emit(int op, int d, int src, int zero, int cbuf, int cc, int kap = 0) {
     if (dry) return;
     if (d < nstrip) {
-      if (local_run) out.push_back(bot_desc(PH_CSYNC, 0, 0, 0, 0, 0, KC_BOT_WARPS));
-      local_run = false;
       gprev = KC_BOT_WARPS;  // a strip phase ends with a cluster barrier
       out.push_back(bot_desc(op, d, src, zero, cbuf, cc, KC_BOT_WARPS, kap) | BD_STRIP_BIT);
       return;
@@ -282,7 +284,6 @@ struct BotBuilder {  // host side
     const int g = (op == PH_TINY && bot_m(m0, d) == 7) ? 2 : bot_warps(bot_m(m0, d));
     if (g > gprev) out.push_back(bot_desc(PH_JOIN, 0, 0, 0, 0, 0, g));
     gprev = g;
-    local_run = true;
     out.push_back(bot_desc(op, d, src, zero, cbuf, cc, g, kap));
   }
   void relax(int d, int count) {
@@ -300,31 +301,28 @@ struct BotBuilder {  // host side
   }
   void rec(int d, int kap) {
     if (mv_mask && !dry && d >= nstrip && bot_m(m0, d) == KC_MV_M && d < nlev - 1) {
-      // frame operator: one cluster-wide phase (all CTAs, like a strip
-      // phase), output into the other buffer; children are scratch
+      // frame operator: one cluster-wide phase (every CTA its rows, outputs
+      // broadcast into every replica).  The output buffer alternates from
+      // frame to frame, so it is never the one a slower CTA may still be
+      // prolongating from (the previous frame's output); a continuing frame
+      // (not a zero guess) reads that previous output and writes the other.
       const int k3 = kap < 3 ? kap : 3;
       const int z = (vz >> d) & 1u;
       const unsigned need = (1u << ((k3 - 1) * 2 + 1)) | (z ? 0u : (1u << ((k3 - 1) * 2)));
       if ((mv_mask & need) == need) {
-        if (local_run) out.push_back(bot_desc(PH_CSYNC, 0, 0, 0, 0, 0, KC_BOT_WARPS));
-        local_run = false;
+        const int src = (cur >> d) & 1u;
+        const int ob = z ? (mv_last >= 0 ? mv_last ^ 1 : src ^ 1) : src ^ 1;
+        if (mv_sync) out.push_back(bot_desc(PH_CSYNC, 0, 0, 0, 0, 0, KC_BOT_WARPS));
+        mv_sync = false;
         gprev = KC_BOT_WARPS;
-        out.push_back(bot_desc(PH_TINY, d, (cur >> d) & 1u, z, 0, 0, KC_BOT_WARPS, k3) | BD_STRIP_BIT);
+        out.push_back(bot_desc(PH_TINY, d, src, z, ob, 0, KC_BOT_WARPS, k3) | BD_STRIP_BIT);
         mv_used |= need;
-        cur ^= 1u << d;
+        mv_last = ob;
+        cur = (cur & ~(1u << d)) | ((unsigned)ob << d);
         vz &= ~(1u << d);
         return;
       }
-      // interpreter frame on CTA 0, then its result into every replica
-      emit(PH_TINY, d, (cur >> d) & 1u, (vz >> d) & 1u, 0, 0, kap);
-      dry = true;
-      rec(d, kap);
-      dry = false;
-      out.push_back(bot_desc(PH_CSYNC, 0, 0, 0, 0, 0, KC_BOT_WARPS));
-      out.push_back(bot_desc(PH_BCAST, d, (cur >> d) & 1u, 0, 0, 0, KC_BOT_WARPS) | BD_STRIP_BIT);
-      local_run = false;
-      gprev = KC_BOT_WARPS;
-      return;
+      mv_sync = true;  // interpreter frame below (every CTA on its replica)
     }
     if (tiny && fuse && !dry && d >= nstrip && bot_m(m0, d) <= KC_BOT_TINY_M && d < nlev - 1 && kap <= 15) {
       // one descriptor; bot_tiny follows the rules below (J2Z on), so
@@ -743,8 +741,8 @@ struct BotTiny {
 // a zero guess), inputs gathered from CTA 0's side-15 level, outputs stored
 // into CTA 0's other v buffer (so no CTA overwrites an input another CTA may
 // still read); the caller ends the phase with a cluster barrier.
-__device__ __forceinline__ void bot_mv_frame(double* sm, const BotParams& bp, const BotLv& L, int src, bool zero,
-                                             int kap, int rank, int cs) {
+__device__ __forceinline__ void bot_mv_frame(double* sm, const BotParams& bp, const BotLv& L, int src, int ob,
+                                             bool zero, int kap, int rank, int cs) {
   cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
   const int R = bp.mv_rows;
   asm volatile("cp.async.wait_all;" ::: "memory");  // the blocks (prologue copies)
@@ -761,7 +759,7 @@ __device__ __forceinline__ void bot_mv_frame(double* sm, const BotParams& bp, co
     if (!zero) xv[i] = vin[o];
   }
   __syncthreads();
-  double* out = sm + (src ? L.vo0 : L.vo1);
+  double* out = sm + (ob ? L.vo1 : L.vo0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i0 = rank * R;
   for (int r = warp; r < R && i0 + r < KC_MV_N; r += KC_BOT_WARPS) {
@@ -979,7 +977,7 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
     }
     const bool strip = (e & BD_STRIP_BIT) != 0u;
     const int g = bot_desc_g(e);
-    if (!strip && (rank != 0 || warp >= g)) continue;
+    if (!strip && warp >= g) continue;  // replicated levels: every CTA on its copy
     if (op == PH_JOIN) {
       bot_sync(g);
       continue;
@@ -1012,15 +1010,10 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
       double* fc = sm + C.fo;
       double* vc = sm + C.vo0;
       BotPush ps{nullptr, nullptr, -1};
-      if (strip && bp.mv_rep && d + 1 == bp.mv_d) {  // into every CTA's replica of the side-15 level
+      if (strip && d + 1 >= nstrip) {  // into every CTA's replica of the first replicated level
         bot_restrict_bcast(zero ? f : u, L, fc + (L.a / 2) * C.S, C.m, C.S, tid, nth, cs);
       } else {
-        if (strip && d + 1 < nstrip) {
-          ps = bot_push(fc, C, true, rank, cs);
-        } else if (strip) {  // into CTA 0's level, at this strip's first coarse row
-          fc = cl.map_shared_rank(fc, 0) + (L.a / 2) * C.S;
-          vc = cl.map_shared_rank(vc, 0);
-        }
+        if (strip) ps = bot_push(fc, C, true, rank, cs);  // strip child: halo rows to the neighbours
         bot_restrict(zero ? f : u, L, fc, C.m, C.S, vc, tab[d + 1].center, BD_CC(e), tid, nth, ps);
       }
     } else if (op == PH_PROLONG) {
@@ -1031,21 +1024,11 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
         __syncthreads();
         continue;
       }
-      if (strip && bp.mv_rep && d + 1 == bp.mv_d)  // the local replica of the side-15 level
+      if (strip)  // from this CTA's replica of the child, at this strip's first coarse row
         vc += (L.a / 2) * C.S;
-      else if (strip)  // from CTA 0's level, at this strip's first coarse row
-        vc = cl.map_shared_rank(const_cast<double*>(vc), 0) + (L.a / 2) * C.S;
       bot_prolong(u, vc, L, C.m, C.S, zero, tid, nth, bot_push(u, L, strip, rank, cs));
-    } else if (op == PH_BCAST) {  // CTA 0's side-15 v (buffer src) into this CTA's replica
-      if (rank != 0) {
-        const double* v0 = cl.map_shared_rank(u, 0);
-        for (int i = tid; i < m * m; i += KC_BOT_THREADS) {
-          const int y = i / m, x = i - y * m;
-          u[y * S + x] = v0[y * S + x];
-        }
-      }
     } else if (strip) {  // PH_TINY as a frame operator (all CTAs; FMA build)
-      bot_mv_frame(sm, bp, L, src, zero, BD_KAP(e), rank, cs);
+      bot_mv_frame(sm, bp, L, src, BD_CBUF(e), zero, BD_KAP(e), rank, cs);
     } else {  // PH_TINY (CTA 0: warp 0 for sides <= 7, warps 0-7 for side 15)
       const BotTiny t{sm, lv, tab, bp.nu1, bp.nu2, tid, nth};
       int cur = src, vz = zero;

@@ -515,7 +515,7 @@ int get_bot_sched(kc_handle* h, int k1, int k2, int vzero, const unsigned** dev,
     b.nu2 = h->nu2;
     b.vz = vzero ? 1u : 0u;
     b.nstrip = h->bot_base.nstrip;
-    b.mv_mask = h->bot_base.mv_rep ? (unsigned)h->mv_resident : 0u;
+    b.mv_mask = (unsigned)h->mv_resident;
     if (b.nlev > 1) {
       b.rec(0, k1);
       if (k2 > 0) b.rec(0, k2);
@@ -586,7 +586,6 @@ int setup_frame_operators(kc_handle* h, const cudaDeviceProp& prop) {
   bp.mv_mats = h->mv_mats;
   bp.mv_off = off;
   bp.mv_rows = R;
-  bp.mv_d = d15;
   bp.mv_xin = off + nres * R * KC_MV_LD;
   const size_t bytes = sizeof(double) * (size_t)(bp.mv_xin + 2 * KC_MV_N);
   // the cluster must still fit with the larger shared memory
@@ -607,7 +606,6 @@ int setup_frame_operators(kc_handle* h, const cudaDeviceProp& prop) {
     cudaGetLastError();
     return KC_OK;  // keep the interpreter frames
   }
-  bp.mv_rep = 1;
   h->mv_resident = mask;
   h->bot_smem = bytes;
   return KC_OK;

@@ -40,8 +40,7 @@ int main(int argc, char** argv) {
     const int R = (KC_MV_N + cs - 1) / cs, order[5] = {1, 3, 0, 5, 2};
     bp.mv_mats = mats; bp.mv_rows = R; bp.mv_off = (bp.total + 1) & ~1;
     for (int i = 0; i < 5; ++i) { b.mv_mask |= 1u << order[i]; bp.mv_slot[order[i]] = i; }
-    bp.mv_rep = 1;
-    for (int d = 0; d < nlev; ++d) if (bot_m(m0, d) == KC_MV_M) bp.mv_d = d;
+
   }
   b.rec(0, kappa); if (kappa > 1) b.rec(0, kappa - 1);
   bp.mv_copy = (int)b.mv_used;
