@@ -222,7 +222,8 @@ __device__ __forceinline__ void kc_bot_mark(int k) {
 // were measured slower -- larger kernel, longer dependent chains -- and the
 // tiny frames replaced them.)
 enum BotOp {
-  PH_JACOBI = 0, PH_RESID = 1, PH_RESTRICT = 2, PH_PROLONG = 3, PH_JOIN = 4, PH_J2Z = 5, PH_TINY = 8, PH_CSYNC = 9
+  PH_JACOBI = 0, PH_RESID = 1, PH_RESTRICT = 2, PH_PROLONG = 3, PH_JOIN = 4, PH_J2Z = 5, PH_TINY = 8, PH_CSYNC = 9,
+  PH_FRAME31 = 10  // a whole kappa_cycle frame on the replicated side-31 level (BotFrame31)
 };
 #ifndef KC_BOT_TINY_M
 #define KC_BOT_TINY_M 15  // frames on sides <= this run as PH_TINY (side 15 on 8 warps)
@@ -299,23 +300,36 @@ struct BotBuilder {  // host side
       cur ^= 1u << d;
     }
   }
+  bool frame31 = true;      // whole side-31 frames as PH_FRAME31 (replicated levels)
   void rec(int d, int kap) {
-    if (mv_mask && !dry && d >= nstrip && bot_m(m0, d) == KC_MV_M && d < nlev - 1) {
+    if (frame31 && fuse && !dry && d >= nstrip && bot_m(m0, d) == 31 && d + 5 == nlev && kap <= 15) {
+      // one descriptor for the frame and everything below it; the dry replay
+      // below follows BotFrame31 (and the frame-operator bookkeeping)
+      emit(PH_FRAME31, d, (cur >> d) & 1u, (vz >> d) & 1u, 0, 0, kap);
+      dry = true;
+      rec(d, kap);
+      dry = false;
+      return;
+    }
+    if (mv_mask && d >= nstrip && bot_m(m0, d) == KC_MV_M && d < nlev - 1) {
       // frame operator: one cluster-wide phase (every CTA its rows, outputs
       // broadcast into every replica).  The output buffer alternates from
       // frame to frame, so it is never the one a slower CTA may still be
       // prolongating from (the previous frame's output); a continuing frame
       // (not a zero guess) reads that previous output and writes the other.
+      // In a dry replay (inside PH_FRAME31) only the bookkeeping runs.
       const int k3 = kap < 3 ? kap : 3;
       const int z = (vz >> d) & 1u;
       const unsigned need = (1u << ((k3 - 1) * 2 + 1)) | (z ? 0u : (1u << ((k3 - 1) * 2)));
       if ((mv_mask & need) == need) {
         const int src = (cur >> d) & 1u;
         const int ob = z ? (mv_last >= 0 ? mv_last ^ 1 : src ^ 1) : src ^ 1;
-        if (mv_sync) out.push_back(bot_desc(PH_CSYNC, 0, 0, 0, 0, 0, KC_BOT_WARPS));
+        if (!dry) {
+          if (mv_sync) out.push_back(bot_desc(PH_CSYNC, 0, 0, 0, 0, 0, KC_BOT_WARPS));
+          gprev = KC_BOT_WARPS;
+          out.push_back(bot_desc(PH_TINY, d, src, z, ob, 0, KC_BOT_WARPS, k3) | BD_STRIP_BIT);
+        }
         mv_sync = false;
-        gprev = KC_BOT_WARPS;
-        out.push_back(bot_desc(PH_TINY, d, src, z, ob, 0, KC_BOT_WARPS, k3) | BD_STRIP_BIT);
         mv_used |= need;
         mv_last = ob;
         cur = (cur & ~(1u << d)) | ((unsigned)ob << d);
@@ -323,6 +337,13 @@ struct BotBuilder {  // host side
         return;
       }
       mv_sync = true;  // interpreter frame below (every CTA on its replica)
+      if (dry) {  // BotTiny's buffer rules (J2Z on)
+        const bool t = tiny;
+        tiny = false;
+        rec_plain(d, kap);
+        tiny = t;
+        return;
+      }
     }
     if (tiny && fuse && !dry && d >= nstrip && bot_m(m0, d) <= KC_BOT_TINY_M && d < nlev - 1 && kap <= 15) {
       // one descriptor; bot_tiny follows the rules below (J2Z on), so
@@ -333,6 +354,9 @@ struct BotBuilder {  // host side
       dry = false;
       return;
     }
+    rec_plain(d, kap);
+  }
+  void rec_plain(int d, int kap) {
     relax(d, nu1);
     const int c = (cur >> d) & 1u;
     const int z = (vz >> d) & 1u;
@@ -787,6 +811,141 @@ __device__ __forceinline__ void bot_mv_frame(double* sm, const BotParams& bp, co
   }
 }
 
+// PH_FRAME31: a whole kappa_cycle frame on the replicated side-31 level --
+// its sweeps, residual, restriction, the side-15 frames below it (frame
+// operators, or BotTiny on warps 0-7) and the prolongation -- with the side
+// a compile-time constant: no descriptor decode, folded index math, CTA
+// barriers only (every CTA works on its own copy; the frame operators add
+// their cluster barrier).  Follows BotBuilder::rec_plain and the frame-
+// operator bookkeeping (mv_last / mv_sync), which the host replays dry.
+struct BotFrame31 {
+  static constexpr int M = 31, S = M + 2, MC = 15, SC = MC + 2;
+  double* sm;
+  const BotLv* lv;
+  const St9* tab;
+  const BotParams* bp;
+  int tid, rank, cs, nlev;
+  int* slot;      // shared int: a BotTiny frame's final buffer for the other warps
+  int* tiny_child;
+  int mv_last;    // buffer the previous frame operator wrote (-1: none)
+  bool mv_sync;   // an interpreter frame ran since the last frame operator
+  __device__ __forceinline__ double* buf(const BotLv& L, int b) const { return sm + (b ? L.vo1 : L.vo0); }
+  __device__ __forceinline__ void stencil(bool jac, bool zero, const double* u, double* o, const double* f,
+                                          const St9& st) const {
+    const BotPush ps{nullptr, nullptr, -1};
+    bot_stencil<4>(jac, zero, u, o, f, M, M, S, 1.0f / (float)M, st, tid, KC_BOT_THREADS, M * ((M + 3) / 4), ps);
+  }
+  __device__ __forceinline__ void j2z(double* u, const double* f, const St9& st) const {
+    // 2-row items sharing their u1 = 0 + c f values (bot_j2z)
+    for (int it = tid; it < M * ((M + 1) / 2); it += KC_BOT_THREADS) {
+      const int rb = it / M, x = it - rb * M, y0 = 2 * rb;
+      const double* pf = f + y0 * S + x;
+      if (y0 + 2 <= M) {
+        double n1[4][3];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx) n1[k][dx] = kc_jacobi_zero(pf[(k - 1) * S + dx - 1], st.c);
+        const double a0 = kc_sum9(st, n1[0][0], n1[0][1], n1[0][2], n1[1][0], n1[1][1], n1[1][2], n1[2][0],
+                                  n1[2][1], n1[2][2]);
+        const double a1 = kc_sum9(st, n1[1][0], n1[1][1], n1[1][2], n1[2][0], n1[2][1], n1[2][2], n1[3][0],
+                                  n1[3][1], n1[3][2]);
+        u[y0 * S + x] = kc_jacobi_pt(n1[1][1], pf[0], a0, st.c);
+        u[(y0 + 1) * S + x] = kc_jacobi_pt(n1[2][1], pf[S], a1, st.c);
+      } else {
+        u[y0 * S + x] = bot_j2z_pt(pf, S, st);
+      }
+    }
+  }
+  __device__ __forceinline__ void relax(const BotLv& L, const St9& st, int count, int& cur, int& vz) const {
+    int i = 0;
+    const double* f = sm + L.fo;
+    if (count >= 2 && vz) {
+      j2z(buf(L, cur), f, st);
+      __syncthreads();
+      vz = 0;
+      i = 2;
+    }
+    for (; i < count; ++i) {
+      stencil(true, vz, buf(L, cur), buf(L, cur ^ 1), f, st);
+      __syncthreads();
+      vz = 0;
+      cur ^= 1;
+    }
+  }
+  // the side-15 frame below (frame operator or BotTiny), with its buffer
+  __device__ __forceinline__ void frame15(int d, int kap, int& c, int& z) {
+    const int k3 = kap < 3 ? kap : 3;
+    const int need = (1 << ((k3 - 1) * 2 + 1)) | (z ? 0 : (1 << ((k3 - 1) * 2)));
+    if (bp->mv_copy && (bp->mv_copy & need) == need) {
+      if (mv_sync) clu_sync();
+      mv_sync = false;
+      const int ob = z ? (mv_last >= 0 ? mv_last ^ 1 : c ^ 1) : c ^ 1;
+      bot_mv_frame(sm, *bp, lv[d], c, ob, z, k3, rank, cs);
+      clu_sync();
+      mv_last = ob;
+      c = ob;
+      z = 0;
+      return;
+    }
+    if (bp->mv_copy) mv_sync = true;
+    if (tid < 256) {
+      const BotTiny t{sm, lv, tab, bp->nu1, bp->nu2, tid, 256};
+      t.frame(d, kap, nlev, c, z, tiny_child);
+      if (tid == 0) *slot = c;
+    }
+    __syncthreads();
+    c = *slot;
+    z = 0;
+  }
+  __device__ void frame(int d, int kap, int& cur, int& vz) {
+    const BotLv L = lv[d], C = lv[d + 1];
+    const St9 st = tab[d];
+    const int nu1 = bp->nu1, nu2 = bp->nu2;
+    relax(L, st, nu1, cur, vz);
+    const double* f = sm + L.fo;
+    if (!vz) {
+      stencil(false, false, buf(L, cur), buf(L, cur ^ 1), f, st);
+      __syncthreads();
+    }
+    {  // full weighting into the child's f (transfer.py:78-83)
+      const double* r = vz ? f : buf(L, cur ^ 1);
+      double* fc = sm + C.fo;
+      for (int i = tid; i < MC * MC; i += KC_BOT_THREADS) {
+        const int q = i / MC, p = i - q * MC;
+        const double* rc = r + (2 * q + 1) * S + (2 * p + 1);
+        const double* rs = rc - S;
+        const double* rn = rc + S;
+        fc[q * SC + p] = kc_fw(rs[-1], rs[0], rs[1], rc[-1], rc[0], rc[1], rn[-1], rn[0], rn[1]);
+      }
+      __syncthreads();
+    }
+    int c = 0, z = 1;  // the child's zero guess (cycle.py:214)
+    frame15(d + 1, kap, c, z);
+    if (kap > 1) frame15(d + 1, kap - 1, c, z);
+    {  // u += P vc, one coarse cell (2x2 fine points) per item (transfer.py:50-58)
+      double* u = buf(L, cur);
+      const double* vc = buf(C, c);
+      constexpr int NC = MC + 1;
+      for (int i = tid; i < NC * NC; i += KC_BOT_THREADS) {
+        const int q = i / NC, p = i - q * NC;
+        const double c00 = vc[(q - 1) * SC + p - 1], c01 = vc[(q - 1) * SC + p];
+        const double c10 = vc[q * SC + p - 1], c11 = vc[q * SC + p];
+        double* pu = u + (2 * q) * S + 2 * p;
+        pu[0] = DADD(vz ? 0.0 : pu[0], DMUL(0.25, DADD(DADD(DADD(c00, c01), c10), c11)));
+        if (p < MC) pu[1] = DADD(vz ? 0.0 : pu[1], DMUL(0.5, DADD(c01, c11)));
+        if (q < MC) {
+          pu[S] = DADD(vz ? 0.0 : pu[S], DMUL(0.5, DADD(c10, c11)));
+          if (p < MC) pu[S + 1] = DADD(vz ? 0.0 : pu[S + 1], c11);
+        }
+      }
+      __syncthreads();
+    }
+    vz = 0;
+    relax(L, st, nu2, cur, vz);
+  }
+};
+
 // Columns of the side-15 frame operators: CTA (j, k - 1) runs BotTiny::frame
 // (the bottom kernel's own frame code) with counter k on the unit input j
 // (j < 225: v = e_j; else f = e_(j-225)) and stores v_out as column j of
@@ -966,6 +1125,9 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
   // replay the schedule: strip phases run on every CTA and end with a
   // cluster barrier; the others run on CTA 0, where a warp takes part in the
   // phases of its group only and JOIN entries gather a larger group
+  __shared__ int f31_slot;
+  int mv_last = -1;      // frame-operator bookkeeping shared with PH_FRAME31 (BotBuilder mirrors it)
+  bool mv_sync = false;
   unsigned e_next = bp.nsched > 0 ? sched[0] : 0u;
   for (int k = 0; k < bp.nsched; ++k) {
     const unsigned e = e_next;
@@ -973,6 +1135,7 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
     const int op = BD_OP(e);
     if (op == PH_CSYNC) {
       clu_sync();
+      mv_sync = false;
       continue;
     }
     const bool strip = (e & BD_STRIP_BIT) != 0u;
@@ -1027,9 +1190,17 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
       if (strip)  // from this CTA's replica of the child, at this strip's first coarse row
         vc += (L.a / 2) * C.S;
       bot_prolong(u, vc, L, C.m, C.S, zero, tid, nth, bot_push(u, L, strip, rank, cs));
+    } else if (op == PH_FRAME31) {  // every thread of every CTA, on its replica
+      BotFrame31 fr{sm, lv, tab, &bp, tid, rank, cs, nlev, &f31_slot, tiny_child, mv_last, mv_sync};
+      int cur = src, vz = zero;
+      fr.frame(d, BD_KAP(e), cur, vz);
+      mv_last = fr.mv_last;
+      mv_sync = fr.mv_sync;
     } else if (strip) {  // PH_TINY as a frame operator (all CTAs; FMA build)
       bot_mv_frame(sm, bp, L, src, BD_CBUF(e), zero, BD_KAP(e), rank, cs);
-    } else {  // PH_TINY (CTA 0: warp 0 for sides <= 7, warps 0-7 for side 15)
+      mv_last = BD_CBUF(e);
+    } else {  // PH_TINY (every CTA: warp 0 for sides <= 7, warps 0-7 for side 15)
+      if (m == KC_MV_M && bp.mv_copy) mv_sync = true;
       const BotTiny t{sm, lv, tab, bp.nu1, bp.nu2, tid, nth};
       int cur = src, vz = zero;
       t.frame(d, BD_KAP(e), nlev, cur, vz, tiny_child);

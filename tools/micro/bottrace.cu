@@ -103,8 +103,8 @@ int main(int argc, char** argv) {
     int o = op[i] / 16, d = op[i] % 16;
     sum[o][d] += t[i + 1] - t[i]; cmp[o][d] += te[i] - t[i]; cnt[o][d]++;
   }
-  const char* nm[10] = {"jacobi", "resid", "restrict", "prolong", "join", "j2z", "rr", "pj", "tiny", "csync"};
-  for (int o = 0; o < 10; ++o) for (int d = 0; d < nlev; ++d) if (cnt[o][d])
+  const char* nm[11] = {"jacobi", "resid", "restrict", "prolong", "join", "j2z", "rr", "pj", "tiny", "csync", "frame31"};
+  for (int o = 0; o < 11; ++o) for (int d = 0; d < nlev; ++d) if (cnt[o][d])
     printf("  %-9s level %d (m=%3d): %5d phases, %7.0f cycles avg (thread 0 to its barrier %5.0f), %9.0f total\n", nm[o], d,
            bot_m(m0, d), cnt[o][d], sum[o][d] / cnt[o][d], cmp[o][d] / cnt[o][d], sum[o][d]);
   printf("phases traced: %d, total cycles %lld\n", n, n > 1 ? t[n - 1] - t[0] : 0);
