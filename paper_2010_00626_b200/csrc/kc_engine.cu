@@ -93,7 +93,7 @@ struct Level {
   St9 st{};
 };
 
-enum OpKind : int { OP_RELAX, OP_RESTRICT, OP_ZERO, OP_PROLONG, OP_COARSEST, OP_BOTTOM, OP_PRE, OP_POST };
+enum OpKind : int { OP_RELAX, OP_RESTRICT, OP_ZERO, OP_PROLONG, OP_COARSEST, OP_BOTTOM, OP_PRE, OP_POST, OP_POSTPRE };
 #define KC_FUSE_MAXNU 4      // fused streaming kernels exist for nu <= 4
 #define KC_FUSE_MIN_M 127    // HBM levels handled by the fused kernels
 #ifndef KC_TILE_MAX_M
@@ -156,6 +156,7 @@ struct kc_handle {
   bool fuse = true;           // use the fused streaming kernels in native cycles
   bool tile = true;           // overlapped-tile kernels on the mid-size levels
   bool pdl = true;            // programmatic dependent launch around the bottom kernel (KC_PDL=0: off)
+  bool postpre = true;        // fused sibling post+pre passes on the column-tile levels (KC_POSTPRE=0: off)
   bool ks_sym_on = true;      // shared w1/w7 products on symmetric levels (KC_SYM=0: off)
   int num_sms = 148;
   SolveState* d_solve = nullptr;   // device loop state
@@ -839,6 +840,9 @@ int ex_ctile_pre(kc_handle* h, int l) {
 #define KC_CTILE_POST_MAX_M 511  // faster than the streaming post pass up to here (tools/micro/midlev.cu)
 #endif
 #define KC_CTILE_POST_TY 16
+#ifndef KC_PP_TY
+#define KC_PP_TY 16  // rows per fused post+pre tile
+#endif
 int ex_ctile_post(kc_handle* h, int l) {
   Level& L = h->L[l];
   Level& C = h->L[l + 1];
@@ -869,6 +873,62 @@ int ex_ctile_post(kc_handle* h, int l) {
   // the previous kernel (the child's last pass or the bottom kernel, which
   // triggers only after its own wait) completes, so they are fetched before
   // k_ctile_post waits for the coarse v
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tiles);
+  cfg.blockDim = dim3(KC_CT_NW * 32);
+  cfg.stream = h->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  KC_CUDA(h, cudaLaunchKernelEx(&cfg, fn, p));
+  KC_LAUNCH_CHECK(h);
+  ++h->launches;
+  L.cur ^= 1;
+  L.vzero = false;
+  return KC_OK;
+}
+
+// post pass of a call + pre pass of the next call on level l, one launch
+// (k_ctile_postpre); the result of both (NU2 + NU1 sweeps) lands in the
+// other buffer, the restricted residual in the child's f
+int ex_postpre(kc_handle* h, int l) {
+  Level& L = h->L[l];
+  Level& C = h->L[l + 1];
+  TileParams p{};
+  p.u = L.v[L.cur];
+  p.f = L.f;
+  p.uo = L.v[L.cur ^ 1];
+  p.fc = C.f;
+  p.vc = C.v[C.cur];
+  p.m = L.m;
+  p.P = L.P;
+  p.mc = C.m;
+  p.Pc = C.P;
+  p.s = L.st;
+  const bool z = L.vzero;
+  void (*fn)(TileParams) = nullptr;
+  int tx = 0;
+#define KCT_PP(A, B)                                                                                       \
+  do {                                                                                                     \
+    fn = z ? k_ctile_postpre<A, B, true, KC_PP_TY> : k_ctile_postpre<A, B, false, KC_PP_TY>;             \
+    tx = kc_pp_tx(A + B + 1);                                                                              \
+  } while (0)
+  switch (h->nu2 * 3 + h->nu1) {
+    case 0: KCT_PP(0, 0); break;
+    case 1: KCT_PP(0, 1); break;
+    case 2: KCT_PP(0, 2); break;
+    case 3: KCT_PP(1, 0); break;
+    case 4: KCT_PP(1, 1); break;
+    case 5: KCT_PP(1, 2); break;
+    case 6: KCT_PP(2, 0); break;
+    case 7: KCT_PP(2, 1); break;
+    default: KCT_PP(2, 2); break;
+  }
+#undef KCT_PP
+  p.tiles_x = (L.m + tx - 1) / tx;
+  const int tiles = p.tiles_x * ((L.m + KC_PP_TY - 1) / KC_PP_TY);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tiles);
   cfg.blockDim = dim3(KC_CT_NW * 32);
@@ -961,6 +1021,7 @@ int ex_op(kc_handle* h, const Op& op) {
   switch (op.kind) {
     case OP_PRE: return ex_pre(h, op.level, op.b != 0);
     case OP_POST: return ex_post(h, op.level, op.b);
+    case OP_POSTPRE: return ex_postpre(h, op.level);
     case OP_RELAX: return ex_relax(h, op.level, op.a);
     case OP_RESTRICT: return ex_restrict(h, op.level);
     case OP_ZERO: h->L[op.level].vzero = true; return KC_OK;
@@ -982,6 +1043,19 @@ bool fusable(const kc_handle* h, int l) {
 // norms: 0 none, 1 after the cycle (fused into the level-0 post), 2 of the
 // cycle's input (fused into the level-0 pre; the device solve loop), 3 the
 // PCG r . z of a preconditioning cycle (fused into the level-0 post).
+// the fused sibling pass (k_ctile_postpre) applies on the column-tile levels
+// up to KC_PP_MAX_M: per launch (in-graph estimates from eager timings at
+// n = 12, FMA build) 255^2 7.4 vs 5.6 + 5.9 us, 511^2 12.2 vs 7.7 + 7.3 us,
+// but 1023^2 36 vs 12 + 14.5 us -- its 20-of-31-column tiles recompute too
+// much once the level is throughput-bound
+#ifndef KC_PP_MAX_M
+#define KC_PP_MAX_M 511
+#endif
+bool postpre_ok(const kc_handle* h, int l) {
+  const Level& L = h->L[l];
+  return h->postpre && h->tile && L.m <= KC_PP_MAX_M && h->nu1 <= 2 && h->nu2 <= 2;
+}
+
 void flatten(const kc_handle* h, int l, int kappa, std::vector<Op>& ops, int norms = 0) {
   const int n = h->n;
   if (l == h->Lb) {
@@ -994,7 +1068,13 @@ void flatten(const kc_handle* h, int l, int kappa, std::vector<Op>& ops, int nor
   }
   const bool fu = fusable(h, l);
   if (fu) {
-    ops.push_back({OP_PRE, l, 0, norms == 2 ? 1 : 0});
+    // the previous op is the post pass of this level's previous call (the
+    // kappa-cycle's two recursive calls are adjacent): one fused pass
+    if (!norms && postpre_ok(h, l) && !ops.empty() && ops.back().kind == OP_POST && ops.back().level == l &&
+        ops.back().b == 0)
+      ops.back() = {OP_POSTPRE, l, 0, 0};
+    else
+      ops.push_back({OP_PRE, l, 0, norms == 2 ? 1 : 0});
   } else {
     ops.push_back({OP_RELAX, l, h->nu1, 0});
     ops.push_back({OP_RESTRICT, l, 0, 0});
@@ -1292,6 +1372,8 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
   {
     const char* penv = getenv("KC_PDL");
     h->pdl = !(penv && penv[0] == '0');
+    const char* ppenv = getenv("KC_POSTPRE");
+    h->postpre = !(ppenv && ppenv[0] == '0');
     const char* senv = getenv("KC_SYM");
     // the shared-product form only saves work when products are separately
     // rounded; in the FMA build every product is fused into its sum

@@ -401,3 +401,143 @@ __global__ void __launch_bounds__(NW * 32) k_ctile_post(const TileParams p) {
     if (t < NU) __syncthreads();
   }
 }
+
+// ---------------------------------------------------------------------------
+// Fused sibling passes (k_ctile_postpre): a routine call's post pass (v + P vc,
+// NU2 sweeps; cycle.py:219-220) immediately followed by the NEXT call's pre
+// pass on the same level (NU1 sweeps, residual, full weighting; cycle.py:211-
+// 213) -- the kappa-cycle's second recursive call (cycle.py:215-218) starts
+// exactly where the first one ended, so the intermediate v (after the post
+// sweeps) is consumed only by the following sweeps and never leaves the
+// tile.  One launch and one pass over the level instead of two, with the
+// same per-point arithmetic (kc_common.cuh).  Column tiles as k_ctile_pre
+// with D = NU2 + NU1 + 1 stages after the prolongation stage (region W =
+// TX + 1 + 2 D <= 32 columns, so TX = 20 at D = 5).
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int kc_pp_tx(int D) { return ((32 - 1 - 2 * D) / 2) * 2; }
+
+template <int NU2, int NU1, bool VZ, int TY, int NW = KC_CT_NW>
+__global__ void __launch_bounds__(NW * 32) k_ctile_postpre(const TileParams p) {
+  constexpr int NS = NU2 + NU1;  // sweeps
+  constexpr int D = NS + 1;      // + the residual stage
+  constexpr int TX = kc_pp_tx(D);
+  constexpr int W = TX + 1 + 2 * D;
+  constexpr int H = TY + 1 + 2 * D;
+  constexpr int RB = (H - 2 + NW - 1) / NW;  // rows per warp in a stage
+  constexpr int R0 = (H + NW - 1) / NW;      // rows per warp in the prolongation
+  constexpr int CH = (H + 1) / 2 + 3;        // coarse patch rows
+  static_assert(W <= 32 && TX >= 2, "one lane per region column");
+  __shared__ double su[2][H][32];
+  __shared__ double sf[H][32];
+  __shared__ double sc[CH][32];
+  // a programmatically launched successor (the bottom kernel) may start its
+  // independent prologue on free SMs now; it waits for this grid itself
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tx = blockIdx.x % p.tiles_x, ty = blockIdx.x / p.tiles_x;
+  const int y0 = ty * TY, x0 = tx * TX;
+  const int m = p.m, P = p.P;
+  const St9 s = p.s;
+  const int gx = x0 - D + lane;
+  const bool xin = gx >= 0 && gx < m;
+  const int qy0 = ((y0 - D) >> 1) - 1, qx0 = ((x0 - D) >> 1) - 1;  // coarse patch origin
+  {
+    const int cx = min(max(gx, -1), m);
+    for (int r = w; r < H; r += NW) {
+      const int cy = min(max(y0 - D + r, -1), m);
+      if (lane < W) {
+        const size_t gi = kc_idx(P, cy, cx);
+        kt_cp8(&sf[r][lane], p.f + gi);
+        if (!VZ) kt_cp8(&su[1][r][lane], p.u + gi);
+      }
+    }
+    // this level's f and v are final already; the coarse v is the previous
+    // grid's output (and the coarse f, written below, its input)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int qx = min(max(qx0 + lane, -1), p.mc);
+    for (int r = w; r < CH; r += NW) {
+      const int qy = min(max(qy0 + r, -1), p.mc);
+      kt_cp8(&sc[r][lane], p.vc + kc_idx(p.Pc, qy, qx));
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+  __syncthreads();
+  // stage 0: v + P vc on the region (transfer.py:50-58, cycle.py:174-176)
+  if (lane < W) {
+    auto cp = [&](int q, int pc) { return sc[q - qy0][pc - qx0]; };
+#pragma unroll
+    for (int k = 0; k < R0; ++k) {
+      const int r = w * R0 + k;
+      if (r < H) {
+        const int gy = y0 - D + r;
+        double v = 0.0;
+        if (xin && gy >= 0 && gy < m) v = DADD(VZ ? 0.0 : su[1][r][lane], kc_prolong_val(gy, gx, cp));
+        su[0][r][lane] = v;
+        if (NS == 0 && r >= D && r < D + TY && lane >= D && lane < D + TX && xin && gy >= 0 && gy < m)
+          p.uo[kc_idx(P, gy, gx)] = v;
+      }
+    }
+  }
+  __syncthreads();
+  // stages 1 .. NS: the NU2 post sweeps then the NU1 pre sweeps; stage D:
+  // the residual f - A v
+#pragma unroll
+  for (int t = 1; t <= D; ++t) {
+    const double(*src)[32] = su[(t - 1) & 1];
+    double(*dst)[32] = su[t & 1];
+    const bool lane_on = lane >= t && lane < W - t;
+    const int r0 = t + w * RB, r1 = min(r0 + RB, H - t);
+    if (lane_on && r0 < r1) {
+      double out[RB];
+      if (r1 - r0 == RB) {  // full block: every load first, RB independent chains
+        double v[RB + 2][3], fv[RB];
+#pragma unroll
+        for (int k = 0; k < RB + 2; ++k)
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx) v[k][dx] = src[r0 - 1 + k][lane - 1 + dx];
+#pragma unroll
+        for (int k = 0; k < RB; ++k) fv[k] = sf[r0 + k][lane];
+#pragma unroll
+        for (int k = 0; k < RB; ++k) {
+          const double au = kc_sum9(s, v[k][0], v[k][1], v[k][2], v[k + 1][0], v[k + 1][1], v[k + 1][2], v[k + 2][0],
+                                    v[k + 2][1], v[k + 2][2]);
+          out[k] = t <= NS ? kc_jacobi_pt(v[k + 1][1], fv[k], au, s.c) : DSUB(fv[k], au);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < RB; ++k)
+          if (r0 + k < r1) {
+            const int r = r0 + k;
+            const double au = kc_sum9(s, src[r - 1][lane - 1], src[r - 1][lane], src[r - 1][lane + 1], src[r][lane - 1],
+                                      src[r][lane], src[r][lane + 1], src[r + 1][lane - 1], src[r + 1][lane],
+                                      src[r + 1][lane + 1]);
+            out[k] = t <= NS ? kc_jacobi_pt(src[r][lane], sf[r][lane], au, s.c) : DSUB(sf[r][lane], au);
+          }
+      }
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        const int r = r0 + k;
+        if (r < r1) {
+          const int gy = y0 - D + r;
+          const double v = (xin && gy >= 0 && gy < m) ? out[k] : 0.0;
+          dst[r][lane] = v;
+          // v after all NS sweeps: owned points straight to HBM
+          if (t == NS && r >= D && r < D + TY && lane >= D && lane < D + TX && xin && gy >= 0 && gy < m)
+            p.uo[kc_idx(P, gy, gx)] = v;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // full weighting of the residual rows y0 .. y0+TY, columns x0 .. x0+TX
+  const double(*r)[32] = su[D & 1];
+  for (int i = threadIdx.x; i < (TY / 2) * (TX / 2); i += NW * 32) {
+    const int qy = i / (TX / 2), qx = i - qy * (TX / 2);
+    const int q = y0 / 2 + qy, pc = x0 / 2 + qx;
+    if (q < p.mc && pc < p.mc) {
+      const int cy = D + 2 * qy + 1, cx = D + 2 * qx + 1;
+      p.fc[kc_idx(p.Pc, q, pc)] = kc_fw(r[cy - 1][cx - 1], r[cy - 1][cx], r[cy - 1][cx + 1], r[cy][cx - 1], r[cy][cx],
+                                        r[cy][cx + 1], r[cy + 1][cx - 1], r[cy + 1][cx], r[cy + 1][cx + 1]);
+    }
+  }
+}

@@ -343,7 +343,8 @@ class CudaGridState:
     def fill_zero(self, level: int = 1, which: str = "f"):
         self._check(self._lib.kc_fill_zero(self._h, level, N.KC_WHICH_F if which == "f" else N.KC_WHICH_V))
 
-    OP_NAMES = ("relax", "restrict_residual", "zero_guess", "prolong_add", "coarsest", "bottom", "pre", "post")
+    OP_NAMES = ("relax", "restrict_residual", "zero_guess", "prolong_add", "coarsest", "bottom", "pre", "post",
+                "postpre")
 
     def profile_cycle(self, kappa: int) -> list[dict]:
         """One eager cycle with CUDA events around every scheduled op."""

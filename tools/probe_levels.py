@@ -1,10 +1,12 @@
 """Per-(level, op) eager timings of one kappa-cycle (CUDA events around each
-scheduled op), several reps, min over reps.  Usage: probe_levels.py N KAPPA"""
-import sys, collections, numpy as np
+scheduled op), several reps, min over reps.  Usage: probe_levels.py N KAPPA [exact|fast]"""
+import os, sys, collections, numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2010_00626_b200 as kc
 
 n = int(sys.argv[1]); k = int(sys.argv[2])
-st = kc.build_state(kc.ProblemSpec(1e-4, 45.0, seed=0), kc.CycleConfig(n=n, kappa=k))
+arith = sys.argv[3] if len(sys.argv) > 3 else "exact"
+st = kc.build_state(kc.ProblemSpec(1e-4, 45.0, seed=0), kc.CycleConfig(n=n, kappa=k), arith=arith)
 m = 2 ** n - 1
 st.v[0] = np.random.default_rng(0).random((m, m))
 best = {}
