@@ -157,6 +157,10 @@ struct kc_handle {
   bool tile = true;           // overlapped-tile kernels on the mid-size levels
   bool pdl = true;            // programmatic dependent launch around the bottom kernel (KC_PDL=0: off)
   bool postpre = true;        // fused sibling post+pre passes on the column-tile levels (KC_POSTPRE=0: off)
+  // the streaming k_postpre on 1023^2 and up (KC_POSTPRE_STREAM=1: on): bit-exact,
+  // but as slow as the two passes it replaces (2047^2: 57 vs 32 + 27 us;
+  // these passes are issue-bound, not traffic-bound), so off by default
+  bool postpre_stream = false;
   bool ks_sym_on = true;      // shared w1/w7 products on symmetric levels (KC_SYM=0: off)
   int num_sms = 148;
   SolveState* d_solve = nullptr;   // device loop state
@@ -843,6 +847,12 @@ int ex_ctile_pre(kc_handle* h, int l) {
 #ifndef KC_PP_TY
 #define KC_PP_TY 16  // rows per fused post+pre tile
 #endif
+#ifndef KC_PP_MAX_M
+#define KC_PP_MAX_M 511
+#endif
+#ifndef KC_PP_STREAM_MIN_M
+#define KC_PP_STREAM_MIN_M 1023  // streaming k_postpre on the larger levels
+#endif
 int ex_ctile_post(kc_handle* h, int l) {
   Level& L = h->L[l];
   Level& C = h->L[l + 1];
@@ -893,9 +903,40 @@ int ex_ctile_post(kc_handle* h, int l) {
 // post pass of a call + pre pass of the next call on level l, one launch
 // (k_ctile_postpre); the result of both (NU2 + NU1 sweeps) lands in the
 // other buffer, the restricted residual in the child's f
+int ex_postpre_stream(kc_handle* h, int l) {
+  Level& L = h->L[l];
+  int rc = ex_materialize(h, l + 1);
+  if (rc) return rc;
+  const bool z = L.vzero;
+  KsFn fn = nullptr;
+#define KS_PP(A, B) fn = z ? k_postpre<A, B, true> : k_postpre<A, B, false>
+  switch (h->nu2 * 3 + h->nu1) {
+    case 0: KS_PP(0, 0); break;
+    case 1: KS_PP(0, 1); break;
+    case 2: KS_PP(0, 2); break;
+    case 3: KS_PP(1, 0); break;
+    case 4: KS_PP(1, 1); break;
+    case 5: KS_PP(1, 2); break;
+    case 6: KS_PP(2, 0); break;
+    case 7: KS_PP(2, 1); break;
+    default: KS_PP(2, 2); break;
+  }
+#undef KS_PP
+  const int D = h->nu1 + h->nu2 + 1;
+  int nw = 0;
+  StreamParams p = ks_params(h, l, D, &nw, (const void*)fn);
+  fn<<<(nw + 3) / 4, 128, ks_smem_bytes(D), h->stream>>>(p);  // ks_params set the smem attribute
+  KC_LAUNCH_CHECK(h);
+  ++h->launches;
+  L.cur ^= 1;
+  L.vzero = false;
+  return KC_OK;
+}
+
 int ex_postpre(kc_handle* h, int l) {
   Level& L = h->L[l];
   Level& C = h->L[l + 1];
+  if (L.m > KC_PP_MAX_M) return ex_postpre_stream(h, l);
   TileParams p{};
   p.u = L.v[L.cur];
   p.f = L.f;
@@ -1048,12 +1089,11 @@ bool fusable(const kc_handle* h, int l) {
 // n = 12, FMA build) 255^2 7.4 vs 5.6 + 5.9 us, 511^2 12.2 vs 7.7 + 7.3 us,
 // but 1023^2 36 vs 12 + 14.5 us -- its 20-of-31-column tiles recompute too
 // much once the level is throughput-bound
-#ifndef KC_PP_MAX_M
-#define KC_PP_MAX_M 511
-#endif
 bool postpre_ok(const kc_handle* h, int l) {
   const Level& L = h->L[l];
-  return h->postpre && h->tile && L.m <= KC_PP_MAX_M && h->nu1 <= 2 && h->nu2 <= 2;
+  if (!h->postpre || h->nu1 > 2 || h->nu2 > 2) return false;
+  if (L.m <= KC_PP_MAX_M) return h->tile;
+  return h->postpre_stream && L.m >= KC_PP_STREAM_MIN_M;  // the streaming k_postpre above
 }
 
 void flatten(const kc_handle* h, int l, int kappa, std::vector<Op>& ops, int norms = 0) {
@@ -1374,6 +1414,8 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
     h->pdl = !(penv && penv[0] == '0');
     const char* ppenv = getenv("KC_POSTPRE");
     h->postpre = !(ppenv && ppenv[0] == '0');
+    const char* ppsenv = getenv("KC_POSTPRE_STREAM");
+    h->postpre_stream = ppsenv && ppsenv[0] == '1';
     const char* senv = getenv("KC_SYM");
     // the shared-product form only saves work when products are separately
     // rounded; in the FMA build every product is fused into its sum

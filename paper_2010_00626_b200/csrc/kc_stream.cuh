@@ -383,6 +383,119 @@ __global__ void __launch_bounds__(128, KS_MINB) k_post(const StreamParams p) {
   if (NORMS) ks_warp_partials(acc_e, acc_r, p.part, wg, lane);
 }
 
+// ---------------------------------------------------------------------------
+// POSTPRE: a routine call's post pass (v + P vc, NU2 sweeps; cycle.py:219-
+// 220) fused with the NEXT call's pre pass on the same level (NU1 sweeps,
+// residual, full weighting; cycle.py:211-213): the kappa-cycle's second
+// recursive call (cycle.py:215-218) starts where the first one ended, so the
+// intermediate v never leaves the chip.  Stage 0 is k_post's corrected input
+// row, stages 1..NS (NS = NU2 + NU1) are sweeps, stage D = NS + 1 the
+// residual, restricted as in k_pre; the chunk geometry is k_pre's.
+// ---------------------------------------------------------------------------
+#ifndef KS_MINB_PP
+#define KS_MINB_PP 3  // six stages' pending sums need more than 128 registers
+#endif
+template <int NU2, int NU1, bool VZ>
+__global__ void __launch_bounds__(128, KS_MINB_PP) k_postpre(const StreamParams p) {
+  constexpr int NS = NU2 + NU1;
+  constexpr int D = NS + 1;
+  using G = KsGeom<D>;
+  const int lane = threadIdx.x & 31;
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int band = wg % p.nbands, chunk = wg / p.nbands;
+  const int P0 = band * G::NPB, Q0 = chunk * p.nq;
+  if (Q0 > p.mc) return;  // whole warp
+  const int m = p.m, P = p.P;
+  const int XS = 2 * P0 - G::HL;
+  const int c0 = XS + 2 * lane;
+  const bool colx_in = c0 >= 0 && c0 < m, coly_in = c0 + 1 >= 0 && c0 + 1 < m;
+  const int pcol = c0 >> 1;  // coarse column of this lane (c0 even)
+  const bool own_lane = lane >= G::HL / 2 && lane < G::HL / 2 + G::NPB;
+  const St9 s = p.s;
+  KsAcc A[D + 1];
+#pragma unroll
+  for (int t = 0; t <= D; ++t) A[t].b = A[t].c = A[t].cen = make_double2(0.0, 0.0);
+  double2 R[3] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  double RE[3] = {0.0, 0.0, 0.0};
+  const int ys = 2 * Q0 - D;
+  const int ye = 2 * Q0 + 2 * p.nq + D;  // inclusive: residual row 2 (Q0 + nq)
+  const bool edge = XS < 0 || XS + KS_BAND - 1 >= m || ys - D - 2 < 0 || ye + 2 >= m;
+  auto rp = [&](int y) -> size_t { return kc_idx(P, min(max(y, -1), m), c0); };
+  auto ldc = [&](int q) -> double { return __ldg(p.vc + kc_idx(p.Pc, min(max(q, -1), p.mc), pcol)); };
+  int qcur = ys >> 1;  // arithmetic shift: floor
+  double vcp = ldc(qcur - 1), vcc = ldc(qcur), vcn = ldc(qcur + 1);
+  extern __shared__ double ks_smem[];
+  constexpr int FR = ks_fring(D);
+  double* ring = ks_smem + (threadIdx.x >> 5) * ks_warp_smem_doubles(D) + 2 * lane;
+  double* uring = ring;
+  double* fring = ring + KS_URING * KS_BAND;
+  auto fetch = [&](int y, bool with_u) {  // see k_pre: u only from row ys on
+    const size_t i = rp(y);
+    if (!VZ && with_u) ks_cp16(uring + (y & (KS_URING - 1)) * KS_BAND, p.u + i);
+    ks_cp16(fring + (y & (FR - 1)) * KS_BAND, p.f + i);
+    ks_cp_commit();
+  };
+  for (int y = ys - D; y < ys + KS_PF; ++y) fetch(y, y >= ys);
+#pragma unroll 1
+  for (int yin = ys; yin <= ye; ++yin) {
+    fetch(yin + KS_PF, true);
+    ks_cp_wait();
+    const double2 u0 = VZ ? make_double2(0.0, 0.0) : ks_lds2(uring + (yin & (KS_URING - 1)) * KS_BAND);
+    double2 fr[D + 1];
+#pragma unroll
+    for (int t = 1; t <= D; ++t) fr[t] = ks_lds2(fring + ((yin - t) & (FR - 1)) * KS_BAND);
+    const int q = yin >> 1;
+    if (q != qcur) {  // advance the coarse window by one row (yin even); warp-uniform
+      vcp = vcc;
+      vcc = vcn;
+      qcur = q;
+      vcn = ldc(q + 1);
+    }
+    // stage 0: prolongation + correction (transfer.py:50-58, cycle.py:174-176)
+    const double lp = kc_shfl_up1(vcp), lc = kc_shfl_up1(vcc);
+    double ex, ey;
+    if (yin & 1) {
+      ex = DMUL(0.5, DADD(lc, vcc));
+      ey = vcc;
+    } else {
+      ex = DMUL(0.25, DADD(DADD(DADD(lp, vcp), lc), vcc));
+      ey = DMUL(0.5, DADD(vcp, vcc));
+    }
+    double2 nw[D + 1];
+    nw[0] = make_double2(DADD(VZ ? 0.0 : u0.x, ex), DADD(VZ ? 0.0 : u0.y, ey));
+    if (edge) ks_mask(nw[0], yin, m, colx_in, coly_in);
+#pragma unroll
+    for (int t = 1; t <= D; ++t) {
+      double ax, ay;
+      double2 cen;
+      ks_step<false>(s, A[t], nw[t - 1], ax, ay, cen);
+      const double rx = DSUB(fr[t].x, ax), ry = DSUB(fr[t].y, ay);
+      if (t <= NS) nw[t] = make_double2(DADD(cen.x, DMUL(s.c, rx)), DADD(cen.y, DMUL(s.c, ry)));
+      else nw[t] = make_double2(rx, ry);
+      if (edge) ks_mask(nw[t], yin - t, m, colx_in, coly_in);
+    }
+    // restriction of the residual rows yr-2, yr-1, yr (yr = yin - D)
+    R[0] = R[1];
+    R[1] = R[2];
+    R[2] = nw[D];
+    RE[0] = RE[1];
+    RE[1] = RE[2];
+    RE[2] = kc_shfl_dn1(nw[D].x);
+    {
+      const int yr = yin - D;
+      const int qq = (yr >> 1) - 1;
+      if (!(yr & 1) && own_lane && qq >= Q0 && qq < Q0 + p.nq && qq < p.mc && qq >= 0 && pcol < p.mc)
+        p.fc[kc_idx(p.Pc, qq, pcol)] = kc_fw(R[0].x, R[0].y, RE[0], R[1].x, R[1].y, RE[1], R[2].x, R[2].y, RE[2]);
+    }
+    // v after all NS sweeps
+    {
+      const int y = yin - NS;
+      if (own_lane && y >= 2 * Q0 && y < 2 * Q0 + 2 * p.nq && y >= 0 && y < m)
+        *reinterpret_cast<double2*>(p.uo + kc_idx(P, y, c0)) = nw[NS];
+    }
+  }
+}
+
 // deterministic final sum of the per-warp partials: out[0] = sqrt(sum e), out[1] = sqrt(sum r)
 __global__ void __launch_bounds__(256) k_norms_final(const double* __restrict__ part, int nw, double* __restrict__ out) {
   __shared__ double sh[2][8];

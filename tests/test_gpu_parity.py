@@ -773,3 +773,31 @@ def test_shared_product_passes_bit_exact(monkeypatch):
     a, b = out["1"], out["0"]
     assert a[:4] == b[:4]
     assert np.array_equal(a[4], b[4])
+
+
+@pytest.mark.parametrize("stream_pp", ["0", "1"])
+@pytest.mark.parametrize("kappa", [2, 3])
+def test_fused_sibling_passes_bit_exact(stream_pp, kappa, monkeypatch):
+    """k_ctile_postpre (255^2 / 511^2, default) and the streaming k_postpre
+    (1023^2 and up, KC_POSTPRE_STREAM=1) replace a call's post pass and the
+    next call's pre pass: the cycle's iterate stays the reference's, bit for
+    bit, and equals the unfused engine's."""
+    n = 11
+    m = 2 ** n - 1
+    rng = np.random.default_rng(31 + kappa)
+    v0, f0 = rng.random((m, m)), rng.standard_normal((m, m))
+    h = O.Hierarchy(O.hierarchy(1e-4, 45.0, n))
+    h.v[0], h.f[0] = v0.copy(), f0.copy()
+    h.cycle(kappa)
+    cfg = CycleConfig(n=n, kappa=kappa)
+    out = {}
+    for pp in ("1", "0"):
+        monkeypatch.setenv("KC_POSTPRE", pp)
+        monkeypatch.setenv("KC_POSTPRE_STREAM", stream_pp)
+        st = build_state(ProblemSpec(1e-4, 45.0), cfg)
+        st.v[0], st.f[0] = v0, f0
+        run_cycle(st, cfg, CycleStats.for_levels(n))
+        out[pp] = st.v[0]
+        st.close()
+    assert np.array_equal(out["1"], h.v[0])
+    assert np.array_equal(out["0"], h.v[0])
