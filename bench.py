@@ -564,6 +564,20 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # over the algorithmic bytes B(kappa, n) of the fused decomposition
     side = lambda lev: 2 ** (n - lev + 1) - 1  # noqa: E731
     coarse_ms = sum(p["ms"] for p in prof if side(p["level"]) <= 511)
+    # the eager profile charges every op its launch/event overhead (~2.6 us,
+    # tools/probe_levels.py: a zero_guess flag op costs that much), which
+    # inflates the many small coarse ops; the in-graph estimate subtracts the
+    # fine levels' eager time (few, long ops) from the graph-timed cycle
+    def coarse_split(kname):
+        kk = n if kname == "W" else int(kname)
+        state.restore()
+        pr = min((state.profile_cycle(kk) for _ in range(3)), key=lambda ps: sum(q["ms"] for q in ps))
+        tot = sum(q["ms"] for q in pr)
+        fine = sum(q["ms"] for q in pr if side(q["level"]) > 511)
+        cyc = sweep[best_arith][kname]["ms_per_cycle"]
+        return {"eager": (tot - fine) / tot if tot else None,
+                "in_graph_estimate": max(0.0, cyc - fine) / cyc if cyc else None, "cycle_ms": cyc}
+    coarse_by_kappa = {kk: coarse_split(kk) for kk in dict.fromkeys(("2", best)) if kk in sweep[best_arith]}
     nu = 4
     calls = [kc.costmodel.level_calls(math.inf if best == "W" else kbest, lev) for lev in range(1, n + 1)]
     b_cycle = sum(calls[lev - 1] * ((24 * nu + 16) * side(lev) ** 2 + 16 * side(lev + 1) ** 2)
@@ -651,6 +665,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                "per_kappa_estimate_ms": {kk: 1e3 * v for kk, v in est.items()}}
 
     build_info = None
+    libs = {}
+    for name in ("libkcb200.so", "libkcb200_fast.so"):
+        lp = os.path.join(ROOT, "paper_2010_00626_b200", name)
+        if os.path.exists(lp):
+            import hashlib
+            with open(lp, "rb") as fh:
+                libs[name] = {"sha256_16": hashlib.sha256(fh.read()).hexdigest()[:16], "mtime": os.path.getmtime(lp)}
     bpath = os.path.join(ROOT, "build", "build_info.json")
     if os.path.exists(bpath):
         with open(bpath) as fh:
@@ -681,6 +702,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "cycle_profile": {"eager_cycle_ms": cycle_ms_eager, "bottom_kernel_ms": bottom_ms,
                               "per_level_ms": per_level,
                               "coarse_fraction_le511": coarse_ms / cycle_ms_eager if cycle_ms_eager else None,
+                              "coarse_fraction_le511_by_kappa": coarse_by_kappa,
                               "algorithmic_bytes_per_cycle": b_cycle,
                               "survey_convention_gbs": (b_cycle / (ms_per_step / cycles * 1e-3) / 1e9
                                                         if cycles else None),
@@ -694,7 +716,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                                             "moves 48 N_l + 16 N_l+1 per call (fused_bytes_per_cycle), and "
                                             "fused_cycle_frac_of_hbm_peak is the physical cycle utilisation "
                                             "(levels <= 2047^2 are largely L2-resident)"},
-            "build": build_info,
+            "build": build_info, "libraries": libs,
         }
         print(json.dumps(line), flush=True)
     for st in states.values():
