@@ -77,6 +77,7 @@ struct BotLv {
   int a, R, rb4, crows;          // first global row, strip height, RB = 4?, own rows of the child
   float inv, invc, invn;         // 1/m, 1/m_child, 1/(m_child+1)
   int mc;                        // child side
+  int hb;                        // halo rows each side (1; KC_DEEP_HB on the deep-halo strip level)
 };
 
 struct BotParams {
@@ -92,6 +93,7 @@ struct BotParams {
   int nu1, nu2;      // sweeps inside PH_TINY frames
   int nstrip;        // leading levels split into row strips over the cluster (0: single CTA)
   int total;         // shared-memory doubles of all levels (bot_smem_doubles)
+  int deep;          // the deep-halo strip level (PH_FRAME63), or -1
   BotLv lv[KC_BOT_MAXLEV];  // bot_geometry (rank 0's strip rows)
   // side-15 frame operators (KC_FAST cluster launches; see "Frame operators"
   // below): blocks (kap - 1) * 2 + part of [A_kap | B_kap], 225 x KC_MV_LD
@@ -131,16 +133,21 @@ __host__ __device__ __forceinline__ int bot_m(int m0, int d) { return ((m0 + 1) 
 __host__ __device__ __forceinline__ int bot_rows(int m0, int d, int nstrip, int cs) {
   return d < nstrip ? (bot_m(m0, d) + 1) / cs : bot_m(m0, d);
 }
-__host__ __device__ __forceinline__ int bot_off(int m0, int d, int nstrip = 0, int cs = 1) {
+// halo rows each side of level d: KC_DEEP_HB on the deep-halo strip level
+// (PH_FRAME63 computes its stages on the halo rows redundantly), else 1
+#define KC_DEEP_HB 4
+__host__ __device__ __forceinline__ int bot_hb(int d, int deep) { return d == deep ? KC_DEEP_HB : 1; }
+__host__ __device__ __forceinline__ int bot_off(int m0, int d, int nstrip = 0, int cs = 1, int deep = -1) {
   int off = 0;
   for (int j = 0; j < d; ++j) {
     const int s = bot_m(m0, j) + 2;
-    off += 3 * (bot_rows(m0, j, nstrip, cs) + 2) * s;
+    off += 3 * (bot_rows(m0, j, nstrip, cs) + 2 * bot_hb(j, deep)) * s;
   }
   return off;
 }
-__host__ __device__ __forceinline__ int bot_smem_doubles(int m0, int nlev, int nstrip = 0, int cs = 1) {
-  return bot_off(m0, nlev, nstrip, cs);
+__host__ __device__ __forceinline__ int bot_smem_doubles(int m0, int nlev, int nstrip = 0, int cs = 1,
+                                                         int deep = -1) {
+  return bot_off(m0, nlev, nstrip, cs, deep);
 }
 __host__ __device__ __forceinline__ int bot_warps(int m) {
   return m >= 31 ? KC_BOT_WARPS : (m >= 15 ? 8 : 1);  // 2 warps at m = 7 measured slower
@@ -150,10 +157,11 @@ __host__ __device__ __forceinline__ int bot_warps(int m) {
 // what the kernel used to derive with integer divisions in its prologue.
 inline void bot_geometry(BotParams& bp, int m0, int cs) {
   const int nlev = bp.nlev, nstrip = bp.nstrip;
-  bp.total = bot_smem_doubles(m0, nlev, nstrip, cs);
+  bp.total = bot_smem_doubles(m0, nlev, nstrip, cs, bp.deep);
   for (int d = 0; d < nlev; ++d) {
     const bool strip = d < nstrip;
-    const int m = bot_m(m0, d), S = m + 2, base = bot_off(m0, d, nstrip, cs);
+    const int hb = bot_hb(d, bp.deep);
+    const int m = bot_m(m0, d), S = m + 2, base = bot_off(m0, d, nstrip, cs, bp.deep);
     const int R = bot_rows(m0, d, nstrip, cs);
     const int mc = d + 1 < nlev ? bot_m(m0, d + 1) : 1;
     BotLv L{};
@@ -163,9 +171,10 @@ inline void bot_geometry(BotParams& bp, int m0, int cs) {
     L.mc = mc;
     L.a = 0;
     L.rows = strip ? (R < m ? R : m) : m;
-    L.vo0 = base + S + 1;
-    L.vo1 = base + (R + 2) * S + S + 1;
-    L.fo = base + 2 * (R + 2) * S + S + 1;
+    L.hb = hb;
+    L.vo0 = base + hb * S + 1;
+    L.vo1 = base + (R + 2 * hb) * S + hb * S + 1;
+    L.fo = base + 2 * (R + 2 * hb) * S + hb * S + 1;
     L.nitem1 = L.rows * m;
     L.nitem4 = m * ((L.rows + 3) / 4);
     // RB = 4 where a thread would otherwise run more than one item: a full
@@ -223,7 +232,8 @@ __device__ __forceinline__ void kc_bot_mark(int k) {
 // tiny frames replaced them.)
 enum BotOp {
   PH_JACOBI = 0, PH_RESID = 1, PH_RESTRICT = 2, PH_PROLONG = 3, PH_JOIN = 4, PH_J2Z = 5, PH_TINY = 8, PH_CSYNC = 9,
-  PH_FRAME31 = 10  // a whole kappa_cycle frame on the replicated side-31 level (BotFrame31)
+  PH_FRAME31 = 10,  // a whole kappa_cycle frame on the replicated side-31 level (BotFrame31)
+  PH_FRAME63 = 11   // the pair of calls (kappa, kappa - 1) on the deep-halo side-63 strips (BotFrame63)
 };
 #ifndef KC_BOT_TINY_M
 #define KC_BOT_TINY_M 15  // frames on sides <= this run as PH_TINY (side 15 on 8 warps)
@@ -301,6 +311,7 @@ struct BotBuilder {  // host side
     }
   }
   bool frame31 = true;      // whole side-31 frames as PH_FRAME31 (replicated levels)
+  int deep = -1;            // the deep-halo strip level: its call pairs as PH_FRAME63
   void rec(int d, int kap) {
     if (frame31 && fuse && !dry && d >= nstrip && bot_m(m0, d) == 31 && d + 5 == nlev && kap <= 15) {
       // one descriptor for the frame and everything below it; the dry replay
@@ -368,8 +379,18 @@ struct BotBuilder {  // host side
       vz &= ~(1u << (d + 1));  // both coarsest calls: one f/center inside the restriction
     } else {
       vz |= 1u << (d + 1);
-      rec(d + 1, kap);
-      if (kap > 1) rec(d + 1, kap - 1);
+      if (d + 1 == deep && !dry) {
+        // both calls on the deep-halo level as one descriptor (every CTA);
+        // the dry replay follows BotFrame63, which follows these rules
+        emit(PH_FRAME63, d + 1, (cur >> (d + 1)) & 1u, 1, 0, 0, kap);
+        dry = true;
+        rec(d + 1, kap);
+        if (kap > 1) rec(d + 1, kap - 1);
+        dry = false;
+      } else {
+        rec(d + 1, kap);
+        if (kap > 1) rec(d + 1, kap - 1);
+      }
     }
     emit(PH_PROLONG, d, (cur >> d) & 1u, (vz >> d) & 1u, (cur >> (d + 1)) & 1u, 0);
     vz &= ~(1u << d);
@@ -381,26 +402,28 @@ struct BotBuilder {  // host side
 // y = i / m for i < 2^12, m <= 64: float reciprocal, exact for these ranges
 __device__ __forceinline__ int bot_div(int i, float inv) { return (int)(((float)i + 0.5f) * inv); }
 
-// Halo pushes of a strip phase: values on own row 0 also go to the upper
-// neighbour's row R (its halo below), values on own row R-1 to the lower
-// neighbour's row -1.  Null for CTA-local levels and at the strip ends.
+// Halo pushes of a strip phase: values on own rows 0 .. hb-1 also go to the
+// upper neighbour's rows R .. R+hb-1 (its halo below), values on own rows
+// R-hb .. R-1 to the lower neighbour's rows -hb .. -1 (hb = the level's halo
+// depth).  Null for CTA-local levels and at the strip ends.
 struct BotPush {
-  double* up;
-  double* dn;
-  int last;
+  double* up;  // upper neighbour's row R (row y of this CTA -> its row R + y)
+  double* dn;  // lower neighbour's row 0 shifted by -R rows (row y -> its row y - R)
+  int lo, hi;  // rows y < lo go up, rows y >= hi go down
   __device__ __forceinline__ void put(double* o, int S, int y, int x, double v) const {
     o[y * S + x] = v;
-    if (up && y == 0) up[x] = v;
-    if (dn && y == last) dn[x] = v;
+    if (up && y < lo) up[y * S + x] = v;
+    if (dn && y >= hi) dn[y * S + x] = v;
   }
 };
 __device__ __forceinline__ BotPush bot_push(double* origin, const BotLv& L, bool strip, int rank, int cs) {
-  BotPush p{nullptr, nullptr, -1};
+  BotPush p{nullptr, nullptr, 0, 1 << 30};
   if (strip) {
     cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
     if (rank > 0) p.up = cl.map_shared_rank(origin, rank - 1) + L.R * L.S;
-    if (rank + 1 < cs) p.dn = cl.map_shared_rank(origin, rank + 1) - L.S;
-    p.last = L.R - 1;
+    if (rank + 1 < cs) p.dn = cl.map_shared_rank(origin, rank + 1) - L.R * L.S;
+    p.lo = L.hb;
+    p.hi = L.R - L.hb;
   }
   return p;
 }
@@ -832,7 +855,7 @@ struct BotFrame31 {
   __device__ __forceinline__ double* buf(const BotLv& L, int b) const { return sm + (b ? L.vo1 : L.vo0); }
   __device__ __forceinline__ void stencil(bool jac, bool zero, const double* u, double* o, const double* f,
                                           const St9& st) const {
-    const BotPush ps{nullptr, nullptr, -1};
+    const BotPush ps{nullptr, nullptr, 0, 1 << 30};
     bot_stencil<4>(jac, zero, u, o, f, M, M, S, 1.0f / (float)M, st, tid, KC_BOT_THREADS, M * ((M + 3) / 4), ps);
   }
   __device__ __forceinline__ void j2z(double* u, const double* f, const St9& st) const {
@@ -898,7 +921,7 @@ struct BotFrame31 {
     c = *slot;
     z = 0;
   }
-  __device__ void frame(int d, int kap, int& cur, int& vz) {
+  __device__ __forceinline__ void frame(int d, int kap, int& cur, int& vz) {
     const BotLv L = lv[d], C = lv[d + 1];
     const St9 st = tab[d];
     const int nu1 = bp->nu1, nu2 = bp->nu2;
@@ -945,6 +968,175 @@ struct BotFrame31 {
     relax(L, st, nu2, cur, vz);
   }
 };
+
+// PH_FRAME63: the pair of calls (kappa, kappa - 1) on the side-63 strip
+// level (cycle.py:215-218) with DEEP halos.  Each CTA owns R = 4 rows and
+// keeps KC_DEEP_HB = 4 halo rows each side, and computes every stage of a
+// call on as many halo rows as the later stages need -- redundantly, with
+// CTA barriers only -- so a call needs a cluster barrier only where data
+// must cross CTAs: the restriction into the replicated 31^2 level (broadcast)
+// and, for the continuing call, one exchange of v's rows before its sweeps
+// and one of the boundary rows after them (the parent's prolongation reads
+// one halo row).  Zero-guess call: J2Z on rows -3..R+2 (f halo 4), residual
+// on -1..R, restriction of the own coarse rows, the 31^2 frames (BotFrame31),
+// prolongation on -3..R+2, sweeps on -2..R+1 and -1..R.  Continuing call:
+// exchange v (depth 4), sweeps on -3..R+2 and -2..R+1, residual, restriction,
+// frames, prolongation on -2..R+1, sweeps on -1..R and 0..R-1, exchange of
+// the boundary rows.  Rows outside the domain are never written (they stay
+// the zero Dirichlet ghosts).  Same per-point arithmetic and buffer rules as
+// BotBuilder::rec_plain (nu1 = nu2 = 2): bit-identical to the strip phases.
+struct BotFrame63 {
+  static constexpr int M = 63, S = M + 2, R = 4, MC = 31, SC = MC + 2;
+  double* sm;
+  const BotLv* lv;
+  const St9* tab;
+  BotFrame31* f31;
+  int tid, rank, cs;
+  __device__ __forceinline__ double* buf(const BotLv& L, int b) const { return sm + (b ? L.vo1 : L.vo0); }
+  // items (y, x) of rows lo..hi clipped to the domain (local row y = global a + y)
+  template <class Fn>
+  __device__ __forceinline__ void rows_do(int a, int lo, int hi, Fn fn) const {
+    lo = max(lo, -a);
+    hi = min(hi, M - 1 - a);
+    const int n = (hi - lo + 1) * M;
+    for (int i = tid; i < n; i += KC_BOT_THREADS) {
+      const int yy = i / M;
+      fn(lo + yy, i - yy * M);
+    }
+  }
+  __device__ __forceinline__ void push_rows(double* u, int a, int ylo, int yhi) const {
+    // own rows ylo..yhi into both neighbours' halo rows (row y -> up R + y, down y - R)
+    cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+    double* up = rank > 0 ? cl.map_shared_rank(u, rank - 1) + R * S : nullptr;
+    double* dn = rank + 1 < cs ? cl.map_shared_rank(u, rank + 1) - R * S : nullptr;
+    rows_do(a, ylo, yhi, [&](int y, int x) {
+      const double v = u[y * S + x];
+      if (up) up[y * S + x] = v;
+      if (dn) dn[y * S + x] = v;
+    });
+  }
+  // the pre half of a call: sweeps (J2Z on a zero guess), residual,
+  // restriction broadcast into the child's replicas; returns the rows on
+  // which v after the sweeps is valid (lo = -hi + R - 1)
+  __device__ __forceinline__ int pre(int d, int cur, bool zero) {
+    const BotLv L = lv[d];
+    const St9 st = tab[d];
+    const int a = rank * R;
+    const double* f = sm + L.fo;
+    double* u = buf(L, cur);
+    double* w = buf(L, cur ^ 1);
+    int lo;
+    if (zero) {
+      rows_do(a, -3, R + 2, [&](int y, int x) { u[y * S + x] = bot_j2z_pt(f + y * S + x, S, st); });
+      __syncthreads();
+      lo = -3;
+    } else {
+      // v of the previous call, depth 4, into the neighbours' halo rows --
+      // after a barrier: a neighbour may still be using those rows for the
+      // previous call's prolongation and sweeps
+      clu_sync();
+      push_rows(u, a, 0, R - 1);
+      clu_sync();
+      rows_do(a, -3, R + 2, [&](int y, int x) {
+        const int i = y * S + x;
+        w[i] = kc_jacobi_pt(u[i], f[i], kc_apply9(u + i, S, st), st.c);
+      });
+      __syncthreads();
+      rows_do(a, -2, R + 1, [&](int y, int x) {
+        const int i = y * S + x;
+        u[i] = kc_jacobi_pt(w[i], f[i], kc_apply9(w + i, S, st), st.c);
+      });
+      __syncthreads();
+      lo = -2;
+    }
+    // residual into the other buffer, restriction of the own coarse rows into
+    // every CTA's replica of the child level
+    rows_do(a, -1, R, [&](int y, int x) {
+      const int i = y * S + x;
+      w[i] = DSUB(f[i], kc_apply9(u + i, S, st));
+    });
+    __syncthreads();
+    {
+      cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+      double* fc = sm + lv[d + 1].fo + (a / 2) * SC;  // this strip's first coarse row
+      const int n = L.crows * MC;
+      for (int i = tid; i < n; i += KC_BOT_THREADS) {
+        const int q = i / MC, p = i - q * MC;
+        const double* rc = w + (2 * q + 1) * S + (2 * p + 1);
+        const double* rs = rc - S;
+        const double* rn = rc + S;
+        const double fv = kc_fw(rs[-1], rs[0], rs[1], rc[-1], rc[0], rc[1], rn[-1], rn[0], rn[1]);
+        for (int k = 0; k < cs; ++k) *cl.map_shared_rank(fc + q * SC + p, k) = fv;
+      }
+    }
+    clu_sync();
+    return lo;
+  }
+  // the post half: prolongation from the child's local replica (buffer c),
+  // two sweeps; the continuing call then exchanges its boundary rows
+  __device__ __forceinline__ void post(int d, int cur, int c, int lo, bool zero) {
+    const BotLv L = lv[d];
+    const St9 st = tab[d];
+    const int a = rank * R, hi = R - 1 - lo;
+    const double* f = sm + L.fo;
+    double* u = buf(L, cur);
+    double* w = buf(L, cur ^ 1);
+    {
+      const double* vc = buf(lv[d + 1], c);
+      auto cp = [&](int q, int pc) { return vc[q * SC + pc]; };
+      rows_do(a, lo, hi, [&](int y, int x) {
+        const int i = y * S + x;
+        u[i] = DADD(u[i], kc_prolong_val(a + y, x, cp));
+      });
+    }
+    __syncthreads();
+    rows_do(a, lo + 1, hi - 1, [&](int y, int x) {
+      const int i = y * S + x;
+      w[i] = kc_jacobi_pt(u[i], f[i], kc_apply9(u + i, S, st), st.c);
+    });
+    __syncthreads();
+    rows_do(a, lo + 2, hi - 2, [&](int y, int x) {
+      const int i = y * S + x;
+      u[i] = kc_jacobi_pt(w[i], f[i], kc_apply9(w + i, S, st), st.c);
+    });
+    __syncthreads();
+    if (!zero) {  // the parent's prolongation reads one halo row each side
+      clu_sync();   // (the neighbours' post sweeps read their halo rows)
+      push_rows(u, a, 0, 0);
+      push_rows(u, a, R - 1, R - 1);
+      clu_sync();
+    }
+  }
+  // both calls; one inlined site of each half and of the child frame
+  __device__ __forceinline__ void pair(int d, int kap, int cur) {
+    for (int i = 0; i < (kap > 1 ? 2 : 1); ++i) {
+      const bool zero = i == 0;
+      const int lo = pre(d, cur, zero);
+      int c = 0, z = 1;  // the child's zero guess (cycle.py:214)
+      for (int j = 0; j < (kap - i > 1 ? 2 : 1); ++j) f31->frame(d + 1, kap - i - j, c, z);
+      post(d, cur, c, lo, zero);
+    }
+  }
+};
+
+// The compile-time frames, out of line so that the interpreter loop of
+// k_bottom does not carry their registers: PH_FRAME31 (one call on the
+// replicated side-31 level) or PH_FRAME63 (the call pair on the deep-halo
+// side-63 strips).  mvs: the frame-operator bookkeeping (mv_last, mv_sync).
+__device__ __forceinline__ void bot_run_frame(int op, double* sm, const BotLv* lv, const St9* tab, const BotParams* bp,
+                                           int d, int kap, int src, int zero, int rank, int cs, int nlev, int* slot,
+                                           int* tiny_child, int* mvs) {
+  BotFrame31 fr{sm, lv, tab, bp, (int)threadIdx.x, rank, cs, nlev, slot, tiny_child, mvs[0], mvs[1] != 0};
+  if (op == PH_FRAME63) {
+    BotFrame63 f63{sm, lv, tab, &fr, (int)threadIdx.x, rank, cs};
+    f63.pair(d, kap, src);
+  } else {
+    int cur = src, vz = zero;
+    fr.frame(d, kap, cur, vz);
+  }
+  mvs[0] = fr.mv_last;
+  mvs[1] = fr.mv_sync ? 1 : 0;
+}
 
 // Columns of the side-15 frame operators: CTA (j, k - 1) runs BotTiny::frame
 // (the bottom kernel's own frame code) with counter k on the unit input j
@@ -1172,7 +1364,7 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
       const BotLv C = lv[d + 1];
       double* fc = sm + C.fo;
       double* vc = sm + C.vo0;
-      BotPush ps{nullptr, nullptr, -1};
+      BotPush ps{nullptr, nullptr, 0, 1 << 30};
       if (strip && d + 1 >= nstrip) {  // into every CTA's replica of the first replicated level
         bot_restrict_bcast(zero ? f : u, L, fc + (L.a / 2) * C.S, C.m, C.S, tid, nth, cs);
       } else {
@@ -1190,12 +1382,11 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
       if (strip)  // from this CTA's replica of the child, at this strip's first coarse row
         vc += (L.a / 2) * C.S;
       bot_prolong(u, vc, L, C.m, C.S, zero, tid, nth, bot_push(u, L, strip, rank, cs));
-    } else if (op == PH_FRAME31) {  // every thread of every CTA, on its replica
-      BotFrame31 fr{sm, lv, tab, &bp, tid, rank, cs, nlev, &f31_slot, tiny_child, mv_last, mv_sync};
-      int cur = src, vz = zero;
-      fr.frame(d, BD_KAP(e), cur, vz);
-      mv_last = fr.mv_last;
-      mv_sync = fr.mv_sync;
+    } else if (op == PH_FRAME63 || op == PH_FRAME31) {  // every thread of every CTA
+      int mvs[2] = {mv_last, mv_sync ? 1 : 0};
+      bot_run_frame(op, sm, lv, tab, &bp, d, BD_KAP(e), src, zero, rank, cs, nlev, &f31_slot, tiny_child, mvs);
+      mv_last = mvs[0];
+      mv_sync = mvs[1] != 0;
     } else if (strip) {  // PH_TINY as a frame operator (all CTAs; FMA build)
       bot_mv_frame(sm, bp, L, src, BD_CBUF(e), zero, BD_KAP(e), rank, cs);
       mv_last = BD_CBUF(e);

@@ -521,6 +521,7 @@ int get_bot_sched(kc_handle* h, int k1, int k2, int vzero, const unsigned** dev,
     b.vz = vzero ? 1u : 0u;
     b.nstrip = h->bot_base.nstrip;
     b.mv_mask = (unsigned)h->mv_resident;
+    b.deep = h->bot_base.deep;
     if (b.nlev > 1) {
       b.rec(0, k1);
       if (k2 > 0) b.rec(0, k2);
@@ -563,6 +564,7 @@ int setup_frame_operators(kc_handle* h, const cudaDeviceProp& prop) {
     if (bot_m(h->bot_m0, d) == KC_MV_M) d15 = d;
   if (d15 < bp.nstrip || d15 + 4 != bp.nlev) return KC_OK;
   BotParams tp{};
+  tp.deep = -1;
   tp.nlev = 4;
   tp.nu1 = h->nu1;
   tp.nu2 = h->nu2;
@@ -1487,7 +1489,7 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
   // at side <= 255 with the sides >= 31 in row strips, else one CTA
   // entering at side <= 63 (kc_bottom.cuh); KC_BOT_CLUSTER=0 forces one CTA.
   // Only the Jacobi / full-coarsening path has fused kernels.
-  int lb = -1, cs = 1, nstrip = 0;
+  int lb = -1, cs = 1, nstrip = 0, deep = -1;
   size_t smem = 0;
   if (smoother_kind == KC_SMOOTH_JACOBI && coarsening == KC_COARSEN_FULL) {
     cudaFuncAttributes fa{};
@@ -1503,6 +1505,8 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
     const int clu_max = eenv ? std::min(atoi(eenv), KC_CLU_MAX_M) : KC_CLU_ENTRY_M;
     const char* csenv = getenv("KC_BOT_CS");
     const int cs_first = csenv && atoi(csenv) == 8 ? 8 : 16;
+    const char* denv = getenv("KC_DEEP");
+    const bool use_deep = !(denv && denv[0] == '0');
     // smallest strip side (KC_BOT_MINSTRIP overrides): coarser levels live in CTA 0
     const char* msenv = getenv("KC_BOT_MINSTRIP");
     const int min_strip = msenv ? std::max(atoi(msenv), 31) : KC_CLU_MIN_STRIP;
@@ -1519,7 +1523,10 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
           ++ns;
         }
         if (ns == 0) break;  // coarser entries have no strips either
-        const size_t bytes = sizeof(double) * (size_t)bot_smem_doubles(m0, nl, ns, csz);
+        // deep halos on the 63^2 strips (PH_FRAME63): 16 CTAs of 4 rows,
+        // entry 127^2, the 31^2 level replicated below, nu = (2, 2)
+        const int dp = (use_deep && csz == 16 && m0 == 127 && ns == 2 && nl == 7 && nu1 == 2 && nu2 == 2) ? 1 : -1;
+        const size_t bytes = sizeof(double) * (size_t)bot_smem_doubles(m0, nl, ns, csz, dp);
         if (bytes > smem_max) continue;
         if (bot_smem_attr(bytes) != cudaSuccess) continue;
         cudaLaunchConfig_t cfg = {};
@@ -1542,6 +1549,7 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
         cs = csz;
         nstrip = ns;
         smem = bytes;
+        deep = dp;
       }
     }
     cudaGetLastError();
@@ -1561,6 +1569,7 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
     bp.nu1 = nu1;
     bp.nu2 = nu2;
     bp.nstrip = nstrip;
+    bp.deep = deep;
     for (int j = 0; j < bp.nlev; ++j) bp.st[j] = h->L[lb + j].st;
     h->bot_m0 = h->L[lb].m;
     h->bot_cs = cs;

@@ -33,6 +33,9 @@ int main(int argc, char** argv) {
   // argv[5] = 1: side-15 frame operators (FMA build; dummy matrix values),
   // the five blocks B1, B2, A1, B3, A2 resident
   const bool mv = argc > 5 && atoi(argv[5]) != 0;
+  // argv[6] = 1: deep halos on the 63^2 strips (PH_FRAME63; entry 127, 16 CTAs)
+  bp.deep = (argc > 6 && atoi(argv[6]) != 0 && cs == 16 && m0 == 127 && nstrip == 2) ? 1 : -1;
+  b.deep = bp.deep;
   bp.nu1 = 2; bp.nu2 = 2; bp.nstrip = nstrip; bot_geometry(bp, m0, cs);
   if (mv) {
     double* mats; cudaMalloc(&mats, sizeof(double) * 6 * KC_MV_N * KC_MV_LD);
@@ -48,7 +51,7 @@ int main(int argc, char** argv) {
   cudaMemcpy(ds, b.out.data(), b.out.size() * 4, cudaMemcpyHostToDevice);
   bp.gv = gv; bp.gf = gf; bp.gP = P; bp.v_zero = 1; bp.sched = ds; bp.nsched = (int)b.out.size(); bp.final_cur = b.cur & 1;
   if (mv) bp.mv_xin = bp.mv_off + 5 * ((KC_MV_N + cs - 1) / cs) * KC_MV_LD;
-  size_t smem = sizeof(double) * (mv ? (size_t)(bp.mv_xin + 2 * KC_MV_N) : (size_t)bot_smem_doubles(m0, nlev, nstrip, cs));
+  size_t smem = sizeof(double) * (mv ? (size_t)(bp.mv_xin + 2 * KC_MV_N) : (size_t)bp.total);
   cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_bottom, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
@@ -103,8 +106,9 @@ int main(int argc, char** argv) {
     int o = op[i] / 16, d = op[i] % 16;
     sum[o][d] += t[i + 1] - t[i]; cmp[o][d] += te[i] - t[i]; cnt[o][d]++;
   }
-  const char* nm[11] = {"jacobi", "resid", "restrict", "prolong", "join", "j2z", "rr", "pj", "tiny", "csync", "frame31"};
-  for (int o = 0; o < 11; ++o) for (int d = 0; d < nlev; ++d) if (cnt[o][d])
+  const char* nm[12] = {"jacobi", "resid", "restrict", "prolong", "join", "j2z", "rr", "pj", "tiny", "csync", "frame31",
+                        "frame63"};
+  for (int o = 0; o < 12; ++o) for (int d = 0; d < nlev; ++d) if (cnt[o][d])
     printf("  %-9s level %d (m=%3d): %5d phases, %7.0f cycles avg (thread 0 to its barrier %5.0f), %9.0f total\n", nm[o], d,
            bot_m(m0, d), cnt[o][d], sum[o][d] / cnt[o][d], cmp[o][d] / cnt[o][d], sum[o][d]);
   printf("phases traced: %d, total cycles %lld\n", n, n > 1 ? t[n - 1] - t[0] : 0);
