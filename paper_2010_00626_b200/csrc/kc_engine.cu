@@ -1288,6 +1288,12 @@ int get_solve_graph(kc_handle* h, int kappa, SolveGraph** out) {
   for (int j = 1; j < h->n; ++j) h->L[j].cur = 0;
   SolveGraph sg;
   int rc = capture_ops(h, ops, 0, 1, &sg.pre, &sg.kernels_pre);
+  std::vector<int> s1_cur(h->n);  // the state after the pre op: where the loop body starts
+  std::vector<char> s1_vz(h->n);
+  for (int j = 0; j < h->n; ++j) {
+    s1_cur[j] = h->L[j].cur;
+    s1_vz[j] = h->L[j].vzero;
+  }
   if (rc == KC_OK) rc = capture_ops(h, ops, 1, ops.size(), &sg.rest, &sg.kernels_rest);
   sg.end_cur0 = L0.cur;
   for (int j = 0; j < h->n; ++j) {
@@ -1322,10 +1328,38 @@ int get_solve_graph(kc_handle* h, int kappa, SolveGraph** out) {
   wp.conditional.size = 1;
   KC_CUDA(h, cudaGraphAddNode(&wn, cg, &chk0, 1, &wp));
   cudaGraph_t body = wp.conditional.phGraph_out[0];
-  cudaGraphNode_t rest_node, pre_node, chk_node;
-  KC_CUDA(h, cudaGraphAddChildGraphNode(&rest_node, body, nullptr, 0, sg.rest));
-  KC_CUDA(h, cudaGraphAddChildGraphNode(&pre_node, body, &rest_node, 1, sg.pre));
-  KC_CUDA(h, cudaGraphAddKernelNode(&chk_node, body, &pre_node, 1, &kp));
+  const char* fenv = getenv("KC_FLATBODY");
+  if (fenv && fenv[0] == '0') {  // the body as three child-graph nodes (A/B)
+    cudaGraphNode_t rest_node, pre_node, chk_node;
+    KC_CUDA(h, cudaGraphAddChildGraphNode(&rest_node, body, nullptr, 0, sg.rest));
+    KC_CUDA(h, cudaGraphAddChildGraphNode(&pre_node, body, &rest_node, 1, sg.pre));
+    KC_CUDA(h, cudaGraphAddKernelNode(&chk_node, body, &pre_node, 1, &kp));
+  } else {
+    // the body captured straight into the conditional node's graph: one
+    // flat chain of kernel nodes (rest of the cycle, pre, check) instead of
+    // child-graph nodes
+    for (int j = 0; j < h->n; ++j) {
+      h->L[j].cur = s1_cur[j];
+      h->L[j].vzero = s1_vz[j];
+    }
+    const int l0 = h->launches;
+    KC_CUDA(h, cudaStreamBeginCaptureToGraph(h->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    for (size_t i = 1; i < ops.size() && rc == KC_OK; ++i) rc = ex_op(h, ops[i]);
+    if (rc == KC_OK) rc = ex_op(h, ops[0]);
+    if (rc == KC_OK) {
+      k_stop_check<<<1, 32, 0, h->stream>>>(h_loop, h_none, set_rest, st, scal);
+      if (cudaGetLastError() != cudaSuccess) rc = KC_ECUDA;
+    }
+    cudaGraph_t same = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(h->stream, &same);
+    h->launches = l0;
+    for (int j = 0; j < h->n; ++j) {
+      h->L[j].cur = save_cur[j];
+      h->L[j].vzero = save_vz[j];
+    }
+    if (rc) return rc;
+    if (ce != cudaSuccess) KC_FAIL(h, KC_ECUDA, "loop body capture: %s", cudaGetErrorString(ce));
+  }
   KC_CUDA(h, cudaGraphInstantiate(&sg.exec, cg, 0));
   sg.graph = cg;
   auto ins = h->solve_graphs.emplace(key, sg);

@@ -526,9 +526,13 @@ __global__ void __launch_bounds__(256) k_norms_final(const double* __restrict__ 
 }
 
 // Deterministic sum of n (a, b) pairs over KS_NB blocks; the last block to
-// finish adds the block sums in order: out = (sum a, sum b), square roots
-// taken when SQRT.
-#define KS_NB 32
+// finish adds the block sums with a fixed-order tree: out = (sum a, sum b),
+// square roots taken when SQRT.  (32 blocks and a one-thread serial final
+// sum: ~3 us more per stand-alone iteration.)
+#ifndef KS_NB
+#define KS_NB 148
+#endif
+static_assert(KS_NB <= 256, "one block sum per thread in the final tree");
 template <bool SQRT>
 __global__ void __launch_bounds__(256) k_norms_lanes(const double2* __restrict__ part, int n, double2* __restrict__ bsum,
                                                      unsigned* __restrict__ counter, double* __restrict__ out) {
@@ -563,16 +567,32 @@ __global__ void __launch_bounds__(256) k_norms_lanes(const double2* __restrict__
     last = atomicAdd(counter, 1u) == KS_NB - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    double ta = 0.0, tb = 0.0;
-    for (int k = 0; k < KS_NB; ++k) {
-      const double2 v = __ldcg(bsum + k);  // L2: written by other blocks
-      ta += v.x;
-      tb += v.y;
+  if (!last) return;  // block-uniform
+  __threadfence();
+  double ta = 0.0, tb = 0.0;
+  if (threadIdx.x < KS_NB) {
+    const double2 v = __ldcg(bsum + threadIdx.x);  // L2: written by other blocks
+    ta = v.x;
+    tb = v.y;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    ta += __shfl_down_sync(0xffffffffu, ta, o);
+    tb += __shfl_down_sync(0xffffffffu, tb, o);
+  }
+  __syncthreads();  // sh reused
+  if (lane == 0) {
+    sh[0][w] = ta;
+    sh[1][w] = tb;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sa = 0.0, sb = 0.0;
+    for (int k = 0; k < 8; ++k) {
+      sa += sh[0][k];
+      sb += sh[1][k];
     }
-    out[0] = SQRT ? sqrt(ta) : ta;
-    out[1] = SQRT ? sqrt(tb) : tb;
+    out[0] = SQRT ? sqrt(sa) : sa;
+    out[1] = SQRT ? sqrt(sb) : sb;
     *counter = 0u;
   }
 }
