@@ -188,15 +188,40 @@ inline void bot_geometry(BotParams& bp, int m0, int cs) {
   }
 }
 
+// Schedule perturbation (race testing; compute-sanitizer is closed on this
+// pool): the KC_BOT_JITTER builds (libkcb200*_jitter.so, tests only) make
+// about one warp in four sleep up to KC_BOT_JITTER ns right after every
+// barrier, so a missing barrier between a stage that writes data and one
+// that reads it (in this CTA or, through DSMEM, in another) shows up as a
+// wrong, non-reproducible result (tests/test_gpu_jitter.py).
+#ifdef KC_BOT_JITTER
+__device__ __forceinline__ void bot_jitter() {
+  unsigned h = (unsigned)clock64() ^ (blockIdx.x * 0x9E3779B9u) ^ ((threadIdx.x >> 5) * 0x85EBCA6Bu);
+  h ^= h >> 13;
+  h *= 0xC2B2AE35u;
+  h ^= h >> 16;
+  h = __shfl_sync(0xffffffffu, h, 0);  // warp-uniform
+  if ((h & 3u) == 0u) __nanosleep(h % KC_BOT_JITTER);
+}
+#else
+__device__ __forceinline__ void bot_jitter() {}
+#endif
+// a CTA barrier of the bottom kernel (with the jitter of the test builds)
+__device__ __forceinline__ void bot_bar() {
+  __syncthreads();
+  bot_jitter();
+}
 __device__ __forceinline__ void bot_sync(int g) {
-  if (g == KC_BOT_WARPS) __syncthreads();
+  if (g == KC_BOT_WARPS) bot_bar();
   else if (g == 1) __syncwarp();
   else if (g == 8) asm volatile("bar.sync 1, 256;" ::: "memory");
   else asm volatile("bar.sync 2, 64;" ::: "memory");
+  bot_jitter();
 }
 // every thread of every CTA of the cluster; orders the DSMEM stores before it
 __device__ __forceinline__ void clu_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  bot_jitter();
 }
 
 #ifdef KC_BOT_TRACE
@@ -688,6 +713,7 @@ struct BotTiny {
     if (nth == 32) __syncwarp();
     else if (nth == 64) asm volatile("bar.sync 2, 64;" ::: "memory");
     else asm volatile("bar.sync 1, 256;" ::: "memory");
+    bot_jitter();
   }
   __device__ __forceinline__ double* buf(const BotLv& L, int b) const { return sm + (b ? L.vo1 : L.vo0); }
   template <int M>
@@ -793,7 +819,7 @@ __device__ __forceinline__ void bot_mv_frame(double* sm, const BotParams& bp, co
   cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
   const int R = bp.mv_rows;
   asm volatile("cp.async.wait_all;" ::: "memory");  // the blocks (prologue copies)
-  __syncthreads();
+  bot_bar();
   const double* B = sm + bp.mv_off + bp.mv_slot[(kap - 1) * 2 + 1] * R * KC_MV_LD;
   const double* A = sm + bp.mv_off + bp.mv_slot[(kap - 1) * 2] * R * KC_MV_LD;
   const double* vin = sm + (src ? L.vo1 : L.vo0);  // this CTA's replica
@@ -805,7 +831,7 @@ __device__ __forceinline__ void bot_mv_frame(double* sm, const BotParams& bp, co
     xf[i] = fin[o];
     if (!zero) xv[i] = vin[o];
   }
-  __syncthreads();
+  bot_bar();
   double* out = sm + (ob ? L.vo1 : L.vo0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i0 = rank * R;
@@ -885,13 +911,13 @@ struct BotFrame31 {
     const double* f = sm + L.fo;
     if (count >= 2 && vz) {
       j2z(buf(L, cur), f, st);
-      __syncthreads();
+      bot_bar();
       vz = 0;
       i = 2;
     }
     for (; i < count; ++i) {
       stencil(true, vz, buf(L, cur), buf(L, cur ^ 1), f, st);
-      __syncthreads();
+      bot_bar();
       vz = 0;
       cur ^= 1;
     }
@@ -917,7 +943,7 @@ struct BotFrame31 {
       t.frame(d, kap, nlev, c, z, tiny_child);
       if (tid == 0) *slot = c;
     }
-    __syncthreads();
+    bot_bar();
     c = *slot;
     z = 0;
   }
@@ -929,7 +955,7 @@ struct BotFrame31 {
     const double* f = sm + L.fo;
     if (!vz) {
       stencil(false, false, buf(L, cur), buf(L, cur ^ 1), f, st);
-      __syncthreads();
+      bot_bar();
     }
     {  // full weighting into the child's f (transfer.py:78-83)
       const double* r = vz ? f : buf(L, cur ^ 1);
@@ -941,7 +967,7 @@ struct BotFrame31 {
         const double* rn = rc + S;
         fc[q * SC + p] = kc_fw(rs[-1], rs[0], rs[1], rc[-1], rc[0], rc[1], rn[-1], rn[0], rn[1]);
       }
-      __syncthreads();
+      bot_bar();
     }
     int c = 0, z = 1;  // the child's zero guess (cycle.py:214)
     frame15(d + 1, kap, c, z);
@@ -962,7 +988,7 @@ struct BotFrame31 {
           if (p < MC) pu[S + 1] = DADD(vz ? 0.0 : pu[S + 1], c11);
         }
       }
-      __syncthreads();
+      bot_bar();
     }
     vz = 0;
     relax(L, st, nu2, cur, vz);
@@ -1028,7 +1054,7 @@ struct BotFrame63 {
     int lo;
     if (zero) {
       rows_do(a, -3, R + 2, [&](int y, int x) { u[y * S + x] = bot_j2z_pt(f + y * S + x, S, st); });
-      __syncthreads();
+      bot_bar();
       lo = -3;
     } else {
       // v of the previous call, depth 4, into the neighbours' halo rows --
@@ -1041,12 +1067,12 @@ struct BotFrame63 {
         const int i = y * S + x;
         w[i] = kc_jacobi_pt(u[i], f[i], kc_apply9(u + i, S, st), st.c);
       });
-      __syncthreads();
+      bot_bar();
       rows_do(a, -2, R + 1, [&](int y, int x) {
         const int i = y * S + x;
         u[i] = kc_jacobi_pt(w[i], f[i], kc_apply9(w + i, S, st), st.c);
       });
-      __syncthreads();
+      bot_bar();
       lo = -2;
     }
     // residual into the other buffer, restriction of the own coarse rows into
@@ -1055,7 +1081,7 @@ struct BotFrame63 {
       const int i = y * S + x;
       w[i] = DSUB(f[i], kc_apply9(u + i, S, st));
     });
-    __syncthreads();
+    bot_bar();
     {
       cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
       double* fc = sm + lv[d + 1].fo + (a / 2) * SC;  // this strip's first coarse row
@@ -1089,17 +1115,17 @@ struct BotFrame63 {
         u[i] = DADD(u[i], kc_prolong_val(a + y, x, cp));
       });
     }
-    __syncthreads();
+    bot_bar();
     rows_do(a, lo + 1, hi - 1, [&](int y, int x) {
       const int i = y * S + x;
       w[i] = kc_jacobi_pt(u[i], f[i], kc_apply9(u + i, S, st), st.c);
     });
-    __syncthreads();
+    bot_bar();
     rows_do(a, lo + 2, hi - 2, [&](int y, int x) {
       const int i = y * S + x;
       u[i] = kc_jacobi_pt(w[i], f[i], kc_apply9(w + i, S, st), st.c);
     });
-    __syncthreads();
+    bot_bar();
     if (!zero) {  // the parent's prolongation reads one halo row each side
       clu_sync();   // (the neighbours' post sweeps read their halo rows)
       push_rows(u, a, 0, 0);
@@ -1153,17 +1179,17 @@ __global__ void __launch_bounds__(256) k_tiny_mats(const BotParams tp, double* _
     tab[threadIdx.x] = tp.st[threadIdx.x];
     lv[threadIdx.x] = tp.lv[threadIdx.x];
   }
-  __syncthreads();
+  bot_bar();
   const BotLv L0 = lv[0];
   if (threadIdx.x == 0) {
     const int jj = j % KC_MV_N, y = jj / KC_MV_M, x = jj - y * KC_MV_M;
     sm[(j < KC_MV_N ? L0.vo0 : L0.fo) + y * L0.S + x] = 1.0;
   }
-  __syncthreads();
+  bot_bar();
   const BotTiny t{sm, lv, tab, tp.nu1, tp.nu2, (int)threadIdx.x, 256};
   int cur = 0, vz = 0;
   t.frame(0, kap, 4, cur, vz, child);
-  __syncthreads();
+  bot_bar();
   const double* o = sm + (cur ? L0.vo1 : L0.vo0);
   double* blk = mats + (size_t)((kap - 1) * 2 + (j < KC_MV_N ? 0 : 1)) * KC_MV_N * KC_MV_LD;
   for (int i = threadIdx.x; i < KC_MV_N; i += 256) {
@@ -1288,7 +1314,7 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
     KC_BOT_MARK(1);
     clu_sync();  // every CTA initialised before any halo push lands
   } else {
-    __syncthreads();
+    bot_bar();
     KC_BOT_MARK(1);
     const int S = m0 + 2;
     double* v = sm + S + 1;
@@ -1302,7 +1328,7 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
+    bot_bar();
   }
 
   KC_BOT_MARK(2);
@@ -1376,7 +1402,7 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
       const double* vc = sm + (BD_CBUF(e) ? C.vo1 : C.vo0);
       if (strip && d + 1 < nstrip) {  // halo rows formed locally: no exchange (CTA barrier below)
         bot_prolong_ext(u, vc, L, C.m, C.S, zero, tid, nth);
-        __syncthreads();
+        bot_bar();
         continue;
       }
       if (strip)  // from this CTA's replica of the child, at this strip's first coarse row
@@ -1402,7 +1428,7 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
     if (strip) clu_sync();
     else bot_sync(g);
   }
-  __syncthreads();
+  bot_bar();
   KC_BOT_MARK(3);
   {
     const BotLv L = lv[0];
