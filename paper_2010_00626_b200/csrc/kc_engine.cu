@@ -344,7 +344,9 @@ int zebra_setup(kc_handle* h, const double* w) {
       const int n = axis == 0 ? L.m : L.ny;
       const HostZPlan hp = axis == 0 ? gtsv_plan(wl[3], wl[4], wl[5], n) : gtsv_plan(wl[1], wl[4], wl[7], n);
       L.zsing[axis] = hp.singular;
-      const size_t nd = hp.fact.size() + hp.d.size() + hp.du.size() + hp.dl.size();
+      std::vector<double> rd(hp.d.size());
+      for (size_t i = 0; i < rd.size(); ++i) rd[i] = 1.0 / hp.d[i];  // the FMA build's back substitution
+      const size_t nd = hp.fact.size() + hp.d.size() + hp.du.size() + hp.dl.size() + rd.size();
       const size_t bytes = sizeof(double) * (nd + 1) + hp.piv.size() + 16;
       KC_CUDA(h, cudaMalloc(&L.zmem[axis], bytes));
       std::vector<char> host(bytes, 0);
@@ -355,13 +357,13 @@ int zebra_setup(kc_handle* h, const double* w) {
         for (double x : v) hd[o++] = x;
         return at;
       };
-      const size_t of = put(hp.fact), od = put(hp.d), odu = put(hp.du), odl = put(hp.dl);
+      const size_t of = put(hp.fact), od = put(hp.d), odu = put(hp.du), odl = put(hp.dl), ord = put(rd);
       unsigned char* hpv = reinterpret_cast<unsigned char*>(hd + nd + 1);
       for (size_t i = 0; i < hp.piv.size(); ++i) hpv[i] = hp.piv[i];
       KC_CUDA(h, cudaMemcpy(L.zmem[axis], host.data(), bytes, cudaMemcpyHostToDevice));
       const double* dd = reinterpret_cast<const double*>(L.zmem[axis]);
       L.zp[axis] = ZPlan{dd + of, dd + od, dd + odu, dd + odl,
-                         reinterpret_cast<const unsigned char*>(dd + nd + 1), n};
+                         reinterpret_cast<const unsigned char*>(dd + nd + 1), n, dd + ord};
       // cross-line stencil: the line's row (x-lines) or column (y-lines) of
       // taps zeroed; y-lines accumulate in the transposed C order
       St9 off{};

@@ -34,7 +34,20 @@ struct ZPlan {
   const double* dl;
   const unsigned char* piv;
   int n;
+  const double* rd;  // 1 / d (the FMA build's back substitution multiplies)
 };
+
+// one back-substitution quotient: the exact build divides (dgtsv's
+// B(i) / D(i), correctly rounded); the FMA build multiplies by the
+// precomputed reciprocal (a ~100-cycle dependent division per line step
+// becomes one multiply; last-bit differences, tolerance parity)
+__device__ __forceinline__ double kz_quot(double x, const ZPlan& pl, int i) {
+#if KC_FAST
+  return DMUL(x, __ldg(pl.rd + i));
+#else
+  return __ddiv_rn(x, __ldg(pl.d + i));
+#endif
+}
 
 // rhs of the x-lines y = par, par + 2, ...: f - sum over rows y-1, y+1 (C order)
 __global__ void k_zebra_rhs_x(double* __restrict__ u, const double* __restrict__ f, int ny, int nx, int P, St9 off,
@@ -111,11 +124,11 @@ __device__ __forceinline__ void kz_gtsv_line(double* __restrict__ line, size_t s
     }
   }
   // ---- back substitution: B(i) = (B(i) - DU(i) B(i+1) - DL(i) B(i+2)) / D(i) ----
-  double b1 = __ddiv_rn(cur, __ldg(pl.d + n - 1));
+  double b1 = kz_quot(cur, pl, n - 1);
   line[(size_t)(n - 1) * stride] = b1;
   if (n < 2) return;
   // row n-2 was stored by the forward pass; it is re-read here
-  double b0 = __ddiv_rn(DSUB(line[(size_t)(n - 2) * stride], DMUL(__ldg(pl.du + n - 2), b1)), __ldg(pl.d + n - 2));
+  double b0 = kz_quot(DSUB(line[(size_t)(n - 2) * stride], DMUL(__ldg(pl.du + n - 2), b1)), pl, n - 2);
   line[(size_t)(n - 2) * stride] = b0;
   {
     double bv[2][KZ_CH], dv[2][KZ_CH], uv[2][KZ_CH], lv2[2][KZ_CH];
@@ -125,7 +138,7 @@ __device__ __forceinline__ void kz_gtsv_line(double* __restrict__ line, size_t s
         const int i = i0 - k;
         if (i >= 0) {
           bv[buf][k] = line[(size_t)i * stride];
-          dv[buf][k] = __ldg(pl.d + i);
+          dv[buf][k] = __ldg((KC_FAST ? pl.rd : pl.d) + i);
           uv[buf][k] = __ldg(pl.du + i);
           lv2[buf][k] = __ldg(pl.dl + i);
         }
@@ -142,8 +155,12 @@ __device__ __forceinline__ void kz_gtsv_line(double* __restrict__ line, size_t s
         for (int k = 0; k < KZ_CH; ++k) {
           const int i = ib - k;
           if (i >= 0) {
+#if KC_FAST
+            const double v = DMUL(DSUB(DSUB(bv[half][k], DMUL(uv[half][k], b0)), DMUL(lv2[half][k], b1)), dv[half][k]);
+#else
             const double v = __ddiv_rn(DSUB(DSUB(bv[half][k], DMUL(uv[half][k], b0)), DMUL(lv2[half][k], b1)),
                                        dv[half][k]);
+#endif
             line[(size_t)i * stride] = v;
             b1 = b0;
             b0 = v;
