@@ -82,7 +82,9 @@ struct Level {
   // zebra (kc_zebra.cuh): dgtsv plans of the x- and y-line systems, the
   // cross-line stencils (line row / column zeroed; the y one transposed)
   ZPlan zp[2]{};
+  ZPart zpart[2]{};  // the FMA build's partition-method plans (s = 0: none)
   void* zmem[2] = {nullptr, nullptr};
+  void* zpmem[2] = {nullptr, nullptr};
   bool zsing[2] = {false, false};
   St9 zoff[2]{};
   size_t elems = 0;
@@ -333,6 +335,48 @@ HostZPlan gtsv_plan(double lo, double di, double up, int n) {
   return p;
 }
 
+// Partition-method plan (kc_zebra.cuh k_zebra_solve_part) of the constant
+// line system tridiag(a, d, c) of order n = K (s + 1) - 1 (FMA build).
+int zpart_setup(kc_handle* h, double a, double d, double c, int n, ZPart* out, void** mem) {
+  *out = ZPart{};
+  if (n < 2 * KZP_K - 1 || (n + 1) % KZP_K != 0) return KC_OK;  // short lines keep dgtsv
+  const int s = (n + 1) / KZP_K - 1;
+  std::vector<double> seg(4 * (size_t)s), red(2 * (KZP_K - 1));
+  double *cp = seg.data(), *m = cp + s, *p = m + s, *q = p + s;
+  for (int i = 0; i < s; ++i) {
+    const double den = i == 0 ? d : d - a * cp[i - 1];
+    if (den == 0.0) return KC_OK;
+    m[i] = 1.0 / den;
+    cp[i] = c * m[i];
+  }
+  auto thomas = [&](std::vector<double> b, double* x) {  // T_s x = b with the factors above
+    std::vector<double> z(s);
+    for (int i = 0; i < s; ++i) z[i] = (b[i] - (i ? a * z[i - 1] : 0.0)) * m[i];
+    x[s - 1] = z[s - 1];
+    for (int i = s - 2; i >= 0; --i) x[i] = z[i] - cp[i] * x[i + 1];
+  };
+  std::vector<double> e0(s, 0.0), e1(s, 0.0);
+  e0[0] = a;
+  e1[s - 1] = c;
+  thomas(e0, p);
+  thomas(e1, q);
+  const double ra = -a * p[s - 1], rd = d - a * q[s - 1] - c * p[0], rc = -c * q[0];
+  double *rcp = red.data(), *rm = rcp + (KZP_K - 1);
+  for (int j = 0; j < KZP_K - 1; ++j) {
+    const double den = j == 0 ? rd : rd - ra * rcp[j - 1];
+    if (den == 0.0) return KC_OK;
+    rm[j] = 1.0 / den;
+    rcp[j] = rc * rm[j];
+  }
+  const size_t bytes = sizeof(double) * (seg.size() + red.size());
+  KC_CUDA(h, cudaMalloc(mem, bytes));
+  double* dv = reinterpret_cast<double*>(*mem);
+  KC_CUDA(h, cudaMemcpy(dv, seg.data(), sizeof(double) * seg.size(), cudaMemcpyHostToDevice));
+  KC_CUDA(h, cudaMemcpy(dv + seg.size(), red.data(), sizeof(double) * red.size(), cudaMemcpyHostToDevice));
+  *out = ZPart{dv, dv + seg.size(), a, c, ra, s};
+  return KC_OK;
+}
+
 int zebra_setup(kc_handle* h, const double* w) {
   for (int l = 0; l < h->n; ++l) {
     Level& L = h->L[l];
@@ -344,6 +388,17 @@ int zebra_setup(kc_handle* h, const double* w) {
       const int n = axis == 0 ? L.m : L.ny;
       const HostZPlan hp = axis == 0 ? gtsv_plan(wl[3], wl[4], wl[5], n) : gtsv_plan(wl[1], wl[4], wl[7], n);
       L.zsing[axis] = hp.singular;
+#if KC_FAST
+      {  // the partition-method plan (dgtsv never pivots on these dominant systems)
+        bool pivots = false;
+        for (unsigned char pv : hp.piv) pivots |= pv != 0;
+        if (!pivots && !hp.singular) {
+          const int rc = axis == 0 ? zpart_setup(h, wl[3], wl[4], wl[5], n, &L.zpart[axis], &L.zpmem[axis])
+                                   : zpart_setup(h, wl[1], wl[4], wl[7], n, &L.zpart[axis], &L.zpmem[axis]);
+          if (rc) return rc;
+        }
+      }
+#endif
       std::vector<double> rd(hp.d.size());
       for (size_t i = 0; i < rd.size(); ++i) rd[i] = 1.0 / hp.d[i];  // the FMA build's back substitution
       const size_t nd = hp.fact.size() + hp.d.size() + hp.du.size() + hp.dl.size() + rd.size();
@@ -405,13 +460,23 @@ int ex_zebra(kc_handle* h, int l, int axis) {
       const int nl = (L.ny - par + 1) / 2;
       k_zebra_rhs_x<<<dim3((L.m + 31) / 32, (nl + 7) / 8), dim3(32, 8), 0, h->stream>>>(u, L.f, L.ny, L.m, L.P,
                                                                                        L.zoff[0], par);
-      k_zebra_solve_x<<<(nl + 63) / 64, 64, 0, h->stream>>>(u, L.ny, L.P, L.zp[0], par);
+      if (L.zpart[0].s) {
+        const size_t sm = sizeof(double) * (4 * (size_t)L.zpart[0].s + (size_t)KZP_K * 32 * (KZP_TC + 1));
+        KC_CUDA(h, cudaFuncSetAttribute(k_zebra_solve_part_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_zebra_solve_part_x<<<(nl + 31) / 32, KZP_K * 32, sm, h->stream>>>(u, L.P, L.zpart[0], par, nl);
+      }
+      else
+        k_zebra_solve_x<<<(nl + 63) / 64, 64, 0, h->stream>>>(u, L.ny, L.P, L.zp[0], par);
     } else {
       if (par >= L.m) break;
       const int nl = (L.m - par + 1) / 2;
       k_zebra_rhs_y<<<dim3((nl + 31) / 32, (L.ny + 7) / 8), dim3(32, 8), 0, h->stream>>>(u, L.f, L.ny, L.m, L.P,
                                                                                         L.zoff[1], par);
-      k_zebra_solve_y<<<(nl + 63) / 64, 64, 0, h->stream>>>(u, L.m, L.P, L.zp[1], par);
+      if (L.zpart[1].s)
+        k_zebra_solve_part<false><<<(nl + 31) / 32, KZP_K * 32, sizeof(double) * 4 * L.zpart[1].s, h->stream>>>(
+            u, L.P, L.zpart[1], par, nl);
+      else
+        k_zebra_solve_y<<<(nl + 63) / 64, 64, 0, h->stream>>>(u, L.m, L.P, L.zp[1], par);
     }
     KC_LAUNCH_CHECK(h);
     h->launches += 2;
@@ -1667,6 +1732,8 @@ int kc_destroy(kc_handle* h) {
     cudaFree(L.f);
     cudaFree(L.zmem[0]);
     cudaFree(L.zmem[1]);
+    cudaFree(L.zpmem[0]);
+    cudaFree(L.zpmem[1]);
   }
   cudaFree(h->x);
   cudaFree(h->p);

@@ -171,6 +171,203 @@ __device__ __forceinline__ void kz_gtsv_line(double* __restrict__ line, size_t s
   }
 }
 
+// ---------------------------------------------------------------------------
+// FMA build: the line solves as a PARTITION method (separators), one block
+// per 32 lines.  A line of n = K (s + 1) - 1 unknowns (K = 32 segments of s
+// rows, separator rows k (s + 1) - 1 between them) is solved in three steps
+// by the 32 threads of one lane position (one warp per segment):
+//   1. each segment: y = T_s^-1 b (Thomas with precomputed factors);
+//   2. the K-1 separators: a constant-coefficient tridiagonal system
+//        (-a p_end) x_{j-1} + (d - a q_end - c p_0) x_j + (-c q_0) x_{j+1}
+//          = b_sep - a y_last(seg j) - c y_first(seg j+1),
+//      one thread per line;
+//   3. each segment: x = y - x_left p - x_right q, p = T_s^-1 (a e_0) and
+//      q = T_s^-1 (c e_end) the spikes of a separator on the segment.
+// Algebraically dgtsv's solution (the constant line systems are diagonally
+// dominant, so dgtsv never pivots on them); the operations differ, so the
+// exact build keeps the serial dgtsv replay.  ~2.5 us per half-sweep at
+// 4095 instead of one dependent 8k-step chain per line.
+// ---------------------------------------------------------------------------
+#define KZP_K 32
+struct ZPart {
+  const double* seg;  // cp[s], m[s], p[s], q[s] (segment Thomas factors and spikes)
+  const double* red;  // rcp[K-1], rm[K-1] (separator Thomas factors)
+  double a, c, ra;    // line sub / super diagonal, separator sub-diagonal (-a p_end)
+  int s;              // segment length; 0: no partition plan (line too short)
+};
+template <bool XL>
+__global__ void __launch_bounds__(KZP_K * 32) k_zebra_solve_part(double* __restrict__ u, int P, ZPart zp, int par,
+                                                                int nl) {
+  extern __shared__ double zsm[];
+  const int s = zp.s;
+  double* cp = zsm;  // 4 s segment constants
+  double* mm = cp + s;
+  double* pp = mm + s;
+  double* qq = pp + s;
+  __shared__ double yF[KZP_K][33], yL[KZP_K][33], xs[KZP_K][33];
+  for (int i = threadIdx.x; i < 4 * s; i += blockDim.x) zsm[i] = __ldg(zp.seg + i);
+  __syncthreads();
+  const int t = threadIdx.x & 31, k = threadIdx.x >> 5;  // line within the block, segment
+  const int j = blockIdx.x * 32 + t;                    // line in parity order
+  const bool on = j < nl;
+  const int line = par + 2 * j;
+  auto at = [&](int i) -> double* { return XL ? u + kc_idx(P, line, i) : u + kc_idx(P, i, line); };
+  const double a = zp.a, c = zp.c;
+  const int r0 = k * (s + 1);
+  // 1. y = T_s^-1 b on segment k (in place)
+  if (on) {
+    double z = DMUL(*at(r0), mm[0]);
+    *at(r0) = z;
+    for (int i = 1; i < s; ++i) {
+      z = DMUL(DSUB(*at(r0 + i), DMUL(a, z)), mm[i]);
+      *at(r0 + i) = z;
+    }
+    double y = z;  // y_{s-1} = z_{s-1}
+    yL[k][t] = y;
+    for (int i = s - 2; i >= 0; --i) {
+      y = DSUB(*at(r0 + i), DMUL(cp[i], y));
+      *at(r0 + i) = y;
+    }
+    yF[k][t] = y;
+  }
+  __syncthreads();
+  // 2. the separators (warp 0: one line per lane)
+  if (k == 0 && on) {
+    const double* rcp = zp.red;
+    const double* rm = rcp + (KZP_K - 1);
+    double prev = 0.0;
+    for (int q = 0; q < KZP_K - 1; ++q) {  // forward sweep, z kept in xs
+      const int sep = (q + 1) * (s + 1) - 1;
+      const double rhs = DSUB(DSUB(*at(sep), DMUL(a, yL[q][t])), DMUL(c, yF[q + 1][t]));
+      prev = DMUL(DSUB(rhs, DMUL(zp.ra, prev)), __ldg(rm + q));
+      xs[q][t] = prev;
+    }
+    double x = prev;
+    *at((KZP_K - 1) * (s + 1) - 1) = x;
+    for (int q = KZP_K - 3; q >= 0; --q) {
+      x = DSUB(xs[q][t], DMUL(__ldg(rcp + q), x));
+      xs[q][t] = x;
+      *at((q + 1) * (s + 1) - 1) = x;
+    }
+  }
+  __syncthreads();
+  // 3. x = y - x_left p - x_right q on segment k
+  if (on) {
+    const double xl = k > 0 ? xs[k - 1][t] : 0.0;
+    const double xr = k < KZP_K - 1 ? xs[k][t] : 0.0;
+    for (int i = 0; i < s; ++i) {
+      double* e = at(r0 + i);
+      *e = DSUB(DSUB(*e, DMUL(xl, pp[i])), DMUL(xr, qq[i]));
+    }
+  }
+}
+
+// The same partition method for x-lines, whose values are contiguous along
+// a line: the 32 lines of a block are 32 different rows, so a lane-per-line
+// access touches 32 cache lines per instruction.  Each warp instead moves its
+// segment through a shared-memory tile of 32 lines x KZP_TC columns, loaded
+// and stored row by row (coalesced), and every lane runs its recurrence on
+// the tile.  Same operations as k_zebra_solve_part<true>.
+#define KZP_TC 16
+__global__ void __launch_bounds__(KZP_K * 32) k_zebra_solve_part_x(double* __restrict__ u, int P, ZPart zp, int par,
+                                                                  int nl) {
+  extern __shared__ double zsm[];
+  const int s = zp.s;
+  double* cp = zsm;
+  double* mm = cp + s;
+  double* pp = mm + s;
+  double* qq = pp + s;
+  double* tiles = qq + s;  // KZP_K warps x 32 lines x (KZP_TC + 1)
+  __shared__ double yF[KZP_K][33], yL[KZP_K][33], xs[KZP_K][33];
+  for (int i = threadIdx.x; i < 4 * s; i += blockDim.x) zsm[i] = __ldg(zp.seg + i);
+  __syncthreads();
+  const int t = threadIdx.x & 31, k = threadIdx.x >> 5;
+  const int j0 = blockIdx.x * 32;
+  const int nw = min(32, nl - j0);
+  const bool on = t < nw;
+  double(*T)[KZP_TC + 1] = reinterpret_cast<double(*)[KZP_TC + 1]>(tiles + (size_t)k * 32 * (KZP_TC + 1));
+  const double a = zp.a, c = zp.c;
+  const int r0 = k * (s + 1);
+  double* base = u + kc_idx(P, par + 2 * j0, r0);  // line j0's segment k
+  const size_t ls = (size_t)2 * P;
+  // two lines per warp instruction: lanes 0-15 line 2rr, lanes 16-31 line 2rr+1
+  const int hl = t >> 4, col = t & 15;
+  auto load = [&](int c0, int cnt) {
+    for (int rr = 0; rr < 16; ++rr) {
+      const int r = 2 * rr + hl;
+      if (r < nw && col < cnt) T[r][col] = base[r * ls + c0 + col];
+    }
+    __syncwarp();
+  };
+  auto store = [&](int c0, int cnt) {
+    __syncwarp();
+    for (int rr = 0; rr < 16; ++rr) {
+      const int r = 2 * rr + hl;
+      if (r < nw && col < cnt) base[r * ls + c0 + col] = T[r][col];
+    }
+    __syncwarp();
+  };
+  // 1. y = T_s^-1 b: forward over the chunks, then backward
+  double z = 0.0;
+  for (int c0 = 0; c0 < s; c0 += KZP_TC) {
+    const int cnt = min(KZP_TC, s - c0);
+    load(c0, cnt);
+    if (on)
+      for (int kk = 0; kk < cnt; ++kk) {
+        const int i = c0 + kk;
+        z = i == 0 ? DMUL(T[t][kk], mm[0]) : DMUL(DSUB(T[t][kk], DMUL(a, z)), mm[i]);
+        T[t][kk] = z;
+      }
+    store(c0, cnt);
+  }
+  double y = z;  // y_{s-1} = z_{s-1}
+  if (on) yL[k][t] = y;
+  for (int ctop = s - 2; ctop >= 0; ctop -= KZP_TC) {
+    const int c0 = max(0, ctop - KZP_TC + 1), cnt = ctop - c0 + 1;
+    load(c0, cnt);
+    if (on)
+      for (int kk = cnt - 1; kk >= 0; --kk) {
+        y = DSUB(T[t][kk], DMUL(cp[c0 + kk], y));
+        T[t][kk] = y;
+      }
+    store(c0, cnt);
+  }
+  if (on) yF[k][t] = y;
+  __syncthreads();
+  // 2. the separators (warp 0: one line per lane)
+  if (k == 0 && on) {
+    const double* rcp = zp.red;
+    const double* rm = rcp + (KZP_K - 1);
+    double* line = u + kc_idx(P, par + 2 * (j0 + t), 0);
+    double prev = 0.0;
+    for (int q = 0; q < KZP_K - 1; ++q) {
+      const int sep = (q + 1) * (s + 1) - 1;
+      const double rhs = DSUB(DSUB(line[sep], DMUL(a, yL[q][t])), DMUL(c, yF[q + 1][t]));
+      prev = DMUL(DSUB(rhs, DMUL(zp.ra, prev)), __ldg(rm + q));
+      xs[q][t] = prev;
+    }
+    double x = prev;
+    line[(KZP_K - 1) * (s + 1) - 1] = x;
+    for (int q = KZP_K - 3; q >= 0; --q) {
+      x = DSUB(xs[q][t], DMUL(__ldg(rcp + q), x));
+      xs[q][t] = x;
+      line[(q + 1) * (s + 1) - 1] = x;
+    }
+  }
+  __syncthreads();
+  // 3. x = y - x_left p - x_right q
+  const double xl = (on && k > 0) ? xs[k - 1][t] : 0.0;
+  const double xr = (on && k < KZP_K - 1) ? xs[k][t] : 0.0;
+  for (int c0 = 0; c0 < s; c0 += KZP_TC) {
+    const int cnt = min(KZP_TC, s - c0);
+    load(c0, cnt);
+    if (on)
+      for (int kk = 0; kk < cnt; ++kk)
+        T[t][kk] = DSUB(DSUB(T[t][kk], DMUL(xl, pp[c0 + kk])), DMUL(xr, qq[c0 + kk]));
+    store(c0, cnt);
+  }
+}
+
 __global__ void k_zebra_solve_x(double* __restrict__ u, int ny, int P, ZPlan pl, int par) {
   const int y = par + 2 * (blockIdx.x * blockDim.x + threadIdx.x);
   if (y >= ny) return;

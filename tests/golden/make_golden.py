@@ -509,6 +509,30 @@ CLI_CASES = [
 CLI_FIT_INPUT = "kappa,levels,ms\n1,4,0.1\n2,5,0.3\n3,6,0.9\ninf,7,2.5\n"
 
 
+def gen_zebra9():
+    """n = 9 zebra solves (the paper's Tables 5-8 solvers at a size the
+    reference finishes in minutes): alternating zebra with full coarsening
+    and zebra-x with y-semi-coarsening, kappa 2 / 3, eps 1e-5 and 1e-4,
+    phi 45, error reduction 1e8 (cycle.py:303-366) -- pins the FMA build's
+    partitioned line solver (kc_zebra.cuh k_zebra_solve_part) by counts and
+    histories."""
+    out = {}
+    for sm, co in (("zebra-xy", "full"), ("zebra-x", "semi-y")):
+        for eps in (1e-5, 1e-4):
+            for kappa in (2, 3):
+                problem, cfg = problem_config(9, kappa, eps=eps, smoother=_smoother(sm), coarsening=_coarsening(co))
+                t0 = time.perf_counter()
+                rep = kc.solve_standalone(problem, cfg, 1e8, max_cycles=3000)
+                key = f"{sm}_{co}_n9_k{kappa}_eps{eps:g}"
+                out[key] = {"smoother": sm, "coarsening": co, "n": 9, "kappa": kappa, "epsilon": eps, "phi": 45.0,
+                            "status": rep.status, "iterations": rep.iterations,
+                            "initial_error_norm": rep.initial_error_norm, "final_error_norm": rep.final_error_norm,
+                            "per_cycle_reduction": rep.per_cycle_reduction,
+                            "seconds": time.perf_counter() - t0}
+                print(key, rep.status, rep.iterations, f"{time.perf_counter() - t0:.0f}s", flush=True)
+                dump("zebra_n9.json", out)
+
+
 def gen_cli():
     """The reference CLI (cli.py) on fixed argument lists: stdout and exit
     code; solve records without the run-dependent fields (wall_ms,
@@ -548,7 +572,7 @@ def gen_cli():
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["small", "solve", "pcg", "costmodel", "cli", "zebra"])
+    ap.add_argument("what", choices=["small", "solve", "pcg", "costmodel", "cli", "zebra", "zebra9"])
     ap.add_argument("--n", type=int, default=12)
     ap.add_argument("--kappa", default="1")
     ap.add_argument("--cap", type=int, default=20000)
@@ -562,6 +586,9 @@ def main():
         return
     if a.what == "zebra":
         gen_zebra()
+        return
+    if a.what == "zebra9":
+        gen_zebra9()
         return
     if a.what == "small":
         gen_stencils()

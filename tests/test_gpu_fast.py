@@ -160,3 +160,46 @@ def test_fast_n14_norms_vs_reference_golden():
     _hist(rep.error_history, g["err_hist"], 1e-10)
     _hist(rep.residual_history, g["res_hist"], 1e-10)
     st.close()
+
+
+# ---------------------------------------------------------------------------
+# zebra / semi-coarsening (paper solvers 3-6): the FMA build's partitioned
+# line solver (kc_zebra.cuh k_zebra_solve_part*) against the reference
+# ---------------------------------------------------------------------------
+
+def _zebra_cfg(rec):
+    from paper_2010_00626_b200.mesh import Coarsening
+    from paper_2010_00626_b200.smoother import SmootherKind, SmootherSpec
+    return CycleConfig(n=rec["n"], kappa=int(rec["kappa"]), smoother=SmootherSpec(SmootherKind(rec["smoother"]), 0.8),
+                       coarsening=Coarsening(rec["coarsening"]))
+
+
+def _zebra_check(rep, rec):
+    assert rep.status == rec["status"] and rep.iterations == rec["iterations"]
+    assert rep.initial_error_norm == pytest.approx(rec["initial_error_norm"], rel=1e-12)
+    assert rep.final_error_norm == pytest.approx(rec["final_error_norm"], rel=1e-10)
+    assert np.allclose(rep.per_cycle_reduction, rec["per_cycle_reduction"], rtol=1e-9, atol=0)
+
+
+@pytest.mark.parametrize("key", sorted(load_json("zebra_meta.json")["solves"]))
+def test_fast_zebra_solves_small(key):
+    rec = load_json("zebra_meta.json")["solves"][key]
+    cfg = _zebra_cfg(rec)
+    st = _fast(ProblemSpec(1e-4, 45.0, seed=0), cfg)
+    _zebra_check(solve_standalone(ProblemSpec(1e-4, 45.0, seed=0), cfg, 1e8, max_cycles=3000, state=st), rec)
+    st.close()
+
+
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+@pytest.mark.parametrize("key", sorted(load_json("zebra_n9.json")) if golden_exists("zebra_n9.json") else [])
+def test_zebra_n9_paper_solvers(arith, key):
+    """The paper's Tables 5-8 solvers (alternating zebra + full coarsening,
+    zebra-x + y-semi-coarsening; eps 1e-5 and 1e-4, phi 45, error reduction
+    1e8) at n = 9 against the real reference: identical counts, norms within
+    1e-10 (exact build: dgtsv replay; fast build: partitioned line solves)."""
+    rec = load_json("zebra_n9.json")[key]
+    cfg = _zebra_cfg(rec)
+    problem = ProblemSpec(rec["epsilon"], rec["phi"], seed=0)
+    st = build_state(problem, cfg, arith=arith)
+    _zebra_check(solve_standalone(problem, cfg, 1e8, max_cycles=3000, state=st), rec)
+    st.close()
