@@ -83,8 +83,10 @@ struct Level {
   // cross-line stencils (line row / column zeroed; the y one transposed)
   ZPlan zp[2]{};
   ZPart zpart[2]{};  // the FMA build's partition-method plans (s = 0: none)
+  ZPart zpline[2]{};  // ... with KZL_K segments, one block per line (few lines, the coarsest line)
   void* zmem[2] = {nullptr, nullptr};
   void* zpmem[2] = {nullptr, nullptr};
+  void* zplmem[2] = {nullptr, nullptr};
   bool zsing[2] = {false, false};
   St9 zoff[2]{};
   size_t elems = 0;
@@ -159,6 +161,7 @@ struct kc_handle {
   bool tile = true;           // overlapped-tile kernels on the mid-size levels
   bool pdl = true;            // programmatic dependent launch around the bottom kernel (KC_PDL=0: off)
   bool postpre = true;        // fused sibling post+pre passes on the column-tile levels (KC_POSTPRE=0: off)
+  int zebra_few = 256;        // KZ_FEW: most lines per half-sweep for the one-line-per-block kernel
   // the streaming k_postpre on 1023^2 and up (KC_POSTPRE_STREAM=1: on): bit-exact,
   // but as slow as the two passes it replaces (2047^2: 57 vs 32 + 27 us;
   // these passes are issue-bound, not traffic-bound), so off by default
@@ -337,11 +340,11 @@ HostZPlan gtsv_plan(double lo, double di, double up, int n) {
 
 // Partition-method plan (kc_zebra.cuh k_zebra_solve_part) of the constant
 // line system tridiag(a, d, c) of order n = K (s + 1) - 1 (FMA build).
-int zpart_setup(kc_handle* h, double a, double d, double c, int n, ZPart* out, void** mem) {
+int zpart_setup(kc_handle* h, double a, double d, double c, int n, ZPart* out, void** mem, int K = KZP_K) {
   *out = ZPart{};
-  if (n < 2 * KZP_K - 1 || (n + 1) % KZP_K != 0) return KC_OK;  // short lines keep dgtsv
-  const int s = (n + 1) / KZP_K - 1;
-  std::vector<double> seg(4 * (size_t)s), red(2 * (KZP_K - 1));
+  if (n < 2 * K - 1 || (n + 1) % K != 0) return KC_OK;  // short lines keep dgtsv
+  const int s = (n + 1) / K - 1;
+  std::vector<double> seg(4 * (size_t)s), red(2 * (size_t)(K - 1));
   double *cp = seg.data(), *m = cp + s, *p = m + s, *q = p + s;
   for (int i = 0; i < s; ++i) {
     const double den = i == 0 ? d : d - a * cp[i - 1];
@@ -361,8 +364,8 @@ int zpart_setup(kc_handle* h, double a, double d, double c, int n, ZPart* out, v
   thomas(e0, p);
   thomas(e1, q);
   const double ra = -a * p[s - 1], rd = d - a * q[s - 1] - c * p[0], rc = -c * q[0];
-  double *rcp = red.data(), *rm = rcp + (KZP_K - 1);
-  for (int j = 0; j < KZP_K - 1; ++j) {
+  double *rcp = red.data(), *rm = rcp + (K - 1);
+  for (int j = 0; j < K - 1; ++j) {
     const double den = j == 0 ? rd : rd - ra * rcp[j - 1];
     if (den == 0.0) return KC_OK;
     rm[j] = 1.0 / den;
@@ -396,6 +399,10 @@ int zebra_setup(kc_handle* h, const double* w) {
           const int rc = axis == 0 ? zpart_setup(h, wl[3], wl[4], wl[5], n, &L.zpart[axis], &L.zpmem[axis])
                                    : zpart_setup(h, wl[1], wl[4], wl[7], n, &L.zpart[axis], &L.zpmem[axis]);
           if (rc) return rc;
+          const int rc2 = axis == 0
+                              ? zpart_setup(h, wl[3], wl[4], wl[5], n, &L.zpline[axis], &L.zplmem[axis], KZL_K)
+                              : zpart_setup(h, wl[1], wl[4], wl[7], n, &L.zpline[axis], &L.zplmem[axis], KZL_K);
+          if (rc2) return rc2;
         }
       }
 #endif
@@ -446,6 +453,12 @@ int zebra_setup(kc_handle* h, const double* w) {
   return KC_OK;
 }
 
+// few long lines per half-sweep (y-semi-coarsened levels): the FMA build
+// solves one line per block with KZL_K segments (n = 12 zebra-x + semi-y
+// kappa=2: 35.3 -> 30.4 ms per cycle with the threshold 256; the aspect
+// condition keeps full coarsening on the 32-segment kernel, which the
+// one-line kernel slows down there: 9.05 -> 9.65 ms)
+#define KZ_FEW(nl, len) ((nl) <= h->zebra_few && (len) >= 4 * (nl))
 // One zebra sweep with lines along x (axis 0) or y (axis 1), in place:
 // even lines, then odd lines with the updated even ones (smoother.py:107-135)
 int ex_zebra(kc_handle* h, int l, int axis) {
@@ -460,7 +473,10 @@ int ex_zebra(kc_handle* h, int l, int axis) {
       const int nl = (L.ny - par + 1) / 2;
       k_zebra_rhs_x<<<dim3((L.m + 31) / 32, (nl + 7) / 8), dim3(32, 8), 0, h->stream>>>(u, L.f, L.ny, L.m, L.P,
                                                                                        L.zoff[0], par);
-      if (L.zpart[0].s) {
+      if (L.zpline[0].s && KZ_FEW(nl, L.m)) {
+        k_zebra_solve_line<true><<<nl, KZL_K, sizeof(double) * 4 * L.zpline[0].s, h->stream>>>(u, u, L.P, L.zpline[0],
+                                                                                             par);
+      } else if (L.zpart[0].s) {
         const size_t sm = sizeof(double) * (4 * (size_t)L.zpart[0].s + (size_t)KZP_K * 32 * (KZP_TC + 1));
         KC_CUDA(h, cudaFuncSetAttribute(k_zebra_solve_part_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         k_zebra_solve_part_x<<<(nl + 31) / 32, KZP_K * 32, sm, h->stream>>>(u, L.P, L.zpart[0], par, nl);
@@ -472,7 +488,10 @@ int ex_zebra(kc_handle* h, int l, int axis) {
       const int nl = (L.m - par + 1) / 2;
       k_zebra_rhs_y<<<dim3((nl + 31) / 32, (L.ny + 7) / 8), dim3(32, 8), 0, h->stream>>>(u, L.f, L.ny, L.m, L.P,
                                                                                         L.zoff[1], par);
-      if (L.zpart[1].s)
+      if (L.zpline[1].s && KZ_FEW(nl, L.ny))
+        k_zebra_solve_line<false><<<nl, KZL_K, sizeof(double) * 4 * L.zpline[1].s, h->stream>>>(u, u, L.P,
+                                                                                              L.zpline[1], par);
+      else if (L.zpart[1].s)
         k_zebra_solve_part<false><<<(nl + 31) / 32, KZP_K * 32, sizeof(double) * 4 * L.zpart[1].s, h->stream>>>(
             u, L.P, L.zpart[1], par, nl);
       else
@@ -559,8 +578,12 @@ int ex_coarsest(kc_handle* h) {
   Level& L = h->L[h->n - 1];
   if (L.ny == 1 && L.m > 1 && h->coarsening == KC_COARSEN_SEMI_Y) {  // one x-line, cycle.py:191-200
     if (h->line_singular) KC_FAIL(h, KC_ESINGULAR, "zero pivot in tridiagonal elimination");
-    k_coarsest_line<<<1, 32, 0, h->stream>>>(L.v[L.cur], L.f, L.v[L.cur ^ 1], L.m, L.P, h->line_w[0], h->line_w[1],
-                                             h->line_w[2]);
+    if (L.zpline[0].s)  // FMA build: the partition method on the single line (its own x-line system)
+      k_zebra_solve_line<true><<<1, KZL_K, sizeof(double) * 4 * L.zpline[0].s, h->stream>>>(L.v[L.cur], L.f, L.P,
+                                                                                           L.zpline[0], 0);
+    else
+      k_coarsest_line<<<1, 32, 0, h->stream>>>(L.v[L.cur], L.f, L.v[L.cur ^ 1], L.m, L.P, h->line_w[0],
+                                               h->line_w[1], h->line_w[2]);
     KC_LAUNCH_CHECK(h);
     ++h->launches;
     L.vzero = false;
@@ -1515,6 +1538,8 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
   {
     const char* penv = getenv("KC_PDL");
     h->pdl = !(penv && penv[0] == '0');
+    const char* zfenv = getenv("KC_ZEBRA_FEW");
+    if (zfenv) h->zebra_few = atoi(zfenv);
     const char* ppenv = getenv("KC_POSTPRE");
     h->postpre = !(ppenv && ppenv[0] == '0');
     const char* ppsenv = getenv("KC_POSTPRE_STREAM");
@@ -1734,6 +1759,8 @@ int kc_destroy(kc_handle* h) {
     cudaFree(L.zmem[1]);
     cudaFree(L.zpmem[0]);
     cudaFree(L.zpmem[1]);
+    cudaFree(L.zplmem[0]);
+    cudaFree(L.zplmem[1]);
   }
   cudaFree(h->x);
   cudaFree(h->p);

@@ -368,6 +368,71 @@ __global__ void __launch_bounds__(KZP_K * 32) k_zebra_solve_part_x(double* __res
   }
 }
 
+// Levels with few lines (y-semi-coarsening keeps 16383-long x-lines down to
+// a single one) and the coarsest line: one block per line and KZL_K = 256
+// segments, one thread each (s = (n + 1) / 256 - 1 rows), the separator
+// system solved by thread 0.  `src` holds the right-hand sides (the line
+// itself, or f for the coarsest solve), `u` receives the solution.
+#define KZL_K 256
+template <bool XL>
+__global__ void __launch_bounds__(KZL_K) k_zebra_solve_line(double* __restrict__ u, const double* __restrict__ src,
+                                                            int P, ZPart zp, int par) {
+  extern __shared__ double zsm[];
+  const int s = zp.s;
+  double* cp = zsm;
+  double* mm = cp + s;
+  double* pp = mm + s;
+  double* qq = pp + s;
+  __shared__ double yF[KZL_K], yL[KZL_K], xs[KZL_K];
+  for (int i = threadIdx.x; i < 4 * s; i += blockDim.x) zsm[i] = __ldg(zp.seg + i);
+  __syncthreads();
+  const int k = threadIdx.x;
+  const int line = par + 2 * blockIdx.x;
+  auto at = [&](double* b, int i) -> double* { return XL ? b + kc_idx(P, line, i) : b + kc_idx(P, i, line); };
+  auto atc = [&](const double* b, int i) -> double { return XL ? b[kc_idx(P, line, i)] : b[kc_idx(P, i, line)]; };
+  const double a = zp.a, c = zp.c;
+  const int r0 = k * (s + 1);
+  double z = DMUL(atc(src, r0), mm[0]);
+  *at(u, r0) = z;
+  for (int i = 1; i < s; ++i) {
+    z = DMUL(DSUB(atc(src, r0 + i), DMUL(a, z)), mm[i]);
+    *at(u, r0 + i) = z;
+  }
+  double y = z;
+  yL[k] = y;
+  for (int i = s - 2; i >= 0; --i) {
+    y = DSUB(*at(u, r0 + i), DMUL(cp[i], y));
+    *at(u, r0 + i) = y;
+  }
+  yF[k] = y;
+  __syncthreads();
+  if (k == 0) {
+    const double* rcp = zp.red;
+    const double* rm = rcp + (KZL_K - 1);
+    double prev = 0.0;
+    for (int q = 0; q < KZL_K - 1; ++q) {
+      const int sep = (q + 1) * (s + 1) - 1;
+      const double rhs = DSUB(DSUB(atc(src, sep), DMUL(a, yL[q])), DMUL(c, yF[q + 1]));
+      prev = DMUL(DSUB(rhs, DMUL(zp.ra, prev)), __ldg(rm + q));
+      xs[q] = prev;
+    }
+    double x = prev;
+    *at(u, (KZL_K - 1) * (s + 1) - 1) = x;
+    for (int q = KZL_K - 3; q >= 0; --q) {
+      x = DSUB(xs[q], DMUL(__ldg(rcp + q), x));
+      xs[q] = x;
+      *at(u, (q + 1) * (s + 1) - 1) = x;
+    }
+  }
+  __syncthreads();
+  const double xl = k > 0 ? xs[k - 1] : 0.0;
+  const double xr = k < KZL_K - 1 ? xs[k] : 0.0;
+  for (int i = 0; i < s; ++i) {
+    double* e = at(u, r0 + i);
+    *e = DSUB(DSUB(*e, DMUL(xl, pp[i])), DMUL(xr, qq[i]));
+  }
+}
+
 __global__ void k_zebra_solve_x(double* __restrict__ u, int ny, int P, ZPlan pl, int par) {
   const int y = par + 2 * (blockIdx.x * blockDim.x + threadIdx.x);
   if (y >= ny) return;
