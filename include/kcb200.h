@@ -202,6 +202,20 @@ int kc_strip_pre(const double* u, const double* f, double* uo, double* fc, int r
 int kc_strip_post(const double* u, const double* f, double* uo, const double* vc, int rows, int nx, int pitch,
                   int pitch_c, int crows, int gy0, int mg, int hb, int hbc, const double* w9, double omega, int nu2,
                   int v_zero, void* stream);
+/* The same passes restricted to the coarse-row window [q_lo, q_hi) of the
+ * chunk positions 0..crows (position crows carries a last rank's trailing
+ * fine row): pre writes fc rows [q_lo, min(q_hi, crows)) and uo rows
+ * [2 q_lo, min(2 q_hi, rows)); post writes uo rows [2 q_lo, min(2 q_hi, rows)).
+ * hb / hbc may be as small as the rows the window's outputs depend on
+ * (KC_EINVAL otherwise): a window of interior rows with hb = hbc = 0 never
+ * touches the halo rows, so it runs while the caller's halo exchange is in
+ * flight, and the boundary windows run after it (distributed.py overlap). */
+int kc_strip_pre_window(const double* u, const double* f, double* uo, double* fc, int rows, int nx, int pitch,
+                        int pitch_c, int crows, int gy0, int mg, int hb, int q_lo, int q_hi, const double* w9,
+                        double omega, int nu1, int zero_u, void* stream);
+int kc_strip_post_window(const double* u, const double* f, double* uo, const double* vc, int rows, int nx, int pitch,
+                         int pitch_c, int crows, int gy0, int mg, int hb, int hbc, int q_lo, int q_hi,
+                         const double* w9, double omega, int nu2, int v_zero, void* stream);
 
 /* level data from / to device memory with an explicit row pitch (doubles):
  * agglomeration of distributed levels onto the native engine */

@@ -89,6 +89,10 @@ _SIGS = {
                      + [_dp, C.c_double, C.c_int, C.c_int, C.c_void_p]),
     "kc_strip_post": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p] + [C.c_int] * 9
                       + [_dp, C.c_double, C.c_int, C.c_int, C.c_void_p]),
+    "kc_strip_pre_window": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p] + [C.c_int] * 10
+                            + [_dp, C.c_double, C.c_int, C.c_int, C.c_void_p]),
+    "kc_strip_post_window": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p] + [C.c_int] * 11
+                             + [_dp, C.c_double, C.c_int, C.c_int, C.c_void_p]),
     "kc_set_device": (C.c_int, [_h, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_longlong, C.c_longlong]),
     "kc_get_device": (C.c_int, [_h, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_longlong, C.c_longlong]),
     "kc_set_device_async": (C.c_int, [_h, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_longlong, C.c_longlong]),

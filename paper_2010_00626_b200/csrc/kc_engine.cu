@@ -10,7 +10,9 @@
 // captured once as a CUDA graph per (kappa, level-1 buffer state).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cfloat>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -2593,7 +2595,7 @@ KsFn strip_post_fn(int nu, bool vz) {
   return nullptr;
 }
 StreamParams strip_params(int rows, int nx, int pitch, int pitch_c, int crows, int gy0, int mg, int hb, int hbc,
-                          const double* w9, double omega, int D, const void* fn, int* nwarps) {
+                          int qlo, int qhi, const double* w9, double omega, int D, const void* fn, int* nwarps) {
   StreamParams p{};
   p.m = nx;
   p.P = pitch;
@@ -2606,22 +2608,59 @@ StreamParams strip_params(int rows, int nx, int pitch, int pitch_c, int crows, i
   p.hb = hb;
   p.mcr = crows;
   p.hbc = hbc;
+  p.qlo = qlo;
+  p.qhi = qhi;
   p.nbands = (p.mc + 1 + ks_npb(D) - 1) / ks_npb(D);
-  p.nq = ks_choose_nq(crows, p.nbands, strip_slots(fn, D));
-  *nwarps = p.nbands * ((crows + 1 + p.nq - 1) / p.nq);
+  p.nq = ks_choose_nq(qhi - qlo - 1, p.nbands, strip_slots(fn, D));
+  *nwarps = p.nbands * ((qhi - qlo + p.nq - 1) / p.nq);
   return p;
+}
+int floor2(int a) { return a >= 0 ? a / 2 : -((1 - a) / 2); }
+// the fine input rows [*lo, *hi] (local) the owned outputs of a window
+// [qlo, qhi) depend on; false: nothing owned
+bool pre_window_rows(int rows, int crows, int nu1, int qlo, int qhi, int* lo, int* hi) {
+  const int D = nu1 + 1;
+  const int fe = std::min(2 * qhi, rows), ce = std::min(qhi, crows);  // owned fine rows end, coarse rows end
+  const bool fine = nu1 > 0 && fe > 2 * qlo, coarse = ce > qlo;
+  if (!fine && !coarse) return false;
+  *lo = 2 * qlo - D;
+  *hi = std::max(fine ? fe - 1 + nu1 : INT_MIN, coarse ? 2 * ce + D : INT_MIN);
+  return true;
+}
+// post: fine input rows and coarse rows of vc
+bool post_window_rows(int rows, int nu2, int qlo, int qhi, int* lo, int* hi, int* clo, int* chi) {
+  const int fe = std::min(2 * qhi, rows);
+  if (fe <= 2 * qlo) return false;
+  *lo = 2 * qlo - nu2;
+  *hi = fe - 1 + nu2;
+  *clo = (*lo % 2 == 0) ? *lo / 2 - 1 : floor2(*lo);  // fine row 2q reads coarse rows q-1, q; 2q+1 reads q
+  *chi = floor2(*hi);
+  return true;
 }
 }  // namespace
 
 extern "C" int kc_strip_pre(const double* u, const double* f, double* uo, double* fc, int rows, int nx, int pitch,
                             int pitch_c, int crows, int gy0, int mg, int hb, const double* w9, double omega, int nu1,
                             int zero_u, void* stream) {
-  if (!f || !uo || !fc || !w9 || rows < 1 || nx < 3 || crows < 0 || hb < nu1 + 2 || gy0 < 0 || gy0 % 2) return KC_EINVAL;
+  if (hb < nu1 + 2 || crows < 0) return KC_EINVAL;
+  return kc_strip_pre_window(u, f, uo, fc, rows, nx, pitch, pitch_c, crows, gy0, mg, hb, 0, crows + 1, w9, omega, nu1,
+                             zero_u, stream);
+}
+
+extern "C" int kc_strip_pre_window(const double* u, const double* f, double* uo, double* fc, int rows, int nx,
+                                   int pitch, int pitch_c, int crows, int gy0, int mg, int hb, int q_lo, int q_hi,
+                                   const double* w9, double omega, int nu1, int zero_u, void* stream) {
+  if (!f || !uo || !fc || !w9 || rows < 1 || nx < 3 || crows < 0 || hb < 0 || gy0 < 0 || gy0 % 2) return KC_EINVAL;
   if (!zero_u && !u) return KC_EINVAL;
   if (nu1 < 0 || nu1 > 4 || (nu1 > 0 && w9[4] == 0.0)) return KC_EINVAL;
+  if (q_lo < 0 || q_hi < q_lo || q_hi > crows + 1) return KC_EINVAL;
+  int lo = 0, hi = 0;
+  if (!pre_window_rows(rows, crows, nu1, q_lo, q_hi, &lo, &hi)) return KC_OK;  // nothing owned
+  if (lo < -hb || hi > rows + hb - 1) return KC_EINVAL;  // the window reaches rows the buffers do not hold
   int nw = 0;
   KsFn fn = strip_pre_fn(nu1, zero_u != 0);
-  StreamParams p = strip_params(rows, nx, pitch, pitch_c, crows, gy0, mg, hb, 1, w9, omega, nu1 + 1, (const void*)fn, &nw);
+  StreamParams p = strip_params(rows, nx, pitch, pitch_c, crows, gy0, mg, hb, 1, q_lo, q_hi, w9, omega, nu1 + 1,
+                                (const void*)fn, &nw);
   // the kernels index from the padded-array base: kc_idx(P, 0, 0) = P + KC_OX
   const ptrdiff_t ob = (ptrdiff_t)pitch + KC_OX, obc = (ptrdiff_t)pitch_c + KC_OX;
   p.u = u ? u - ob : nullptr;
@@ -2635,15 +2674,27 @@ extern "C" int kc_strip_pre(const double* u, const double* f, double* uo, double
 extern "C" int kc_strip_post(const double* u, const double* f, double* uo, const double* vc, int rows, int nx,
                              int pitch, int pitch_c, int crows, int gy0, int mg, int hb, int hbc, const double* w9,
                              double omega, int nu2, int v_zero, void* stream) {
-  if (!f || !uo || !vc || !w9 || rows < 1 || nx < 3 || crows < 0 || hb < nu2 || hbc < nu2 / 2 + 1 || gy0 < 0 ||
-      gy0 % 2)
+  if (hb < nu2 || hbc < nu2 / 2 + 1 || crows < 0) return KC_EINVAL;
+  return kc_strip_post_window(u, f, uo, vc, rows, nx, pitch, pitch_c, crows, gy0, mg, hb, hbc, 0, crows + 1, w9,
+                              omega, nu2, v_zero, stream);
+}
+
+extern "C" int kc_strip_post_window(const double* u, const double* f, double* uo, const double* vc, int rows,
+                                    int nx, int pitch, int pitch_c, int crows, int gy0, int mg, int hb, int hbc,
+                                    int q_lo, int q_hi, const double* w9, double omega, int nu2, int v_zero,
+                                    void* stream) {
+  if (!f || !uo || !vc || !w9 || rows < 1 || nx < 3 || crows < 0 || hb < 0 || hbc < 0 || gy0 < 0 || gy0 % 2)
     return KC_EINVAL;
   if (!v_zero && !u) return KC_EINVAL;
   if (nu2 < 0 || nu2 > 4 || (nu2 > 0 && w9[4] == 0.0)) return KC_EINVAL;
+  if (q_lo < 0 || q_hi < q_lo || q_hi > crows + 1) return KC_EINVAL;
+  int lo = 0, hi = 0, clo = 0, chi = 0;
+  if (!post_window_rows(rows, nu2, q_lo, q_hi, &lo, &hi, &clo, &chi)) return KC_OK;
+  if (lo < -hb || hi > rows + hb - 1 || clo < -hbc || chi > crows + hbc - 1) return KC_EINVAL;
   int nw = 0;
   KsFn fn = strip_post_fn(nu2, v_zero != 0);
-  StreamParams p = strip_params(rows, nx, pitch, pitch_c, crows, gy0, mg, hb, hbc, w9, omega, nu2 > 0 ? nu2 : 1,
-                                (const void*)fn, &nw);
+  StreamParams p = strip_params(rows, nx, pitch, pitch_c, crows, gy0, mg, hb, hbc, q_lo, q_hi, w9, omega,
+                                nu2 > 0 ? nu2 : 1, (const void*)fn, &nw);
   const ptrdiff_t ob = (ptrdiff_t)pitch + KC_OX, obc = (ptrdiff_t)pitch_c + KC_OX;  // see kc_strip_pre
   p.u = u ? u - ob : nullptr;
   p.f = f - ob;

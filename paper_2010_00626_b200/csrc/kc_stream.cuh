@@ -53,6 +53,10 @@ struct StreamParams {
   // halo rows above and below in the buffer; mcr local coarse rows with hbc
   // coarse halo rows.  Masks use global rows, memory stays in the buffer.
   int rows, gy0, mg, hb, mcr, hbc;
+  // strips: the chunks cover coarse-row positions [qlo, qhi) only (a window:
+  // the interior rows a pass can compute while the halo exchange is in
+  // flight, or the boundary rows after it; whole strip: 0, mcr + 1)
+  int qlo, qhi;
 };
 
 __device__ __forceinline__ double kc_shfl_up1(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
@@ -154,8 +158,9 @@ __global__ void __launch_bounds__(128, KS_MINB) k_pre(const StreamParams p) {
   const int lane = threadIdx.x & 31;
   const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int band = wg % p.nbands, chunk = wg / p.nbands;
-  const int P0 = band * G::NPB, Q0 = chunk * p.nq;
-  if (Q0 > g_mcr) {  // whole warp
+  const int P0 = band * G::NPB, Q0 = (STRIP ? p.qlo : 0) + chunk * p.nq;
+  const int Qe = STRIP ? min(Q0 + p.nq, p.qhi) : Q0 + p.nq;  // this chunk's coarse rows: [Q0, Qe)
+  if (Q0 > g_mcr || (STRIP && Q0 >= p.qhi)) {  // whole warp
     if (NORMS) reinterpret_cast<double2*>(p.part)[wg * 32 + lane] = make_double2(0.0, 0.0);
     return;
   }
@@ -175,7 +180,7 @@ __global__ void __launch_bounds__(128, KS_MINB) k_pre(const StreamParams p) {
   double RE[3] = {0.0, 0.0, 0.0};  // their values one column east of the lane's pair
 
   const int ys = 2 * Q0 - D;
-  const int ye = 2 * Q0 + 2 * p.nq + D;  // inclusive: residual row 2 (Q0 + nq)
+  const int ye = 2 * Qe + D;  // inclusive: residual row 2 Qe
   // only warps touching the domain boundary need masks / row clamping
   const bool edge = XS < 0 || XS + KS_BAND - 1 >= m || g_y0 + ys - D - 1 < 0 || g_y0 + ye + 1 >= g_mg;
   // rows outside the buffer read its edge rows (the all-zero ghost rows of a
@@ -212,8 +217,8 @@ __global__ void __launch_bounds__(128, KS_MINB) k_pre(const StreamParams p) {
     // NORMS: rows owned by this chunk, interior columns owned by this lane;
     // the input's residual is the first stage's f - A u at row yin - 1
     const int y1 = yin - 1;
-    const bool own_e = NORMS && own_lane && yin >= 2 * Q0 && yin < 2 * Q0 + 2 * p.nq && yin < g_rows;
-    const bool own_r = NORMS && own_lane && y1 >= 2 * Q0 && y1 < 2 * Q0 + 2 * p.nq && y1 >= 0 && y1 < g_rows;
+    const bool own_e = NORMS && own_lane && yin >= 2 * Q0 && yin < 2 * Qe && yin < g_rows;
+    const bool own_r = NORMS && own_lane && y1 >= 2 * Q0 && y1 < 2 * Qe && y1 >= 0 && y1 < g_rows;
     if (own_e) acc_e = fma(u0.y, u0.y, fma(u0.x, u0.x, acc_e));
     double2 nw[D + 1];
     nw[0] = u0;
@@ -252,13 +257,13 @@ __global__ void __launch_bounds__(128, KS_MINB) k_pre(const StreamParams p) {
     {
       const int yr = yin - D;
       const int q = (yr >> 1) - 1;
-      if (!(yr & 1) && own_lane && q >= Q0 && q < Q0 + p.nq && q < g_mcr && q >= 0 && pcol < p.mc)
+      if (!(yr & 1) && own_lane && q >= Q0 && q < Qe && q < g_mcr && q >= 0 && pcol < p.mc)
         p.fc[kc_idx(p.Pc, q, pcol)] = kc_fw(R[0].x, R[0].y, RE[0], R[1].x, R[1].y, RE[1], R[2].x, R[2].y, RE[2]);
     }
     // ---- output v after NU sweeps ----------------------------------------
     if (NU > 0) {
       const int y = yin - NU;
-      if (own_lane && y >= 2 * Q0 && y < 2 * Q0 + 2 * p.nq && y >= 0 && y < g_rows)
+      if (own_lane && y >= 2 * Q0 && y < 2 * Qe && y >= 0 && y < g_rows)
         *reinterpret_cast<double2*>(p.uo + kc_idx(P, y, c0)) = nw[NU];
     }
     // per-lane partials, stored from inside the loop: any code after it (a
@@ -286,9 +291,10 @@ __global__ void __launch_bounds__(128, KS_MINB) k_post(const StreamParams p) {
   const int lane = threadIdx.x & 31;
   const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int band = wg % p.nbands, chunk = wg / p.nbands;
-  const int P0 = band * G::NPB, Q0 = chunk * p.nq;
+  const int P0 = band * G::NPB, Q0 = (STRIP ? p.qlo : 0) + chunk * p.nq;
+  const int Qe = STRIP ? min(Q0 + p.nq, p.qhi) : Q0 + p.nq;  // see k_pre
   double acc_e = 0.0, acc_r = 0.0;
-  const bool active = Q0 <= g_mcr;
+  const bool active = Q0 <= g_mcr && (!STRIP || Q0 < p.qhi);
   if (DOT && !active) reinterpret_cast<double2*>(p.part)[wg * 32 + lane] = make_double2(0.0, 0.0);
   const int m = p.m, P = p.P;
   const int XS = 2 * P0 - G::HL;
@@ -303,7 +309,7 @@ __global__ void __launch_bounds__(128, KS_MINB) k_post(const StreamParams p) {
 #pragma unroll
     for (int t = 0; t <= DD; ++t) A[t].b = A[t].c = A[t].cen = make_double2(0.0, 0.0);
     const int ys = 2 * Q0 - D;
-    const int ye = 2 * Q0 + 2 * p.nq - 1 + D;
+    const int ye = 2 * Qe - 1 + D;
     const bool edge = XS < 0 || XS + KS_BAND - 1 >= m || g_y0 + ys - D - 2 < 0 || g_y0 + ye + 2 >= g_mg;
     auto rp = [&](int y) -> size_t { return kc_idx(P, min(max(y, -g_hb), g_rows + g_hb - 1), c0); };
     auto ldc = [&](int q) -> double {
@@ -366,7 +372,7 @@ __global__ void __launch_bounds__(128, KS_MINB) k_post(const StreamParams p) {
       // output after NU sweeps (stage NU; NU = 0 writes the corrected v)
       {
         const int y = yin - NU;
-        if (own_lane && y >= 2 * Q0 && y < 2 * Q0 + 2 * p.nq && y >= 0 && y < g_rows) {
+        if (own_lane && y >= 2 * Q0 && y < 2 * Qe && y >= 0 && y < g_rows) {
           *reinterpret_cast<double2*>(p.uo + kc_idx(P, y, c0)) = nw[NU];
           if (NORMS) acc_e = fma(nw[NU].y, nw[NU].y, fma(nw[NU].x, nw[NU].x, acc_e));
           if (DOT) acc_e = fma(fr[NU > 0 ? NU : 1].y, nw[NU].y, fma(fr[NU > 0 ? NU : 1].x, nw[NU].x, acc_e));
@@ -374,7 +380,7 @@ __global__ void __launch_bounds__(128, KS_MINB) k_post(const StreamParams p) {
       }
       if (NORMS) {
         const int y = yin - D;
-        if (own_lane && y >= 2 * Q0 && y < 2 * Q0 + 2 * p.nq && y >= 0 && y < g_rows)
+        if (own_lane && y >= 2 * Q0 && y < 2 * Qe && y >= 0 && y < g_rows)
           acc_r = fma(nw[D].y, nw[D].y, fma(nw[D].x, nw[D].x, acc_r));
       }
       if (DOT && yin == ye) reinterpret_cast<double2*>(p.part)[wg * 32 + lane] = make_double2(acc_e, 0.0);

@@ -50,6 +50,47 @@ KC_OX = 16
 FUSE_MIN_M = 127  # narrower levels keep the per-op strip kernels (kc_engine.cu KC_FUSE_MIN_M)
 
 
+def _floor2(a: int) -> int:
+    return a // 2  # Python floors negative halves, as kc_engine.cu floor2
+
+
+def pre_windows(rows: int, crows: int, nu1: int):
+    """Interior / boundary coarse-row windows of a fused strip pre pass
+    (kc_strip_pre_window): the interior window's outputs depend on the strip's
+    own rows only (fine input rows [2 qa - D, 2 qb + D], D = nu1 + 1), so it
+    runs with hb = 0 while the halo exchange is in flight; the boundary
+    windows [0, qa) and [qb, crows + 1) run after it.  None: too few rows."""
+    d = nu1 + 1
+    qa, qb = (d + 1) // 2, min(crows, (rows - 1 - d) // 2)
+    if qb - qa < 1:
+        return None
+    return (qa, qb), [(0, qa), (qb, crows + 1)]
+
+
+def post_windows(rows: int, crows: int, nu2: int, vc_halo: bool):
+    """The same for a fused strip post pass (kc_strip_post_window): fine rows
+    [2q - nu2, 2q' - 1 + nu2] of u and, when vc's halo is exchanged too
+    (vc_halo), the coarse rows those fine rows prolong from, inside the strip."""
+    def lo_ok(q):
+        lo = 2 * q - nu2
+        clo = lo // 2 - 1 if lo % 2 == 0 else _floor2(lo)
+        return lo >= 0 and (not vc_halo or clo >= 0)
+
+    def hi_ok(q):
+        hi = min(2 * q, rows) - 1 + nu2
+        return hi <= rows - 1 and (not vc_halo or _floor2(hi) <= crows - 1)
+
+    qa = 0
+    while qa <= crows and not lo_ok(qa):
+        qa += 1
+    qb = crows + 1
+    while qb > qa and not hi_ok(qb):
+        qb -= 1
+    if qb - qa < 1:
+        return None
+    return (qa, qb), [(0, qa), (qb, crows + 1)]
+
+
 def kc_pitch(m: int) -> int:
     """Row pitch (doubles) of a level with side m; mirrors kc_common.cuh."""
     return (KC_OX + m + 128 + 15) & ~15
@@ -153,17 +194,32 @@ class ThreadComm:
         sh = cls._Shared(world)
         return [cls(sh, r) for r in range(world)]
 
+    @staticmethod
+    def _settle(ts):
+        """CUDA tensors: wait for this thread's current stream, so a copy made
+        on one rank's stream is complete before another rank's stream (the
+        overlap side stream, say) reads it or the allocator reuses it."""
+        for t in ts:
+            if getattr(t, "is_cuda", False):
+                import torch
+                torch.cuda.current_stream(t.device).synchronize()
+                return
+
     def sendrecv(self, sends: dict, recvs: dict):
         self.seq += 1
         with self.s.cv:
-            for peer, t in sends.items():
-                self.s.box[(self.rank, peer, self.seq)] = t.clone()
+            boxed = {peer: t.clone() for peer, t in sends.items()}
+            self._settle(boxed.values())
+            for peer, t in boxed.items():
+                self.s.box[(self.rank, peer, self.seq)] = t
             self.s.cv.notify_all()
             for peer, t in recvs.items():
                 key = (peer, self.rank, self.seq)
                 while key not in self.s.box:
                     self.s.cv.wait()
-                t.copy_(self.s.box.pop(key))
+                src = self.s.box.pop(key)
+                t.copy_(src)
+                self._settle([t])
 
     def allreduce_sum(self, t):
         self.s.slots[self.rank] = t.clone()
@@ -224,16 +280,28 @@ class CudaStripOps:
         self.N.check(self.N.lib.kc_strip_prolong_add(self._p(v, HALO), self._p(vc, HALO), ny, nx, v.shape[1],
                                                      vc.shape[1], int(zero), self._stream()))
 
-    # fused passes (kc_strip_pre / kc_strip_post): the single-GPU streaming kernels on the strip
-    def pre(self, u, f, uo, fc, ny, nx, crows, gy0, mg, w, omega, nu1, zero):
-        self.N.check(self.N.lib.kc_strip_pre(self._p(u, HALO), self._p(f, HALO), self._p(uo, HALO), self._p(fc, HALO),
-                                             ny, nx, u.shape[1], fc.shape[1], crows, gy0, mg, HALO, self._w(w),
-                                             omega, nu1, int(zero), self._stream()))
+    # fused passes (kc_strip_pre / kc_strip_post): the single-GPU streaming kernels on the strip;
+    # window = (q_lo, q_hi): only those coarse-row chunk positions (kc_strip_*_window), reading
+    # no more than hb fine / hbc coarse halo rows
+    def pre(self, u, f, uo, fc, ny, nx, crows, gy0, mg, w, omega, nu1, zero, window=None, hb=HALO):
+        N = self.N
+        args = (self._p(u, HALO), self._p(f, HALO), self._p(uo, HALO), self._p(fc, HALO), ny, nx, u.shape[1],
+                fc.shape[1], crows, gy0, mg)
+        if window is None:
+            N.check(N.lib.kc_strip_pre(*args, HALO, self._w(w), omega, nu1, int(zero), self._stream()))
+        else:
+            N.check(N.lib.kc_strip_pre_window(*args, hb, window[0], window[1], self._w(w), omega, nu1, int(zero),
+                                              self._stream()))
 
-    def post(self, u, f, uo, vc, ny, nx, crows, gy0, mg, w, omega, nu2, zero):
-        self.N.check(self.N.lib.kc_strip_post(self._p(u, HALO), self._p(f, HALO), self._p(uo, HALO),
-                                              self._p(vc, HALO), ny, nx, u.shape[1], vc.shape[1], crows, gy0, mg,
-                                              HALO, HALO, self._w(w), omega, nu2, int(zero), self._stream()))
+    def post(self, u, f, uo, vc, ny, nx, crows, gy0, mg, w, omega, nu2, zero, window=None, hb=HALO, hbc=HALO):
+        N = self.N
+        args = (self._p(u, HALO), self._p(f, HALO), self._p(uo, HALO), self._p(vc, HALO), ny, nx, u.shape[1],
+                vc.shape[1], crows, gy0, mg)
+        if window is None:
+            N.check(N.lib.kc_strip_post(*args, HALO, HALO, self._w(w), omega, nu2, int(zero), self._stream()))
+        else:
+            N.check(N.lib.kc_strip_post_window(*args, hb, hbc, window[0], window[1], self._w(w), omega, nu2,
+                                               int(zero), self._stream()))
 
     def norms(self, v, f, ny, nx, w, out=None):
         """(sum v^2, sum (f - A v)^2) over the strip into `out` (2 doubles; new tensor if None)."""
@@ -331,6 +399,7 @@ class _Strip:
         self.f = ops.zeros(rows, pitch)
         self.cur = 0
         self.vzero = True
+        self.fpend = False  # f's halo rows still to exchange (restricted into, not yet exchanged)
 
 
 class DistributedKappaSolver:
@@ -341,7 +410,7 @@ class DistributedKappaSolver:
     """
 
     def __init__(self, problem: ProblemSpec, config: CycleConfig, comm, ops=None, make_coarse=None,
-                 min_rows: int = 64, device: int = 0, graphs: bool = True):
+                 min_rows: int = 64, device: int = 0, graphs: bool = True, overlap: bool | None = None):
         if config.coarsening is not Coarsening.FULL_STANDARD:
             raise ValueError("distributed cycles support full coarsening only")
         self.problem, self.config, self.comm = problem, config, comm
@@ -380,6 +449,15 @@ class DistributedKappaSolver:
         if self._graphs_ok:
             import torch
             self._nrm = torch.zeros(2, dtype=torch.float64, device=self.ops.device)
+        # halo exchange overlapped with the interior rows of the fused strip
+        # passes (a side stream; default: on with CUDA strips and > 1 rank;
+        # True forces the interior / boundary split even without exchanges)
+        cuda = isinstance(self.ops, CudaStripOps)
+        self.overlap = (cuda and self.world > 1) if overlap is None else (bool(overlap) and cuda)
+        self._side = None
+        if self.overlap:
+            import torch
+            self._side = torch.cuda.Stream(device=self.ops.device, priority=-1)
 
     # -- data in/out -------------------------------------------------------
     def set_level1(self, which: str, full: np.ndarray):
@@ -425,6 +503,30 @@ class DistributedKappaSolver:
             # views): receive straight into the ghost rows
             self.comm.sendrecv(sends, recvs)
 
+    def _exchange_then(self, exchanges, whole, inner, outer):
+        """Run the halo exchanges, then a fused strip pass.  With overlap the
+        exchanges go to a side stream (forked from and joined back into the
+        current stream, so a captured graph keeps the order) while the pass's
+        interior window `inner()` runs on the current stream; the boundary
+        windows `outer()` follow the join.  Otherwise exchange, then `whole()`."""
+        if not self.overlap or inner is None:
+            for ex in exchanges:
+                self._halo(*ex)
+            whole()
+            return
+        torch = self.ops.torch
+        main = torch.cuda.current_stream(self.ops.device)
+        side = self._side
+        if exchanges:
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                for ex in exchanges:
+                    self._halo(*ex)
+        inner()
+        if exchanges:
+            main.wait_stream(side)
+        outer()
+
     def _materialize(self, s: _Strip):
         if s.vzero:
             s.v[s.cur].zero_()
@@ -447,45 +549,70 @@ class DistributedKappaSolver:
                 and self.nu1 + 2 <= HALO and self.nu2 + 1 <= HALO
                 and min(b - a for a, b in self.plan.rows[l - 1]) >= HALO)
 
+    def _fused_pre(self, l: int, fc, crows: int, exchanges):
+        """nu1 sweeps + residual + full weighting in one pass (cycle.py:211-213)
+        into fc (crows local coarse rows), after / overlapped with `exchanges`."""
+        s = self.strips[l - 1]
+        u, uo, zero = s.v[s.cur], s.v[s.cur ^ 1], s.vzero
+        args = (u, s.f, uo, fc, s.ny, s.m, crows, s.a, s.m, self.w[l - 1], self.omega, self.nu1, zero)
+        win = pre_windows(s.ny, crows, self.nu1) if self.overlap else None
+        self._exchange_then(
+            exchanges, lambda: self.ops.pre(*args),
+            None if win is None else (lambda: self.ops.pre(*args, window=win[0], hb=0)),
+            None if win is None else (lambda: [self.ops.pre(*args, window=w) for w in win[1]]))
+        if self.nu1 > 0:
+            s.cur ^= 1
+            s.vzero = False
+
+    def _fused_post(self, l: int, vc, vc_rows: int, exchanges, vc_halo: bool):
+        """v + P vc and nu2 sweeps in one pass (cycle.py:219-220)."""
+        s = self.strips[l - 1]
+        args = (s.v[s.cur], s.f, s.v[s.cur ^ 1], vc, s.ny, s.m, vc_rows, s.a, s.m, self.w[l - 1], self.omega,
+                self.nu2, s.vzero)
+        win = post_windows(s.ny, vc_rows, self.nu2, vc_halo) if self.overlap else None
+        hbc = 0 if vc_halo else HALO
+        self._exchange_then(
+            exchanges, lambda: self.ops.post(*args),
+            None if win is None else (lambda: self.ops.post(*args, window=win[0], hb=0, hbc=hbc)),
+            None if win is None else (lambda: [self.ops.post(*args, window=w) for w in win[1]]))
+        s.cur ^= 1
+        s.vzero = False
+
     def _cycle(self, l: int, kappa: int):
         s = self.strips[l - 1]
         nd = self.plan.n_dist
         fused = self._fused(l)
-        if fused:  # nu1 sweeps + residual + full weighting in one pass (cycle.py:211-213)
-            if not s.vzero:  # the last owned coarse row reaches nu1 + 2 fine rows below the strip
-                self._halo(s, s.v[s.cur], self.nu1 + 2)
+        pending = [(s, s.f, HALO)] if s.fpend else []  # f restricted into this level by the parent
+        s.fpend = False
+        if fused:  # the last owned coarse row reaches nu1 + 2 fine rows below the strip
+            if not s.vzero:
+                pending.append((s, s.v[s.cur], self.nu1 + 2))
         else:
+            for ex in pending:
+                self._halo(*ex)
             self._relax(l, self.nu1)
             if not s.vzero:
                 self._halo(s, s.v[s.cur], 2)
         if l < nd:  # restrict into the next distributed strip
             c = self.strips[l]
             if fused:
-                self.ops.pre(s.v[s.cur], s.f, s.v[s.cur ^ 1], c.f, s.ny, s.m, c.ny, s.a, s.m, self.w[l - 1],
-                             self.omega, self.nu1, s.vzero)
-                if self.nu1 > 0:
-                    s.cur ^= 1
-                    s.vzero = False
+                self._fused_pre(l, c.f, c.ny, pending)
             else:
                 self.ops.resid_restrict(s.v[s.cur], s.f, c.f, c.ny, c.m, self.w[l - 1], s.vzero)
-            self._halo(c, c.f, HALO)
+            c.fpend = True  # exchanged by the child's first pass (overlapped with its interior rows)
             c.vzero = True
             self._cycle(l + 1, kappa)
             if kappa > 1:
                 self._cycle(l + 1, kappa - 1)
-            self._halo(c, c.v[c.cur], self.nu2 // 2 + 2)
             vc, vc_rows = c.v[c.cur], c.ny
+            post_ex = [(c, vc, self.nu2 // 2 + 2)]
         else:  # agglomerate: all-gather the coarse rows, replicated sub-cycle
             mc = self.plan.side(l + 1)
             q0, q1 = s.a // 2, (s.b // 2 if self.rank < self.world - 1 else mc)
             maxq = max((b // 2 if r < self.world - 1 else mc) - a // 2 for r, (a, b) in enumerate(self.plan.rows[l - 1]))
             part = self.ops.zeros(maxq + 2 * HALO, self.cfull.shape[1])
             if fused:
-                self.ops.pre(s.v[s.cur], s.f, s.v[s.cur ^ 1], part, s.ny, s.m, q1 - q0, s.a, s.m, self.w[l - 1],
-                             self.omega, self.nu1, s.vzero)
-                if self.nu1 > 0:
-                    s.cur ^= 1
-                    s.vzero = False
+                self._fused_pre(l, part, q1 - q0, pending)
             else:
                 self.ops.resid_restrict(s.v[s.cur], s.f, part, q1 - q0, mc, self.w[l - 1], s.vzero)
             parts = self.comm.allgather(part)
@@ -501,14 +628,14 @@ class DistributedKappaSolver:
             vc = self.vfull[q0:]  # local coarse row 0 <-> global row q0 (ghost rows above)
             # view whose interior origin (row HALO) is coarse row q0: vfull row HALO + q0
             vc_rows = q1 - q0
-        if fused:  # v + P vc and nu2 sweeps in one pass (cycle.py:219-220)
+            post_ex = []
+        if fused:
             if not s.vzero:
-                self._halo(s, s.v[s.cur], max(self.nu2, 1))
-            self.ops.post(s.v[s.cur], s.f, s.v[s.cur ^ 1], vc, s.ny, s.m, vc_rows, s.a, s.m, self.w[l - 1],
-                          self.omega, self.nu2, s.vzero)
-            s.cur ^= 1
-            s.vzero = False
+                post_ex.append((s, s.v[s.cur], max(self.nu2, 1)))
+            self._fused_post(l, vc, vc_rows, post_ex, vc_halo=l < nd)
         else:
+            for ex in post_ex:
+                self._halo(*ex)
             self.ops.prolong_add(s.v[s.cur], vc, s.ny, s.m, s.vzero)
             s.vzero = False
             self._relax(l, self.nu2)

@@ -345,3 +345,79 @@ def test_gloo_two_ranks_pcg_and_device_stop():
         assert sst == "converged"
     n5 = O.standalone(1e-4, 45.0, 5, 2, target=1e8, stop="residual")
     assert all(r[4] == n5["iterations"] for r in res), (res[0][4], n5["iterations"])
+
+
+# ---------------------------------------------------------------------------
+# interior / boundary windows of the overlapped fused strip passes
+# ---------------------------------------------------------------------------
+
+def _pre_deps(rows, crows, nu1, qlo, qhi):
+    """Fine input rows the owned outputs of a pre window read (brute force)."""
+    d = nu1 + 1
+    need = set()
+    for y in range(2 * qlo, min(2 * qhi, rows)):  # uo rows after nu1 sweeps
+        if nu1:
+            need.update(range(y - nu1, y + nu1 + 1))
+    for q in range(qlo, min(qhi, crows)):  # residual rows 2q..2q+2, one more stencil, nu1 sweeps
+        need.update(range(2 * q - d, 2 * q + 2 + d + 1))
+    return need
+
+
+def _post_deps(rows, nu2, qlo, qhi):
+    need, cneed = set(), set()
+    for y in range(2 * qlo, min(2 * qhi, rows)):
+        for yy in range(y - nu2, y + nu2 + 1):
+            need.add(yy)
+            cneed.update({yy // 2 - 1, yy // 2} if yy % 2 == 0 else {yy // 2})
+    return need, cneed
+
+
+@pytest.mark.parametrize("rows,crows", [(86, 43), (84, 42), (85, 42), (512, 256), (17, 8), (30, 15)])
+@pytest.mark.parametrize("nu", [0, 1, 2, 3, 4])
+def test_overlap_windows_cover_and_stay_inside(rows, crows, nu):
+    from paper_2010_00626_b200.distributed import post_windows, pre_windows
+    win = pre_windows(rows, crows, nu)
+    if win is not None:
+        (qa, qb), outer = win
+        assert outer == [(0, qa), (qb, crows + 1)] and 0 < qa < qb <= crows
+        dep = _pre_deps(rows, crows, nu, qa, qb)
+        assert min(dep) >= 0 and max(dep) <= rows - 1  # interior: no halo row
+        assert min(_pre_deps(rows, crows, nu, qa - 1, qb)) < 0 or max(_pre_deps(rows, crows, nu, qa, qb + 1)) > rows - 1
+    else:
+        assert rows < 2 * (nu + 3)
+    for vc_halo in (True, False):
+        win = post_windows(rows, crows, nu, vc_halo)
+        if win is None:
+            continue
+        (qa, qb), outer = win
+        assert outer == [(0, qa), (qb, crows + 1)]
+        dep, cdep = _post_deps(rows, nu, qa, qb)
+        assert min(dep) >= 0 and max(dep) <= rows - 1
+        if vc_halo:
+            assert min(cdep) >= 0 and max(cdep) <= crows - 1
+        # maximal: one more position on either side would read a halo row
+        d0, c0 = _post_deps(rows, nu, qa - 1, qb) if qa > 0 else ({-1}, {-1})
+        assert min(d0) < 0 or (vc_halo and min(c0) < 0)
+
+
+def test_window_entry_points_reject_halo_reads_without_gpu():
+    """kc_strip_*_window validate the window against hb / hbc before touching
+    the device: one coarse row too far reads a halo row -> KC_EINVAL (the
+    overlap split relies on hb = 0 meaning 'no halo row')."""
+    import ctypes as C
+
+    from paper_2010_00626_b200 import _native as N
+    from paper_2010_00626_b200.distributed import post_windows, pre_windows
+    w = (C.c_double * 9)(*([-1.0] * 4 + [8.0] + [-1.0] * 4))
+    fake = 1 << 20  # never dereferenced: validation fails first
+    rows, crows, nu = 86, 43, 2
+    (qa, qb), _ = pre_windows(rows, crows, nu)
+    for lo, hi in [(qa - 1, qb), (qa, qb + 1)]:
+        rc = N.lib.kc_strip_pre_window(fake, fake, fake, fake, rows, 255, 288, 160, crows, 86, 255, 0, lo, hi, w, 0.8,
+                                       nu, 0, None)
+        assert rc == N.KC_EINVAL, (lo, hi)
+    (qa, qb), _ = post_windows(rows, crows, nu, True)
+    for lo, hi in [(qa - 1, qb), (qa, qb + 1)]:
+        rc = N.lib.kc_strip_post_window(fake, fake, fake, fake, rows, 255, 288, 160, crows, 86, 255, 0, 0, lo, hi, w,
+                                        0.8, nu, 0, None)
+        assert rc == N.KC_EINVAL, (lo, hi)

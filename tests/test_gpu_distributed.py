@@ -114,3 +114,86 @@ def test_nccl_world1_graph_batched_pcg_and_solve():
         assert any(k[0] == "pcg" for k in s._graphs) and any(k[0] == "solve" for k in s._graphs)
     finally:
         dist.destroy_process_group()
+
+
+def _strip_bufs(ops, glob, a, rows, pitch, halo_fill=None):
+    """A strip buffer holding global rows [a - HALO, a + rows + HALO) of glob
+    (zero outside the domain); halo_fill replaces the halo rows (e.g. NaN)."""
+    import torch
+
+    from paper_2010_00626_b200.distributed import HALO, KC_OX
+    mg, m = glob.shape
+    host = np.zeros((rows + 2 * HALO, pitch))
+    for r in range(rows + 2 * HALO):
+        g = a - HALO + r
+        if 0 <= g < mg:
+            host[r, KC_OX:KC_OX + m] = glob[g]
+    if halo_fill is not None:
+        host[:HALO, KC_OX:KC_OX + m] = halo_fill
+        host[HALO + rows:, KC_OX:KC_OX + m] = halo_fill
+    return torch.from_numpy(host).to(ops.device)
+
+
+@pytest.mark.parametrize("nu", [0, 1, 2, 3, 4])
+def test_strip_windows_equal_whole_pass(nu):
+    """kc_strip_pre_window / kc_strip_post_window: the interior window with
+    hb = hbc = 0 reads no halo row (the halos are NaN during it) and, with the
+    boundary windows after it, reproduces the whole-strip pass bit for bit --
+    the overlap split of distributed.py."""
+    from paper_2010_00626_b200.distributed import HALO, KC_OX, CudaStripOps, kc_pitch, post_windows, pre_windows
+    from paper_2010_00626_b200.stencil import rotated_anisotropic_stencil
+    ops = CudaStripOps(0)
+    mg, mc = 255, 127
+    P, Pc = kc_pitch(mg), kc_pitch(mc)
+    rng = np.random.default_rng(nu)
+    U, F, VC = rng.random((mg, mg)), rng.standard_normal((mg, mg)), rng.random((mc, mc))
+    w = np.asarray(rotated_anisotropic_stencil(1e-4, 45.0).w, dtype=np.float64).reshape(9)
+    for a, b in [(0, 86), (86, 170), (170, 255)]:
+        rows = b - a
+        crows = (b // 2 if b < mg else mc) - a // 2
+        win = pre_windows(rows, crows, nu)
+        assert win is not None
+        outs = []
+        for split in (False, True):
+            u = _strip_bufs(ops, U, a, rows, P)
+            f = _strip_bufs(ops, F, a, rows, P)
+            uo, fc = ops.zeros(rows + 2 * HALO, P), ops.zeros(crows + 2 * HALO, Pc)
+            args = (u, f, uo, fc, rows, mg, crows, a, mg, w, 0.8, nu, False)
+            if not split:
+                ops.pre(*args)
+            else:
+                un = _strip_bufs(ops, U, a, rows, P, halo_fill=np.nan)
+                fn_ = _strip_bufs(ops, F, a, rows, P, halo_fill=np.nan)
+                ops.pre(un, fn_, uo, fc, *args[4:], window=win[0], hb=0)
+                for wd in win[1]:
+                    ops.pre(*args, window=wd)
+            outs.append((uo[HALO:HALO + rows, KC_OX:KC_OX + mg].cpu().numpy(),
+                         fc[HALO:HALO + crows, KC_OX:KC_OX + mc].cpu().numpy()))
+        assert np.isfinite(outs[1][1]).all()
+        if nu:
+            assert np.array_equal(outs[0][0], outs[1][0]), (a, b)
+        assert np.array_equal(outs[0][1], outs[1][1]), (a, b)
+        # post: v + P vc, nu sweeps; vc's halo exchanged (distributed coarse level) or local
+        for vc_halo in (True, False):
+            pw = post_windows(rows, crows, nu, vc_halo)
+            assert pw is not None
+            q0 = a // 2
+            res = []
+            for split in (False, True):
+                u = _strip_bufs(ops, U, a, rows, P)
+                f = _strip_bufs(ops, F, a, rows, P)
+                vc = _strip_bufs(ops, VC, q0, crows, Pc)
+                uo = ops.zeros(rows + 2 * HALO, P)
+                args = (u, f, uo, vc, rows, mg, crows, a, mg, w, 0.8, nu, False)
+                if not split:
+                    ops.post(*args)
+                else:
+                    un = _strip_bufs(ops, U, a, rows, P, halo_fill=np.nan)
+                    fn_ = _strip_bufs(ops, F, a, rows, P, halo_fill=np.nan)
+                    vcn = _strip_bufs(ops, VC, q0, crows, Pc, halo_fill=np.nan) if vc_halo else vc
+                    ops.post(un, fn_, uo, vcn, *args[4:], window=pw[0], hb=0, hbc=0 if vc_halo else HALO)
+                    for wd in pw[1]:
+                        ops.post(*args, window=wd)
+                res.append(uo[HALO:HALO + rows, KC_OX:KC_OX + mg].cpu().numpy())
+            assert np.isfinite(res[1]).all()
+            assert np.array_equal(res[0], res[1]), (a, b, vc_halo)

@@ -594,13 +594,17 @@ def test_n12_pcg_vs_reference(kname):
 # multi-rank decomposition with the CUDA strip kernels (thread ranks on one GPU)
 # ---------------------------------------------------------------------------
 
+@pytest.mark.parametrize("overlap", [False, True])
 @pytest.mark.parametrize("world,kappa,nu", [(1, 2, (2, 2)), (2, 1, (2, 2)), (2, 3, (2, 2)), (3, 1, (2, 2)),
                                              (3, 3, (2, 2)),
                                              (2, 2, (1, 1)), (2, 2, (3, 0)), (3, 2, (0, 3)), (2, 2, (4, 4))])
-def test_distributed_cuda_strips_bit_exact(world, kappa, nu):
+def test_distributed_cuda_strips_bit_exact(world, kappa, nu, overlap):
     """Thread ranks on one GPU: the fused strip passes (kc_strip_pre/post with
     deep halos) on the distributed levels >= 127 wide, per-op strip kernels
-    below and for nu1 > 3, agglomeration onto the native engine."""
+    below and for nu1 > 3, agglomeration onto the native engine.  overlap:
+    each fused pass as an interior window (no halo rows read) on the compute
+    stream while the halos move on a side stream, then the boundary windows
+    (kc_strip_*_window)."""
     import threading
 
     from paper_2010_00626_b200.distributed import DistributedKappaSolver, ThreadComm
@@ -621,8 +625,8 @@ def test_distributed_cuda_strips_bit_exact(world, kappa, nu):
     def body(r):
         try:
             s = DistributedKappaSolver(ProblemSpec(eps, phi), CycleConfig(n=n, kappa=kappa, nu1=nu1, nu2=nu2),
-                                       comms[r], min_rows=32)
-            assert s.plan.n_dist >= 2
+                                       comms[r], min_rows=32, overlap=overlap)
+            assert s.plan.n_dist >= 2 and s.overlap == overlap
             s.set_level1("v", v0)
             s.set_level1("f", f0)
             got = []
@@ -732,8 +736,10 @@ def test_distributed_nccl_world1_graph_replay_bit_exact():
     torch.cuda.set_device(0)
     dist.init_process_group("nccl", device_id=torch.device("cuda:0"), rank=0, world_size=1)
     try:
-        s = DistributedKappaSolver(ProblemSpec(eps, phi), CycleConfig(n=n, kappa=kappa), TorchComm(), min_rows=32)
-        assert s.plan.n_dist >= 2 and s._graphs_ok
+        # overlap forced: the side-stream fork / join and the window launches inside the captured graph
+        s = DistributedKappaSolver(ProblemSpec(eps, phi), CycleConfig(n=n, kappa=kappa), TorchComm(), min_rows=32,
+                                   overlap=True)
+        assert s.plan.n_dist >= 2 and s._graphs_ok and s.overlap
         s.set_level1("v", v0)
         s.set_level1("f", f0)
         for c in range(4):
