@@ -168,7 +168,7 @@ struct kc_handle {
   // but as slow as the two passes it replaces (2047^2: 57 vs 32 + 27 us;
   // these passes are issue-bound, not traffic-bound), so off by default
   bool postpre_stream = false;
-  bool ks_sym_on = true;      // shared w1/w7 products on symmetric levels (KC_SYM=0: off)
+  int ks_sym_max = 2;         // shared products on symmetric levels: 0 off, 1 w1/w7 only, 2 all (KC_SYM)
   int num_sms = 148;
   SolveState* d_solve = nullptr;   // device loop state
   double* d_hist = nullptr;        // err | res histories for the device loop
@@ -766,11 +766,18 @@ int ks_choose_nq(int mc, int nbands, int slots) {
 }
 
 typedef void (*KsFn)(StreamParams);
-// sym: the level's stencil has w7 == w1 bitwise (ks_step<SYM>); the shared
-// products are instantiated for the nu = 2 passes that stream level 1
-bool ks_sym(const St9& s) { return std::memcmp(&s.w[1], &s.w[7], sizeof(double)) == 0; }
-KsFn ks_pre_fn(int nu, bool zero, bool norms = false, bool sym = false) {
-  if (sym && nu == 2 && !zero) return norms ? k_pre<2, false, true, false, true> : k_pre<2, false, false, false, true>;
+// sym: 1 if the level's stencil has w7 == w1 bitwise, 2 if it is moreover
+// point-symmetric with w0 == -w2 (ks_step<SYM>); the shared products are
+// instantiated for the nu = 2 passes that stream level 1
+int ks_sym(const St9& s) {
+  auto eq = [](double a, double b) { return std::memcmp(&a, &b, sizeof(double)) == 0; };
+  if (!eq(s.w[1], s.w[7])) return 0;
+  if (eq(s.w[0], s.w[8]) && eq(s.w[2], s.w[6]) && eq(s.w[3], s.w[5]) && eq(s.w[0], -s.w[2])) return 2;
+  return 1;
+}
+KsFn ks_pre_fn(int nu, bool zero, bool norms = false, int sym = 0) {
+  if (sym == 2 && nu == 2 && !zero) return norms ? k_pre<2, false, true, false, 2> : k_pre<2, false, false, false, 2>;
+  if (sym && nu == 2 && !zero) return norms ? k_pre<2, false, true, false, 1> : k_pre<2, false, false, false, 1>;
 #define KS_PRE(N) return zero ? k_pre<N, true> : (norms ? k_pre<N, false, true> : k_pre<N, false>)
   switch (nu) {
     case 0: KS_PRE(0);
@@ -782,8 +789,11 @@ KsFn ks_pre_fn(int nu, bool zero, bool norms = false, bool sym = false) {
 #undef KS_PRE
   return nullptr;
 }
-KsFn ks_post_fn(int nu, bool vz, int nm, bool sym = false) {
-  if (sym && nu == 2 && nm == 0) return vz ? k_post<2, true, 0, false, true> : k_post<2, false, 0, false, true>;
+// the post pass keeps SYM = 1: with all products shared it needs 100
+// registers instead of 78 (5 instead of 6 blocks per SM) and level-1 post
+// slows down 94 -> 102 us, while the pre pass gains 112 -> 107 us (exact)
+KsFn ks_post_fn(int nu, bool vz, int nm, int sym = 0) {
+  if (sym && nu == 2 && nm == 0) return vz ? k_post<2, true, 0, false, 1> : k_post<2, false, 0, false, 1>;
 #define KS_POST(N)                                                                            \
   return vz ? (nm == 1 ? k_post<N, true, 1> : nm == 2 ? k_post<N, true, (N > 0 ? 2 : 0)> : k_post<N, true, 0>) \
             : (nm == 1 ? k_post<N, false, 1> : nm == 2 ? k_post<N, false, (N > 0 ? 2 : 0)> : k_post<N, false, 0>)
@@ -1089,7 +1099,7 @@ int ex_pre(kc_handle* h, int l, bool norms = false) {
   if (L.m <= KC_CTILE_MAX_M && h->tile && !norms && h->nu1 <= 2) return ex_ctile_pre(h, l);
   if (L.m <= KC_TILE_MAX_M && h->tile && !norms) return ex_tile(h, l, true);
   int nw = 0;
-  KsFn fn = ks_pre_fn(h->nu1, L.vzero, norms, h->ks_sym_on && ks_sym(L.st));
+  KsFn fn = ks_pre_fn(h->nu1, L.vzero, norms, std::min(h->ks_sym_max, ks_sym(L.st)));
   StreamParams p = ks_params(h, l, h->nu1 + 1, &nw, (const void*)fn);
   if (norms) {
     if (32 * nw > h->npart_cap) KC_FAIL(h, KC_EINVAL, "norm partial buffer too small (%d < %d)", h->npart_cap, 32 * nw);
@@ -1125,7 +1135,7 @@ int ex_post(kc_handle* h, int l, int nm) {
   if (L.m <= KC_TILE_POST_MAX_M && h->tile && !nm) return ex_tile(h, l, false);
   int nw = 0;
   const int D = h->nu2 + (nm == 1 ? 1 : 0);
-  KsFn fn = ks_post_fn(h->nu2, L.vzero, nm, h->ks_sym_on && ks_sym(L.st));
+  KsFn fn = ks_post_fn(h->nu2, L.vzero, nm, std::min(h->ks_sym_max, ks_sym(L.st)));
   StreamParams p = ks_params(h, l, D > 0 ? D : 1, &nw, (const void*)fn);
   p.vc = C.v[C.cur];
   if (nm) {
@@ -1549,7 +1559,7 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
     const char* senv = getenv("KC_SYM");
     // the shared-product form only saves work when products are separately
     // rounded; in the FMA build every product is fused into its sum
-    h->ks_sym_on = senv ? senv[0] != '0' : !KC_FAST;
+    h->ks_sym_max = senv ? atoi(senv) : (KC_FAST ? 0 : 2);
   }
   h->num_sms = prop.multiProcessorCount;
   h->n = n;

@@ -89,10 +89,14 @@ __device__ __forceinline__ double2 ks_ld2(const double* __restrict__ a, size_t i
 // cp.async (LDGSTS): each lane copies and later reads back only its own 16
 // bytes, so no warp synchronisation is needed, and a load in flight never
 // holds a register (a register queue would make every shift wait for it).
-#define KS_PF 4       // prefetch distance (rows)
-#define KS_URING 8    // u ring slots (> KS_PF)
+#ifndef KS_PF
+#define KS_PF 4       // prefetch distance (rows); 3 / 6 / 8 measured: 6 and 8 slower (not latency-bound)
+#endif
+#define KS_URING (KS_PF < 8 ? 8 : 16)  // u ring slots (> KS_PF)
 // f ring: stage t reads row yin - t, so rows yin - D .. yin + KS_PF are live
-__host__ __device__ constexpr int ks_fring(int D) { return D + KS_PF + 1 <= 8 ? 8 : 16; }
+__host__ __device__ constexpr int ks_fring(int D) {
+  return D + KS_PF + 1 <= 8 ? 8 : (D + KS_PF + 1 <= 16 ? 16 : 32);
+}
 __host__ __device__ constexpr int ks_warp_smem_doubles(int D) { return (KS_URING + ks_fring(D)) * KS_BAND; }
 // dynamic shared memory of a 128-thread streaming block with D stages
 __host__ __device__ constexpr int ks_smem_bytes(int D) { return 4 * ks_warp_smem_doubles(D) * (int)sizeof(double); }
@@ -117,9 +121,33 @@ struct KsAcc {
 // SYM: the stencil's north and south centre taps are bitwise equal (w7 ==
 // w1, true of the finest level's stencil), so w7 * n and w1 * n are the same
 // rounded product and each is computed once: 2 fewer multiplies per stage.
-template <bool SYM = false>
+// SYM = 2: the stencil is also point-symmetric (w0 = w8, w2 = w6, w3 = w5)
+// with w0 = -w2 bitwise (the finest level's rotated stencil, stencil.py:
+// 97-105): every product an input value takes part in is one of cross*u,
+// ns*u, ew*u, c*u, so each is computed once, the west/east neighbours'
+// products arrive by shuffle instead of their values, and w0*u, w8*u are the
+// exact negations of cross*u (IEEE negation is exact; x + (-y) is x - y, and
+// 0 + w0*l -- DMUL0 -- is 0 - cross*l, signed zeros included): 26 fp64
+// operations per step instead of 32, bit-identical.
+template <int SYM = 0>
 __device__ __forceinline__ void ks_step(const St9& s, KsAcc& a, double2 n, double& aux, double& auy,
                                         double2& cen) {
+  if constexpr (SYM == 2) {
+    const double cx = DMUL(s.w[2], n.x), cy = DMUL(s.w[2], n.y);  // w2 = w6 = -w0 = -w8
+    const double sx = DMUL(s.w[1], n.x), sy = DMUL(s.w[1], n.y);  // w1 = w7
+    const double ex = DMUL(s.w[3], n.x), ey = DMUL(s.w[3], n.y);  // w3 = w5
+    const double cl = kc_shfl_up1(cy), el = kc_shfl_up1(ey);      // column c0 - 1
+    const double cr = kc_shfl_dn1(cx), er = kc_shfl_dn1(ex);      // column c0 + 2
+    aux = DSUB(DADD(DADD(a.c.x, cl), sx), cy);
+    auy = DSUB(DADD(DADD(a.c.y, cx), sy), cr);
+    cen = a.cen;
+    a.c.x = DADD(DADD(DADD(a.b.x, el), DMUL(s.w[4], n.x)), ey);
+    a.c.y = DADD(DADD(DADD(a.b.y, ex), DMUL(s.w[4], n.y)), er);
+    a.b.x = DADD(DADD(DSUB(0.0, cl), sx), cy);
+    a.b.y = DADD(DADD(DSUB(0.0, cx), sy), cr);
+    a.cen = n;
+    return;
+  }
   const double l = kc_shfl_up1(n.y), e = kc_shfl_dn1(n.x);
   const double p1x = DMUL(s.w[1], n.x), p1y = DMUL(s.w[1], n.y);
   const double p7x = SYM ? p1x : DMUL(s.w[7], n.x), p7y = SYM ? p1y : DMUL(s.w[7], n.y);
@@ -148,7 +176,7 @@ __device__ __forceinline__ void ks_mask(double2& v, int y, int mg, bool colx_in,
 // Stage t (1..D) consumes the row stage t-1 produced in the same step and
 // completes its own output one row behind it (ks_step), so stage t emits row
 // yin - t and a chunk needs only D warm-up rows per side.
-template <int NU, bool ZERO, bool NORMS = false, bool STRIP = false, bool SYM = false>
+template <int NU, bool ZERO, bool NORMS = false, bool STRIP = false, int SYM = 0>
 __global__ void __launch_bounds__(128, KS_MINB) k_pre(const StreamParams p) {
   constexpr int D = NU + 1;
   // row geometry (StreamParams): compile-time whole-level values unless STRIP
@@ -279,7 +307,7 @@ __global__ void __launch_bounds__(128, KS_MINB) k_pre(const StreamParams p) {
 // NM = 0: plain; 1: ||v'||^2 and ||f - A v'||^2 (one extra residual stage,
 // per-warp partials); 2: f . v' (the PCG rz = r . z of a preconditioning
 // cycle, whose f is r and whose result is z; per-lane partials, NU >= 1).
-template <int NU, bool VZ, int NM, bool STRIP = false, bool SYM = false>
+template <int NU, bool VZ, int NM, bool STRIP = false, int SYM = 0>
 __global__ void __launch_bounds__(128, KS_MINB) k_post(const StreamParams p) {
   constexpr bool NORMS = NM == 1, DOT = NM == 2;
   const int g_rows = STRIP ? p.rows : p.m, g_y0 = STRIP ? p.gy0 : 0, g_mg = STRIP ? p.mg : p.m;

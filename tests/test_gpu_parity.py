@@ -753,10 +753,12 @@ def test_distributed_nccl_world1_graph_replay_bit_exact():
 
 @pytest.mark.gpu
 def test_shared_product_passes_bit_exact(monkeypatch):
-    """The level-1 streaming passes with the shared w1/w7 products (KC_SYM,
-    ks_step<SYM>; the finest stencil is bitwise north/south symmetric) give the
-    oracle's iterates bit-for-bit, and the fused-norms pre pass used by the
-    solve loop gives the same histories and result as the plain passes."""
+    """The level-1 streaming passes with shared products (KC_SYM, ks_step<SYM>:
+    1 = the w1/w7 products, the finest stencil being bitwise north/south
+    symmetric; 2 = every product, the stencil being point-symmetric with
+    w0 = -w2) give the oracle's iterates bit-for-bit, and the fused-norms pre
+    pass used by the solve loop gives the same histories and result as the
+    plain passes."""
     n, m = 11, 2047
     rng = np.random.default_rng(11)
     v0, f0 = rng.random((m, m)), rng.standard_normal((m, m))
@@ -766,7 +768,7 @@ def test_shared_product_passes_bit_exact(monkeypatch):
     h.cycle(2)
     ref = h.v[0].copy()
     out = {}
-    for sym in ("1", "0"):
+    for sym in ("2", "1", "0"):
         monkeypatch.setenv("KC_SYM", sym)
         st = build_state(ProblemSpec(1e-4, 45.0), cfg)
         st.v[0], st.f[0] = v0, f0
@@ -776,9 +778,10 @@ def test_shared_product_passes_bit_exact(monkeypatch):
         k, status, _, err, res = st.solve_device(2, stop="residual", target_reduction=1e10, max_cycles=12)
         out[sym] = (k, status, err, res, np.asarray(st.v[0]).copy())
         st.close()
-    a, b = out["1"], out["0"]
-    assert a[:4] == b[:4]
-    assert np.array_equal(a[4], b[4])
+    for sym in ("2", "1"):
+        a, b = out[sym], out["0"]
+        assert a[:4] == b[:4], sym
+        assert np.array_equal(a[4], b[4]), sym
 
 
 @pytest.mark.parametrize("stream_pp", ["0", "1"])
