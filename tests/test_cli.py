@@ -13,6 +13,7 @@ import contextlib
 import io
 import json
 import math
+import os
 import sys
 
 import pytest
@@ -101,3 +102,32 @@ def test_solve_matches_reference(case):
                 assert _close(row[k], v, 1e-8), k
             else:
                 assert row[k] == v, k
+
+
+@pytest.mark.gpu
+def test_bench_timed_matches_reference_counts():
+    """`bench --reps 2` (bench_cycle's timed path, cycle.py:381-410): every
+    cell is timed on the device (mean_ms > 0) and its launch and unknown-touch
+    counts are the real reference's dry-run counts (golden `bench --reps 0`)."""
+    gold = next(c for c in json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cli.json")))
+                if c["argv"][0] == "bench")
+    rc, out = run(["bench", "--kappa", "1,2,inf", "--levels", "4-6", "--reps", "2"])
+    assert rc == 0
+    got = [line.split(",") for line in out.strip().splitlines()]
+    ref = [line.split(",") for line in gold["stdout"].strip().splitlines()]
+    assert got[0] == ref[0] and len(got) == len(ref)
+    for g, r in zip(got[1:], ref[1:]):
+        assert g[0:2] == r[0:2] and g[3:] == r[3:], (g, r)
+        assert float(g[2]) > 0.0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kappa", [1, 3, math.inf])
+def test_bench_cycle_api_timed(kappa):
+    from paper_2010_00626_b200 import CycleConfig, ProblemSpec
+    from paper_2010_00626_b200.cycle import bench_cycle
+    cfg = CycleConfig(n=9, kappa=kappa)
+    dry = bench_cycle(ProblemSpec(1e-4, 45.0), cfg, 0)
+    res = bench_cycle(ProblemSpec(1e-4, 45.0), cfg, 3)
+    assert dry.mean_ms is None and res.mean_ms is not None and 0.0 < res.mean_ms < 1e3
+    assert (res.launches, res.op_units) == (dry.launches, dry.op_units)
