@@ -2580,7 +2580,15 @@ int strip_slots(const void* fn, int D) {
     blocks = 1;
   return cache[fn] = blocks * 4 * sms;
 }
-KsFn strip_pre_fn(int nu, bool zero) {
+// sym: shared stencil products as in ks_pre_fn / ks_post_fn (exact build
+// only; the post pass keeps SYM <= 1)
+int strip_sym(const double* w9, double omega) {
+  static const int sym_max = getenv("KC_SYM") ? atoi(getenv("KC_SYM")) : (KC_FAST ? 0 : 2);
+  return std::min(sym_max, ks_sym(strip_stencil(w9, omega)));
+}
+KsFn strip_pre_fn(int nu, bool zero, int sym = 0) {
+  if (sym == 2 && nu == 2 && !zero) return k_pre<2, false, false, true, 2>;
+  if (sym && nu == 2 && !zero) return k_pre<2, false, false, true, 1>;
 #define KS_SPRE(N) return zero ? k_pre<N, true, false, true> : k_pre<N, false, false, true>
   switch (nu) {
     case 0: KS_SPRE(0);
@@ -2592,7 +2600,8 @@ KsFn strip_pre_fn(int nu, bool zero) {
 #undef KS_SPRE
   return nullptr;
 }
-KsFn strip_post_fn(int nu, bool vz) {
+KsFn strip_post_fn(int nu, bool vz, int sym = 0) {
+  if (sym && nu == 2) return vz ? k_post<2, true, 0, true, 1> : k_post<2, false, 0, true, 1>;
 #define KS_SPOST(N) return vz ? k_post<N, true, 0, true> : k_post<N, false, 0, true>
   switch (nu) {
     case 0: KS_SPOST(0);
@@ -2668,7 +2677,7 @@ extern "C" int kc_strip_pre_window(const double* u, const double* f, double* uo,
   if (!pre_window_rows(rows, crows, nu1, q_lo, q_hi, &lo, &hi)) return KC_OK;  // nothing owned
   if (lo < -hb || hi > rows + hb - 1) return KC_EINVAL;  // the window reaches rows the buffers do not hold
   int nw = 0;
-  KsFn fn = strip_pre_fn(nu1, zero_u != 0);
+  KsFn fn = strip_pre_fn(nu1, zero_u != 0, strip_sym(w9, omega));
   StreamParams p = strip_params(rows, nx, pitch, pitch_c, crows, gy0, mg, hb, 1, q_lo, q_hi, w9, omega, nu1 + 1,
                                 (const void*)fn, &nw);
   // the kernels index from the padded-array base: kc_idx(P, 0, 0) = P + KC_OX
@@ -2702,7 +2711,7 @@ extern "C" int kc_strip_post_window(const double* u, const double* f, double* uo
   if (!post_window_rows(rows, nu2, q_lo, q_hi, &lo, &hi, &clo, &chi)) return KC_OK;
   if (lo < -hb || hi > rows + hb - 1 || clo < -hbc || chi > crows + hbc - 1) return KC_EINVAL;
   int nw = 0;
-  KsFn fn = strip_post_fn(nu2, v_zero != 0);
+  KsFn fn = strip_post_fn(nu2, v_zero != 0, strip_sym(w9, omega));
   StreamParams p = strip_params(rows, nx, pitch, pitch_c, crows, gy0, mg, hb, hbc, q_lo, q_hi, w9, omega,
                                 nu2 > 0 ? nu2 : 1, (const void*)fn, &nw);
   const ptrdiff_t ob = (ptrdiff_t)pitch + KC_OX, obc = (ptrdiff_t)pitch_c + KC_OX;  // see kc_strip_pre

@@ -244,15 +244,23 @@ class ThreadComm:
 # ---------------------------------------------------------------------------
 
 class CudaStripOps:
-    """Row-strip kernels (kc_strip_*) on torch CUDA tensors of shape (rows, pitch)."""
+    """Row-strip kernels (kc_strip_*) on torch CUDA tensors of shape (rows, pitch),
+    from the exact (bit-identical to the reference) or the fast (FMA) build."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, arith: str | None = None):
         import torch
 
         from . import _native as N
         self.torch = torch
         self.N = N
+        self.arith = N.default_arith() if arith is None else arith
+        self.lib = N.lib_for(self.arith)
         self.device = torch.device("cuda", device)
+        self.launches = 0
+
+    def _chk(self, rc, kernels: int = 1):
+        self.N.check(rc, None, self.lib)  # the error text lives in the library that failed
+        self.launches += kernels  # kernels the call enqueued (bench gpu_launches)
 
     def zeros(self, rows, pitch):
         return self.torch.zeros((rows, pitch), dtype=self.torch.float64, device=self.device)
@@ -268,48 +276,46 @@ class CudaStripOps:
         return self.N.dptr(self._wbuf)
 
     def jacobi(self, u, f, o, ny, nx, w, omega, zero):
-        self.N.check(self.N.lib.kc_strip_jacobi(self._p(u, HALO), self._p(f, HALO), self._p(o, HALO), ny, nx,
+        self._chk(self.lib.kc_strip_jacobi(self._p(u, HALO), self._p(f, HALO), self._p(o, HALO), ny, nx,
                                                 u.shape[1], self._w(w), omega, int(zero), self._stream()))
 
     def resid_restrict(self, u, f, fc, ncy, ncx, w, zero):
-        self.N.check(self.N.lib.kc_strip_resid_restrict(self._p(u, HALO), self._p(f, HALO), self._p(fc, HALO),
+        self._chk(self.lib.kc_strip_resid_restrict(self._p(u, HALO), self._p(f, HALO), self._p(fc, HALO),
                                                         ncy, ncx, u.shape[1], fc.shape[1], self._w(w), int(zero),
                                                         self._stream()))
 
     def prolong_add(self, v, vc, ny, nx, zero):
-        self.N.check(self.N.lib.kc_strip_prolong_add(self._p(v, HALO), self._p(vc, HALO), ny, nx, v.shape[1],
+        self._chk(self.lib.kc_strip_prolong_add(self._p(v, HALO), self._p(vc, HALO), ny, nx, v.shape[1],
                                                      vc.shape[1], int(zero), self._stream()))
 
     # fused passes (kc_strip_pre / kc_strip_post): the single-GPU streaming kernels on the strip;
     # window = (q_lo, q_hi): only those coarse-row chunk positions (kc_strip_*_window), reading
     # no more than hb fine / hbc coarse halo rows
     def pre(self, u, f, uo, fc, ny, nx, crows, gy0, mg, w, omega, nu1, zero, window=None, hb=HALO):
-        N = self.N
         args = (self._p(u, HALO), self._p(f, HALO), self._p(uo, HALO), self._p(fc, HALO), ny, nx, u.shape[1],
                 fc.shape[1], crows, gy0, mg)
         if window is None:
-            N.check(N.lib.kc_strip_pre(*args, HALO, self._w(w), omega, nu1, int(zero), self._stream()))
+            self._chk(self.lib.kc_strip_pre(*args, HALO, self._w(w), omega, nu1, int(zero), self._stream()))
         else:
-            N.check(N.lib.kc_strip_pre_window(*args, hb, window[0], window[1], self._w(w), omega, nu1, int(zero),
-                                              self._stream()))
+            self._chk(self.lib.kc_strip_pre_window(*args, hb, window[0], window[1], self._w(w), omega, nu1,
+                                                   int(zero), self._stream()))
 
     def post(self, u, f, uo, vc, ny, nx, crows, gy0, mg, w, omega, nu2, zero, window=None, hb=HALO, hbc=HALO):
-        N = self.N
         args = (self._p(u, HALO), self._p(f, HALO), self._p(uo, HALO), self._p(vc, HALO), ny, nx, u.shape[1],
                 vc.shape[1], crows, gy0, mg)
         if window is None:
-            N.check(N.lib.kc_strip_post(*args, HALO, HALO, self._w(w), omega, nu2, int(zero), self._stream()))
+            self._chk(self.lib.kc_strip_post(*args, HALO, HALO, self._w(w), omega, nu2, int(zero), self._stream()))
         else:
-            N.check(N.lib.kc_strip_post_window(*args, hb, hbc, window[0], window[1], self._w(w), omega, nu2,
-                                               int(zero), self._stream()))
+            self._chk(self.lib.kc_strip_post_window(*args, hb, hbc, window[0], window[1], self._w(w), omega, nu2,
+                                                    int(zero), self._stream()))
 
     def norms(self, v, f, ny, nx, w, out=None):
         """(sum v^2, sum (f - A v)^2) over the strip into `out` (2 doubles; new tensor if None)."""
         if out is None:
             out = self.torch.zeros(2, dtype=self.torch.float64, device=self.device)
         if ny > 0:
-            self.N.check(self.N.lib.kc_strip_norms(self._p(v, HALO), self._p(f, HALO), ny, nx, v.shape[1],
-                                                   self._w(w), out.data_ptr(), self._stream()))
+            self._chk(self.lib.kc_strip_norms(self._p(v, HALO), self._p(f, HALO), ny, nx, v.shape[1],
+                                                   self._w(w), out.data_ptr(), self._stream()), 2)
         else:
             out.zero_()
         return out
@@ -319,32 +325,32 @@ class CudaStripOps:
         return self.torch.zeros(n, dtype=self.torch.float64, device=self.device)
 
     def apply_dot(self, p, ap, ny, nx, w, part, scal, slot):
-        self.N.check(self.N.lib.kc_strip_apply_dot(self._p(p, HALO), self._p(ap, HALO), ny, nx, p.shape[1], self._w(w),
-                                                   part.data_ptr(), scal.data_ptr(), slot, self._stream()))
+        self._chk(self.lib.kc_strip_apply_dot(self._p(p, HALO), self._p(ap, HALO), ny, nx, p.shape[1], self._w(w),
+                                                   part.data_ptr(), scal.data_ptr(), slot, self._stream()), 2)
 
     def dot(self, a, b, ny, nx, part, scal, slot):
-        self.N.check(self.N.lib.kc_strip_dot(self._p(a, HALO), self._p(b, HALO), ny, nx, a.shape[1], part.data_ptr(),
-                                             scal.data_ptr(), slot, self._stream()))
+        self._chk(self.lib.kc_strip_dot(self._p(a, HALO), self._p(b, HALO), ny, nx, a.shape[1], part.data_ptr(),
+                                             scal.data_ptr(), slot, self._stream()), 2)
 
     def pcg_update_xr(self, x, r, p, ap, ny, nx, measure_x, part, scal):
-        self.N.check(self.N.lib.kc_strip_pcg_update_xr(self._p(x, HALO), self._p(r, HALO), self._p(p, HALO),
+        self._chk(self.lib.kc_strip_pcg_update_xr(self._p(x, HALO), self._p(r, HALO), self._p(p, HALO),
                                                        self._p(ap, HALO), ny, nx, x.shape[1], int(measure_x),
-                                                       part.data_ptr(), scal.data_ptr(), self._stream()))
+                                                       part.data_ptr(), scal.data_ptr(), self._stream()), 2)
 
     def pcg_update_p(self, p, z, ny, nx, scal):
-        self.N.check(self.N.lib.kc_strip_pcg_update_p(self._p(p, HALO), self._p(z, HALO), ny, nx, p.shape[1],
+        self._chk(self.lib.kc_strip_pcg_update_p(self._p(p, HALO), self._p(z, HALO), ny, nx, p.shape[1],
                                                       scal.data_ptr(), self._stream()))
 
     def residual(self, x, f, r, ny, nx, w):
-        self.N.check(self.N.lib.kc_strip_residual(self._p(x, HALO), self._p(f, HALO), self._p(r, HALO), ny, nx,
+        self._chk(self.lib.kc_strip_residual(self._p(x, HALO), self._p(f, HALO), self._p(r, HALO), ny, nx,
                                                   x.shape[1], self._w(w), self._stream()))
 
     def copy_if(self, src, dst, ny, nx, scal):
-        self.N.check(self.N.lib.kc_strip_copy_if(self._p(src, HALO), self._p(dst, HALO), ny, nx, src.shape[1],
+        self._chk(self.lib.kc_strip_copy_if(self._p(src, HALO), self._p(dst, HALO), ny, nx, src.shape[1],
                                                  scal.data_ptr(), self._stream()))
 
     def dist_step(self, kind, scal, hist):
-        self.N.check(self.N.lib.kc_dist_step(kind, scal.data_ptr(), hist.data_ptr(), self._stream()))
+        self._chk(self.lib.kc_dist_step(kind, scal.data_ptr(), hist.data_ptr(), self._stream()))
 
 
 class CudaCoarse:
@@ -353,37 +359,45 @@ class CudaCoarse:
     engine follows torch's stream, so a distributed cycle can be captured
     into one CUDA graph)."""
 
-    def __init__(self, problem: ProblemSpec, n_levels: int, ops, smoother, nu1, nu2, device=0):
+    def __init__(self, problem: ProblemSpec, n_levels: int, ops, smoother, nu1, nu2, device=0, arith=None):
         from .cycle import CudaGridState
         spec = build_hierarchy(n_levels, Coarsening.FULL_STANDARD)
-        self.state = CudaGridState(spec, ops, smoother, nu1, nu2, device=device)
+        self.state = CudaGridState(spec, ops, smoother, nu1, nu2, device=device, arith=arith)
+        self.lib = self.state._lib
+        self.launches = 0
+        # kernels of one cycle per counter, counted now while the handle still
+        # has its own stream (kc_cycle_launches captures a graph on it)
+        self.levels = n_levels
+        self._per_cycle = {k: self.state.launches_per_cycle(k) for k in range(1, n_levels + 1)}
         self.m = spec.dims[0][0]
 
     def _bind_stream(self):
         import torch
 
         from . import _native as N
-        N.check(N.lib.kc_set_stream(self.state._h, torch.cuda.current_stream().cuda_stream), self.state._h)
+        N.check(self.lib.kc_set_stream(self.state._h, torch.cuda.current_stream().cuda_stream), self.state._h,
+                self.lib)
 
     def set_f(self, full):  # full: (m + 2*HALO, pitch) tensor with interior at (HALO, KC_OX)
         from . import _native as N
         self._bind_stream()
         ptr = full.data_ptr() + 8 * (HALO * full.shape[1] + KC_OX)
-        N.check(N.lib.kc_set_device_async(self.state._h, 1, N.KC_WHICH_F, ptr, self.m, self.m, full.shape[1]),
-                self.state._h)
+        N.check(self.lib.kc_set_device_async(self.state._h, 1, N.KC_WHICH_F, ptr, self.m, self.m, full.shape[1]),
+                self.state._h, self.lib)
 
     def zero_guess(self):
         self.state.zero_guess(1)
 
     def run(self, kappa):
         from . import _native as N
-        N.check(N.lib.kc_cycle_enqueue(self.state._h, int(kappa)), self.state._h)
+        N.check(self.lib.kc_cycle_enqueue(self.state._h, int(kappa)), self.state._h, self.lib)
+        self.launches += self._per_cycle[max(1, min(int(kappa), self.levels))]
 
     def get_v(self, full):
         from . import _native as N
         ptr = full.data_ptr() + 8 * (HALO * full.shape[1] + KC_OX)
-        N.check(N.lib.kc_get_device_async(self.state._h, 1, N.KC_WHICH_V, ptr, self.m, self.m, full.shape[1]),
-                self.state._h)
+        N.check(self.lib.kc_get_device_async(self.state._h, 1, N.KC_WHICH_V, ptr, self.m, self.m, full.shape[1]),
+                self.state._h, self.lib)
 
 
 # ---------------------------------------------------------------------------
@@ -410,7 +424,8 @@ class DistributedKappaSolver:
     """
 
     def __init__(self, problem: ProblemSpec, config: CycleConfig, comm, ops=None, make_coarse=None,
-                 min_rows: int = 64, device: int = 0, graphs: bool = True, overlap: bool | None = None):
+                 min_rows: int = 64, device: int = 0, graphs: bool = True, overlap: bool | None = None,
+                 arith: str | None = None):
         if config.coarsening is not Coarsening.FULL_STANDARD:
             raise ValueError("distributed cycles support full coarsening only")
         self.problem, self.config, self.comm = problem, config, comm
@@ -422,7 +437,7 @@ class DistributedKappaSolver:
         self.w = [s.w for s in self.stencils]
         self.omega = config.smoother.omega
         self.nu1, self.nu2 = config.nu1, config.nu2
-        self.ops = ops if ops is not None else CudaStripOps(device)
+        self.ops = ops if ops is not None else CudaStripOps(device, arith)
         self.strips = []
         for l in range(1, self.plan.n_dist + 1):
             a, b = self.plan.rows[l - 1][self.rank]
@@ -434,7 +449,7 @@ class DistributedKappaSolver:
         if make_coarse is None:
             def make_coarse(levels, ws):
                 return CudaCoarse(problem, levels, [self.stencils[nd + i] for i in range(levels)],
-                                  config.smoother, self.nu1, self.nu2, device)
+                                  config.smoother, self.nu1, self.nu2, device, getattr(self.ops, "arith", arith))
         self.coarse = make_coarse(self.nc, self.w[nd:])
         self.cfull = self.ops.zeros(mc + 2 * HALO, kc_pitch(mc))   # replicated level n_dist+1 (f, then v)
         self.vfull = self.ops.zeros(mc + 2 * HALO, kc_pitch(mc))
@@ -445,6 +460,8 @@ class DistributedKappaSolver:
                            and isinstance(self.coarse, CudaCoarse))
         self._graphs = {}
         self._warm = set()
+        self._key_launches = {}  # kernels one call of a graphed body enqueues
+        self._replayed = 0       # kernels launched by graph replays
         self.graph_fallback = None
         if self._graphs_ok:
             import torch
@@ -679,9 +696,21 @@ class DistributedKappaSolver:
                 g = self._capture(key, fn)
             if g is not None:
                 g.replay()
+                self._replayed += self._key_launches.get(key, 0)
                 return
+        before = self._enqueued()
         fn()
+        self._key_launches[key] = self._enqueued() - before
         self._warm.add(key)
+
+    def _enqueued(self) -> int:
+        return getattr(self.ops, "launches", 0) + getattr(self.coarse, "launches", 0)
+
+    def kernels_launched(self) -> int:
+        """Kernels this rank has launched so far: eager calls (counted by the
+        strip ops and the coarse engine) plus graph replays (each replay counts
+        the kernels its body enqueued when it ran eagerly); bench gpu_launches."""
+        return self._replayed + self._enqueued()
 
     def _capture(self, key, fn):
         """Capture fn() into a CUDA graph; None (eager from then on, with a
@@ -690,6 +719,7 @@ class DistributedKappaSolver:
         or cannot be captured."""
         import torch
         state0 = self._host_state()
+        counts0 = (getattr(self.ops, "launches", 0), getattr(self.coarse, "launches", 0))
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         why = None
@@ -701,6 +731,11 @@ class DistributedKappaSolver:
         else:
             if self._host_state() != state0:
                 why = "the captured work does not return the strips to their buffer parity"
+        # the capture enqueued nothing: undo what the host walk counted
+        if hasattr(self.ops, "launches"):
+            self.ops.launches = counts0[0]
+        if hasattr(self.coarse, "launches"):
+            self.coarse.launches = counts0[1]
         if why is not None:
             for st, (cur, vz) in zip(self.strips, state0):
                 st.cur, st.vzero = cur, vz
@@ -828,6 +863,7 @@ class DistributedKappaSolver:
 
         stats = CycleStats.for_levels(self.n)
         t0 = time.perf_counter()
+        k0 = self.kernels_launched()
         norms_step()  # cycle 0: the initial norms and target (cycle.py:333-341)
         done = self._read_scalars(scal)[DS["DONE"]] != 0.0
         while not done:
@@ -846,7 +882,7 @@ class DistributedKappaSolver:
                 self._stats_cache[k] = st
             stats.absorb(self._stats_cache[k], it)
         return {"status": status, "iterations": it, "err_hist": h[:, 0].tolist(), "res_hist": h[:, 1].tolist(),
-                "stats": stats, "wall_ms": wall_ms}
+                "stats": stats, "wall_ms": wall_ms, "gpu_launches": self.kernels_launched() - k0}
 
     def pcg_solve(self, f, x0=None, target_reduction=1e8, max_iterations=10000, stop="residual", batch: int = 4,
                   kappa=None, resident: bool = False, gather: bool = True):

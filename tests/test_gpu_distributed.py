@@ -65,18 +65,24 @@ def test_cuda_strips_pcg_vs_reference(world, n, kname, stop, tgt, key):
         check_pcg_hist(rep["hist"], g["x_hist" if stop == "error" else "r_hist"])
 
 
+@pytest.mark.parametrize("arith", ["exact", "fast"])
 @pytest.mark.parametrize("world,kname", [(2, "2"), (3, "3")])
-def test_cuda_strips_device_stop_standalone_vs_reference(world, kname):
+def test_cuda_strips_device_stop_standalone_vs_reference(world, kname, arith):
+    """Both builds of the strip kernels and the agglomerated engine (the FMA
+    build at the north star's bar: same counts, histories within 1e-10)."""
     n = 9
     g = load_json("solves_small.json")["standalone"][f"n{n}_k{kname}"]
     kappa = int(kname)
 
     def fn(comm):
-        s = DistributedKappaSolver(ProblemSpec(1e-4, 45.0, seed=0), CycleConfig(n=n, kappa=kappa), comm, min_rows=16)
+        s = DistributedKappaSolver(ProblemSpec(1e-4, 45.0, seed=0), CycleConfig(n=n, kappa=kappa), comm, min_rows=16,
+                                   arith=arith)
+        assert s.ops.arith == arith and s.coarse.state.arith == arith
         return s.solve_standalone(1e10, max_cycles=2000, stop="residual", batch=6)
 
     for rep in _threads(world, fn):
         assert rep["status"] == "converged" and rep["iterations"] == g["iters_residual_1e10"]
+        assert rep["gpu_launches"] > rep["iterations"]
         rr = np.asarray(g["res_hist"][: len(rep["res_hist"])])
         assert np.max(np.abs(np.asarray(rep["res_hist"]) - rr) / rr) < 1e-10
 
@@ -107,9 +113,12 @@ def test_nccl_world1_graph_batched_pcg_and_solve():
             assert rep["status"] == "converged" and rep["iterations"] == gp["iters"]["residual_1e10"]
             check_pcg_hist(rep["hist"], gp["r_hist"])
         gs = load_json("solves_small.json")["standalone"][f"n{n}_k2"]
-        for _ in range(2):
+        counts = []
+        for _ in range(3):  # eager, captured, replayed: the same kernels each time
             sol = s.solve_standalone(1e10, max_cycles=2000, stop="residual", batch=8)
             assert sol["status"] == "converged" and sol["iterations"] == gs["iters_residual_1e10"]
+            counts.append(sol["gpu_launches"])
+        assert counts[0] == counts[1] == counts[2] and counts[0] > sol["iterations"], counts
         assert s.graph_fallback is None, s.graph_fallback
         assert any(k[0] == "pcg" for k in s._graphs) and any(k[0] == "solve" for k in s._graphs)
     finally:
