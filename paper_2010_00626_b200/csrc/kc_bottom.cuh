@@ -94,6 +94,7 @@ struct BotParams {
   int nstrip;        // leading levels split into row strips over the cluster (0: single CTA)
   int total;         // shared-memory doubles of all levels (bot_smem_doubles)
   int deep;          // the deep-halo strip level (PH_FRAME63), or -1
+  int deep0;         // the entry level has deep halos too and launches run as PH_FRAME127
   BotLv lv[KC_BOT_MAXLEV];  // bot_geometry (rank 0's strip rows)
   // side-15 frame operators (KC_FAST cluster launches; see "Frame operators"
   // below): blocks (kap - 1) * 2 + part of [A_kap | B_kap], 225 x KC_MV_LD
@@ -136,18 +137,21 @@ __host__ __device__ __forceinline__ int bot_rows(int m0, int d, int nstrip, int 
 // halo rows each side of level d: KC_DEEP_HB on the deep-halo strip level
 // (PH_FRAME63 computes its stages on the halo rows redundantly), else 1
 #define KC_DEEP_HB 4
-__host__ __device__ __forceinline__ int bot_hb(int d, int deep) { return d == deep ? KC_DEEP_HB : 1; }
-__host__ __device__ __forceinline__ int bot_off(int m0, int d, int nstrip = 0, int cs = 1, int deep = -1) {
+__host__ __device__ __forceinline__ int bot_hb(int d, int deep, int deep0 = 0) {
+  return (d == deep || (deep0 && d == 0)) ? KC_DEEP_HB : 1;
+}
+__host__ __device__ __forceinline__ int bot_off(int m0, int d, int nstrip = 0, int cs = 1, int deep = -1,
+                                                int deep0 = 0) {
   int off = 0;
   for (int j = 0; j < d; ++j) {
     const int s = bot_m(m0, j) + 2;
-    off += 3 * (bot_rows(m0, j, nstrip, cs) + 2 * bot_hb(j, deep)) * s;
+    off += 3 * (bot_rows(m0, j, nstrip, cs) + 2 * bot_hb(j, deep, deep0)) * s;
   }
   return off;
 }
 __host__ __device__ __forceinline__ int bot_smem_doubles(int m0, int nlev, int nstrip = 0, int cs = 1,
-                                                         int deep = -1) {
-  return bot_off(m0, nlev, nstrip, cs, deep);
+                                                         int deep = -1, int deep0 = 0) {
+  return bot_off(m0, nlev, nstrip, cs, deep, deep0);
 }
 __host__ __device__ __forceinline__ int bot_warps(int m) {
   return m >= 31 ? KC_BOT_WARPS : (m >= 15 ? 8 : 1);  // 2 warps at m = 7 measured slower
@@ -157,11 +161,11 @@ __host__ __device__ __forceinline__ int bot_warps(int m) {
 // what the kernel used to derive with integer divisions in its prologue.
 inline void bot_geometry(BotParams& bp, int m0, int cs) {
   const int nlev = bp.nlev, nstrip = bp.nstrip;
-  bp.total = bot_smem_doubles(m0, nlev, nstrip, cs, bp.deep);
+  bp.total = bot_smem_doubles(m0, nlev, nstrip, cs, bp.deep, bp.deep0);
   for (int d = 0; d < nlev; ++d) {
     const bool strip = d < nstrip;
-    const int hb = bot_hb(d, bp.deep);
-    const int m = bot_m(m0, d), S = m + 2, base = bot_off(m0, d, nstrip, cs, bp.deep);
+    const int hb = bot_hb(d, bp.deep, bp.deep0);
+    const int m = bot_m(m0, d), S = m + 2, base = bot_off(m0, d, nstrip, cs, bp.deep, bp.deep0);
     const int R = bot_rows(m0, d, nstrip, cs);
     const int mc = d + 1 < nlev ? bot_m(m0, d + 1) : 1;
     BotLv L{};
@@ -258,7 +262,8 @@ __device__ __forceinline__ void kc_bot_mark(int k) {
 enum BotOp {
   PH_JACOBI = 0, PH_RESID = 1, PH_RESTRICT = 2, PH_PROLONG = 3, PH_JOIN = 4, PH_J2Z = 5, PH_TINY = 8, PH_CSYNC = 9,
   PH_FRAME31 = 10,  // a whole kappa_cycle frame on the replicated side-31 level (BotFrame31)
-  PH_FRAME63 = 11   // the pair of calls (kappa, kappa - 1) on the deep-halo side-63 strips (BotFrame63)
+  PH_FRAME63 = 11,  // the pair of calls (kappa, kappa - 1) on the deep-halo side-63 strips (BotDeep)
+  PH_FRAME127 = 12  // the whole launch: the 127^2 pair from a zero guess, deep halos on 127^2 and 63^2 (BotDeep)
 };
 #ifndef KC_BOT_TINY_M
 #define KC_BOT_TINY_M 15  // frames on sides <= this run as PH_TINY (side 15 on 8 warps)
@@ -337,6 +342,21 @@ struct BotBuilder {  // host side
   }
   bool frame31 = true;      // whole side-31 frames as PH_FRAME31 (replicated levels)
   int deep = -1;            // the deep-halo strip level: its call pairs as PH_FRAME63
+  bool deep0 = false;       // deep halos on the entry level too: a zero-guess pair as PH_FRAME127
+  // the launch's calls on the entry level: (k1) and, if k2 > 0, (k2)
+  void top(int k1, int k2) {
+    if (deep0 && !dry && (vz & 1u) && (k2 == k1 - 1 || (k1 == 1 && k2 == 0))) {
+      // one descriptor for the whole launch; the dry replay follows BotDeep
+      emit(PH_FRAME127, 0, cur & 1u, 1, 0, 0, k1);
+      dry = true;
+      rec(0, k1);
+      if (k2 > 0) rec(0, k2);
+      dry = false;
+      return;
+    }
+    rec(0, k1);
+    if (k2 > 0) rec(0, k2);
+  }
   void rec(int d, int kap) {
     if (frame31 && fuse && !dry && d >= nstrip && bot_m(m0, d) == 31 && d + 5 == nlev && kap <= 15) {
       // one descriptor for the frame and everything below it; the dry replay
@@ -820,8 +840,13 @@ __device__ __forceinline__ void bot_mv_frame(double* sm, const BotParams& bp, co
   const int R = bp.mv_rows;
   asm volatile("cp.async.wait_all;" ::: "memory");  // the blocks (prologue copies)
   bot_bar();
-  const double* B = sm + bp.mv_off + bp.mv_slot[(kap - 1) * 2 + 1] * R * KC_MV_LD;
-  const double* A = sm + bp.mv_off + bp.mv_slot[(kap - 1) * 2] * R * KC_MV_LD;
+  // this CTA's row slice of the blocks: in shared memory (resident), else
+  // straight from global memory (2.4 MB for all six blocks: L2-resident)
+  const int bb = (kap - 1) * 2 + 1, ba = (kap - 1) * 2, i0 = rank * R;
+  const double* B = bp.mv_slot[bb] >= 0 ? sm + bp.mv_off + bp.mv_slot[bb] * R * KC_MV_LD
+                                        : bp.mv_mats + ((size_t)bb * KC_MV_N + i0) * KC_MV_LD;
+  const double* A = bp.mv_slot[ba] >= 0 ? sm + bp.mv_off + bp.mv_slot[ba] * R * KC_MV_LD
+                                        : bp.mv_mats + ((size_t)ba * KC_MV_N + i0) * KC_MV_LD;
   const double* vin = sm + (src ? L.vo1 : L.vo0);  // this CTA's replica
   const double* fin = sm + L.fo;
   double* xv = sm + bp.mv_xin;  // inputs packed row-major: v (225), f (225)
@@ -834,7 +859,6 @@ __device__ __forceinline__ void bot_mv_frame(double* sm, const BotParams& bp, co
   bot_bar();
   double* out = sm + (ob ? L.vo1 : L.vo0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int i0 = rank * R;
   for (int r = warp; r < R && i0 + r < KC_MV_N; r += KC_BOT_WARPS) {
     const double* br = B + r * KC_MV_LD;
     const double* ar = A + r * KC_MV_LD;
@@ -1011,8 +1035,19 @@ struct BotFrame31 {
 // the boundary rows.  Rows outside the domain are never written (they stay
 // the zero Dirichlet ghosts).  Same per-point arithmetic and buffer rules as
 // BotBuilder::rec_plain (nu1 = nu2 = 2): bit-identical to the strip phases.
-struct BotFrame63 {
-  static constexpr int M = 63, S = M + 2, R = 4, MC = 31, SC = MC + 2;
+//
+// PH_FRAME127 (a whole launch from a zero guess on the 127^2 entry level):
+// the same scheme one level up -- 127^2 strips of R = 8 rows with deep halos
+// too (the entry load brings 4 halo rows of f), its pair of calls around the
+// 63^2 pairs.  Its restriction writes the child's strip rows AND pushes them
+// into both neighbours' deep halos (4 rows = a whole 63^2 strip), so the
+// 63^2 calls start without an exchange; the last 63^2 call of each pair
+// pushes 2 boundary rows (the 127^2 prolongation of rows -2..R+1 reads child
+// rows -2..R/2), and the 127^2 post pass keeps only its own rows valid (the
+// next call exchanges depth 4, the last one is written back).  Cluster
+// barriers per 127^2 call: 1 (zero guess) or 3, against 6-7 strip phases.
+struct BotDeep {
+  static constexpr int HB = KC_DEEP_HB;
   double* sm;
   const BotLv* lv;
   const St9* tab;
@@ -1020,7 +1055,7 @@ struct BotFrame63 {
   int tid, rank, cs;
   __device__ __forceinline__ double* buf(const BotLv& L, int b) const { return sm + (b ? L.vo1 : L.vo0); }
   // items (y, x) of rows lo..hi clipped to the domain (local row y = global a + y)
-  template <class Fn>
+  template <int M, class Fn>
   __device__ __forceinline__ void rows_do(int a, int lo, int hi, Fn fn) const {
     lo = max(lo, -a);
     hi = min(hi, M - 1 - a);
@@ -1030,21 +1065,27 @@ struct BotFrame63 {
       fn(lo + yy, i - yy * M);
     }
   }
+  // own rows ylo..yhi into the neighbours' halo rows: rows y < HB to the
+  // upper one (its row R + y), rows y >= R - HB to the lower one (row y - R)
+  template <int M>
   __device__ __forceinline__ void push_rows(double* u, int a, int ylo, int yhi) const {
-    // own rows ylo..yhi into both neighbours' halo rows (row y -> up R + y, down y - R)
+    constexpr int R = (M + 1) / 16, S = M + 2;
     cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
     double* up = rank > 0 ? cl.map_shared_rank(u, rank - 1) + R * S : nullptr;
     double* dn = rank + 1 < cs ? cl.map_shared_rank(u, rank + 1) - R * S : nullptr;
-    rows_do(a, ylo, yhi, [&](int y, int x) {
+    rows_do<M>(a, ylo, yhi, [&](int y, int x) {
       const double v = u[y * S + x];
-      if (up) up[y * S + x] = v;
-      if (dn) dn[y * S + x] = v;
+      if (up && y < HB) up[y * S + x] = v;
+      if (dn && y >= R - HB) dn[y * S + x] = v;
     });
   }
   // the pre half of a call: sweeps (J2Z on a zero guess), residual,
-  // restriction broadcast into the child's replicas; returns the rows on
-  // which v after the sweeps is valid (lo = -hi + R - 1)
+  // restriction -- broadcast into the child's replicas (M = 63) or into the
+  // child's strips with their deep halos (M = 127); returns the first row on
+  // which v after the sweeps is valid (the last is R - 1 - lo)
+  template <int M>
   __device__ __forceinline__ int pre(int d, int cur, bool zero) {
+    constexpr int R = (M + 1) / 16, S = M + 2, MC = (M - 1) / 2, SC = MC + 2;
     const BotLv L = lv[d];
     const St9 st = tab[d];
     const int a = rank * R;
@@ -1053,7 +1094,7 @@ struct BotFrame63 {
     double* w = buf(L, cur ^ 1);
     int lo;
     if (zero) {
-      rows_do(a, -3, R + 2, [&](int y, int x) { u[y * S + x] = bot_j2z_pt(f + y * S + x, S, st); });
+      rows_do<M>(a, -3, R + 2, [&](int y, int x) { u[y * S + x] = bot_j2z_pt(f + y * S + x, S, st); });
       bot_bar();
       lo = -3;
     } else {
@@ -1061,46 +1102,65 @@ struct BotFrame63 {
       // after a barrier: a neighbour may still be using those rows for the
       // previous call's prolongation and sweeps
       clu_sync();
-      push_rows(u, a, 0, R - 1);
+      push_rows<M>(u, a, 0, R - 1);
       clu_sync();
-      rows_do(a, -3, R + 2, [&](int y, int x) {
+      rows_do<M>(a, -3, R + 2, [&](int y, int x) {
         const int i = y * S + x;
         w[i] = kc_jacobi_pt(u[i], f[i], kc_apply9(u + i, S, st), st.c);
       });
       bot_bar();
-      rows_do(a, -2, R + 1, [&](int y, int x) {
+      rows_do<M>(a, -2, R + 1, [&](int y, int x) {
         const int i = y * S + x;
         u[i] = kc_jacobi_pt(w[i], f[i], kc_apply9(w + i, S, st), st.c);
       });
       bot_bar();
       lo = -2;
     }
-    // residual into the other buffer, restriction of the own coarse rows into
-    // every CTA's replica of the child level
-    rows_do(a, -1, R, [&](int y, int x) {
+    // residual into the other buffer, restriction of the own coarse rows
+    rows_do<M>(a, -1, R, [&](int y, int x) {
       const int i = y * S + x;
       w[i] = DSUB(f[i], kc_apply9(u + i, S, st));
     });
     bot_bar();
     {
       cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
-      double* fc = sm + lv[d + 1].fo + (a / 2) * SC;  // this strip's first coarse row
       const int n = L.crows * MC;
-      for (int i = tid; i < n; i += KC_BOT_THREADS) {
-        const int q = i / MC, p = i - q * MC;
-        const double* rc = w + (2 * q + 1) * S + (2 * p + 1);
-        const double* rs = rc - S;
-        const double* rn = rc + S;
-        const double fv = kc_fw(rs[-1], rs[0], rs[1], rc[-1], rc[0], rc[1], rn[-1], rn[0], rn[1]);
-        for (int k = 0; k < cs; ++k) *cl.map_shared_rank(fc + q * SC + p, k) = fv;
+      double* fc0 = sm + lv[d + 1].fo;
+      if (M == 127) {  // the child's strip (row 0 = coarse row a / 2) and its neighbours' deep halos
+        constexpr int RC = R / 2;
+        double* up = rank > 0 ? cl.map_shared_rank(fc0, rank - 1) + RC * SC : nullptr;
+        double* dn = rank + 1 < cs ? cl.map_shared_rank(fc0, rank + 1) - RC * SC : nullptr;
+        for (int i = tid; i < n; i += KC_BOT_THREADS) {
+          const int q = i / MC, p = i - q * MC;
+          const double* rc = w + (2 * q + 1) * S + (2 * p + 1);
+          const double* rs = rc - S;
+          const double* rn = rc + S;
+          const double fv = kc_fw(rs[-1], rs[0], rs[1], rc[-1], rc[0], rc[1], rn[-1], rn[0], rn[1]);
+          fc0[q * SC + p] = fv;
+          if (up && q < HB) up[q * SC + p] = fv;
+          if (dn && q >= RC - HB) dn[q * SC + p] = fv;
+        }
+      } else {  // every CTA's replica of the child, at this strip's first coarse row
+        double* fc = fc0 + (a / 2) * SC;
+        for (int i = tid; i < n; i += KC_BOT_THREADS) {
+          const int q = i / MC, p = i - q * MC;
+          const double* rc = w + (2 * q + 1) * S + (2 * p + 1);
+          const double* rs = rc - S;
+          const double* rn = rc + S;
+          const double fv = kc_fw(rs[-1], rs[0], rs[1], rc[-1], rc[0], rc[1], rn[-1], rn[0], rn[1]);
+          for (int k = 0; k < cs; ++k) *cl.map_shared_rank(fc + q * SC + p, k) = fv;
+        }
       }
     }
     clu_sync();
     return lo;
   }
-  // the post half: prolongation from the child's local replica (buffer c),
-  // two sweeps; the continuing call then exchanges its boundary rows
-  __device__ __forceinline__ void post(int d, int cur, int c, int lo, bool zero) {
+  // the post half of a 63^2 call: prolongation from the child's local
+  // replica (buffer c), two sweeps; then np boundary rows to the neighbours
+  // (1: the continuing call under a 127^2 interpreter parent, which reads one
+  // halo row; 2: the last call of a pair under PH_FRAME127)
+  __device__ __forceinline__ void post63(int d, int cur, int c, int lo, int np) {
+    constexpr int M = 63, R = 4, S = M + 2, SC = 31 + 2;
     const BotLv L = lv[d];
     const St9 st = tab[d];
     const int a = rank * R, hi = R - 1 - lo;
@@ -1110,37 +1170,79 @@ struct BotFrame63 {
     {
       const double* vc = buf(lv[d + 1], c);
       auto cp = [&](int q, int pc) { return vc[q * SC + pc]; };
-      rows_do(a, lo, hi, [&](int y, int x) {
+      rows_do<M>(a, lo, hi, [&](int y, int x) {
         const int i = y * S + x;
         u[i] = DADD(u[i], kc_prolong_val(a + y, x, cp));
       });
     }
     bot_bar();
-    rows_do(a, lo + 1, hi - 1, [&](int y, int x) {
+    rows_do<M>(a, lo + 1, hi - 1, [&](int y, int x) {
       const int i = y * S + x;
       w[i] = kc_jacobi_pt(u[i], f[i], kc_apply9(u + i, S, st), st.c);
     });
     bot_bar();
-    rows_do(a, lo + 2, hi - 2, [&](int y, int x) {
+    rows_do<M>(a, lo + 2, hi - 2, [&](int y, int x) {
       const int i = y * S + x;
       u[i] = kc_jacobi_pt(w[i], f[i], kc_apply9(w + i, S, st), st.c);
     });
     bot_bar();
-    if (!zero) {  // the parent's prolongation reads one halo row each side
-      clu_sync();   // (the neighbours' post sweeps read their halo rows)
-      push_rows(u, a, 0, 0);
-      push_rows(u, a, R - 1, R - 1);
+    if (np > 0) {  // after a barrier: the neighbours' post sweeps read their halo rows
+      clu_sync();
+      push_rows<M>(u, a, 0, np - 1);
+      push_rows<M>(u, a, R - np, R - 1);
       clu_sync();
     }
   }
-  // both calls; one inlined site of each half and of the child frame
-  __device__ __forceinline__ void pair(int d, int kap, int cur) {
-    for (int i = 0; i < (kap > 1 ? 2 : 1); ++i) {
-      const bool zero = i == 0;
-      const int lo = pre(d, cur, zero);
-      int c = 0, z = 1;  // the child's zero guess (cycle.py:214)
-      for (int j = 0; j < (kap - i > 1 ? 2 : 1); ++j) f31->frame(d + 1, kap - i - j, c, z);
-      post(d, cur, c, lo, zero);
+  // the post half of a 127^2 call under PH_FRAME127: prolongation from the
+  // child's strip (buffer c, local row 0 = coarse row a / 2) on rows
+  // -2..R+1, sweeps on -1..R and 0..R-1 (own rows only: see above)
+  __device__ __forceinline__ void post127(int cur, int c) {
+    constexpr int M = 127, R = 8, S = M + 2, SC = 63 + 2;
+    const BotLv L = lv[0];
+    const St9 st = tab[0];
+    const int a = rank * R;
+    const double* f = sm + L.fo;
+    double* u = buf(L, cur);
+    double* w = buf(L, cur ^ 1);
+    {
+      const double* vc = buf(lv[1], c) - (a / 2) * SC;  // indexed by the global coarse row
+      auto cp = [&](int q, int pc) { return vc[q * SC + pc]; };
+      rows_do<M>(a, -2, R + 1, [&](int y, int x) {
+        const int i = y * S + x;
+        u[i] = DADD(u[i], kc_prolong_val(a + y, x, cp));
+      });
+    }
+    bot_bar();
+    rows_do<M>(a, -1, R, [&](int y, int x) {
+      const int i = y * S + x;
+      w[i] = kc_jacobi_pt(u[i], f[i], kc_apply9(u + i, S, st), st.c);
+    });
+    bot_bar();
+    rows_do<M>(a, 0, R - 1, [&](int y, int x) {
+      const int i = y * S + x;
+      u[i] = kc_jacobi_pt(w[i], f[i], kc_apply9(w + i, S, st), st.c);
+    });
+    bot_bar();
+  }
+  // PH_FRAME63 (top = false: the pair on level d63, v in buffer cur) or
+  // PH_FRAME127 (top: the 127^2 pair from a zero guess, v in buffer cur, the
+  // 63^2 level's v in buffer 0 as BotBuilder::rec_plain leaves it); one
+  // inlined site of each half and of the child frame
+  __device__ __forceinline__ void run(bool top, int d63, int kap, int cur) {
+    const int ni = top ? (kap > 1 ? 2 : 1) : 1;
+    for (int i = 0; i < ni; ++i) {
+      if (top) pre<127>(0, cur, i == 0);
+      const int k1 = top ? kap - i : kap;
+      const int cur63 = top ? 0 : cur;
+      const int nj = k1 > 1 ? 2 : 1;
+      for (int j = 0; j < nj; ++j) {
+        const bool zero = j == 0;
+        const int lo = pre<63>(d63, cur63, zero);
+        int c = 0, z = 1;  // the child's zero guess (cycle.py:214)
+        for (int jj = 0; jj < (k1 - j > 1 ? 2 : 1); ++jj) f31->frame(d63 + 1, k1 - j - jj, c, z);
+        post63(d63, cur63, c, lo, top ? (j == nj - 1 ? 2 : 0) : (zero ? 0 : 1));
+      }
+      if (top) post127(cur, cur63);
     }
   }
 };
@@ -1153,9 +1255,9 @@ __device__ __forceinline__ void bot_run_frame(int op, double* sm, const BotLv* l
                                            int d, int kap, int src, int zero, int rank, int cs, int nlev, int* slot,
                                            int* tiny_child, int* mvs) {
   BotFrame31 fr{sm, lv, tab, bp, (int)threadIdx.x, rank, cs, nlev, slot, tiny_child, mvs[0], mvs[1] != 0};
-  if (op == PH_FRAME63) {
-    BotFrame63 f63{sm, lv, tab, &fr, (int)threadIdx.x, rank, cs};
-    f63.pair(d, kap, src);
+  if (op == PH_FRAME63 || op == PH_FRAME127) {
+    BotDeep dp{sm, lv, tab, &fr, (int)threadIdx.x, rank, cs};
+    dp.run(op == PH_FRAME127, op == PH_FRAME127 ? 1 : d, kap, src);
   } else {
     int cur = src, vz = zero;
     fr.frame(d, kap, cur, vz);
@@ -1254,13 +1356,14 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
   if (nstrip > 0) {
-    // strip entry: own rows plus one halo row each side (rows -1 .. m0
-    // exist in HBM, ghost rows zero), ghost columns included; level 0 is
-    // the first block: v0 rows at [0, (R+2) S), f rows at [2 (R+2) S, ...)
-    const int S = bp.lv[0].S, R = bp.lv[0].R, a = rank * R;
-    const int y0 = a - 1, y1 = min(a + R, m0);
-    const int w0 = (y0 - a + 1) * S, w1 = (y1 - a + 2) * S;  // loaded storage rows, as an offset range
-    const int fbase = 2 * (R + 2) * S;
+    // strip entry: own rows plus hb halo rows each side (1, or 4 with deep
+    // halos on the entry level), within the rows -1 .. m0 that exist in
+    // HBM (ghost rows zero), ghost columns included; level 0 is the first
+    // block: v0 rows at [0, (R+2hb) S), f rows at [2 (R+2hb) S, ...)
+    const int S = bp.lv[0].S, R = bp.lv[0].R, hb = bp.lv[0].hb, a = rank * R;
+    const int y0 = max(a - hb, -1), y1 = min(a + R + hb - 1, m0);
+    const int w0 = (y0 - a + hb) * S, w1 = (y1 - a + hb + 1) * S;  // loaded storage rows, as an offset range
+    const int fbase = 2 * (R + 2 * hb) * S;
     if (bp.v_zero) zero(0, fbase + w0);
     else {
       zero(0, w0);
@@ -1276,7 +1379,7 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
     for (int y = y0 + wid; y <= y1; y += KC_BOT_WARPS) {
       const double* gfr = bp.gf + kc_idx(bp.gP, y, -1);
       const double* gvr = bp.gv + kc_idx(bp.gP, y, -1);
-      const int o = (y - a + 1) * S;
+      const int o = (y - a + hb) * S;
       for (int c = lane; c < S; c += 32) {
         cp8(sm + fbase + o + c, gfr + c);
         if (!bp.v_zero) cp8(sm + o + c, gvr + c);
@@ -1408,7 +1511,7 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
       if (strip)  // from this CTA's replica of the child, at this strip's first coarse row
         vc += (L.a / 2) * C.S;
       bot_prolong(u, vc, L, C.m, C.S, zero, tid, nth, bot_push(u, L, strip, rank, cs));
-    } else if (op == PH_FRAME63 || op == PH_FRAME31) {  // every thread of every CTA
+    } else if (op == PH_FRAME63 || op == PH_FRAME31 || op == PH_FRAME127) {  // every thread of every CTA
       int mvs[2] = {mv_last, mv_sync ? 1 : 0};
       bot_run_frame(op, sm, lv, tab, &bp, d, BD_KAP(e), src, zero, rank, cs, nlev, &f31_slot, tiny_child, mvs);
       mv_last = mvs[0];

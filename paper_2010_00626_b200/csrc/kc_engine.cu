@@ -140,6 +140,7 @@ struct kc_handle {
   int bot_cs = 1;  // CTAs per bottom launch (thread-block cluster when > 1)
   double* mv_mats = nullptr;  // side-15 frame operators (FMA build, kc_bottom.cuh)
   int mv_resident = 0;        // blocks resident in the bottom kernel's shared memory
+  int mv_avail = 0;           // blocks computed (frames with non-resident blocks read them from L2)
   double line_w[3] = {0, 0, 0};  // semi-y coarsest line: lower, diag, upper (raw w[1][:])
   bool line_singular = false;
   // host-built bottom phase schedules, keyed by (kappa1, kappa2, v_zero)
@@ -612,12 +613,10 @@ int get_bot_sched(kc_handle* h, int k1, int k2, int vzero, const unsigned** dev,
     b.nu2 = h->nu2;
     b.vz = vzero ? 1u : 0u;
     b.nstrip = h->bot_base.nstrip;
-    b.mv_mask = (unsigned)h->mv_resident;
+    b.mv_mask = (unsigned)h->mv_avail;
     b.deep = h->bot_base.deep;
-    if (b.nlev > 1) {
-      b.rec(0, k1);
-      if (k2 > 0) b.rec(0, k2);
-    }
+    b.deep0 = h->bot_base.deep0 != 0;
+    if (b.nlev > 1) b.top(k1, k2);
     if ((int)b.out.size() > KC_BOT_MAXPH)
       KC_FAIL(h, KC_EINVAL, "bottom schedule of %zu phases exceeds %d", b.out.size(), KC_BOT_MAXPH);
     unsigned* d = nullptr;
@@ -676,6 +675,7 @@ int setup_frame_operators(kc_handle* h, const cudaDeviceProp& prop) {
   const size_t per = sizeof(double) * (size_t)R * KC_MV_LD;
   const int order[6] = {1, 3, 0, 5, 2, 4};
   int mask = 0, nres = 0;
+  for (int b = 0; b < 6; ++b) bp.mv_slot[b] = -1;  // not resident: bot_mv_frame reads it from global (L2)
   for (int b : order) {
     if (sizeof(double) * (size_t)(off + 2 * KC_MV_N) + per * (size_t)(nres + 1) > smem_max) break;
     mask |= 1 << b;
@@ -706,6 +706,7 @@ int setup_frame_operators(kc_handle* h, const cudaDeviceProp& prop) {
     return KC_OK;  // keep the interpreter frames
   }
   h->mv_resident = mask;
+  h->mv_avail = 0x3F;
   h->bot_smem = bytes;
   return KC_OK;
 }
@@ -718,6 +719,7 @@ int ex_bottom(kc_handle* h, int l, int k1, int k2) {
   bp.gP = L.P;
   bp.v_zero = L.vzero ? 1 : 0;
   int rc = get_bot_sched(h, k1, k2, bp.v_zero, &bp.sched, &bp.nsched, &bp.final_cur, &bp.mv_copy);
+  bp.mv_copy &= h->mv_resident;  // the prologue copies the resident blocks the schedule uses
   if (rc) return rc;
   if (h->L[h->n - 1].st.center == 0.0) KC_FAIL(h, KC_ESINGULAR, "singular coarsest operator");
   if (h->bot_cs > 1) {
@@ -1627,7 +1629,7 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
   // at side <= 255 with the sides >= 31 in row strips, else one CTA
   // entering at side <= 63 (kc_bottom.cuh); KC_BOT_CLUSTER=0 forces one CTA.
   // Only the Jacobi / full-coarsening path has fused kernels.
-  int lb = -1, cs = 1, nstrip = 0, deep = -1;
+  int lb = -1, cs = 1, nstrip = 0, deep = -1, deep0 = 0;
   size_t smem = 0;
   if (smoother_kind == KC_SMOOTH_JACOBI && coarsening == KC_COARSEN_FULL) {
     cudaFuncAttributes fa{};
@@ -1645,6 +1647,10 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
     const int cs_first = csenv && atoi(csenv) == 8 ? 8 : 16;
     const char* denv = getenv("KC_DEEP");
     const bool use_deep = !(denv && denv[0] == '0');
+    // deep halos on the 127^2 entry strips too, zero-guess launches as one
+    // PH_FRAME127 descriptor (KC_DEEP127=0: off)
+    const char* d0env = getenv("KC_DEEP127");
+    const bool use_deep0 = !(d0env && d0env[0] == '0');
     // smallest strip side (KC_BOT_MINSTRIP overrides): coarser levels live in CTA 0
     const char* msenv = getenv("KC_BOT_MINSTRIP");
     const int min_strip = msenv ? std::max(atoi(msenv), 31) : KC_CLU_MIN_STRIP;
@@ -1664,7 +1670,8 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
         // deep halos on the 63^2 strips (PH_FRAME63): 16 CTAs of 4 rows,
         // entry 127^2, the 31^2 level replicated below, nu = (2, 2)
         const int dp = (use_deep && csz == 16 && m0 == 127 && ns == 2 && nl == 7 && nu1 == 2 && nu2 == 2) ? 1 : -1;
-        const size_t bytes = sizeof(double) * (size_t)bot_smem_doubles(m0, nl, ns, csz, dp);
+        const int dp0 = (dp == 1 && use_deep0) ? 1 : 0;
+        const size_t bytes = sizeof(double) * (size_t)bot_smem_doubles(m0, nl, ns, csz, dp, dp0);
         if (bytes > smem_max) continue;
         if (bot_smem_attr(bytes) != cudaSuccess) continue;
         cudaLaunchConfig_t cfg = {};
@@ -1688,6 +1695,7 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
         nstrip = ns;
         smem = bytes;
         deep = dp;
+        deep0 = dp0;
       }
     }
     cudaGetLastError();
@@ -1708,6 +1716,7 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
     bp.nu2 = nu2;
     bp.nstrip = nstrip;
     bp.deep = deep;
+    bp.deep0 = deep0;
     for (int j = 0; j < bp.nlev; ++j) bp.st[j] = h->L[lb + j].st;
     h->bot_m0 = h->L[lb].m;
     h->bot_cs = cs;

@@ -36,21 +36,28 @@ int main(int argc, char** argv) {
   // argv[6] = 1: deep halos on the 63^2 strips (PH_FRAME63; entry 127, 16 CTAs)
   bp.deep = (argc > 6 && atoi(argv[6]) != 0 && cs == 16 && m0 == 127 && nstrip == 2) ? 1 : -1;
   b.deep = bp.deep;
+  // argv[7] = 1: deep halos on the 127^2 entry strips too (PH_FRAME127)
+  bp.deep0 = (argc > 7 && atoi(argv[7]) != 0 && bp.deep == 1) ? 1 : 0;
+  b.deep0 = bp.deep0 != 0;
   bp.nu1 = 2; bp.nu2 = 2; bp.nstrip = nstrip; bot_geometry(bp, m0, cs);
   if (mv) {
     double* mats; cudaMalloc(&mats, sizeof(double) * 6 * KC_MV_N * KC_MV_LD);
     cudaMemset(mats, 0, sizeof(double) * 6 * KC_MV_N * KC_MV_LD);
     const int R = (KC_MV_N + cs - 1) / cs, order[5] = {1, 3, 0, 5, 2};
     bp.mv_mats = mats; bp.mv_rows = R; bp.mv_off = (bp.total + 1) & ~1;
-    for (int i = 0; i < 5; ++i) { b.mv_mask |= 1u << order[i]; bp.mv_slot[order[i]] = i; }
+    const int nres = bp.deep0 ? 4 : 5;  // the deeper 127^2 strips leave room for 4 blocks
+    for (int i = 0; i < 6; ++i) bp.mv_slot[i] = -1;  // the others are read from global memory
+    for (int i = 0; i < nres; ++i) bp.mv_slot[order[i]] = i;
+    b.mv_mask = 0x3F;
 
   }
-  b.rec(0, kappa); if (kappa > 1) b.rec(0, kappa - 1);
+  b.top(kappa, kappa > 1 ? kappa - 1 : 0);
   bp.mv_copy = (int)b.mv_used;
+  if (mv) for (int i = 0; i < 6; ++i) if (bp.mv_slot[i] < 0) bp.mv_copy &= ~(1 << i);
   unsigned* ds; cudaMalloc(&ds, b.out.size() * 4);
   cudaMemcpy(ds, b.out.data(), b.out.size() * 4, cudaMemcpyHostToDevice);
   bp.gv = gv; bp.gf = gf; bp.gP = P; bp.v_zero = 1; bp.sched = ds; bp.nsched = (int)b.out.size(); bp.final_cur = b.cur & 1;
-  if (mv) bp.mv_xin = bp.mv_off + 5 * ((KC_MV_N + cs - 1) / cs) * KC_MV_LD;
+  if (mv) bp.mv_xin = bp.mv_off + (bp.deep0 ? 4 : 5) * ((KC_MV_N + cs - 1) / cs) * KC_MV_LD;
   size_t smem = sizeof(double) * (mv ? (size_t)(bp.mv_xin + 2 * KC_MV_N) : (size_t)bp.total);
   cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_bottom, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -106,9 +113,9 @@ int main(int argc, char** argv) {
     int o = op[i] / 16, d = op[i] % 16;
     sum[o][d] += t[i + 1] - t[i]; cmp[o][d] += te[i] - t[i]; cnt[o][d]++;
   }
-  const char* nm[12] = {"jacobi", "resid", "restrict", "prolong", "join", "j2z", "rr", "pj", "tiny", "csync", "frame31",
-                        "frame63"};
-  for (int o = 0; o < 12; ++o) for (int d = 0; d < nlev; ++d) if (cnt[o][d])
+  const char* nm[13] = {"jacobi", "resid", "restrict", "prolong", "join", "j2z", "rr", "pj", "tiny", "csync", "frame31",
+                        "frame63", "frame127"};
+  for (int o = 0; o < 13; ++o) for (int d = 0; d < nlev; ++d) if (cnt[o][d])
     printf("  %-9s level %d (m=%3d): %5d phases, %7.0f cycles avg (thread 0 to its barrier %5.0f), %9.0f total\n", nm[o], d,
            bot_m(m0, d), cnt[o][d], sum[o][d] / cnt[o][d], cmp[o][d] / cnt[o][d], sum[o][d]);
   printf("phases traced: %d, total cycles %lld\n", n, n > 1 ? t[n - 1] - t[0] : 0);
