@@ -200,6 +200,10 @@ __global__ void __launch_bounds__(128, KS_MINB) k_pre(const StreamParams p) {
   const int pcol = c0 >> 1;  // coarse column of this lane (c0 even)
   const bool own_lane = lane >= G::HL / 2 && lane < G::HL / 2 + G::NPB;
   const St9 s = p.s;
+  // the rows this lane writes, as half-open ranges (one unsigned compare each)
+  const int ya = max(2 * Q0, 0), yb = own_lane ? min(2 * Qe, g_rows) : ya;  // uo rows
+  const int qa = max(Q0, 0), qb = (own_lane && pcol < p.mc) ? min(Qe, g_mcr) : qa;  // fc rows
+  auto in_rng = [](int v, int lo, int hi) { return (unsigned)(v - lo) < (unsigned)(hi - lo); };
 
   KsAcc A[D + 1];  // pending sums of stages 1..D
 #pragma unroll
@@ -285,14 +289,13 @@ __global__ void __launch_bounds__(128, KS_MINB) k_pre(const StreamParams p) {
     {
       const int yr = yin - D;
       const int q = (yr >> 1) - 1;
-      if (!(yr & 1) && own_lane && q >= Q0 && q < Qe && q < g_mcr && q >= 0 && pcol < p.mc)
+      if (!(yr & 1) && in_rng(q, qa, qb))
         p.fc[kc_idx(p.Pc, q, pcol)] = kc_fw(R[0].x, R[0].y, RE[0], R[1].x, R[1].y, RE[1], R[2].x, R[2].y, RE[2]);
     }
     // ---- output v after NU sweeps ----------------------------------------
     if (NU > 0) {
       const int y = yin - NU;
-      if (own_lane && y >= 2 * Q0 && y < 2 * Qe && y >= 0 && y < g_rows)
-        *reinterpret_cast<double2*>(p.uo + kc_idx(P, y, c0)) = nw[NU];
+      if (in_rng(y, ya, yb)) *reinterpret_cast<double2*>(p.uo + kc_idx(P, y, c0)) = nw[NU];
     }
     // per-lane partials, stored from inside the loop: any code after it (a
     // warp reduction, even a store) makes the compiler wrap the hot loop in
@@ -331,6 +334,8 @@ __global__ void __launch_bounds__(128, KS_MINB) k_post(const StreamParams p) {
   const int pc = c0 >> 1;
   const bool own_lane = lane >= G::HL / 2 && lane < G::HL / 2 + G::NPB;
   const St9 s = p.s;
+  const int ya = max(2 * Q0, 0), yb = own_lane ? min(2 * Qe, g_rows) : ya;  // uo rows (see k_pre)
+  auto in_rng = [](int v, int lo, int hi) { return (unsigned)(v - lo) < (unsigned)(hi - lo); };
 
   if (active) {
     KsAcc A[DD + 1];
@@ -400,7 +405,7 @@ __global__ void __launch_bounds__(128, KS_MINB) k_post(const StreamParams p) {
       // output after NU sweeps (stage NU; NU = 0 writes the corrected v)
       {
         const int y = yin - NU;
-        if (own_lane && y >= 2 * Q0 && y < 2 * Qe && y >= 0 && y < g_rows) {
+        if (in_rng(y, ya, yb)) {
           *reinterpret_cast<double2*>(p.uo + kc_idx(P, y, c0)) = nw[NU];
           if (NORMS) acc_e = fma(nw[NU].y, nw[NU].y, fma(nw[NU].x, nw[NU].x, acc_e));
           if (DOT) acc_e = fma(fr[NU > 0 ? NU : 1].y, nw[NU].y, fma(fr[NU > 0 ? NU : 1].x, nw[NU].x, acc_e));
@@ -408,7 +413,7 @@ __global__ void __launch_bounds__(128, KS_MINB) k_post(const StreamParams p) {
       }
       if (NORMS) {
         const int y = yin - D;
-        if (own_lane && y >= 2 * Q0 && y < 2 * Qe && y >= 0 && y < g_rows)
+        if (in_rng(y, ya, yb))
           acc_r = fma(nw[D].y, nw[D].y, fma(nw[D].x, nw[D].x, acc_r));
       }
       if (DOT && yin == ye) reinterpret_cast<double2*>(p.part)[wg * 32 + lane] = make_double2(acc_e, 0.0);

@@ -14,6 +14,7 @@ n = 12
 m = 2 ** n - 1
 VARIANTS = {
     "entry127_cs16_min31": {},
+    "no_deep127": {"KC_DEEP127": "0"},
     "no_frame_operators": {"KC_TINY_MV": "0"},
     "no_postpre": {"KC_POSTPRE": "0"},
     "postpre_stream": {"KC_POSTPRE_STREAM": "1"},
@@ -23,7 +24,7 @@ VARIANTS = {
     "entry127_cs8_min31": {"KC_BOT_CS": "8"},
     "entry63_single": {"KC_BOT_CLUSTER": "0"},
 }
-KEYS = ("KC_BOT_ENTRY", "KC_BOT_MINSTRIP", "KC_BOT_CS", "KC_BOT_CLUSTER", "KC_TINY_MV", "KC_POSTPRE", "KC_POSTPRE_STREAM")
+KEYS = ("KC_DEEP127", "KC_BOT_ENTRY", "KC_BOT_MINSTRIP", "KC_BOT_CS", "KC_BOT_CLUSTER", "KC_TINY_MV", "KC_POSTPRE", "KC_POSTPRE_STREAM")
 if len(sys.argv) > 2:
     VARIANTS = {k: VARIANTS[k] for k in sys.argv[2].split(",")}
 v0 = np.random.default_rng(0).random((m, m))
