@@ -237,14 +237,21 @@ __global__ void __launch_bounds__(128, KS_MINB) k_pre(const StreamParams p) {
   for (int y = ys - D; y < ys + KS_PF; ++y) fetch(y, y >= ys);
   // deeper stages, and the shared-product norms pass, spill when unrolled x4
   constexpr int UR = NU > 2 ? 1 : (SYM && NORMS && KS_UNROLL > 2) ? 2 : KS_UNROLL;
+  // f of the row each stage completes (yin - t), carried in registers: stage
+  // t+1's row is the one stage t had one step earlier, so a step reads one
+  // new f row (yin - 1); rows ys-2 .. ys-D are loaded before the loop
+  double2 fr[D + 1];
+  asm volatile("cp.async.wait_group %0;" ::"n"(KS_PF + 1) : "memory");  // rows <= ys - 2 have landed
+#pragma unroll
+  for (int t = 1; t < D; ++t) fr[t] = ks_lds2(fring + ((ys - 1 - t) & (FR - 1)) * KS_BAND);
 #pragma unroll UR
   for (int yin = ys; yin <= ye; ++yin) {
     fetch(yin + KS_PF, true);
     ks_cp_wait();  // all but the newest KS_PF groups done: rows <= yin have landed
     const double2 u0 = ZERO ? make_double2(0.0, 0.0) : ks_lds2(uring + (yin & (KS_URING - 1)) * KS_BAND);
-    double2 fr[D + 1];  // f of the row each stage completes (yin - t)
 #pragma unroll
-    for (int t = 1; t <= D; ++t) fr[t] = ks_lds2(fring + ((yin - t) & (FR - 1)) * KS_BAND);
+    for (int t = D; t > 1; --t) fr[t] = fr[t - 1];
+    fr[1] = ks_lds2(fring + ((yin - 1) & (FR - 1)) * KS_BAND);
 
     // NORMS: rows owned by this chunk, interior columns owned by this lane;
     // the input's residual is the first stage's f - A u at row yin - 1
@@ -364,14 +371,18 @@ __global__ void __launch_bounds__(128, KS_MINB) k_post(const StreamParams p) {
     };
     for (int y = ys - D; y < ys + KS_PF; ++y) fetch(y, y >= ys);
     constexpr int UR = (NU <= 2 || !NORMS) ? KS_UNROLL_POST : 1;  // deeper norm stages spill
+    double2 fr[DD + 1];  // f of row yin - t, carried across steps (see k_pre)
+    asm volatile("cp.async.wait_group %0;" ::"n"(KS_PF + 1) : "memory");
+#pragma unroll
+    for (int t = 1; t < D; ++t) fr[t] = ks_lds2(fring + ((ys - 1 - t) & (FR - 1)) * KS_BAND);
 #pragma unroll UR
     for (int yin = ys; yin <= ye; ++yin) {
       fetch(yin + KS_PF, true);
       ks_cp_wait();
       const double2 u0 = VZ ? make_double2(0.0, 0.0) : ks_lds2(uring + (yin & (KS_URING - 1)) * KS_BAND);
-      double2 fr[DD + 1];  // f of row yin - t
 #pragma unroll
-      for (int t = 1; t <= D; ++t) fr[t] = ks_lds2(fring + ((yin - t) & (FR - 1)) * KS_BAND);
+      for (int t = D; t > 1; --t) fr[t] = fr[t - 1];
+      if (D > 0) fr[1] = ks_lds2(fring + ((yin - 1) & (FR - 1)) * KS_BAND);
       const int q = yin >> 1;
       if (q != qcur) {  // advance the coarse window by one row (yin even); warp-uniform
         vcp = vcc;
