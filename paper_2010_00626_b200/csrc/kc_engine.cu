@@ -25,6 +25,7 @@
 #include "../../include/kcb200.h"
 #include "kc_bottom.cuh"
 #include "kc_common.cuh"
+#include "kc_loop.cuh"
 #include "kc_grid_kernels.cuh"
 #include "kc_pcg.cuh"
 #include "kc_zebra.cuh"
@@ -37,45 +38,15 @@ namespace {
 
 thread_local std::string g_create_err;
 
-// Device-resident stand-alone loop state (cycle.py:332-353), advanced by
 // k_stop_check inside the conditional WHILE graph of the stand-alone solve:
 // it runs after the level-0 pre kernel has produced the norms of the
 // current iterate v_it (cycle.py:338-353) and decides whether the rest of
-// the cycle and the next iteration run (the WHILE condition; set_rest: also
-// an IF node's).
-struct SolveState {
-  double target, prev, reduction;
-  int it, max_it, streak, status, stop_mode, pad;
-  double* err_hist;
-  double* res_hist;
-};
-
+// the cycle and the next iteration run (kc_loop.cuh; the loop body folds
+// the same test into the norm reduction's last block)
 __global__ void k_stop_check(cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_rest, int set_rest,
                              SolveState* st, const double* __restrict__ scal) {
   if (threadIdx.x != 0) return;
-  const int it = st->it;  // cycles completed
-  const double e = scal[0], r = scal[1];
-  st->err_hist[it] = e;
-  st->res_hist[it] = r;
-  const double cur = st->stop_mode == KC_STOP_ERROR ? e : r;
-  if (it == 0) st->target = cur / st->reduction;  // cycle.py:338-341
-  unsigned go = 1u;
-  if (cur <= st->target) {  // cycle.py:347
-    st->status = KC_STATUS_CONVERGED;
-    go = 0u;
-  } else if (it > 0) {  // cycle.py:350-353: five consecutive growth steps
-    const int streak = cur > st->prev ? st->streak + 1 : 0;
-    st->streak = streak;
-    if (streak >= 5) {
-      st->status = KC_STATUS_DIVERGED;
-      go = 0u;
-    }
-  }
-  st->prev = cur;
-  if (go && it >= st->max_it) go = 0u;  // status stays MAX_CYCLES
-  if (go) st->it = it + 1;
-  cudaGraphSetConditional(h_loop, go);
-  if (set_rest) cudaGraphSetConditional(h_rest, go);
+  kc_stop_test(LoopCheck{h_loop, h_rest, set_rest, st}, scal[0], scal[1]);
 }
 
 struct Level {
@@ -172,6 +143,8 @@ struct kc_handle {
   int ks_sym_max = 2;         // shared products on symmetric levels: 0 off, 1 w1/w7 only, 2 all (KC_SYM)
   int num_sms = 148;
   SolveState* d_solve = nullptr;   // device loop state
+  LoopCheck loop_ck{};             // while capturing the loop body: the norm reduction runs the stop test
+  bool loop_ck_on = false;
   double* d_hist = nullptr;        // err | res histories for the device loop
   int hist_cap = 0;
   std::map<const void*, int> ks_occ;  // warp slots per streaming kernel (one wave)
@@ -1111,8 +1084,12 @@ int ex_pre(kc_handle* h, int l, bool norms = false) {
   KC_LAUNCH_CHECK(h);
   ++h->launches;
   if (norms) {
-    k_norms_lanes<true><<<KS_NB, 256, 0, h->stream>>>(reinterpret_cast<const double2*>(h->d_npart), nw * 32,
-                                                 reinterpret_cast<double2*>(h->d_nblk), h->d_ncount, h->d_scal);
+    const double2* part = reinterpret_cast<const double2*>(h->d_npart);
+    double2* nblk = reinterpret_cast<double2*>(h->d_nblk);
+    if (h->loop_ck_on)
+      k_norms_lanes<true, true><<<KS_NB, 256, 0, h->stream>>>(part, nw * 32, nblk, h->d_ncount, h->d_scal, h->loop_ck);
+    else
+      k_norms_lanes<true><<<KS_NB, 256, 0, h->stream>>>(part, nw * 32, nblk, h->d_ncount, h->d_scal);
     KC_LAUNCH_CHECK(h);
     ++h->launches;
   }
@@ -1449,8 +1426,15 @@ int get_solve_graph(kc_handle* h, int kappa, SolveGraph** out) {
     const int l0 = h->launches;
     KC_CUDA(h, cudaStreamBeginCaptureToGraph(h->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     for (size_t i = 1; i < ops.size() && rc == KC_OK; ++i) rc = ex_op(h, ops[i]);
+    // the pre pass's norm reduction runs the stop test in its last block
+    // (KC_FUSED_CHECK=0: a separate k_stop_check kernel)
+    const char* cenv = getenv("KC_FUSED_CHECK");
+    const bool fused_check = !(cenv && cenv[0] == '0');
+    h->loop_ck = LoopCheck{h_loop, h_none, set_rest, st};
+    h->loop_ck_on = fused_check;
     if (rc == KC_OK) rc = ex_op(h, ops[0]);
-    if (rc == KC_OK) {
+    h->loop_ck_on = false;
+    if (rc == KC_OK && !fused_check) {
       k_stop_check<<<1, 32, 0, h->stream>>>(h_loop, h_none, set_rest, st, scal);
       if (cudaGetLastError() != cudaSuccess) rc = KC_ECUDA;
     }

@@ -25,6 +25,7 @@
 // forced to +0.0 at every stage (the Dirichlet ghost values).
 #pragma once
 #include "kc_common.cuh"
+#include "kc_loop.cuh"
 
 #define KS_BAND 64  // fine columns per warp band (2 per lane)
 #ifndef KS_MINB
@@ -583,9 +584,12 @@ __global__ void __launch_bounds__(256) k_norms_final(const double* __restrict__ 
 #define KS_NB 148
 #endif
 static_assert(KS_NB <= 256, "one block sum per thread in the final tree");
-template <bool SQRT>
+// CHECK: the last block also runs the stand-alone loop's stop test on the
+// sums (kc_loop.cuh) -- one kernel less per loop iteration
+template <bool SQRT, bool CHECK = false>
 __global__ void __launch_bounds__(256) k_norms_lanes(const double2* __restrict__ part, int n, double2* __restrict__ bsum,
-                                                     unsigned* __restrict__ counter, double* __restrict__ out) {
+                                                     unsigned* __restrict__ counter, double* __restrict__ out,
+                                                     LoopCheck ck = LoopCheck{}) {
   __shared__ double sh[2][8];
   __shared__ bool last;
   const int per = (n + KS_NB - 1) / KS_NB;
@@ -644,5 +648,6 @@ __global__ void __launch_bounds__(256) k_norms_lanes(const double2* __restrict__
     out[0] = SQRT ? sqrt(sa) : sa;
     out[1] = SQRT ? sqrt(sb) : sb;
     *counter = 0u;
+    if (CHECK) kc_stop_test(ck, out[0], out[1]);
   }
 }
