@@ -103,6 +103,7 @@ struct BotParams {
   // shared memory at mv_off, slot mv_slot[block]
   const double* mv_mats;
   int mv_copy, mv_off, mv_rows, mv_xin;  // mv_xin: 2 x 225 doubles of packed inputs
+  int mv_avail;      // blocks that exist (resident or read from global memory): frames use them
   int mv_slot[6];
 };
 
@@ -950,7 +951,7 @@ struct BotFrame31 {
   __device__ __forceinline__ void frame15(int d, int kap, int& c, int& z) {
     const int k3 = kap < 3 ? kap : 3;
     const int need = (1 << ((k3 - 1) * 2 + 1)) | (z ? 0 : (1 << ((k3 - 1) * 2)));
-    if (bp->mv_copy && (bp->mv_copy & need) == need) {
+    if ((bp->mv_avail & need) == need) {
       if (mv_sync) clu_sync();
       mv_sync = false;
       const int ob = z ? (mv_last >= 0 ? mv_last ^ 1 : c ^ 1) : c ^ 1;
@@ -961,7 +962,7 @@ struct BotFrame31 {
       z = 0;
       return;
     }
-    if (bp->mv_copy) mv_sync = true;
+    if (bp->mv_avail) mv_sync = true;
     if (tid < 256) {
       const BotTiny t{sm, lv, tab, bp->nu1, bp->nu2, tid, 256};
       t.frame(d, kap, nlev, c, z, tiny_child);
@@ -1520,7 +1521,7 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
       bot_mv_frame(sm, bp, L, src, BD_CBUF(e), zero, BD_KAP(e), rank, cs);
       mv_last = BD_CBUF(e);
     } else {  // PH_TINY (every CTA: warp 0 for sides <= 7, warps 0-7 for side 15)
-      if (m == KC_MV_M && bp.mv_copy) mv_sync = true;
+      if (m == KC_MV_M && bp.mv_avail) mv_sync = true;
       const BotTiny t{sm, lv, tab, bp.nu1, bp.nu2, tid, nth};
       int cur = src, vz = zero;
       t.frame(d, BD_KAP(e), nlev, cur, vz, tiny_child);

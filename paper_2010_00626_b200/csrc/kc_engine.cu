@@ -693,6 +693,7 @@ int ex_bottom(kc_handle* h, int l, int k1, int k2) {
   bp.v_zero = L.vzero ? 1 : 0;
   int rc = get_bot_sched(h, k1, k2, bp.v_zero, &bp.sched, &bp.nsched, &bp.final_cur, &bp.mv_copy);
   bp.mv_copy &= h->mv_resident;  // the prologue copies the resident blocks the schedule uses
+  bp.mv_avail = h->mv_avail;     // the frames (device) use every block the schedule (host) assumed
   if (rc) return rc;
   if (h->L[h->n - 1].st.center == 0.0) KC_FAIL(h, KC_ESINGULAR, "singular coarsest operator");
   if (h->bot_cs > 1) {

@@ -49,6 +49,7 @@ int main(int argc, char** argv) {
     for (int i = 0; i < 6; ++i) bp.mv_slot[i] = -1;  // the others are read from global memory
     for (int i = 0; i < nres; ++i) bp.mv_slot[order[i]] = i;
     b.mv_mask = 0x3F;
+    bp.mv_avail = 0x3F;
 
   }
   b.top(kappa, kappa > 1 ? kappa - 1 : 0);
