@@ -71,6 +71,33 @@ def test_fast_cycle_close_to_oracle(n):
     st.close()
 
 
+@pytest.mark.parametrize("kappa", [2, 3, 4, 9])
+def test_fast_frame_operator_variants_close_to_oracle(kappa, monkeypatch):
+    """The bottom kernel's side-15 frames as frame operators (resident in
+    shared memory or read from L2) or as the frames' own code, with and
+    without the deep-halo 127^2 entry: each within the FMA build's bar of the
+    reference cycle (n = 9, entry 127^2, every counter incl. W)."""
+    n = 9
+    m = 2 ** n - 1
+    rng = np.random.default_rng(40 + kappa)
+    v0, f0 = rng.random((m, m)), rng.standard_normal((m, m))
+    h = O.Hierarchy(O.hierarchy(1e-4, 45.0, n))
+    h.v[0], h.f[0] = v0.copy(), f0.copy()
+    h.cycle(min(kappa, n))
+    cfg = CycleConfig(n=n, kappa=kappa)
+    for env in ({}, {"KC_TINY_MV": "0"}, {"KC_DEEP127": "0"}):
+        for k in ("KC_TINY_MV", "KC_DEEP127"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        st = _fast(ProblemSpec(1e-4, 45.0), cfg)
+        st.v[0], st.f[0] = v0, f0
+        run_cycle(st, cfg, CycleStats.for_levels(n))
+        d = np.max(np.abs(st.v[0] - h.v[0]))
+        assert d <= 1e-13 * np.max(np.abs(h.v[0])), (env, d)
+        st.close()
+
+
 @pytest.mark.parametrize("n", [5, 7, 9])
 @pytest.mark.parametrize("kname", ["1", "2", "3", "4", "W"])
 def test_fast_standalone_counts_and_histories(n, kname):

@@ -8,9 +8,24 @@ import subprocess
 import sys
 
 CHILD = r'''
-import collections, json, os, sys
+import collections, ctypes, json, os, sys
 import numpy as np
 sys.path.insert(0, os.environ["KC_ROOT"])
+if os.environ.get("AB_LENIENT") == "1":  # an older library: entry points it lacks become inert stubs
+    _CDLL = ctypes.CDLL
+
+    class _Lenient:
+        def __init__(self, *a, **k):
+            self._h = _CDLL(*a, **k)
+
+        def __getattr__(self, name):
+            try:
+                return getattr(self._h, name)
+            except AttributeError:
+                f = lambda *a: 1  # noqa: E731
+                f.restype = f.argtypes = None
+                return f
+    ctypes.CDLL = _Lenient
 import paper_2010_00626_b200 as kc
 n, k, arith = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
 st = kc.build_state(kc.ProblemSpec(1e-4, 45.0, seed=0), kc.CycleConfig(n=n, kappa=k), arith=arith)
