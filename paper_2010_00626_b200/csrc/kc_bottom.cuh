@@ -61,7 +61,15 @@
 #endif
 #define KC_BOT_MAXLEV 8
 #ifndef KC_BOT_THREADS
-#define KC_BOT_THREADS 384  // 12 warps: 147 registers without spills (512 spills at the 128 cap)
+// FMA build: 8 warps, up to 255 registers without spills (at 384 threads the
+// frame-operator and pair paths spill at the 168-register cap: n=12 kappa=3
+// cycle 0.889 vs 0.845 ms); exact build (interpreter frames): 12 warps
+// (256 threads: 1.148 -> 1.206 ms)
+#if KC_FAST
+#define KC_BOT_THREADS 256
+#else
+#define KC_BOT_THREADS 384
+#endif
 #endif
 #define KC_BOT_WARPS (KC_BOT_THREADS / 32)
 #define KC_BOT_RB 4  // rows per thread in stencil phases
@@ -79,6 +87,19 @@ struct BotLv {
   int mc;                        // child side
   int hb;                        // halo rows each side (1; KC_DEEP_HB on the deep-halo strip level)
 };
+
+#define KC_MV_M 15
+#define KC_MV_N (KC_MV_M * KC_MV_M)  // 225 unknowns of a side-15 level
+#define KC_MV_LD 226                 // row stride (16-byte multiple: cp.async)
+// blocks: (k - 1) * 2 + {0: A_k, 1: B_k} for k = 1..3, then the PAIR
+// operators P = A_kb B_ka + B_kb of the two frames a side-31 call makes from
+// a zero guess, counters (ka, kb) = (2, 1), (3, 2), (3, 3): one
+// matrix-vector phase instead of two (BotFrame31::frame)
+#define KC_MV_PAIR0 6
+#define KC_MV_NBLK 9
+__host__ __device__ __forceinline__ int kc_mv_pair(int kap) {  // kap >= 2: the pair block of frames (kap, kap - 1)
+  return kap == 2 ? KC_MV_PAIR0 : (kap == 3 ? KC_MV_PAIR0 + 1 : KC_MV_PAIR0 + 2);
+}
 
 struct BotParams {
   int nlev;  // levels resident in smem: entry level .. coarsest
@@ -104,7 +125,7 @@ struct BotParams {
   const double* mv_mats;
   int mv_copy, mv_off, mv_rows, mv_xin;  // mv_xin: 2 x 225 doubles of packed inputs
   int mv_avail;      // blocks that exist (resident or read from global memory): frames use them
-  int mv_slot[6];
+  int mv_slot[KC_MV_NBLK];
 };
 
 // Frame operators (FMA build, cluster launches only).  A kappa_cycle frame on
@@ -123,9 +144,6 @@ struct BotParams {
 // blocks are not resident runs the interpreter on every CTA's copy.  The product rounds
 // differently from the frame's own operation sequence, so this is FAST-only
 // (the exact build keeps the frames); parity bar as for the FMA build.
-#define KC_MV_M 15
-#define KC_MV_N (KC_MV_M * KC_MV_M)  // 225 unknowns of a side-15 level
-#define KC_MV_LD 226                 // row stride (16-byte multiple: cp.async)
 
 // smem geometry of level d (entry side m0): side m_d = ((m0+1) >> d) - 1,
 // stride S = m+2, three arrays v0, v1, f of (rows+2) x S, rows = m, or the
@@ -433,6 +451,18 @@ struct BotBuilder {  // host side
         rec(d + 1, kap);
         if (kap > 1) rec(d + 1, kap - 1);
         dry = false;
+      } else if (dry && kap > 1 && bot_m(m0, d) == 31 && bot_m(m0, d + 1) == KC_MV_M &&
+                 ((mv_mask >> kc_mv_pair(kap)) & 1u)) {
+        // inside BotFrame31: the pair operator of frames (kap, kap - 1) from
+        // the zero guess, one matrix-vector phase (its buffer rule is a zero
+        // frame's)
+        const int src = (cur >> (d + 1)) & 1u;
+        const int ob = mv_last >= 0 ? mv_last ^ 1 : src ^ 1;
+        mv_sync = false;
+        mv_used |= 1u << kc_mv_pair(kap);
+        mv_last = ob;
+        cur = (cur & ~(1u << (d + 1))) | ((unsigned)ob << (d + 1));
+        vz &= ~(1u << (d + 1));
       } else {
         rec(d + 1, kap);
         if (kap > 1) rec(d + 1, kap - 1);
@@ -835,19 +865,21 @@ struct BotTiny {
 // a zero guess), inputs gathered from CTA 0's side-15 level, outputs stored
 // into CTA 0's other v buffer (so no CTA overwrites an input another CTA may
 // still read); the caller ends the phase with a cluster barrier.
+// (bb, ba: the blocks applied to f and to v; bb = -1 selects B_kap / A_kap)
 __device__ __forceinline__ void bot_mv_frame(double* sm, const BotParams& bp, const BotLv& L, int src, int ob,
-                                             bool zero, int kap, int rank, int cs) {
+                                             bool zero, int kap, int rank, int cs, int bb = -1, int ba = -1) {
   cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
   const int R = bp.mv_rows;
   asm volatile("cp.async.wait_all;" ::: "memory");  // the blocks (prologue copies)
   bot_bar();
   // this CTA's row slice of the blocks: in shared memory (resident), else
   // straight from global memory (2.4 MB for all six blocks: L2-resident)
-  const int bb = (kap - 1) * 2 + 1, ba = (kap - 1) * 2, i0 = rank * R;
-  const double* B = bp.mv_slot[bb] >= 0 ? sm + bp.mv_off + bp.mv_slot[bb] * R * KC_MV_LD
-                                        : bp.mv_mats + ((size_t)bb * KC_MV_N + i0) * KC_MV_LD;
-  const double* A = bp.mv_slot[ba] >= 0 ? sm + bp.mv_off + bp.mv_slot[ba] * R * KC_MV_LD
-                                        : bp.mv_mats + ((size_t)ba * KC_MV_N + i0) * KC_MV_LD;
+  if (bb < 0) {
+    bb = (kap - 1) * 2 + 1;
+    ba = (kap - 1) * 2;
+  }
+  if (ba < 0) ba = bb;  // a pair operator on a zero guess: A is never read
+  const int i0 = rank * R;
   const double* vin = sm + (src ? L.vo1 : L.vo0);  // this CTA's replica
   const double* fin = sm + L.fo;
   double* xv = sm + bp.mv_xin;  // inputs packed row-major: v (225), f (225)
@@ -860,29 +892,38 @@ __device__ __forceinline__ void bot_mv_frame(double* sm, const BotParams& bp, co
   bot_bar();
   double* out = sm + (ob ? L.vo1 : L.vo0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int r = warp; r < R && i0 + r < KC_MV_N; r += KC_BOT_WARPS) {
-    const double* br = B + r * KC_MV_LD;
-    const double* ar = A + r * KC_MV_LD;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // independent chains
+  auto rows = [&](const double* B, const double* A) {
+    for (int r = warp; r < R && i0 + r < KC_MV_N; r += KC_BOT_WARPS) {
+      const double* br = B + r * KC_MV_LD;
+      const double* ar = A + r * KC_MV_LD;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // independent chains
 #pragma unroll
-    for (int k = 0; k < (KC_MV_N + 31) / 32; ++k) {
-      const int j = lane + 32 * k;
-      if (j < KC_MV_N) {
-        if (k & 1) a1 = fma(br[j], xf[j], a1);
-        else a0 = fma(br[j], xf[j], a0);
-        if (!zero) {
-          if (k & 1) a3 = fma(ar[j], xv[j], a3);
-          else a2 = fma(ar[j], xv[j], a2);
+      for (int k = 0; k < (KC_MV_N + 31) / 32; ++k) {
+        const int j = lane + 32 * k;
+        if (j < KC_MV_N) {
+          if (k & 1) a1 = fma(br[j], xf[j], a1);
+          else a0 = fma(br[j], xf[j], a0);
+          if (!zero) {
+            if (k & 1) a3 = fma(ar[j], xv[j], a3);
+            else a2 = fma(ar[j], xv[j], a2);
+          }
         }
       }
-    }
-    double acc = (a0 + a1) + (a2 + a3);
+      double acc = (a0 + a1) + (a2 + a3);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    // every lane holds the row's value: lane k stores it into CTA k's replica
-    const int i = i0 + r, y = i / KC_MV_M, x = i - y * KC_MV_M;
-    if (lane < cs) *cl.map_shared_rank(out + y * L.S + x, lane) = acc;
-  }
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      // every lane holds the row's value: lane k stores it into CTA k's replica
+      const int i = i0 + r, y = i / KC_MV_M, x = i - y * KC_MV_M;
+      if (lane < cs) *cl.map_shared_rank(out + y * L.S + x, lane) = acc;
+    }
+  };
+  // shared-memory loads where the blocks are resident (a pointer that may
+  // be either would make every load a generic one)
+  const int sb = bp.mv_slot[bb], sa = bp.mv_slot[ba];
+  if (sb >= 0 && (zero || sa >= 0))
+    rows(sm + bp.mv_off + sb * R * KC_MV_LD, sm + bp.mv_off + (zero ? sb : sa) * R * KC_MV_LD);
+  else
+    rows(bp.mv_mats + ((size_t)bb * KC_MV_N + i0) * KC_MV_LD, bp.mv_mats + ((size_t)ba * KC_MV_N + i0) * KC_MV_LD);
 }
 
 // PH_FRAME31: a whole kappa_cycle frame on the replicated side-31 level --
@@ -951,7 +992,7 @@ struct BotFrame31 {
   __device__ __forceinline__ void frame15(int d, int kap, int& c, int& z) {
     const int k3 = kap < 3 ? kap : 3;
     const int need = (1 << ((k3 - 1) * 2 + 1)) | (z ? 0 : (1 << ((k3 - 1) * 2)));
-    if ((bp->mv_avail & need) == need) {
+    if (KC_FAST && (bp->mv_avail & need) == need) {  // frame operators exist in the FMA build only
       if (mv_sync) clu_sync();
       mv_sync = false;
       const int ob = z ? (mv_last >= 0 ? mv_last ^ 1 : c ^ 1) : c ^ 1;
@@ -995,8 +1036,20 @@ struct BotFrame31 {
       bot_bar();
     }
     int c = 0, z = 1;  // the child's zero guess (cycle.py:214)
-    frame15(d + 1, kap, c, z);
-    if (kap > 1) frame15(d + 1, kap - 1, c, z);
+    if (KC_FAST && kap > 1 && ((bp->mv_avail >> kc_mv_pair(kap)) & 1)) {
+      // both frames (kap, kap - 1) from the zero guess as one operator
+      if (mv_sync) clu_sync();
+      mv_sync = false;
+      const int ob = mv_last >= 0 ? mv_last ^ 1 : c ^ 1;
+      bot_mv_frame(sm, *bp, lv[d + 1], c, ob, true, kap, rank, cs, kc_mv_pair(kap));
+      clu_sync();
+      mv_last = ob;
+      c = ob;
+      z = 0;
+    } else {
+      frame15(d + 1, kap, c, z);
+      if (kap > 1) frame15(d + 1, kap - 1, c, z);
+    }
     {  // u += P vc, one coarse cell (2x2 fine points) per item (transfer.py:50-58)
       double* u = buf(L, cur);
       const double* vc = buf(C, c);
@@ -1271,12 +1324,20 @@ __device__ __forceinline__ void bot_run_frame(int op, double* sm, const BotLv* l
 // (the bottom kernel's own frame code) with counter k on the unit input j
 // (j < 225: v = e_j; else f = e_(j-225)) and stores v_out as column j of
 // [A_k | B_k].  tp: the 4-level geometry of a side-15 entry.
+// blockIdx.y >= 3: the pair operators (KC_MV_PAIR0 + y - 3): CTA j (< 225)
+// runs the two frames a side-31 call makes, (2, 1), (3, 2) or (3, 3), from a
+// zero v on f = e_j.  One call site of BotTiny::frame in this kernel: a
+// second one (a separate pair kernel) changed how the frame code is inlined
+// into k_bottom and slowed the exact build's cycle by 6 %.
 __global__ void __launch_bounds__(256) k_tiny_mats(const BotParams tp, double* __restrict__ mats) {
   extern __shared__ double sm[];
   __shared__ St9 tab[4];
   __shared__ BotLv lv[4];
   __shared__ int child[2];
-  const int j = blockIdx.x, kap = blockIdx.y + 1;
+  const bool pair = blockIdx.y >= 3;
+  const int j = blockIdx.x, py = blockIdx.y - 3;
+  if (pair && j >= KC_MV_N) return;  // pairs take f inputs only
+  const int ka = pair ? (py == 0 ? 2 : 3) : blockIdx.y + 1, kb = py == 0 ? 1 : (py == 1 ? 2 : 3);
   for (int i = threadIdx.x; i < tp.total; i += 256) sm[i] = 0.0;
   if (threadIdx.x < 4) {
     tab[threadIdx.x] = tp.st[threadIdx.x];
@@ -1286,20 +1347,23 @@ __global__ void __launch_bounds__(256) k_tiny_mats(const BotParams tp, double* _
   const BotLv L0 = lv[0];
   if (threadIdx.x == 0) {
     const int jj = j % KC_MV_N, y = jj / KC_MV_M, x = jj - y * KC_MV_M;
-    sm[(j < KC_MV_N ? L0.vo0 : L0.fo) + y * L0.S + x] = 1.0;
+    sm[(j < KC_MV_N && !pair ? L0.vo0 : L0.fo) + y * L0.S + x] = 1.0;
   }
   bot_bar();
   const BotTiny t{sm, lv, tab, tp.nu1, tp.nu2, (int)threadIdx.x, 256};
   int cur = 0, vz = 0;
-  t.frame(0, kap, 4, cur, vz, child);
-  bot_bar();
+  for (int s = 0; s < (pair ? 2 : 1); ++s) {
+    t.frame(0, s == 0 ? ka : kb, 4, cur, vz, child);
+    bot_bar();
+  }
   const double* o = sm + (cur ? L0.vo1 : L0.vo0);
-  double* blk = mats + (size_t)((kap - 1) * 2 + (j < KC_MV_N ? 0 : 1)) * KC_MV_N * KC_MV_LD;
+  double* blk = mats + (size_t)(pair ? KC_MV_PAIR0 + py : (ka - 1) * 2 + (j < KC_MV_N ? 0 : 1)) * KC_MV_N * KC_MV_LD;
   for (int i = threadIdx.x; i < KC_MV_N; i += 256) {
     const int y = i / KC_MV_M, x = i - y * KC_MV_M;
     blk[(size_t)i * KC_MV_LD + j % KC_MV_N] = o[y * L0.S + x];
   }
 }
+
 
 __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp, int m0) {
   extern __shared__ double sm[];
@@ -1345,7 +1409,7 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
     // grid; completed by the cp.async.wait_all below or in bot_mv_frame)
     const int R = bp.mv_rows, i0 = rank * R;
     const int rows = min(R, KC_MV_N - i0);
-    for (int b = 0; b < 6; ++b) {
+    for (int b = 0; b < KC_MV_NBLK; ++b) {
       if (!((bp.mv_copy >> b) & 1) || rows <= 0) continue;
       const double* src = bp.mv_mats + ((size_t)b * KC_MV_N + i0) * KC_MV_LD;
       double* dst = sm + bp.mv_off + bp.mv_slot[b] * R * KC_MV_LD;
@@ -1517,7 +1581,7 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
       bot_run_frame(op, sm, lv, tab, &bp, d, BD_KAP(e), src, zero, rank, cs, nlev, &f31_slot, tiny_child, mvs);
       mv_last = mvs[0];
       mv_sync = mvs[1] != 0;
-    } else if (strip) {  // PH_TINY as a frame operator (all CTAs; FMA build)
+    } else if (KC_FAST && strip) {  // PH_TINY as a frame operator (all CTAs; FMA build only)
       bot_mv_frame(sm, bp, L, src, BD_CBUF(e), zero, BD_KAP(e), rank, cs);
       mv_last = BD_CBUF(e);
     } else {  // PH_TINY (every CTA: warp 0 for sides <= 7, warps 0-7 for side 15)

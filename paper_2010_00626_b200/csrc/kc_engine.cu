@@ -634,10 +634,13 @@ int setup_frame_operators(kc_handle* h, const cudaDeviceProp& prop) {
   tp.nu2 = h->nu2;
   for (int j = 0; j < 4; ++j) tp.st[j] = bp.st[d15 + j];
   bot_geometry(tp, KC_MV_M, 1);
-  const size_t mbytes = sizeof(double) * 6 * (size_t)KC_MV_N * KC_MV_LD;
+  const size_t mbytes = sizeof(double) * KC_MV_NBLK * (size_t)KC_MV_N * KC_MV_LD;
   KC_CUDA(h, cudaMalloc(&h->mv_mats, mbytes));
   KC_CUDA(h, cudaMemset(h->mv_mats, 0, mbytes));
-  k_tiny_mats<<<dim3(2 * KC_MV_N, 3), 256, sizeof(double) * tp.total>>>(tp, h->mv_mats);
+  // with the pair operators (KC_TINY_PAIRS=0: the side-31 calls keep two frames)
+  const char* penv = getenv("KC_TINY_PAIRS");
+  const bool pairs = !(penv && penv[0] == '0');
+  k_tiny_mats<<<dim3(2 * KC_MV_N, pairs ? 6 : 3), 256, sizeof(double) * tp.total>>>(tp, h->mv_mats);
   KC_LAUNCH_CHECK(h);
   KC_CUDA(h, cudaDeviceSynchronize());
   cudaFuncAttributes fa{};
@@ -646,10 +649,13 @@ int setup_frame_operators(kc_handle* h, const cudaDeviceProp& prop) {
   const int R = (KC_MV_N + h->bot_cs - 1) / h->bot_cs;
   const int off = (bp.total + 1) & ~1;
   const size_t per = sizeof(double) * (size_t)R * KC_MV_LD;
-  const int order[6] = {1, 3, 0, 5, 2, 4};
+  // residency: the blocks the side-31 frames use first (B1 and the pairs),
+  // then the single frames' in the order the kappa-cycles use them
+  const int order[KC_MV_NBLK] = {1, KC_MV_PAIR0, KC_MV_PAIR0 + 1, KC_MV_PAIR0 + 2, 3, 0, 5, 2, 4};
   int mask = 0, nres = 0;
-  for (int b = 0; b < 6; ++b) bp.mv_slot[b] = -1;  // not resident: bot_mv_frame reads it from global (L2)
+  for (int b = 0; b < KC_MV_NBLK; ++b) bp.mv_slot[b] = -1;  // not resident: bot_mv_frame reads it from global (L2)
   for (int b : order) {
+    if (b >= KC_MV_PAIR0 && !pairs) continue;
     if (sizeof(double) * (size_t)(off + 2 * KC_MV_N) + per * (size_t)(nres + 1) > smem_max) break;
     mask |= 1 << b;
     bp.mv_slot[b] = nres++;
@@ -679,7 +685,7 @@ int setup_frame_operators(kc_handle* h, const cudaDeviceProp& prop) {
     return KC_OK;  // keep the interpreter frames
   }
   h->mv_resident = mask;
-  h->mv_avail = 0x3F;
+  h->mv_avail = pairs ? (1 << KC_MV_NBLK) - 1 : (1 << KC_MV_PAIR0) - 1;
   h->bot_smem = bytes;
   return KC_OK;
 }

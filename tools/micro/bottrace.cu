@@ -41,20 +41,20 @@ int main(int argc, char** argv) {
   b.deep0 = bp.deep0 != 0;
   bp.nu1 = 2; bp.nu2 = 2; bp.nstrip = nstrip; bot_geometry(bp, m0, cs);
   if (mv) {
-    double* mats; cudaMalloc(&mats, sizeof(double) * 6 * KC_MV_N * KC_MV_LD);
-    cudaMemset(mats, 0, sizeof(double) * 6 * KC_MV_N * KC_MV_LD);
-    const int R = (KC_MV_N + cs - 1) / cs, order[5] = {1, 3, 0, 5, 2};
+    double* mats; cudaMalloc(&mats, sizeof(double) * KC_MV_NBLK * KC_MV_N * KC_MV_LD);
+    cudaMemset(mats, 0, sizeof(double) * KC_MV_NBLK * KC_MV_N * KC_MV_LD);
+    const int R = (KC_MV_N + cs - 1) / cs, order[5] = {1, KC_MV_PAIR0, KC_MV_PAIR0 + 1, KC_MV_PAIR0 + 2, 3};
     bp.mv_mats = mats; bp.mv_rows = R; bp.mv_off = (bp.total + 1) & ~1;
     const int nres = bp.deep0 ? 4 : 5;  // the deeper 127^2 strips leave room for 4 blocks
-    for (int i = 0; i < 6; ++i) bp.mv_slot[i] = -1;  // the others are read from global memory
+    for (int i = 0; i < KC_MV_NBLK; ++i) bp.mv_slot[i] = -1;  // the others are read from global memory
     for (int i = 0; i < nres; ++i) bp.mv_slot[order[i]] = i;
-    b.mv_mask = 0x3F;
-    bp.mv_avail = 0x3F;
+    b.mv_mask = (1u << KC_MV_NBLK) - 1;
+    bp.mv_avail = (1 << KC_MV_NBLK) - 1;
 
   }
   b.top(kappa, kappa > 1 ? kappa - 1 : 0);
   bp.mv_copy = (int)b.mv_used;
-  if (mv) for (int i = 0; i < 6; ++i) if (bp.mv_slot[i] < 0) bp.mv_copy &= ~(1 << i);
+  if (mv) for (int i = 0; i < KC_MV_NBLK; ++i) if (bp.mv_slot[i] < 0) bp.mv_copy &= ~(1 << i);
   unsigned* ds; cudaMalloc(&ds, b.out.size() * 4);
   cudaMemcpy(ds, b.out.data(), b.out.size() * 4, cudaMemcpyHostToDevice);
   bp.gv = gv; bp.gf = gf; bp.gP = P; bp.v_zero = 1; bp.sched = ds; bp.nsched = (int)b.out.size(); bp.final_cur = b.cur & 1;
