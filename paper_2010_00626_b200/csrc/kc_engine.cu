@@ -136,6 +136,7 @@ struct kc_handle {
   bool pdl = true;            // programmatic dependent launch around the bottom kernel (KC_PDL=0: off)
   bool postpre = true;        // fused sibling post+pre passes on the column-tile levels (KC_POSTPRE=0: off)
   int zebra_few = 256;        // KZ_FEW: most lines per half-sweep for the one-line-per-block kernel
+  int ctile_small_m = 255;    // column-tile pre passes with half-height tiles up to this side (KC_CTILE_SMALL_M)
   // the streaming k_postpre on 1023^2 and up (KC_POSTPRE_STREAM=1: on): bit-exact,
   // but as slow as the two passes it replaces (2047^2: 57 vs 32 + 27 us;
   // these passes are issue-bound, not traffic-bound), so off by default
@@ -909,10 +910,15 @@ int ex_ctile_pre(kc_handle* h, int l) {
   p.Pc = C.P;
   p.s = L.st;
   p.tiles_x = (L.m + KC_CT_TX - 1) / KC_CT_TX;
-  const int tiles = p.tiles_x * ((L.m + KC_CTILE_TY - 1) / KC_CTILE_TY);
   const int nu = h->nu1;
   const bool z = L.vzero;
-  auto fn = nu == 0 ? (z ? k_ctile_pre<0, true, KC_CTILE_TY> : k_ctile_pre<0, false, KC_CTILE_TY>)
+  // small levels: half-height tiles, so the grid covers the SMs (255^2: 88
+  // tiles of 32 rows on 148 SMs; KC_CTILE_SMALL_M=0: off)
+  const bool small = L.m <= h->ctile_small_m && nu == 2;
+  const int ty = small ? KC_CTILE_TY / 2 : KC_CTILE_TY;
+  const int tiles = p.tiles_x * ((L.m + ty - 1) / ty);
+  auto fn = small ? (z ? k_ctile_pre<2, true, KC_CTILE_TY / 2> : k_ctile_pre<2, false, KC_CTILE_TY / 2>)
+          : nu == 0 ? (z ? k_ctile_pre<0, true, KC_CTILE_TY> : k_ctile_pre<0, false, KC_CTILE_TY>)
           : nu == 1 ? (z ? k_ctile_pre<1, true, KC_CTILE_TY> : k_ctile_pre<1, false, KC_CTILE_TY>)
                     : (z ? k_ctile_pre<2, true, KC_CTILE_TY> : k_ctile_pre<2, false, KC_CTILE_TY>);
   fn<<<tiles, KC_CT_NW * 32, 0, h->stream>>>(p);
@@ -1543,6 +1549,8 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
   {
     const char* penv = getenv("KC_PDL");
     h->pdl = !(penv && penv[0] == '0');
+    const char* csmenv = getenv("KC_CTILE_SMALL_M");
+    if (csmenv) h->ctile_small_m = atoi(csmenv);
     const char* zfenv = getenv("KC_ZEBRA_FEW");
     if (zfenv) h->zebra_few = atoi(zfenv);
     const char* ppenv = getenv("KC_POSTPRE");
