@@ -137,6 +137,7 @@ struct kc_handle {
   bool postpre = true;        // fused sibling post+pre passes on the column-tile levels (KC_POSTPRE=0: off)
   int zebra_few = 256;        // KZ_FEW: most lines per half-sweep for the one-line-per-block kernel
   int ctile_small_m = 255;    // column-tile pre passes with half-height tiles up to this side (KC_CTILE_SMALL_M)
+  int ctile_post_small_m = 255;  // ... post passes (KC_CTILE_POST_SMALL_M)
   // the streaming k_postpre on 1023^2 and up (KC_POSTPRE_STREAM=1: on): bit-exact,
   // but as slow as the two passes it replaces (2047^2: 57 vs 32 + 27 us;
   // these passes are issue-bound, not traffic-bound), so off by default
@@ -959,11 +960,15 @@ int ex_ctile_post(kc_handle* h, int l) {
   p.Pc = C.P;
   p.s = L.st;
   p.tiles_x = (L.m + KC_CT_TX - 1) / KC_CT_TX;
-  const int tiles = p.tiles_x * ((L.m + KC_CTILE_POST_TY - 1) / KC_CTILE_POST_TY);
   const bool z = L.vzero;
+  // small levels: half-height tiles (KC_CTILE_POST_SMALL_M)
+  const bool small = L.m <= h->ctile_post_small_m && h->nu2 == 2;
+  const int ty = small ? KC_CTILE_POST_TY / 2 : KC_CTILE_POST_TY;
+  const int tiles = p.tiles_x * ((L.m + ty - 1) / ty);
 #define KCT_POST(N) (z ? k_ctile_post<N, true, KC_CTILE_POST_TY> : k_ctile_post<N, false, KC_CTILE_POST_TY>)
   void (*fn)(TileParams) = nullptr;
-  switch (h->nu2) {
+  if (small) fn = z ? k_ctile_post<2, true, KC_CTILE_POST_TY / 2> : k_ctile_post<2, false, KC_CTILE_POST_TY / 2>;
+  else switch (h->nu2) {
     case 0: fn = KCT_POST(0); break;
     case 1: fn = KCT_POST(1); break;
     case 2: fn = KCT_POST(2); break;
@@ -1551,6 +1556,8 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
     h->pdl = !(penv && penv[0] == '0');
     const char* csmenv = getenv("KC_CTILE_SMALL_M");
     if (csmenv) h->ctile_small_m = atoi(csmenv);
+    const char* cpsenv = getenv("KC_CTILE_POST_SMALL_M");
+    if (cpsenv) h->ctile_post_small_m = atoi(cpsenv);
     const char* zfenv = getenv("KC_ZEBRA_FEW");
     if (zfenv) h->zebra_few = atoi(zfenv);
     const char* ppenv = getenv("KC_POSTPRE");
