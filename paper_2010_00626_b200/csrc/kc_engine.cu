@@ -893,7 +893,10 @@ int ex_tile(kc_handle* h, int l, bool pre) {
 
 // the same pre pass on column tiles (k_ctile_pre, nu1 <= 2)
 #ifndef KC_CTILE_MAX_M
-#define KC_CTILE_MAX_M 1023  // measured faster than the streaming pass up to here (tools/micro/midlev.cu)
+// column tiles measured faster than the streaming pre pass up to here; the
+// FMA build's trimmed streaming pass now wins at 1023^2 (n=12 kappa=3 cycle
+// 0.829 -> 0.823 ms, kappa=2 0.516 -> 0.512 ms; exact build: neutral)
+#define KC_CTILE_MAX_M (KC_FAST ? 511 : 1023)
 #endif
 #define KC_CTILE_TY 32
 int ex_ctile_pre(kc_handle* h, int l) {
