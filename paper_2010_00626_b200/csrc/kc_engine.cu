@@ -1453,9 +1453,20 @@ int get_solve_graph(kc_handle* h, int kappa, SolveGraph** out) {
     const bool fused_check = !(cenv && cenv[0] == '0');
     h->loop_ck = LoopCheck{h_loop, h_none, set_rest, st};
     h->loop_ck_on = fused_check;
-    if (rc == KC_OK) rc = ex_op(h, ops[0]);
+    // KC_LOOP_PROBE=1 (loop-overhead measurement only, tools/probe_loop.py):
+    // the plain pre pass, no norms, a separate check on stale norms
+    const char* lpenv = getenv("KC_LOOP_PROBE");
+    const bool probe = lpenv && lpenv[0] == '1';
+    if (probe) {
+      Op plain = ops[0];
+      plain.b = 0;
+      h->loop_ck_on = false;
+      if (rc == KC_OK) rc = ex_op(h, plain);
+    } else if (rc == KC_OK) {
+      rc = ex_op(h, ops[0]);
+    }
     h->loop_ck_on = false;
-    if (rc == KC_OK && !fused_check) {
+    if (rc == KC_OK && (!fused_check || probe)) {
       k_stop_check<<<1, 32, 0, h->stream>>>(h_loop, h_none, set_rest, st, scal);
       if (cudaGetLastError() != cudaSuccess) rc = KC_ECUDA;
     }

@@ -257,8 +257,8 @@ __global__ void __launch_bounds__(128, KS_MINB) k_pre(const StreamParams p) {
     // NORMS: rows owned by this chunk, interior columns owned by this lane;
     // the input's residual is the first stage's f - A u at row yin - 1
     const int y1 = yin - 1;
-    const bool own_e = NORMS && own_lane && yin >= 2 * Q0 && yin < 2 * Qe && yin < g_rows;
-    const bool own_r = NORMS && own_lane && y1 >= 2 * Q0 && y1 < 2 * Qe && y1 >= 0 && y1 < g_rows;
+    const bool own_e = NORMS && in_rng(yin, ya, yb);
+    const bool own_r = NORMS && in_rng(y1, ya, yb);
     if (own_e) acc_e = fma(u0.y, u0.y, fma(u0.x, u0.x, acc_e));
     double2 nw[D + 1];
     nw[0] = u0;
