@@ -215,7 +215,9 @@ __global__ void __launch_bounds__(128, KS_MINB) k_pre(const StreamParams p) {
   const int ys = 2 * Q0 - D;
   const int ye = 2 * Qe + D;  // inclusive: residual row 2 Qe
   // only warps touching the domain boundary need masks / row clamping
-  const bool edge = XS < 0 || XS + KS_BAND - 1 >= m || g_y0 + ys - D - 1 < 0 || g_y0 + ye + 1 >= g_mg;
+  // (a warp vote: the compiler then knows the branches on it are uniform)
+  const bool edge = __any_sync(0xffffffffu, XS < 0 || XS + KS_BAND - 1 >= m || g_y0 + ys - D - 1 < 0 ||
+                                                g_y0 + ye + 1 >= g_mg);
   // rows outside the buffer read its edge rows (the all-zero ghost rows of a
   // whole level): branch-free
   auto rp = [&](int y) -> size_t { return kc_idx(P, min(max(y, -g_hb), g_rows + g_hb - 1), c0); };
@@ -351,7 +353,8 @@ __global__ void __launch_bounds__(128, KS_MINB) k_post(const StreamParams p) {
     for (int t = 0; t <= DD; ++t) A[t].b = A[t].c = A[t].cen = make_double2(0.0, 0.0);
     const int ys = 2 * Q0 - D;
     const int ye = 2 * Qe - 1 + D;
-    const bool edge = XS < 0 || XS + KS_BAND - 1 >= m || g_y0 + ys - D - 2 < 0 || g_y0 + ye + 2 >= g_mg;
+    const bool edge = __any_sync(0xffffffffu, XS < 0 || XS + KS_BAND - 1 >= m || g_y0 + ys - D - 2 < 0 ||
+                                                  g_y0 + ye + 2 >= g_mg);
     auto rp = [&](int y) -> size_t { return kc_idx(P, min(max(y, -g_hb), g_rows + g_hb - 1), c0); };
     auto ldc = [&](int q) -> double {
       return __ldg(p.vc + kc_idx(p.Pc, min(max(q, -g_hbc), g_mcr + g_hbc - 1), pc));
@@ -470,7 +473,7 @@ __global__ void __launch_bounds__(128, KS_MINB_PP) k_postpre(const StreamParams 
   double RE[3] = {0.0, 0.0, 0.0};
   const int ys = 2 * Q0 - D;
   const int ye = 2 * Q0 + 2 * p.nq + D;  // inclusive: residual row 2 (Q0 + nq)
-  const bool edge = XS < 0 || XS + KS_BAND - 1 >= m || ys - D - 2 < 0 || ye + 2 >= m;
+  const bool edge = __any_sync(0xffffffffu, XS < 0 || XS + KS_BAND - 1 >= m || ys - D - 2 < 0 || ye + 2 >= m);
   auto rp = [&](int y) -> size_t { return kc_idx(P, min(max(y, -1), m), c0); };
   auto ldc = [&](int q) -> double { return __ldg(p.vc + kc_idx(p.Pc, min(max(q, -1), p.mc), pcol)); };
   int qcur = ys >> 1;  // arithmetic shift: floor
