@@ -423,6 +423,24 @@ def run_ours_distributed(args, rank: int, world: int, local_rank: int):
                          f"(unknowns {m}^2 / 4095^2) x {cycles} cycles (this run's count, which equals the "
                          f"reference's wherever goldens exist) -- extrapolated", "cpu": cpu_model()}
 
+    # context for the driver's scaling numbers (the N = 1 bench line is config
+    # C2): the single-GPU engine on this same problem and kappa, on rank 0's
+    # GPU while the other ranks wait
+    single = None
+    if not args.quick and (world > 1 or os.environ.get("KC_BENCH_SINGLE_REF") == "1"):
+        if rank == 0:
+            cfg1 = kc.CycleConfig(n=n, kappa=kap(best))
+            st1 = kc.build_state(problem, cfg1, arith=arith)
+            st1.v[0] = v0
+            st1.snapshot()
+            st1.solve_device(kap(best), "residual", args.target, 20000)  # warm + graph capture
+            st1.restore()
+            it1, status1, dms1, _, _ = st1.solve_device(kap(best), "residual", args.target, 20000)
+            single = {"ms": dms1, "cycles": it1, "status": status1, "kappa": best, "arith": arith,
+                      "note": "the single-GPU engine (kc_solve) on this config, rank 0's GPU, same run"}
+            st1.close()
+        dist.barrier()
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
@@ -439,6 +457,7 @@ def run_ours_distributed(args, rank: int, world: int, local_rank: int):
             "e2e": {"value": te, "unit": "ms", "h2d_bytes_per_step": 8 * m * m,
                     "d2h_bytes_per_step": 8 * m * m, "host_wall_ms": host_wall},
             "gpu_launches": None if launches is None else launches * args.steps,
+            "single_gpu_same_config": single,
             "clocks": clk.summary(), "status": rep["status"], "sweep": sweep, "pcg": pcg,
             "solution_checksum": float(np.sum(sol)), "graph_fallback": s.graph_fallback,
         }
