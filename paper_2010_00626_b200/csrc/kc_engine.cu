@@ -2263,8 +2263,8 @@ int get_pcg_graph(kc_handle* h, int kappa, bool mx, SolveGraph** out) {
   SolveGraph sg;
   // A: Ap, pAp, x/r update, measure
   KC_CUDA(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-  k_pcg_apply_dot<<<grid2(m, m, KC_RY), kBlock, 0, h->stream>>>(h->p, h->ap, m, P, L0.st, h->d_pcgpart);
-  k_red_final<false><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_pcgpart, KC_PCG_BLOCKS(m), h->d_scal + S_PAP);
+  k_pcg_apply_dot2<<<grid2((m + 1) / 2, m, KC_RY), kBlock, 0, h->stream>>>(h->p, h->ap, m, P, L0.st, h->d_pcgpart);
+  k_red_final<false><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_pcgpart, KC_PCG_BLOCKS2(m), h->d_scal + S_PAP);
   if (mx)
     k_pcg_update_xr<true><<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(h->x, r, h->p, h->ap, m, P, h->d_scal, S_RZ,
                                                                             S_PAP, h->d_part, st);
@@ -2409,9 +2409,10 @@ extern "C" int kc_pcg(kc_handle* h, int kappa, const double* f, const double* x0
       st = KC_STATUS_BREAKDOWN;
     } else {
       for (it = 1; it <= max_it; ++it) {
-        k_pcg_apply_dot<<<grid2(m, m, KC_RY), kBlock, 0, h->stream>>>(h->p, h->ap, m, P, L0.st, h->d_pcgpart);
+        k_pcg_apply_dot2<<<grid2((m + 1) / 2, m, KC_RY), kBlock, 0, h->stream>>>(h->p, h->ap, m, P, L0.st,
+                                                                              h->d_pcgpart);
         KC_LAUNCH_CHECK(h);
-        k_red_final<false><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_pcgpart, KC_PCG_BLOCKS(m), h->d_scal + S_PAP);
+        k_red_final<false><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_pcgpart, KC_PCG_BLOCKS2(m), h->d_scal + S_PAP);
         KC_LAUNCH_CHECK(h);
         if (mx)
           k_pcg_update_xr<true><<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(h->x, r, h->p, h->ap, m, P, h->d_scal,

@@ -64,6 +64,58 @@ __global__ void __launch_bounds__(KC_BX* KC_BY)
   }
 }
 
+// The same with two columns per thread: one 16-byte load of the row pair
+// plus its two outer neighbours per row (3 loads per 2 outputs instead of 3
+// per output; the one-column kernel reached ~0.53 of HBM peak, ncu host-loop
+// capture, tools/ncu_pcg.py host).  Per-point arithmetic unchanged.
+#define KC_PCG_BLOCKS2(m) (((m) + 2 * KC_BX - 1) / (2 * KC_BX) * (((m) + KC_BY * KC_RY - 1) / (KC_BY * KC_RY)))
+__global__ void __launch_bounds__(KC_BX* KC_BY)
+    k_pcg_apply_dot2(const double* __restrict__ p, double* __restrict__ ap, int m, int P, St9 s,
+                     double* __restrict__ part) {
+  const int x0 = 2 * (blockIdx.x * KC_BX + threadIdx.x);
+  const int y0 = (blockIdx.y * KC_BY + threadIdx.y) * KC_RY;
+  double acc = 0.0;
+  if (x0 < m && y0 < m) {
+    const double* pu = p + kc_idx(P, y0, x0);  // 16-byte aligned: P, KC_OX and x0 even
+    auto row = [&](const double* q, double& l, double2& c, double& r) {
+      c = __ldg(reinterpret_cast<const double2*>(q));
+      l = __ldg(q - 1);
+      r = __ldg(q + 2);
+    };
+    double al, ar, bl, br;
+    double2 ac, bc;
+    row(pu - P, al, ac, ar);
+    row(pu, bl, bc, br);
+    const bool two = x0 + 1 < m;
+#pragma unroll
+    for (int k = 0; k < KC_RY; ++k) {
+      if (y0 + k >= m) break;
+      double cl, cr;
+      double2 cc;
+      row(pu + (size_t)(k + 1) * P, cl, cc, cr);
+      const double a0 = kc_sum9(s, al, ac.x, ac.y, bl, bc.x, bc.y, cl, cc.x, cc.y);
+      const double a1 = kc_sum9(s, ac.x, ac.y, ar, bc.x, bc.y, br, cc.x, cc.y, cr);
+      double* o = ap + kc_idx(P, y0 + k, x0);
+      if (two) *reinterpret_cast<double2*>(o) = make_double2(a0, a1);
+      else o[0] = a0;
+      acc = fma(bc.x, a0, acc);
+      if (two) acc = fma(bc.y, a1, acc);
+      al = bl; ac = bc; ar = br;
+      bl = cl; bc = cc; br = cr;
+    }
+  }
+  __shared__ double sh[KC_BX * KC_BY / 32];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  const int t = threadIdx.y * KC_BX + threadIdx.x;
+  if ((t & 31) == 0) sh[t >> 5] = acc;
+  __syncthreads();
+  if (t == 0) {
+    double b = 0.0;
+    for (int w = 0; w < KC_BX * KC_BY / 32; ++w) b += sh[w];
+    part[blockIdx.y * gridDim.x + blockIdx.x] = b;
+  }
+}
+
 // Device-resident PCG loop state (kc_engine.cu get_pcg_graph): iterations
 // completed, limits, outcome, history of the stopping measure.
 struct PcgState {
