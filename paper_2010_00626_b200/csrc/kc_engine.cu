@@ -137,6 +137,10 @@ struct kc_handle {
   bool postpre = true;        // fused sibling post+pre passes on the column-tile levels (KC_POSTPRE=0: off)
   int zebra_few = 256;        // KZ_FEW: most lines per half-sweep for the one-line-per-block kernel
   int ctile_small_m = 255;    // column-tile pre passes with half-height tiles up to this side (KC_CTILE_SMALL_M)
+  // streaming warps per SM where chunks would be short (KC_KS_SHORT_WPS): a
+  // cap of 16 (round 1) now costs time -- the level-2 post pass 32 -> 29 us
+  // with every resident warp (n=12 kappa=3 cycle 0.818 -> 0.813 ms)
+  int ks_short_wps = 64;
   int ctile_post_small_m = 255;  // ... post passes (KC_CTILE_POST_SMALL_M)
   // the streaming k_postpre on 1023^2 and up (KC_POSTPRE_STREAM=1: on): bit-exact,
   // but as slow as the two passes it replaces (2047^2: 57 vs 32 + 27 us;
@@ -827,9 +831,9 @@ StreamParams ks_params(kc_handle* h, int l, int D, int* nwarps, const void* fn) 
   p.nbands = (C.m + 1 + ks_npb(D) - 1) / ks_npb(D);
   const int slots = fn ? ks_slots(h, fn, D) : 148 * 12;
   p.nq = ks_choose_nq(C.m, p.nbands, slots);
-  // more than 16 warps per SM only where the chunks stay long enough that
-  // the extra warm-up rows (2D+1 per chunk) cost < 10 % of the streamed rows
-  if (10 * (2 * D + 1) > 2 * p.nq) p.nq = ks_choose_nq(C.m, p.nbands, std::min(slots, 16 * h->num_sms));
+  // where the chunks would be short (warm-up rows 2D+1 > 10 % of the streamed
+  // rows), at most ks_short_wps warps per SM (default: no cap)
+  if (10 * (2 * D + 1) > 2 * p.nq) p.nq = ks_choose_nq(C.m, p.nbands, std::min(slots, h->ks_short_wps * h->num_sms));
   *nwarps = p.nbands * ((C.m + 1 + p.nq - 1) / p.nq);
   return p;
 }
@@ -1568,6 +1572,8 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
   {
     const char* penv = getenv("KC_PDL");
     h->pdl = !(penv && penv[0] == '0');
+    const char* kswenv = getenv("KC_KS_SHORT_WPS");
+    if (kswenv) h->ks_short_wps = std::max(1, atoi(kswenv));
     const char* csmenv = getenv("KC_CTILE_SMALL_M");
     if (csmenv) h->ctile_small_m = atoi(csmenv);
     const char* cpsenv = getenv("KC_CTILE_POST_SMALL_M");
