@@ -1119,6 +1119,34 @@ struct BotDeep {
       fn(lo + yy, i - yy * M);
     }
   }
+  // a Jacobi sweep (JAC) or the residual on rows lo..hi (clipped): items of
+  // two rows sharing their loads (12 instead of 18 per pair), the per-point
+  // arithmetic of kc_apply9 / kc_jacobi_pt
+  template <int M, bool JAC>
+  __device__ __forceinline__ void stencil2(int a, int lo, int hi, const double* __restrict__ u, double* __restrict__ o,
+                                           const double* __restrict__ f, const St9& st) const {
+    constexpr int S = M + 2;
+    lo = max(lo, -a);
+    hi = min(hi, M - 1 - a);
+    const int n = ((hi - lo + 2) >> 1) * M;
+    for (int it = tid; it < n; it += KC_BOT_THREADS) {
+      const int yy = it / M, x = it - yy * M, y = lo + 2 * yy;
+      const bool two = y + 1 <= hi;
+      const int i = y * S + x;
+      const double* q = u + i;
+      double r[4][3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) r[k][dx] = q[(k - 1) * S + dx - 1];
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) r[3][dx] = two ? q[2 * S + dx - 1] : 0.0;
+      const double a0 = kc_sum9(st, r[0][0], r[0][1], r[0][2], r[1][0], r[1][1], r[1][2], r[2][0], r[2][1], r[2][2]);
+      const double a1 = kc_sum9(st, r[1][0], r[1][1], r[1][2], r[2][0], r[2][1], r[2][2], r[3][0], r[3][1], r[3][2]);
+      o[i] = JAC ? kc_jacobi_pt(r[1][1], f[i], a0, st.c) : DSUB(f[i], a0);
+      if (two) o[i + S] = JAC ? kc_jacobi_pt(r[2][1], f[i + S], a1, st.c) : DSUB(f[i + S], a1);
+    }
+  }
   // own rows ylo..yhi into the neighbours' halo rows: rows y < HB to the
   // upper one (its row R + y), rows y >= R - HB to the lower one (row y - R)
   template <int M>
@@ -1158,23 +1186,14 @@ struct BotDeep {
       clu_sync();
       push_rows<M>(u, a, 0, R - 1);
       clu_sync();
-      rows_do<M>(a, -3, R + 2, [&](int y, int x) {
-        const int i = y * S + x;
-        w[i] = kc_jacobi_pt(u[i], f[i], kc_apply9(u + i, S, st), st.c);
-      });
+      stencil2<M, true>(a, -3, R + 2, u, w, f, st);
       bot_bar();
-      rows_do<M>(a, -2, R + 1, [&](int y, int x) {
-        const int i = y * S + x;
-        u[i] = kc_jacobi_pt(w[i], f[i], kc_apply9(w + i, S, st), st.c);
-      });
+      stencil2<M, true>(a, -2, R + 1, w, u, f, st);
       bot_bar();
       lo = -2;
     }
     // residual into the other buffer, restriction of the own coarse rows
-    rows_do<M>(a, -1, R, [&](int y, int x) {
-      const int i = y * S + x;
-      w[i] = DSUB(f[i], kc_apply9(u + i, S, st));
-    });
+    stencil2<M, false>(a, -1, R, u, w, f, st);
     bot_bar();
     {
       cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
@@ -1230,15 +1249,9 @@ struct BotDeep {
       });
     }
     bot_bar();
-    rows_do<M>(a, lo + 1, hi - 1, [&](int y, int x) {
-      const int i = y * S + x;
-      w[i] = kc_jacobi_pt(u[i], f[i], kc_apply9(u + i, S, st), st.c);
-    });
+    stencil2<M, true>(a, lo + 1, hi - 1, u, w, f, st);
     bot_bar();
-    rows_do<M>(a, lo + 2, hi - 2, [&](int y, int x) {
-      const int i = y * S + x;
-      u[i] = kc_jacobi_pt(w[i], f[i], kc_apply9(w + i, S, st), st.c);
-    });
+    stencil2<M, true>(a, lo + 2, hi - 2, w, u, f, st);
     bot_bar();
     if (np > 0) {  // after a barrier: the neighbours' post sweeps read their halo rows
       clu_sync();
@@ -1267,15 +1280,9 @@ struct BotDeep {
       });
     }
     bot_bar();
-    rows_do<M>(a, -1, R, [&](int y, int x) {
-      const int i = y * S + x;
-      w[i] = kc_jacobi_pt(u[i], f[i], kc_apply9(u + i, S, st), st.c);
-    });
+    stencil2<M, true>(a, -1, R, u, w, f, st);
     bot_bar();
-    rows_do<M>(a, 0, R - 1, [&](int y, int x) {
-      const int i = y * S + x;
-      u[i] = kc_jacobi_pt(w[i], f[i], kc_apply9(w + i, S, st), st.c);
-    });
+    stencil2<M, true>(a, 0, R - 1, w, u, f, st);
     bot_bar();
   }
   // PH_FRAME63 (top = false: the pair on level d63, v in buffer cur) or
