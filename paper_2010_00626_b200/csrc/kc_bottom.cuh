@@ -1147,6 +1147,35 @@ struct BotDeep {
       if (two) o[i + S] = JAC ? kc_jacobi_pt(r[2][1], f[i + S], a1, st.c) : DSUB(f[i + S], a1);
     }
   }
+  // J2Z (two sweeps from the zero guess, bot_j2z_pt) on two-row items: the
+  // u1 = 0 + c f values of rows y-1 .. y+2 shared by both outputs
+  template <int M>
+  __device__ __forceinline__ void j2z2(int a, int lo, int hi, double* __restrict__ u, const double* __restrict__ f,
+                                       const St9& st) const {
+    constexpr int S = M + 2;
+    lo = max(lo, -a);
+    hi = min(hi, M - 1 - a);
+    const int n = ((hi - lo + 2) >> 1) * M;
+    for (int it = tid; it < n; it += KC_BOT_THREADS) {
+      const int yy = it / M, x = it - yy * M, y = lo + 2 * yy;
+      const bool two = y + 1 <= hi;
+      const int i = y * S + x;
+      const double* pf = f + i;
+      double n1[4][3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) n1[k][dx] = kc_jacobi_zero(pf[(k - 1) * S + dx - 1], st.c);
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) n1[3][dx] = two ? kc_jacobi_zero(pf[2 * S + dx - 1], st.c) : 0.0;
+      const double a0 =
+          kc_sum9(st, n1[0][0], n1[0][1], n1[0][2], n1[1][0], n1[1][1], n1[1][2], n1[2][0], n1[2][1], n1[2][2]);
+      const double a1 =
+          kc_sum9(st, n1[1][0], n1[1][1], n1[1][2], n1[2][0], n1[2][1], n1[2][2], n1[3][0], n1[3][1], n1[3][2]);
+      u[i] = kc_jacobi_pt(n1[1][1], pf[0], a0, st.c);
+      if (two) u[i + S] = kc_jacobi_pt(n1[2][1], pf[S], a1, st.c);
+    }
+  }
   // own rows ylo..yhi into the neighbours' halo rows: rows y < HB to the
   // upper one (its row R + y), rows y >= R - HB to the lower one (row y - R)
   template <int M>
@@ -1176,7 +1205,7 @@ struct BotDeep {
     double* w = buf(L, cur ^ 1);
     int lo;
     if (zero) {
-      rows_do<M>(a, -3, R + 2, [&](int y, int x) { u[y * S + x] = bot_j2z_pt(f + y * S + x, S, st); });
+      j2z2<M>(a, -3, R + 2, u, f, st);
       bot_bar();
       lo = -3;
     } else {
