@@ -1147,6 +1147,35 @@ struct BotDeep {
       if (two) o[i + S] = JAC ? kc_jacobi_pt(r[2][1], f[i + S], a1, st.c) : DSUB(f[i + S], a1);
     }
   }
+  // u += P vc on rows lo..hi (clipped) by coarse cells: cell (q, p) holds the
+  // fine points (2q|2q+1, 2p|2p+1) of global rows and reads the four coarse
+  // values they share (cp(q, p): coarse row q by its global index) -- no
+  // divergence on the column parity, 4 loads per 4 points; the arithmetic of
+  // kc_prolong_val (transfer.py:54-57)
+  template <int M, class CP>
+  __device__ __forceinline__ void prolong_cells(int a, int lo, int hi, double* __restrict__ u, CP cp) const {
+    constexpr int S = M + 2, NC = (M + 1) / 2;
+    lo = max(lo, -a);
+    hi = min(hi, M - 1 - a);
+    const int q0 = (a + lo) >> 1, q1 = (a + hi) >> 1;
+    const int n = (q1 - q0 + 1) * NC;
+    for (int it = tid; it < n; it += KC_BOT_THREADS) {
+      const int qq = it / NC, pc = it - qq * NC, q = q0 + qq;
+      const double c00 = cp(q - 1, pc - 1), c01 = cp(q - 1, pc), c10 = cp(q, pc - 1), c11 = cp(q, pc);
+      const int ly = 2 * q - a, x = 2 * pc;
+      const bool xo = x + 1 < M;
+      if (ly >= lo && ly <= hi) {  // fine row 2q
+        double* pu = u + ly * S + x;
+        pu[0] = DADD(pu[0], DMUL(0.25, DADD(DADD(DADD(c00, c01), c10), c11)));
+        if (xo) pu[1] = DADD(pu[1], DMUL(0.5, DADD(c01, c11)));
+      }
+      if (ly + 1 >= lo && ly + 1 <= hi) {  // fine row 2q + 1
+        double* pu = u + (ly + 1) * S + x;
+        pu[0] = DADD(pu[0], DMUL(0.5, DADD(c10, c11)));
+        if (xo) pu[1] = DADD(pu[1], c11);
+      }
+    }
+  }
   // J2Z (two sweeps from the zero guess, bot_j2z_pt) on two-row items: the
   // u1 = 0 + c f values of rows y-1 .. y+2 shared by both outputs
   template <int M>
@@ -1272,10 +1301,7 @@ struct BotDeep {
     {
       const double* vc = buf(lv[d + 1], c);
       auto cp = [&](int q, int pc) { return vc[q * SC + pc]; };
-      rows_do<M>(a, lo, hi, [&](int y, int x) {
-        const int i = y * S + x;
-        u[i] = DADD(u[i], kc_prolong_val(a + y, x, cp));
-      });
+      prolong_cells<M>(a, lo, hi, u, cp);
     }
     bot_bar();
     stencil2<M, true>(a, lo + 1, hi - 1, u, w, f, st);
@@ -1303,10 +1329,7 @@ struct BotDeep {
     {
       const double* vc = buf(lv[1], c) - (a / 2) * SC;  // indexed by the global coarse row
       auto cp = [&](int q, int pc) { return vc[q * SC + pc]; };
-      rows_do<M>(a, -2, R + 1, [&](int y, int x) {
-        const int i = y * S + x;
-        u[i] = DADD(u[i], kc_prolong_val(a + y, x, cp));
-      });
+      prolong_cells<M>(a, -2, R + 1, u, cp);
     }
     bot_bar();
     stencil2<M, true>(a, -1, R, u, w, f, st);
