@@ -9,8 +9,9 @@ data another warp or CTA has not finished writing would see it and change
 the result.  Bar: with jitter, the exact build's cycles stay bit-identical to
 the oracle (the reference's arithmetic) and the fast build's stay
 bit-identical to the same build without jitter, over repeated runs and the
-launch shapes the engine uses (16-CTA cluster with deep halos, without, and
-one CTA).
+launch shapes the engine uses (16-CTA cluster with deep halos on the 127^2
+entry and 63^2 strips (PH_FRAME127), on the 63^2 strips only (PH_FRAME63),
+without, and one CTA).
 """
 
 import hashlib
@@ -91,7 +92,8 @@ def _cases(arith, shapes, ns, kappas, reps=3, cycles=2):
     return out
 
 
-SHAPES = [("deep", {}), ("nodeep", {"KC_DEEP": "0"}), ("onecta", {"KC_BOT_CLUSTER": "0"})]
+SHAPES = [("deep", {}), ("deep63", {"KC_DEEP127": "0"}), ("nodeep", {"KC_DEEP": "0"}),
+          ("onecta", {"KC_BOT_CLUSTER": "0"})]
 
 
 def test_jitter_libraries_present_and_perturbing():
@@ -130,7 +132,7 @@ def test_exact_build_under_jitter_bit_exact_vs_oracle():
 
 
 def test_fast_build_under_jitter_equals_fast_build():
-    cases = _cases("fast", SHAPES[:2], [9, 12], [1, 2, 3, 12], reps=2)
+    cases = _cases("fast", SHAPES[:3], [9, 12], [1, 2, 3, 12], reps=2)
     cases = [c for c in cases if not (c["n"] == 9 and c["kappa"] == 12)]
     got = _run_jitter(cases)
     for c in cases:
