@@ -14,9 +14,10 @@
 // cycles, __syncthreads 47-115, __syncwarp 31, a bare 3x3 Jacobi phase ~340,
 // cluster barrier ~490 / ~940 with remote stores outstanding):
 //  * one control loop replays one phase descriptor per iteration at a single
-//    inlined site, so the kernel stays small; 384 threads per CTA leave 170
-//    registers per thread (the loop is register-bound: 512 threads spilled);
-//  * the warps that work on a level scale with its size: all 12 for sides
+//    inlined site, so the kernel stays small; 384 threads per CTA (exact
+//    build; 256 in the FMA build, see KC_BOT_THREADS) leave 170 registers
+//    per thread (the loop is register-bound: 512 threads spilled);
+//  * the warps that work on a level scale with its size: all for sides
 //    >= 31 (CTA or cluster barrier), 8 for 15 (named barrier), 1-2 for the
 //    smallest (__syncwarp / named barrier), and idle warps skip the phase;
 //    whole frames on sides <= 15 run as one descriptor (PH_TINY);
