@@ -158,6 +158,7 @@ struct kc_handle {
   std::string err;
   // PCG vectors (lazily allocated), finest padded layout
   double *x = nullptr, *p = nullptr, *ap = nullptr, *fb = nullptr;
+  double* p2 = nullptr;  // the device PCG loop alternates p between p and p2
   double* snap = nullptr;  // kc_snapshot copy of the finest v
 };
 
@@ -1811,6 +1812,7 @@ int kc_destroy(kc_handle* h) {
   }
   cudaFree(h->x);
   cudaFree(h->p);
+  cudaFree(h->p2);
   cudaFree(h->ap);
   cudaFree(h->fb);
   cudaFree(h->snap);
@@ -2196,7 +2198,7 @@ namespace {
 int ensure_pcg_buffers(kc_handle* h) {
   const size_t bytes = h->L[0].elems * sizeof(double);
   if (!h->d_pcgpart) KC_CUDA(h, cudaMalloc(&h->d_pcgpart, sizeof(double) * (size_t)KC_PCG_BLOCKS(h->L[0].m)));
-  double** bufs[4] = {&h->x, &h->p, &h->ap, &h->fb};
+  double** bufs[5] = {&h->x, &h->p, &h->ap, &h->fb, &h->p2};
   for (double** b : bufs) {
     if (*b) continue;
     cudaError_t ce = cudaMalloc(b, bytes);
@@ -2288,6 +2290,33 @@ int get_pcg_graph(kc_handle* h, int kappa, bool mx, SolveGraph** out) {
   if (ce != cudaSuccess) KC_FAIL(h, KC_ECUDA, "PCG capture: %s", cudaGetErrorString(ce));
   sg.kernels_pre = 4;
   sg.kernels_rest = g->kernels + 2;
+  // the body's tail fused with the next A (KC_PCG_FUSED=0: separate kernels):
+  // p_new = z + beta p_old and A p_new in one pass, p alternating between
+  // the two buffers, so the loop body holds two iterations (the second under
+  // an IF node the first check sets)
+  const char* pfenv = getenv("KC_PCG_FUSED");
+  const bool fused = !(pfenv && pfenv[0] == '0');
+  cudaGraph_t tail_a[2] = {nullptr, nullptr};
+  if (fused) {
+    for (int b = 0; b < 2; ++b) {
+      double* pin = b ? h->p2 : h->p;
+      double* pout = b ? h->p : h->p2;
+      KC_CUDA(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+      k_pcg_update_p_apply_dot2<<<grid2((m + 1) / 2, m, KC_RY), kBlock, 0, h->stream>>>(
+          z, pin, pout, h->ap, m, P, L0.st, h->d_scal, S_RZN, S_RZ, h->d_pcgpart);
+      k_copy_scalar<<<1, 32, 0, h->stream>>>(h->d_scal, S_RZ, S_RZN);
+      k_red_final<false><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_pcgpart, KC_PCG_BLOCKS2(m), h->d_scal + S_PAP);
+      if (mx)
+        k_pcg_update_xr<true><<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(h->x, r, pout, h->ap, m, P, h->d_scal,
+                                                                                S_RZ, S_PAP, h->d_part, st);
+      else
+        k_pcg_update_xr<false><<<KC_RED_BLOCKS, KC_RED_THREADS, 0, h->stream>>>(h->x, r, pout, h->ap, m, P,
+                                                                                 h->d_scal, S_RZ, S_PAP, h->d_part, st);
+      k_red_final<true><<<1, KC_RED_THREADS, 0, h->stream>>>(h->d_part, KC_RED_BLOCKS, h->d_scal + S_MEAS);
+      ce = cudaStreamEndCapture(h->stream, &tail_a[b]);
+      if (ce != cudaSuccess) KC_FAIL(h, KC_ECUDA, "PCG capture: %s", cudaGetErrorString(ce));
+    }
+  }
   // A ; check ; WHILE(go) { cycle ; tail ; A ; check } -- the sequence of
   // WHILE { A ; check ; IF(go) { cycle ; tail } } without the IF node
   cudaGraph_t cg = nullptr;
@@ -2313,6 +2342,36 @@ int get_pcg_graph(kc_handle* h, int kappa, bool mx, SolveGraph** out) {
   wp.conditional.size = 1;
   KC_CUDA(h, cudaGraphAddNode(&wn, cg, &chk0, 1, &wp));
   cudaGraph_t body = wp.conditional.phGraph_out[0];
+  if (fused) {
+    // WHILE { cycle ; tailA(p -> p2) ; check (also sets the IF) ;
+    //         IF(go) { cycle ; tailA(p2 -> p) ; check } }
+    cudaGraphConditionalHandle h_if;
+    KC_CUDA(h, cudaGraphConditionalHandleCreate(&h_if, body, 0, cudaGraphCondAssignDefault));
+    int set1 = 1;
+    void* args1[] = {&h_loop, &h_if, &set1, &st, &scal, &s_rz, &s_pap, &s_meas};
+    cudaKernelNodeParams kp1 = kp;
+    kp1.kernelParams = args1;
+    cudaGraphNode_t c1, t1, k1, ifn, c2, t2, k2;
+    KC_CUDA(h, cudaGraphAddChildGraphNode(&c1, body, nullptr, 0, g->graph));
+    KC_CUDA(h, cudaGraphAddChildGraphNode(&t1, body, &c1, 1, tail_a[0]));
+    KC_CUDA(h, cudaGraphAddKernelNode(&k1, body, &t1, 1, &kp1));
+    cudaGraphNodeParams ip{};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = h_if;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    KC_CUDA(h, cudaGraphAddNode(&ifn, body, &k1, 1, &ip));
+    cudaGraph_t ib = ip.conditional.phGraph_out[0];
+    KC_CUDA(h, cudaGraphAddChildGraphNode(&c2, ib, nullptr, 0, g->graph));
+    KC_CUDA(h, cudaGraphAddChildGraphNode(&t2, ib, &c2, 1, tail_a[1]));
+    KC_CUDA(h, cudaGraphAddKernelNode(&k2, ib, &t2, 1, &kp));
+    KC_CUDA(h, cudaGraphInstantiate(&sg.exec, cg, 0));
+    sg.graph = cg;
+    sg.end_cur0 = cur0;
+    auto ins = h->pcg_graphs.emplace(key, sg);
+    *out = &ins.first->second;
+    return KC_OK;
+  }
   cudaGraphNode_t cyc_node, tail_node, a_node, chk_node;
   KC_CUDA(h, cudaGraphAddChildGraphNode(&cyc_node, body, nullptr, 0, g->graph));
   KC_CUDA(h, cudaGraphAddChildGraphNode(&tail_node, body, &cyc_node, 1, sg.rest));

@@ -116,6 +116,72 @@ __global__ void __launch_bounds__(KC_BX* KC_BY)
   }
 }
 
+// p_new = z + beta p_old (krylov.py:126; beta = rz_next / rz, p unchanged
+// when rz_next <= 0 -- the loop stops there) fused with Ap and p.Ap of the
+// NEXT iteration (krylov.py:109-110): the stencil's p_new values around each
+// output are formed from z and p_old on the fly, so p_new is written to the
+// other p buffer (the graph alternates them) -- one pass over z, p_old,
+// p_new, Ap instead of two (k_pcg_update_p, k_pcg_apply_dot2).  Per-point
+// arithmetic unchanged.
+__global__ void __launch_bounds__(KC_BX* KC_BY)
+    k_pcg_update_p_apply_dot2(const double* __restrict__ z, const double* __restrict__ pold,
+                              double* __restrict__ pnew, double* __restrict__ ap, int m, int P, St9 s,
+                              const double* __restrict__ scal, int s_rz_next, int s_rz, double* __restrict__ part) {
+  const double rzn = scal[s_rz_next];
+  const bool upd = rzn > 0.0;
+  const double beta = upd ? __ddiv_rn(rzn, scal[s_rz]) : 0.0;
+  const int x0 = 2 * (blockIdx.x * KC_BX + threadIdx.x);
+  const int y0 = (blockIdx.y * KC_BY + threadIdx.y) * KC_RY;
+  double acc = 0.0;
+  if (x0 < m && y0 < m) {
+    const size_t o0 = kc_idx(P, y0, x0);
+    auto pv = [&](double zz, double pp) { return upd ? DADD(zz, DMUL(beta, pp)) : pp; };
+    auto row = [&](size_t o, double& l, double2& c, double& r) {
+      const double2 zc = __ldg(reinterpret_cast<const double2*>(z + o));
+      const double2 pc = __ldg(reinterpret_cast<const double2*>(pold + o));
+      c = make_double2(pv(zc.x, pc.x), pv(zc.y, pc.y));
+      l = pv(__ldg(z + o - 1), __ldg(pold + o - 1));
+      r = pv(__ldg(z + o + 2), __ldg(pold + o + 2));
+    };
+    double al, ar, bl, br;
+    double2 ac, bc;
+    row(o0 - P, al, ac, ar);
+    row(o0, bl, bc, br);
+    const bool two = x0 + 1 < m;
+#pragma unroll
+    for (int k = 0; k < KC_RY; ++k) {
+      if (y0 + k >= m) break;
+      double cl, cr;
+      double2 cc;
+      row(o0 + (size_t)(k + 1) * P, cl, cc, cr);
+      const double a0 = kc_sum9(s, al, ac.x, ac.y, bl, bc.x, bc.y, cl, cc.x, cc.y);
+      const double a1 = kc_sum9(s, ac.x, ac.y, ar, bc.x, bc.y, br, cc.x, cc.y, cr);
+      const size_t o = o0 + (size_t)k * P;
+      if (two) {
+        *reinterpret_cast<double2*>(ap + o) = make_double2(a0, a1);
+        *reinterpret_cast<double2*>(pnew + o) = bc;
+      } else {
+        ap[o] = a0;
+        pnew[o] = bc.x;
+      }
+      acc = fma(bc.x, a0, acc);
+      if (two) acc = fma(bc.y, a1, acc);
+      al = bl; ac = bc; ar = br;
+      bl = cl; bc = cc; br = cr;
+    }
+  }
+  __shared__ double sh[KC_BX * KC_BY / 32];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  const int t = threadIdx.y * KC_BX + threadIdx.x;
+  if ((t & 31) == 0) sh[t >> 5] = acc;
+  __syncthreads();
+  if (t == 0) {
+    double b = 0.0;
+    for (int w = 0; w < KC_BX * KC_BY / 32; ++w) b += sh[w];
+    part[blockIdx.y * gridDim.x + blockIdx.x] = b;
+  }
+}
+
 // Device-resident PCG loop state (kc_engine.cu get_pcg_graph): iterations
 // completed, limits, outcome, history of the stopping measure.
 struct PcgState {
