@@ -253,6 +253,18 @@ __device__ long long kc_bot_trace[KC_BOT_TRACE];
 __device__ int kc_bot_trace_op[KC_BOT_TRACE];
 __device__ int kc_bot_trace_n;
 __device__ long long kc_bot_trace_end[KC_BOT_TRACE];
+// sub-phase stamps inside the compiled frames (tools/micro/bottrace.cu):
+// CTA 0, thread 0, a code per point of BotDeep::run
+__device__ long long kc_bot_sub[KC_BOT_TRACE];
+__device__ int kc_bot_sub_code[KC_BOT_TRACE];
+__device__ int kc_bot_sub_n;
+#define KC_BOT_SUB(code)                                                      \
+  do {                                                                        \
+    if (threadIdx.x == 0 && blockIdx.x == 0 && kc_bot_sub_n < KC_BOT_TRACE) { \
+      kc_bot_sub[kc_bot_sub_n] = clock64();                                   \
+      kc_bot_sub_code[kc_bot_sub_n++] = (code);                               \
+    }                                                                         \
+  } while (0)
 __device__ unsigned long long kc_bot_stamp[8];  // globaltimer: start, init, entry, phases, end (CTA 0)
 __device__ __forceinline__ void kc_bot_mark(int k) {
   if (threadIdx.x == 0 && cooperative_groups::this_cluster().block_rank() == 0) {
@@ -264,6 +276,9 @@ __device__ __forceinline__ void kc_bot_mark(int k) {
 #define KC_BOT_MARK(k) kc_bot_mark(k)
 #else
 #define KC_BOT_MARK(k)
+#define KC_BOT_SUB(code) \
+  do {                   \
+  } while (0)
 #endif
 
 // Phase kinds (host-built list, BotBuilder below):
@@ -1345,18 +1360,24 @@ struct BotDeep {
   __device__ __forceinline__ void run(bool top, int d63, int kap, int cur) {
     const int ni = top ? (kap > 1 ? 2 : 1) : 1;
     for (int i = 0; i < ni; ++i) {
+      KC_BOT_SUB(1);
       if (top) pre<127>(0, cur, i == 0);
       const int k1 = top ? kap - i : kap;
       const int cur63 = top ? 0 : cur;
       const int nj = k1 > 1 ? 2 : 1;
       for (int j = 0; j < nj; ++j) {
         const bool zero = j == 0;
+        KC_BOT_SUB(2);
         const int lo = pre<63>(d63, cur63, zero);
+        KC_BOT_SUB(3);
         int c = 0, z = 1;  // the child's zero guess (cycle.py:214)
         for (int jj = 0; jj < (k1 - j > 1 ? 2 : 1); ++jj) f31->frame(d63 + 1, k1 - j - jj, c, z);
+        KC_BOT_SUB(4);
         post63(d63, cur63, c, lo, top ? (j == nj - 1 ? 2 : 0) : (zero ? 0 : 1));
       }
+      KC_BOT_SUB(5);
       if (top) post127(cur, cur63);
+      KC_BOT_SUB(6);
     }
   }
 };

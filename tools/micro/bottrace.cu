@@ -73,6 +73,7 @@ int main(int argc, char** argv) {
   int zero = 0;
   for (int rep = 0; rep < 2; ++rep) {
     cudaMemcpyToSymbol(kc_bot_trace_n, &zero, sizeof(int));
+    cudaMemcpyToSymbol(kc_bot_sub_n, &zero, sizeof(int));
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
     cudaLaunchKernelEx(&cfg, k_bottom, bp, m0);
@@ -120,5 +121,17 @@ int main(int argc, char** argv) {
     printf("  %-9s level %d (m=%3d): %5d phases, %7.0f cycles avg (thread 0 to its barrier %5.0f), %9.0f total\n", nm[o], d,
            bot_m(m0, d), cnt[o][d], sum[o][d] / cnt[o][d], cmp[o][d] / cnt[o][d], sum[o][d]);
   printf("phases traced: %d, total cycles %lld\n", n, n > 1 ? t[n - 1] - t[0] : 0);
+  {  // sub-phase stamps of the compiled deep frames: 1 pre127 | 2 ... pre63 | 3 frames31 | 4 post63 | 5 ... post127 | 6
+    int ns = 0;
+    cudaMemcpyFromSymbol(&ns, kc_bot_sub_n, sizeof(int));
+    std::vector<long long> ts(ns);
+    std::vector<int> cs(ns);
+    cudaMemcpyFromSymbol(ts.data(), kc_bot_sub, ns * 8);
+    cudaMemcpyFromSymbol(cs.data(), kc_bot_sub_code, ns * 4);
+    const char* what[7] = {"", "pre127", "pre63", "frames31", "post63", "post127", "end"};
+    double acc[7] = {};
+    for (int i = 0; i + 1 < ns; ++i) acc[cs[i]] += ts[i + 1] - ts[i];
+    for (int c = 1; c < 6; ++c) if (acc[c] > 0) printf("  deep frames: %-16s %8.0f cycles\n", what[c], acc[c]);
+  }
   return 0;
 }
