@@ -810,3 +810,32 @@ def test_fused_sibling_passes_bit_exact(stream_pp, kappa, monkeypatch):
         st.close()
     assert np.array_equal(out["1"], h.v[0])
     assert np.array_equal(out["0"], h.v[0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("eps,phi", [(1.0, 0.0), (1e-2, 30.0), (1e-5, 75.0), (0.5, 90.0)])
+@pytest.mark.parametrize("kappa", [2, 3])
+def test_other_problems_cycle_bit_exact_and_fast_close(eps, phi, kappa):
+    """Beyond the headline problem: other (epsilon, phi) -- isotropic, phi = 0
+    (the cross taps vanish: no all-products sharing), steep anisotropy -- one
+    n = 9 cycle through the fused passes, deep-halo frames and frame
+    operators: the exact build bit-identical to the oracle, the FMA build
+    within its bar."""
+    n = 9
+    m = 2 ** n - 1
+    rng = np.random.default_rng(int(1000 * eps) + int(phi) + kappa)
+    v0, f0 = rng.random((m, m)), rng.standard_normal((m, m))
+    h = O.Hierarchy(O.hierarchy(eps, phi, n))
+    h.v[0], h.f[0] = v0.copy(), f0.copy()
+    h.cycle(kappa)
+    cfg = CycleConfig(n=n, kappa=kappa)
+    for arith in ("exact", "fast"):
+        st = build_state(ProblemSpec(eps, phi), cfg, arith=arith)
+        st.v[0], st.f[0] = v0, f0
+        run_cycle(st, cfg, CycleStats.for_levels(n))
+        got = st.v[0]
+        if arith == "exact":
+            assert np.array_equal(got, h.v[0]), (eps, phi, kappa)
+        else:
+            assert np.max(np.abs(got - h.v[0])) <= 1e-12 * np.max(np.abs(h.v[0])), (eps, phi, kappa)
+        st.close()
