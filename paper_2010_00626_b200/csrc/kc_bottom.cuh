@@ -876,6 +876,18 @@ struct BotTiny {
   }
 };
 
+#ifndef KC_MV_TWO
+#define KC_MV_TWO 1
+#endif
+#ifndef KC_MV_ASYNC
+#define KC_MV_ASYNC 1
+#endif
+__device__ __forceinline__ unsigned bot_sa(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned bot_mapa(unsigned a, int rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
 // One frame operator phase on every CTA of the cluster: this CTA's rows
 // i in [rank * R, rank * R + R) of v' = A_k v + B_k f (the A part skipped on
 // a zero guess), inputs gathered from CTA 0's side-15 level, outputs stored
@@ -883,11 +895,13 @@ struct BotTiny {
 // still read); the caller ends the phase with a cluster barrier.
 // (bb, ba: the blocks applied to f and to v; bb = -1 selects B_kap / A_kap)
 __device__ __forceinline__ void bot_mv_frame(double* sm, const BotParams& bp, const BotLv& L, int src, int ob,
-                                             bool zero, int kap, int rank, int cs, int bb = -1, int ba = -1) {
+                                             bool zero, int kap, int rank, int cs, int bb = -1, int ba = -1,
+                                             unsigned long long* mvb = nullptr) {
   cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
   const int R = bp.mv_rows;
   asm volatile("cp.async.wait_all;" ::: "memory");  // the blocks (prologue copies)
   bot_bar();
+  KC_BOT_SUB(14);
   // this CTA's row slice of the blocks: in shared memory (resident), else
   // straight from global memory (2.4 MB for all six blocks: L2-resident)
   if (bb < 0) {
@@ -905,9 +919,63 @@ __device__ __forceinline__ void bot_mv_frame(double* sm, const BotParams& bp, co
     xf[i] = fin[o];
     if (!zero) xv[i] = vin[o];
   }
+  if (mvb && threadIdx.x == 0)  // this CTA's replica receives all KC_MV_N outputs of the phase
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bot_sa(mvb)), "r"(KC_MV_N * 8)
+                 : "memory");
   bot_bar();
+  KC_BOT_SUB(15);
   double* out = sm + (ob ? L.vo1 : L.vo0);
+  // lane l's row value into CTA l's replica: a DSMEM store, or (mvb) an
+  // st.async completing its bytes on CTA l's mbarrier
+  auto put = [&](double* p, int l, double v) {
+    if (!mvb) {
+      *cl.map_shared_rank(p, l) = v;
+      return;
+    }
+    const unsigned ra = bot_mapa(bot_sa(p), l), rb = bot_mapa(bot_sa(mvb), l);
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(ra), "d"(v),
+                 "r"(rb)
+                 : "memory");
+  };
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#if KC_MV_TWO
+  // two rows per warp pass (r, r + warps) with independent chains; their
+  // reductions share the shuffles: one exchange splits the lanes into a row-r
+  // half and a row-(r + warps) half, four more reduce within each half
+  auto rows = [&](const double* B, const double* A) {
+    for (int r = warp; r < R && i0 + r < KC_MV_N; r += 2 * KC_BOT_WARPS) {
+      const int r2 = r + KC_BOT_WARPS;
+      const bool two = r2 < R && i0 + r2 < KC_MV_N;
+      const double* br = B + r * KC_MV_LD;
+      const double* ar = A + r * KC_MV_LD;
+      const double* br2 = B + (two ? r2 : r) * KC_MV_LD;
+      const double* ar2 = A + (two ? r2 : r) * KC_MV_LD;
+      double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < (KC_MV_N + 31) / 32; ++k) {
+        const int j = lane + 32 * k;
+        if (j < KC_MV_N) {
+          const double x = xf[j];
+          a0 = fma(br[j], x, a0);
+          b0 = fma(br2[j], x, b0);
+          if (!zero) {
+            const double y = xv[j];
+            a1 = fma(ar[j], y, a1);
+            b1 = fma(ar2[j], y, b1);
+          }
+        }
+      }
+      const double va = a0 + a1, vb = b0 + b1;
+      const bool hi = lane >= 16;
+      double acc = (hi ? vb : va) + __shfl_xor_sync(0xffffffffu, hi ? va : vb, 16);
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      // lanes 0-15: row r, lanes 16-31: row r2; lane k & 15 stores into CTA k's replica
+      const int i = i0 + (hi ? r2 : r), y = i / KC_MV_M, x = i - y * KC_MV_M;
+      if ((lane & 15) < cs && (!hi || two)) put(out + y * L.S + x, lane & 15, acc);
+    }
+  };
+#else
   auto rows = [&](const double* B, const double* A) {
     for (int r = warp; r < R && i0 + r < KC_MV_N; r += KC_BOT_WARPS) {
       const double* br = B + r * KC_MV_LD;
@@ -930,9 +998,10 @@ __device__ __forceinline__ void bot_mv_frame(double* sm, const BotParams& bp, co
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       // every lane holds the row's value: lane k stores it into CTA k's replica
       const int i = i0 + r, y = i / KC_MV_M, x = i - y * KC_MV_M;
-      if (lane < cs) *cl.map_shared_rank(out + y * L.S + x, lane) = acc;
+      if (lane < cs) put(out + y * L.S + x, lane, acc);
     }
   };
+#endif
   // shared-memory loads where the blocks are resident (a pointer that may
   // be either would make every load a generic one)
   const int sb = bp.mv_slot[bb], sa = bp.mv_slot[ba];
@@ -940,6 +1009,21 @@ __device__ __forceinline__ void bot_mv_frame(double* sm, const BotParams& bp, co
     rows(sm + bp.mv_off + sb * R * KC_MV_LD, sm + bp.mv_off + (zero ? sb : sa) * R * KC_MV_LD);
   else
     rows(bp.mv_mats + ((size_t)bb * KC_MV_N + i0) * KC_MV_LD, bp.mv_mats + ((size_t)ba * KC_MV_N + i0) * KC_MV_LD);
+  KC_BOT_SUB(16);
+}
+// the end of an st.async frame-operator phase (bot_mv_frame with mvb): every
+// thread waits until all KC_MV_N outputs have landed in this CTA's replica
+// (phase parity ph of this mbarrier).  No cluster barrier: a CTA that passes
+// has every CTA's outputs, so every CTA is past its input reads; the next
+// phase writes the other buffer, into the other mbarrier.
+__device__ __forceinline__ void bot_mv_wait(unsigned long long* mvb, unsigned ph) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W%=:\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t@!p bra W%=;\n}" ::"r"(
+          bot_sa(mvb)),
+      "r"(ph)
+      : "memory");
+  bot_jitter();
 }
 
 // PH_FRAME31: a whole kappa_cycle frame on the replicated side-31 level --
@@ -960,6 +1044,21 @@ struct BotFrame31 {
   int* tiny_child;
   int mv_last;    // buffer the previous frame operator wrote (-1: none)
   bool mv_sync;   // an interpreter frame ran since the last frame operator
+  unsigned long long* mvbar;  // two mbarriers for the st.async frame-operator phases (KC_MV_ASYNC)
+  int mv_n;                   // st.async phases so far this launch (the same count on every CTA)
+  // one frame-operator phase and its completion: bot_mv_frame, then the
+  // cluster barrier, or (KC_MV_ASYNC) the wait on this CTA's mbarrier
+  __device__ __forceinline__ void mv(const BotLv& L, int src, int ob, bool zero, int kap, int bb = -1) {
+    if (KC_MV_ASYNC && cs > 1) {
+      unsigned long long* b = mvbar + (mv_n & 1);
+      bot_mv_frame(sm, *bp, L, src, ob, zero, kap, rank, cs, bb, -1, b);
+      bot_mv_wait(b, (mv_n >> 1) & 1);
+      ++mv_n;
+    } else {
+      bot_mv_frame(sm, *bp, L, src, ob, zero, kap, rank, cs, bb);
+      clu_sync();
+    }
+  }
   __device__ __forceinline__ double* buf(const BotLv& L, int b) const { return sm + (b ? L.vo1 : L.vo0); }
   __device__ __forceinline__ void stencil(bool jac, bool zero, const double* u, double* o, const double* f,
                                           const St9& st) const {
@@ -1012,8 +1111,7 @@ struct BotFrame31 {
       if (mv_sync) clu_sync();
       mv_sync = false;
       const int ob = z ? (mv_last >= 0 ? mv_last ^ 1 : c ^ 1) : c ^ 1;
-      bot_mv_frame(sm, *bp, lv[d], c, ob, z, k3, rank, cs);
-      clu_sync();
+      mv(lv[d], c, ob, z, k3);
       mv_last = ob;
       c = ob;
       z = 0;
@@ -1033,12 +1131,15 @@ struct BotFrame31 {
     const BotLv L = lv[d], C = lv[d + 1];
     const St9 st = tab[d];
     const int nu1 = bp->nu1, nu2 = bp->nu2;
+    KC_BOT_SUB(7);
     relax(L, st, nu1, cur, vz);
+    KC_BOT_SUB(8);
     const double* f = sm + L.fo;
     if (!vz) {
       stencil(false, false, buf(L, cur), buf(L, cur ^ 1), f, st);
       bot_bar();
     }
+    KC_BOT_SUB(9);
     {  // full weighting into the child's f (transfer.py:78-83)
       const double* r = vz ? f : buf(L, cur ^ 1);
       double* fc = sm + C.fo;
@@ -1051,14 +1152,14 @@ struct BotFrame31 {
       }
       bot_bar();
     }
+    KC_BOT_SUB(10);
     int c = 0, z = 1;  // the child's zero guess (cycle.py:214)
     if (KC_FAST && kap > 1 && ((bp->mv_avail >> kc_mv_pair(kap)) & 1)) {
       // both frames (kap, kap - 1) from the zero guess as one operator
       if (mv_sync) clu_sync();
       mv_sync = false;
       const int ob = mv_last >= 0 ? mv_last ^ 1 : c ^ 1;
-      bot_mv_frame(sm, *bp, lv[d + 1], c, ob, true, kap, rank, cs, kc_mv_pair(kap));
-      clu_sync();
+      mv(lv[d + 1], c, ob, true, kap, kc_mv_pair(kap));
       mv_last = ob;
       c = ob;
       z = 0;
@@ -1066,6 +1167,7 @@ struct BotFrame31 {
       frame15(d + 1, kap, c, z);
       if (kap > 1) frame15(d + 1, kap - 1, c, z);
     }
+    KC_BOT_SUB(11);
     {  // u += P vc, one coarse cell (2x2 fine points) per item (transfer.py:50-58)
       double* u = buf(L, cur);
       const double* vc = buf(C, c);
@@ -1084,8 +1186,10 @@ struct BotFrame31 {
       }
       bot_bar();
     }
+    KC_BOT_SUB(12);
     vz = 0;
     relax(L, st, nu2, cur, vz);
+    KC_BOT_SUB(13);
   }
 };
 
@@ -1385,11 +1489,12 @@ struct BotDeep {
 // The compile-time frames, out of line so that the interpreter loop of
 // k_bottom does not carry their registers: PH_FRAME31 (one call on the
 // replicated side-31 level) or PH_FRAME63 (the call pair on the deep-halo
-// side-63 strips).  mvs: the frame-operator bookkeeping (mv_last, mv_sync).
+// side-63 strips).  mvs: the frame-operator bookkeeping (mv_last, mv_sync,
+// mv_n); mvbar: the two mbarriers of the st.async frame-operator phases.
 __device__ __forceinline__ void bot_run_frame(int op, double* sm, const BotLv* lv, const St9* tab, const BotParams* bp,
                                            int d, int kap, int src, int zero, int rank, int cs, int nlev, int* slot,
-                                           int* tiny_child, int* mvs) {
-  BotFrame31 fr{sm, lv, tab, bp, (int)threadIdx.x, rank, cs, nlev, slot, tiny_child, mvs[0], mvs[1] != 0};
+                                           int* tiny_child, int* mvs, unsigned long long* mvbar) {
+  BotFrame31 fr{sm, lv, tab, bp, (int)threadIdx.x, rank, cs, nlev, slot, tiny_child, mvs[0], mvs[1] != 0, mvbar, mvs[2]};
   if (op == PH_FRAME63 || op == PH_FRAME127) {
     BotDeep dp{sm, lv, tab, &fr, (int)threadIdx.x, rank, cs};
     dp.run(op == PH_FRAME127, op == PH_FRAME127 ? 1 : d, kap, src);
@@ -1399,6 +1504,7 @@ __device__ __forceinline__ void bot_run_frame(int op, double* sm, const BotLv* l
   }
   mvs[0] = fr.mv_last;
   mvs[1] = fr.mv_sync ? 1 : 0;
+  mvs[2] = fr.mv_n;
 }
 
 // Columns of the side-15 frame operators: CTA (j, k - 1) runs BotTiny::frame
@@ -1452,8 +1558,14 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
   __shared__ BotLv lv[KC_BOT_MAXLEV];
   __shared__ unsigned sched[KC_BOT_MAXPH];
   __shared__ int tiny_child[2];
+  __shared__ alignas(8) unsigned long long mvbar[2];
   cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
   const int rank = (int)cl.block_rank(), cs = (int)cl.num_blocks();
+  if (KC_MV_ASYNC && threadIdx.x == 0) {  // published by the prologue's barrier
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bot_sa(&mvbar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bot_sa(&mvbar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   const int nlev = bp.nlev, nstrip = bp.nstrip;
   KC_BOT_MARK(0);
   // Prologue, ordered so the global latencies overlap: schedule and level
@@ -1595,6 +1707,7 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
   __shared__ int f31_slot;
   int mv_last = -1;      // frame-operator bookkeeping shared with PH_FRAME31 (BotBuilder mirrors it)
   bool mv_sync = false;
+  int mv_n = 0;
   unsigned e_next = bp.nsched > 0 ? sched[0] : 0u;
   for (int k = 0; k < bp.nsched; ++k) {
     const unsigned e = e_next;
@@ -1658,10 +1771,11 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
         vc += (L.a / 2) * C.S;
       bot_prolong(u, vc, L, C.m, C.S, zero, tid, nth, bot_push(u, L, strip, rank, cs));
     } else if (op == PH_FRAME63 || op == PH_FRAME31 || op == PH_FRAME127) {  // every thread of every CTA
-      int mvs[2] = {mv_last, mv_sync ? 1 : 0};
-      bot_run_frame(op, sm, lv, tab, &bp, d, BD_KAP(e), src, zero, rank, cs, nlev, &f31_slot, tiny_child, mvs);
+      int mvs[3] = {mv_last, mv_sync ? 1 : 0, mv_n};
+      bot_run_frame(op, sm, lv, tab, &bp, d, BD_KAP(e), src, zero, rank, cs, nlev, &f31_slot, tiny_child, mvs, mvbar);
       mv_last = mvs[0];
       mv_sync = mvs[1] != 0;
+      mv_n = mvs[2];
     } else if (KC_FAST && strip) {  // PH_TINY as a frame operator (all CTAs; FMA build only)
       bot_mv_frame(sm, bp, L, src, BD_CBUF(e), zero, BD_KAP(e), rank, cs);
       mv_last = BD_CBUF(e);

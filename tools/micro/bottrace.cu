@@ -128,10 +128,19 @@ int main(int argc, char** argv) {
     std::vector<int> cs(ns);
     cudaMemcpyFromSymbol(ts.data(), kc_bot_sub, ns * 8);
     cudaMemcpyFromSymbol(cs.data(), kc_bot_sub_code, ns * 4);
-    const char* what[7] = {"", "pre127", "pre63", "frames31", "post63", "post127", "end"};
-    double acc[7] = {};
-    for (int i = 0; i + 1 < ns; ++i) acc[cs[i]] += ts[i + 1] - ts[i];
-    for (int c = 1; c < 6; ++c) if (acc[c] > 0) printf("  deep frames: %-16s %8.0f cycles\n", what[c], acc[c]);
+    const char* what[17] = {"", "pre127", "pre63", "frames31", "post63", "post127", "end", "f31 pre-sweeps",
+                            "f31 residual", "f31 restrict", "f31 frame15", "f31 prolong", "f31 post-sweeps", "f31 end", "mv wait", "mv pack", "mv rows", };
+    double acc[17] = {};
+    int cnt[17] = {};
+    for (int i = 0; i + 1 < ns; ++i) {
+      acc[cs[i]] += ts[i + 1] - ts[i];
+      cnt[cs[i]]++;
+    }
+    // codes 3 (frames31) now include the stamps 7..13 inside: sum them back
+    for (int c = 7; c < 17; ++c) if (c != 13) acc[3] += acc[c];
+    for (int c = 1; c < 17; ++c)
+      if (acc[c] > 0 && c != 6) printf("  deep frames: %-16s %8.0f cycles in %d intervals (%.0f each)\n", what[c], acc[c],
+                                       cnt[c], acc[c] / (cnt[c] ? cnt[c] : 1));
   }
   return 0;
 }
