@@ -882,6 +882,9 @@ struct BotTiny {
 #ifndef KC_MV_ASYNC
 #define KC_MV_ASYNC 1
 #endif
+#ifndef KC_RB_ASYNC  // the 63^2 -> 31^2 restriction broadcast of the deep frames as st.async
+#define KC_RB_ASYNC 1
+#endif
 __device__ __forceinline__ unsigned bot_sa(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ unsigned bot_mapa(unsigned a, int rank) {
   unsigned r;
@@ -1046,6 +1049,7 @@ struct BotFrame31 {
   bool mv_sync;   // an interpreter frame ran since the last frame operator
   unsigned long long* mvbar;  // two mbarriers for the st.async frame-operator phases (KC_MV_ASYNC)
   int mv_n;                   // st.async phases so far this launch (the same count on every CTA)
+  int rb_n;                   // st.async restriction broadcasts into the 31^2 replicas so far (KC_RB_ASYNC)
   // one frame-operator phase and its completion: bot_mv_frame, then the
   // cluster barrier, or (KC_MV_ASYNC) the wait on this CTA's mbarrier
   __device__ __forceinline__ void mv(const BotLv& L, int src, int ob, bool zero, int kap, int bb = -1) {
@@ -1393,13 +1397,35 @@ struct BotDeep {
         }
       } else {  // every CTA's replica of the child, at this strip's first coarse row
         double* fc = fc0 + (a / 2) * SC;
+        unsigned long long* rb = f31->mvbar + 2;
+        if (KC_RB_ASYNC && tid == 0)  // this CTA's replica receives the whole MC x MC child f
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bot_sa(rb)), "r"(MC * MC * 8)
+                       : "memory");
         for (int i = tid; i < n; i += KC_BOT_THREADS) {
           const int q = i / MC, p = i - q * MC;
           const double* rc = w + (2 * q + 1) * S + (2 * p + 1);
           const double* rs = rc - S;
           const double* rn = rc + S;
           const double fv = kc_fw(rs[-1], rs[0], rs[1], rc[-1], rc[0], rc[1], rn[-1], rn[0], rn[1]);
-          for (int k = 0; k < cs; ++k) *cl.map_shared_rank(fc + q * SC + p, k) = fv;
+          if (KC_RB_ASYNC) {
+            const unsigned la = bot_sa(fc + q * SC + p), lb = bot_sa(rb);
+            for (int k = 0; k < cs; ++k)
+              asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(
+                               bot_mapa(la, k)),
+                           "d"(fv), "r"(bot_mapa(lb, k))
+                           : "memory");
+          } else {
+            for (int k = 0; k < cs; ++k) *cl.map_shared_rank(fc + q * SC + p, k) = fv;
+          }
+        }
+        if (KC_RB_ASYNC) {
+          // every CTA's rows landed here; no cluster barrier: between this
+          // CTA's last read of the child's f and any CTA's next broadcast
+          // lies a cluster barrier (the next call's v exchange, the 127^2
+          // restriction or the interpreter's phases), so one mbarrier serves
+          bot_mv_wait(rb, f31->rb_n & 1);
+          ++f31->rb_n;
+          return lo;
         }
       }
     }
@@ -1494,7 +1520,7 @@ struct BotDeep {
 __device__ __forceinline__ void bot_run_frame(int op, double* sm, const BotLv* lv, const St9* tab, const BotParams* bp,
                                            int d, int kap, int src, int zero, int rank, int cs, int nlev, int* slot,
                                            int* tiny_child, int* mvs, unsigned long long* mvbar) {
-  BotFrame31 fr{sm, lv, tab, bp, (int)threadIdx.x, rank, cs, nlev, slot, tiny_child, mvs[0], mvs[1] != 0, mvbar, mvs[2]};
+  BotFrame31 fr{sm, lv, tab, bp, (int)threadIdx.x, rank, cs, nlev, slot, tiny_child, mvs[0], mvs[1] != 0, mvbar, mvs[2], mvs[3]};
   if (op == PH_FRAME63 || op == PH_FRAME127) {
     BotDeep dp{sm, lv, tab, &fr, (int)threadIdx.x, rank, cs};
     dp.run(op == PH_FRAME127, op == PH_FRAME127 ? 1 : d, kap, src);
@@ -1505,6 +1531,7 @@ __device__ __forceinline__ void bot_run_frame(int op, double* sm, const BotLv* l
   mvs[0] = fr.mv_last;
   mvs[1] = fr.mv_sync ? 1 : 0;
   mvs[2] = fr.mv_n;
+  mvs[3] = fr.rb_n;
 }
 
 // Columns of the side-15 frame operators: CTA (j, k - 1) runs BotTiny::frame
@@ -1558,12 +1585,11 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
   __shared__ BotLv lv[KC_BOT_MAXLEV];
   __shared__ unsigned sched[KC_BOT_MAXPH];
   __shared__ int tiny_child[2];
-  __shared__ alignas(8) unsigned long long mvbar[2];
+  __shared__ alignas(8) unsigned long long mvbar[3];  // frame-operator phases (2), 63^2 -> 31^2 broadcast
   cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
   const int rank = (int)cl.block_rank(), cs = (int)cl.num_blocks();
-  if (KC_MV_ASYNC && threadIdx.x == 0) {  // published by the prologue's barrier
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bot_sa(&mvbar[0])));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bot_sa(&mvbar[1])));
+  if ((KC_MV_ASYNC || KC_RB_ASYNC) && threadIdx.x == 0) {  // published by the prologue's cluster barrier
+    for (int b = 0; b < 3; ++b) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bot_sa(&mvbar[b])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const int nlev = bp.nlev, nstrip = bp.nstrip;
@@ -1707,7 +1733,7 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
   __shared__ int f31_slot;
   int mv_last = -1;      // frame-operator bookkeeping shared with PH_FRAME31 (BotBuilder mirrors it)
   bool mv_sync = false;
-  int mv_n = 0;
+  int mv_n = 0, rb_n = 0;
   unsigned e_next = bp.nsched > 0 ? sched[0] : 0u;
   for (int k = 0; k < bp.nsched; ++k) {
     const unsigned e = e_next;
@@ -1771,11 +1797,12 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
         vc += (L.a / 2) * C.S;
       bot_prolong(u, vc, L, C.m, C.S, zero, tid, nth, bot_push(u, L, strip, rank, cs));
     } else if (op == PH_FRAME63 || op == PH_FRAME31 || op == PH_FRAME127) {  // every thread of every CTA
-      int mvs[3] = {mv_last, mv_sync ? 1 : 0, mv_n};
+      int mvs[4] = {mv_last, mv_sync ? 1 : 0, mv_n, rb_n};
       bot_run_frame(op, sm, lv, tab, &bp, d, BD_KAP(e), src, zero, rank, cs, nlev, &f31_slot, tiny_child, mvs, mvbar);
       mv_last = mvs[0];
       mv_sync = mvs[1] != 0;
       mv_n = mvs[2];
+      rb_n = mvs[3];
     } else if (KC_FAST && strip) {  // PH_TINY as a frame operator (all CTAs; FMA build only)
       bot_mv_frame(sm, bp, L, src, BD_CBUF(e), zero, BD_KAP(e), rank, cs);
       mv_last = BD_CBUF(e);
