@@ -885,6 +885,9 @@ struct BotTiny {
 #ifndef KC_RB_ASYNC  // the 63^2 -> 31^2 restriction broadcast of the deep frames as st.async
 #define KC_RB_ASYNC 1
 #endif
+#ifndef KC_XB_ASYNC  // the deep frames' halo exchanges (v rows) as st.async: measured no
+#define KC_XB_ASYNC 0     // faster in the FMA build, 1.4 % slower per cycle in the exact one
+#endif
 __device__ __forceinline__ unsigned bot_sa(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ unsigned bot_mapa(unsigned a, int rank) {
   unsigned r;
@@ -1050,6 +1053,7 @@ struct BotFrame31 {
   unsigned long long* mvbar;  // two mbarriers for the st.async frame-operator phases (KC_MV_ASYNC)
   int mv_n;                   // st.async phases so far this launch (the same count on every CTA)
   int rb_n;                   // st.async restriction broadcasts into the 31^2 replicas so far (KC_RB_ASYNC)
+  int xb_n;                   // st.async deep-halo exchanges so far (KC_XB_ASYNC)
   // one frame-operator phase and its completion: bot_mv_frame, then the
   // cluster barrier, or (KC_MV_ASYNC) the wait on this CTA's mbarrier
   __device__ __forceinline__ void mv(const BotLv& L, int src, int ob, bool zero, int kap, int bb = -1) {
@@ -1334,6 +1338,25 @@ struct BotDeep {
   template <int M>
   __device__ __forceinline__ void push_rows(double* u, int a, int ylo, int yhi) const {
     constexpr int R = (M + 1) / 16, S = M + 2;
+    if (KC_XB_ASYNC) {  // st.async completing on the neighbour's exchange mbarrier
+      const unsigned ub = bot_sa(u), bb = bot_sa(f31->mvbar + 3);
+      const bool hu = rank > 0, hd = rank + 1 < cs;
+      const unsigned bu = hu ? bot_mapa(bb, rank - 1) : 0u, bd = hd ? bot_mapa(bb, rank + 1) : 0u;
+      rows_do<M>(a, ylo, yhi, [&](int y, int x) {
+        const double v = u[y * S + x];
+        if (hu && y < HB)
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(
+                           bot_mapa(ub + 8u * (unsigned)((R + y) * S + x), rank - 1)),
+                       "d"(v), "r"(bu)
+                       : "memory");
+        if (hd && y >= R - HB)
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(
+                           bot_mapa(ub + 8u * (unsigned)((y - R) * S + x), rank + 1)),
+                       "d"(v), "r"(bd)
+                       : "memory");
+      });
+      return;
+    }
     cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
     double* up = rank > 0 ? cl.map_shared_rank(u, rank - 1) + R * S : nullptr;
     double* dn = rank + 1 < cs ? cl.map_shared_rank(u, rank + 1) - R * S : nullptr;
@@ -1342,6 +1365,41 @@ struct BotDeep {
       if (up && y < HB) up[y * S + x] = v;
       if (dn && y >= R - HB) dn[y * S + x] = v;
     });
+  }
+  // bytes this CTA receives when every CTA runs push_rows<M>(.., ylo, yhi):
+  // rows y < HB of the CTA below it, rows y >= R - HB of the one above
+  template <int M>
+  __device__ __forceinline__ int push_bytes(int ylo, int yhi) const {
+    constexpr int R = (M + 1) / 16;
+    auto cnt = [&](int s, bool to_up) {
+      const int hi = min(yhi, M - 1 - s * R);
+      int c = 0;
+      for (int y = ylo; y <= hi; ++y) c += to_up ? (y < HB) : (y >= R - HB);
+      return c;
+    };
+    int n = 0;
+    if (rank + 1 < cs) n += cnt(rank + 1, true);
+    if (rank > 0) n += cnt(rank - 1, false);
+    return n * M * 8;
+  }
+  // a halo exchange of push_rows: the expected bytes on this CTA's exchange
+  // mbarrier before the pushes, the wait after them (KC_XB_ASYNC), else the
+  // cluster barrier.  Every exchange is preceded by a cluster barrier (the
+  // write-after-read guard), so the next exchange's bytes cannot reach this
+  // CTA before it has waited for this one: one mbarrier serves.
+  __device__ __forceinline__ void xchg_begin(int bytes) const {
+    if (KC_XB_ASYNC && tid == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bot_sa(f31->mvbar + 3)),
+                   "r"(bytes)
+                   : "memory");
+  }
+  __device__ __forceinline__ void xchg_end() const {
+    if (KC_XB_ASYNC) {
+      bot_mv_wait(f31->mvbar + 3, f31->xb_n & 1);
+      ++f31->xb_n;
+    } else {
+      clu_sync();
+    }
   }
   // the pre half of a call: sweeps (J2Z on a zero guess), residual,
   // restriction -- broadcast into the child's replicas (M = 63) or into the
@@ -1366,8 +1424,9 @@ struct BotDeep {
       // after a barrier: a neighbour may still be using those rows for the
       // previous call's prolongation and sweeps
       clu_sync();
+      xchg_begin(push_bytes<M>(0, R - 1));
       push_rows<M>(u, a, 0, R - 1);
-      clu_sync();
+      xchg_end();
       stencil2<M, true>(a, -3, R + 2, u, w, f, st);
       bot_bar();
       stencil2<M, true>(a, -2, R + 1, w, u, f, st);
@@ -1456,9 +1515,10 @@ struct BotDeep {
     bot_bar();
     if (np > 0) {  // after a barrier: the neighbours' post sweeps read their halo rows
       clu_sync();
+      xchg_begin(push_bytes<M>(0, np - 1) + push_bytes<M>(R - np, R - 1));
       push_rows<M>(u, a, 0, np - 1);
       push_rows<M>(u, a, R - np, R - 1);
-      clu_sync();
+      xchg_end();
     }
   }
   // the post half of a 127^2 call under PH_FRAME127: prolongation from the
@@ -1520,7 +1580,7 @@ struct BotDeep {
 __device__ __forceinline__ void bot_run_frame(int op, double* sm, const BotLv* lv, const St9* tab, const BotParams* bp,
                                            int d, int kap, int src, int zero, int rank, int cs, int nlev, int* slot,
                                            int* tiny_child, int* mvs, unsigned long long* mvbar) {
-  BotFrame31 fr{sm, lv, tab, bp, (int)threadIdx.x, rank, cs, nlev, slot, tiny_child, mvs[0], mvs[1] != 0, mvbar, mvs[2], mvs[3]};
+  BotFrame31 fr{sm, lv, tab, bp, (int)threadIdx.x, rank, cs, nlev, slot, tiny_child, mvs[0], mvs[1] != 0, mvbar, mvs[2], mvs[3], mvs[4]};
   if (op == PH_FRAME63 || op == PH_FRAME127) {
     BotDeep dp{sm, lv, tab, &fr, (int)threadIdx.x, rank, cs};
     dp.run(op == PH_FRAME127, op == PH_FRAME127 ? 1 : d, kap, src);
@@ -1532,6 +1592,7 @@ __device__ __forceinline__ void bot_run_frame(int op, double* sm, const BotLv* l
   mvs[1] = fr.mv_sync ? 1 : 0;
   mvs[2] = fr.mv_n;
   mvs[3] = fr.rb_n;
+  mvs[4] = fr.xb_n;
 }
 
 // Columns of the side-15 frame operators: CTA (j, k - 1) runs BotTiny::frame
@@ -1585,11 +1646,12 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
   __shared__ BotLv lv[KC_BOT_MAXLEV];
   __shared__ unsigned sched[KC_BOT_MAXPH];
   __shared__ int tiny_child[2];
-  __shared__ alignas(8) unsigned long long mvbar[3];  // frame-operator phases (2), 63^2 -> 31^2 broadcast
+  // mbarriers: frame-operator phases (2), 63^2 -> 31^2 broadcast, deep-halo exchanges
+  __shared__ alignas(8) unsigned long long mvbar[4];
   cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
   const int rank = (int)cl.block_rank(), cs = (int)cl.num_blocks();
-  if ((KC_MV_ASYNC || KC_RB_ASYNC) && threadIdx.x == 0) {  // published by the prologue's cluster barrier
-    for (int b = 0; b < 3; ++b) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bot_sa(&mvbar[b])));
+  if ((KC_MV_ASYNC || KC_RB_ASYNC || KC_XB_ASYNC) && threadIdx.x == 0) {  // published by the prologue's cluster barrier
+    for (int b = 0; b < 4; ++b) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bot_sa(&mvbar[b])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const int nlev = bp.nlev, nstrip = bp.nstrip;
@@ -1733,7 +1795,7 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
   __shared__ int f31_slot;
   int mv_last = -1;      // frame-operator bookkeeping shared with PH_FRAME31 (BotBuilder mirrors it)
   bool mv_sync = false;
-  int mv_n = 0, rb_n = 0;
+  int mv_n = 0, rb_n = 0, xb_n = 0;
   unsigned e_next = bp.nsched > 0 ? sched[0] : 0u;
   for (int k = 0; k < bp.nsched; ++k) {
     const unsigned e = e_next;
@@ -1797,12 +1859,13 @@ __global__ void __launch_bounds__(KC_BOT_THREADS, 1) k_bottom(const BotParams bp
         vc += (L.a / 2) * C.S;
       bot_prolong(u, vc, L, C.m, C.S, zero, tid, nth, bot_push(u, L, strip, rank, cs));
     } else if (op == PH_FRAME63 || op == PH_FRAME31 || op == PH_FRAME127) {  // every thread of every CTA
-      int mvs[4] = {mv_last, mv_sync ? 1 : 0, mv_n, rb_n};
+      int mvs[5] = {mv_last, mv_sync ? 1 : 0, mv_n, rb_n, xb_n};
       bot_run_frame(op, sm, lv, tab, &bp, d, BD_KAP(e), src, zero, rank, cs, nlev, &f31_slot, tiny_child, mvs, mvbar);
       mv_last = mvs[0];
       mv_sync = mvs[1] != 0;
       mv_n = mvs[2];
       rb_n = mvs[3];
+      xb_n = mvs[4];
     } else if (KC_FAST && strip) {  // PH_TINY as a frame operator (all CTAs; FMA build only)
       bot_mv_frame(sm, bp, L, src, BD_CBUF(e), zero, BD_KAP(e), rank, cs);
       mv_last = BD_CBUF(e);
