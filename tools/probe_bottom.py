@@ -28,8 +28,11 @@ KEYS = ("KC_DEEP127", "KC_BOT_ENTRY", "KC_BOT_MINSTRIP", "KC_BOT_CS", "KC_BOT_CL
 if len(sys.argv) > 2:
     VARIANTS = {k: VARIANTS[k] for k in sys.argv[2].split(",")}
 v0 = np.random.default_rng(0).random((m, m))
+only = [v for v in os.environ.get("PROBE_ONLY", "").split(",") if v]  # a subset of VARIANTS
 for rep in range(2):
     for name, env in VARIANTS.items():
+        if only and name not in only:
+            continue
         for k in KEYS:
             os.environ.pop(k, None)
         os.environ.update(env)
