@@ -127,6 +127,10 @@ struct BotParams {
   int mv_copy, mv_off, mv_rows, mv_xin;  // mv_xin: 2 x 225 doubles of packed inputs
   int mv_avail;      // blocks that exist (resident or read from global memory): frames use them
   int mv_slot[KC_MV_NBLK];
+  // st.async phases (jitter builds: a runtime switch within the compile-time
+  // KC_MV_ASYNC / KC_RB_ASYNC): bit 0 the frame-operator outputs, bit 1 the
+  // 63^2 -> 31^2 broadcast
+  int async;
 };
 
 // Frame operators (FMA build, cluster launches only).  A kappa_cycle frame on
@@ -885,6 +889,15 @@ struct BotTiny {
 #ifndef KC_RB_ASYNC  // the 63^2 -> 31^2 restriction broadcast of the deep frames as st.async
 #define KC_RB_ASYNC 1
 #endif
+// the st.async phases as a runtime switch (BotParams::async) in the jitter
+// builds only, where tests/test_gpu_jitter.py runs both schemes under
+// perturbation; the production builds compile the st.async path alone (the
+// switch cost 0.5 % per cycle there)
+#ifdef KC_BOT_JITTER
+#define KC_ASYNC_ON(bp, bit) ((((bp)->async) >> (bit)) & 1)
+#else
+#define KC_ASYNC_ON(bp, bit) true
+#endif
 #ifndef KC_XB_ASYNC  // the deep frames' halo exchanges (v rows) as st.async: measured no
 #define KC_XB_ASYNC 0     // faster in the FMA build, 1.4 % slower per cycle in the exact one
 #endif
@@ -1057,7 +1070,7 @@ struct BotFrame31 {
   // one frame-operator phase and its completion: bot_mv_frame, then the
   // cluster barrier, or (KC_MV_ASYNC) the wait on this CTA's mbarrier
   __device__ __forceinline__ void mv(const BotLv& L, int src, int ob, bool zero, int kap, int bb = -1) {
-    if (KC_MV_ASYNC && cs > 1) {
+    if (KC_MV_ASYNC && cs > 1 && KC_ASYNC_ON(bp, 0)) {
       unsigned long long* b = mvbar + (mv_n & 1);
       bot_mv_frame(sm, *bp, L, src, ob, zero, kap, rank, cs, bb, -1, b);
       bot_mv_wait(b, (mv_n >> 1) & 1);
@@ -1457,7 +1470,8 @@ struct BotDeep {
       } else {  // every CTA's replica of the child, at this strip's first coarse row
         double* fc = fc0 + (a / 2) * SC;
         unsigned long long* rb = f31->mvbar + 2;
-        if (KC_RB_ASYNC && tid == 0)  // this CTA's replica receives the whole MC x MC child f
+        const bool as = KC_RB_ASYNC && KC_ASYNC_ON(f31->bp, 1);
+        if (as && tid == 0)  // this CTA's replica receives the whole MC x MC child f
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bot_sa(rb)), "r"(MC * MC * 8)
                        : "memory");
         for (int i = tid; i < n; i += KC_BOT_THREADS) {
@@ -1466,7 +1480,7 @@ struct BotDeep {
           const double* rs = rc - S;
           const double* rn = rc + S;
           const double fv = kc_fw(rs[-1], rs[0], rs[1], rc[-1], rc[0], rc[1], rn[-1], rn[0], rn[1]);
-          if (KC_RB_ASYNC) {
+          if (as) {
             const unsigned la = bot_sa(fc + q * SC + p), lb = bot_sa(rb);
             for (int k = 0; k < cs; ++k)
               asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(
@@ -1477,7 +1491,7 @@ struct BotDeep {
             for (int k = 0; k < cs; ++k) *cl.map_shared_rank(fc + q * SC + p, k) = fv;
           }
         }
-        if (KC_RB_ASYNC) {
+        if (as) {
           // every CTA's rows landed here; no cluster barrier: between this
           // CTA's last read of the child's f and any CTA's next broadcast
           // lies a cluster barrier (the next call's v exchange, the 127^2

@@ -1744,6 +1744,12 @@ int kc_create(int n, int coarsening, const double* w, int smoother_kind, double 
     bp.nstrip = nstrip;
     bp.deep = deep;
     bp.deep0 = deep0;
+    // st.async frame-operator outputs / 63^2 -> 31^2 broadcast (KC_MV_ASYNC=0,
+    // KC_RB_ASYNC=0: DSMEM stores + cluster barriers, the same iterates; read
+    // by the jitter builds only, kc_bottom.cuh KC_ASYNC_ON)
+    const char* maenv = getenv("KC_MV_ASYNC");
+    const char* raenv = getenv("KC_RB_ASYNC");
+    bp.async = ((maenv && maenv[0] == '0') ? 0 : 1) | ((raenv && raenv[0] == '0') ? 0 : 2);
     for (int j = 0; j < bp.nlev; ++j) bp.st[j] = h->L[lb + j].st;
     h->bot_m0 = h->L[lb].m;
     h->bot_cs = cs;

@@ -92,8 +92,12 @@ def _cases(arith, shapes, ns, kappas, reps=3, cycles=2):
     return out
 
 
+# "barriers": the st.async phases (frame-operator outputs, the 63^2 -> 31^2
+# broadcast; mbarrier completion) switched back to DSMEM stores + cluster
+# barriers -- a runtime switch of the jitter builds only (kc_bottom.cuh
+# KC_ASYNC_ON): the same iterates either way, under perturbation
 SHAPES = [("deep", {}), ("deep63", {"KC_DEEP127": "0"}), ("nodeep", {"KC_DEEP": "0"}),
-          ("onecta", {"KC_BOT_CLUSTER": "0"})]
+          ("onecta", {"KC_BOT_CLUSTER": "0"}), ("barriers", {"KC_MV_ASYNC": "0", "KC_RB_ASYNC": "0"})]
 
 
 def test_jitter_libraries_present_and_perturbing():
@@ -132,7 +136,7 @@ def test_exact_build_under_jitter_bit_exact_vs_oracle():
 
 
 def test_fast_build_under_jitter_equals_fast_build():
-    cases = _cases("fast", SHAPES[:3], [9, 12], [1, 2, 3, 12], reps=2)
+    cases = _cases("fast", SHAPES[:3] + SHAPES[4:], [9, 12], [1, 2, 3, 12], reps=2)
     cases = [c for c in cases if not (c["n"] == 9 and c["kappa"] == 12)]
     got = _run_jitter(cases)
     for c in cases:
